@@ -1,0 +1,181 @@
+/*
+ * mfh.h — C-ABI of the B200-native HODLR-multifrontal hot path (libmfh.so).
+ *
+ * This is the drop-in boundary. Plain pointers, sizes and opaque handles only;
+ * no torch / numpy types. Every entry point returns 0 on success and a nonzero
+ * error kind on failure, with the message (reference text) in mfh_last_error():
+ *
+ *   MFH_EVALUE  -> Python ValueError              (reference raises ValueError)
+ *   MFH_EPIVOT  -> PivotMonotonicityError          (_kernels/_core.pyx:17)
+ *   MFH_ERUNTIME-> RuntimeError (CUDA failure, bad handle, internal error)
+ *
+ * Each entry point cites the reference interface it replaces
+ * (/root/reference/pkg/src/mfhodlr/<file>:<line>). The Python binding that a
+ * maintainer adds on the reference side is shown in INTEGRATION.md.
+ */
+#ifndef MFH_H_
+#define MFH_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MFH_OK 0
+#define MFH_EVALUE 1
+#define MFH_EPIVOT 2
+#define MFH_ERUNTIME 3
+
+typedef struct mfh_ctx mfh_ctx;          /* device + stream + workspaces          */
+typedef struct mfh_nd mfh_nd;            /* separator tree (ordering.py:32-56)    */
+typedef struct mfh_etree mfh_etree;      /* elimination tree (ordering.py:238-261)*/
+typedef struct mfh_factor mfh_factor;    /* MfFactorization (multifrontal.py:227) */
+typedef struct mfh_csr mfh_csr;          /* device CSR operator (krylov.py:21-33) */
+
+/* MfParams (multifrontal.py:34-48); max_rank < 0 means None. */
+typedef struct {
+  int64_t n_c;
+  double eps;
+  int64_t d;
+  int64_t n_leaf;
+  int64_t max_rank;
+} mfh_params;
+
+/* mode (multifrontal.py:30-31, 459-470) */
+#define MFH_CONVENTIONAL 0
+#define MFH_ACCELERATED 1
+
+/* FactorStats counters (multifrontal.py:61-103) */
+typedef struct {
+  int64_t peak_stored_reals;
+  int64_t retained_reals;
+  int64_t structured_fronts;
+  int64_t dense_fronts;
+  int64_t full_square_allocs;
+  int64_t n_records;
+  int64_t stored_reals; /* MfFactorization.stored_reals() (multifrontal.py:239) */
+  /* device-side truth, not in the reference */
+  int64_t device_bytes_peak;
+  int64_t n_blocks;    /* compressed off-diagonal blocks */
+  int64_t n_dense_fallback;
+} mfh_stats_t;
+
+/* one FrontRecord (multifrontal.py:51-58); path: 0 empty, 1 dense, 2 structured */
+typedef struct {
+  int64_t node_id, front_size, n_pivot, path, max_offdiag_rank, stored_reals;
+} mfh_record_t;
+
+/* per-phase device timing of the last mfh_factorize (ms, CUDA events) */
+typedef struct {
+  double total_ms;
+  double sample_ms, pivot_lu_ms, skeleton_ms, hodlr_factor_ms, dense_front_ms, eliminate_ms;
+  double host_ms;
+  int64_t kernel_launches;
+  double pivot_lu_visits; /* algorithmic trailing-entry visits */
+  double sample_entries;
+} mfh_timing_t;
+
+/* ---- errors --------------------------------------------------------------- */
+const char *mfh_last_error(void);
+int mfh_version(void);
+
+/* ---- context -------------------------------------------------------------- */
+int mfh_ctx_create(int device, mfh_ctx **out);
+void mfh_ctx_destroy(mfh_ctx *ctx);
+int mfh_ctx_sync(mfh_ctx *ctx);
+
+/* ---- host symbolic analysis (bit-identical to the reference) -------------- */
+/* AdjGraph.from_pattern (sparse.py:102-111): symmetrized pattern of the
+ * nonzero-valued entries, diagonal removed, rows sorted. Two-call protocol:
+ * pass indices_out == NULL to get nnz_out, then call again with buffers. */
+int mfh_adjacency(int64_t n, const int64_t *indptr, const int64_t *indices, const double *values,
+                  int64_t *indptr_out, int64_t *indices_out, int64_t *nnz_out);
+
+/* nested_dissection (ordering.py:157-208) */
+int mfh_nd_create(int64_t n, const int64_t *g_indptr, const int64_t *g_indices, int64_t leaf_size,
+                  mfh_nd **out);
+int mfh_nd_sizes(const mfh_nd *nd, int64_t *n_nodes, int64_t *n_vertices, int64_t *root);
+int mfh_nd_fetch(const mfh_nd *nd, int64_t *perm, int64_t *vptr, int64_t *verts, int64_t *left,
+                 int64_t *right, int64_t *parent);
+void mfh_nd_free(mfh_nd *nd);
+
+/* build_elimination_tree (ordering.py:264-312). A given as CSR (rows sorted). */
+int mfh_etree_create(int64_t n, const int64_t *indptr, const int64_t *indices, const double *values,
+                     const mfh_nd *nd, mfh_etree **out);
+int mfh_etree_sizes(const mfh_etree *t, int64_t *n_nodes, int64_t *n_piv_total,
+                    int64_t *n_frontal_total, int64_t *root);
+int mfh_etree_fetch(const mfh_etree *t, int64_t *post_order, int64_t *piv_ptr, int64_t *piv,
+                    int64_t *fr_ptr, int64_t *fr, int64_t *parent);
+void mfh_etree_free(mfh_etree *t);
+
+/* ---- numeric factorization (mf_factorize, multifrontal.py:459-530) --------- */
+/* A is the ORIGINAL matrix as CSR (rows sorted, no duplicates); the etree
+ * carries the permutation. The numeric work runs on the context's GPU. */
+int mfh_factorize(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const int64_t *indptr,
+                  const int64_t *indices, const double *values, int mode, const mfh_params *params,
+                  mfh_factor **out);
+int mfh_factor_stats(const mfh_factor *f, mfh_stats_t *out);
+int mfh_factor_records(const mfh_factor *f, mfh_record_t *out /* n_records */);
+int mfh_factor_timing(const mfh_factor *f, mfh_timing_t *out);
+/* integer parity record of every compressed block, in the reference's visiting
+ * order: per block (node_id, m, n, |I|, |J|, rank, dense_fallback) and the
+ * pivot sequences row_perm[:rank], col_perm[:rank] concatenated. Two-call. */
+int mfh_factor_blocks(const mfh_factor *f, int64_t *n_blocks, int64_t *n_perm, int64_t *info /*7*n*/,
+                      int64_t *perms /* 2*n_perm */, double *ratios /* n */);
+void mfh_factor_free(mfh_factor *f);
+
+/* ---- preconditioner apply (mf_solve, multifrontal.py:533-560) ------------- */
+/* b, x: host (on_device == 0) or device (on_device == 1) arrays of n*nrhs,
+ * column-major per right-hand side. */
+int mfh_apply(mfh_factor *f, const double *b, double *x, int64_t nrhs, int on_device);
+/* time `reps` device-resident applies; returns mean ms and algorithmic bytes/apply */
+int mfh_apply_bench(mfh_factor *f, int64_t reps, double *ms_per_apply, double *bytes_per_apply);
+
+/* ---- sparse operator (spmv, sparse.py:277-284; LinearOperator.from_matrix) */
+int mfh_csr_create(mfh_ctx *ctx, int64_t n_rows, int64_t n_cols, const int64_t *indptr,
+                   const int64_t *indices, const double *values, mfh_csr **out);
+int mfh_spmv(mfh_csr *A, const double *x, double *y, int on_device);
+void mfh_csr_free(mfh_csr *A);
+/* dense operator (LinearOperator.from_matrix(ndarray), krylov.py:32-33): row-major n x n */
+int mfh_dense_create(mfh_ctx *ctx, int64_t n, const double *values, mfh_csr **out);
+
+/* ---- GMRES (gmres, krylov.py:68-161) -------------------------------------- */
+/* host callback operator: y = op(x), both host arrays of length n */
+typedef void (*mfh_host_op)(void *user, const double *x, double *y);
+
+typedef struct {
+  mfh_csr *A;          /* device operator, or NULL to use A_cb */
+  mfh_host_op A_cb;
+  void *A_user;
+  mfh_factor *M;       /* device preconditioner (accelerated-mf), or NULL */
+  mfh_host_op M_cb;    /* host preconditioner callback when M == NULL; NULL = identity */
+  void *M_user;
+} mfh_gmres_ops;
+
+/* b, x host arrays of n; hist receives up to max_iter residuals (or 1 when
+ * ||b|| == 0). Returns iterations, converged, n_hist. */
+int mfh_gmres(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const double *b, double *x,
+              double tol, int64_t max_iter, int64_t restart, double *hist, int64_t *n_hist,
+              int64_t *iterations, int *converged);
+/* same, b/x already on the device (x overwritten); used by the benchmark */
+int mfh_gmres_device(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const double *d_b,
+                     double *d_x, double tol, int64_t max_iter, int64_t restart, double *hist,
+                     int64_t *n_hist, int64_t *iterations, int *converged);
+
+/* ---- kernel plugin (full_pivot_lu, _kernels/__init__.py:25; _core.pyx:23) - */
+/* Batched complete-pivot LU on the device. Blocks are row-major, packed at
+ * offs[i] (doubles) in `blocks` (host); shapes ms[i] x ns[i]. Outputs: lu
+ * overwritten in place in the reference's (physically permuted) layout;
+ * row_perm packed at sum(ms[:i]), col_perm at sum(ns[:i]); ranks; next
+ * ratios; status 1 = PivotMonotonicityError with err[3i..3i+2] = (k, pivot,
+ * previous pivot), for the exact reference message. */
+int mfh_full_pivot_lu_batched(mfh_ctx *ctx, int64_t batch, const int64_t *offs, const int64_t *ms,
+                              const int64_t *ns, double *blocks, int64_t total, double eps,
+                              const int64_t *max_ranks, int64_t *row_perm, int64_t *col_perm,
+                              int64_t *ranks, double *ratios, int64_t *status, double *err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MFH_H_ */

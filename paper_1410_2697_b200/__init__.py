@@ -1,0 +1,30 @@
+"""B200-native HODLR-multifrontal preconditioner (arXiv 1410.2697 hot path).
+
+Drop-in for the reference package's hot path (``mfhodlr``: ``mf_factorize``,
+``mf_solve``, ``gmres``, ``full_pivot_lu``): same names, arguments, statistics
+and error messages, with the numeric work in hand-written sm_100a CUDA kernels
+behind the C-ABI of ``include/mfh.h`` (``libmfh.so``).
+"""
+
+from ._lib import PivotMonotonicityError
+from .kernels import BACKEND as KERNEL_BACKEND, full_pivot_lu, full_pivot_lu_batched
+from .krylov import (ConvergenceHistory, LinearOperator, Preconditioner, gmres,
+                     identity_preconditioner, mf_preconditioner)
+from .multifrontal import (ACCELERATED, CONVENTIONAL, FactorStats, FrontRecord, MfFactorization,
+                           MfParams, mf_factorize, mf_solve)
+from .ordering import (EliminationTree, EtNode, SeparatorTree, SepNode, build_elimination_tree,
+                       nested_dissection)
+from .problems import gen_hex_q1, gen_p1_delaunay, gen_poisson7, gen_q1_2d, seeded_rhs
+from .sparse import AdjGraph, SparseMatrix, adjacency_graph, spmv
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ACCELERATED", "AdjGraph", "CONVENTIONAL", "ConvergenceHistory", "EliminationTree", "EtNode",
+    "FactorStats", "FrontRecord", "KERNEL_BACKEND", "LinearOperator", "MfFactorization", "MfParams",
+    "PivotMonotonicityError", "Preconditioner", "SepNode", "SeparatorTree", "SparseMatrix",
+    "adjacency_graph", "build_elimination_tree", "full_pivot_lu", "full_pivot_lu_batched",
+    "gen_hex_q1", "gen_p1_delaunay", "gen_poisson7", "gen_q1_2d", "gmres",
+    "identity_preconditioner", "mf_factorize", "mf_preconditioner", "mf_solve",
+    "nested_dissection", "seeded_rhs", "spmv",
+]

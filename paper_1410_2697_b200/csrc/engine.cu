@@ -1,0 +1,2329 @@
+// Host orchestrator for the B200 HODLR-multifrontal factorization, the
+// preconditioner apply and GMRES, plus their C-ABI entry points.
+//
+// Schedule: the elimination tree is processed by HEIGHT (children strictly
+// below parents), every front of a height in the same batched launches:
+//   dense fronts  (front < n_c): sample (assemble + extend-add), getrf(F_pp),
+//                                getrs(F_pp, F_pf), Schur GEMM  (multifrontal.py:283-310)
+//   structured fronts (>= n_c): sample leaves + BDLR panels, complete-pivot LU
+//                                of every core, [one host sync for the ranks],
+//                                skeleton TRSMs / dense fallbacks, level-batched
+//                                HODLR factorization, W/V update (multifrontal.py:353-456)
+// BDLR selections (bdlr.py:89-136) are integer graph work done on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <numeric>
+
+#include "internal.h"
+#include "kernels.cuh"
+
+namespace mfh {
+
+thread_local std::string g_last_error;
+void set_last_error(const std::string &m) { g_last_error = m; }
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess)                                                                      \
+      throw runtime_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #x);    \
+  } while (0)
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------------------
+// device memory: chunked bump arena
+// ---------------------------------------------------------------------------
+struct Arena {
+  std::vector<std::pair<char *, size_t>> chunks;
+  size_t cur = 0, off = 0;
+  size_t chunk = size_t(256) << 20;
+  size_t in_use = 0, peak = 0;
+  void *alloc(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes == 0) bytes = 256;
+    while (true) {
+      if (cur < chunks.size()) {
+        if (off + bytes <= chunks[cur].second) {
+          void *p = chunks[cur].first + off;
+          off += bytes;
+          in_use += bytes;
+          peak = std::max(peak, in_use);
+          return p;
+        }
+        ++cur;
+        off = 0;
+        continue;
+      }
+      size_t sz = std::max(chunk, bytes);
+      char *p = nullptr;
+      CK(cudaMalloc(&p, sz));
+      chunks.push_back({p, sz});
+      // cur now indexes the new chunk
+    }
+  }
+  double *d(size_t n) { return (double *)alloc(n * sizeof(double)); }
+  int *i(size_t n) { return (int *)alloc(n * sizeof(int)); }
+  void reset() {
+    cur = 0;
+    off = 0;
+    in_use = 0;
+  }
+  void release() {
+    for (auto &c : chunks) cudaFree(c.first);
+    chunks.clear();
+    reset();
+  }
+  size_t capacity() const {
+    size_t s = 0;
+    for (auto &c : chunks) s += c.second;
+    return s;
+  }
+};
+
+// pinned staging for descriptor arrays (async H2D, rewound at sync points)
+struct Stage {
+  char *h = nullptr, *d = nullptr;
+  size_t cap = 0, off = 0;
+  void init(size_t c) {
+    cap = c;
+    CK(cudaMallocHost(&h, cap));
+    CK(cudaMalloc(&d, cap));
+  }
+  void release() {
+    if (h) cudaFreeHost(h);
+    if (d) cudaFree(d);
+    h = d = nullptr;
+  }
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t s = nullptr;
+  Stage stage;
+  Arena scratch;
+  double *d_part = nullptr;  // reduction partials
+  double *d_scal = nullptr;  // small device scalars
+  int64_t launches = 0;
+};
+
+// ---------------------------------------------------------------------------
+// Sink: where descriptors go and how launches happen.
+//   immediate: staged async copy, launch now (factorization)
+//   record:    persistent copy, launch recorded for graph capture (apply)
+// ---------------------------------------------------------------------------
+struct Sink {
+  Ctx *ctx;
+  Arena *persist = nullptr;  // record mode
+  bool record = false;
+  std::vector<std::function<void(cudaStream_t)>> ops;
+
+  void sync_reset() {
+    CK(cudaStreamSynchronize(ctx->s));
+    ctx->stage.off = 0;
+  }
+  void *push_bytes(const void *src, size_t bytes) {
+    if (bytes == 0) return nullptr;
+    if (record) {
+      void *p = persist->alloc(bytes);
+      CK(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice));
+      return p;
+    }
+    Stage &st = ctx->stage;
+    size_t b = (bytes + 255) & ~size_t(255);
+    if (st.off + b > st.cap) {
+      sync_reset();
+      if (b > st.cap) {  // grow
+        st.release();
+        st.init(std::max(b * 2, st.cap * 2));
+      }
+    }
+    std::memcpy(st.h + st.off, src, bytes);
+    void *dp = st.d + st.off;
+    CK(cudaMemcpyAsync(dp, st.h + st.off, bytes, cudaMemcpyHostToDevice, ctx->s));
+    st.off += b;
+    return dp;
+  }
+  template <class T>
+  T *push(const std::vector<T> &v) {
+    return (T *)push_bytes(v.data(), v.size() * sizeof(T));
+  }
+  // copy into scratch device memory that survives staging rewinds (until the
+  // end of the height, when the scratch arena is reset)
+  template <class T>
+  T *push_keep(const std::vector<T> &v) {
+    size_t bytes = v.size() * sizeof(T);
+    if (bytes == 0) return nullptr;
+    if (record) return push(v);
+    void *dst = ctx->scratch.alloc(bytes);
+    Stage &st = ctx->stage;
+    size_t b = (bytes + 255) & ~size_t(255);
+    if (st.off + b > st.cap) {
+      sync_reset();
+      if (b > st.cap) {
+        st.release();
+        st.init(std::max(b * 2, st.cap * 2));
+      }
+    }
+    std::memcpy(st.h + st.off, v.data(), bytes);
+    CK(cudaMemcpyAsync(dst, st.h + st.off, bytes, cudaMemcpyHostToDevice, ctx->s));
+    st.off += b;
+    return (T *)dst;
+  }
+  double *scratch_d(size_t n) { return record ? persist->d(n) : ctx->scratch.d(n); }
+  int *scratch_i(size_t n) { return record ? persist->i(n) : ctx->scratch.i(n); }
+  void launch(std::function<void(cudaStream_t)> f) {
+    ctx->launches++;
+    if (record)
+      ops.push_back(std::move(f));
+    else
+      f(ctx->s);
+  }
+};
+
+static void check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw runtime_error(std::string("CUDA launch error: ") + cudaGetErrorString(e));
+}
+
+// ---- batched launch helpers -------------------------------------------------
+static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
+  if (jobs.empty()) return;
+  std::vector<int4> tiles;
+  for (int j = 0; j < (int)jobs.size(); ++j) {
+    const GemmJob &g = jobs[j];
+    if (g.m <= 0 || g.n <= 0) continue;
+    int tm = (int)cdiv(g.m, GEMM_BM), tn = (int)cdiv(g.n, GEMM_BN);
+    for (int a = 0; a < tm; ++a)
+      for (int b = 0; b < tn; ++b) tiles.push_back(make_int4(j, a, b, 0));
+  }
+  if (tiles.empty()) return;
+  GemmJob *dj = sk.push(jobs);
+  int4 *dt = sk.push(tiles);
+  int nt = (int)tiles.size();
+  int grid = std::min(nt, 148 * 16);
+  sk.launch([=](cudaStream_t s) {
+    k_gemm<<<grid, 256, 0, s>>>(dj, dt, nt);
+    check_launch();
+  });
+}
+
+static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
+  if (jobs.empty()) return;
+  int maxn = 0;
+  for (auto &j : jobs) maxn = std::max(maxn, j.n);
+  LuJob *dj = sk.push(jobs);
+  int nb = (int)jobs.size();
+  int th = maxn > 128 ? 512 : (maxn > 32 ? 256 : 64);
+  sk.launch([=](cudaStream_t s) {
+    k_getrf<<<nb, th, 0, s>>>(dj);
+    check_launch();
+  });
+}
+
+static void run_check_finite(Sink &sk, const std::vector<LuJob> &jobs) {
+  if (jobs.empty()) return;
+  LuJob *dj = sk.push(jobs);
+  int nb = (int)jobs.size();
+  sk.launch([=](cudaStream_t s) {
+    k_check_finite<<<nb, 256, 0, s>>>(dj);
+    check_launch();
+  });
+}
+
+static void run_getrs(Sink &sk, const std::vector<RsJob> &jobs) {
+  if (jobs.empty()) return;
+  RsJob *dj = sk.push(jobs);
+  int nb = (int)jobs.size();
+  sk.launch([=](cudaStream_t s) {
+    k_getrs<<<nb, 256, 0, s>>>(dj);
+    check_launch();
+  });
+}
+
+static void run_copy(Sink &sk, const std::vector<CopyJob> &jobs) {
+  for (size_t b = 0; b < jobs.size(); b += 60000) {
+    std::vector<CopyJob> part(jobs.begin() + b, jobs.begin() + std::min(jobs.size(), b + 60000));
+    int64_t mx = 0;
+    for (auto &j : part) mx = std::max<int64_t>(mx, (int64_t)j.m * j.n);
+    if (mx == 0) continue;
+    CopyJob *dj = sk.push(part);
+    dim3 grid((unsigned)std::min<int64_t>(cdiv(mx, 256), 64), (unsigned)part.size());
+    sk.launch([=](cudaStream_t s) {
+      k_copy<<<grid, 256, 0, s>>>(dj, 0);
+      check_launch();
+    });
+  }
+}
+
+static void run_identity(Sink &sk, const std::vector<double *> &ptrs, const std::vector<int> &dims,
+                         const std::vector<int> &lds) {
+  for (size_t b = 0; b < ptrs.size(); b += 60000) {
+    size_t e = std::min(ptrs.size(), b + 60000);
+    std::vector<double *> p(ptrs.begin() + b, ptrs.begin() + e);
+    std::vector<int> d(dims.begin() + b, dims.begin() + e), l(lds.begin() + b, lds.begin() + e);
+    int64_t mx = 0;
+    for (int x : d) mx = std::max<int64_t>(mx, (int64_t)x * x);
+    double **dp = sk.push(p);
+    int *dd = sk.push(d);
+    int *dl = sk.push(l);
+    dim3 grid((unsigned)std::min<int64_t>(cdiv(mx, 256), 64), (unsigned)p.size());
+    sk.launch([=](cudaStream_t s) {
+      k_identity<<<grid, 256, 0, s>>>(dp, dd, dl);
+      check_launch();
+    });
+  }
+}
+
+// ---------------------------------------------------------------------------
+// HODLR factor tree (device pointers kept on the host side)
+// ---------------------------------------------------------------------------
+struct FacView {  // DenseBlock.as_factors / LowRankFactor.as_factors (hodlr.py:59-63)
+  const double *col = nullptr;
+  int ldc = 0;
+  const double *row = nullptr;
+  int ldr = 0;
+  int rank = 0;
+};
+
+struct BlockH {
+  int fi = -1;
+  int r0 = 0, m = 0, c0 = 0, n = 0;
+  std::vector<int> I, J;
+  bool fullI = false, fullJ = false;
+  int kmax = 0;
+  // temporaries
+  double *R = nullptr, *C = nullptr, *core = nullptr;
+  int ldR = 0, ldC = 0;
+  int *d_I = nullptr, *d_J = nullptr, *d_inter = nullptr;
+  int *pint = nullptr;     // PLU int scratch
+  double *pdbl = nullptr;  // PLU double scratch
+  int *res = nullptr;      // device [rank,status,errk]
+  double *resd = nullptr;  // device [ratio, errpiv, errprev]
+  // results
+  int rank = 0, status = 0, errk = 0;
+  double ratio = 0.0, errpiv = 0.0, errprev = 0.0;
+  bool dense = false;
+  std::vector<int> rowperm, colperm;  // first `rank` pivots (parity log)
+  double *col = nullptr, *row = nullptr, *val = nullptr;
+  int64_t stored() const { return dense ? (int64_t)m * n : (int64_t)(m + n) * rank; }
+  int erank() const { return dense ? std::min(m, n) : rank; }
+  HBlk dev() const {
+    HBlk b{};
+    if (dense) {
+      b.kind = 1;
+      b.a = val;
+      b.lda = n;
+    } else {
+      b.kind = 0;
+      b.a = col;
+      b.lda = rank;
+      b.b = row;
+      b.ldb = n;
+      b.rank = rank;
+    }
+    return b;
+  }
+};
+
+struct HTree {
+  int fi = -1, base = 0, n = 0;
+  int nslots = 0;
+  std::vector<int> lo, hi, depth;
+  std::vector<char> leaf;  // 1 leaf, 0 internal, -1 absent
+  std::vector<int> up, lw;  // block ids
+  std::vector<double *> lval;  // leaf values (LU in place after factorization)
+  std::vector<int *> lpiv;
+  std::vector<int> lflag;  // flag slot
+  // factorization data (internal nodes)
+  std::vector<double *> xt, xb, core;
+  std::vector<int *> cpiv;
+  std::vector<int> r1, r2;
+  std::vector<FacView> f1, f2;
+  HNode *d_nodes = nullptr;
+  int maxdepth = 0;
+};
+
+// ---------------------------------------------------------------------------
+// factorization object
+// ---------------------------------------------------------------------------
+struct FrontH {
+  int64_t node = -1;
+  int npv = 0, nf = 0, nh = 0;
+  int64_t piv_lo = 0;
+  std::vector<int64_t> ids;
+  int height = 0;
+  bool structured = false;
+  std::vector<int> kids;  // fronts with a non-empty update, in node.children order
+  int64_t freed = 0;
+  long long *d_ids = nullptr;
+  // dense path
+  double *F = nullptr;
+  int *piv = nullptr;
+  // structured path
+  int pp = -1, ff = -1, pf = -1, fp = -1;  // tree / block ids
+  // update for the parent
+  int upd = -1;  // -1 none, 0 dense, 1 hodlr
+  const double *upd_dense = nullptr;
+  int upd_ld = 0;
+  const double *W = nullptr, *Vt = nullptr;
+  int rw = 0, ldw = 0, ldv = 0;
+  // accounting
+  int64_t front_reals = 0, factor_reals = 0, upd_reals = 0;
+  int64_t hint = 0;
+  int flag_slot = -1;
+};
+
+struct ApplyPlan;
+
+}  // namespace mfh
+
+struct mfh_ctx {
+  mfh::Ctx c;
+};
+
+struct mfh_factor {
+  mfh::Ctx *ctx = nullptr;
+  mfh::Arena arena;
+  int64_t n = 0;
+  int mode = 0;
+  mfh_params params{};
+  std::vector<int64_t> perm;
+  long long *d_perm = nullptr;
+  std::vector<mfh::FrontH> fronts;       // by post-order index
+  std::vector<int64_t> post;             // node ids in post order
+  std::vector<mfh::BlockH> blocks;
+  std::vector<mfh::HTree> trees;
+  std::vector<std::vector<int>> front_blocks;  // per front, block ids in visiting order
+  double *ident = nullptr;
+  int ident_ld = 0;
+  // stats
+  mfh_stats_t stats{};
+  std::vector<mfh_record_t> records;
+  mfh_timing_t timing{};
+  // apply
+  std::unique_ptr<mfh::ApplyPlan> apply;
+};
+
+namespace mfh {
+
+// ---------------------------------------------------------------------------
+// HODLR level-batched multi-RHS solve (hodlr.py:360-383)
+// ---------------------------------------------------------------------------
+struct HProblem {
+  const HTree *t;
+  int root;  // heap slot of the subtree root
+  double *rhs;
+  int ld, k;
+};
+
+static void collect_subtree(const HTree &t, int root, std::vector<int> &out) {
+  std::vector<int> st{root};
+  while (!st.empty()) {
+    int v = st.back();
+    st.pop_back();
+    out.push_back(v);
+    if (!t.leaf[v]) {
+      st.push_back(2 * v + 2);
+      st.push_back(2 * v + 1);
+    }
+  }
+}
+
+static void hodlr_solve_batched(Sink &sk, const std::vector<HProblem> &probs) {
+  if (probs.empty()) return;
+  std::vector<RsJob> leaves;
+  int maxd = 0;
+  struct Item {
+    int p, v;
+  };
+  std::vector<std::vector<Item>> bydepth;
+  for (int p = 0; p < (int)probs.size(); ++p) {
+    const HProblem &P = probs[p];
+    if (P.k == 0) continue;
+    std::vector<int> nodes;
+    collect_subtree(*P.t, P.root, nodes);
+    int base_lo = P.t->lo[P.root];
+    for (int v : nodes) {
+      if (P.t->leaf[v]) {
+        RsJob j{};
+        j.a = P.t->lval[v];
+        j.piv = P.t->lpiv[v];
+        j.n = P.t->hi[v] - P.t->lo[v];
+        j.lda = j.n;
+        j.b = P.rhs + (int64_t)(P.t->lo[v] - base_lo) * P.ld;
+        j.ldb = P.ld;
+        j.k = P.k;
+        if (j.n > 0) leaves.push_back(j);
+      } else {
+        int d = P.t->depth[v];
+        if ((int)bydepth.size() <= d) bydepth.resize(d + 1);
+        bydepth[d].push_back({p, v});
+        maxd = std::max(maxd, d);
+      }
+    }
+  }
+  run_getrs(sk, leaves);
+  for (int d = (int)bydepth.size() - 1; d >= 0; --d) {
+    auto &items = bydepth[d];
+    if (items.empty()) continue;
+    std::vector<GemmJob> g1, g2;
+    std::vector<RsJob> rs;
+    for (auto &it : items) {
+      const HProblem &P = probs[it.p];
+      const HTree &t = *P.t;
+      int v = it.v;
+      int r1 = t.r1[v], r2 = t.r2[v];
+      if (r1 + r2 == 0) continue;
+      int base_lo = t.lo[P.root];
+      int lo = t.lo[v], hi = t.hi[v], mid = (lo + hi) >> 1;
+      double *zt = P.rhs + (int64_t)(lo - base_lo) * P.ld;
+      double *zb = P.rhs + (int64_t)(mid - base_lo) * P.ld;
+      double *w = sk.scratch_d((size_t)(r1 + r2) * P.k);
+      // w_top = row_top @ z_bot ; w_bot = row_bot @ z_top
+      if (r1) g1.push_back(GemmJob{t.f1[v].row, zb, w, r1, P.k, hi - mid, t.f1[v].ldr, P.ld, P.k, 1.0, 0.0});
+      if (r2)
+        g1.push_back(GemmJob{t.f2[v].row, zt, w + (int64_t)r1 * P.k, r2, P.k, mid - lo, t.f2[v].ldr,
+                             P.ld, P.k, 1.0, 0.0});
+      rs.push_back(RsJob{t.core[v], t.cpiv[v], w, r1 + r2, r1 + r2, P.k, P.k});
+      if (r1) g2.push_back(GemmJob{t.xt[v], w, zt, mid - lo, P.k, r1, r1, P.k, P.ld, -1.0, 1.0});
+      if (r2)
+        g2.push_back(GemmJob{t.xb[v], w + (int64_t)r1 * P.k, zb, hi - mid, P.k, r2, r2, P.k, P.ld, -1.0, 1.0});
+    }
+    run_gemm(sk, g1);
+    run_getrs(sk, rs);
+    run_gemm(sk, g2);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the factorization driver
+// ---------------------------------------------------------------------------
+struct Factorizer {
+  mfh_factor *F;
+  Ctx *ctx;
+  const mfh_etree *et;
+  mfh_params P;
+  bool accel;
+  int64_t n;
+  // permuted matrix on device
+  std::vector<int64_t> ap_ptr;
+  std::vector<int> ap_col;
+  std::vector<double> ap_val;
+  long long *d_ap_ptr = nullptr;
+  int *d_ap_col = nullptr;
+  double *d_ap_val = nullptr;
+  Graph graph;  // BDLR graph over permuted ids
+  // selection scratch
+  std::vector<int64_t> mark;
+  int64_t stamp = 0;
+  std::vector<int> distv;
+  // error flags
+  int *d_flags = nullptr;
+  int nflags = 0;
+  std::vector<std::string> flag_msg;
+  std::vector<int64_t> flag_order;  // post index for ordering
+
+  Sink sk() { return Sink{ctx}; }
+
+  // ---- selection (bdlr.py:89-136), positions are front-local ----
+  void select(const FrontH &f, int r0, int m, int c0, int nn, std::vector<int> &I,
+              std::vector<int> &J) {
+    I.clear();
+    J.clear();
+    const int64_t *ids = f.ids.data();
+    if ((int64_t)mark.size() < graph.n) {
+      mark.assign(graph.n, 0);
+      distv.assign(graph.n, 0);
+    }
+    auto near_set = [&](int s0, int sn, int t0, int tn, std::vector<int> &out) {
+      // out = positions t in [t0,t0+tn) whose vertex is within distance d of {ids[s0..s0+sn)}
+      ++stamp;
+      if (P.d == 1) {
+        for (int s = s0; s < s0 + sn; ++s) mark[ids[s]] = stamp;
+        for (int t = t0; t < t0 + tn; ++t) {
+          int64_t v = ids[t];
+          for (int64_t q = graph.ptr[v]; q < graph.ptr[v + 1]; ++q)
+            if (mark[graph.idx[q]] == stamp) {
+              out.push_back(t);
+              break;
+            }
+        }
+        return;
+      }
+      std::vector<int64_t> queue;
+      for (int s = s0; s < s0 + sn; ++s) {
+        mark[ids[s]] = stamp;
+        distv[ids[s]] = 0;
+        queue.push_back(ids[s]);
+      }
+      size_t head = 0;
+      while (head < queue.size()) {
+        int64_t v = queue[head++];
+        if (distv[v] >= P.d) continue;
+        for (int64_t q = graph.ptr[v]; q < graph.ptr[v + 1]; ++q) {
+          int64_t w = graph.idx[q];
+          if (mark[w] != stamp) {
+            mark[w] = stamp;
+            distv[w] = distv[v] + 1;
+            queue.push_back(w);
+          }
+        }
+      }
+      for (int t = t0; t < t0 + tn; ++t) {
+        int64_t v = ids[t];
+        if (mark[v] == stamp && distv[v] <= P.d) out.push_back(t);
+      }
+    };
+    near_set(c0, nn, r0, m, I);
+    near_set(r0, m, c0, nn, J);
+    if (I.empty())
+      for (int t = r0; t < r0 + m; ++t) I.push_back(t);
+    if (J.empty())
+      for (int t = c0; t < c0 + nn; ++t) J.push_back(t);
+  }
+
+  int flag_cap = 0;
+  int new_flag(const std::string &msg, int64_t order) {
+    if (nflags >= flag_cap) throw runtime_error("internal: error-flag capacity exceeded");
+    flag_msg.push_back(msg);
+    flag_order.push_back(order);
+    return nflags++;
+  }
+
+  // ---- tree construction (hodlr.py:203-246 recursion order) ----
+  int make_tree(int fi, int base, int nloc, std::vector<int> &blist) {
+    HTree t;
+    t.fi = fi;
+    t.base = base;
+    t.n = nloc;
+    // slots
+    int cap = 1;
+    {
+      // depth bound
+      int d = 0;
+      int64_t s = nloc;
+      while (s > P.n_leaf) {
+        s = (s + 1) / 2;
+        ++d;
+      }
+      cap = (1 << (d + 2));
+    }
+    t.nslots = cap;
+    t.lo.assign(cap, -1);
+    t.hi.assign(cap, -1);
+    t.depth.assign(cap, 0);
+    t.leaf.assign(cap, -1);
+    t.up.assign(cap, -1);
+    t.lw.assign(cap, -1);
+    t.lval.assign(cap, nullptr);
+    t.lpiv.assign(cap, nullptr);
+    t.lflag.assign(cap, -1);
+    t.xt.assign(cap, nullptr);
+    t.xb.assign(cap, nullptr);
+    t.core.assign(cap, nullptr);
+    t.cpiv.assign(cap, nullptr);
+    t.r1.assign(cap, 0);
+    t.r2.assign(cap, 0);
+    t.f1.assign(cap, FacView{});
+    t.f2.assign(cap, FacView{});
+    F->trees.push_back(std::move(t));
+    int tid = (int)F->trees.size() - 1;
+    // recursion with explicit stack: (slot, lo, hi, depth, stage)
+    struct Fr {
+      int v, lo, hi, d, stage;
+    };
+    std::vector<Fr> st{{0, 0, nloc, 0, 0}};
+    while (!st.empty()) {
+      Fr &fr = st.back();
+      HTree &T = F->trees[tid];
+      if (fr.stage == 0) {
+        T.lo[fr.v] = fr.lo;
+        T.hi[fr.v] = fr.hi;
+        T.depth[fr.v] = fr.d;
+        T.maxdepth = std::max(T.maxdepth, fr.d);
+        if (fr.hi - fr.lo <= P.n_leaf) {
+          T.leaf[fr.v] = 1;
+          st.pop_back();
+          continue;
+        }
+        T.leaf[fr.v] = 0;
+        fr.stage = 1;
+        int mid = (fr.lo + fr.hi) >> 1;
+        Fr c{2 * fr.v + 1, fr.lo, mid, fr.d + 1, 0};
+        st.push_back(c);
+      } else if (fr.stage == 1) {
+        fr.stage = 2;
+        int mid = (fr.lo + fr.hi) >> 1;
+        Fr c{2 * fr.v + 2, mid, fr.hi, fr.d + 1, 0};
+        st.push_back(c);
+      } else {
+        int lo = fr.lo, hi = fr.hi, mid = (lo + hi) >> 1;
+        int v = fr.v;
+        st.pop_back();
+        int bu = new_block(fi, base + lo, mid - lo, base + mid, hi - mid);
+        int bl = new_block(fi, base + mid, hi - mid, base + lo, mid - lo);
+        F->trees[tid].up[v] = bu;
+        F->trees[tid].lw[v] = bl;
+        blist.push_back(bu);
+        blist.push_back(bl);
+      }
+    }
+    return tid;
+  }
+
+  int new_block(int fi, int r0, int m, int c0, int nn) {
+    BlockH b;
+    b.fi = fi;
+    b.r0 = r0;
+    b.m = m;
+    b.c0 = c0;
+    b.n = nn;
+    F->blocks.push_back(std::move(b));
+    return (int)F->blocks.size() - 1;
+  }
+
+  void check_flags(int64_t upto_flags) {
+    if (nflags == 0) return;
+    std::vector<int> h(nflags);
+    CK(cudaMemcpy(h.data(), d_flags, sizeof(int) * nflags, cudaMemcpyDeviceToHost));
+    int best = -1;
+    for (int q = 0; q < nflags; ++q)
+      if (h[q] && (best < 0 || flag_order[q] < flag_order[best])) best = q;
+    if (best >= 0) throw value_error(flag_msg[best]);
+    (void)upto_flags;
+  }
+
+  // ---- child descriptors + to_child maps for a set of fronts ----
+  void build_fronts_dev(Sink &s, const std::vector<int> &fis, std::vector<DFront> &dfr,
+                        std::vector<DChild> &dch, std::vector<int> &slot_of) {
+    slot_of.assign(F->fronts.size(), -1);
+    for (int fi : fis) {
+      FrontH &f = F->fronts[fi];
+      DFront d{};
+      d.ids = f.d_ids;
+      d.nh = f.nh;
+      d.npv = f.npv;
+      d.child_begin = (int)dch.size();
+      for (int ci : f.kids) {
+        FrontH &c = F->fronts[ci];
+        // to_child map: parent position -> child update position (multifrontal.py:270-280, 321-327)
+        std::vector<int> to(f.nh, -1);
+        const int64_t *cid = c.ids.data() + c.npv;
+        int cn = c.nf;
+        int p = 0;
+        for (int q = 0; q < cn; ++q) {
+          int64_t g = cid[q];
+          while (p < f.nh && f.ids[p] < g) ++p;
+          if (p >= f.nh || f.ids[p] != g)
+            throw value_error("update index " + std::to_string(g) + " not present in parent front (node " +
+                              std::to_string(f.node) + ")");
+          to[p] = q;
+        }
+        DChild ch{};
+        ch.to_child = s.push_keep(to);
+        ch.n = cn;
+        if (c.upd == 0) {
+          ch.kind = 0;
+          ch.dense = c.upd_dense;
+          ch.ldd = c.upd_ld;
+        } else {
+          ch.kind = 1;
+          ch.hn = F->trees[c.ff].d_nodes;
+          ch.W = c.W;
+          ch.Vt = c.Vt;
+          ch.rw = c.rw;
+          ch.ldw = c.ldw;
+          ch.ldv = c.ldv;
+        }
+        dch.push_back(ch);
+      }
+      d.child_end = (int)dch.size();
+      slot_of[fi] = (int)dfr.size();
+      dfr.push_back(d);
+    }
+  }
+
+  void run_sample(Sink &s, const std::vector<SReq> &reqs, DFront *dF, DChild *dC) {
+    if (reqs.empty()) return;
+    std::vector<int2> tiles;
+    for (int q = 0; q < (int)reqs.size(); ++q) {
+      int64_t nt = cdiv(reqs[q].nr, SAMPLE_TR) * cdiv(reqs[q].nc, SAMPLE_TC);
+      for (int64_t t = 0; t < nt; ++t) tiles.push_back(make_int2(q, (int)t));
+      F->timing.sample_entries += (double)reqs[q].nr * reqs[q].nc;
+    }
+    if (tiles.empty()) return;
+    SReq *dr = s.push(reqs);
+    int2 *dt = s.push(tiles);
+    int nt = (int)tiles.size();
+    long long *pp = d_ap_ptr;
+    int *pc = d_ap_col;
+    double *pv = d_ap_val;
+    int grid = std::min(nt, 148 * 32);
+    s.launch([=](cudaStream_t st) {
+      k_sample<<<grid, dim3(SAMPLE_TC, SAMPLE_TR), 0, st>>>(dr, dt, nt, dF, dC, pp, pc, pv);
+      check_launch();
+    });
+  }
+
+  FacView as_factors(const BlockH &b) {
+    FacView v;
+    if (!b.dense) {
+      v.col = b.col;
+      v.ldc = b.rank;
+      v.row = b.row;
+      v.ldr = b.n;
+      v.rank = b.rank;
+      return v;
+    }
+    if (b.n <= b.m) {
+      v.col = b.val;
+      v.ldc = b.n;
+      v.row = F->ident;
+      v.ldr = F->ident_ld;
+      v.rank = b.n;
+    } else {
+      v.col = F->ident;
+      v.ldc = F->ident_ld;
+      v.row = b.val;
+      v.ldr = b.n;
+      v.rank = b.m;
+    }
+    return v;
+  }
+
+  // ---- one height ----
+  void process_height(const std::vector<int> &fis, cudaEvent_t *ev) {
+    Sink s{ctx};
+    std::vector<int> D, S;
+    for (int fi : fis) (F->fronts[fi].structured ? S : D).push_back(fi);
+    std::vector<DFront> dfr;
+    std::vector<DChild> dch;
+    std::vector<int> slot;
+    build_fronts_dev(s, fis, dfr, dch, slot);
+    DFront *dF = s.push_keep(dfr);
+    DChild *dC = dch.empty() ? nullptr : s.push_keep(dch);
+
+    std::vector<SReq> reqs;
+    // ------------------------------------------------ dense fronts: assemble
+    for (int fi : D) {
+      FrontH &f = F->fronts[fi];
+      f.F = F->arena.d((size_t)f.nh * f.nh);
+      if (f.npv) f.piv = F->arena.i(f.npv);
+      reqs.push_back(SReq{slot[fi], f.nh, f.nh, nullptr, nullptr, 0, 0, f.F, f.nh});
+    }
+    // ------------------------------------------------ structured: plan blocks
+    std::vector<int> sblocks;  // all compressed blocks at this height
+    for (int fi : S) {
+      FrontH &f = F->fronts[fi];
+      std::vector<int> blist;
+      if (f.npv) f.pp = make_tree(fi, 0, f.npv, blist);
+      if (f.npv && f.nf) {
+        f.pf = new_block(fi, 0, f.npv, f.npv, f.nf);
+        f.fp = new_block(fi, f.npv, f.nf, 0, f.npv);
+        blist.push_back(f.pf);
+        blist.push_back(f.fp);
+      }
+      if (f.nf) f.ff = make_tree(fi, f.npv, f.nf, blist);
+      F->front_blocks[fi] = blist;
+      sblocks.insert(sblocks.end(), blist.begin(), blist.end());
+      // leaves: sampled straight into their storage
+      for (int tt : {f.pp, f.ff}) {
+        if (tt < 0) continue;
+        HTree &T = F->trees[tt];
+        for (int v = 0; v < T.nslots; ++v)
+          if (T.leaf[v] == 1) {
+            int sz = T.hi[v] - T.lo[v];
+            T.lval[v] = F->arena.d((size_t)sz * sz);
+            reqs.push_back(SReq{slot[fi], sz, sz, nullptr, nullptr, T.base + T.lo[v], T.base + T.lo[v],
+                                T.lval[v], sz});
+          }
+      }
+    }
+    auto t_sel0 = std::chrono::steady_clock::now();
+    std::vector<CopyJob> core_copies;
+    std::vector<PluJob> plu;
+    // one contiguous int / double scratch for every core of the height, so the
+    // ranks and pivot sequences come back in a single D2H copy
+    int64_t itot = 0, dtot = 0;
+    std::vector<int64_t> ioff, doff;
+    for (int bi : sblocks) {
+      BlockH &b = F->blocks[bi];
+      FrontH &f = F->fronts[b.fi];
+      select(f, b.r0, b.m, b.c0, b.n, b.I, b.J);
+      ioff.push_back(itot);
+      doff.push_back(dtot);
+      itot += 4 * ((int64_t)b.I.size() + b.J.size()) + 3;
+      dtot += (int64_t)b.I.size() + b.J.size() + 3;
+    }
+    int *pint_all = sblocks.empty() ? nullptr : ctx->scratch.i(itot);
+    double *pdbl_all = sblocks.empty() ? nullptr : ctx->scratch.d(dtot);
+    for (size_t qb = 0; qb < sblocks.size(); ++qb) {
+      int bi = sblocks[qb];
+      BlockH &b = F->blocks[bi];
+      b.fullI = (int)b.I.size() == b.m;
+      b.fullJ = (int)b.J.size() == b.n;
+      int nI = (int)b.I.size(), nJ = (int)b.J.size();
+      int cap = P.max_rank >= 0 ? (int)P.max_rank : std::min(nI, nJ);
+      if (cap < 1) throw value_error("max_rank must be at least 1");
+      b.kmax = std::min(std::min(nI, nJ), cap);
+      // R = B(I, :)
+      b.R = ctx->scratch.d((size_t)nI * b.n);
+      b.ldR = b.n;
+      b.d_I = b.fullI ? nullptr : s.push(b.I);
+      reqs.push_back(SReq{slot[b.fi], nI, b.n, b.d_I, nullptr, b.I[0], b.c0, b.R, b.ldR});
+      if (b.fullI && b.fullJ) {
+        b.C = b.R;
+        b.ldC = b.n;
+      } else {
+        b.C = ctx->scratch.d((size_t)b.m * nJ);
+        b.ldC = nJ;
+        b.d_J = b.fullJ ? nullptr : s.push(b.J);
+        reqs.push_back(SReq{slot[b.fi], b.m, nJ, nullptr, b.d_J, b.r0, b.J[0], b.C, b.ldC});
+      }
+      // core = R[:, J - c0]
+      b.core = ctx->scratch.d((size_t)nI * nJ);
+      std::vector<int> inter(nJ);
+      for (int q = 0; q < nJ; ++q) inter[q] = b.J[q] - b.c0;
+      b.d_inter = b.fullJ ? nullptr : s.push(inter);
+      core_copies.push_back(CopyJob{b.R, b.core, nI, nJ, b.ldR, nJ, nullptr, b.d_inter});
+      // PLU scratch
+      b.pint = pint_all + ioff[qb];
+      b.pdbl = pdbl_all + doff[qb];
+      PluJob j{};
+      j.a = b.core;
+      j.m = nI;
+      j.n = nJ;
+      j.ld = nJ;
+      j.kmax = b.kmax;
+      int *pi = b.pint;
+      j.rowAt = pi;
+      j.posR = pi + nI;
+      j.actR = pi + 2 * nI;
+      j.idxR = pi + 3 * nI;
+      pi += 4 * nI;
+      j.colAt = pi;
+      j.posC = pi + nJ;
+      j.actC = pi + 2 * nJ;
+      j.idxC = pi + 3 * nJ;
+      pi += 4 * nJ;
+      j.out = pi;
+      b.res = pi;
+      j.mult = b.pdbl;
+      j.prow = b.pdbl + nI;
+      j.outd = b.pdbl + nI + nJ;
+      b.resd = j.outd;
+      plu.push_back(j);
+      F->timing.pivot_lu_visits += 0;  // filled after ranks are known
+    }
+    F->timing.host_ms +=
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_sel0).count();
+
+    cudaEventRecord(ev[0], ctx->s);
+    run_sample(s, reqs, dF, dC);
+    cudaEventRecord(ev[1], ctx->s);
+
+    // ------------------------------------------------ dense fronts: eliminate
+    {
+      std::vector<LuJob> lus;
+      std::vector<CopyJob> cps;
+      std::vector<RsJob> rss;
+      std::vector<GemmJob> gms;
+      for (int fi : D) {
+        FrontH &f = F->fronts[fi];
+        if (!f.npv) continue;
+        f.flag_slot = new_flag("singular pivot block at node " + std::to_string(f.node), fi);
+        lus.push_back(LuJob{f.F, f.npv, f.nh, f.piv, d_flags + f.flag_slot});
+        if (f.nf) {
+          double *X = ctx->scratch.d((size_t)f.npv * f.nf);
+          cps.push_back(CopyJob{f.F + f.npv, X, f.npv, f.nf, f.nh, f.nf, nullptr, nullptr});
+          rss.push_back(RsJob{f.F, f.piv, X, f.npv, f.nh, f.nf, f.nf});
+          gms.push_back(GemmJob{f.F + (int64_t)f.npv * f.nh, X, f.F + (int64_t)f.npv * f.nh + f.npv, f.nf,
+                                f.nf, f.npv, f.nh, f.nf, f.nh, -1.0, 1.0});
+        }
+      }
+      run_getrf(s, lus);
+      run_copy(s, cps);
+      run_getrs(s, rss);
+      run_gemm(s, gms);
+      for (int fi : D) {
+        FrontH &f = F->fronts[fi];
+        if (f.nf) {
+          f.upd = 0;
+          f.upd_dense = f.F + (int64_t)f.npv * f.nh + f.npv;
+          f.upd_ld = f.nh;
+        }
+        f.front_reals = (int64_t)f.nh * f.nh;
+        f.factor_reals = (f.npv ? (int64_t)f.npv * f.npv : 0) + 2 * (int64_t)f.npv * f.nf;
+        f.upd_reals = (int64_t)f.nf * f.nf;
+      }
+    }
+    cudaEventRecord(ev[2], ctx->s);
+    if (S.empty()) {
+      for (int q = 3; q < 8; ++q) cudaEventRecord(ev[q], ctx->s);
+      return;
+    }
+
+    // ------------------------------------------------ structured: pivot LU
+    run_copy(s, core_copies);
+    {
+      PluJob *dj = s.push(plu);
+      int nb = (int)plu.size();
+      double eps = P.eps;
+      s.launch([=](cudaStream_t st) {
+        k_full_pivot_lu<<<nb, 512, 0, st>>>(dj, eps);
+        check_launch();
+      });
+    }
+    cudaEventRecord(ev[3], ctx->s);
+    // read ranks, status and pivot sequences: one D2H pair for the height
+    {
+      std::vector<int> hi(itot);
+      std::vector<double> hd(dtot);
+      CK(cudaMemcpyAsync(hi.data(), pint_all, sizeof(int) * itot, cudaMemcpyDeviceToHost, ctx->s));
+      CK(cudaMemcpyAsync(hd.data(), pdbl_all, sizeof(double) * dtot, cudaMemcpyDeviceToHost, ctx->s));
+      s.sync_reset();
+      check_flags(0);
+      int first_err = -1;
+      for (size_t q = 0; q < sblocks.size(); ++q) {
+        BlockH &b = F->blocks[sblocks[q]];
+        int nI = (int)b.I.size(), nJ = (int)b.J.size();
+        const int *p = hi.data() + ioff[q];
+        const int *out = p + 4 * (nI + nJ);
+        const double *od = hd.data() + doff[q] + nI + nJ;
+        b.rank = out[0];
+        b.status = out[1];
+        b.errk = out[2];
+        b.ratio = od[0];
+        b.errpiv = od[1];
+        b.errprev = od[2];
+        if (b.status && first_err < 0) first_err = (int)q;
+        b.rowperm.assign(p, p + b.rank);
+        b.colperm.assign(p + 4 * nI, p + 4 * nI + b.rank);
+        // algorithmic visits: sum_{k < min(rank+1, min(I,J))} (|I|-k)(|J|-k)
+        int kk = std::min(b.rank + 1, std::min(nI, nJ));
+        double vis = 0;
+        for (int k = 0; k < kk; ++k) vis += (double)(nI - k) * (nJ - k);
+        F->timing.pivot_lu_visits += vis;
+      }
+      if (first_err >= 0) {
+        BlockH &b = F->blocks[sblocks[first_err]];
+        char buf[256];
+        snprintf(buf, sizeof buf, "pivot %d magnitude %.3e exceeds twice the previous %.3e", b.errk,
+                 b.errpiv, b.errprev);
+        throw Error(MFH_EPIVOT, buf);
+      }
+    }
+    // ------------------------------------------------ decisions + skeletons
+    std::vector<LuExtractJob> lux;
+    std::vector<SkelJob> skel;
+    std::vector<SReq> dreq;
+    for (int bi : sblocks) {
+      BlockH &b = F->blocks[bi];
+      int nI = (int)b.I.size(), nJ = (int)b.J.size();
+      bool capped = P.max_rank >= 0 && b.rank == P.max_rank;
+      bool full = b.fullI && b.fullJ;
+      bool exhausted = b.rank == std::min(nI, nJ);
+      bool unc = exhausted && !full && !capped;  // strict certificate (hodlr.py:92-97)
+      int64_t lr_stored = (int64_t)(b.m + b.n) * b.rank;
+      b.dense = unc || lr_stored > (int64_t)b.m * b.n;
+      if (b.dense) {
+        b.val = F->arena.d((size_t)b.m * b.n);
+        dreq.push_back(SReq{slot[b.fi], b.m, b.n, nullptr, nullptr, b.r0, b.c0, b.val, b.n});
+        F->stats.n_dense_fallback++;
+      } else if (b.rank > 0) {
+        int r = b.rank;
+        double *lu = ctx->scratch.d((size_t)r * r);
+        lux.push_back(LuExtractJob{b.core, nJ, r, b.pint, b.pint + 4 * nI, lu});
+        b.row = F->arena.d((size_t)r * b.n);
+        b.col = F->arena.d((size_t)b.m * r);
+        SkelJob sj{};
+        sj.lu = lu;
+        sj.r = r;
+        sj.R = b.R;
+        sj.ldR = b.ldR;
+        sj.n = b.n;
+        sj.rp = b.pint;
+        sj.C = b.C;
+        sj.ldC = b.ldC;
+        sj.m = b.m;
+        sj.cp = b.pint + 4 * nI;
+        sj.row_out = b.row;
+        sj.col_out = b.col;
+        skel.push_back(sj);
+      }
+      F->stats.n_blocks++;
+    }
+    cudaEventRecord(ev[4], ctx->s);
+    if (!lux.empty()) {
+      LuExtractJob *dj = s.push(lux);
+      int64_t mx = 0;
+      for (auto &j : lux) mx = std::max<int64_t>(mx, (int64_t)j.r * j.r);
+      for (size_t b0 = 0; b0 < lux.size(); b0 += 60000) {
+        unsigned cnt = (unsigned)std::min<size_t>(60000, lux.size() - b0);
+        LuExtractJob *p = dj + b0;
+        dim3 grid((unsigned)std::min<int64_t>(cdiv(mx, 256), 32), cnt);
+        s.launch([=](cudaStream_t st) {
+          k_lu_extract<<<grid, 256, 0, st>>>(p);
+          check_launch();
+        });
+      }
+      SkelJob *dsj = s.push(skel);
+      std::vector<int2> rch, cch;
+      for (int q = 0; q < (int)skel.size(); ++q) {
+        for (int c = 0; c < (int)cdiv(skel[q].n, 128); ++c) rch.push_back(make_int2(q, c));
+        for (int c = 0; c < (int)cdiv(skel[q].m, 128); ++c) cch.push_back(make_int2(q, c));
+      }
+      int2 *drc = s.push(rch), *dcc = s.push(cch);
+      int nr = (int)rch.size(), nc = (int)cch.size();
+      s.launch([=](cudaStream_t st) {
+        k_skel_row<<<std::min(nr, 148 * 16), 128, 0, st>>>(dsj, drc, nr);
+        check_launch();
+        k_skel_col<<<std::min(nc, 148 * 16), 128, 0, st>>>(dsj, dcc, nc);
+        check_launch();
+      });
+    }
+    run_sample(s, dreq, dF, dC);
+    cudaEventRecord(ev[5], ctx->s);
+
+    // ------------------------------------------------ device HNode tables
+    for (int fi : S) {
+      FrontH &f = F->fronts[fi];
+      for (int tt : {f.pp, f.ff}) {
+        if (tt < 0) continue;
+        HTree &T = F->trees[tt];
+        std::vector<HNode> nodes(T.nslots);
+        for (int v = 0; v < T.nslots; ++v) {
+          HNode h{};
+          if (T.leaf[v] == 1)
+            h.leaf = T.lval[v];
+          else if (T.leaf[v] == 0) {
+            h.up = F->blocks[T.up[v]].dev();
+            h.lw = F->blocks[T.lw[v]].dev();
+          }
+          nodes[v] = h;
+        }
+        T.d_nodes = (HNode *)F->arena.alloc(sizeof(HNode) * nodes.size());
+        CK(cudaMemcpyAsync(T.d_nodes, nodes.data(), sizeof(HNode) * nodes.size(), cudaMemcpyHostToDevice,
+                           ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));  // host vector goes out of scope
+      }
+    }
+
+    // ------------------------------------------------ HODLR factorization of pp
+    std::vector<int> ptrees;
+    for (int fi : S)
+      if (F->fronts[fi].pp >= 0) ptrees.push_back(F->fronts[fi].pp);
+    {
+      std::vector<LuJob> leaves;
+      for (int tt : ptrees) {
+        HTree &T = F->trees[tt];
+        for (int v = 0; v < T.nslots; ++v)
+          if (T.leaf[v] == 1) {
+            int sz = T.hi[v] - T.lo[v];
+            T.lpiv[v] = F->arena.i(sz);
+            std::string msg = "singular pivot in leaf block [" + std::to_string(T.lo[v]) + ", " +
+                              std::to_string(T.hi[v]) + ")";
+            T.lflag[v] = new_flag(msg, (int64_t)T.fi * 1000000 + v);
+            leaves.push_back(LuJob{T.lval[v], sz, sz, T.lpiv[v], d_flags + T.lflag[v]});
+          }
+      }
+      run_getrf(s, leaves);
+      int maxd = 0;
+      for (int tt : ptrees) maxd = std::max(maxd, F->trees[tt].maxdepth);
+      for (int d = maxd; d >= 0; --d) {
+        std::vector<CopyJob> cps;
+        std::vector<HProblem> probs;
+        std::vector<std::pair<int, int>> nodes;
+        for (int tt : ptrees) {
+          HTree &T = F->trees[tt];
+          for (int v = 0; v < T.nslots; ++v) {
+            if (T.leaf[v] != 0 || T.depth[v] != d) continue;
+            nodes.push_back({tt, v});
+            FacView f1 = as_factors(F->blocks[T.up[v]]);
+            FacView f2 = as_factors(F->blocks[T.lw[v]]);
+            T.f1[v] = f1;
+            T.f2[v] = f2;
+            int lo = T.lo[v], hi = T.hi[v], mid = (lo + hi) >> 1;
+            int m1 = mid - lo, m2 = hi - mid;
+            T.r1[v] = f1.rank;
+            T.r2[v] = f2.rank;
+            T.xt[v] = F->arena.d((size_t)m1 * std::max(1, f1.rank));
+            T.xb[v] = F->arena.d((size_t)m2 * std::max(1, f2.rank));
+            if (f1.rank) {
+              cps.push_back(CopyJob{f1.col, T.xt[v], m1, f1.rank, f1.ldc, f1.rank, nullptr, nullptr});
+              probs.push_back(HProblem{&T, 2 * v + 1, T.xt[v], f1.rank, f1.rank});
+            }
+            if (f2.rank) {
+              cps.push_back(CopyJob{f2.col, T.xb[v], m2, f2.rank, f2.ldc, f2.rank, nullptr, nullptr});
+              probs.push_back(HProblem{&T, 2 * v + 2, T.xb[v], f2.rank, f2.rank});
+            }
+          }
+        }
+        if (nodes.empty()) continue;
+        run_copy(s, cps);
+        hodlr_solve_batched(s, probs);
+        // Woodbury cores
+        std::vector<double *> ip;
+        std::vector<int> idim, ild;
+        std::vector<GemmJob> gms;
+        std::vector<LuJob> lus;
+        for (auto &nv : nodes) {
+          HTree &T = F->trees[nv.first];
+          int v = nv.second;
+          int r1 = T.r1[v], r2 = T.r2[v];
+          if (r1 + r2 == 0) continue;
+          int lo = T.lo[v], hi = T.hi[v], mid = (lo + hi) >> 1;
+          int rr = r1 + r2;
+          T.core[v] = F->arena.d((size_t)rr * rr);
+          T.cpiv[v] = F->arena.i(rr);
+          ip.push_back(T.core[v]);
+          idim.push_back(rr);
+          ild.push_back(rr);
+          // core[:r1, r1:] += row_top @ x_bot ; core[r1:, :r1] += row_bot @ x_top
+          if (r1 && r2) {
+            gms.push_back(GemmJob{T.f1[v].row, T.xb[v], T.core[v] + r1, r1, r2, hi - mid, T.f1[v].ldr, r2, rr,
+                                  1.0, 1.0});
+            gms.push_back(GemmJob{T.f2[v].row, T.xt[v], T.core[v] + (int64_t)r1 * rr, r2, r1, mid - lo,
+                                  T.f2[v].ldr, r1, rr, 1.0, 1.0});
+          }
+          std::string msg = "singular coupling core at node [" + std::to_string(lo) + ", " +
+                            std::to_string(hi) + ")";
+          int fl = new_flag(msg, (int64_t)T.fi * 1000000 + v);
+          lus.push_back(LuJob{T.core[v], rr, rr, T.cpiv[v], d_flags + fl});
+        }
+        run_identity(s, ip, idim, ild);
+        run_gemm(s, gms);
+        run_check_finite(s, lus);
+        run_getrf(s, lus);
+      }
+    }
+    cudaEventRecord(ev[6], ctx->s);
+
+    // ------------------------------------------------ eliminate_hodlr (W, V)
+    {
+      std::vector<CopyJob> cps;
+      std::vector<HProblem> probs;
+      struct El {
+        int fi;
+        FacView pf, fp;
+        double *x;
+      };
+      std::vector<El> els;
+      for (int fi : S) {
+        FrontH &f = F->fronts[fi];
+        if (!(f.npv && f.nf)) continue;
+        El e;
+        e.fi = fi;
+        e.pf = as_factors(F->blocks[f.pf]);
+        e.fp = as_factors(F->blocks[f.fp]);
+        e.x = ctx->scratch.d((size_t)f.npv * std::max(1, e.pf.rank));
+        if (e.pf.rank) {
+          cps.push_back(CopyJob{e.pf.col, e.x, f.npv, e.pf.rank, e.pf.ldc, e.pf.rank, nullptr, nullptr});
+          probs.push_back(HProblem{&F->trees[f.pp], 0, e.x, e.pf.rank, e.pf.rank});
+        }
+        els.push_back(e);
+      }
+      run_copy(s, cps);
+      hodlr_solve_batched(s, probs);
+      std::vector<GemmJob> g1, g2;
+      for (auto &e : els) {
+        FrontH &f = F->fronts[e.fi];
+        int rpf = e.pf.rank, rfp = e.fp.rank;
+        if (rpf == 0 || rfp == 0) {
+          // outer product of rank min(r_pf, r_fp) = 0 after the branch below
+        }
+        double *core = ctx->scratch.d((size_t)std::max(1, rfp) * std::max(1, rpf));
+        if (rfp && rpf)
+          g1.push_back(GemmJob{e.fp.row, e.x, core, rfp, rpf, f.npv, e.fp.ldr, rpf, rpf, 1.0, 0.0});
+        if (rpf <= rfp) {
+          // W = col_fp @ core (nf x r_pf), V = row_pf^T  -> Vt = row_pf
+          f.rw = rpf;
+          if (rpf) {
+            double *W = F->arena.d((size_t)f.nf * rpf);
+            g2.push_back(GemmJob{e.fp.col, core, W, f.nf, rpf, rfp, e.fp.ldc, rpf, rpf, 1.0, 0.0});
+            f.W = W;
+            f.ldw = rpf;
+            f.Vt = e.pf.row;
+            f.ldv = e.pf.ldr;
+          }
+        } else {
+          // W = col_fp, V = (core @ row_pf)^T -> Vt = core @ row_pf (r_fp x nf)
+          f.rw = rfp;
+          f.W = e.fp.col;
+          f.ldw = e.fp.ldc;
+          double *Vt = F->arena.d((size_t)rfp * f.nf);
+          g2.push_back(GemmJob{core, e.pf.row, Vt, rfp, f.nf, rpf, rpf, e.pf.ldr, f.nf, 1.0, 0.0});
+          f.Vt = Vt;
+          f.ldv = f.nf;
+        }
+      }
+      run_gemm(s, g1);
+      run_gemm(s, g2);
+    }
+    cudaEventRecord(ev[7], ctx->s);
+
+    // ------------------------------------------------ accounting (host)
+    for (int fi : S) {
+      FrontH &f = F->fronts[fi];
+      auto tree_stored = [&](int tt) -> int64_t {
+        if (tt < 0) return 0;
+        HTree &T = F->trees[tt];
+        int64_t s2 = 0;
+        for (int v = 0; v < T.nslots; ++v) {
+          if (T.leaf[v] == 1) {
+            int64_t sz = T.hi[v] - T.lo[v];
+            s2 += sz * sz;
+          } else if (T.leaf[v] == 0) {
+            s2 += F->blocks[T.up[v]].stored() + F->blocks[T.lw[v]].stored();
+          }
+        }
+        return s2;
+      };
+      auto tree_hint = [&](int tt) -> int64_t {
+        if (tt < 0) return 0;
+        HTree &T = F->trees[tt];
+        int64_t h = 0;
+        for (int v = 0; v < T.nslots; ++v)
+          if (T.leaf[v] == 0)
+            h = std::max<int64_t>(h, std::max(F->blocks[T.up[v]].erank(), F->blocks[T.lw[v]].erank()));
+        return h;
+      };
+      auto factor_stored = [&](int tt) -> int64_t {
+        if (tt < 0) return 0;
+        HTree &T = F->trees[tt];
+        int64_t s2 = 0;
+        for (int v = 0; v < T.nslots; ++v) {
+          if (T.leaf[v] == 1) {
+            int64_t sz = T.hi[v] - T.lo[v];
+            s2 += sz * sz;
+          } else if (T.leaf[v] == 0) {
+            int lo = T.lo[v], hi = T.hi[v], mid = (lo + hi) >> 1;
+            int64_t m1 = mid - lo, m2 = hi - mid, r1 = T.r1[v], r2 = T.r2[v];
+            s2 += m1 * r1 + m2 * r2 + r1 * m2 + r2 * m1;
+            if (r1 + r2) s2 += (r1 + r2) * (r1 + r2);
+          }
+        }
+        return s2;
+      };
+      int64_t pfs = f.pf >= 0 ? F->blocks[f.pf].stored() : 0;
+      int64_t fps = f.fp >= 0 ? F->blocks[f.fp].stored() : 0;
+      f.front_reals = tree_stored(f.pp) + pfs + fps + tree_stored(f.ff);
+      f.factor_reals = factor_stored(f.pp) + pfs + fps;
+      f.upd_reals = f.nf ? tree_stored(f.ff) + 2 * (int64_t)f.nf * f.rw : 0;
+      int64_t h = std::max(tree_hint(f.pp), tree_hint(f.ff));
+      if (f.pf >= 0) h = std::max<int64_t>(h, F->blocks[f.pf].erank());
+      if (f.fp >= 0) h = std::max<int64_t>(h, F->blocks[f.fp].erank());
+      f.hint = h;
+      if (f.nf) f.upd = 1;
+      // structured_alloc_note(nf) on x, W, V (multifrontal.py:421-438)
+      if (f.npv && f.nf) {
+        int64_t rpf = as_factors(F->blocks[f.pf]).rank;
+        auto note = [&](int64_t r, int64_t c) {
+          if (f.nf > 0 && r >= f.nf && c >= f.nf) F->stats.full_square_allocs++;
+        };
+        note(f.npv, rpf);
+        note(f.nf, f.rw);
+        note(f.nf, f.rw);
+      }
+    }
+  }
+
+  void run(const HostCsr &A, int mode) {
+    auto t0 = std::chrono::steady_clock::now();
+    n = A.n;
+    accel = mode == MFH_ACCELERATED;
+    F->n = n;
+    F->perm = et->perm;
+    F->mode = mode;
+    F->params = P;
+    // ---- P A P^T as CSR (multifrontal.py:245-250)
+    {
+      const std::vector<int64_t> &perm = et->perm;
+      std::vector<int64_t> cnt(n + 1, 0);
+      for (int64_t i = 0; i < n; ++i) cnt[perm[i] + 1] += A.ptr[i + 1] - A.ptr[i];
+      for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+      ap_ptr = cnt;
+      ap_col.resize(cnt[n]);
+      ap_val.resize(cnt[n]);
+      std::vector<std::pair<int, double>> row;
+      for (int64_t i = 0; i < n; ++i) {
+        int64_t pi = perm[i];
+        row.clear();
+        for (int64_t p = A.ptr[i]; p < A.ptr[i + 1]; ++p) row.push_back({(int)perm[A.idx[p]], A.val[p]});
+        std::sort(row.begin(), row.end(), [](auto &a, auto &b) { return a.first < b.first; });
+        int64_t q = ap_ptr[pi];
+        for (auto &e : row) {
+          ap_col[q] = e.first;
+          ap_val[q] = e.second;
+          ++q;
+        }
+      }
+      d_ap_ptr = (long long *)F->arena.alloc(sizeof(int64_t) * (n + 1));
+      d_ap_col = F->arena.i(std::max<int64_t>(1, ap_col.size()));
+      d_ap_val = F->arena.d(std::max<int64_t>(1, ap_val.size()));
+      CK(cudaMemcpy(d_ap_ptr, ap_ptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+      if (!ap_col.empty()) {
+        CK(cudaMemcpy(d_ap_col, ap_col.data(), sizeof(int) * ap_col.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d_ap_val, ap_val.data(), sizeof(double) * ap_val.size(), cudaMemcpyHostToDevice));
+      }
+      if (accel) {
+        std::vector<int64_t> ptr64(ap_ptr), col64(ap_col.begin(), ap_col.end());
+        graph = adjacency_from_csr(n, ptr64.data(), col64.data(), ap_val.data());
+      }
+    }
+    // ---- fronts in post order
+    int64_t nn = (int64_t)et->parent.size();
+    std::vector<int> pidx(nn, -1);
+    F->post = et->post;
+    F->fronts.resize(et->post.size());
+    F->front_blocks.assign(et->post.size(), {});
+    double thr = accel ? (double)P.n_c : INFINITY;
+    int maxh = 0;
+    int64_t max_nh = 1;
+    bool any_struct = false;
+    for (size_t q = 0; q < et->post.size(); ++q) {
+      int64_t p = et->post[q];
+      pidx[p] = (int)q;
+      FrontH &f = F->fronts[q];
+      f.node = p;
+      int64_t pb = et->piv_ptr[p], pe = et->piv_ptr[p + 1], fb = et->fr_ptr[p], fe = et->fr_ptr[p + 1];
+      f.npv = (int)(pe - pb);
+      f.nf = (int)(fe - fb);
+      f.nh = f.npv + f.nf;
+      f.ids.assign(et->piv.begin() + pb, et->piv.begin() + pe);
+      f.ids.insert(f.ids.end(), et->fr.begin() + fb, et->fr.begin() + fe);
+      f.piv_lo = f.npv ? f.ids[0] : 0;
+      for (int q2 = 1; q2 < f.npv; ++q2)
+        if (f.ids[q2] != f.ids[q2 - 1] + 1) throw runtime_error("pivot ids are not a contiguous run");
+      int h = 0;
+      for (int64_t c : et->children[p]) {
+        int ci = pidx[c];
+        h = std::max(h, F->fronts[ci].height + 1);
+        FrontH &cf = F->fronts[ci];
+        if (cf.nh > 0 && cf.nf > 0) {
+          f.kids.push_back(ci);
+        }
+      }
+      f.height = h;
+      maxh = std::max(maxh, h);
+      f.structured = f.nh > 0 && (double)f.nh >= thr;
+      any_struct |= f.structured;
+      max_nh = std::max<int64_t>(max_nh, f.nh);
+    }
+    if (any_struct) {
+      if (!(P.eps > 0.0 && P.eps < 1.0)) throw value_error("eps must lie in (0, 1)");
+      if (P.n_leaf < 1) throw value_error("n_leaf must be positive");
+      if (P.d < 1) throw value_error("distance must be at least 1");
+      // identity for DenseBlock.as_factors
+      F->ident_ld = (int)max_nh;
+      F->ident = F->arena.d((size_t)max_nh * max_nh);
+      Sink s{ctx};
+      run_identity(s, {F->ident}, {(int)max_nh}, {(int)max_nh});
+    }
+    F->d_perm = (long long *)F->arena.alloc(sizeof(int64_t) * std::max<int64_t>(1, n));
+    if (n) CK(cudaMemcpy(F->d_perm, et->perm.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+    // device ids + flags
+    for (auto &f : F->fronts) {
+      if (f.nh == 0) continue;
+      f.d_ids = (long long *)F->arena.alloc(sizeof(int64_t) * f.nh);
+      CK(cudaMemcpy(f.d_ids, f.ids.data(), sizeof(int64_t) * f.nh, cudaMemcpyHostToDevice));
+    }
+    int max_flags = 0;
+    for (auto &f : F->fronts) max_flags += 1 + (f.structured ? 8 * (int)(f.nh / std::max<int64_t>(1, P.n_leaf) + 2) : 0);
+    flag_cap = max_flags + 16;
+    d_flags = F->arena.i(max_flags + 16);
+    CK(cudaMemset(d_flags, 0, sizeof(int) * (max_flags + 16)));
+    // ---- heights
+    std::vector<std::vector<int>> byh(maxh + 1);
+    for (size_t q = 0; q < F->fronts.size(); ++q)
+      if (F->fronts[q].nh > 0) byh[F->fronts[q].height].push_back((int)q);
+    cudaEvent_t ev[8];
+    for (auto &e : ev) CK(cudaEventCreate(&e));
+    double tsum[7] = {0, 0, 0, 0, 0, 0, 0};
+    auto host_done = std::chrono::steady_clock::now();
+    F->timing.host_ms += std::chrono::duration<double, std::milli>(host_done - t0).count();
+    cudaEvent_t e_begin, e_end;
+    CK(cudaEventCreate(&e_begin));
+    CK(cudaEventCreate(&e_end));
+    CK(cudaEventRecord(e_begin, ctx->s));
+    for (int h = 0; h <= maxh; ++h) {
+      if (byh[h].empty()) continue;
+      for (auto &e : ev) CK(cudaEventRecord(e, ctx->s));
+      process_height(byh[h], ev);
+      Sink s{ctx};
+      s.sync_reset();
+      float ms;
+      CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+      tsum[0] += ms;
+      CK(cudaEventElapsedTime(&ms, ev[1], ev[2]));
+      tsum[4] += ms;
+      CK(cudaEventElapsedTime(&ms, ev[2], ev[3]));
+      tsum[1] += ms;
+      CK(cudaEventElapsedTime(&ms, ev[4], ev[5]));
+      tsum[2] += ms;
+      CK(cudaEventElapsedTime(&ms, ev[5], ev[6]));
+      tsum[3] += ms;
+      CK(cudaEventElapsedTime(&ms, ev[6], ev[7]));
+      tsum[5] += ms;
+      check_flags(0);
+      ctx->scratch.reset();
+    }
+    CK(cudaEventRecord(e_end, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    float tot;
+    CK(cudaEventElapsedTime(&tot, e_begin, e_end));
+    for (auto &e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(e_begin);
+    cudaEventDestroy(e_end);
+    F->timing.sample_ms = tsum[0];
+    F->timing.dense_front_ms = tsum[4];
+    F->timing.pivot_lu_ms = tsum[1];
+    F->timing.skeleton_ms = tsum[2];
+    F->timing.hodlr_factor_ms = tsum[3];
+    F->timing.eliminate_ms = tsum[5];
+    // ---- stats replay in post order (multifrontal.py:76-86, 478-529)
+    int64_t retained = 0, live = 0, peak = 0;
+    F->records.clear();
+    for (size_t q = 0; q < F->fronts.size(); ++q) {
+      FrontH &f = F->fronts[q];
+      int64_t freed = 0;
+      for (int64_t c : et->children[f.node]) {
+        FrontH &cf = F->fronts[pidx[c]];
+        if (cf.nh > 0 && cf.nf > 0) freed += cf.upd_reals;
+      }
+      mfh_record_t r{};
+      r.node_id = f.node;
+      if (f.nh == 0) {
+        r.path = 0;
+      } else {
+        peak = std::max(peak, retained + live + f.front_reals);  // note_front
+        r.front_size = f.nh;
+        r.n_pivot = f.npv;
+        r.path = f.structured ? 2 : 1;
+        r.max_offdiag_rank = f.structured ? f.hint : 0;
+        r.stored_reals = f.factor_reals;
+        if (f.structured)
+          F->stats.structured_fronts++;
+        else
+          F->stats.dense_fronts++;
+      }
+      int64_t newr = (f.nh > 0 && f.nf > 0) ? f.upd_reals : 0;
+      retained += r.stored_reals;
+      live += newr - freed;
+      peak = std::max(peak, retained + live);
+      F->records.push_back(r);
+    }
+    F->stats.peak_stored_reals = peak;
+    F->stats.retained_reals = retained;
+    F->stats.n_records = (int64_t)F->records.size();
+    F->stats.stored_reals = retained;
+    F->stats.device_bytes_peak = (int64_t)F->arena.capacity() + (int64_t)ctx->scratch.capacity();
+    F->timing.total_ms = tot;
+    F->timing.kernel_launches = ctx->launches;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// preconditioner apply plan (mf_solve, multifrontal.py:533-560), recorded once
+// and replayed as a CUDA graph
+// ---------------------------------------------------------------------------
+struct ApplyPlan {
+  double *d_b = nullptr, *d_x = nullptr;  // user-facing input / output
+  double *bu = nullptr, *xw = nullptr, *y = nullptr, *cbuf = nullptr, *xf = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  double bytes = 0;  // algorithmic bytes per apply
+  int64_t nodes = 0;
+};
+
+static void build_apply(mfh_factor *F) {
+  Ctx *ctx = F->ctx;
+  auto AP = std::make_unique<ApplyPlan>();
+  int64_t n = F->n;
+  Arena &ar = F->arena;
+  AP->d_b = ar.d(std::max<int64_t>(1, n));
+  AP->d_x = ar.d(std::max<int64_t>(1, n));
+  AP->bu = ar.d(std::max<int64_t>(1, n));
+  AP->xw = ar.d(std::max<int64_t>(1, n));
+  AP->y = ar.d(std::max<int64_t>(1, n));
+  // contribution offsets (post order)
+  std::vector<int64_t> off(F->fronts.size(), -1);
+  int64_t tot = 0;
+  for (size_t q = 0; q < F->fronts.size(); ++q) {
+    FrontH &f = F->fronts[q];
+    if (f.nh == 0 || f.npv == 0 || f.nf == 0) continue;
+    off[q] = tot;
+    tot += f.nf;
+  }
+  AP->cbuf = ar.d(std::max<int64_t>(1, tot));
+  AP->xf = ar.d(std::max<int64_t>(1, tot));
+  // contributions to each global id, in post order
+  std::vector<int64_t> cptr(n + 1, 0), coff(tot);
+  for (size_t q = 0; q < F->fronts.size(); ++q)
+    if (off[q] >= 0)
+      for (int j = 0; j < F->fronts[q].nf; ++j) cptr[F->fronts[q].ids[F->fronts[q].npv + j] + 1]++;
+  for (int64_t i = 0; i < n; ++i) cptr[i + 1] += cptr[i];
+  {
+    std::vector<int64_t> fill(cptr.begin(), cptr.end() - 1);
+    for (size_t q = 0; q < F->fronts.size(); ++q)
+      if (off[q] >= 0) {
+        FrontH &f = F->fronts[q];
+        for (int j = 0; j < f.nf; ++j) coff[fill[f.ids[f.npv + j]]++] = off[q] + j;
+      }
+  }
+  long long *d_cptr = (long long *)ar.alloc(sizeof(int64_t) * (n + 1));
+  long long *d_coff = (long long *)ar.alloc(sizeof(int64_t) * std::max<int64_t>(1, tot));
+  CK(cudaMemcpy(d_cptr, cptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+  if (tot) CK(cudaMemcpy(d_coff, coff.data(), sizeof(int64_t) * tot, cudaMemcpyHostToDevice));
+
+  Sink sk{ctx};
+  sk.record = true;
+  sk.persist = &ar;
+  double *bu = AP->bu, *xw = AP->xw, *y = AP->y, *cbuf = AP->cbuf, *xf = AP->xf;
+  double bytes = 0;
+  int maxh = 0;
+  for (auto &f : F->fronts) maxh = std::max(maxh, f.height);
+  std::vector<std::vector<int>> byh(maxh + 1);
+  for (size_t q = 0; q < F->fronts.size(); ++q) {
+    FrontH &f = F->fronts[q];
+    if (f.nh > 0 && f.npv > 0) byh[f.height].push_back((int)q);
+  }
+  long long *perm = F->d_perm;
+  double *db = AP->d_b, *dx = AP->d_x;
+  int grid_n = (int)std::min<int64_t>(cdiv(std::max<int64_t>(n, 1), 256), 148 * 8);
+  sk.launch([=](cudaStream_t s) {
+    k_scatter_perm<<<grid_n, 256, 0, s>>>(db, perm, bu, n);
+    check_launch();
+  });
+  bytes += 24.0 * n;
+  auto fstored = [&](const FrontH &f) -> double {
+    return (double)f.factor_reals;
+  };
+  // ---------------- upward
+  for (int h = 0; h <= maxh; ++h) {
+    auto &fis = byh[h];
+    if (fis.empty()) continue;
+    std::vector<int64_t> gl;
+    for (int q : fis) {
+      FrontH &f = F->fronts[q];
+      for (int j = 0; j < f.npv; ++j) gl.push_back(f.ids[j]);
+    }
+    long long *dgl = (long long *)sk.push(gl);
+    int cnt = (int)gl.size();
+    sk.launch([=](cudaStream_t s) {
+      k_contrib_gather<<<(int)std::min<int64_t>(cdiv(cnt, 256), 1184), 256, 0, s>>>(dgl, cnt, d_cptr, d_coff,
+                                                                                  cbuf, bu, y);
+      check_launch();
+    });
+    std::vector<RsJob> rs;
+    std::vector<HProblem> hp;
+    std::vector<GemmJob> g1, g2;
+    for (int q : fis) {
+      FrontH &f = F->fronts[q];
+      if (f.nf == 0) continue;
+      double *yv = y + f.piv_lo;
+      bytes += 8.0 * fstored(f);
+      if (!f.structured) {
+        rs.push_back(RsJob{f.F, f.piv, yv, f.npv, f.nh, 1, 1});
+        g2.push_back(GemmJob{f.F + (int64_t)f.npv * f.nh, yv, cbuf + off[q], f.nf, 1, f.npv, f.nh, 1, 1, 1.0, 0.0});
+      } else {
+        hp.push_back(HProblem{&F->trees[f.pp], 0, yv, 1, 1});
+        BlockH &b = F->blocks[f.fp];
+        if (b.dense) {
+          g2.push_back(GemmJob{b.val, yv, cbuf + off[q], f.nf, 1, f.npv, b.n, 1, 1, 1.0, 0.0});
+        } else if (b.rank) {
+          double *tmp = ar.d(b.rank);
+          g1.push_back(GemmJob{b.row, yv, tmp, b.rank, 1, f.npv, b.n, 1, 1, 1.0, 0.0});
+          g2.push_back(GemmJob{b.col, tmp, cbuf + off[q], f.nf, 1, b.rank, b.rank, 1, 1, 1.0, 0.0});
+        } else {
+          // rank-0 coupling: contribution is exactly zero
+          g2.push_back(GemmJob{b.col, yv, cbuf + off[q], f.nf, 1, 0, 1, 1, 1, 1.0, 0.0});
+        }
+      }
+    }
+    run_getrs(sk, rs);
+    hodlr_solve_batched(sk, hp);
+    run_gemm(sk, g1);
+    run_gemm(sk, g2);
+  }
+  // ---------------- downward
+  for (int h = maxh; h >= 0; --h) {
+    auto &fis = byh[h];
+    if (fis.empty()) continue;
+    std::vector<int64_t> gidx, pl;
+    std::vector<RsJob> rs;
+    std::vector<HProblem> hp;
+    std::vector<GemmJob> g1, g2;
+    for (int q : fis) {
+      FrontH &f = F->fronts[q];
+      for (int j = 0; j < f.npv; ++j) pl.push_back(f.ids[j]);
+      double *xv = xw + f.piv_lo;
+      if (f.nf) {
+        for (int j = 0; j < f.nf; ++j) gidx.push_back(f.ids[f.npv + j]);
+        double *xfv = xf + (gidx.size() - f.nf);
+        if (!f.structured) {
+          g2.push_back(GemmJob{f.F + f.npv, xfv, xv, f.npv, 1, f.nf, f.nh, 1, 1, -1.0, 1.0});
+        } else {
+          BlockH &b = F->blocks[f.pf];
+          if (b.dense) {
+            g2.push_back(GemmJob{b.val, xfv, xv, f.npv, 1, f.nf, b.n, 1, 1, -1.0, 1.0});
+          } else if (b.rank) {
+            double *tmp = ar.d(b.rank);
+            g1.push_back(GemmJob{b.row, xfv, tmp, b.rank, 1, f.nf, b.n, 1, 1, 1.0, 0.0});
+            g2.push_back(GemmJob{b.col, tmp, xv, f.npv, 1, b.rank, b.rank, 1, 1, -1.0, 1.0});
+          }
+        }
+      }
+      if (!f.structured)
+        rs.push_back(RsJob{f.F, f.piv, xv, f.npv, f.nh, 1, 1});
+      else
+        hp.push_back(HProblem{&F->trees[f.pp], 0, xv, 1, 1});
+    }
+    // xf (gathered frontal x) shares the cbuf offsets layout only per height; use a compact list
+    long long *dg = gidx.empty() ? nullptr : (long long *)sk.push(gidx);
+    long long *dp = (long long *)sk.push(pl);
+    int64_t ng = (int64_t)gidx.size(), np_ = (int64_t)pl.size();
+    sk.launch([=](cudaStream_t s) {
+      if (ng) {
+        k_gather_idx<<<(int)std::min<int64_t>(cdiv(ng, 256), 1184), 256, 0, s>>>(dg, xw, xf, ng);
+        check_launch();
+      }
+      k_copy_idx<<<(int)std::min<int64_t>(cdiv(np_, 256), 1184), 256, 0, s>>>(dp, bu, xw, np_);
+      check_launch();
+    });
+    for (int q : fis) bytes += 8.0 * fstored(F->fronts[q]);
+    run_gemm(sk, g1);
+    run_gemm(sk, g2);
+    run_getrs(sk, rs);
+    hodlr_solve_batched(sk, hp);
+  }
+  sk.launch([=](cudaStream_t s) {
+    k_gather_perm<<<grid_n, 256, 0, s>>>(xw, perm, dx, n);
+    check_launch();
+  });
+  // capture
+  CK(cudaStreamSynchronize(ctx->s));
+  CK(cudaStreamBeginCapture(ctx->s, cudaStreamCaptureModeThreadLocal));
+  for (auto &op : sk.ops) op(ctx->s);
+  CK(cudaStreamEndCapture(ctx->s, &AP->graph));
+  CK(cudaGraphInstantiate(&AP->exec, AP->graph, 0));
+  AP->bytes = bytes;
+  AP->nodes = (int64_t)sk.ops.size();
+  F->apply = std::move(AP);
+}
+
+static void apply_device(mfh_factor *F, const double *d_in, double *d_out) {
+  Ctx *ctx = F->ctx;
+  if (!F->apply) build_apply(F);
+  ApplyPlan *A = F->apply.get();
+  int64_t n = F->n;
+  if (n == 0) return;
+  CK(cudaMemcpyAsync(A->d_b, d_in, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s));
+  CK(cudaGraphLaunch(A->exec, ctx->s));
+  CK(cudaMemcpyAsync(d_out, A->d_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s));
+}
+
+}  // namespace mfh
+
+// ---------------------------------------------------------------------------
+// operators for GMRES
+// ---------------------------------------------------------------------------
+struct mfh_csr {
+  mfh::Ctx *ctx = nullptr;
+  int kind = 0;  // 0 csr, 1 dense
+  int64_t nr = 0, nc = 0;
+  long long *ptr = nullptr;
+  int *col = nullptr;
+  double *val = nullptr;
+  mfh::GemmJob *djob = nullptr;  // dense GEMV descriptor (x/y patched per call)
+};
+
+namespace mfh {
+
+static void op_apply_device(mfh_csr *A, const double *x, double *y) {
+  Ctx *ctx = A->ctx;
+  if (A->kind == 0) {
+    int64_t nw = A->nr;
+    int grid = (int)std::min<int64_t>(cdiv(nw * 32, 256), 148 * 16);
+    if (grid < 1) grid = 1;
+    k_spmv<<<grid, 256, 0, ctx->s>>>(A->nr, A->ptr, A->col, A->val, x, y);
+    check_launch();
+  } else {
+    GemmJob j{A->val, x, y, (int)A->nr, 1, (int)A->nc, (int)A->nc, 1, 1, 1.0, 0.0};
+    Sink s{ctx};
+    run_gemm(s, {j});
+  }
+}
+
+}  // namespace mfh
+
+using namespace mfh;
+
+#define MFH_TRY try {
+#define MFH_CATCH                           \
+  }                                         \
+  catch (const mfh::Error &e) {             \
+    set_last_error(e.what());               \
+    return e.kind;                          \
+  }                                         \
+  catch (const std::exception &e) {         \
+    set_last_error(e.what());               \
+    return MFH_ERUNTIME;                    \
+  }                                         \
+  return MFH_OK;
+
+extern "C" const char *mfh_last_error(void) { return g_last_error.c_str(); }
+extern "C" int mfh_version(void) { return 1; }
+
+extern "C" int mfh_ctx_create(int device, mfh_ctx **out) {
+  MFH_TRY
+  CK(cudaSetDevice(device));
+  auto *c = new mfh_ctx();
+  c->c.device = device;
+  CK(cudaStreamCreateWithFlags(&c->c.s, cudaStreamNonBlocking));
+  c->c.stage.init(size_t(64) << 20);
+  c->c.scratch.chunk = size_t(512) << 20;
+  CK(cudaMalloc(&c->c.d_part, sizeof(double) * (RED_BLOCKS + 64)));
+  CK(cudaMalloc(&c->c.d_scal, sizeof(double) * 4096));
+  *out = c;
+  MFH_CATCH
+}
+
+extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->c.s);
+  ctx->c.stage.release();
+  ctx->c.scratch.release();
+  cudaFree(ctx->c.d_part);
+  cudaFree(ctx->c.d_scal);
+  cudaStreamDestroy(ctx->c.s);
+  delete ctx;
+}
+
+extern "C" int mfh_ctx_sync(mfh_ctx *ctx) {
+  MFH_TRY
+  CK(cudaStreamSynchronize(ctx->c.s));
+  MFH_CATCH
+}
+
+extern "C" int mfh_factorize(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const int64_t *indptr,
+                             const int64_t *indices, const double *values, int mode,
+                             const mfh_params *params, mfh_factor **out) {
+  mfh_factor *F = nullptr;
+  MFH_TRY
+  if (mode != MFH_CONVENTIONAL && mode != MFH_ACCELERATED) throw value_error("unknown mode");
+  if (t->n != n) throw value_error("separator tree size does not match the matrix");
+  CK(cudaSetDevice(ctx->c.device));
+  HostCsr A;
+  A.n = n;
+  A.ptr.assign(indptr, indptr + n + 1);
+  A.idx.assign(indices, indices + A.ptr[n]);
+  A.val.assign(values, values + A.ptr[n]);
+  F = new mfh_factor();
+  F->ctx = &ctx->c;
+  ctx->c.launches = 0;
+  Factorizer fz{};
+  fz.F = F;
+  fz.ctx = &ctx->c;
+  fz.et = t;
+  fz.P = *params;
+  fz.run(A, mode);
+  *out = F;
+  F = nullptr;
+  }
+  catch (const mfh::Error &e) {
+    set_last_error(e.what());
+    if (F) {
+      cudaStreamSynchronize(ctx->c.s);
+      ctx->c.scratch.reset();
+      ctx->c.stage.off = 0;
+      F->arena.release();
+      delete F;
+    }
+    return e.kind;
+  }
+  catch (const std::exception &e) {
+    set_last_error(e.what());
+    if (F) {
+      cudaStreamSynchronize(ctx->c.s);
+      ctx->c.scratch.reset();
+      ctx->c.stage.off = 0;
+      F->arena.release();
+      delete F;
+    }
+    return MFH_ERUNTIME;
+  }
+  return MFH_OK;
+}
+
+extern "C" int mfh_factor_stats(const mfh_factor *f, mfh_stats_t *out) {
+  MFH_TRY
+  *out = f->stats;
+  MFH_CATCH
+}
+
+extern "C" int mfh_factor_records(const mfh_factor *f, mfh_record_t *out) {
+  MFH_TRY
+  std::memcpy(out, f->records.data(), sizeof(mfh_record_t) * f->records.size());
+  MFH_CATCH
+}
+
+extern "C" int mfh_factor_timing(const mfh_factor *f, mfh_timing_t *out) {
+  MFH_TRY
+  *out = f->timing;
+  MFH_CATCH
+}
+
+extern "C" int mfh_factor_blocks(const mfh_factor *f, int64_t *n_blocks, int64_t *n_perm, int64_t *info,
+                                 int64_t *perms, double *ratios) {
+  MFH_TRY
+  int64_t nb = 0, np_ = 0;
+  for (size_t q = 0; q < f->fronts.size(); ++q)
+    for (int b : f->front_blocks[q]) {
+      const BlockH &B = f->blocks[b];
+      if (info) {
+        int64_t *r = info + 7 * nb;
+        r[0] = f->fronts[q].node;
+        r[1] = B.m;
+        r[2] = B.n;
+        r[3] = (int64_t)B.I.size();
+        r[4] = (int64_t)B.J.size();
+        r[5] = B.rank;
+        r[6] = B.dense ? 1 : 0;
+      }
+      if (ratios) ratios[nb] = B.ratio;
+      if (perms) {
+        for (int k = 0; k < B.rank; ++k) {
+          perms[2 * (np_ + k)] = B.rowperm[k];
+          perms[2 * (np_ + k) + 1] = B.colperm[k];
+        }
+      }
+      nb++;
+      np_ += B.rank;
+    }
+  *n_blocks = nb;
+  *n_perm = np_;
+  MFH_CATCH
+}
+
+extern "C" void mfh_factor_free(mfh_factor *f) {
+  if (!f) return;
+  cudaStreamSynchronize(f->ctx->s);
+  if (f->apply) {
+    if (f->apply->exec) cudaGraphExecDestroy(f->apply->exec);
+    if (f->apply->graph) cudaGraphDestroy(f->apply->graph);
+  }
+  f->arena.release();
+  delete f;
+}
+
+extern "C" int mfh_apply(mfh_factor *f, const double *b, double *x, int64_t nrhs, int on_device) {
+  MFH_TRY
+  Ctx *ctx = f->ctx;
+  int64_t n = f->n;
+  if (!f->apply) build_apply(f);
+  ApplyPlan *A = f->apply.get();
+  for (int64_t r = 0; r < nrhs; ++r) {
+    if (n == 0) continue;
+    if (on_device) {
+      apply_device(f, b + r * n, x + r * n);
+    } else {
+      CK(cudaMemcpyAsync(A->d_b, b + r * n, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->s));
+      CK(cudaGraphLaunch(A->exec, ctx->s));
+      CK(cudaMemcpyAsync(x + r * n, A->d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->s));
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->s));
+  MFH_CATCH
+}
+
+extern "C" int mfh_apply_bench(mfh_factor *f, int64_t reps, double *ms_per_apply, double *bytes_per_apply) {
+  MFH_TRY
+  Ctx *ctx = f->ctx;
+  if (!f->apply) build_apply(f);
+  ApplyPlan *A = f->apply.get();
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaGraphLaunch(A->exec, ctx->s));
+  CK(cudaEventRecord(e0, ctx->s));
+  for (int64_t r = 0; r < reps; ++r) CK(cudaGraphLaunch(A->exec, ctx->s));
+  CK(cudaEventRecord(e1, ctx->s));
+  CK(cudaEventSynchronize(e1));
+  float ms;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  *ms_per_apply = ms / std::max<int64_t>(1, reps);
+  *bytes_per_apply = A->bytes;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  MFH_CATCH
+}
+
+extern "C" int mfh_csr_create(mfh_ctx *ctx, int64_t n_rows, int64_t n_cols, const int64_t *indptr,
+                              const int64_t *indices, const double *values, mfh_csr **out) {
+  MFH_TRY
+  auto *A = new mfh_csr();
+  A->ctx = &ctx->c;
+  A->kind = 0;
+  A->nr = n_rows;
+  A->nc = n_cols;
+  int64_t nnz = indptr[n_rows];
+  CK(cudaMalloc(&A->ptr, sizeof(int64_t) * (n_rows + 1)));
+  CK(cudaMalloc(&A->col, sizeof(int) * std::max<int64_t>(1, nnz)));
+  CK(cudaMalloc(&A->val, sizeof(double) * std::max<int64_t>(1, nnz)));
+  std::vector<int> c32(indices, indices + nnz);
+  CK(cudaMemcpy(A->ptr, indptr, sizeof(int64_t) * (n_rows + 1), cudaMemcpyHostToDevice));
+  if (nnz) {
+    CK(cudaMemcpy(A->col, c32.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(A->val, values, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  }
+  *out = A;
+  MFH_CATCH
+}
+
+extern "C" int mfh_dense_create(mfh_ctx *ctx, int64_t n, const double *values, mfh_csr **out) {
+  MFH_TRY
+  auto *A = new mfh_csr();
+  A->ctx = &ctx->c;
+  A->kind = 1;
+  A->nr = n;
+  A->nc = n;
+  CK(cudaMalloc(&A->val, sizeof(double) * std::max<int64_t>(1, n * n)));
+  if (n) CK(cudaMemcpy(A->val, values, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+  *out = A;
+  MFH_CATCH
+}
+
+extern "C" void mfh_csr_free(mfh_csr *A) {
+  if (!A) return;
+  cudaStreamSynchronize(A->ctx->s);
+  cudaFree(A->ptr);
+  cudaFree(A->col);
+  cudaFree(A->val);
+  delete A;
+}
+
+extern "C" int mfh_spmv(mfh_csr *A, const double *x, double *y, int on_device) {
+  MFH_TRY
+  Ctx *ctx = A->ctx;
+  if (on_device) {
+    op_apply_device(A, x, y);
+  } else {
+    double *dx, *dy;
+    CK(cudaMallocAsync(&dx, sizeof(double) * std::max<int64_t>(1, A->nc), ctx->s));
+    CK(cudaMallocAsync(&dy, sizeof(double) * std::max<int64_t>(1, A->nr), ctx->s));
+    CK(cudaMemcpyAsync(dx, x, sizeof(double) * A->nc, cudaMemcpyHostToDevice, ctx->s));
+    op_apply_device(A, dx, dy);
+    CK(cudaMemcpyAsync(y, dy, sizeof(double) * A->nr, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaFreeAsync(dx, ctx->s));
+    CK(cudaFreeAsync(dy, ctx->s));
+  }
+  CK(cudaStreamSynchronize(ctx->s));
+  MFH_CATCH
+}
+
+// ---------------------------------------------------------------------------
+// GMRES (krylov.py:68-161): vectors on the device, Hessenberg/Givens on host
+// ---------------------------------------------------------------------------
+namespace mfh {
+
+struct GmresRun {
+  Ctx *ctx;
+  const mfh_gmres_ops *ops;
+  int64_t n;
+  std::vector<double> hx, hy;  // host bounce buffers for callbacks
+  double *tmp = nullptr, *tmp2 = nullptr;
+
+  int gridn() const { return (int)std::min<int64_t>(cdiv(std::max<int64_t>(n, 1), 256), 148 * 8); }
+
+  void host_op(mfh_host_op cb, void *user, const double *dx, double *dy) {
+    hx.resize(n);
+    hy.resize(n);
+    CK(cudaMemcpyAsync(hx.data(), dx, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    cb(user, hx.data(), hy.data());
+    CK(cudaMemcpyAsync(dy, hy.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+  }
+  void A(const double *x, double *y) {
+    if (ops->A)
+      op_apply_device(ops->A, x, y);
+    else
+      host_op(ops->A_cb, ops->A_user, x, y);
+  }
+  void M(const double *x, double *y) {
+    if (ops->M)
+      apply_device(ops->M, x, y);
+    else if (ops->M_cb)
+      host_op(ops->M_cb, ops->M_user, x, y);
+    else
+      CK(cudaMemcpyAsync(y, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s));
+  }
+  // dot into device scalar slot, deterministic
+  void dot(const double *x, const double *y, double *out, bool do_sqrt) {
+    k_dot_part<<<RED_BLOCKS, RED_THREADS, 0, ctx->s>>>(x, y, n, ctx->d_part);
+    k_finish<<<1, 32, 0, ctx->s>>>(ctx->d_part, out, do_sqrt ? 1 : 0);
+    check_launch();
+  }
+  double host_scalar(double *d) {
+    double v;
+    CK(cudaMemcpyAsync(&v, d, sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    return v;
+  }
+
+  void run(const double *d_b, double *d_x, double tol, int64_t max_iter, int64_t restart,
+           std::vector<double> &res, int64_t &its, bool &conv) {
+    if (!(tol > 0.0 && tol < 1.0)) throw value_error("tol must lie in (0, 1)");
+    if (max_iter < 1 || restart < 1) throw value_error("max_iter and restart must be positive");
+    res.clear();
+    its = 0;
+    conv = false;
+    double *S = ctx->d_scal;  // [0] norm b, [1] beta, [2] hn, [8..] H column
+    CK(cudaMemsetAsync(d_x, 0, sizeof(double) * n, ctx->s));
+    dot(d_b, d_b, S, true);
+    double nb = host_scalar(S);
+    if (nb == 0.0) {
+      conv = true;
+      res.push_back(0.0);
+      return;
+    }
+    int64_t mcap = std::min(restart, max_iter);
+    double *V = nullptr, *w = nullptr, *r = nullptr, *z = nullptr;
+    CK(cudaMallocAsync(&V, sizeof(double) * n * (mcap + 1), ctx->s));
+    CK(cudaMallocAsync(&w, sizeof(double) * n, ctx->s));
+    CK(cudaMallocAsync(&r, sizeof(double) * n, ctx->s));
+    CK(cudaMallocAsync(&z, sizeof(double) * n, ctx->s));
+    double *dy = S + 2048;
+    int g = gridn();
+    auto cleanup = [&]() {
+      cudaFreeAsync(V, ctx->s);
+      cudaFreeAsync(w, ctx->s);
+      cudaFreeAsync(r, ctx->s);
+      cudaFreeAsync(z, ctx->s);
+      cudaStreamSynchronize(ctx->s);
+    };
+    try {
+      while (its < max_iter && !conv) {
+        A(d_x, w);
+        k_sub<<<g, 256, 0, ctx->s>>>(d_b, w, r, n);
+        dot(r, r, S + 1, true);
+        double beta = host_scalar(S + 1);
+        if (!std::isfinite(beta)) throw value_error("GMRES residual is not finite");
+        if (beta / nb <= tol) {
+          conv = true;
+          if (res.empty()) res.push_back(beta / nb);
+          break;
+        }
+        int64_t m = std::min(restart, max_iter - its);
+        std::vector<double> H((m + 1) * m, 0.0), cs(m, 0.0), sn(m, 0.0), gg(m + 1, 0.0);
+        auto h = [&](int64_t i, int64_t j) -> double & { return H[i * m + j]; };
+        gg[0] = beta;
+        k_scale_inv<<<g, 256, 0, ctx->s>>>(S + 1, r, V, n);
+        int64_t j = 0;
+        bool lucky_stop = false;
+        std::vector<double> hcol(m + 2);
+        while (j < m) {
+          M(V + j * n, z);
+          A(z, w);
+          for (int64_t i = 0; i <= j; ++i) {
+            k_dot_part<<<RED_BLOCKS, RED_THREADS, 0, ctx->s>>>(V + i * n, w, n, ctx->d_part);
+            k_mgs_axpy<<<g, 256, 0, ctx->s>>>(ctx->d_part, S + 8 + i, V + i * n, w, n);
+          }
+          dot(w, w, S + 2, true);
+          check_launch();
+          CK(cudaMemcpyAsync(hcol.data(), S + 8, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, ctx->s));
+          double hn = host_scalar(S + 2);
+          for (int64_t i = 0; i <= j; ++i) h(i, j) = hcol[i];
+          if (!std::isfinite(hn)) throw value_error("GMRES residual is not finite");
+          h(j + 1, j) = hn;
+          for (int64_t i = 0; i < j; ++i) {
+            double t = cs[i] * h(i, j) + sn[i] * h(i + 1, j);
+            h(i + 1, j) = -sn[i] * h(i, j) + cs[i] * h(i + 1, j);
+            h(i, j) = t;
+          }
+          double den = std::hypot(h(j, j), h(j + 1, j));
+          if (den == 0.0) throw value_error("GMRES breakdown: zero Hessenberg column");
+          cs[j] = h(j, j) / den;
+          sn[j] = h(j + 1, j) / den;
+          h(j, j) = den;
+          h(j + 1, j) = 0.0;
+          gg[j + 1] = -sn[j] * gg[j];
+          gg[j] = cs[j] * gg[j];
+          its += 1;
+          double rel = std::fabs(gg[j + 1]) / nb;
+          res.push_back(rel);
+          bool lucky = hn == 0.0;
+          j += 1;
+          if (rel <= tol || lucky) {
+            lucky_stop = lucky;
+            break;
+          }
+          if (j < m) k_scale_inv<<<g, 256, 0, ctx->s>>>(S + 2, w, V + j * n, n);
+        }
+        if (j > 0) {
+          std::vector<double> y(j, 0.0);
+          for (int64_t i = j - 1; i >= 0; --i) {
+            double s = 0.0;
+            for (int64_t q = i + 1; q < j; ++q) s += h(i, q) * y[q];
+            y[i] = (gg[i] - s) / h(i, i);
+          }
+          CK(cudaMemcpyAsync(dy, y.data(), sizeof(double) * j, cudaMemcpyHostToDevice, ctx->s));
+          k_combine<<<g, 256, 0, ctx->s>>>(V, dy, (int)j, n, w);
+          M(w, z);
+          k_add<<<g, 256, 0, ctx->s>>>(z, d_x, n);
+          CK(cudaStreamSynchronize(ctx->s));  // dy host buffer lifetime
+        }
+        A(d_x, w);
+        k_sub<<<g, 256, 0, ctx->s>>>(d_b, w, r, n);
+        dot(r, r, S + 3, true);
+        double tr = host_scalar(S + 3) / nb;
+        if (!std::isfinite(tr)) throw value_error("GMRES residual is not finite");
+        if (!res.empty()) res.back() = tr;
+        if (tr <= tol || lucky_stop) conv = true;
+      }
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  }
+};
+
+}  // namespace mfh
+
+static int gmres_common(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const double *d_b, double *d_x,
+                        double tol, int64_t max_iter, int64_t restart, double *hist, int64_t *n_hist,
+                        int64_t *iterations, int *converged) {
+  MFH_TRY
+  GmresRun g{&ctx->c, ops, n};
+  std::vector<double> res;
+  int64_t its = 0;
+  bool conv = false;
+  g.run(d_b, d_x, tol, max_iter, restart, res, its, conv);
+  if (hist) std::memcpy(hist, res.data(), sizeof(double) * res.size());
+  *n_hist = (int64_t)res.size();
+  *iterations = its;
+  *converged = conv ? 1 : 0;
+  MFH_CATCH
+}
+
+extern "C" int mfh_gmres_device(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const double *d_b,
+                                double *d_x, double tol, int64_t max_iter, int64_t restart, double *hist,
+                                int64_t *n_hist, int64_t *iterations, int *converged) {
+  return gmres_common(ctx, ops, n, d_b, d_x, tol, max_iter, restart, hist, n_hist, iterations, converged);
+}
+
+extern "C" int mfh_gmres(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const double *b, double *x,
+                         double tol, int64_t max_iter, int64_t restart, double *hist, int64_t *n_hist,
+                         int64_t *iterations, int *converged) {
+  double *db = nullptr, *dx = nullptr;
+  cudaStream_t s = ctx->c.s;
+  if (cudaMalloc(&db, sizeof(double) * std::max<int64_t>(1, n)) != cudaSuccess ||
+      cudaMalloc(&dx, sizeof(double) * std::max<int64_t>(1, n)) != cudaSuccess) {
+    set_last_error("CUDA allocation failed in mfh_gmres");
+    return MFH_ERUNTIME;
+  }
+  cudaMemcpyAsync(db, b, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+  int rc = gmres_common(ctx, ops, n, db, dx, tol, max_iter, restart, hist, n_hist, iterations, converged);
+  if (rc == MFH_OK) {
+    cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+  }
+  cudaFree(db);
+  cudaFree(dx);
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
+// kernel plugin: batched full_pivot_lu (_core.pyx:23-86)
+// ---------------------------------------------------------------------------
+extern "C" int mfh_full_pivot_lu_batched(mfh_ctx *ctx, int64_t batch, const int64_t *offs, const int64_t *ms,
+                                         const int64_t *ns, double *blocks, int64_t total, double eps,
+                                         const int64_t *max_ranks, int64_t *row_perm, int64_t *col_perm,
+                                         int64_t *ranks, double *ratios, int64_t *status, double *err) {
+  MFH_TRY
+  Ctx *c = &ctx->c;
+  if (batch == 0) return MFH_OK;
+  double *d_blocks = c->scratch.d(std::max<int64_t>(1, total));
+  CK(cudaMemcpyAsync(d_blocks, blocks, sizeof(double) * total, cudaMemcpyHostToDevice, c->s));
+  std::vector<PluJob> jobs(batch);
+  std::vector<int64_t> ioff(batch), doff(batch);
+  int64_t itot = 0, dtot = 0;
+  for (int64_t b = 0; b < batch; ++b) {
+    ioff[b] = itot;
+    doff[b] = dtot;
+    itot += 4 * (ms[b] + ns[b]) + 3;
+    dtot += ms[b] + ns[b] + 3;
+  }
+  int *ibuf = c->scratch.i(std::max<int64_t>(1, itot));
+  double *dbuf = c->scratch.d(std::max<int64_t>(1, dtot));
+  for (int64_t b = 0; b < batch; ++b) {
+    PluJob &j = jobs[b];
+    int m = (int)ms[b], n = (int)ns[b];
+    j.a = d_blocks + offs[b];
+    j.m = m;
+    j.n = n;
+    j.ld = n;
+    j.kmax = (int)std::min<int64_t>(std::min(m, n), max_ranks[b]);
+    int *p = ibuf + ioff[b];
+    j.rowAt = p;
+    j.posR = p + m;
+    j.actR = p + 2 * m;
+    j.idxR = p + 3 * m;
+    p += 4 * m;
+    j.colAt = p;
+    j.posC = p + n;
+    j.actC = p + 2 * n;
+    j.idxC = p + 3 * n;
+    p += 4 * n;
+    j.out = p;
+    j.mult = dbuf + doff[b];
+    j.prow = dbuf + doff[b] + m;
+    j.outd = dbuf + doff[b] + m + n;
+  }
+  Sink s{c};
+  PluJob *dj = s.push(jobs);
+  k_full_pivot_lu<<<(int)batch, 512, 0, c->s>>>(dj, eps);
+  check_launch();
+  std::vector<int> hi(itot);
+  std::vector<double> hd(dtot);
+  CK(cudaMemcpyAsync(hi.data(), ibuf, sizeof(int) * itot, cudaMemcpyDeviceToHost, c->s));
+  CK(cudaMemcpyAsync(hd.data(), dbuf, sizeof(double) * dtot, cudaMemcpyDeviceToHost, c->s));
+  std::vector<double> raw(total);
+  CK(cudaMemcpyAsync(raw.data(), d_blocks, sizeof(double) * total, cudaMemcpyDeviceToHost, c->s));
+  CK(cudaStreamSynchronize(c->s));
+  c->scratch.reset();
+  c->stage.off = 0;
+  int64_t ro = 0, co = 0;
+  for (int64_t b = 0; b < batch; ++b) {
+    int m = (int)ms[b], n = (int)ns[b];
+    const int *p = hi.data() + ioff[b];
+    const int *rowAt = p, *colAt = p + 4 * m;
+    const int *out = p + 4 * m + 4 * n;
+    const double *od = hd.data() + doff[b] + m + n;
+    ranks[b] = out[0];
+    status[b] = out[1];
+    ratios[b] = od[0];
+    err[3 * b] = out[2];
+    err[3 * b + 1] = od[1];
+    err[3 * b + 2] = od[2];
+    for (int i = 0; i < m; ++i) row_perm[ro + i] = rowAt[i];
+    for (int j = 0; j < n; ++j) col_perm[co + j] = colAt[j];
+    // reference layout: lu[p][q] = a[rowAt[p]][colAt[q]]
+    const double *a = raw.data() + offs[b];
+    double *o = blocks + offs[b];
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < n; ++j) o[(int64_t)i * n + j] = a[(int64_t)rowAt[i] * n + colAt[j]];
+    ro += m;
+    co += n;
+  }
+  MFH_CATCH
+}

@@ -1,0 +1,62 @@
+// Internal declarations shared by the host symbolic code and the CUDA engine.
+#pragma once
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mfh.h"
+
+namespace mfh {
+
+// Exceptions carry the C-ABI error kind; the C entry points translate them.
+struct Error : public std::runtime_error {
+  int kind;
+  Error(int k, const std::string &m) : std::runtime_error(m), kind(k) {}
+};
+inline Error value_error(const std::string &m) { return Error(MFH_EVALUE, m); }
+inline Error runtime_error(const std::string &m) { return Error(MFH_ERUNTIME, m); }
+
+void set_last_error(const std::string &m);
+
+// Undirected graph in CSR, neighbours sorted, no self loops.
+struct Graph {
+  int64_t n = 0;
+  std::vector<int64_t> ptr, idx;
+  int64_t degree(int64_t v) const { return ptr[v + 1] - ptr[v]; }
+};
+
+// Host CSR of a square matrix (rows sorted, no duplicates).
+struct HostCsr {
+  int64_t n = 0;
+  std::vector<int64_t> ptr, idx;
+  std::vector<double> val;
+};
+
+Graph adjacency_from_csr(int64_t n, const int64_t *indptr, const int64_t *indices,
+                         const double *values);
+
+}  // namespace mfh
+
+// Separator tree produced by nested dissection (ordering.py:19-56).
+struct mfh_nd {
+  int64_t n = 0;
+  int64_t root = -1;
+  std::vector<int64_t> perm;
+  std::vector<int64_t> vptr, verts;  // per node vertex list (creation order ids)
+  std::vector<int64_t> left, right, parent;
+  std::vector<int64_t> post_order() const;
+};
+
+// Elimination tree in the permuted numbering (ordering.py:211-261).
+struct mfh_etree {
+  int64_t n = 0;
+  int64_t root = -1;
+  std::vector<int64_t> perm;
+  std::vector<int64_t> post;               // node ids in post order
+  std::vector<int64_t> piv_ptr, piv;       // pivot ids (sorted, contiguous run)
+  std::vector<int64_t> fr_ptr, fr;         // frontal ids (sorted, > pivots)
+  std::vector<int64_t> parent;             // -1 for root
+  std::vector<std::vector<int64_t>> children;  // (left, right) order
+};

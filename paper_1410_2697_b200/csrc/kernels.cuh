@@ -1,0 +1,845 @@
+// Batched FP64 kernels for the HODLR-multifrontal hot path (sm_100a).
+//
+// Everything is row-major with explicit leading dimensions, like the
+// reference's C-ordered numpy arrays. Each kernel processes a whole batch of
+// variable-size problems (one etree height, one HODLR level) per launch; the
+// host builds the descriptor arrays.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mfh {
+
+constexpr int kZeroPivotNum = 1;  // marker
+#define MFH_ZERO_PIVOT_RATIO 1e-14
+#define MFH_PIVOT_GROWTH_BOUND (2.0 * (1.0 + 1e-10))
+
+// ---------------------------------------------------------------------------
+// descriptors
+// ---------------------------------------------------------------------------
+
+// off-diagonal HODLR block as stored on the device
+struct HBlk {
+  const double *a;  // LR: col factor (m x rank, lda); dense: values (m x n, lda)
+  const double *b;  // LR: row factor (rank x n, ldb)
+  int rank, kind;   // kind 0 = low rank, 1 = dense
+  int lda, ldb;
+};
+
+// heap-indexed HODLR node (children 2i+1, 2i+2); leaf != nullptr marks a leaf
+struct HNode {
+  const double *leaf;  // (hi-lo)^2 row-major
+  HBlk up, lw;         // rows lo:mid x cols mid:hi ; rows mid:hi x cols lo:mid
+};
+
+// child update as seen by the parent's entry sampler
+struct DChild {
+  const int *to_child;  // parent front position -> child position or -1
+  int kind;             // 0 dense (Schur block), 1 HODLR - W Vt
+  int n;                // update dimension
+  const double *dense;
+  int ldd;
+  const HNode *hn;
+  const double *W;   // n x rw (ldw)
+  const double *Vt;  // rw x n (ldv)
+  int rw, ldw, ldv;
+};
+
+struct DFront {
+  const long long *ids;  // front global ids (permuted numbering), sorted
+  int nh, npv;
+  int child_begin, child_end;
+};
+
+// one entry-sampling request F(rows, cols) -> out (nr x nc, ld)
+struct SReq {
+  int front;
+  int nr, nc;
+  const int *rows;  // front-local positions, or nullptr for r0..r0+nr-1
+  const int *cols;
+  int r0, c0;
+  double *out;
+  int ld;
+};
+
+struct GemmJob {  // C = alpha * A(m x k) * B(k x n) + beta * C
+  const double *A;
+  const double *B;
+  double *C;
+  int m, n, k, lda, ldb, ldc;
+  double alpha, beta;
+};
+
+struct LuJob {  // partial-pivot LU (getrf) of n x n in place
+  double *a;
+  int n, lda;
+  int *piv;
+  int *flag;  // set to 1 when singular / non-finite (reference diag checks)
+};
+
+struct RsJob {  // getrs: solve with LU+piv, B (n x k, ldb) in place
+  const double *a;
+  const int *piv;
+  double *b;
+  int n, lda, k, ldb;
+};
+
+struct CopyJob {  // dst (m x n, ldd) = src (m x n, lds); optional row/col maps on src
+  const double *src;
+  double *dst;
+  int m, n, lds, ldd;
+  const int *rmap;
+  const int *cmap;
+};
+
+struct PluJob {  // complete-pivot partial LU of an m x n core (logical permutation)
+  double *a;
+  int m, n, ld;
+  int kmax;
+  int *rowAt, *colAt;  // position -> original index (outputs: row_perm, col_perm)
+  int *posR, *posC;    // original index -> position
+  int *actR, *actC;    // active original indices
+  int *idxR, *idxC;    // original index -> slot in the active list
+  double *mult, *prow; // scratch m and n
+  int *out;            // [0]=rank [1]=status [2]=err_k
+  double *outd;        // [0]=ratio [1]=err_piv [2]=err_prev
+};
+
+struct SkelJob {  // skeleton factors from a factored core
+  const double *lu;  // compact r x r (L unit-lower strict, U upper), ld r
+  int r;
+  const double *R;  // |I| x n panel, ldR
+  int ldR, n;
+  const int *rp;  // rowAt (first r entries used)
+  const double *C;  // m x |J| panel, ldC
+  int ldC, m;
+  const int *cp;  // colAt
+  double *row_out;  // r x n
+  double *col_out;  // m x r
+};
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double blk_entry(const HBlk &b, int rr, int cc) {
+  if (b.kind == 1) return b.a[(long long)rr * b.lda + cc];
+  double s = 0.0;
+  const double *a = b.a + (long long)rr * b.lda;
+  const double *bb = b.b + cc;
+  for (int t = 0; t < b.rank; ++t) s = fma(a[t], bb[(long long)t * b.ldb], s);
+  return s;
+}
+
+// entry (r, c) of a HODLR matrix of size n at local positions (hodlr.py:386-426)
+__device__ __forceinline__ double hodlr_entry(const HNode *hn, int n, int r, int c) {
+  int idx = 0, lo = 0, hi = n;
+  while (true) {
+    const HNode &nd = hn[idx];
+    if (nd.leaf) return nd.leaf[(long long)(r - lo) * (hi - lo) + (c - lo)];
+    int mid = (lo + hi) >> 1;
+    if (r < mid) {
+      if (c < mid) {
+        idx = 2 * idx + 1;
+        hi = mid;
+        continue;
+      }
+      return blk_entry(nd.up, r - lo, c - mid);
+    }
+    if (c >= mid) {
+      idx = 2 * idx + 2;
+      lo = mid;
+      continue;
+    }
+    return blk_entry(nd.lw, r - mid, c - lo);
+  }
+}
+
+__device__ __forceinline__ double seed_entry(const long long *Ap_ptr, const int *Ap_col,
+                                             const double *Ap_val, long long gr, long long gc) {
+  long long lo = Ap_ptr[gr], hi = Ap_ptr[gr + 1];
+  int key = (int)gc;
+  while (lo < hi) {
+    long long mid = (lo + hi) >> 1;
+    int v = Ap_col[mid];
+    if (v < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  if (lo < Ap_ptr[gr + 1] && Ap_col[lo] == key) return Ap_val[lo];
+  return 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// extend-add sampler (multifrontal.py:313-350 + hodlr.py:386-463)
+// value = seed(r,c) [+ child_1] [+ child_2] ... in node.children order;
+// child value = HODLR entry - W[r,:] . V[c,:]
+// ---------------------------------------------------------------------------
+constexpr int SAMPLE_TR = 8, SAMPLE_TC = 32;
+
+__global__ void k_sample(const SReq *__restrict__ reqs, const int2 *__restrict__ tiles, int ntiles,
+                         const DFront *__restrict__ fronts, const DChild *__restrict__ kids,
+                         const long long *__restrict__ Ap_ptr, const int *__restrict__ Ap_col,
+                         const double *__restrict__ Ap_val) {
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int2 tl = tiles[t];
+    const SReq rq = reqs[tl.x];
+    int tpr = (rq.nc + SAMPLE_TC - 1) / SAMPLE_TC;
+    int i = (tl.y / tpr) * SAMPLE_TR + threadIdx.y;
+    int j = (tl.y % tpr) * SAMPLE_TC + threadIdx.x;
+    if (i >= rq.nr || j >= rq.nc) continue;
+    int r = rq.rows ? rq.rows[i] : rq.r0 + i;
+    int c = rq.cols ? rq.cols[j] : rq.c0 + j;
+    const DFront F = fronts[rq.front];
+    double v = 0.0;
+    if (r < F.npv || c < F.npv) v = seed_entry(Ap_ptr, Ap_col, Ap_val, F.ids[r], F.ids[c]);
+    for (int q = F.child_begin; q < F.child_end; ++q) {
+      const DChild &ch = kids[q];
+      int cr = ch.to_child[r];
+      if (cr < 0) continue;
+      int cc = ch.to_child[c];
+      if (cc < 0) continue;
+      double sub;
+      if (ch.kind == 0) {
+        sub = ch.dense[(long long)cr * ch.ldd + cc];
+      } else {
+        sub = hodlr_entry(ch.hn, ch.n, cr, cc);
+        if (ch.rw) {
+          double s = 0.0;
+          const double *w = ch.W + (long long)cr * ch.ldw;
+          for (int u = 0; u < ch.rw; ++u) s = fma(w[u], ch.Vt[(long long)u * ch.ldv + cc], s);
+          sub = sub - s;
+        }
+      }
+      v = v + sub;
+    }
+    rq.out[(long long)i * rq.ld + j] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// batched 2-D copy / gather
+// ---------------------------------------------------------------------------
+__global__ void k_copy(const CopyJob *__restrict__ jobs, int njobs) {
+  const CopyJob J = jobs[blockIdx.y];
+  long long total = (long long)J.m * J.n;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(e / J.n), j = (int)(e % J.n);
+    int si = J.rmap ? J.rmap[i] : i;
+    int sj = J.cmap ? J.cmap[j] : j;
+    J.dst[(long long)i * J.ldd + j] = J.src[(long long)si * J.lds + sj];
+  }
+}
+
+// identity in an m x m block (ld)
+__global__ void k_identity(double *const *__restrict__ ptrs, const int *__restrict__ dims,
+                           const int *__restrict__ lds) {
+  double *p = ptrs[blockIdx.y];
+  int m = dims[blockIdx.y], ld = lds[blockIdx.y];
+  long long total = (long long)m * m;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(e / m), j = (int)(e % m);
+    p[(long long)i * ld + j] = (i == j) ? 1.0 : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// vbatched GEMM, NN, row-major: 64x64 tiles, BK 16, 256 threads, 4x4 per thread
+// ---------------------------------------------------------------------------
+constexpr int GEMM_BM = 64, GEMM_BN = 64, GEMM_BK = 16;
+
+__global__ void __launch_bounds__(256) k_gemm(const GemmJob *__restrict__ jobs,
+                                              const int4 *__restrict__ tiles, int ntiles) {
+  __shared__ double As[GEMM_BK][GEMM_BM + 1];
+  __shared__ double Bs[GEMM_BK][GEMM_BN];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int4 tl = tiles[t];
+    const GemmJob J = jobs[tl.x];
+    const int m0 = tl.y * GEMM_BM, n0 = tl.z * GEMM_BN;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int k0 = 0; k0 < J.k; k0 += GEMM_BK) {
+      // A tile: 64 rows x 16 k
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int e = tid + q * 256;
+        int mm = e >> 4, kk = e & 15;
+        int gm = m0 + mm, gk = k0 + kk;
+        As[kk][mm] = (gm < J.m && gk < J.k) ? J.A[(long long)gm * J.lda + gk] : 0.0;
+      }
+      // B tile: 16 k x 64 cols
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int e = tid + q * 256;
+        int kk = e >> 6, nn = e & 63;
+        int gk = k0 + kk, gn = n0 + nn;
+        Bs[kk][nn] = (gk < J.k && gn < J.n) ? J.B[(long long)gk * J.ldb + gn] : 0.0;
+      }
+      __syncthreads();
+      int kc = min(GEMM_BK, J.k - k0);
+      for (int kk = 0; kk < kc; ++kk) {
+        double a[4], b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a[q] = As[kk][ty + 16 * q];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) b[q] = Bs[kk][tx + 16 * q];
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      int gm = m0 + ty + 16 * p;
+      if (gm >= J.m) continue;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int gn = n0 + tx + 16 * q;
+        if (gn >= J.n) continue;
+        double *c = J.C + (long long)gm * J.ldc + gn;
+        double v = J.alpha * acc[p][q];
+        *c = (J.beta == 0.0) ? v : J.beta * (*c) + v;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// block reductions
+// ---------------------------------------------------------------------------
+struct MaxLoc {
+  double v;
+  long long key;
+};
+
+__device__ __forceinline__ bool better(double v, long long k, double bv, long long bk) {
+  return v > bv || (v == bv && k < bk);
+}
+
+__device__ __forceinline__ MaxLoc block_maxloc(double v, long long key, MaxLoc *sh) {
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov = __shfl_down_sync(0xffffffffu, v, o);
+    long long ok = __shfl_down_sync(0xffffffffu, key, o);
+    if (better(ov, ok, v, key)) {
+      v = ov;
+      key = ok;
+    }
+  }
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if (lane == 0) sh[w] = MaxLoc{v, key};
+  __syncthreads();
+  if (w == 0) {
+    MaxLoc m = lane < nw ? sh[lane] : MaxLoc{-2.0, 0x7fffffffffffffffLL};
+    v = m.v;
+    key = m.key;
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_down_sync(0xffffffffu, v, o);
+      long long ok = __shfl_down_sync(0xffffffffu, key, o);
+      if (better(ov, ok, v, key)) {
+        v = ov;
+        key = ok;
+      }
+    }
+    if (lane == 0) sh[32] = MaxLoc{v, key};
+  }
+  __syncthreads();
+  MaxLoc r = sh[32];
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// complete-pivot partial LU with rank cut (_core.pyx:23-86), one CTA per core.
+// Logical permutation: values stay at their original (row, col); the pivot
+// search ranks candidates by (|a|, -(pos_r * n + pos_c)) with the CURRENT
+// positions, which reproduces the reference's row-major first-max rule and its
+// whole-row / whole-column swaps exactly. Update is mul + sub (no FMA).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) k_full_pivot_lu(const PluJob *__restrict__ jobs,
+                                                       double eps) {
+  __shared__ MaxLoc red[33];
+  __shared__ int s_done, s_bi, s_bj, s_ar, s_ac;
+  __shared__ double s_akk, s_u11, s_prev;
+  const PluJob J = jobs[blockIdx.x];
+  const int m = J.m, n = J.n, ld = J.ld;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int kmin = min(m, n);
+  for (int i = tid; i < m; i += nt) {
+    J.rowAt[i] = i;
+    J.posR[i] = i;
+    J.actR[i] = i;
+    J.idxR[i] = i;
+  }
+  for (int j = tid; j < n; j += nt) {
+    J.colAt[j] = j;
+    J.posC[j] = j;
+    J.actC[j] = j;
+    J.idxC[j] = j;
+  }
+  if (tid == 0) {
+    s_done = 0;
+    s_ar = m;
+    s_ac = n;
+    s_prev = 0.0;
+    s_u11 = 0.0;
+    J.out[0] = 0;
+    J.out[1] = 0;
+    J.out[2] = 0;
+    J.outd[0] = 0.0;
+  }
+  // initial scan (step 0 candidates)
+  double bv = -1.0;
+  long long bk = 0x7fffffffffffffffLL;
+  {
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (int i = warp; i < m; i += nw) {
+      const double *row = J.a + (long long)i * ld;
+      for (int j = lane; j < n; j += 32) {
+        double v = fabs(row[j]);
+        long long key = (long long)i * n + j;
+        if (better(v, key, bv, bk)) {
+          bv = v;
+          bk = key;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < kmin; ++k) {
+    MaxLoc best = block_maxloc(bv, bk, red);
+    if (tid == 0) {
+      double piv = best.v;
+      long long key = best.key;
+      // key encodes CURRENT positions -> translate to original indices
+      int pr = (int)(key / n), pc = (int)(key % n);
+      int bi = J.rowAt[pr], bj = J.colAt[pc];
+      if (best.key == 0x7fffffffffffffffLL) {  // nothing beat -1 (all NaN): position (k,k)
+        piv = -1.0;
+        bi = J.rowAt[k];
+        bj = J.colAt[k];
+      }
+      if (k == 0) {
+        s_u11 = piv;
+        if (piv == 0.0) {
+          J.out[0] = 0;
+          J.outd[0] = 0.0;
+          s_done = 1;
+        }
+      } else {
+        if (piv > s_prev * MFH_PIVOT_GROWTH_BOUND) {
+          J.out[1] = 1;
+          J.out[2] = k;
+          J.outd[1] = piv;
+          J.outd[2] = s_prev;
+          s_done = 1;
+        } else {
+          double ratio = piv / s_u11;
+          if (ratio < eps || piv <= MFH_ZERO_PIVOT_RATIO * s_u11) {
+            J.out[0] = k;
+            J.outd[0] = ratio;
+            s_done = 1;
+          }
+        }
+      }
+      if (!s_done && k == J.kmax) {
+        J.out[0] = J.kmax;
+        J.outd[0] = piv / s_u11;
+        s_done = 1;
+      }
+      if (!s_done) {
+        // swap positions k <-> pos(bi) for rows, k <-> pos(bj) for cols
+        int pbi = J.posR[bi], ak = J.rowAt[k];
+        J.rowAt[k] = bi;
+        J.rowAt[pbi] = ak;
+        J.posR[bi] = k;
+        J.posR[ak] = pbi;
+        int pbj = J.posC[bj], ck = J.colAt[k];
+        J.colAt[k] = bj;
+        J.colAt[pbj] = ck;
+        J.posC[bj] = k;
+        J.posC[ck] = pbj;
+        // drop the pivot row / column from the active lists
+        int s = J.idxR[bi], last = J.actR[s_ar - 1];
+        J.actR[s] = last;
+        J.idxR[last] = s;
+        s_ar -= 1;
+        s = J.idxC[bj];
+        last = J.actC[s_ac - 1];
+        J.actC[s] = last;
+        J.idxC[last] = s;
+        s_ac -= 1;
+        s_bi = bi;
+        s_bj = bj;
+        double akk = J.a[(long long)bi * ld + bj];
+        s_akk = akk;
+        s_prev = fabs(akk);
+        J.out[0] = k + 1;
+      }
+    }
+    __syncthreads();
+    if (s_done) break;
+    const int bi = s_bi, bj = s_bj, ar = s_ar, ac = s_ac;
+    const double akk = s_akk;
+    // phase A: multipliers a[i, bj] /= akk, pivot row snapshot
+    for (int ii = tid; ii < ar; ii += nt) {
+      int i = J.actR[ii];
+      double l = J.a[(long long)i * ld + bj] / akk;
+      J.a[(long long)i * ld + bj] = l;
+      J.mult[ii] = l;
+    }
+    for (int jj = tid; jj < ac; jj += nt) J.prow[jj] = J.a[(long long)bi * ld + J.actC[jj]];
+    __syncthreads();
+    // phase B: rank-1 update of the trailing block fused with the next argmax
+    bv = -1.0;
+    bk = 0x7fffffffffffffffLL;
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (int ii = warp; ii < ar; ii += nw) {
+      int i = J.actR[ii];
+      double l = J.mult[ii];
+      double *row = J.a + (long long)i * ld;
+      long long pr = (long long)J.posR[i] * n;
+      for (int jj = lane; jj < ac; jj += 32) {
+        int j = J.actC[jj];
+        double v = __dsub_rn(row[j], __dmul_rn(l, J.prow[jj]));
+        row[j] = v;
+        double av = fabs(v);
+        long long key = pr + J.posC[j];
+        if (better(av, key, bv, bk)) {
+          bv = av;
+          bk = key;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// compact r x r LU of a factored core: lu[i][j] = a[rowAt[i]][colAt[j]]
+struct LuExtractJob {
+  const double *a;
+  int ld, r;
+  const int *rowAt, *colAt;
+  double *out;
+};
+__global__ void k_lu_extract(const LuExtractJob *__restrict__ jobs) {
+  const LuExtractJob J = jobs[blockIdx.y];
+  long long total = (long long)J.r * J.r;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(e / J.r), j = (int)(e % J.r);
+    J.out[e] = J.a[(long long)J.rowAt[i] * J.ld + J.colAt[j]];
+  }
+}
+
+// row factor: row_out = L^{-1} R[rp[:r], :]   (bdlr.py:178-181), thread per column
+__global__ void k_skel_row(const SkelJob *__restrict__ jobs, const int2 *__restrict__ chunks,
+                           int nchunks) {
+  for (int t = blockIdx.x; t < nchunks; t += gridDim.x) {
+    int2 ch = chunks[t];
+    const SkelJob J = jobs[ch.x];
+    int j = ch.y * blockDim.x + threadIdx.x;
+    if (j >= J.n) continue;
+    for (int i = 0; i < J.r; ++i) {
+      double acc = J.R[(long long)J.rp[i] * J.ldR + j];
+      const double *L = J.lu + (long long)i * J.r;
+      for (int k = 0; k < i; ++k) acc = fma(-L[k], J.row_out[(long long)k * J.n + j], acc);
+      J.row_out[(long long)i * J.n + j] = acc;
+    }
+  }
+}
+
+// col factor: col_out = C[:, cp[:r]] U^{-1}   (bdlr.py:182-183), thread per row
+__global__ void k_skel_col(const SkelJob *__restrict__ jobs, const int2 *__restrict__ chunks,
+                           int nchunks) {
+  for (int t = blockIdx.x; t < nchunks; t += gridDim.x) {
+    int2 ch = chunks[t];
+    const SkelJob J = jobs[ch.x];
+    int i = ch.y * blockDim.x + threadIdx.x;
+    if (i >= J.m) continue;
+    double *x = J.col_out + (long long)i * J.r;
+    const double *c = J.C + (long long)i * J.ldC;
+    for (int j = 0; j < J.r; ++j) {
+      double acc = c[J.cp[j]];
+      for (int k = 0; k < j; ++k) acc = fma(-J.lu[(long long)k * J.r + j], x[k], acc);
+      x[j] = acc / J.lu[(long long)j * J.r + j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// getrf (partial pivoting, LAPACK dgetf2 semantics: first max |a|, row swaps
+// of whole rows, reciprocal scaling), one CTA per matrix, in place.
+// flag: 1 if a zero / non-finite diagonal (reference singular checks) or a
+// non-finite input (hodlr.py:346).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) k_getrf(const LuJob *__restrict__ jobs) {
+  __shared__ MaxLoc red[33];
+  __shared__ int s_p;
+  const LuJob J = jobs[blockIdx.x];
+  const int n = J.n, lda = J.lda, tid = threadIdx.x, nt = blockDim.x;
+  double *a = J.a;
+  for (int k = 0; k < n; ++k) {
+    double bv = -1.0;
+    long long bk = 0x7fffffffffffffffLL;
+    for (int i = k + tid; i < n; i += nt) {
+      double v = fabs(a[(long long)i * lda + k]);
+      if (better(v, i, bv, bk)) {
+        bv = v;
+        bk = i;
+      }
+    }
+    MaxLoc best = block_maxloc(bv, bk, red);
+    if (tid == 0) {
+      int p = (best.key == 0x7fffffffffffffffLL) ? k : (int)best.key;
+      J.piv[k] = p;
+      s_p = p;
+    }
+    __syncthreads();
+    const int p = s_p;
+    const double pv = a[(long long)p * lda + k];
+    if (pv != 0.0) {
+      if (p != k)
+        for (int j = tid; j < n; j += nt) {
+          double t = a[(long long)k * lda + j];
+          a[(long long)k * lda + j] = a[(long long)p * lda + j];
+          a[(long long)p * lda + j] = t;
+        }
+      __syncthreads();
+      const double rinv = 1.0 / pv;
+      for (int i = k + 1 + tid; i < n; i += nt) a[(long long)i * lda + k] *= rinv;
+    }
+    __syncthreads();
+    const int w = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (int i = k + 1 + w; i < n; i += nw) {
+      const double l = a[(long long)i * lda + k];
+      double *ri = a + (long long)i * lda;
+      const double *rk = a + (long long)k * lda;
+      for (int j = k + 1 + lane; j < n; j += 32) ri[j] = fma(-l, rk[j], ri[j]);
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && J.flag) {
+    int bad = 0;
+    for (int k = 0; k < n; ++k) {
+      double d = fabs(a[(long long)k * lda + k]);
+      if (d == 0.0 || !isfinite(d)) bad = 1;
+    }
+    if (bad) *J.flag = 1;
+  }
+}
+
+// non-finite scan of a square block (hodlr.py:346 check before the core LU)
+__global__ void k_check_finite(const LuJob *__restrict__ jobs) {
+  const LuJob J = jobs[blockIdx.x];
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  long long total = (long long)J.n * J.n;
+  for (long long e = threadIdx.x; e < total; e += blockDim.x) {
+    int i = (int)(e / J.n), j = (int)(e % J.n);
+    if (!isfinite(J.a[(long long)i * J.lda + j])) bad = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && bad && J.flag) *J.flag = 1;
+}
+
+// getrs: B <- (LU)^{-1} P B, column-oriented substitution (dtrsm order)
+__global__ void __launch_bounds__(256) k_getrs(const RsJob *__restrict__ jobs) {
+  const RsJob J = jobs[blockIdx.x];
+  const int n = J.n, k = J.k, tid = threadIdx.x, nt = blockDim.x;
+  const double *a = J.a;
+  double *b = J.b;
+  // row interchanges (dlaswp), each thread owns whole columns
+  for (int c = tid; c < k; c += nt)
+    for (int i = 0; i < n; ++i) {
+      int p = J.piv[i];
+      if (p != i) {
+        double t = b[(long long)i * J.ldb + c];
+        b[(long long)i * J.ldb + c] = b[(long long)p * J.ldb + c];
+        b[(long long)p * J.ldb + c] = t;
+      }
+    }
+  __syncthreads();
+  // forward: unit lower
+  for (int i = 0; i < n - 1; ++i) {
+    int rows = n - 1 - i;
+    long long work = (long long)rows * k;
+    for (long long e = tid; e < work; e += nt) {
+      int r = i + 1 + (int)(e / k), c = (int)(e % k);
+      b[(long long)r * J.ldb + c] = fma(-a[(long long)r * J.lda + i], b[(long long)i * J.ldb + c],
+                                        b[(long long)r * J.ldb + c]);
+    }
+    __syncthreads();
+  }
+  // backward: upper
+  for (int i = n - 1; i >= 0; --i) {
+    for (int c = tid; c < k; c += nt) b[(long long)i * J.ldb + c] /= a[(long long)i * J.lda + i];
+    __syncthreads();
+    long long work = (long long)i * k;
+    for (long long e = tid; e < work; e += nt) {
+      int r = (int)(e / k), c = (int)(e % k);
+      b[(long long)r * J.ldb + c] = fma(-a[(long long)r * J.lda + i], b[(long long)i * J.ldb + c],
+                                        b[(long long)r * J.ldb + c]);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// solve-phase vector kernels
+// ---------------------------------------------------------------------------
+__global__ void k_scatter_perm(const double *__restrict__ b, const long long *__restrict__ perm,
+                               double *__restrict__ bu, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    bu[perm[i]] = b[i];
+}
+__global__ void k_gather_perm(const double *__restrict__ x, const long long *__restrict__ perm,
+                              double *__restrict__ out, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = x[perm[i]];
+}
+// b_u[g] -= contributions in post order (multifrontal.py:549 applied lazily)
+__global__ void k_contrib_gather(const long long *__restrict__ gl, int cnt,
+                                 const long long *__restrict__ cptr,
+                                 const long long *__restrict__ coff, const double *__restrict__ cbuf,
+                                 double *__restrict__ bu, double *__restrict__ y) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
+    long long g = gl[t];
+    double acc = bu[g];
+    for (long long q = cptr[g]; q < cptr[g + 1]; ++q) acc = acc - cbuf[coff[q]];
+    bu[g] = acc;
+    if (y) y[g] = acc;
+  }
+}
+// xf[off + j] = x[fro[j]] for all (off, fro) of a height
+__global__ void k_gather_idx(const long long *__restrict__ src_idx, const double *__restrict__ x,
+                             double *__restrict__ dst, long long cnt) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < cnt;
+       t += (long long)gridDim.x * blockDim.x)
+    dst[t] = x[src_idx[t]];
+}
+__global__ void k_copy_idx(const long long *__restrict__ idx, const double *__restrict__ src,
+                           double *__restrict__ dst, long long cnt) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < cnt;
+       t += (long long)gridDim.x * blockDim.x) {
+    long long g = idx[t];
+    dst[g] = src[g];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Krylov vector kernels (deterministic reductions: fixed grid, ordered final sum)
+// ---------------------------------------------------------------------------
+constexpr int RED_BLOCKS = 296, RED_THREADS = 256;
+
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) r += sh[q];
+    sh[32] = r;
+  }
+  __syncthreads();
+  r = sh[32];
+  __syncthreads();
+  return r;
+}
+
+// partial[b] = sum over block b of x.y
+__global__ void __launch_bounds__(RED_THREADS) k_dot_part(const double *__restrict__ x,
+                                                          const double *__restrict__ y,
+                                                          long long n, double *__restrict__ part) {
+  __shared__ double sh[33];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    s = fma(x[i], y[i], s);
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__device__ __forceinline__ double sum_parts(const double *part) {
+  double s = 0.0;
+  for (int q = 0; q < RED_BLOCKS; ++q) s += part[q];
+  return s;
+}
+// out = sum(part) (single thread), optionally sqrt
+__global__ void k_finish(const double *__restrict__ part, double *__restrict__ out, int do_sqrt) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = sum_parts(part);
+    *out = do_sqrt ? sqrt(s) : s;
+  }
+}
+// h = sum(part); w -= h * v ; block 0 stores h
+__global__ void k_mgs_axpy(const double *__restrict__ part, double *__restrict__ hout,
+                           const double *__restrict__ v, double *__restrict__ w, long long n) {
+  __shared__ double h;
+  if (threadIdx.x == 0) h = sum_parts(part);
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *hout = h;
+  const double hh = h;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    w[i] = __dsub_rn(w[i], __dmul_rn(hh, v[i]));  // numpy: w - (h * v)
+}
+// y = a*x (a = 1/s with s read on device)  : V[:, j] = w / h
+__global__ void k_scale_inv(const double *__restrict__ s, const double *__restrict__ x,
+                            double *__restrict__ y, long long n) {
+  const double d = *s;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = x[i] / d;
+}
+__global__ void k_sub(const double *__restrict__ a, const double *__restrict__ b,
+                      double *__restrict__ y, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = a[i] - b[i];
+}
+__global__ void k_add(const double *__restrict__ a, double *__restrict__ y, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = y[i] + a[i];
+}
+// y = sum_i c[i] * V_i   (V_i = V + i*n), fixed order i = 0..j-1
+__global__ void k_combine(const double *__restrict__ V, const double *__restrict__ c, int j,
+                          long long n, double *__restrict__ y) {
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < j; ++i) s = fma(V[(long long)i * n + r], c[i], s);
+    y[r] = s;
+  }
+}
+
+// CSR SpMV, one warp per row (A @ x, sparse.py:277-284)
+__global__ void __launch_bounds__(256) k_spmv(long long nrows, const long long *__restrict__ ptr,
+                                              const int *__restrict__ col,
+                                              const double *__restrict__ val,
+                                              const double *__restrict__ x, double *__restrict__ y) {
+  long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = warp; r < nrows; r += nw) {
+    double s = 0.0;
+    for (long long p = ptr[r] + lane; p < ptr[r + 1]; p += 32) s = fma(val[p], x[col[p]], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) y[r] = s;
+  }
+}
+
+}  // namespace mfh

@@ -1,0 +1,354 @@
+"""Benchmark: HODLR-multifrontal factorization + preconditioned GMRES solve.
+
+One step = ``mf_factorize`` (numeric, accelerated mode) + ``gmres`` (restart
+30, tol 1e-10) of BASELINE.json's configs[1] (C2): 3D 7-point Poisson 48^3,
+N = 110,592, HODLR leaf 64, eps 1e-5, RHS N(0,1) seed 0. The free BDLR
+parameters are fixed as SURVEY.md 6.5 / BASELINE.md 3b recommend so that the
+REFERENCE converges: d = 1, n_c = 1024 (the reference default n_c = 256 stalls
+at 4,000 iterations). The symbolic analysis (ND + etree, host) is done once
+outside the timed region and reported separately.
+
+Arms:
+  default             this framework (libmfh.so, sm_100a)
+  --impl reference    the reference algorithm on the host cores (the CPU
+                      oracle restatement; the Python reference cannot travel
+                      to the GPU box), timed on the full workload (1 core)
+
+Multi-GPU (torchrun, N > 1): replicas only — every rank factors and solves its
+own copy (independent systems, no collective on the data path); value is the
+max-over-ranks step time.
+"""
+
+from __future__ import annotations
+
+import os
+
+# The reference algorithm's many tiny BLAS calls are 5-15x slower with more
+# than one BLAS thread; the CPU legs run single-threaded. Must be
+# set before numpy loads OpenBLAS.
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+
+import argparse
+import json
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (generator, nd_leaf, params, restart, tol, rhs)
+    "c2": dict(desc="3D Poisson 7-pt 48^3 (BASELINE configs[1])", gen=("poisson7", (48, 48, 48)), leaf=64,
+               params=dict(n_c=1024, eps=1e-5, d=1, n_leaf=64), restart=30, tol=1e-10, rhs="normal"),
+    "c1": dict(desc="2D Q1 128^2 (BASELINE configs[0])", gen=("q1_2d", (128,)), leaf=64,
+               params=dict(n_c=256, eps=1e-6, d=1, n_leaf=32), restart=30, tol=1e-10, rhs="uniform"),
+    "c2_nc256": dict(desc="3D Poisson 48^3, reference defaults d=1 n_c=256", gen=("poisson7", (48, 48, 48)),
+                     leaf=64, params=dict(n_c=256, eps=1e-5, d=1, n_leaf=64), restart=30, tol=1e-10,
+                     rhs="normal"),
+    "p32": dict(desc="3D Poisson 32^3 (C2 params)", gen=("poisson7", (32, 32, 32)), leaf=64,
+                params=dict(n_c=256, eps=1e-5, d=1, n_leaf=64), restart=30, tol=1e-10, rhs="normal"),
+}
+METRIC = "factor+GMRES solve time (s) at N; HODLR front GFLOP/s & % of FP64/HBM roofline"
+
+
+def make_problem(cfg):
+    from paper_1410_2697_b200 import problems as PR
+    kind, args = cfg["gen"]
+    A, _ = {"poisson7": PR.gen_poisson7, "q1_2d": PR.gen_q1_2d}[kind](*args)
+    b = PR.seeded_rhs(A.n_rows, 0, cfg["rhs"])
+    return A, b
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace('.', '').isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace('.', '').isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples if len(s) >= 6 for k in range(4)
+                          if s[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world <= 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm: the oracle (reference algorithm restated)
+# ---------------------------------------------------------------------------
+
+class OracleWorkload:
+    """The reference algorithm (CPU oracle restatement) on the bench workload.
+
+    The symbolic analysis is done once (outside the timed step, like the GPU
+    arm); one step = the full numeric factorization + the preconditioned GMRES
+    solve, single-threaded (OPENBLAS_NUM_THREADS=1: the reference's many tiny
+    BLAS calls run 5-15x slower with more BLAS threads).
+    """
+
+    def __init__(self, cfg):
+        from oracle import mfh_oracle as O
+        self.O = O
+        self.cfg = cfg
+        self.A, self.b = make_problem(cfg)
+        ip, ix = O.adjacency(self.A._csc)
+        t0 = time.perf_counter()
+        self.et = O.build_elimination_tree(O.nested_dissection(ip, ix, self.A.n_rows, cfg["leaf"]), self.A._csc)
+        self.t_symbolic = time.perf_counter() - t0
+
+    def step(self):
+        O, cfg, A, b = self.O, self.cfg, self.A, self.b
+        t0 = time.perf_counter()
+        F = O.factorize(A._csc, self.et, "accelerated", **cfg["params"])
+        t1 = time.perf_counter()
+        x, res, its, conv = O.gmres(lambda v: A._csc @ v, b, lambda v: O.solve(F, v), tol=cfg["tol"],
+                                    restart=cfg["restart"])
+        t2 = time.perf_counter()
+        return dict(t=t2 - t0, t_factor=t1 - t0, t_gmres=t2 - t1, its=its, conv=conv, res=res[-1])
+
+
+def sample_text(r, w):
+    return (f"full workload on 1 host core (OPENBLAS_NUM_THREADS=1): oracle factorization "
+            f"{r['t_factor']:.1f} s + GMRES {r['t_gmres']:.1f} s ({r['its']} iterations, converged="
+            f"{r['conv']}); symbolic analysis {w.t_symbolic:.1f} s excluded like the GPU arm")
+
+
+def run_reference_arm(args, cfg, world, rank):
+    if rank != 0:
+        return
+    import multiprocessing
+    w = OracleWorkload(cfg)
+    # the CPU arm has nothing to warm up beyond imports: one warm-up step is a
+    # small instance of the same pipeline, the K timed steps are the full workload
+    small = dict(cfg, gen=("poisson7", (8, 8, 8)), params=dict(cfg["params"], n_c=64))
+    for _ in range(args.warmup):
+        OracleWorkload(small).step()
+    steps = [w.step() for _ in range(args.steps)]
+    t = float(np.mean([r["t"] for r in steps]))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": t, "unit": "s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], **cfg["params"], "restart": cfg["restart"], "tol": cfg["tol"]},
+        "cpu_baseline": {"value": t, "unit": "s", "cores": 1, "kind": "port", "sample": sample_text(steps[-1], w)},
+        "e2e": {"value": t, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gmres": {"iterations": steps[-1]["its"], "converged": steps[-1]["conv"]},
+        "host_cores_available": multiprocessing.cpu_count(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_gpu_arm(args, cfg, world, rank, local):
+    import ctypes as C
+    import torch
+    import paper_1410_2697_b200 as P
+    from paper_1410_2697_b200 import _lib
+
+    os.environ.setdefault("MFH_DEVICE", str(local))
+    torch.cuda.set_device(local)
+    ctx = _lib.context()
+    stream_ptr, _ = ctx.info()
+    lib_stream = torch.cuda.ExternalStream(stream_ptr)
+    A, b = make_problem(cfg)
+    n = A.n_rows
+    t0 = time.perf_counter()
+    et = P.build_elimination_tree(P.nested_dissection(P.adjacency_graph(A), cfg["leaf"]), A)
+    t_sym = time.perf_counter() - t0
+    params = P.MfParams(**cfg["params"])
+    d_b = torch.from_numpy(b).cuda()
+    d_x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    dev_op = A.device_operator()
+    hist = np.empty(4000)
+
+    def step_device():
+        F = P.mf_factorize(A, et, P.ACCELERATED, params)
+        ops = _lib.mfh_gmres_ops()
+        ops.A = dev_op.handle
+        ops.M = F._h
+        nh, its, conv = C.c_int64(), C.c_int64(), C.c_int()
+        _lib.check(_lib.lib().mfh_gmres_device(ctx.handle, C.byref(ops), n, C.c_void_p(d_b.data_ptr()),
+                                               C.c_void_p(d_x.data_ptr()), cfg["tol"], 4000, cfg["restart"],
+                                               _lib.ptr(hist), C.byref(nh), C.byref(its), C.byref(conv)))
+        return F, its.value, bool(conv.value), hist[max(0, nh.value - 1)]
+
+    def step_e2e():  # public API, host b -> host x
+        F = P.mf_factorize(A, et, P.ACCELERATED, params)
+        x, h = P.gmres(A, b, M=P.mf_preconditioner(F), tol=cfg["tol"], restart=cfg["restart"])
+        return F, x, h
+
+    for _ in range(args.warmup):
+        F, its, conv, res = step_device()
+    barrier(world)
+    times, e2e_times = [], []
+    launches0 = ctx.info()[1]
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            barrier(world)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(lib_stream)
+            F, its, conv, res = step_device()
+            e1.record(lib_stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        launches = (ctx.info()[1] - launches0) / max(1, args.steps)
+        for _ in range(max(1, min(args.steps, 3))):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            barrier(world)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(lib_stream)
+            Fe, xe, he = step_e2e()
+            e1.record(lib_stream)
+            torch.cuda.synchronize()
+            e2e_times.append(e0.elapsed_time(e1) / 1e3)
+    t_step = max_over_ranks(float(np.mean(times)), world)
+    t_e2e = max_over_ranks(float(np.mean(e2e_times)), world)
+    true_res = float(np.linalg.norm(A._csc @ xe - b) / np.linalg.norm(b))
+    tim = F.timing()
+    apply_ms, apply_bytes = F.apply_bench(20)
+    pk, pk_kind = peaks()
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    # dominant kernel: complete-pivot LU (k_full_pivot_lu); 8 algorithmic bytes per
+    # trailing-entry visit, per launch = per structured height
+    plu_ms = tim["pivot_lu_ms"]
+    plu_gbs = 8.0 * tim["pivot_lu_visits"] / (plu_ms * 1e-3) / 1e9 if plu_ms > 0 else 0.0
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "n": n, "nnz": A.nnz, **cfg["params"], "nd_leaf": cfg["leaf"],
+                   "restart": cfg["restart"], "tol": cfg["tol"], "rhs": f"{cfg['rhs']} seed 0",
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "flushed (256 MiB write) before every timed step"},
+        "gmres": {"iterations": its, "converged": conv, "final_rel_residual": float(res),
+                  "true_rel_residual_e2e": true_res, "e2e_iterations": he.iterations},
+        "factor": {"device_ms": tim["total_ms"], "host_plan_ms": tim["host_ms"],
+                   "phases_ms": {k: tim[k] for k in ("sample_ms", "pivot_lu_ms", "skeleton_ms",
+                                                     "hodlr_factor_ms", "dense_front_ms", "eliminate_ms")},
+                   "structured_fronts": F.stats.structured_fronts, "dense_fronts": F.stats.dense_fronts,
+                   "peak_stored_reals": F.stats.peak_stored_reals, "device_bytes": F.stats.device_bytes,
+                   "symbolic_s": t_sym},
+        "apply": {"ms": apply_ms, "bytes": apply_bytes, "gbs": apply_bytes / (apply_ms * 1e-3) / 1e9,
+                  "frac_of_hbm": apply_bytes / (apply_ms * 1e-3) / 1e9 / hbm},
+        "roofline": {"kernel": "k_full_pivot_lu", "bound": "hbm", "achieved": plu_gbs, "peak": hbm,
+                     "unit": "GB/s", "frac": plu_gbs / hbm, "traffic": None, "peak_kind": pk_kind},
+        "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": int(8 * (n + A.nnz) + 4 * A.nnz + 8 * (n + 1)),
+                "d2h_bytes_per_step": int(8 * n)},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        w = OracleWorkload(cfg)
+        r = w.step()
+        line["cpu_baseline"] = {"value": r["t"], "unit": "s", "cores": 1, "kind": "port",
+                                "sample": sample_text(r, w)}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    world, rank, local = (1, 0, 0)
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference_arm(args, cfg, world, rank)
+        return
+    world, rank, local = dist_setup(args.gpus)
+    run_gpu_arm(args, cfg, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -84,6 +84,9 @@ int mfh_version(void);
 int mfh_ctx_create(int device, mfh_ctx **out);
 void mfh_ctx_destroy(mfh_ctx *ctx);
 int mfh_ctx_sync(mfh_ctx *ctx);
+/* the context's cudaStream_t (for event timing by the caller) and the number
+ * of kernels this context has launched so far (graph replays count nodes) */
+int mfh_ctx_info(mfh_ctx *ctx, void **stream, int64_t *launches);
 
 /* ---- host symbolic analysis (bit-identical to the reference) -------------- */
 /* AdjGraph.from_pattern (sparse.py:102-111): symmetrized pattern of the

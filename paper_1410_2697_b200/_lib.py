@@ -59,6 +59,39 @@ class mfh_gmres_ops(C.Structure):
 
 _lib = None
 _lock = threading.Lock()
+_finalized = False
+_live = []  # weak references to objects owning native handles
+
+
+def register(obj):
+    """Track an object with a ``_release()`` method so it is freed before CUDA tears down."""
+    import weakref
+    _live.append(weakref.ref(obj))
+
+
+def _shutdown():
+    # Python atexit runs before the CUDA runtime's own exit handlers: release
+    # every device object while the context is still alive.
+    global _finalized, _ctx
+    for r in reversed(_live):
+        o = r()
+        if o is not None:
+            try:
+                o._release()
+            except Exception:
+                pass
+    _live.clear()
+    if _ctx is not None:
+        try:
+            _ctx._release()
+        except Exception:
+            pass
+    _finalized = True
+
+
+import atexit as _atexit  # noqa: E402
+
+_atexit.register(_shutdown)
 P = C.c_void_p
 I64 = C.c_int64
 PP = C.POINTER(C.c_void_p)
@@ -74,6 +107,7 @@ def _sig(lib):
         "mfh_ctx_create": (C.c_int, [C.c_int, PP]),
         "mfh_ctx_destroy": (None, [P]),
         "mfh_ctx_sync": (C.c_int, [P]),
+        "mfh_ctx_info": (C.c_int, [P, PP, pi]),
         "mfh_adjacency": (C.c_int, [I64, P, P, P, P, P, pi]),
         "mfh_nd_create": (C.c_int, [I64, P, P, I64, PP]),
         "mfh_nd_sizes": (C.c_int, [P, pi, pi, pi]),
@@ -165,11 +199,20 @@ class Context:
     def sync(self):
         check(lib().mfh_ctx_sync(self.handle))
 
+    def info(self):
+        """(cudaStream_t as int, kernels launched so far)."""
+        s, n = C.c_void_p(), C.c_int64()
+        check(lib().mfh_ctx_info(self.handle, C.byref(s), C.byref(n)))
+        return s.value or 0, n.value
+
+    def _release(self):
+        if self.handle and not _finalized:
+            lib().mfh_ctx_destroy(self.handle)
+        self.handle = None
+
     def __del__(self):
         try:
-            if self.handle:
-                lib().mfh_ctx_destroy(self.handle)
-                self.handle = None
+            self._release()
         except Exception:
             pass
 

@@ -179,11 +179,12 @@ struct Sink {
   double *scratch_d(size_t n) { return record ? persist->d(n) : ctx->scratch.d(n); }
   int *scratch_i(size_t n) { return record ? persist->i(n) : ctx->scratch.i(n); }
   void launch(std::function<void(cudaStream_t)> f) {
-    ctx->launches++;
-    if (record)
+    if (record) {
       ops.push_back(std::move(f));
-    else
+    } else {
+      ctx->launches++;
       f(ctx->s);
+    }
   }
 };
 
@@ -1526,7 +1527,6 @@ struct Factorizer {
     F->stats.stored_reals = retained;
     F->stats.device_bytes_peak = (int64_t)F->arena.capacity() + (int64_t)ctx->scratch.capacity();
     F->timing.total_ms = tot;
-    F->timing.kernel_launches = ctx->launches;
   }
 };
 
@@ -1727,6 +1727,7 @@ static void apply_device(mfh_factor *F, const double *d_in, double *d_out) {
   if (n == 0) return;
   CK(cudaMemcpyAsync(A->d_b, d_in, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s));
   CK(cudaGraphLaunch(A->exec, ctx->s));
+  ctx->launches += A->nodes;
   CK(cudaMemcpyAsync(d_out, A->d_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s));
 }
 
@@ -1755,6 +1756,7 @@ static void op_apply_device(mfh_csr *A, const double *x, double *y) {
     if (grid < 1) grid = 1;
     k_spmv<<<grid, 256, 0, ctx->s>>>(A->nr, A->ptr, A->col, A->val, x, y);
     check_launch();
+    ctx->launches++;
   } else {
     GemmJob j{A->val, x, y, (int)A->nr, 1, (int)A->nc, (int)A->nc, 1, 1, 1.0, 0.0};
     Sink s{ctx};
@@ -1807,6 +1809,13 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   delete ctx;
 }
 
+extern "C" int mfh_ctx_info(mfh_ctx *ctx, void **stream, int64_t *launches) {
+  MFH_TRY
+  if (stream) *stream = (void *)ctx->c.s;
+  if (launches) *launches = ctx->c.launches;
+  MFH_CATCH
+}
+
 extern "C" int mfh_ctx_sync(mfh_ctx *ctx) {
   MFH_TRY
   CK(cudaStreamSynchronize(ctx->c.s));
@@ -1828,13 +1837,14 @@ extern "C" int mfh_factorize(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const 
   A.val.assign(values, values + A.ptr[n]);
   F = new mfh_factor();
   F->ctx = &ctx->c;
-  ctx->c.launches = 0;
+  int64_t launches0 = ctx->c.launches;
   Factorizer fz{};
   fz.F = F;
   fz.ctx = &ctx->c;
   fz.et = t;
   fz.P = *params;
   fz.run(A, mode);
+  F->timing.kernel_launches = ctx->c.launches - launches0;
   *out = F;
   F = nullptr;
   }
@@ -1937,6 +1947,7 @@ extern "C" int mfh_apply(mfh_factor *f, const double *b, double *x, int64_t nrhs
     } else {
       CK(cudaMemcpyAsync(A->d_b, b + r * n, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->s));
       CK(cudaGraphLaunch(A->exec, ctx->s));
+      ctx->launches += A->nodes;
       CK(cudaMemcpyAsync(x + r * n, A->d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->s));
     }
   }
@@ -2068,6 +2079,7 @@ struct GmresRun {
   }
   // dot into device scalar slot, deterministic
   void dot(const double *x, const double *y, double *out, bool do_sqrt) {
+    ctx->launches += 2;
     k_dot_part<<<RED_BLOCKS, RED_THREADS, 0, ctx->s>>>(x, y, n, ctx->d_part);
     k_finish<<<1, 32, 0, ctx->s>>>(ctx->d_part, out, do_sqrt ? 1 : 0);
     check_launch();
@@ -2114,6 +2126,7 @@ struct GmresRun {
       while (its < max_iter && !conv) {
         A(d_x, w);
         k_sub<<<g, 256, 0, ctx->s>>>(d_b, w, r, n);
+        ctx->launches += 2;
         dot(r, r, S + 1, true);
         double beta = host_scalar(S + 1);
         if (!std::isfinite(beta)) throw value_error("GMRES residual is not finite");
@@ -2134,6 +2147,7 @@ struct GmresRun {
           M(V + j * n, z);
           A(z, w);
           for (int64_t i = 0; i <= j; ++i) {
+            ctx->launches += 2;
             k_dot_part<<<RED_BLOCKS, RED_THREADS, 0, ctx->s>>>(V + i * n, w, n, ctx->d_part);
             k_mgs_axpy<<<g, 256, 0, ctx->s>>>(ctx->d_part, S + 8 + i, V + i * n, w, n);
           }
@@ -2166,7 +2180,10 @@ struct GmresRun {
             lucky_stop = lucky;
             break;
           }
-          if (j < m) k_scale_inv<<<g, 256, 0, ctx->s>>>(S + 2, w, V + j * n, n);
+          if (j < m) {
+            k_scale_inv<<<g, 256, 0, ctx->s>>>(S + 2, w, V + j * n, n);
+            ctx->launches++;
+          }
         }
         if (j > 0) {
           std::vector<double> y(j, 0.0);
@@ -2179,6 +2196,7 @@ struct GmresRun {
           k_combine<<<g, 256, 0, ctx->s>>>(V, dy, (int)j, n, w);
           M(w, z);
           k_add<<<g, 256, 0, ctx->s>>>(z, d_x, n);
+          ctx->launches += 2;
           CK(cudaStreamSynchronize(ctx->s));  // dy host buffer lifetime
         }
         A(d_x, w);

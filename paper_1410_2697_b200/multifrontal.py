@@ -87,6 +87,7 @@ class MfFactorization:
                    for r in recs[:st.n_records]]
         self.stats = FactorStats(st, records)
         self._stored = int(st.stored_reals)
+        _lib.register(self)
 
     def stored_reals(self):
         return self._stored
@@ -122,11 +123,14 @@ class MfFactorization:
         _lib.check(_lib.lib().mfh_apply_bench(self._h, int(reps), C.byref(ms), C.byref(by)))
         return ms.value, by.value
 
+    def _release(self):
+        if self._h and not _lib._finalized:
+            _lib.lib().mfh_factor_free(self._h)
+        self._h = None
+
     def __del__(self):
         try:
-            if self._h:
-                _lib.lib().mfh_factor_free(self._h)
-                self._h = None
+            self._release()
         except Exception:
             pass
 

@@ -105,6 +105,7 @@ class DeviceCsr:
                                              _lib.ptr(ix), _lib.ptr(dv), C.byref(h)))
         self.handle = h
         self.n_rows, self.n_cols = A.n_rows, A.n_cols
+        _lib.register(self)
 
     def matvec(self, x):
         x = _lib.f64(x)
@@ -112,11 +113,14 @@ class DeviceCsr:
         _lib.check(_lib.lib().mfh_spmv(self.handle, _lib.ptr(x), _lib.ptr(y), 0))
         return y
 
+    def _release(self):
+        if self.handle and not _lib._finalized:
+            _lib.lib().mfh_csr_free(self.handle)
+        self.handle = None
+
     def __del__(self):
         try:
-            if self.handle:
-                _lib.lib().mfh_csr_free(self.handle)
-                self.handle = None
+            self._release()
         except Exception:
             pass
 
@@ -134,6 +138,7 @@ class DeviceDense:
         _lib.check(_lib.lib().mfh_dense_create(self.ctx.handle, M.shape[0], _lib.ptr(M), C.byref(h)))
         self.handle = h
         self.n_rows = self.n_cols = M.shape[0]
+        _lib.register(self)
 
     def matvec(self, x):
         x = _lib.f64(x)
@@ -141,11 +146,14 @@ class DeviceDense:
         _lib.check(_lib.lib().mfh_spmv(self.handle, _lib.ptr(x), _lib.ptr(y), 0))
         return y
 
+    def _release(self):
+        if self.handle and not _lib._finalized:
+            _lib.lib().mfh_csr_free(self.handle)
+        self.handle = None
+
     def __del__(self):
         try:
-            if self.handle:
-                _lib.lib().mfh_csr_free(self.handle)
-                self.handle = None
+            self._release()
         except Exception:
             pass
 

@@ -1,0 +1,65 @@
+"""GPU complete-pivot LU (k_full_pivot_lu) against the reference's own outputs:
+bit-exact factors, pivot sequences, ranks and ratios on identical inputs
+(the reference's tests/test_kernels.py:22-37 pattern, golden cores included)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_fplu_bit_exact_on_golden_cores(golden):
+    import paper_1410_2697_b200 as P
+    g = golden("fplu.npz")
+    cnt = int(g["count"])
+    # batched: several eps values -> group by eps
+    by_eps = {}
+    for k in range(cnt):
+        eps = float(g[f"meta{k}"][0])
+        by_eps.setdefault(eps, []).append(k)
+    for eps, ks in by_eps.items():
+        outs = P.full_pivot_lu_batched([g[f"b{k}"] for k in ks], eps,
+                                       [int(g[f"meta{k}"][1]) for k in ks])
+        for k, (lu, rp, cp, rank, ratio) in zip(ks, outs):
+            _, _, r_ref, q_ref = g[f"meta{k}"]
+            assert rank == int(r_ref), k
+            assert ratio == q_ref, k
+            np.testing.assert_array_equal(rp, g[f"rp{k}"])
+            np.testing.assert_array_equal(cp, g[f"cp{k}"])
+            np.testing.assert_array_equal(lu, g[f"lu{k}"])
+
+
+def test_fplu_edge_cases():
+    import paper_1410_2697_b200 as P
+    lu, rp, cp, rank, ratio = P.full_pivot_lu(np.zeros((4, 5)), 1e-8, 4)
+    assert rank == 0 and ratio == 0.0
+    lu, rp, cp, rank, ratio = P.full_pivot_lu(np.array([[1.0, -1.0], [1.0, 1.0]]), 1e-15, 2)
+    assert rank == 2
+    lu, rp, cp, rank, ratio = P.full_pivot_lu(np.ones((1, 1)), 0.5, 1)
+    assert rank == 1 and ratio == 0.0
+
+
+def test_fplu_large_random_vs_oracle(oracle):
+    import paper_1410_2697_b200 as P
+    rng = np.random.default_rng(7)
+    blocks, caps = [], []
+    for m, n, r in ((300, 280, 40), (517, 129, 129), (64, 900, 30), (1, 700, 1), (700, 1, 1)):
+        B = rng.standard_normal((m, r)) @ rng.standard_normal((r, n))
+        blocks.append(B)
+        caps.append(min(m, n))
+    outs = P.full_pivot_lu_batched(blocks, 1e-9, caps)
+    for B, cap, (lu, rp, cp, rank, ratio) in zip(blocks, caps, outs):
+        olu, orp, ocp, orank, oratio = oracle.full_pivot_lu(B, 1e-9, cap)
+        assert rank == orank and ratio == oratio
+        np.testing.assert_array_equal(rp, orp)
+        np.testing.assert_array_equal(cp, ocp)
+        np.testing.assert_array_equal(lu, olu)
+
+
+def test_spmv_matches_scipy():
+    import paper_1410_2697_b200 as P
+    A, _ = P.gen_poisson7(20, 17, 13)
+    x = np.random.default_rng(0).standard_normal(A.n_rows)
+    y = P.spmv(A, x)
+    assert np.linalg.norm(y - A._csc @ x) <= 1e-14 * np.linalg.norm(A._csc @ x)
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        P.spmv(A, np.ones(3))

@@ -135,13 +135,21 @@ def barrier(world):
 
 
 def max_over_ranks(v, world):
+    """Max of a host scalar over ranks (NCCL on the GPU box, gloo in the CPU tests)."""
     if world <= 1:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def replica_plan(world, rank, n_rhs=1):
+    """Replica mode (round 1): every rank factors its own copy of the system; the
+    right-hand sides of a multi-RHS workload are dealt round-robin to ranks."""
+    return [k for k in range(n_rhs) if k % world == rank]
 
 
 # ---------------------------------------------------------------------------

@@ -87,25 +87,58 @@ struct Arena {
   }
 };
 
-// pinned staging for descriptor arrays (async H2D, rewound at sync points)
+// pinned staging for descriptor arrays: async H2D from pinned chunks into
+// matching device chunks; chunks are only rewound at stream sync points, so a
+// descriptor stays valid until the kernels that read it have completed
 struct Stage {
-  char *h = nullptr, *d = nullptr;
-  size_t cap = 0, off = 0;
-  void init(size_t c) {
-    cap = c;
-    CK(cudaMallocHost(&h, cap));
-    CK(cudaMalloc(&d, cap));
+  struct Chunk {
+    char *h = nullptr, *d = nullptr;
+    size_t cap = 0;
+  };
+  std::vector<Chunk> chunks;
+  size_t cur = 0, off = 0, chunk = size_t(64) << 20;
+  void init(size_t c) { chunk = c; }
+  // returns (host, device) addresses for `bytes`
+  std::pair<char *, char *> take(size_t bytes) {
+    size_t b = (bytes + 255) & ~size_t(255);
+    while (true) {
+      if (cur < chunks.size()) {
+        if (off + b <= chunks[cur].cap) {
+          auto r = std::make_pair(chunks[cur].h + off, chunks[cur].d + off);
+          off += b;
+          return r;
+        }
+        ++cur;
+        off = 0;
+        continue;
+      }
+      Chunk c;
+      c.cap = std::max(chunk, b);
+      CK(cudaMallocHost(&c.h, c.cap));
+      CK(cudaMalloc(&c.d, c.cap));
+      chunks.push_back(c);
+    }
+  }
+  void rewind() {
+    cur = 0;
+    off = 0;
   }
   void release() {
-    if (h) cudaFreeHost(h);
-    if (d) cudaFree(d);
-    h = d = nullptr;
+    for (auto &c : chunks) {
+      cudaFreeHost(c.h);
+      cudaFree(c.d);
+    }
+    chunks.clear();
+    rewind();
   }
 };
 
 struct Ctx {
   int device = 0;
   cudaStream_t s = nullptr;
+  cudaStream_t side = nullptr;  // concurrent large-core cluster kernels
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int cluster_size = 16;
   Stage stage;
   Arena scratch;
   double *d_part = nullptr;  // reduction partials
@@ -126,7 +159,7 @@ struct Sink {
 
   void sync_reset() {
     CK(cudaStreamSynchronize(ctx->s));
-    ctx->stage.off = 0;
+    ctx->stage.rewind();
   }
   void *push_bytes(const void *src, size_t bytes) {
     if (bytes == 0) return nullptr;
@@ -135,45 +168,25 @@ struct Sink {
       CK(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice));
       return p;
     }
-    Stage &st = ctx->stage;
-    size_t b = (bytes + 255) & ~size_t(255);
-    if (st.off + b > st.cap) {
-      sync_reset();
-      if (b > st.cap) {  // grow
-        st.release();
-        st.init(std::max(b * 2, st.cap * 2));
-      }
-    }
-    std::memcpy(st.h + st.off, src, bytes);
-    void *dp = st.d + st.off;
-    CK(cudaMemcpyAsync(dp, st.h + st.off, bytes, cudaMemcpyHostToDevice, ctx->s));
-    st.off += b;
-    return dp;
+    auto hd = ctx->stage.take(bytes);
+    std::memcpy(hd.first, src, bytes);
+    CK(cudaMemcpyAsync(hd.second, hd.first, bytes, cudaMemcpyHostToDevice, ctx->s));
+    return hd.second;
   }
   template <class T>
   T *push(const std::vector<T> &v) {
     return (T *)push_bytes(v.data(), v.size() * sizeof(T));
   }
-  // copy into scratch device memory that survives staging rewinds (until the
-  // end of the height, when the scratch arena is reset)
+  // copy into scratch device memory that survives until the end of the height
   template <class T>
   T *push_keep(const std::vector<T> &v) {
     size_t bytes = v.size() * sizeof(T);
     if (bytes == 0) return nullptr;
     if (record) return push(v);
     void *dst = ctx->scratch.alloc(bytes);
-    Stage &st = ctx->stage;
-    size_t b = (bytes + 255) & ~size_t(255);
-    if (st.off + b > st.cap) {
-      sync_reset();
-      if (b > st.cap) {
-        st.release();
-        st.init(std::max(b * 2, st.cap * 2));
-      }
-    }
-    std::memcpy(st.h + st.off, v.data(), bytes);
-    CK(cudaMemcpyAsync(dst, st.h + st.off, bytes, cudaMemcpyHostToDevice, ctx->s));
-    st.off += b;
+    auto hd = ctx->stage.take(bytes);
+    std::memcpy(hd.first, v.data(), bytes);
+    CK(cudaMemcpyAsync(dst, hd.first, bytes, cudaMemcpyHostToDevice, ctx->s));
     return (T *)dst;
   }
   double *scratch_d(size_t n) { return record ? persist->d(n) : ctx->scratch.d(n); }
@@ -215,15 +228,87 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
   });
 }
 
+constexpr int BIG_N = 192;  // above this, LU / solves run blocked across the GPU
+
+static void run_trsm(Sink &sk, const std::vector<TrsmJob> &jobs) {
+  if (jobs.empty()) return;
+  std::vector<int2> ch;
+  for (int q = 0; q < (int)jobs.size(); ++q)
+    for (int c = 0; c < (int)cdiv(jobs[q].ncols, 256); ++c) ch.push_back(make_int2(q, c));
+  if (ch.empty()) return;
+  TrsmJob *dj = sk.push(jobs);
+  int2 *dc = sk.push(ch);
+  int nc = (int)ch.size();
+  sk.launch([=](cudaStream_t st) {
+    k_trsm_small<<<std::min(nc, 148 * 8), 256, 0, st>>>(dj, dc, nc);
+    check_launch();
+  });
+}
+
+static void run_laswp(Sink &sk, const std::vector<SwapJob> &jobs) {
+  for (size_t b = 0; b < jobs.size(); b += 60000) {
+    std::vector<SwapJob> part(jobs.begin() + b, jobs.begin() + std::min(jobs.size(), b + 60000));
+    int mx = 1;
+    for (auto &j : part) mx = std::max(mx, j.ncols);
+    SwapJob *dj = sk.push(part);
+    dim3 grid((unsigned)cdiv(mx, 128), (unsigned)part.size());
+    sk.launch([=](cudaStream_t st) {
+      k_laswp<<<grid, 128, 0, st>>>(dj);
+      check_launch();
+    });
+  }
+}
+
 static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
   if (jobs.empty()) return;
+  std::vector<LuJob> small, big;
+  for (auto &j : jobs) (j.n > BIG_N ? big : small).push_back(j);
+  if (!small.empty()) {
+    int maxn = 0;
+    for (auto &j : small) maxn = std::max(maxn, j.n);
+    LuJob *dj = sk.push(small);
+    int nb = (int)small.size();
+    int th = maxn > 128 ? 512 : (maxn > 32 ? 256 : 64);
+    sk.launch([=](cudaStream_t s) {
+      k_getrf<<<nb, th, 0, s>>>(dj);
+      check_launch();
+    });
+  }
+  if (big.empty()) return;
   int maxn = 0;
-  for (auto &j : jobs) maxn = std::max(maxn, j.n);
-  LuJob *dj = sk.push(jobs);
-  int nb = (int)jobs.size();
-  int th = maxn > 128 ? 512 : (maxn > 32 ? 256 : 64);
+  for (auto &j : big) maxn = std::max(maxn, j.n);
+  for (int c0 = 0; c0 < maxn; c0 += PNB) {
+    std::vector<PanelJob> pj;
+    std::vector<SwapJob> sw;
+    std::vector<TrsmJob> tr;
+    std::vector<GemmJob> gm;
+    for (auto &j : big) {
+      if (j.n <= c0) continue;
+      int w = std::min(PNB, j.n - c0);
+      pj.push_back(PanelJob{j.a, j.n, j.lda, c0, w, j.piv, j.flag});
+      sw.push_back(SwapJob{j.a, j.lda, j.n, j.piv, c0, c0 + w, c0, c0 + w});
+      int rest = j.n - c0 - w;
+      if (rest > 0) {
+        double *A11 = j.a + (int64_t)c0 * j.lda + c0;
+        tr.push_back(TrsmJob{A11, j.lda, w, A11 + w, j.lda, rest, 0});
+        gm.push_back(GemmJob{A11 + (int64_t)w * j.lda, A11 + w, A11 + (int64_t)w * j.lda + w, rest, rest, w, j.lda,
+                             j.lda, j.lda, -1.0, 1.0});
+      }
+    }
+    PanelJob *dp = sk.push(pj);
+    int np_ = (int)pj.size();
+    sk.launch([=](cudaStream_t s) {
+      k_getrf_panel<<<np_, 512, 0, s>>>(dp);
+      check_launch();
+    });
+    run_laswp(sk, sw);
+    run_trsm(sk, tr);
+    run_gemm(sk, gm);
+  }
+  LuJob *dj = sk.push(big);
+  int nb = (int)big.size();
   sk.launch([=](cudaStream_t s) {
-    k_getrf<<<nb, th, 0, s>>>(dj);
+    k_diag_check<<<nb, 256, 0, s>>>(dj);
     check_launch();
   });
 }
@@ -240,12 +325,59 @@ static void run_check_finite(Sink &sk, const std::vector<LuJob> &jobs) {
 
 static void run_getrs(Sink &sk, const std::vector<RsJob> &jobs) {
   if (jobs.empty()) return;
-  RsJob *dj = sk.push(jobs);
-  int nb = (int)jobs.size();
-  sk.launch([=](cudaStream_t s) {
-    k_getrs<<<nb, 256, 0, s>>>(dj);
-    check_launch();
-  });
+  std::vector<RsJob> small, big;
+  for (auto &j : jobs) (j.n > BIG_N ? big : small).push_back(j);
+  if (!small.empty()) {
+    RsJob *dj = sk.push(small);
+    int nb = (int)small.size();
+    sk.launch([=](cudaStream_t s) {
+      k_getrs<<<nb, 256, 0, s>>>(dj);
+      check_launch();
+    });
+  }
+  if (big.empty()) return;
+  // row interchanges, then blocked forward (unit lower) and backward (upper)
+  std::vector<SwapJob> sw;
+  int maxn = 0;
+  for (auto &j : big) {
+    sw.push_back(SwapJob{j.b, j.ldb, j.k, j.piv, 0, j.n, 0, 0});
+    maxn = std::max(maxn, j.n);
+  }
+  run_laswp(sk, sw);
+  for (int c0 = 0; c0 < maxn; c0 += PNB) {
+    std::vector<TrsmJob> tr;
+    std::vector<GemmJob> gm;
+    for (auto &j : big) {
+      if (j.n <= c0) continue;
+      int w = std::min(PNB, j.n - c0);
+      const double *T = j.a + (int64_t)c0 * j.lda + c0;
+      double *Bt = j.b + (int64_t)c0 * j.ldb;
+      tr.push_back(TrsmJob{T, j.lda, w, Bt, j.ldb, j.k, 0});
+      int rest = j.n - c0 - w;
+      if (rest > 0)
+        gm.push_back(GemmJob{T + (int64_t)w * j.lda, Bt, Bt + (int64_t)w * j.ldb, rest, j.k, w, j.lda, j.ldb, j.ldb,
+                             -1.0, 1.0});
+    }
+    run_trsm(sk, tr);
+    run_gemm(sk, gm);
+  }
+  int nblk = (int)cdiv(maxn, PNB);
+  for (int t = nblk - 1; t >= 0; --t) {
+    int c0 = t * PNB;
+    std::vector<TrsmJob> tr;
+    std::vector<GemmJob> gm;
+    for (auto &j : big) {
+      if (j.n <= c0) continue;
+      int w = std::min(PNB, j.n - c0);
+      const double *T = j.a + (int64_t)c0 * j.lda + c0;
+      double *Bt = j.b + (int64_t)c0 * j.ldb;
+      tr.push_back(TrsmJob{T, j.lda, w, Bt, j.ldb, j.k, 1});
+      if (c0 > 0)
+        gm.push_back(GemmJob{j.a + c0, Bt, j.b, c0, j.k, w, j.lda, j.ldb, j.ldb, -1.0, 1.0});
+    }
+    run_trsm(sk, tr);
+    run_gemm(sk, gm);
+  }
 }
 
 static void run_copy(Sink &sk, const std::vector<CopyJob> &jobs) {
@@ -280,6 +412,101 @@ static void run_identity(Sink &sk, const std::vector<double *> &ptrs, const std:
       check_launch();
     });
   }
+}
+
+// complete-pivot LU of a batch of cores: small cores run with the core in
+// shared memory, mid-size cores from L2 with bookkeeping in shared memory,
+// large cores on a thread-block cluster (on the side stream, concurrently)
+constexpr size_t PLU_SMEM_MAX = 227 * 1024;
+constexpr long long PLU_CLUSTER_MIN = 96 * 1024;  // entries
+
+static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
+  if (jobs.empty()) return;
+  Ctx *ctx = sk.ctx;
+  static bool attr_done = false;
+  if (!attr_done) {
+    CK(cudaFuncSetAttribute(k_plu_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLU_SMEM_MAX));
+    CK(cudaFuncSetAttribute(k_plu_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLU_SMEM_MAX));
+    CK(cudaFuncSetAttribute(k_plu_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLU_SMEM_MAX));
+    cudaError_t e = cudaFuncSetAttribute(k_plu_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      ctx->cluster_size = 8;
+    }
+    attr_done = true;
+  }
+  std::vector<int> small[3], mid, big;
+  size_t smax[3] = {48 * 1024, 100 * 1024, PLU_SMEM_MAX};
+  for (int q = 0; q < (int)jobs.size(); ++q) {
+    const PluJob &j = jobs[q];
+    long long ent = (long long)j.m * j.n;
+    size_t with_core = plu_smem_bytes(j.m, j.n, true);
+    size_t book = plu_smem_bytes(j.m, j.n, false);
+    if (book > PLU_SMEM_MAX) throw runtime_error("complete-pivot core too large for the shared-memory bookkeeping");
+    if (ent >= PLU_CLUSTER_MIN) {
+      big.push_back(q);
+    } else if (with_core <= PLU_SMEM_MAX) {
+      int b = with_core <= smax[0] ? 0 : (with_core <= smax[1] ? 1 : 2);
+      small[b].push_back(q);
+    } else {
+      mid.push_back(q);
+    }
+  }
+  PluJob *dj = sk.push(jobs);
+  if (!big.empty()) {
+    int *dids = sk.push(big);
+    size_t sm = 0;
+    for (int q : big) sm = std::max(sm, plu_smem_bytes(jobs[q].m, jobs[q].n, false));
+    int cs = ctx->cluster_size;
+    int nb = (int)big.size();
+    CK(cudaEventRecord(ctx->ev_fork, ctx->s));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb * cs);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = ctx->side;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_plu_cluster, (const PluJob *)dj, (const int *)dids, eps);
+    if (e != cudaSuccess && cs == 16) {  // fall back to the portable cluster size
+      cudaGetLastError();
+      ctx->cluster_size = cs = 8;
+      cfg.gridDim = dim3(nb * cs);
+      at[0].val.clusterDim.x = cs;
+      e = cudaLaunchKernelEx(&cfg, k_plu_cluster, (const PluJob *)dj, (const int *)dids, eps);
+    }
+    if (e != cudaSuccess) throw runtime_error(std::string("cluster launch failed: ") + cudaGetErrorString(e));
+    ctx->launches++;
+    CK(cudaEventRecord(ctx->ev_join, ctx->side));
+  }
+  for (int b = 0; b < 3; ++b) {
+    if (small[b].empty()) continue;
+    int *dids = sk.push(small[b]);
+    size_t sm = 0;
+    for (int q : small[b]) sm = std::max(sm, plu_smem_bytes(jobs[q].m, jobs[q].n, true));
+    int nb = (int)small[b].size();
+    sk.launch([=](cudaStream_t st) {
+      k_plu_cta<true><<<nb, b == 0 ? 256 : 512, sm, st>>>(dj, dids, eps);
+      check_launch();
+    });
+  }
+  if (!mid.empty()) {
+    int *dids = sk.push(mid);
+    size_t sm = 0;
+    for (int q : mid) sm = std::max(sm, plu_smem_bytes(jobs[q].m, jobs[q].n, false));
+    int nb = (int)mid.size();
+    sk.launch([=](cudaStream_t st) {
+      k_plu_cta<false><<<nb, 512, sm, st>>>(dj, dids, eps);
+      check_launch();
+    });
+  }
+  if (!big.empty()) CK(cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0));
 }
 
 // ---------------------------------------------------------------------------
@@ -362,6 +589,7 @@ struct FrontH {
   int height = 0;
   bool structured = false;
   std::vector<int> kids;  // fronts with a non-empty update, in node.children order
+  std::vector<int> allkids;  // every child front (post-order index)
   int64_t freed = 0;
   long long *d_ids = nullptr;
   // dense path
@@ -973,15 +1201,7 @@ struct Factorizer {
 
     // ------------------------------------------------ structured: pivot LU
     run_copy(s, core_copies);
-    {
-      PluJob *dj = s.push(plu);
-      int nb = (int)plu.size();
-      double eps = P.eps;
-      s.launch([=](cudaStream_t st) {
-        k_full_pivot_lu<<<nb, 512, 0, st>>>(dj, eps);
-        check_launch();
-      });
-    }
+    run_plu(s, plu, P.eps);
     cudaEventRecord(ev[3], ctx->s);
     // read ranks, status and pivot sequences: one D2H pair for the height
     {
@@ -1406,6 +1626,7 @@ struct Factorizer {
       int h = 0;
       for (int64_t c : et->children[p]) {
         int ci = pidx[c];
+        f.allkids.push_back(ci);
         h = std::max(h, F->fronts[ci].height + 1);
         FrontH &cf = F->fronts[ci];
         if (cf.nh > 0 && cf.nf > 0) {
@@ -1588,13 +1809,25 @@ static void build_apply(mfh_factor *F) {
   sk.persist = &ar;
   double *bu = AP->bu, *xw = AP->xw, *y = AP->y, *cbuf = AP->cbuf, *xf = AP->xf;
   double bytes = 0;
+  // apply levels count only pivot-carrying nodes: merge nodes (npv = 0) do no
+  // solve work, and skipping them collapses the long merge chains
+  std::vector<int> ah(F->fronts.size(), -1), sub(F->fronts.size(), -1);
   int maxh = 0;
-  for (auto &f : F->fronts) maxh = std::max(maxh, f.height);
-  std::vector<std::vector<int>> byh(maxh + 1);
   for (size_t q = 0; q < F->fronts.size(); ++q) {
     FrontH &f = F->fronts[q];
-    if (f.nh > 0 && f.npv > 0) byh[f.height].push_back((int)q);
+    int below = -1;
+    for (int c : f.allkids) below = std::max(below, sub[c]);
+    if (f.nh > 0 && f.npv > 0) {
+      ah[q] = below + 1;
+      sub[q] = ah[q];
+      maxh = std::max(maxh, ah[q]);
+    } else {
+      sub[q] = below;
+    }
   }
+  std::vector<std::vector<int>> byh(maxh + 1);
+  for (size_t q = 0; q < F->fronts.size(); ++q)
+    if (ah[q] >= 0) byh[ah[q]].push_back((int)q);
   long long *perm = F->d_perm;
   double *db = AP->d_b, *dx = AP->d_x;
   int grid_n = (int)std::min<int64_t>(cdiv(std::max<int64_t>(n, 1), 256), 148 * 8);
@@ -1790,6 +2023,9 @@ extern "C" int mfh_ctx_create(int device, mfh_ctx **out) {
   auto *c = new mfh_ctx();
   c->c.device = device;
   CK(cudaStreamCreateWithFlags(&c->c.s, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->c.side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->c.ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->c.ev_join, cudaEventDisableTiming));
   c->c.stage.init(size_t(64) << 20);
   c->c.scratch.chunk = size_t(512) << 20;
   CK(cudaMalloc(&c->c.d_part, sizeof(double) * (RED_BLOCKS + 64)));
@@ -1805,6 +2041,10 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   ctx->c.scratch.release();
   cudaFree(ctx->c.d_part);
   cudaFree(ctx->c.d_scal);
+  cudaStreamSynchronize(ctx->c.side);
+  cudaEventDestroy(ctx->c.ev_fork);
+  cudaEventDestroy(ctx->c.ev_join);
+  cudaStreamDestroy(ctx->c.side);
   cudaStreamDestroy(ctx->c.s);
   delete ctx;
 }
@@ -1853,7 +2093,7 @@ extern "C" int mfh_factorize(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const 
     if (F) {
       cudaStreamSynchronize(ctx->c.s);
       ctx->c.scratch.reset();
-      ctx->c.stage.off = 0;
+      ctx->c.stage.rewind();
       F->arena.release();
       delete F;
     }
@@ -1864,7 +2104,7 @@ extern "C" int mfh_factorize(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const 
     if (F) {
       cudaStreamSynchronize(ctx->c.s);
       ctx->c.scratch.reset();
-      ctx->c.stage.off = 0;
+      ctx->c.stage.rewind();
       F->arena.release();
       delete F;
     }
@@ -2308,9 +2548,7 @@ extern "C" int mfh_full_pivot_lu_batched(mfh_ctx *ctx, int64_t batch, const int6
     j.outd = dbuf + doff[b] + m + n;
   }
   Sink s{c};
-  PluJob *dj = s.push(jobs);
-  k_full_pivot_lu<<<(int)batch, 512, 0, c->s>>>(dj, eps);
-  check_launch();
+  run_plu(s, jobs, eps);
   std::vector<int> hi(itot);
   std::vector<double> hd(dtot);
   CK(cudaMemcpyAsync(hi.data(), ibuf, sizeof(int) * itot, cudaMemcpyDeviceToHost, c->s));
@@ -2319,7 +2557,7 @@ extern "C" int mfh_full_pivot_lu_batched(mfh_ctx *ctx, int64_t batch, const int6
   CK(cudaMemcpyAsync(raw.data(), d_blocks, sizeof(double) * total, cudaMemcpyDeviceToHost, c->s));
   CK(cudaStreamSynchronize(c->s));
   c->scratch.reset();
-  c->stage.off = 0;
+  c->stage.rewind();
   int64_t ro = 0, co = 0;
   for (int64_t b = 0; b < batch; ++b) {
     int m = (int)ms[b], n = (int)ns[b];

@@ -5,8 +5,11 @@
 // variable-size problems (one etree height, one HODLR level) per launch; the
 // host builds the descriptor arrays.
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+namespace cg = cooperative_groups;
 
 namespace mfh {
 
@@ -359,169 +362,304 @@ __device__ __forceinline__ MaxLoc block_maxloc(double v, long long key, MaxLoc *
 }
 
 // ---------------------------------------------------------------------------
-// complete-pivot partial LU with rank cut (_core.pyx:23-86), one CTA per core.
+// complete-pivot partial LU with rank cut (_core.pyx:23-86).
 // Logical permutation: values stay at their original (row, col); the pivot
 // search ranks candidates by (|a|, -(pos_r * n + pos_c)) with the CURRENT
 // positions, which reproduces the reference's row-major first-max rule and its
 // whole-row / whole-column swaps exactly. Update is mul + sub (no FMA).
+//
+// Two kernels share the step logic:
+//   k_plu_cta<SMEM>  one CTA per core; bookkeeping in shared memory, and the
+//                    core itself too when it fits (SMEM = true)
+//   k_plu_cluster    one thread-block cluster (8-16 CTAs) per large core; the
+//                    core stays in L2/HBM, bookkeeping is replicated per CTA,
+//                    the per-step argmax is reduced through DSMEM, one
+//                    cluster barrier per elimination step
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(512) k_full_pivot_lu(const PluJob *__restrict__ jobs,
-                                                       double eps) {
-  __shared__ MaxLoc red[33];
-  __shared__ int s_done, s_bi, s_bj, s_ar, s_ac;
-  __shared__ double s_akk, s_u11, s_prev;
-  const PluJob J = jobs[blockIdx.x];
-  const int m = J.m, n = J.n, ld = J.ld;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int kmin = min(m, n);
-  for (int i = tid; i < m; i += nt) {
-    J.rowAt[i] = i;
-    J.posR[i] = i;
-    J.actR[i] = i;
-    J.idxR[i] = i;
+struct PluSmem {
+  double *mult, *prow;
+  int *rowAt, *posR, *actR, *idxR, *colAt, *posC, *actC, *idxC;
+};
+
+__host__ __device__ inline size_t plu_smem_bytes(int m, int n, bool core) {
+  size_t b = sizeof(double) * (size_t)(m + n) + sizeof(int) * 4 * (size_t)(m + n);
+  if (core) b += sizeof(double) * (size_t)m * n;
+  return (b + 15) & ~size_t(15);
+}
+
+__device__ __forceinline__ PluSmem plu_carve(char *base, int m, int n) {
+  PluSmem s;
+  s.mult = (double *)base;
+  s.prow = s.mult + m;
+  int *ip = (int *)(s.prow + n);
+  s.rowAt = ip;
+  s.posR = ip + m;
+  s.actR = ip + 2 * m;
+  s.idxR = ip + 3 * m;
+  ip += 4 * m;
+  s.colAt = ip;
+  s.posC = ip + n;
+  s.actC = ip + 2 * n;
+  s.idxC = ip + 3 * n;
+  return s;
+}
+
+struct PluState {
+  int done, bi, bj, ar, ac, rank, status, errk;
+  double akk, u11, prev, ratio, errpiv, errprev;
+};
+
+// step bookkeeping, executed by one thread (identically in every CTA of a cluster)
+__device__ __forceinline__ void plu_decide(PluState &st, PluSmem &S, const double *a, int ld, int n,
+                                           int k, int kmax, double eps, MaxLoc best) {
+  double piv = best.v;
+  int bi, bj;
+  if (best.key == 0x7fffffffffffffffLL) {  // nothing beat -1 (all NaN): reference keeps (k, k)
+    piv = -1.0;
+    bi = S.rowAt[k];
+    bj = S.colAt[k];
+  } else {
+    bi = S.rowAt[(int)(best.key / n)];
+    bj = S.colAt[(int)(best.key % n)];
   }
-  for (int j = tid; j < n; j += nt) {
-    J.colAt[j] = j;
-    J.posC[j] = j;
-    J.actC[j] = j;
-    J.idxC[j] = j;
+  if (k == 0) {
+    st.u11 = piv;
+    if (piv == 0.0) {
+      st.rank = 0;
+      st.ratio = 0.0;
+      st.done = 1;
+      return;
+    }
+  } else {
+    if (piv > st.prev * MFH_PIVOT_GROWTH_BOUND) {
+      st.status = 1;
+      st.errk = k;
+      st.errpiv = piv;
+      st.errprev = st.prev;
+      st.done = 1;
+      return;
+    }
+    double ratio = piv / st.u11;
+    if (ratio < eps || piv <= MFH_ZERO_PIVOT_RATIO * st.u11) {
+      st.rank = k;
+      st.ratio = ratio;
+      st.done = 1;
+      return;
+    }
   }
-  if (tid == 0) {
-    s_done = 0;
-    s_ar = m;
-    s_ac = n;
-    s_prev = 0.0;
-    s_u11 = 0.0;
-    J.out[0] = 0;
-    J.out[1] = 0;
-    J.out[2] = 0;
-    J.outd[0] = 0.0;
+  if (k == kmax) {
+    st.rank = kmax;
+    st.ratio = piv / st.u11;
+    st.done = 1;
+    return;
   }
-  // initial scan (step 0 candidates)
-  double bv = -1.0;
-  long long bk = 0x7fffffffffffffffLL;
-  {
-    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-    for (int i = warp; i < m; i += nw) {
-      const double *row = J.a + (long long)i * ld;
-      for (int j = lane; j < n; j += 32) {
-        double v = fabs(row[j]);
-        long long key = (long long)i * n + j;
-        if (better(v, key, bv, bk)) {
-          bv = v;
-          bk = key;
-        }
+  int pbi = S.posR[bi], ak = S.rowAt[k];
+  S.rowAt[k] = bi;
+  S.rowAt[pbi] = ak;
+  S.posR[bi] = k;
+  S.posR[ak] = pbi;
+  int pbj = S.posC[bj], ck = S.colAt[k];
+  S.colAt[k] = bj;
+  S.colAt[pbj] = ck;
+  S.posC[bj] = k;
+  S.posC[ck] = pbj;
+  int sl = S.idxR[bi], last = S.actR[st.ar - 1];
+  S.actR[sl] = last;
+  S.idxR[last] = sl;
+  st.ar -= 1;
+  sl = S.idxC[bj];
+  last = S.actC[st.ac - 1];
+  S.actC[sl] = last;
+  S.idxC[last] = sl;
+  st.ac -= 1;
+  st.bi = bi;
+  st.bj = bj;
+  st.akk = a[(long long)bi * ld + bj];
+  st.prev = fabs(st.akk);
+  st.rank = k + 1;
+}
+
+__device__ __forceinline__ void plu_init(PluSmem &S, int m, int n) {
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    S.rowAt[i] = i;
+    S.posR[i] = i;
+    S.actR[i] = i;
+    S.idxR[i] = i;
+  }
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    S.colAt[j] = j;
+    S.posC[j] = j;
+    S.actC[j] = j;
+    S.idxC[j] = j;
+  }
+}
+
+// rank-1 update of the rows slot = r0, r0+rstep, ... fused with the next argmax
+__device__ __forceinline__ void plu_update(double *a, int ld, int n, const PluSmem &S, int ar, int ac,
+                                           int r0, int rstep, double &bv, long long &bk) {
+  bv = -1.0;
+  bk = 0x7fffffffffffffffLL;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int ii = r0 + warp * rstep; ii < ar; ii += nw * rstep) {
+    int i = S.actR[ii];
+    double l = S.mult[ii];
+    double *row = a + (long long)i * ld;
+    long long pr = (long long)S.posR[i] * n;
+    for (int jj = lane; jj < ac; jj += 32) {
+      int j = S.actC[jj];
+      double v = __dsub_rn(row[j], __dmul_rn(l, S.prow[jj]));
+      row[j] = v;
+      double av = fabs(v);
+      long long key = pr + S.posC[j];
+      if (better(av, key, bv, bk)) {
+        bv = av;
+        bk = key;
       }
     }
+  }
+}
+
+__device__ __forceinline__ void plu_scan(const double *a, int ld, int n, int m, int r0, int rstep,
+                                         double &bv, long long &bk) {
+  bv = -1.0;
+  bk = 0x7fffffffffffffffLL;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = r0 + warp * rstep; i < m; i += nw * rstep) {
+    const double *row = a + (long long)i * ld;
+    for (int j = lane; j < n; j += 32) {
+      double v = fabs(row[j]);
+      long long key = (long long)i * n + j;
+      if (better(v, key, bv, bk)) {
+        bv = v;
+        bk = key;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void plu_finish(const PluJob &J, const PluSmem &S, const PluState &st, int m, int n) {
+  for (int i = threadIdx.x; i < m; i += blockDim.x) J.rowAt[i] = S.rowAt[i];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) J.colAt[j] = S.colAt[j];
+  if (threadIdx.x == 0) {
+    J.out[0] = st.rank;
+    J.out[1] = st.status;
+    J.out[2] = st.errk;
+    J.outd[0] = st.ratio;
+    J.outd[1] = st.errpiv;
+    J.outd[2] = st.errprev;
+  }
+}
+
+template <bool SMEM_CORE>
+__global__ void __launch_bounds__(512) k_plu_cta(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
+                                                 double eps) {
+  extern __shared__ __align__(16) char dsm[];
+  __shared__ MaxLoc red[33];
+  __shared__ PluState st;
+  const PluJob J = jobs[ids[blockIdx.x]];
+  const int m = J.m, n = J.n;
+  double *a = J.a;
+  int ld = J.ld;
+  char *base = dsm;
+  if (SMEM_CORE) {
+    double *sa = (double *)dsm;
+    for (long long e = threadIdx.x; e < (long long)m * n; e += blockDim.x)
+      sa[e] = J.a[(e / n) * J.ld + (e % n)];
+    a = sa;
+    ld = n;
+    base = dsm + sizeof(double) * (size_t)m * n;
+  }
+  PluSmem S = plu_carve(base, m, n);
+  plu_init(S, m, n);
+  if (threadIdx.x == 0) {
+    st = PluState{};
+    st.ar = m;
+    st.ac = n;
   }
   __syncthreads();
+  double bv;
+  long long bk;
+  plu_scan(a, ld, n, m, 0, 1, bv, bk);
+  const int kmin = min(m, n);
   for (int k = 0; k < kmin; ++k) {
     MaxLoc best = block_maxloc(bv, bk, red);
-    if (tid == 0) {
-      double piv = best.v;
-      long long key = best.key;
-      // key encodes CURRENT positions -> translate to original indices
-      int pr = (int)(key / n), pc = (int)(key % n);
-      int bi = J.rowAt[pr], bj = J.colAt[pc];
-      if (best.key == 0x7fffffffffffffffLL) {  // nothing beat -1 (all NaN): position (k,k)
-        piv = -1.0;
-        bi = J.rowAt[k];
-        bj = J.colAt[k];
-      }
-      if (k == 0) {
-        s_u11 = piv;
-        if (piv == 0.0) {
-          J.out[0] = 0;
-          J.outd[0] = 0.0;
-          s_done = 1;
-        }
-      } else {
-        if (piv > s_prev * MFH_PIVOT_GROWTH_BOUND) {
-          J.out[1] = 1;
-          J.out[2] = k;
-          J.outd[1] = piv;
-          J.outd[2] = s_prev;
-          s_done = 1;
-        } else {
-          double ratio = piv / s_u11;
-          if (ratio < eps || piv <= MFH_ZERO_PIVOT_RATIO * s_u11) {
-            J.out[0] = k;
-            J.outd[0] = ratio;
-            s_done = 1;
-          }
-        }
-      }
-      if (!s_done && k == J.kmax) {
-        J.out[0] = J.kmax;
-        J.outd[0] = piv / s_u11;
-        s_done = 1;
-      }
-      if (!s_done) {
-        // swap positions k <-> pos(bi) for rows, k <-> pos(bj) for cols
-        int pbi = J.posR[bi], ak = J.rowAt[k];
-        J.rowAt[k] = bi;
-        J.rowAt[pbi] = ak;
-        J.posR[bi] = k;
-        J.posR[ak] = pbi;
-        int pbj = J.posC[bj], ck = J.colAt[k];
-        J.colAt[k] = bj;
-        J.colAt[pbj] = ck;
-        J.posC[bj] = k;
-        J.posC[ck] = pbj;
-        // drop the pivot row / column from the active lists
-        int s = J.idxR[bi], last = J.actR[s_ar - 1];
-        J.actR[s] = last;
-        J.idxR[last] = s;
-        s_ar -= 1;
-        s = J.idxC[bj];
-        last = J.actC[s_ac - 1];
-        J.actC[s] = last;
-        J.idxC[last] = s;
-        s_ac -= 1;
-        s_bi = bi;
-        s_bj = bj;
-        double akk = J.a[(long long)bi * ld + bj];
-        s_akk = akk;
-        s_prev = fabs(akk);
-        J.out[0] = k + 1;
-      }
-    }
+    if (threadIdx.x == 0) plu_decide(st, S, a, ld, n, k, J.kmax, eps, best);
     __syncthreads();
-    if (s_done) break;
-    const int bi = s_bi, bj = s_bj, ar = s_ar, ac = s_ac;
-    const double akk = s_akk;
-    // phase A: multipliers a[i, bj] /= akk, pivot row snapshot
-    for (int ii = tid; ii < ar; ii += nt) {
-      int i = J.actR[ii];
-      double l = J.a[(long long)i * ld + bj] / akk;
-      J.a[(long long)i * ld + bj] = l;
-      J.mult[ii] = l;
+    if (st.done) break;
+    const int bi = st.bi, bj = st.bj, ar = st.ar, ac = st.ac;
+    const double akk = st.akk;
+    for (int ii = threadIdx.x; ii < ar; ii += blockDim.x) {
+      int i = S.actR[ii];
+      double l = a[(long long)i * ld + bj] / akk;
+      a[(long long)i * ld + bj] = l;
+      S.mult[ii] = l;
     }
-    for (int jj = tid; jj < ac; jj += nt) J.prow[jj] = J.a[(long long)bi * ld + J.actC[jj]];
+    for (int jj = threadIdx.x; jj < ac; jj += blockDim.x) S.prow[jj] = a[(long long)bi * ld + S.actC[jj]];
     __syncthreads();
-    // phase B: rank-1 update of the trailing block fused with the next argmax
-    bv = -1.0;
-    bk = 0x7fffffffffffffffLL;
-    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-    for (int ii = warp; ii < ar; ii += nw) {
-      int i = J.actR[ii];
-      double l = J.mult[ii];
-      double *row = J.a + (long long)i * ld;
-      long long pr = (long long)J.posR[i] * n;
-      for (int jj = lane; jj < ac; jj += 32) {
-        int j = J.actC[jj];
-        double v = __dsub_rn(row[j], __dmul_rn(l, J.prow[jj]));
-        row[j] = v;
-        double av = fabs(v);
-        long long key = pr + J.posC[j];
-        if (better(av, key, bv, bk)) {
-          bv = av;
-          bk = key;
-        }
-      }
-    }
+    plu_update(a, ld, n, S, ar, ac, 0, 1, bv, bk);
     __syncthreads();
   }
+  if (SMEM_CORE) {
+    for (long long e = threadIdx.x; e < (long long)m * n; e += blockDim.x)
+      J.a[(e / n) * J.ld + (e % n)] = a[e];
+  }
+  plu_finish(J, S, st, m, n);
+}
+
+// one cluster per core; CTA c owns the active-row slots ii with ii % csize == c
+__global__ void __launch_bounds__(512) k_plu_cluster(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
+                                                     double eps) {
+  extern __shared__ __align__(16) char dsm[];
+  __shared__ MaxLoc red[33];
+  __shared__ MaxLoc slot[2];
+  __shared__ PluState st;
+  cg::cluster_group cl = cg::this_cluster();
+  const int crank = (int)cl.block_rank(), csize = (int)cl.num_blocks();
+  const PluJob J = jobs[ids[blockIdx.x / csize]];
+  const int m = J.m, n = J.n, ld = J.ld;
+  double *a = J.a;
+  PluSmem S = plu_carve(dsm, m, n);
+  plu_init(S, m, n);
+  if (threadIdx.x == 0) {
+    st = PluState{};
+    st.ar = m;
+    st.ac = n;
+  }
+  __syncthreads();
+  double bv;
+  long long bk;
+  plu_scan(a, ld, n, m, crank, csize, bv, bk);
+  const int kmin = min(m, n);
+  for (int k = 0; k < kmin; ++k) {
+    MaxLoc best = block_maxloc(bv, bk, red);
+    if (threadIdx.x == 0) slot[k & 1] = best;
+    cl.sync();  // publishes slots and this step's global writes
+    if (threadIdx.x == 0) {
+      MaxLoc g = {-2.0, 0x7fffffffffffffffLL};
+      for (int c = 0; c < csize; ++c) {
+        MaxLoc *rs = cl.map_shared_rank(&slot[k & 1], c);
+        MaxLoc o = *rs;
+        if (better(o.v, o.key, g.v, g.key)) g = o;
+      }
+      plu_decide(st, S, a, ld, n, k, J.kmax, eps, g);
+    }
+    __syncthreads();
+    if (st.done) break;
+    const int bi = st.bi, bj = st.bj, ar = st.ar, ac = st.ac;
+    const double akk = st.akk;
+    for (int ii = crank + (int)threadIdx.x * csize; ii < ar; ii += (int)blockDim.x * csize) {
+      int i = S.actR[ii];
+      double l = a[(long long)i * ld + bj] / akk;
+      a[(long long)i * ld + bj] = l;
+      S.mult[ii] = l;
+    }
+    for (int jj = threadIdx.x; jj < ac; jj += blockDim.x) S.prow[jj] = a[(long long)bi * ld + S.actC[jj]];
+    __syncthreads();
+    plu_update(a, ld, n, S, ar, ac, crank, csize, bv, bk);
+    __syncthreads();
+  }
+  if (crank == 0) plu_finish(J, S, st, m, n);
+  cl.sync();  // no CTA leaves while another may still read its slots
 }
 
 // compact r x r LU of a factored core: lu[i][j] = a[rowAt[i]][colAt[j]]
@@ -636,6 +774,142 @@ __global__ void __launch_bounds__(512) k_getrf(const LuJob *__restrict__ jobs) {
     }
     if (bad) *J.flag = 1;
   }
+}
+
+// ---------------------------------------------------------------------------
+// blocked getrf / getrs building blocks for large matrices (right-looking,
+// panel width PNB; the trailing update is k_gemm across the whole GPU)
+// ---------------------------------------------------------------------------
+constexpr int PNB = 64;
+
+struct PanelJob {  // panel columns [c0, c0+w) of an n x n matrix, rows c0..n-1
+  double *a;
+  int n, lda, c0, w;
+  int *piv;
+  int *flag;
+};
+
+// partial-pivot LU of a tall panel, swaps restricted to the panel columns
+__global__ void __launch_bounds__(512) k_getrf_panel(const PanelJob *__restrict__ jobs) {
+  __shared__ MaxLoc red[33];
+  __shared__ int s_p;
+  const PanelJob J = jobs[blockIdx.x];
+  const int n = J.n, lda = J.lda, c0 = J.c0, w = J.w, tid = threadIdx.x, nt = blockDim.x;
+  double *a = J.a;
+  for (int k = c0; k < c0 + w; ++k) {
+    double bv = -1.0;
+    long long bk = 0x7fffffffffffffffLL;
+    for (int i = k + tid; i < n; i += nt) {
+      double v = fabs(a[(long long)i * lda + k]);
+      if (better(v, i, bv, bk)) {
+        bv = v;
+        bk = i;
+      }
+    }
+    MaxLoc best = block_maxloc(bv, bk, red);
+    if (tid == 0) {
+      int p = (best.key == 0x7fffffffffffffffLL) ? k : (int)best.key;
+      J.piv[k] = p;
+      s_p = p;
+    }
+    __syncthreads();
+    const int p = s_p;
+    const double pv = a[(long long)p * lda + k];
+    if (pv != 0.0) {
+      if (p != k)
+        for (int j = c0 + tid; j < c0 + w; j += nt) {
+          double t = a[(long long)k * lda + j];
+          a[(long long)k * lda + j] = a[(long long)p * lda + j];
+          a[(long long)p * lda + j] = t;
+        }
+      __syncthreads();
+      const double rinv = 1.0 / pv;
+      for (int i = k + 1 + tid; i < n; i += nt) a[(long long)i * lda + k] *= rinv;
+    }
+    __syncthreads();
+    const int wp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (int i = k + 1 + wp; i < n; i += nw) {
+      const double l = a[(long long)i * lda + k];
+      double *ri = a + (long long)i * lda;
+      const double *rk = a + (long long)k * lda;
+      for (int j = k + 1 + lane; j < c0 + w; j += 32) ri[j] = fma(-l, rk[j], ri[j]);
+    }
+    __syncthreads();
+  }
+}
+
+// apply the panel's row swaps to the columns outside the panel
+struct SwapJob {
+  double *a;
+  int lda, ncols;  // columns 0..ncols-1 of a
+  const int *piv;
+  int k0, k1;      // swaps k0..k1-1 (piv[k] = row swapped with row k)
+  int skip0, skip1;  // columns [skip0, skip1) are left alone
+};
+__global__ void k_laswp(const SwapJob *__restrict__ jobs) {
+  const SwapJob J = jobs[blockIdx.y];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < J.ncols; j += gridDim.x * blockDim.x) {
+    if (j >= J.skip0 && j < J.skip1) continue;
+    for (int k = J.k0; k < J.k1; ++k) {
+      int p = J.piv[k];
+      if (p != k) {
+        double t = J.a[(long long)k * J.lda + j];
+        J.a[(long long)k * J.lda + j] = J.a[(long long)p * J.lda + j];
+        J.a[(long long)p * J.lda + j] = t;
+      }
+    }
+  }
+}
+
+// B (w x ncols, ldb) <- T^{-1} B with T = w x w diagonal block (unit lower, or
+// non-unit upper), thread per column, T staged in shared memory
+struct TrsmJob {
+  const double *T;
+  int ldt, w;
+  double *B;
+  int ldb, ncols;
+  int upper;
+};
+__global__ void __launch_bounds__(256) k_trsm_small(const TrsmJob *__restrict__ jobs, const int2 *__restrict__ chunks,
+                                                    int nchunks) {
+  __shared__ double Ts[PNB * PNB];
+  for (int t = blockIdx.x; t < nchunks; t += gridDim.x) {
+    int2 ch = chunks[t];
+    const TrsmJob J = jobs[ch.x];
+    __syncthreads();
+    for (int e = threadIdx.x; e < J.w * J.w; e += blockDim.x) Ts[e] = J.T[(long long)(e / J.w) * J.ldt + (e % J.w)];
+    __syncthreads();
+    int c = ch.y * blockDim.x + threadIdx.x;
+    if (c >= J.ncols) continue;
+    double *b = J.B + c;
+    const int w = J.w;
+    if (!J.upper) {
+      for (int i = 0; i < w; ++i) {
+        double xi = b[(long long)i * J.ldb];
+        for (int r = i + 1; r < w; ++r) b[(long long)r * J.ldb] = fma(-Ts[r * w + i], xi, b[(long long)r * J.ldb]);
+      }
+    } else {
+      for (int i = w - 1; i >= 0; --i) {
+        double xi = b[(long long)i * J.ldb] / Ts[i * w + i];
+        b[(long long)i * J.ldb] = xi;
+        for (int r = 0; r < i; ++r) b[(long long)r * J.ldb] = fma(-Ts[r * w + i], xi, b[(long long)r * J.ldb]);
+      }
+    }
+  }
+}
+
+// diagonal check after a blocked LU
+__global__ void k_diag_check(const LuJob *__restrict__ jobs) {
+  const LuJob J = jobs[blockIdx.x];
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < J.n; k += blockDim.x) {
+    double d = fabs(J.a[(long long)k * J.lda + k]);
+    if (d == 0.0 || !isfinite(d)) bad = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && bad && J.flag) *J.flag = 1;
 }
 
 // non-finite scan of a square block (hodlr.py:346 check before the core LU)

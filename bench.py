@@ -260,6 +260,11 @@ def run_gpu_arm(args, cfg, world, rank, local):
         x, h = P.gmres(A, b, M=P.mf_preconditioner(F), tol=cfg["tol"], restart=cfg["restart"])
         return F, x, h
 
+    if args.profile:  # exactly one factorization + solve, for ncu launch lists
+        F, its, conv, res = step_device()
+        torch.cuda.synchronize()
+        print(json.dumps({"profile_step": True, "iterations": its, "converged": conv}), flush=True)
+        return
     for _ in range(args.warmup):
         F, its, conv, res = step_device()
     barrier(world)
@@ -343,6 +348,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="one untimed step (for ncu)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world, rank, local = (1, 0, 0)

@@ -58,7 +58,7 @@ class mfh_gmres_ops(C.Structure):
 
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()
 _finalized = False
 _live = []  # weak references to objects owning native handles
 

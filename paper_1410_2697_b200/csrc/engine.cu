@@ -228,22 +228,35 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
   });
 }
 
-constexpr int BIG_N = 192;  // above this, LU / solves run blocked across the GPU
-
+// TRSM with a w x w (w <= 64) triangular diagonal block: invert the block
+// (k_trinv), then B <- T^{-1} B as an in-place GEMM (safe: m = w fits one
+// 64-row GEMM tile, so every CTA reads its whole column strip before writing)
 static void run_trsm(Sink &sk, const std::vector<TrsmJob> &jobs) {
   if (jobs.empty()) return;
-  std::vector<int2> ch;
-  for (int q = 0; q < (int)jobs.size(); ++q)
-    for (int c = 0; c < (int)cdiv(jobs[q].ncols, 256); ++c) ch.push_back(make_int2(q, c));
-  if (ch.empty()) return;
-  TrsmJob *dj = sk.push(jobs);
-  int2 *dc = sk.push(ch);
-  int nc = (int)ch.size();
+  std::vector<TrinvJob> ti;
+  std::vector<GemmJob> gm;
+  for (auto &j : jobs) {
+    if (j.ncols <= 0 || j.w <= 0) continue;
+    double *inv = sk.scratch_d((size_t)j.w * j.w);
+    ti.push_back(TrinvJob{j.T, j.ldt, j.w, j.upper, inv});
+    gm.push_back(GemmJob{inv, j.B, j.B, j.w, j.ncols, j.w, j.w, j.ldb, j.ldb, 1.0, 0.0});
+  }
+  if (ti.empty()) return;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_trinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRINV_SMEM));
+    attr = true;
+  }
+  TrinvJob *dj = sk.push(ti);
+  int nb = (int)ti.size();
   sk.launch([=](cudaStream_t st) {
-    k_trsm_small<<<std::min(nc, 148 * 8), 256, 0, st>>>(dj, dc, nc);
+    k_trinv<<<nb, 64, TRINV_SMEM, st>>>(dj);
     check_launch();
   });
+  run_gemm(sk, gm);
 }
+
+constexpr int BIG_N = INV_SMALL;  // above this, LU / solves run blocked across the GPU
 
 static void run_laswp(Sink &sk, const std::vector<SwapJob> &jobs) {
   for (size_t b = 0; b < jobs.size(); b += 60000) {
@@ -380,6 +393,67 @@ static void run_getrs(Sink &sk, const std::vector<RsJob> &jobs) {
   }
 }
 
+struct InvReq {
+  double *a;  // n x n, lda (destroyed for n > INV_SMALL: holds the LU)
+  int n, lda;
+  double *out;  // inverse (n x n, ldo); may equal a when n <= INV_SMALL
+  int ldo;
+  int *piv;     // n ints (blocked path)
+  int *flag;
+};
+static void run_copy(Sink &sk, const std::vector<CopyJob> &jobs);
+static void run_identity(Sink &sk, const std::vector<double *> &ptrs, const std::vector<int> &dims,
+                         const std::vector<int> &lds);
+
+// explicit inverses: in-shared-memory Gauss-Jordan for n <= 128, blocked LU +
+// GEMM-based solve against the identity above that
+static void run_inverse(Sink &sk, const std::vector<InvReq> &reqs) {
+  if (reqs.empty()) return;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_inv_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(sizeof(double) * INV_SMALL * INV_SMALL)));
+    attr = true;
+  }
+  std::vector<InvJob> small;
+  std::vector<CopyJob> cps;
+  std::vector<LuJob> lus;
+  std::vector<RsJob> rss;
+  std::vector<double *> ip;
+  std::vector<int> idim, ild;
+  int maxs = 1;
+  for (auto &r : reqs) {
+    if (r.n <= 0) continue;
+    if (r.n <= INV_SMALL) {
+      if (r.out != r.a) cps.push_back(CopyJob{r.a, r.out, r.n, r.n, r.lda, r.ldo, nullptr, nullptr});
+      small.push_back(InvJob{r.out, r.n, r.ldo, r.flag});
+      maxs = std::max(maxs, r.n);
+    } else {
+      lus.push_back(LuJob{r.a, r.n, r.lda, r.piv, r.flag});
+      ip.push_back(r.out);
+      idim.push_back(r.n);
+      ild.push_back(r.ldo);
+      rss.push_back(RsJob{r.a, r.piv, r.out, r.n, r.lda, r.n, r.ldo});
+    }
+  }
+  run_copy(sk, cps);
+  if (!small.empty()) {
+    InvJob *dj = sk.push(small);
+    int nb = (int)small.size();
+    size_t sm = sizeof(double) * (size_t)maxs * maxs;
+    int th = maxs > 64 ? 512 : 256;
+    sk.launch([=](cudaStream_t st) {
+      k_inv_small<<<nb, th, sm, st>>>(dj);
+      check_launch();
+    });
+  }
+  if (!lus.empty()) {
+    run_getrf(sk, lus);
+    run_identity(sk, ip, idim, ild);
+    run_getrs(sk, rss);
+  }
+}
+
 static void run_copy(Sink &sk, const std::vector<CopyJob> &jobs) {
   for (size_t b = 0; b < jobs.size(); b += 60000) {
     std::vector<CopyJob> part(jobs.begin() + b, jobs.begin() + std::min(jobs.size(), b + 60000));
@@ -417,17 +491,26 @@ static void run_identity(Sink &sk, const std::vector<double *> &ptrs, const std:
 // complete-pivot LU of a batch of cores: small cores run with the core in
 // shared memory, mid-size cores from L2 with bookkeeping in shared memory,
 // large cores on a thread-block cluster (on the side stream, concurrently)
-constexpr size_t PLU_SMEM_MAX = 227 * 1024;
 constexpr long long PLU_CLUSTER_MIN = 96 * 1024;  // entries
 
 static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
   if (jobs.empty()) return;
   Ctx *ctx = sk.ctx;
   static bool attr_done = false;
+  static size_t dyn_max = 0;
   if (!attr_done) {
-    CK(cudaFuncSetAttribute(k_plu_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLU_SMEM_MAX));
-    CK(cudaFuncSetAttribute(k_plu_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLU_SMEM_MAX));
-    CK(cudaFuncSetAttribute(k_plu_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLU_SMEM_MAX));
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    size_t stat = 0;
+    for (const void *fn : {(const void *)k_plu_cta<true>, (const void *)k_plu_cta<false>, (const void *)k_plu_cluster}) {
+      cudaFuncAttributes fa;
+      CK(cudaFuncGetAttributes(&fa, fn));
+      stat = std::max(stat, fa.sharedSizeBytes);
+    }
+    dyn_max = (size_t)optin - stat;
+    CK(cudaFuncSetAttribute(k_plu_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
+    CK(cudaFuncSetAttribute(k_plu_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
+    CK(cudaFuncSetAttribute(k_plu_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
     cudaError_t e = cudaFuncSetAttribute(k_plu_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -436,16 +519,16 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
     attr_done = true;
   }
   std::vector<int> small[3], mid, big;
-  size_t smax[3] = {48 * 1024, 100 * 1024, PLU_SMEM_MAX};
+  size_t smax[3] = {48 * 1024, 100 * 1024, dyn_max};
   for (int q = 0; q < (int)jobs.size(); ++q) {
     const PluJob &j = jobs[q];
     long long ent = (long long)j.m * j.n;
     size_t with_core = plu_smem_bytes(j.m, j.n, true);
     size_t book = plu_smem_bytes(j.m, j.n, false);
-    if (book > PLU_SMEM_MAX) throw runtime_error("complete-pivot core too large for the shared-memory bookkeeping");
+    if (book > dyn_max) throw runtime_error("complete-pivot core too large for the shared-memory bookkeeping");
     if (ent >= PLU_CLUSTER_MIN) {
       big.push_back(q);
-    } else if (with_core <= PLU_SMEM_MAX) {
+    } else if (with_core <= dyn_max) {
       int b = with_core <= smax[0] ? 0 : (with_core <= smax[1] ? 1 : 2);
       small[b].push_back(q);
     } else {
@@ -574,6 +657,7 @@ struct HTree {
   std::vector<int *> cpiv;
   std::vector<int> r1, r2;
   std::vector<FacView> f1, f2;
+  std::vector<double *> linv, cinv;  // explicit inverses of leaves / Woodbury cores (apply)
   HNode *d_nodes = nullptr;
   int maxdepth = 0;
 };
@@ -595,6 +679,8 @@ struct FrontH {
   // dense path
   double *F = nullptr;
   int *piv = nullptr;
+  // apply operators (explicit inverse form, computed once at factor time)
+  double *Pinv = nullptr, *Gfp = nullptr, *Gpf = nullptr;
   // structured path
   int pp = -1, ff = -1, pf = -1, fp = -1;  // tree / block ids
   // update for the parent
@@ -667,8 +753,8 @@ static void collect_subtree(const HTree &t, int root, std::vector<int> &out) {
 
 static void hodlr_solve_batched(Sink &sk, const std::vector<HProblem> &probs) {
   if (probs.empty()) return;
-  std::vector<RsJob> leaves;
-  int maxd = 0;
+  std::vector<GemmJob> leaves;
+  std::vector<CopyJob> leaf_copies;
   struct Item {
     int p, v;
   };
@@ -681,29 +767,30 @@ static void hodlr_solve_batched(Sink &sk, const std::vector<HProblem> &probs) {
     int base_lo = P.t->lo[P.root];
     for (int v : nodes) {
       if (P.t->leaf[v]) {
-        RsJob j{};
-        j.a = P.t->lval[v];
-        j.piv = P.t->lpiv[v];
-        j.n = P.t->hi[v] - P.t->lo[v];
-        j.lda = j.n;
-        j.b = P.rhs + (int64_t)(P.t->lo[v] - base_lo) * P.ld;
-        j.ldb = P.ld;
-        j.k = P.k;
-        if (j.n > 0) leaves.push_back(j);
+        int sz = P.t->hi[v] - P.t->lo[v];
+        if (sz == 0) continue;
+        double *b = P.rhs + (int64_t)(P.t->lo[v] - base_lo) * P.ld;
+        // z_leaf = leaf^{-1} b_leaf; in place when the leaf fits one GEMM row tile
+        if (sz <= GEMM_BM) {
+          leaves.push_back(GemmJob{P.t->linv[v], b, b, sz, P.k, sz, sz, P.ld, P.ld, 1.0, 0.0});
+        } else {
+          double *tmp = sk.scratch_d((size_t)sz * P.k);
+          leaf_copies.push_back(CopyJob{b, tmp, sz, P.k, P.ld, P.k, nullptr, nullptr});
+          leaves.push_back(GemmJob{P.t->linv[v], tmp, b, sz, P.k, sz, sz, P.k, P.ld, 1.0, 0.0});
+        }
       } else {
         int d = P.t->depth[v];
         if ((int)bydepth.size() <= d) bydepth.resize(d + 1);
         bydepth[d].push_back({p, v});
-        maxd = std::max(maxd, d);
       }
     }
   }
-  run_getrs(sk, leaves);
+  run_copy(sk, leaf_copies);
+  run_gemm(sk, leaves);
   for (int d = (int)bydepth.size() - 1; d >= 0; --d) {
     auto &items = bydepth[d];
     if (items.empty()) continue;
-    std::vector<GemmJob> g1, g2;
-    std::vector<RsJob> rs;
+    std::vector<GemmJob> g1, g2, g3;
     for (auto &it : items) {
       const HProblem &P = probs[it.p];
       const HTree &t = *P.t;
@@ -715,19 +802,21 @@ static void hodlr_solve_batched(Sink &sk, const std::vector<HProblem> &probs) {
       double *zt = P.rhs + (int64_t)(lo - base_lo) * P.ld;
       double *zb = P.rhs + (int64_t)(mid - base_lo) * P.ld;
       double *w = sk.scratch_d((size_t)(r1 + r2) * P.k);
+      double *y = sk.scratch_d((size_t)(r1 + r2) * P.k);
       // w_top = row_top @ z_bot ; w_bot = row_bot @ z_top
       if (r1) g1.push_back(GemmJob{t.f1[v].row, zb, w, r1, P.k, hi - mid, t.f1[v].ldr, P.ld, P.k, 1.0, 0.0});
       if (r2)
         g1.push_back(GemmJob{t.f2[v].row, zt, w + (int64_t)r1 * P.k, r2, P.k, mid - lo, t.f2[v].ldr,
                              P.ld, P.k, 1.0, 0.0});
-      rs.push_back(RsJob{t.core[v], t.cpiv[v], w, r1 + r2, r1 + r2, P.k, P.k});
-      if (r1) g2.push_back(GemmJob{t.xt[v], w, zt, mid - lo, P.k, r1, r1, P.k, P.ld, -1.0, 1.0});
+      // y = core^{-1} w
+      g2.push_back(GemmJob{t.cinv[v], w, y, r1 + r2, P.k, r1 + r2, r1 + r2, P.k, P.k, 1.0, 0.0});
+      if (r1) g3.push_back(GemmJob{t.xt[v], y, zt, mid - lo, P.k, r1, r1, P.k, P.ld, -1.0, 1.0});
       if (r2)
-        g2.push_back(GemmJob{t.xb[v], w + (int64_t)r1 * P.k, zb, hi - mid, P.k, r2, r2, P.k, P.ld, -1.0, 1.0});
+        g3.push_back(GemmJob{t.xb[v], y + (int64_t)r1 * P.k, zb, hi - mid, P.k, r2, r2, P.k, P.ld, -1.0, 1.0});
     }
     run_gemm(sk, g1);
-    run_getrs(sk, rs);
     run_gemm(sk, g2);
+    run_gemm(sk, g3);
   }
 }
 
@@ -862,6 +951,8 @@ struct Factorizer {
     t.r2.assign(cap, 0);
     t.f1.assign(cap, FacView{});
     t.f2.assign(cap, FacView{});
+    t.linv.assign(cap, nullptr);
+    t.cinv.assign(cap, nullptr);
     F->trees.push_back(std::move(t));
     int tid = (int)F->trees.size() - 1;
     // recursion with explicit stack: (slot, lo, hi, depth, stage)
@@ -1160,27 +1251,30 @@ struct Factorizer {
 
     // ------------------------------------------------ dense fronts: eliminate
     {
-      std::vector<LuJob> lus;
-      std::vector<CopyJob> cps;
-      std::vector<RsJob> rss;
-      std::vector<GemmJob> gms;
+      // F_pp^{-1} explicitly (multifrontal.py:302-306 semantics incl. the singular
+      // check); Gpf = F_pp^{-1} F_pf; Schur update F_ff -= F_fp Gpf; Gfp = F_fp F_pp^{-1}
+      std::vector<InvReq> inv;
+      std::vector<GemmJob> g1, g2;
       for (int fi : D) {
         FrontH &f = F->fronts[fi];
         if (!f.npv) continue;
         f.flag_slot = new_flag("singular pivot block at node " + std::to_string(f.node), fi);
-        lus.push_back(LuJob{f.F, f.npv, f.nh, f.piv, d_flags + f.flag_slot});
+        f.Pinv = F->arena.d((size_t)f.npv * f.npv);
+        int *pv = f.npv > INV_SMALL ? ctx->scratch.i(f.npv) : nullptr;
+        inv.push_back(InvReq{f.F, f.npv, f.nh, f.Pinv, f.npv, pv, d_flags + f.flag_slot});
         if (f.nf) {
-          double *X = ctx->scratch.d((size_t)f.npv * f.nf);
-          cps.push_back(CopyJob{f.F + f.npv, X, f.npv, f.nf, f.nh, f.nf, nullptr, nullptr});
-          rss.push_back(RsJob{f.F, f.piv, X, f.npv, f.nh, f.nf, f.nf});
-          gms.push_back(GemmJob{f.F + (int64_t)f.npv * f.nh, X, f.F + (int64_t)f.npv * f.nh + f.npv, f.nf,
-                                f.nf, f.npv, f.nh, f.nf, f.nh, -1.0, 1.0});
+          f.Gpf = F->arena.d((size_t)f.npv * f.nf);
+          f.Gfp = F->arena.d((size_t)f.nf * f.npv);
+          g1.push_back(GemmJob{f.Pinv, f.F + f.npv, f.Gpf, f.npv, f.nf, f.npv, f.npv, f.nh, f.nf, 1.0, 0.0});
+          g1.push_back(GemmJob{f.F + (int64_t)f.npv * f.nh, f.Pinv, f.Gfp, f.nf, f.npv, f.npv, f.nh, f.npv,
+                               f.npv, 1.0, 0.0});
+          g2.push_back(GemmJob{f.F + (int64_t)f.npv * f.nh, f.Gpf, f.F + (int64_t)f.npv * f.nh + f.npv, f.nf,
+                               f.nf, f.npv, f.nh, f.nf, f.nh, -1.0, 1.0});
         }
       }
-      run_getrf(s, lus);
-      run_copy(s, cps);
-      run_getrs(s, rss);
-      run_gemm(s, gms);
+      run_inverse(s, inv);
+      run_gemm(s, g1);
+      run_gemm(s, g2);
       for (int fi : D) {
         FrontH &f = F->fronts[fi];
         if (f.nf) {
@@ -1342,20 +1436,26 @@ struct Factorizer {
     for (int fi : S)
       if (F->fronts[fi].pp >= 0) ptrees.push_back(F->fronts[fi].pp);
     {
-      std::vector<LuJob> leaves;
+      // leaves: explicit inverses in place (hodlr.py:322-330 incl. the singular check)
+      std::vector<InvReq> leaves;
       for (int tt : ptrees) {
         HTree &T = F->trees[tt];
         for (int v = 0; v < T.nslots; ++v)
           if (T.leaf[v] == 1) {
             int sz = T.hi[v] - T.lo[v];
-            T.lpiv[v] = F->arena.i(sz);
             std::string msg = "singular pivot in leaf block [" + std::to_string(T.lo[v]) + ", " +
                               std::to_string(T.hi[v]) + ")";
             T.lflag[v] = new_flag(msg, (int64_t)T.fi * 1000000 + v);
-            leaves.push_back(LuJob{T.lval[v], sz, sz, T.lpiv[v], d_flags + T.lflag[v]});
+            if (sz > INV_SMALL) {
+              T.lpiv[v] = F->arena.i(sz);
+              T.linv[v] = F->arena.d((size_t)sz * sz);
+            } else {
+              T.linv[v] = T.lval[v];
+            }
+            leaves.push_back(InvReq{T.lval[v], sz, sz, T.linv[v], sz, T.lpiv[v], d_flags + T.lflag[v]});
           }
       }
-      run_getrf(s, leaves);
+      run_inverse(s, leaves);
       int maxd = 0;
       for (int tt : ptrees) maxd = std::max(maxd, F->trees[tt].maxdepth);
       for (int d = maxd; d >= 0; --d) {
@@ -1377,6 +1477,7 @@ struct Factorizer {
             T.r2[v] = f2.rank;
             T.xt[v] = F->arena.d((size_t)m1 * std::max(1, f1.rank));
             T.xb[v] = F->arena.d((size_t)m2 * std::max(1, f2.rank));
+            // x_top = H1^{-1} col1, x_bot = H2^{-1} col2 (hodlr.py:333-338)
             if (f1.rank) {
               cps.push_back(CopyJob{f1.col, T.xt[v], m1, f1.rank, f1.ldc, f1.rank, nullptr, nullptr});
               probs.push_back(HProblem{&T, 2 * v + 1, T.xt[v], f1.rank, f1.rank});
@@ -1390,11 +1491,12 @@ struct Factorizer {
         if (nodes.empty()) continue;
         run_copy(s, cps);
         hodlr_solve_batched(s, probs);
-        // Woodbury cores
+        // Woodbury cores I + [[0, R1 x_bot], [R2 x_top, 0]] and their inverses (hodlr.py:341-352)
         std::vector<double *> ip;
         std::vector<int> idim, ild;
         std::vector<GemmJob> gms;
-        std::vector<LuJob> lus;
+        std::vector<LuJob> fin;
+        std::vector<InvReq> invs;
         for (auto &nv : nodes) {
           HTree &T = F->trees[nv.first];
           int v = nv.second;
@@ -1403,11 +1505,9 @@ struct Factorizer {
           int lo = T.lo[v], hi = T.hi[v], mid = (lo + hi) >> 1;
           int rr = r1 + r2;
           T.core[v] = F->arena.d((size_t)rr * rr);
-          T.cpiv[v] = F->arena.i(rr);
           ip.push_back(T.core[v]);
           idim.push_back(rr);
           ild.push_back(rr);
-          // core[:r1, r1:] += row_top @ x_bot ; core[r1:, :r1] += row_bot @ x_top
           if (r1 && r2) {
             gms.push_back(GemmJob{T.f1[v].row, T.xb[v], T.core[v] + r1, r1, r2, hi - mid, T.f1[v].ldr, r2, rr,
                                   1.0, 1.0});
@@ -1417,12 +1517,19 @@ struct Factorizer {
           std::string msg = "singular coupling core at node [" + std::to_string(lo) + ", " +
                             std::to_string(hi) + ")";
           int fl = new_flag(msg, (int64_t)T.fi * 1000000 + v);
-          lus.push_back(LuJob{T.core[v], rr, rr, T.cpiv[v], d_flags + fl});
+          fin.push_back(LuJob{T.core[v], rr, rr, nullptr, d_flags + fl});
+          if (rr > INV_SMALL) {
+            T.cpiv[v] = F->arena.i(rr);
+            T.cinv[v] = F->arena.d((size_t)rr * rr);
+          } else {
+            T.cinv[v] = T.core[v];
+          }
+          invs.push_back(InvReq{T.core[v], rr, rr, T.cinv[v], rr, T.cpiv[v], d_flags + fl});
         }
         run_identity(s, ip, idim, ild);
         run_gemm(s, gms);
-        run_check_finite(s, lus);
-        run_getrf(s, lus);
+        run_check_finite(s, fin);
+        run_inverse(s, invs);
       }
     }
     cudaEventRecord(ev[6], ctx->s);
@@ -1764,6 +1871,71 @@ struct ApplyPlan {
   int64_t nodes = 0;
 };
 
+static void run_gemv(Sink &sk, const std::vector<GemvJob> &jobs) {
+  if (jobs.empty()) return;
+  std::vector<int2> rows;
+  for (int q = 0; q < (int)jobs.size(); ++q)
+    for (int i = 0; i < jobs[q].m; ++i) rows.push_back(make_int2(q, i));
+  if (rows.empty()) return;
+  GemvJob *dj = sk.push(jobs);
+  int2 *dr = sk.push(rows);
+  int nr = (int)rows.size();
+  int grid = (int)std::min<int64_t>(cdiv((int64_t)nr * 32, 256), 148 * 16);
+  sk.launch([=](cudaStream_t st) {
+    k_gemv2<<<grid, 256, 0, st>>>(dj, dr, nr);
+    check_launch();
+  });
+}
+
+static GemvJob gemv(double *y, const double *y0, int m, const double *A1, int lda1, int k1, const double *x1,
+                    double a1, const double *A2 = nullptr, int lda2 = 0, int k2 = 0, const double *x2 = nullptr,
+                    const long long *idx2 = nullptr, double a2 = 0.0) {
+  return GemvJob{y, y0, m, A1, lda1, k1, x1, a1, A2, lda2, k2, x2, idx2, a2};
+}
+
+// HODLR solve levels (hodlr.py:360-373) on vectors already holding the leaf
+// solutions: per depth, w = [R_top z_bot; R_bot z_top], y = core^{-1} w,
+// z_top -= X_top y_top, z_bot -= X_bot y_bot (three batched GEMV launches)
+struct ApplyTree {
+  const HTree *t;
+  double *z;  // z[lo..hi) of the tree's local range
+};
+
+static void emit_hodlr_levels(Sink &sk, Arena &ar, const std::vector<ApplyTree> &ts) {
+  int maxd = 0;
+  for (auto &a : ts) maxd = std::max(maxd, a.t->maxdepth);
+  for (int d = maxd; d >= 0; --d) {
+    std::vector<GemvJob> j1, j2, j3;
+    for (auto &a : ts) {
+      const HTree &T = *a.t;
+      for (int v = 0; v < T.nslots; ++v) {
+        if (T.leaf[v] != 0 || T.depth[v] != d) continue;
+        int r1 = T.r1[v], r2 = T.r2[v];
+        if (r1 + r2 == 0) continue;
+        int lo = T.lo[v], hi = T.hi[v], mid = (lo + hi) >> 1;
+        double *zt = a.z + lo, *zb = a.z + mid;
+        double *w = ar.d(r1 + r2), *yv = ar.d(r1 + r2);
+        if (r1) j1.push_back(gemv(w, nullptr, r1, T.f1[v].row, T.f1[v].ldr, hi - mid, zb, 1.0));
+        if (r2) j1.push_back(gemv(w + r1, nullptr, r2, T.f2[v].row, T.f2[v].ldr, mid - lo, zt, 1.0));
+        j2.push_back(gemv(yv, nullptr, r1 + r2, T.cinv[v], r1 + r2, r1 + r2, w, 1.0));
+        if (r1) j3.push_back(gemv(zt, zt, mid - lo, T.xt[v], r1, r1, yv, -1.0));
+        if (r2) j3.push_back(gemv(zb, zb, hi - mid, T.xb[v], r2, r2, yv + r1, -1.0));
+      }
+    }
+    run_gemv(sk, j1);
+    run_gemv(sk, j2);
+    run_gemv(sk, j3);
+  }
+}
+
+static void leaf_jobs(const HTree &T, const double *in, double *out, std::vector<GemvJob> &jobs) {
+  for (int v = 0; v < T.nslots; ++v)
+    if (T.leaf[v] == 1) {
+      int lo = T.lo[v], sz = T.hi[v] - T.lo[v];
+      jobs.push_back(gemv(out + lo, nullptr, sz, T.linv[v], sz, sz, in + lo, 1.0));
+    }
+}
+
 static void build_apply(mfh_factor *F) {
   Ctx *ctx = F->ctx;
   auto AP = std::make_unique<ApplyPlan>();
@@ -1774,6 +1946,7 @@ static void build_apply(mfh_factor *F) {
   AP->bu = ar.d(std::max<int64_t>(1, n));
   AP->xw = ar.d(std::max<int64_t>(1, n));
   AP->y = ar.d(std::max<int64_t>(1, n));
+  double *zz = ar.d(std::max<int64_t>(1, n));
   // contribution offsets (post order)
   std::vector<int64_t> off(F->fronts.size(), -1);
   int64_t tot = 0;
@@ -1784,12 +1957,15 @@ static void build_apply(mfh_factor *F) {
     tot += f.nf;
   }
   AP->cbuf = ar.d(std::max<int64_t>(1, tot));
-  AP->xf = ar.d(std::max<int64_t>(1, tot));
-  // contributions to each global id, in post order
-  std::vector<int64_t> cptr(n + 1, 0), coff(tot);
+  // contributions to each global id, in post order (multifrontal.py:549 order)
+  std::vector<int64_t> cptr(n + 1, 0), coff(tot), fro_all(std::max<int64_t>(1, tot));
   for (size_t q = 0; q < F->fronts.size(); ++q)
     if (off[q] >= 0)
-      for (int j = 0; j < F->fronts[q].nf; ++j) cptr[F->fronts[q].ids[F->fronts[q].npv + j] + 1]++;
+      for (int j = 0; j < F->fronts[q].nf; ++j) {
+        int64_t g = F->fronts[q].ids[F->fronts[q].npv + j];
+        cptr[g + 1]++;
+        fro_all[off[q] + j] = g;
+      }
   for (int64_t i = 0; i < n; ++i) cptr[i + 1] += cptr[i];
   {
     std::vector<int64_t> fill(cptr.begin(), cptr.end() - 1);
@@ -1801,13 +1977,17 @@ static void build_apply(mfh_factor *F) {
   }
   long long *d_cptr = (long long *)ar.alloc(sizeof(int64_t) * (n + 1));
   long long *d_coff = (long long *)ar.alloc(sizeof(int64_t) * std::max<int64_t>(1, tot));
+  long long *d_fro = (long long *)ar.alloc(sizeof(int64_t) * std::max<int64_t>(1, tot));
   CK(cudaMemcpy(d_cptr, cptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
-  if (tot) CK(cudaMemcpy(d_coff, coff.data(), sizeof(int64_t) * tot, cudaMemcpyHostToDevice));
+  if (tot) {
+    CK(cudaMemcpy(d_coff, coff.data(), sizeof(int64_t) * tot, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_fro, fro_all.data(), sizeof(int64_t) * tot, cudaMemcpyHostToDevice));
+  }
 
   Sink sk{ctx};
   sk.record = true;
   sk.persist = &ar;
-  double *bu = AP->bu, *xw = AP->xw, *y = AP->y, *cbuf = AP->cbuf, *xf = AP->xf;
+  double *bu = AP->bu, *xw = AP->xw, *y = AP->y, *cbuf = AP->cbuf;
   double bytes = 0;
   // apply levels count only pivot-carrying nodes: merge nodes (npv = 0) do no
   // solve work, and skipping them collapses the long merge chains
@@ -1836,10 +2016,8 @@ static void build_apply(mfh_factor *F) {
     check_launch();
   });
   bytes += 24.0 * n;
-  auto fstored = [&](const FrontH &f) -> double {
-    return (double)f.factor_reals;
-  };
-  // ---------------- upward
+  auto blk_tmp = [&](const BlockH &b) { return b.rank ? ar.d(b.rank) : nullptr; };
+  // ---------------- upward: b_u[fro] -= apply_fp(pp_solve(b_u[piv]))
   for (int h = 0; h <= maxh; ++h) {
     auto &fis = byh[h];
     if (fis.empty()) continue;
@@ -1852,90 +2030,84 @@ static void build_apply(mfh_factor *F) {
     int cnt = (int)gl.size();
     sk.launch([=](cudaStream_t s) {
       k_contrib_gather<<<(int)std::min<int64_t>(cdiv(cnt, 256), 1184), 256, 0, s>>>(dgl, cnt, d_cptr, d_coff,
-                                                                                  cbuf, bu, y);
+                                                                                  cbuf, bu, nullptr);
       check_launch();
     });
-    std::vector<RsJob> rs;
-    std::vector<HProblem> hp;
-    std::vector<GemmJob> g1, g2;
+    std::vector<GemvJob> j0, j1, j2;
+    std::vector<ApplyTree> ts;
+    std::vector<std::pair<int, double *>> lr;  // structured LR fp: (front, tmp)
     for (int q : fis) {
       FrontH &f = F->fronts[q];
       if (f.nf == 0) continue;
-      double *yv = y + f.piv_lo;
-      bytes += 8.0 * fstored(f);
+      const double *bp = bu + f.piv_lo;
+      double *t = cbuf + off[q];
       if (!f.structured) {
-        rs.push_back(RsJob{f.F, f.piv, yv, f.npv, f.nh, 1, 1});
-        g2.push_back(GemmJob{f.F + (int64_t)f.npv * f.nh, yv, cbuf + off[q], f.nf, 1, f.npv, f.nh, 1, 1, 1.0, 0.0});
+        j0.push_back(gemv(t, nullptr, f.nf, f.Gfp, f.npv, f.npv, bp, 1.0));
+        bytes += 8.0 * (double)f.nf * f.npv;
       } else {
-        hp.push_back(HProblem{&F->trees[f.pp], 0, yv, 1, 1});
+        const HTree &T = F->trees[f.pp];
+        double *z = zz + f.piv_lo;
+        leaf_jobs(T, bp, z, j0);
+        ts.push_back(ApplyTree{&T, z});
         BlockH &b = F->blocks[f.fp];
         if (b.dense) {
-          g2.push_back(GemmJob{b.val, yv, cbuf + off[q], f.nf, 1, f.npv, b.n, 1, 1, 1.0, 0.0});
+          j2.push_back(gemv(t, nullptr, f.nf, b.val, b.n, f.npv, z, 1.0));
         } else if (b.rank) {
-          double *tmp = ar.d(b.rank);
-          g1.push_back(GemmJob{b.row, yv, tmp, b.rank, 1, f.npv, b.n, 1, 1, 1.0, 0.0});
-          g2.push_back(GemmJob{b.col, tmp, cbuf + off[q], f.nf, 1, b.rank, b.rank, 1, 1, 1.0, 0.0});
+          double *tmp = blk_tmp(b);
+          j1.push_back(gemv(tmp, nullptr, b.rank, b.row, b.n, f.npv, z, 1.0));
+          j2.push_back(gemv(t, nullptr, f.nf, b.col, b.rank, b.rank, tmp, 1.0));
         } else {
-          // rank-0 coupling: contribution is exactly zero
-          g2.push_back(GemmJob{b.col, yv, cbuf + off[q], f.nf, 1, 0, 1, 1, 1, 1.0, 0.0});
+          j2.push_back(gemv(t, nullptr, f.nf, nullptr, 0, 0, nullptr, 0.0));  // exact zero contribution
         }
+        bytes += 8.0 * (f.factor_reals - F->blocks[f.pf].stored());
       }
     }
-    run_getrs(sk, rs);
-    hodlr_solve_batched(sk, hp);
-    run_gemm(sk, g1);
-    run_gemm(sk, g2);
+    run_gemv(sk, j0);
+    emit_hodlr_levels(sk, ar, ts);
+    run_gemv(sk, j1);
+    run_gemv(sk, j2);
   }
-  // ---------------- downward
+  // ---------------- downward: x[piv] = pp_solve(b_u[piv] - apply_pf(x[fro]))
   for (int h = maxh; h >= 0; --h) {
     auto &fis = byh[h];
     if (fis.empty()) continue;
-    std::vector<int64_t> gidx, pl;
-    std::vector<RsJob> rs;
-    std::vector<HProblem> hp;
-    std::vector<GemmJob> g1, g2;
+    std::vector<GemvJob> ja, jb, jc;
+    std::vector<ApplyTree> ts;
     for (int q : fis) {
       FrontH &f = F->fronts[q];
-      for (int j = 0; j < f.npv; ++j) pl.push_back(f.ids[j]);
+      const double *bp = bu + f.piv_lo;
       double *xv = xw + f.piv_lo;
+      const long long *fro = f.nf ? d_fro + off[q] : nullptr;
+      if (!f.structured) {
+        jb.push_back(gemv(xv, nullptr, f.npv, f.Pinv, f.npv, f.npv, bp, 1.0, f.Gpf, f.nf, f.nf, xw, fro, -1.0));
+        bytes += 8.0 * ((double)f.npv * f.npv + (double)f.npv * f.nf);
+        continue;
+      }
+      const HTree &T = F->trees[f.pp];
+      double *rhs = y + f.piv_lo;
       if (f.nf) {
-        for (int j = 0; j < f.nf; ++j) gidx.push_back(f.ids[f.npv + j]);
-        double *xfv = xf + (gidx.size() - f.nf);
-        if (!f.structured) {
-          g2.push_back(GemmJob{f.F + f.npv, xfv, xv, f.npv, 1, f.nf, f.nh, 1, 1, -1.0, 1.0});
+        BlockH &b = F->blocks[f.pf];
+        if (b.dense) {
+          jb.push_back(gemv(rhs, bp, f.npv, nullptr, 0, 0, nullptr, 0.0, b.val, b.n, f.nf, xw, fro, -1.0));
+        } else if (b.rank) {
+          double *tmp = blk_tmp(b);
+          ja.push_back(gemv(tmp, nullptr, b.rank, nullptr, 0, 0, nullptr, 0.0, b.row, b.n, f.nf, xw, fro, 1.0));
+          jb.push_back(gemv(rhs, bp, f.npv, b.col, b.rank, b.rank, tmp, -1.0));
         } else {
-          BlockH &b = F->blocks[f.pf];
-          if (b.dense) {
-            g2.push_back(GemmJob{b.val, xfv, xv, f.npv, 1, f.nf, b.n, 1, 1, -1.0, 1.0});
-          } else if (b.rank) {
-            double *tmp = ar.d(b.rank);
-            g1.push_back(GemmJob{b.row, xfv, tmp, b.rank, 1, f.nf, b.n, 1, 1, 1.0, 0.0});
-            g2.push_back(GemmJob{b.col, tmp, xv, f.npv, 1, b.rank, b.rank, 1, 1, -1.0, 1.0});
-          }
+          jb.push_back(gemv(rhs, bp, f.npv, nullptr, 0, 0, nullptr, 0.0));
         }
+        bytes += 8.0 * (f.factor_reals - F->blocks[f.fp].stored());
+        leaf_jobs(T, rhs, xv, jc);
+      } else {
+        leaf_jobs(T, bp, xv, jc);
+        bytes += 8.0 * f.factor_reals;
       }
-      if (!f.structured)
-        rs.push_back(RsJob{f.F, f.piv, xv, f.npv, f.nh, 1, 1});
-      else
-        hp.push_back(HProblem{&F->trees[f.pp], 0, xv, 1, 1});
+      ts.push_back(ApplyTree{&T, xv});
     }
-    // xf (gathered frontal x) shares the cbuf offsets layout only per height; use a compact list
-    long long *dg = gidx.empty() ? nullptr : (long long *)sk.push(gidx);
-    long long *dp = (long long *)sk.push(pl);
-    int64_t ng = (int64_t)gidx.size(), np_ = (int64_t)pl.size();
-    sk.launch([=](cudaStream_t s) {
-      if (ng) {
-        k_gather_idx<<<(int)std::min<int64_t>(cdiv(ng, 256), 1184), 256, 0, s>>>(dg, xw, xf, ng);
-        check_launch();
-      }
-      k_copy_idx<<<(int)std::min<int64_t>(cdiv(np_, 256), 1184), 256, 0, s>>>(dp, bu, xw, np_);
-      check_launch();
-    });
-    for (int q : fis) bytes += 8.0 * fstored(F->fronts[q]);
-    run_gemm(sk, g1);
-    run_gemm(sk, g2);
-    run_getrs(sk, rs);
-    hodlr_solve_batched(sk, hp);
+    run_gemv(sk, ja);
+    run_gemv(sk, jb);
+    run_gemv(sk, jc);
+    emit_hodlr_levels(sk, ar, ts);
   }
   sk.launch([=](cudaStream_t s) {
     k_gather_perm<<<grid_n, 256, 0, s>>>(xw, perm, dx, n);

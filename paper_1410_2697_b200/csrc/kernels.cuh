@@ -898,6 +898,136 @@ __global__ void __launch_bounds__(256) k_trsm_small(const TrsmJob *__restrict__ 
   }
 }
 
+// ---------------------------------------------------------------------------
+// explicit inverses (GPU-native replacement for the reference's lu_factor +
+// lu_solve: every later solve becomes a GEMM / GEMV)
+// ---------------------------------------------------------------------------
+constexpr int INV_SMALL = 128;
+
+struct InvJob {  // in-place inverse of an n x n block (n <= INV_SMALL)
+  double *a;
+  int n, lda;
+  int *flag;  // set when a pivot is zero / non-finite (== reference's LU diagonal checks)
+};
+
+// Gauss-Jordan with partial pivoting (first max |a| in the column, LAPACK
+// idamax rule), whole-row swaps, undone as column swaps at the end
+__global__ void __launch_bounds__(512) k_inv_small(const InvJob *__restrict__ jobs) {
+  extern __shared__ double sA[];
+  __shared__ MaxLoc red[33];
+  __shared__ int piv[INV_SMALL];
+  __shared__ double colk[INV_SMALL];
+  __shared__ int bad;
+  const InvJob J = jobs[blockIdx.x];
+  const int n = J.n, tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < n * n; e += nt) sA[e] = J.a[(long long)(e / n) * J.lda + (e % n)];
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    double bv = -1.0;
+    long long bk = 0x7fffffffffffffffLL;
+    for (int i = k + tid; i < n; i += nt) {
+      double v = fabs(sA[i * n + k]);
+      if (better(v, i, bv, bk)) {
+        bv = v;
+        bk = i;
+      }
+    }
+    MaxLoc best = block_maxloc(bv, bk, red);
+    const int p = (best.key == 0x7fffffffffffffffLL) ? k : (int)best.key;
+    if (tid == 0) piv[k] = p;
+    if (p != k)
+      for (int j = tid; j < n; j += nt) {
+        double t = sA[k * n + j];
+        sA[k * n + j] = sA[p * n + j];
+        sA[p * n + j] = t;
+      }
+    __syncthreads();
+    const double pv = sA[k * n + k];
+    if (pv == 0.0 || !isfinite(pv)) {
+      if (tid == 0) bad = 1;
+      break;
+    }
+    const double rinv = 1.0 / pv;
+    for (int i = tid; i < n; i += nt) colk[i] = sA[i * n + k];
+    __syncthreads();
+    for (int j = tid; j < n; j += nt) sA[k * n + j] = (j == k ? 1.0 : sA[k * n + j]) * rinv;
+    __syncthreads();
+    for (int e = tid; e < n * n; e += nt) {
+      int i = e / n, j = e % n;
+      if (i == k) continue;
+      double f = colk[i];
+      double akj = sA[k * n + j];
+      sA[e] = (j == k ? 0.0 : sA[e]) - f * akj;
+    }
+    __syncthreads();
+  }
+  if (!bad) {
+    for (int k = n - 1; k >= 0; --k) {
+      int p = piv[k];
+      if (p != k)
+        for (int i = tid; i < n; i += nt) {
+          double t = sA[i * n + k];
+          sA[i * n + k] = sA[i * n + p];
+          sA[i * n + p] = t;
+        }
+      __syncthreads();
+    }
+  }
+  for (int e = tid; e < n * n; e += nt) J.a[(long long)(e / n) * J.lda + (e % n)] = sA[e];
+  if (tid == 0 && bad && J.flag) *J.flag = 1;
+}
+
+// inverse of a w x w (w <= 64) diagonal block: unit lower (upper = 0) or
+// non-unit upper (upper = 1); out is w x w, ld w
+struct TrinvJob {
+  const double *T;
+  int ldt, w, upper;
+  double *out;
+};
+constexpr size_t TRINV_SMEM = sizeof(double) * (64 * 64 + 64 * 65);
+__global__ void __launch_bounds__(64) k_trinv(const TrinvJob *__restrict__ jobs) {
+  extern __shared__ double tdyn[];
+  double *Ts = tdyn;
+  double *X = tdyn + 64 * 64;
+  const TrinvJob J = jobs[blockIdx.x];
+  const int w = J.w, j = threadIdx.x;
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) Ts[e] = J.T[(long long)(e / w) * J.ldt + (e % w)];
+  __syncthreads();
+  if (j < w) {
+    if (!J.upper) {
+      for (int i = 0; i < w; ++i) {
+        double v;
+        if (i < j)
+          v = 0.0;
+        else if (i == j)
+          v = 1.0;
+        else {
+          v = 0.0;
+          for (int k = j; k < i; ++k) v = fma(-Ts[i * w + k], X[k * 65 + j], v);
+        }
+        X[i * 65 + j] = v;
+      }
+    } else {
+      for (int i = w - 1; i >= 0; --i) {
+        double v;
+        if (i > j)
+          v = 0.0;
+        else if (i == j)
+          v = 1.0 / Ts[j * w + j];
+        else {
+          double sacc = 0.0;
+          for (int k = i + 1; k <= j; ++k) sacc = fma(Ts[i * w + k], X[k * 65 + j], sacc);
+          v = -sacc / Ts[i * w + i];
+        }
+        X[i * 65 + j] = v;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) J.out[e] = X[(e / w) * 65 + (e % w)];
+}
+
 // diagonal check after a blocked LU
 __global__ void k_diag_check(const LuJob *__restrict__ jobs) {
   const LuJob J = jobs[blockIdx.x];
@@ -966,6 +1096,58 @@ __global__ void __launch_bounds__(256) k_getrs(const RsJob *__restrict__ jobs) {
                                         b[(long long)r * J.ldb + c]);
     }
     __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// batched two-term GEMV for the preconditioner apply (one warp per row):
+//   y[i] = (y0 ? y0[i] : 0) + a1 * A1[i,:] . x1 + a2 * A2[i,:] . x2[idx2]
+// ---------------------------------------------------------------------------
+struct GemvJob {
+  double *y;
+  const double *y0;
+  int m;
+  const double *A1;
+  int lda1, k1;
+  const double *x1;
+  double a1;
+  const double *A2;
+  int lda2, k2;
+  const double *x2;
+  const long long *idx2;
+  double a2;
+};
+
+__global__ void __launch_bounds__(256) k_gemv2(const GemvJob *__restrict__ jobs, const int2 *__restrict__ rows,
+                                               int nrows) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < nrows; t += nw) {
+    int2 r = rows[t];
+    const GemvJob &J = jobs[r.x];
+    const int i = r.y;
+    double s1 = 0.0, s2 = 0.0;
+    if (J.k1) {
+      const double *a = J.A1 + (long long)i * J.lda1;
+      for (int k = lane; k < J.k1; k += 32) s1 = fma(a[k], J.x1[k], s1);
+    }
+    if (J.k2) {
+      const double *a = J.A2 + (long long)i * J.lda2;
+      if (J.idx2)
+        for (int k = lane; k < J.k2; k += 32) s2 = fma(a[k], J.x2[J.idx2[k]], s2);
+      else
+        for (int k = lane; k < J.k2; k += 32) s2 = fma(a[k], J.x2[k], s2);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      s1 += __shfl_down_sync(0xffffffffu, s1, o);
+      s2 += __shfl_down_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+      double v = J.y0 ? J.y0[i] : 0.0;
+      if (J.k1) v += J.a1 * s1;
+      if (J.k2) v += J.a2 * s2;
+      J.y[i] = v;
+    }
   }
 }
 

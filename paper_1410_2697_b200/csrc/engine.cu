@@ -393,6 +393,75 @@ static void run_getrs(Sink &sk, const std::vector<RsJob> &jobs) {
   }
 }
 
+// B (n x k, ldb) <- L^{-1} B, L unit lower n x n (ldl): blocked, GEMM-based
+struct LSolve {
+  const double *L;
+  int ldl, n;
+  double *B;
+  int ldb, k;
+};
+static void run_lower_unit_solve(Sink &sk, const std::vector<LSolve> &jobs) {
+  int maxn = 0;
+  for (auto &j : jobs) maxn = std::max(maxn, j.n);
+  for (int c0 = 0; c0 < maxn; c0 += PNB) {
+    std::vector<TrsmJob> tr;
+    std::vector<GemmJob> gm;
+    for (auto &j : jobs) {
+      if (j.n <= c0 || j.k <= 0) continue;
+      int w = std::min(PNB, j.n - c0);
+      const double *T = j.L + (int64_t)c0 * j.ldl + c0;
+      double *Bt = j.B + (int64_t)c0 * j.ldb;
+      tr.push_back(TrsmJob{T, j.ldl, w, Bt, j.ldb, j.k, 0});
+      int rest = j.n - c0 - w;
+      if (rest > 0)
+        gm.push_back(GemmJob{T + (int64_t)w * j.ldl, Bt, Bt + (int64_t)w * j.ldb, rest, j.k, w, j.ldl, j.ldb, j.ldb,
+                             -1.0, 1.0});
+    }
+    run_trsm(sk, tr);
+    run_gemm(sk, gm);
+  }
+}
+
+// X (m x n, ldx) <- X U^{-1}, U upper n x n (ldu), non-unit: blocked by column strips
+struct RSolve {
+  const double *U;
+  int ldu, n;
+  double *X;
+  int ldx, m;
+};
+static void run_right_upper_solve(Sink &sk, const std::vector<RSolve> &jobs) {
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_trinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRINV_SMEM));
+    attr = true;
+  }
+  int maxn = 0;
+  for (auto &j : jobs) maxn = std::max(maxn, j.n);
+  for (int c0 = 0; c0 < maxn; c0 += PNB) {
+    std::vector<GemmJob> upd, apply;
+    std::vector<TrinvJob> ti;
+    for (auto &j : jobs) {
+      if (j.n <= c0 || j.m <= 0) continue;
+      int w = std::min(PNB, j.n - c0);
+      double *Xt = j.X + c0;
+      if (c0 > 0) upd.push_back(GemmJob{j.X, j.U + c0, Xt, j.m, w, c0, j.ldx, j.ldu, j.ldx, -1.0, 1.0});
+      double *inv = sk.scratch_d((size_t)w * w);
+      ti.push_back(TrinvJob{j.U + (int64_t)c0 * j.ldu + c0, j.ldu, w, 1, inv});
+      apply.push_back(GemmJob{Xt, inv, Xt, j.m, w, w, j.ldx, w, j.ldx, 1.0, 0.0});  // in place: one column tile
+    }
+    run_gemm(sk, upd);
+    if (!ti.empty()) {
+      TrinvJob *dj = sk.push(ti);
+      int nb = (int)ti.size();
+      sk.launch([=](cudaStream_t st) {
+        k_trinv<<<nb, 64, TRINV_SMEM, st>>>(dj);
+        check_launch();
+      });
+    }
+    run_gemm(sk, apply);
+  }
+}
+
 struct InvReq {
   double *a;  // n x n, lda (destroyed for n > INV_SMALL: holds the LU)
   int n, lda;
@@ -1389,20 +1458,19 @@ struct Factorizer {
           check_launch();
         });
       }
-      SkelJob *dsj = s.push(skel);
-      std::vector<int2> rch, cch;
-      for (int q = 0; q < (int)skel.size(); ++q) {
-        for (int c = 0; c < (int)cdiv(skel[q].n, 128); ++c) rch.push_back(make_int2(q, c));
-        for (int c = 0; c < (int)cdiv(skel[q].m, 128); ++c) cch.push_back(make_int2(q, c));
+      // row factor = L^{-1} R[rp[:r], :] ; col factor = C[:, cp[:r]] U^{-1} (bdlr.py:178-183)
+      std::vector<CopyJob> gat;
+      std::vector<LSolve> ls;
+      std::vector<RSolve> rs;
+      for (auto &sj : skel) {
+        gat.push_back(CopyJob{sj.R, sj.row_out, sj.r, sj.n, sj.ldR, sj.n, sj.rp, nullptr});
+        gat.push_back(CopyJob{sj.C, sj.col_out, sj.m, sj.r, sj.ldC, sj.r, nullptr, sj.cp});
+        ls.push_back(LSolve{sj.lu, sj.r, sj.r, sj.row_out, sj.n, sj.n});
+        rs.push_back(RSolve{sj.lu, sj.r, sj.r, sj.col_out, sj.r, sj.m});
       }
-      int2 *drc = s.push(rch), *dcc = s.push(cch);
-      int nr = (int)rch.size(), nc = (int)cch.size();
-      s.launch([=](cudaStream_t st) {
-        k_skel_row<<<std::min(nr, 148 * 16), 128, 0, st>>>(dsj, drc, nr);
-        check_launch();
-        k_skel_col<<<std::min(nc, 148 * 16), 128, 0, st>>>(dsj, dcc, nc);
-        check_launch();
-      });
+      run_copy(s, gat);
+      run_lower_unit_solve(s, ls);
+      run_right_upper_solve(s, rs);
     }
     run_sample(s, dreq, dF, dC);
     cudaEventRecord(ev[5], ctx->s);

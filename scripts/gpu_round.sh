@@ -1,7 +1,7 @@
 #!/bin/bash
 # One GPU call: build check, GPU tests (per-file, bounded), smoke, small bench.
 set -u
-mkdir -p gpurun_out
+mkdir -p gpurun_out; rm -f gpurun_out/summary.txt
 export PYTHONFAULTHANDLER=1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.used --format=csv > gpurun_out/gpu.txt 2>&1
 for f in ${TEST_FILES:-tests/test_gpu_kernels.py tests/test_gpu_mf.py tests/test_gpu_gmres.py}; do

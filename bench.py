@@ -244,8 +244,12 @@ def run_gpu_arm(args, cfg, world, rank, local):
     dev_op = A.device_operator()
     hist = np.empty(4000)
 
+    split = {"factor_s": [], "solve_s": []}
+
     def step_device():
+        t0 = time.perf_counter()
         F = P.mf_factorize(A, et, P.ACCELERATED, params)
+        t1 = time.perf_counter()
         ops = _lib.mfh_gmres_ops()
         ops.A = dev_op.handle
         ops.M = F._h
@@ -253,6 +257,8 @@ def run_gpu_arm(args, cfg, world, rank, local):
         _lib.check(_lib.lib().mfh_gmres_device(ctx.handle, C.byref(ops), n, C.c_void_p(d_b.data_ptr()),
                                                C.c_void_p(d_x.data_ptr()), cfg["tol"], 4000, cfg["restart"],
                                                _lib.ptr(hist), C.byref(nh), C.byref(its), C.byref(conv)))
+        split["factor_s"].append(t1 - t0)
+        split["solve_s"].append(time.perf_counter() - t1)
         return F, its.value, bool(conv.value), hist[max(0, nh.value - 1)]
 
     def step_e2e():  # public API, host b -> host x
@@ -283,6 +289,7 @@ def run_gpu_arm(args, cfg, world, rank, local):
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
         launches = (ctx.info()[1] - launches0) / max(1, args.steps)
+        split = {k: float(np.mean(v[-args.steps:])) for k, v in split.items()}
         for _ in range(max(1, min(args.steps, 3))):
             flush.fill_(1)
             torch.cuda.synchronize()
@@ -317,6 +324,7 @@ def run_gpu_arm(args, cfg, world, rank, local):
                    "l2": "flushed (256 MiB write) before every timed step"},
         "gmres": {"iterations": its, "converged": conv, "final_rel_residual": float(res),
                   "true_rel_residual_e2e": true_res, "e2e_iterations": he.iterations},
+        "split_s": split,
         "factor": {"device_ms": tim["total_ms"], "host_plan_ms": tim["host_ms"],
                    "phases_ms": {k: tim[k] for k in ("sample_ms", "pivot_lu_ms", "skeleton_ms",
                                                      "hodlr_factor_ms", "dense_front_ms", "eliminate_ms")},

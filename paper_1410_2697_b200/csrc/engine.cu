@@ -133,6 +133,14 @@ struct Stage {
   }
 };
 
+// host -> device upload ordered on the library stream (a plain cudaMemcpy from
+// pageable memory is only ordered on the legacy default stream)
+static void upload(cudaStream_t st, void *dst, const void *src, size_t bytes) {
+  if (bytes == 0) return;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+}
+
 struct Ctx {
   int device = 0;
   cudaStream_t s = nullptr;
@@ -165,7 +173,7 @@ struct Sink {
     if (bytes == 0) return nullptr;
     if (record) {
       void *p = persist->alloc(bytes);
-      CK(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice));
+      upload(ctx->s, p, src, bytes);
       return p;
     }
     auto hd = ctx->stage.take(bytes);
@@ -560,7 +568,26 @@ static void run_identity(Sink &sk, const std::vector<double *> &ptrs, const std:
 // complete-pivot LU of a batch of cores: small cores run with the core in
 // shared memory, mid-size cores from L2 with bookkeeping in shared memory,
 // large cores on a thread-block cluster (on the side stream, concurrently)
-constexpr long long PLU_CLUSTER_MIN = 96 * 1024;  // entries
+constexpr long long PLU_CTA_MAX = 16 * 1024;  // entries: one CTA with the core in shared memory
+
+static void launch_cluster(const void *fn, int ncores, int cs, size_t smem, cudaStream_t st, const PluJob *dj,
+                           const int *dids, double eps) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncores * cs);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  void *args[3] = {(void *)&dj, (void *)&dids, (void *)&eps};
+  cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+  if (e != cudaSuccess) throw runtime_error(std::string("cluster launch failed: ") + cudaGetErrorString(e));
+}
 
 static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
   if (jobs.empty()) return;
@@ -571,72 +598,67 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     size_t stat = 0;
-    for (const void *fn : {(const void *)k_plu_cta<true>, (const void *)k_plu_cta<false>, (const void *)k_plu_cluster}) {
+    const void *fns[4] = {(const void *)k_plu_cta<true>, (const void *)k_plu_cta<false>,
+                          (const void *)k_plu_cluster, (const void *)k_plu_cluster_smem};
+    for (const void *fn : fns) {
       cudaFuncAttributes fa;
       CK(cudaFuncGetAttributes(&fa, fn));
       stat = std::max(stat, fa.sharedSizeBytes);
     }
-    dyn_max = (size_t)optin - stat;
-    CK(cudaFuncSetAttribute(k_plu_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
-    CK(cudaFuncSetAttribute(k_plu_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
-    CK(cudaFuncSetAttribute(k_plu_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
-    cudaError_t e = cudaFuncSetAttribute(k_plu_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      ctx->cluster_size = 8;
+    dyn_max = (size_t)optin - stat - 64;
+    for (const void *fn : fns) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
+    for (const void *fn : {fns[2], fns[3]}) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        ctx->cluster_size = 8;
+      }
     }
     attr_done = true;
   }
-  std::vector<int> small[3], mid, big;
+  const int CS = ctx->cluster_size;
+  std::vector<int> small[3], mid, cl8, cl16, clg;
   size_t smax[3] = {48 * 1024, 100 * 1024, dyn_max};
   for (int q = 0; q < (int)jobs.size(); ++q) {
     const PluJob &j = jobs[q];
     long long ent = (long long)j.m * j.n;
     size_t with_core = plu_smem_bytes(j.m, j.n, true);
-    size_t book = plu_smem_bytes(j.m, j.n, false);
-    if (book > dyn_max) throw runtime_error("complete-pivot core too large for the shared-memory bookkeeping");
-    if (ent >= PLU_CLUSTER_MIN) {
-      big.push_back(q);
-    } else if (with_core <= dyn_max) {
+    if (ent <= PLU_CTA_MAX && with_core <= dyn_max) {
       int b = with_core <= smax[0] ? 0 : (with_core <= smax[1] ? 1 : 2);
       small[b].push_back(q);
+      continue;
+    }
+    if (ent < 64 * 1024 && plu_dsm_bytes(j.m, j.n, 8, (j.m + 7) / 8) <= dyn_max) {
+      cl8.push_back(q);
+    } else if (plu_dsm_bytes(j.m, j.n, CS, (j.m + CS - 1) / CS) <= dyn_max) {
+      cl16.push_back(q);
+    } else if (plu_smem_bytes(j.m, j.n, false) <= dyn_max) {
+      clg.push_back(q);
     } else {
-      mid.push_back(q);
+      throw runtime_error("complete-pivot core too large for the shared-memory bookkeeping");
     }
   }
   PluJob *dj = sk.push(jobs);
-  if (!big.empty()) {
-    int *dids = sk.push(big);
-    size_t sm = 0;
-    for (int q : big) sm = std::max(sm, plu_smem_bytes(jobs[q].m, jobs[q].n, false));
-    int cs = ctx->cluster_size;
-    int nb = (int)big.size();
+  bool side = !cl8.empty() || !cl16.empty() || !clg.empty();
+  if (side) {
     CK(cudaEventRecord(ctx->ev_fork, ctx->s));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(nb * cs);
-    cfg.blockDim = dim3(512);
-    cfg.dynamicSmemBytes = sm;
-    cfg.stream = ctx->side;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_plu_cluster, (const PluJob *)dj, (const int *)dids, eps);
-    if (e != cudaSuccess && cs == 16) {  // fall back to the portable cluster size
-      cudaGetLastError();
-      ctx->cluster_size = cs = 8;
-      cfg.gridDim = dim3(nb * cs);
-      at[0].val.clusterDim.x = cs;
-      e = cudaLaunchKernelEx(&cfg, k_plu_cluster, (const PluJob *)dj, (const int *)dids, eps);
-    }
-    if (e != cudaSuccess) throw runtime_error(std::string("cluster launch failed: ") + cudaGetErrorString(e));
-    ctx->launches++;
-    CK(cudaEventRecord(ctx->ev_join, ctx->side));
   }
+  auto cluster_group = [&](const std::vector<int> &g, int cs, bool resident) {
+    if (g.empty()) return;
+    int *dids = sk.push(g);
+    size_t sm = 0;
+    for (int q : g)
+      sm = std::max(sm, resident ? plu_dsm_bytes(jobs[q].m, jobs[q].n, cs, (jobs[q].m + cs - 1) / cs)
+                                 : plu_smem_bytes(jobs[q].m, jobs[q].n, false));
+    launch_cluster(resident ? (const void *)k_plu_cluster_smem : (const void *)k_plu_cluster, (int)g.size(), cs,
+                   sm, ctx->side, dj, dids, eps);
+    ctx->launches++;
+  };
+  cluster_group(clg, CS, false);
+  cluster_group(cl16, CS, true);
+  cluster_group(cl8, 8, true);
+  if (side) CK(cudaEventRecord(ctx->ev_join, ctx->side));
   for (int b = 0; b < 3; ++b) {
     if (small[b].empty()) continue;
     int *dids = sk.push(small[b]);
@@ -648,17 +670,8 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
       check_launch();
     });
   }
-  if (!mid.empty()) {
-    int *dids = sk.push(mid);
-    size_t sm = 0;
-    for (int q : mid) sm = std::max(sm, plu_smem_bytes(jobs[q].m, jobs[q].n, false));
-    int nb = (int)mid.size();
-    sk.launch([=](cudaStream_t st) {
-      k_plu_cta<false><<<nb, 512, sm, st>>>(dj, dids, eps);
-      check_launch();
-    });
-  }
-  if (!big.empty()) CK(cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0));
+  (void)mid;
+  if (side) CK(cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0));
 }
 
 // ---------------------------------------------------------------------------
@@ -1475,27 +1488,32 @@ struct Factorizer {
     run_sample(s, dreq, dF, dC);
     cudaEventRecord(ev[5], ctx->s);
 
-    // ------------------------------------------------ device HNode tables
-    for (int fi : S) {
-      FrontH &f = F->fronts[fi];
-      for (int tt : {f.pp, f.ff}) {
-        if (tt < 0) continue;
-        HTree &T = F->trees[tt];
-        std::vector<HNode> nodes(T.nslots);
-        for (int v = 0; v < T.nslots; ++v) {
-          HNode h{};
-          if (T.leaf[v] == 1)
-            h.leaf = T.lval[v];
-          else if (T.leaf[v] == 0) {
-            h.up = F->blocks[T.up[v]].dev();
-            h.lw = F->blocks[T.lw[v]].dev();
+    // ------------------------------------------------ device HNode tables (one upload)
+    {
+      std::vector<HNode> all;
+      std::vector<std::pair<int, size_t>> where;
+      for (int fi : S) {
+        FrontH &f = F->fronts[fi];
+        for (int tt : {f.pp, f.ff}) {
+          if (tt < 0) continue;
+          HTree &T = F->trees[tt];
+          where.push_back({tt, all.size()});
+          for (int v = 0; v < T.nslots; ++v) {
+            HNode h{};
+            if (T.leaf[v] == 1)
+              h.leaf = T.lval[v];
+            else if (T.leaf[v] == 0) {
+              h.up = F->blocks[T.up[v]].dev();
+              h.lw = F->blocks[T.lw[v]].dev();
+            }
+            all.push_back(h);
           }
-          nodes[v] = h;
         }
-        T.d_nodes = (HNode *)F->arena.alloc(sizeof(HNode) * nodes.size());
-        CK(cudaMemcpyAsync(T.d_nodes, nodes.data(), sizeof(HNode) * nodes.size(), cudaMemcpyHostToDevice,
-                           ctx->s));
-        CK(cudaStreamSynchronize(ctx->s));  // host vector goes out of scope
+      }
+      if (!all.empty()) {
+        HNode *d = (HNode *)F->arena.alloc(sizeof(HNode) * all.size());
+        for (auto &w : where) F->trees[w.first].d_nodes = d + w.second;
+        upload(ctx->s, d, all.data(), sizeof(HNode) * all.size());
       }
     }
 
@@ -1764,10 +1782,10 @@ struct Factorizer {
       d_ap_ptr = (long long *)F->arena.alloc(sizeof(int64_t) * (n + 1));
       d_ap_col = F->arena.i(std::max<int64_t>(1, ap_col.size()));
       d_ap_val = F->arena.d(std::max<int64_t>(1, ap_val.size()));
-      CK(cudaMemcpy(d_ap_ptr, ap_ptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+      upload(ctx->s, d_ap_ptr, ap_ptr.data(), sizeof(int64_t) * (n + 1));
       if (!ap_col.empty()) {
-        CK(cudaMemcpy(d_ap_col, ap_col.data(), sizeof(int) * ap_col.size(), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(d_ap_val, ap_val.data(), sizeof(double) * ap_val.size(), cudaMemcpyHostToDevice));
+        upload(ctx->s, d_ap_col, ap_col.data(), sizeof(int) * ap_col.size());
+        upload(ctx->s, d_ap_val, ap_val.data(), sizeof(double) * ap_val.size());
       }
       if (accel) {
         std::vector<int64_t> ptr64(ap_ptr), col64(ap_col.begin(), ap_col.end());
@@ -1825,12 +1843,19 @@ struct Factorizer {
       run_identity(s, {F->ident}, {(int)max_nh}, {(int)max_nh});
     }
     F->d_perm = (long long *)F->arena.alloc(sizeof(int64_t) * std::max<int64_t>(1, n));
-    if (n) CK(cudaMemcpy(F->d_perm, et->perm.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+    upload(ctx->s, F->d_perm, et->perm.data(), sizeof(int64_t) * n);
     // device ids + flags
-    for (auto &f : F->fronts) {
-      if (f.nh == 0) continue;
-      f.d_ids = (long long *)F->arena.alloc(sizeof(int64_t) * f.nh);
-      CK(cudaMemcpy(f.d_ids, f.ids.data(), sizeof(int64_t) * f.nh, cudaMemcpyHostToDevice));
+    {  // all front id lists in one upload
+      int64_t tot = 0;
+      for (auto &f : F->fronts) tot += f.nh;
+      long long *all = (long long *)F->arena.alloc(sizeof(int64_t) * std::max<int64_t>(1, tot));
+      std::vector<int64_t> flat;
+      flat.reserve(tot);
+      for (auto &f : F->fronts) {
+        f.d_ids = f.nh ? all + flat.size() : nullptr;
+        flat.insert(flat.end(), f.ids.begin(), f.ids.end());
+      }
+      upload(ctx->s, all, flat.data(), sizeof(int64_t) * tot);
     }
     int max_flags = 0;
     for (auto &f : F->fronts) max_flags += 1 + (f.structured ? 8 * (int)(f.nh / std::max<int64_t>(1, P.n_leaf) + 2) : 0);
@@ -2046,10 +2071,10 @@ static void build_apply(mfh_factor *F) {
   long long *d_cptr = (long long *)ar.alloc(sizeof(int64_t) * (n + 1));
   long long *d_coff = (long long *)ar.alloc(sizeof(int64_t) * std::max<int64_t>(1, tot));
   long long *d_fro = (long long *)ar.alloc(sizeof(int64_t) * std::max<int64_t>(1, tot));
-  CK(cudaMemcpy(d_cptr, cptr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+  upload(ctx->s, d_cptr, cptr.data(), sizeof(int64_t) * (n + 1));
   if (tot) {
-    CK(cudaMemcpy(d_coff, coff.data(), sizeof(int64_t) * tot, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(d_fro, fro_all.data(), sizeof(int64_t) * tot, cudaMemcpyHostToDevice));
+    upload(ctx->s, d_coff, coff.data(), sizeof(int64_t) * tot);
+    upload(ctx->s, d_fro, fro_all.data(), sizeof(int64_t) * tot);
   }
 
   Sink sk{ctx};
@@ -2470,10 +2495,10 @@ extern "C" int mfh_csr_create(mfh_ctx *ctx, int64_t n_rows, int64_t n_cols, cons
   CK(cudaMalloc(&A->col, sizeof(int) * std::max<int64_t>(1, nnz)));
   CK(cudaMalloc(&A->val, sizeof(double) * std::max<int64_t>(1, nnz)));
   std::vector<int> c32(indices, indices + nnz);
-  CK(cudaMemcpy(A->ptr, indptr, sizeof(int64_t) * (n_rows + 1), cudaMemcpyHostToDevice));
+  upload(A->ctx->s, A->ptr, indptr, sizeof(int64_t) * (n_rows + 1));
   if (nnz) {
-    CK(cudaMemcpy(A->col, c32.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(A->val, values, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+    upload(A->ctx->s, A->col, c32.data(), sizeof(int) * nnz);
+    upload(A->ctx->s, A->val, values, sizeof(double) * nnz);
   }
   *out = A;
   MFH_CATCH
@@ -2487,7 +2512,7 @@ extern "C" int mfh_dense_create(mfh_ctx *ctx, int64_t n, const double *values, m
   A->nr = n;
   A->nc = n;
   CK(cudaMalloc(&A->val, sizeof(double) * std::max<int64_t>(1, n * n)));
-  if (n) CK(cudaMemcpy(A->val, values, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+  upload(A->ctx->s, A->val, values, sizeof(double) * n * n);
   *out = A;
   MFH_CATCH
 }

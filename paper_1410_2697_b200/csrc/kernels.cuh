@@ -662,6 +662,218 @@ __global__ void __launch_bounds__(512) k_plu_cluster(const PluJob *__restrict__ 
   cl.sync();  // no CTA leaves while another may still read its slots
 }
 
+// cluster variant with the core distributed over the CTAs' shared memory:
+// original row i lives in CTA (i % csize) at local row (i / csize); the pivot
+// row is read through DSMEM from its owner; one cluster barrier per step
+__host__ __device__ inline size_t plu_dsm_bytes(int m, int n, int cs, int crank_max_rows) {
+  (void)m;
+  size_t nl = (size_t)crank_max_rows;
+  size_t b = sizeof(double) * (nl * (size_t)n + nl + (size_t)n);      // rows, mult, prow
+  b += sizeof(int) * ((size_t)m + 4 * (size_t)n + 3 * nl);             // rowAt, col books, local row books
+  (void)cs;
+  return (b + 15) & ~size_t(15);
+}
+
+__global__ void __launch_bounds__(512) k_plu_cluster_smem(const PluJob *__restrict__ jobs,
+                                                          const int *__restrict__ ids, double eps) {
+  extern __shared__ __align__(16) char dsm[];
+  __shared__ MaxLoc red[33];
+  __shared__ MaxLoc slot[2];
+  __shared__ PluState st;
+  __shared__ int s_nact;
+  cg::cluster_group cl = cg::this_cluster();
+  const int cr = (int)cl.block_rank(), cs = (int)cl.num_blocks();
+  const PluJob J = jobs[ids[blockIdx.x / cs]];
+  const int m = J.m, n = J.n, ldg = J.ld;
+  const int nl_max = (m + cs - 1) / cs;
+  const int nl = (m - cr + cs - 1) / cs;  // rows owned by this CTA
+  double *rows = (double *)dsm;
+  double *mult = rows + (size_t)nl_max * n;
+  double *prow = mult + nl_max;
+  int *rowAt = (int *)(prow + n);
+  int *colAt = rowAt + m;
+  int *posC = colAt + n;
+  int *actC = posC + n;
+  int *idxC = actC + n;
+  int *posRl = idxC + n;  // position of each owned row
+  int *actRl = posRl + nl_max;  // active owned rows (local indices)
+  int *idxRl = actRl + nl_max;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (long long e = tid; e < (long long)nl * n; e += nt) {
+    int li = (int)(e / n), j = (int)(e % n);
+    rows[e] = J.a[(long long)(li * cs + cr) * ldg + j];
+  }
+  for (int i = tid; i < m; i += nt) rowAt[i] = i;
+  for (int j = tid; j < n; j += nt) {
+    colAt[j] = j;
+    posC[j] = j;
+    actC[j] = j;
+    idxC[j] = j;
+  }
+  for (int li = tid; li < nl; li += nt) {
+    posRl[li] = li * cs + cr;
+    actRl[li] = li;
+    idxRl[li] = li;
+  }
+  if (tid == 0) {
+    st = PluState{};
+    st.ar = m;
+    st.ac = n;
+    s_nact = nl;
+  }
+  __syncthreads();
+  // initial scan of owned rows
+  double bv = -1.0;
+  long long bk = 0x7fffffffffffffffLL;
+  {
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (int li = warp; li < nl; li += nw) {
+      const double *row = rows + (size_t)li * n;
+      long long pr = (long long)(li * cs + cr) * n;
+      for (int j = lane; j < n; j += 32) {
+        double v = fabs(row[j]);
+        if (better(v, pr + j, bv, bk)) {
+          bv = v;
+          bk = pr + j;
+        }
+      }
+    }
+  }
+  const int kmin = min(m, n);
+  for (int k = 0; k < kmin; ++k) {
+    MaxLoc best = block_maxloc(bv, bk, red);
+    if (tid == 0) slot[k & 1] = best;
+    cl.sync();
+    if (tid == 0) {
+      MaxLoc g = {-2.0, 0x7fffffffffffffffLL};
+      for (int c = 0; c < cs; ++c) {
+        MaxLoc o = *cl.map_shared_rank(&slot[k & 1], c);
+        if (better(o.v, o.key, g.v, g.key)) g = o;
+      }
+      double piv = g.v;
+      int pr, pc;
+      if (g.key == 0x7fffffffffffffffLL) {
+        piv = -1.0;
+        pr = k;
+        pc = k;
+      } else {
+        pr = (int)(g.key / n);
+        pc = (int)(g.key % n);
+      }
+      int bi = rowAt[pr], bj = colAt[pc];
+      bool stop = false;
+      if (k == 0) {
+        st.u11 = piv;
+        if (piv == 0.0) {
+          st.rank = 0;
+          st.ratio = 0.0;
+          stop = true;
+        }
+      } else if (piv > st.prev * MFH_PIVOT_GROWTH_BOUND) {
+        st.status = 1;
+        st.errk = k;
+        st.errpiv = piv;
+        st.errprev = st.prev;
+        stop = true;
+      } else {
+        double ratio = piv / st.u11;
+        if (ratio < eps || piv <= MFH_ZERO_PIVOT_RATIO * st.u11) {
+          st.rank = k;
+          st.ratio = ratio;
+          stop = true;
+        }
+      }
+      if (!stop && k == J.kmax) {
+        st.rank = J.kmax;
+        st.ratio = piv / st.u11;
+        stop = true;
+      }
+      st.done = stop ? 1 : 0;
+      if (!stop) {
+        int ak = rowAt[k];
+        rowAt[k] = bi;
+        rowAt[pr] = ak;
+        if (bi % cs == cr) posRl[bi / cs] = k;
+        if (ak % cs == cr) posRl[ak / cs] = pr;
+        int ck = colAt[k];
+        colAt[k] = bj;
+        colAt[pc] = ck;
+        posC[bj] = k;
+        posC[ck] = pc;
+        int sl = idxC[bj], last = actC[st.ac - 1];
+        actC[sl] = last;
+        idxC[last] = sl;
+        st.ac -= 1;
+        if (bi % cs == cr) {
+          int li = bi / cs;
+          int s2 = idxRl[li], l2 = actRl[s_nact - 1];
+          actRl[s2] = l2;
+          idxRl[l2] = s2;
+          s_nact -= 1;
+        }
+        st.ar -= 1;
+        st.bi = bi;
+        st.bj = bj;
+        const double *orow = cl.map_shared_rank(rows, bi % cs) + (size_t)(bi / cs) * n;
+        st.akk = orow[bj];
+        st.prev = fabs(st.akk);
+        st.rank = k + 1;
+      }
+    }
+    __syncthreads();
+    if (st.done) break;
+    const int bi = st.bi, bj = st.bj, ac = st.ac, na = s_nact;
+    const double akk = st.akk;
+    const double *orow = cl.map_shared_rank(rows, bi % cs) + (size_t)(bi / cs) * n;
+    for (int jj = tid; jj < ac; jj += nt) prow[jj] = orow[actC[jj]];
+    for (int q = tid; q < na; q += nt) {
+      int li = actRl[q];
+      double l = rows[(size_t)li * n + bj] / akk;
+      rows[(size_t)li * n + bj] = l;
+      mult[q] = l;
+    }
+    __syncthreads();
+    bv = -1.0;
+    bk = 0x7fffffffffffffffLL;
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (int q = warp; q < na; q += nw) {
+      int li = actRl[q];
+      double l = mult[q];
+      double *row = rows + (size_t)li * n;
+      long long prk = (long long)posRl[li] * n;
+      for (int jj = lane; jj < ac; jj += 32) {
+        int j = actC[jj];
+        double v = __dsub_rn(row[j], __dmul_rn(l, prow[jj]));
+        row[j] = v;
+        double av = fabs(v);
+        long long key = prk + posC[j];
+        if (better(av, key, bv, bk)) {
+          bv = av;
+          bk = key;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (long long e = tid; e < (long long)nl * n; e += nt) {
+    int li = (int)(e / n), j = (int)(e % n);
+    J.a[(long long)(li * cs + cr) * ldg + j] = rows[e];
+  }
+  if (cr == 0) {
+    for (int i = tid; i < m; i += nt) J.rowAt[i] = rowAt[i];
+    for (int j = tid; j < n; j += nt) J.colAt[j] = colAt[j];
+    if (tid == 0) {
+      J.out[0] = st.rank;
+      J.out[1] = st.status;
+      J.out[2] = st.errk;
+      J.outd[0] = st.ratio;
+      J.outd[1] = st.errpiv;
+      J.outd[2] = st.errprev;
+    }
+  }
+  cl.sync();  // DSMEM lifetime: nobody exits while others may read its rows / slots
+}
+
 // compact r x r LU of a factored core: lu[i][j] = a[rowAt[i]][colAt[j]]
 struct LuExtractJob {
   const double *a;

@@ -70,7 +70,8 @@ typedef struct {
 typedef struct {
   double total_ms;
   double sample_ms, pivot_lu_ms, skeleton_ms, hodlr_factor_ms, dense_front_ms, eliminate_ms;
-  double host_ms;
+  double host_ms;        /* host work before the first launch + BDLR selection */
+  double host_preamble_ms, host_select_ms, host_sync_wait_ms, wall_ms;
   int64_t kernel_launches;
   double pivot_lu_visits; /* algorithmic trailing-entry visits */
   double sample_entries;

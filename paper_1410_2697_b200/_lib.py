@@ -45,7 +45,9 @@ class mfh_timing_t(C.Structure):
     _fields_ = [("total_ms", C.c_double), ("sample_ms", C.c_double), ("pivot_lu_ms", C.c_double),
                 ("skeleton_ms", C.c_double), ("hodlr_factor_ms", C.c_double),
                 ("dense_front_ms", C.c_double), ("eliminate_ms", C.c_double),
-                ("host_ms", C.c_double), ("kernel_launches", C.c_int64),
+                ("host_ms", C.c_double), ("host_preamble_ms", C.c_double),
+                ("host_select_ms", C.c_double), ("host_sync_wait_ms", C.c_double), ("wall_ms", C.c_double),
+                ("kernel_launches", C.c_int64),
                 ("pivot_lu_visits", C.c_double), ("sample_entries", C.c_double)]
 
 

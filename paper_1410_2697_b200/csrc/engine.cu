@@ -258,7 +258,7 @@ static void run_trsm(Sink &sk, const std::vector<TrsmJob> &jobs) {
   TrinvJob *dj = sk.push(ti);
   int nb = (int)ti.size();
   sk.launch([=](cudaStream_t st) {
-    k_trinv<<<nb, 64, TRINV_SMEM, st>>>(dj);
+    k_trinv<<<nb, 256, TRINV_SMEM, st>>>(dj);
     check_launch();
   });
   run_gemm(sk, gm);
@@ -462,7 +462,7 @@ static void run_right_upper_solve(Sink &sk, const std::vector<RSolve> &jobs) {
       TrinvJob *dj = sk.push(ti);
       int nb = (int)ti.size();
       sk.launch([=](cudaStream_t st) {
-        k_trinv<<<nb, 64, TRINV_SMEM, st>>>(dj);
+        k_trinv<<<nb, 256, TRINV_SMEM, st>>>(dj);
         check_launch();
       });
     }
@@ -598,8 +598,8 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     size_t stat = 0;
-    const void *fns[4] = {(const void *)k_plu_cta<true>, (const void *)k_plu_cta<false>,
-                          (const void *)k_plu_cluster, (const void *)k_plu_cluster_smem};
+    const void *fns[5] = {(const void *)k_plu_cta<true>, (const void *)k_plu_cta<false>,
+                          (const void *)k_plu_cluster, (const void *)k_plu_cluster_smem, (const void *)k_plu_grid};
     for (const void *fn : fns) {
       cudaFuncAttributes fa;
       CK(cudaFuncGetAttributes(&fa, fn));
@@ -617,7 +617,9 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
     attr_done = true;
   }
   const int CS = ctx->cluster_size;
-  std::vector<int> small[3], mid, cl8, cl16, clg;
+  std::vector<int> small[3], mid, cl8, cl16, clg, grd;
+  int nsm = 148;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
   size_t smax[3] = {48 * 1024, 100 * 1024, dyn_max};
   for (int q = 0; q < (int)jobs.size(); ++q) {
     const PluJob &j = jobs[q];
@@ -632,6 +634,8 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
       cl8.push_back(q);
     } else if (plu_dsm_bytes(j.m, j.n, CS, (j.m + CS - 1) / CS) <= dyn_max) {
       cl16.push_back(q);
+    } else if (plu_grid_bytes(j.m, j.n, nsm) <= dyn_max) {
+      grd.push_back(q);
     } else if (plu_smem_bytes(j.m, j.n, false) <= dyn_max) {
       clg.push_back(q);
     } else {
@@ -639,7 +643,7 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
     }
   }
   PluJob *dj = sk.push(jobs);
-  bool side = !cl8.empty() || !cl16.empty() || !clg.empty();
+  bool side = !cl8.empty() || !cl16.empty() || !clg.empty() || !grd.empty();
   if (side) {
     CK(cudaEventRecord(ctx->ev_fork, ctx->s));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
@@ -658,6 +662,28 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
   cluster_group(clg, CS, false);
   cluster_group(cl16, CS, true);
   cluster_group(cl8, 8, true);
+  if (!grd.empty()) {
+    // whole-GPU cooperative kernel, cores one after another
+    int *dids = sk.push(grd);
+    size_t sm = 0;
+    int nmax = 1;
+    for (int q : grd) {
+      sm = std::max(sm, plu_grid_bytes(jobs[q].m, jobs[q].n, nsm));
+      nmax = std::max(nmax, jobs[q].n);
+    }
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_plu_grid, 512, sm));
+    if (per_sm < 1) throw runtime_error("cooperative pivot-LU kernel does not fit on an SM");
+    GridScratch gs;
+    gs.nmax = nmax;
+    gs.best = (MaxLoc *)ctx->scratch.alloc(sizeof(MaxLoc) * 2 * nsm);
+    gs.cand = ctx->scratch.d((size_t)2 * nsm * nmax);
+    int nc = (int)grd.size();
+    double e = eps;
+    void *args[5] = {(void *)&dj, (void *)&dids, (void *)&nc, (void *)&e, (void *)&gs};
+    CK(cudaLaunchCooperativeKernel((const void *)k_plu_grid, dim3(nsm), dim3(512), args, sm, ctx->side));
+    ctx->launches++;
+  }
   if (side) CK(cudaEventRecord(ctx->ev_join, ctx->side));
   for (int b = 0; b < 3; ++b) {
     if (small[b].empty()) continue;
@@ -1324,8 +1350,11 @@ struct Factorizer {
       plu.push_back(j);
       F->timing.pivot_lu_visits += 0;  // filled after ranks are known
     }
-    F->timing.host_ms +=
-        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_sel0).count();
+    {
+      double dt = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_sel0).count();
+      F->timing.host_ms += dt;
+      F->timing.host_select_ms += dt;
+    }
 
     cudaEventRecord(ev[0], ctx->s);
     run_sample(s, reqs, dF, dC);
@@ -1871,6 +1900,7 @@ struct Factorizer {
     double tsum[7] = {0, 0, 0, 0, 0, 0, 0};
     auto host_done = std::chrono::steady_clock::now();
     F->timing.host_ms += std::chrono::duration<double, std::milli>(host_done - t0).count();
+    F->timing.host_preamble_ms = std::chrono::duration<double, std::milli>(host_done - t0).count();
     cudaEvent_t e_begin, e_end;
     CK(cudaEventCreate(&e_begin));
     CK(cudaEventCreate(&e_end));
@@ -1880,7 +1910,10 @@ struct Factorizer {
       for (auto &e : ev) CK(cudaEventRecord(e, ctx->s));
       process_height(byh[h], ev);
       Sink s{ctx};
+      auto tw = std::chrono::steady_clock::now();
       s.sync_reset();
+      F->timing.host_sync_wait_ms +=
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw).count();
       float ms;
       CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
       tsum[0] += ms;
@@ -1948,6 +1981,7 @@ struct Factorizer {
     F->stats.stored_reals = retained;
     F->stats.device_bytes_peak = (int64_t)F->arena.capacity() + (int64_t)ctx->scratch.capacity();
     F->timing.total_ms = tot;
+    F->timing.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
 };
 

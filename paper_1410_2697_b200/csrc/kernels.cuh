@@ -874,6 +874,247 @@ __global__ void __launch_bounds__(512) k_plu_cluster_smem(const PluJob *__restri
   cl.sync();  // DSMEM lifetime: nobody exits while others may read its rows / slots
 }
 
+// whole-GPU cooperative variant for the largest cores: CTA g of G owns rows
+// i % G == g in shared memory; every step each CTA publishes its best
+// candidate (value, key) AND that candidate's row to global memory, one grid
+// barrier, then all CTAs reduce the G candidates identically and read the
+// winner's published row as the pivot row. Cores are processed one after
+// another with the whole GPU.
+struct GridScratch {
+  MaxLoc *best;   // 2 x G
+  double *cand;   // 2 x G x nmax
+  int nmax;
+};
+
+__global__ void __launch_bounds__(512) k_plu_grid(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
+                                                  int ncores, double eps, GridScratch gs) {
+  extern __shared__ __align__(16) char dsm[];
+  __shared__ MaxLoc red[33];
+  __shared__ PluState st;
+  __shared__ int s_nact, s_win;
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  for (int c = 0; c < ncores; ++c) {
+    const PluJob J = jobs[ids[c]];
+    const int m = J.m, n = J.n, ldg = J.ld;
+    const int nl_max = (m + G - 1) / G;
+    const int nl = (m - g + G - 1) / G;
+    double *rows = (double *)dsm;
+    double *mult = rows + (size_t)nl_max * n;
+    double *prow = mult + nl_max;
+    int *rowAt = (int *)(prow + n);
+    int *colAt = rowAt + m;
+    int *posC = colAt + n;
+    int *actC = posC + n;
+    int *idxC = actC + n;
+    int *posRl = idxC + n;
+    int *actRl = posRl + nl_max;
+    int *idxRl = actRl + nl_max;
+    int *candRow = idxRl + nl_max;  // local row index of this CTA's candidate
+    for (long long e = tid; e < (long long)nl * n; e += nt) {
+      int li = (int)(e / n), j = (int)(e % n);
+      rows[e] = J.a[(long long)(li * G + g) * ldg + j];
+    }
+    for (int i = tid; i < m; i += nt) rowAt[i] = i;
+    for (int j = tid; j < n; j += nt) {
+      colAt[j] = j;
+      posC[j] = j;
+      actC[j] = j;
+      idxC[j] = j;
+    }
+    for (int li = tid; li < nl; li += nt) {
+      posRl[li] = li * G + g;
+      actRl[li] = li;
+      idxRl[li] = li;
+    }
+    if (tid == 0) {
+      st = PluState{};
+      st.ar = m;
+      st.ac = n;
+      s_nact = nl;
+    }
+    __syncthreads();
+    double bv = -1.0;
+    long long bk = 0x7fffffffffffffffLL;
+    {
+      const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+      for (int li = warp; li < nl; li += nw) {
+        const double *row = rows + (size_t)li * n;
+        long long pr = (long long)(li * G + g) * n;
+        for (int j = lane; j < n; j += 32) {
+          double v = fabs(row[j]);
+          if (better(v, pr + j, bv, bk)) {
+            bv = v;
+            bk = pr + j;
+          }
+        }
+      }
+    }
+    const int kmin = min(m, n);
+    for (int k = 0; k < kmin; ++k) {
+      const int par = k & 1;
+      MaxLoc best = block_maxloc(bv, bk, red);
+      // publish the candidate and its row (row = key / n position -> original via rowAt)
+      if (tid == 0) {
+        gs.best[par * G + g] = best;
+        int li = -1;
+        if (best.key != 0x7fffffffffffffffLL) li = rowAt[(int)(best.key / n)] / G;
+        *candRow = li;
+      }
+      __syncthreads();
+      if (*candRow >= 0) {
+        const double *src = rows + (size_t)(*candRow) * n;
+        double *dst = gs.cand + ((size_t)par * G + g) * gs.nmax;
+        for (int j = tid; j < n; j += nt) dst[j] = src[j];
+      }
+      grid.sync();
+      // identical reduction in every CTA
+      {
+        double v = -2.0;
+        long long key = 0x7fffffffffffffffLL;
+        int who = -1;
+        for (int q = tid; q < G; q += nt) {
+          MaxLoc o = gs.best[par * G + q];
+          if (better(o.v, o.key, v, key)) {
+            v = o.v;
+            key = o.key;
+            who = q;
+          }
+        }
+        // carry the owner in the key's tie-free payload: keys are unique, so find it after the reduction
+        MaxLoc gbest = block_maxloc(v, key, red);
+        if (who >= 0 && key == gbest.key && v == gbest.v) s_win = who;
+        __syncthreads();
+        if (tid == 0) {
+          double piv = gbest.v;
+          int pr, pc;
+          if (gbest.key == 0x7fffffffffffffffLL) {
+            piv = -1.0;
+            pr = k;
+            pc = k;
+          } else {
+            pr = (int)(gbest.key / n);
+            pc = (int)(gbest.key % n);
+          }
+          int bi = rowAt[pr], bj = colAt[pc];
+          bool stop = false;
+          if (k == 0) {
+            st.u11 = piv;
+            if (piv == 0.0) {
+              st.rank = 0;
+              st.ratio = 0.0;
+              stop = true;
+            }
+          } else if (piv > st.prev * MFH_PIVOT_GROWTH_BOUND) {
+            st.status = 1;
+            st.errk = k;
+            st.errpiv = piv;
+            st.errprev = st.prev;
+            stop = true;
+          } else {
+            double ratio = piv / st.u11;
+            if (ratio < eps || piv <= MFH_ZERO_PIVOT_RATIO * st.u11) {
+              st.rank = k;
+              st.ratio = ratio;
+              stop = true;
+            }
+          }
+          if (!stop && k == J.kmax) {
+            st.rank = J.kmax;
+            st.ratio = piv / st.u11;
+            stop = true;
+          }
+          st.done = stop ? 1 : 0;
+          if (!stop) {
+            int ak = rowAt[k];
+            rowAt[k] = bi;
+            rowAt[pr] = ak;
+            if (bi % G == g) posRl[bi / G] = k;
+            if (ak % G == g) posRl[ak / G] = pr;
+            int ck = colAt[k];
+            colAt[k] = bj;
+            colAt[pc] = ck;
+            posC[bj] = k;
+            posC[ck] = pc;
+            int sl = idxC[bj], last = actC[st.ac - 1];
+            actC[sl] = last;
+            idxC[last] = sl;
+            st.ac -= 1;
+            if (bi % G == g) {
+              int li = bi / G;
+              int s2 = idxRl[li], l2 = actRl[s_nact - 1];
+              actRl[s2] = l2;
+              idxRl[l2] = s2;
+              s_nact -= 1;
+            }
+            st.ar -= 1;
+            st.bi = bi;
+            st.bj = bj;
+            st.rank = k + 1;
+          }
+        }
+        __syncthreads();
+      }
+      if (st.done) break;
+      const int bj = st.bj, ac = st.ac, na = s_nact;
+      const double *wrow = gs.cand + ((size_t)par * G + s_win) * gs.nmax;
+      const double akk = wrow[bj];
+      if (tid == 0) st.prev = fabs(akk);
+      for (int jj = tid; jj < ac; jj += nt) prow[jj] = wrow[actC[jj]];
+      for (int q = tid; q < na; q += nt) {
+        int li = actRl[q];
+        double l = rows[(size_t)li * n + bj] / akk;
+        rows[(size_t)li * n + bj] = l;
+        mult[q] = l;
+      }
+      __syncthreads();
+      bv = -1.0;
+      bk = 0x7fffffffffffffffLL;
+      const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+      for (int q = warp; q < na; q += nw) {
+        int li = actRl[q];
+        double l = mult[q];
+        double *row = rows + (size_t)li * n;
+        long long prk = (long long)posRl[li] * n;
+        for (int jj = lane; jj < ac; jj += 32) {
+          int j = actC[jj];
+          double v = __dsub_rn(row[j], __dmul_rn(l, prow[jj]));
+          row[j] = v;
+          double av = fabs(v);
+          long long key = prk + posC[j];
+          if (better(av, key, bv, bk)) {
+            bv = av;
+            bk = key;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    for (long long e = tid; e < (long long)nl * n; e += nt) {
+      int li = (int)(e / n), j = (int)(e % n);
+      J.a[(long long)(li * G + g) * ldg + j] = rows[e];
+    }
+    if (g == 0) {
+      for (int i = tid; i < m; i += nt) J.rowAt[i] = rowAt[i];
+      for (int j = tid; j < n; j += nt) J.colAt[j] = colAt[j];
+      if (tid == 0) {
+        J.out[0] = st.rank;
+        J.out[1] = st.status;
+        J.out[2] = st.errk;
+        J.outd[0] = st.ratio;
+        J.outd[1] = st.errpiv;
+        J.outd[2] = st.errprev;
+      }
+    }
+    grid.sync();  // shared scratch / candidate buffers are reused by the next core
+  }
+}
+
+__host__ __device__ inline size_t plu_grid_bytes(int m, int n, int G) {
+  int nl = (m + G - 1) / G;
+  return plu_dsm_bytes(m, n, G, nl) + 16;
+}
+
 // compact r x r LU of a factored core: lu[i][j] = a[rowAt[i]][colAt[j]]
 struct LuExtractJob {
   const double *a;
@@ -1126,51 +1367,66 @@ struct InvJob {  // in-place inverse of an n x n block (n <= INV_SMALL)
 // idamax rule), whole-row swaps, undone as column swaps at the end
 __global__ void __launch_bounds__(512) k_inv_small(const InvJob *__restrict__ jobs) {
   extern __shared__ double sA[];
-  __shared__ MaxLoc red[33];
   __shared__ int piv[INV_SMALL];
   __shared__ double colk[INV_SMALL];
-  __shared__ int bad;
+  __shared__ int s_p, bad;
+  __shared__ double s_pv;
   const InvJob J = jobs[blockIdx.x];
   const int n = J.n, tid = threadIdx.x, nt = blockDim.x;
   for (int e = tid; e < n * n; e += nt) sA[e] = J.a[(long long)(e / n) * J.lda + (e % n)];
   if (tid == 0) bad = 0;
   __syncthreads();
   for (int k = 0; k < n; ++k) {
-    double bv = -1.0;
-    long long bk = 0x7fffffffffffffffLL;
-    for (int i = k + tid; i < n; i += nt) {
-      double v = fabs(sA[i * n + k]);
-      if (better(v, i, bv, bk)) {
-        bv = v;
-        bk = i;
+    // (1) pivot search by warp 0: first max |a[i][k]|, i >= k
+    if (tid < 32) {
+      double bv = -1.0;
+      long long bk = 0x7fffffffffffffffLL;
+      for (int i = k + tid; i < n; i += 32) {
+        double v = fabs(sA[i * n + k]);
+        if (better(v, i, bv, bk)) {
+          bv = v;
+          bk = i;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_down_sync(0xffffffffu, bv, o);
+        long long ok = __shfl_down_sync(0xffffffffu, bk, o);
+        if (better(ov, ok, bv, bk)) {
+          bv = ov;
+          bk = ok;
+        }
+      }
+      if (tid == 0) {
+        int p = bk == 0x7fffffffffffffffLL ? k : (int)bk;
+        s_p = p;
+        piv[k] = p;
+        s_pv = sA[p * n + k];
       }
     }
-    MaxLoc best = block_maxloc(bv, bk, red);
-    const int p = (best.key == 0x7fffffffffffffffLL) ? k : (int)best.key;
-    if (tid == 0) piv[k] = p;
-    if (p != k)
-      for (int j = tid; j < n; j += nt) {
-        double t = sA[k * n + j];
-        sA[k * n + j] = sA[p * n + j];
-        sA[p * n + j] = t;
-      }
     __syncthreads();
-    const double pv = sA[k * n + k];
+    const int p = s_p;
+    const double pv = s_pv;
     if (pv == 0.0 || !isfinite(pv)) {
       if (tid == 0) bad = 1;
       break;
     }
     const double rinv = 1.0 / pv;
-    for (int i = tid; i < n; i += nt) colk[i] = sA[i * n + k];
+    // (2) swap rows k <-> p, scale the new row k, save column k of the other rows
+    for (int t = tid; t < n; t += nt) {
+      double ok_ = sA[k * n + t], op_ = sA[p * n + t];
+      sA[k * n + t] = (t == k ? 1.0 : op_) * rinv;
+      if (p != k) {
+        sA[p * n + t] = ok_;
+        if (t == k) colk[p] = ok_;
+      }
+      if (t != k && t != p) colk[t] = sA[t * n + k];
+    }
     __syncthreads();
-    for (int j = tid; j < n; j += nt) sA[k * n + j] = (j == k ? 1.0 : sA[k * n + j]) * rinv;
-    __syncthreads();
+    // (3) eliminate column k from every other row
     for (int e = tid; e < n * n; e += nt) {
-      int i = e / n, j = e % n;
+      int i = e / n, j = e - (e / n) * n;
       if (i == k) continue;
-      double f = colk[i];
-      double akj = sA[k * n + j];
-      sA[e] = (j == k ? 0.0 : sA[e]) - f * akj;
+      sA[e] = (j == k ? 0.0 : sA[e]) - colk[i] * sA[k * n + j];
     }
     __syncthreads();
   }
@@ -1198,46 +1454,40 @@ struct TrinvJob {
   double *out;
 };
 constexpr size_t TRINV_SMEM = sizeof(double) * (64 * 64 + 64 * 65);
-__global__ void __launch_bounds__(64) k_trinv(const TrinvJob *__restrict__ jobs) {
+// 256 threads: column j = tid / 4, slice s = tid % 4 (the 4 slices of a column
+// sit in one warp); row-by-row substitution, each dot product split 4 ways
+__global__ void __launch_bounds__(256) k_trinv(const TrinvJob *__restrict__ jobs) {
   extern __shared__ double tdyn[];
   double *Ts = tdyn;
   double *X = tdyn + 64 * 64;
   const TrinvJob J = jobs[blockIdx.x];
-  const int w = J.w, j = threadIdx.x;
-  for (int e = threadIdx.x; e < w * w; e += blockDim.x) Ts[e] = J.T[(long long)(e / w) * J.ldt + (e % w)];
+  const int w = J.w, tid = threadIdx.x;
+  const int j = tid >> 2, sl = tid & 3;
+  for (int e = tid; e < w * w; e += blockDim.x) Ts[e] = J.T[(long long)(e / w) * J.ldt + (e % w)];
   __syncthreads();
-  if (j < w) {
-    if (!J.upper) {
-      for (int i = 0; i < w; ++i) {
-        double v;
-        if (i < j)
-          v = 0.0;
-        else if (i == j)
-          v = 1.0;
-        else {
-          v = 0.0;
-          for (int k = j; k < i; ++k) v = fma(-Ts[i * w + k], X[k * 65 + j], v);
-        }
-        X[i * 65 + j] = v;
-      }
-    } else {
-      for (int i = w - 1; i >= 0; --i) {
-        double v;
-        if (i > j)
-          v = 0.0;
-        else if (i == j)
-          v = 1.0 / Ts[j * w + j];
-        else {
-          double sacc = 0.0;
-          for (int k = i + 1; k <= j; ++k) sacc = fma(Ts[i * w + k], X[k * 65 + j], sacc);
-          v = -sacc / Ts[i * w + i];
-        }
-        X[i * 65 + j] = v;
-      }
+  if (!J.upper) {
+    for (int i = 0; i < w; ++i) {
+      double acc = 0.0;
+      if (j < w && i > j)
+        for (int k = j + sl; k < i; k += 4) acc = fma(-Ts[i * w + k], X[k * 65 + j], acc);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (j < w && sl == 0) X[i * 65 + j] = (i < j) ? 0.0 : (i == j ? 1.0 : acc);
+      __syncwarp();
+    }
+  } else {
+    for (int i = w - 1; i >= 0; --i) {
+      double acc = 0.0;
+      if (j < w && i < j)
+        for (int k = i + 1 + sl; k <= j; k += 4) acc = fma(Ts[i * w + k], X[k * 65 + j], acc);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (j < w && sl == 0) X[i * 65 + j] = (i > j) ? 0.0 : (i == j ? 1.0 / Ts[j * w + j] : -acc / Ts[i * w + i]);
+      __syncwarp();
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < w * w; e += blockDim.x) J.out[e] = X[(e / w) * 65 + (e % w)];
+  for (int e = tid; e < w * w; e += blockDim.x) J.out[e] = X[(e / w) * 65 + (e % w)];
 }
 
 // diagonal check after a blocked LU

@@ -43,7 +43,8 @@ def test_fplu_large_random_vs_oracle(oracle):
     rng = np.random.default_rng(7)
     blocks, caps = [], []
     for m, n, r in ((300, 280, 40), (517, 129, 129), (64, 900, 30), (1, 700, 1), (700, 1, 1),
-                    (400, 350, 60), (700, 700, 20), (1200, 300, 35)):  # last three: cluster path
+                    (400, 350, 60), (700, 700, 20), (1200, 300, 35),  # cluster paths
+                    (1300, 1300, 40), (2100, 900, 25)):  # whole-GPU cooperative path
         B = rng.standard_normal((m, r)) @ rng.standard_normal((r, n))
         blocks.append(B)
         caps.append(min(m, n))

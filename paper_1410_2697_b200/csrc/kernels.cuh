@@ -744,12 +744,19 @@ __global__ void __launch_bounds__(512) k_plu_cluster_smem(const PluJob *__restri
     MaxLoc best = block_maxloc(bv, bk, red);
     if (tid == 0) slot[k & 1] = best;
     cl.sync();
-    if (tid == 0) {
+    if (tid < 32) {
+      // one lane per CTA of the cluster reads its slot through DSMEM, then a warp reduction
       MaxLoc g = {-2.0, 0x7fffffffffffffffLL};
-      for (int c = 0; c < cs; ++c) {
-        MaxLoc o = *cl.map_shared_rank(&slot[k & 1], c);
-        if (better(o.v, o.key, g.v, g.key)) g = o;
+      if (tid < cs) g = *cl.map_shared_rank(&slot[k & 1], tid);
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_down_sync(0xffffffffu, g.v, o);
+        long long ok = __shfl_down_sync(0xffffffffu, g.key, o);
+        if (better(ov, ok, g.v, g.key)) {
+          g.v = ov;
+          g.key = ok;
+        }
       }
+      if (tid == 0) {
       double piv = g.v;
       int pr, pc;
       if (g.key == 0x7fffffffffffffffLL) {
@@ -818,6 +825,7 @@ __global__ void __launch_bounds__(512) k_plu_cluster_smem(const PluJob *__restri
         st.akk = orow[bj];
         st.prev = fabs(st.akk);
         st.rank = k + 1;
+      }
       }
     }
     __syncthreads();
@@ -969,11 +977,11 @@ __global__ void __launch_bounds__(512) k_plu_grid(const PluJob *__restrict__ job
       }
       grid.sync();
       // identical reduction in every CTA
-      {
+      if (tid < 32) {
         double v = -2.0;
         long long key = 0x7fffffffffffffffLL;
         int who = -1;
-        for (int q = tid; q < G; q += nt) {
+        for (int q = tid; q < G; q += 32) {
           MaxLoc o = gs.best[par * G + q];
           if (better(o.v, o.key, v, key)) {
             v = o.v;
@@ -981,10 +989,18 @@ __global__ void __launch_bounds__(512) k_plu_grid(const PluJob *__restrict__ job
             who = q;
           }
         }
-        // carry the owner in the key's tie-free payload: keys are unique, so find it after the reduction
-        MaxLoc gbest = block_maxloc(v, key, red);
-        if (who >= 0 && key == gbest.key && v == gbest.v) s_win = who;
-        __syncthreads();
+        for (int o = 16; o > 0; o >>= 1) {
+          double ov = __shfl_down_sync(0xffffffffu, v, o);
+          long long ok = __shfl_down_sync(0xffffffffu, key, o);
+          int ow = __shfl_down_sync(0xffffffffu, who, o);
+          if (better(ov, ok, v, key)) {
+            v = ov;
+            key = ok;
+            who = ow;
+          }
+        }
+        MaxLoc gbest = {v, key};
+        if (tid == 0) s_win = who;
         if (tid == 0) {
           double piv = gbest.v;
           int pr, pc;
@@ -1053,8 +1069,8 @@ __global__ void __launch_bounds__(512) k_plu_grid(const PluJob *__restrict__ job
             st.rank = k + 1;
           }
         }
-        __syncthreads();
       }
+      __syncthreads();
       if (st.done) break;
       const int bj = st.bj, ac = st.ac, na = s_nact;
       const double *wrow = gs.cand + ((size_t)par * G + s_win) * gs.nmax;

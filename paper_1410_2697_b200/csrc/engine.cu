@@ -40,11 +40,38 @@ static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // ---------------------------------------------------------------------------
 // device memory: chunked bump arena
 // ---------------------------------------------------------------------------
+// device chunks are recycled through a per-context pool: factorizations of
+// the same pattern reuse the previous one's memory instead of cudaMalloc/Free
+// inside the timed step
+struct ChunkPool {
+  std::vector<std::pair<char *, size_t>> free_chunks;
+  std::pair<char *, size_t> take(size_t need) {
+    int best = -1;
+    for (int q = 0; q < (int)free_chunks.size(); ++q)
+      if (free_chunks[q].second >= need && (best < 0 || free_chunks[q].second < free_chunks[best].second))
+        best = q;
+    if (best >= 0) {
+      auto c = free_chunks[best];
+      free_chunks.erase(free_chunks.begin() + best);
+      return c;
+    }
+    char *p = nullptr;
+    CK(cudaMalloc(&p, need));
+    return {p, need};
+  }
+  void give(std::pair<char *, size_t> c) { free_chunks.push_back(c); }
+  void release() {
+    for (auto &c : free_chunks) cudaFree(c.first);
+    free_chunks.clear();
+  }
+};
+
 struct Arena {
   std::vector<std::pair<char *, size_t>> chunks;
   size_t cur = 0, off = 0;
   size_t chunk = size_t(256) << 20;
   size_t in_use = 0, peak = 0;
+  ChunkPool *pool = nullptr;
   void *alloc(size_t bytes) {
     bytes = (bytes + 255) & ~size_t(255);
     if (bytes == 0) bytes = 256;
@@ -62,10 +89,13 @@ struct Arena {
         continue;
       }
       size_t sz = std::max(chunk, bytes);
-      char *p = nullptr;
-      CK(cudaMalloc(&p, sz));
-      chunks.push_back({p, sz});
-      // cur now indexes the new chunk
+      if (pool) {
+        chunks.push_back(pool->take(sz));
+      } else {
+        char *p = nullptr;
+        CK(cudaMalloc(&p, sz));
+        chunks.push_back({p, sz});
+      }
     }
   }
   double *d(size_t n) { return (double *)alloc(n * sizeof(double)); }
@@ -76,7 +106,12 @@ struct Arena {
     in_use = 0;
   }
   void release() {
-    for (auto &c : chunks) cudaFree(c.first);
+    for (auto &c : chunks) {
+      if (pool)
+        pool->give(c);
+      else
+        cudaFree(c.first);
+    }
     chunks.clear();
     reset();
   }
@@ -147,6 +182,7 @@ struct Ctx {
   cudaStream_t side = nullptr;  // concurrent large-core cluster kernels
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int cluster_size = 16;
+  ChunkPool pool;
   Stage stage;
   Arena scratch;
   double *d_part = nullptr;  // reduction partials
@@ -594,12 +630,13 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
   Ctx *ctx = sk.ctx;
   static bool attr_done = false;
   static size_t dyn_max = 0;
+  static const void *fns[6] = {(const void *)k_plu_cta2<true>,      (const void *)k_plu_cta2<false>,
+                               (const void *)k_plu_cluster2<true>,  (const void *)k_plu_cluster2<false>,
+                               (const void *)k_plu_grid2<true>,     (const void *)k_plu_grid2<false>};
   if (!attr_done) {
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     size_t stat = 0;
-    const void *fns[5] = {(const void *)k_plu_cta<true>, (const void *)k_plu_cta<false>,
-                          (const void *)k_plu_cluster, (const void *)k_plu_cluster_smem, (const void *)k_plu_grid};
     for (const void *fn : fns) {
       cudaFuncAttributes fa;
       CK(cudaFuncGetAttributes(&fa, fn));
@@ -617,86 +654,84 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
     attr_done = true;
   }
   const int CS = ctx->cluster_size;
-  std::vector<int> small[3], mid, cl8, cl16, clg, grd;
   int nsm = 148;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
+  auto cta_bytes = [](int m, int n) { return sizeof(double) * (size_t)m * n + sizeof(int) * (size_t)(m + n) + 16; };
+  std::vector<int> small[3], cl8, cl16, grd_s, grd_g;
   size_t smax[3] = {48 * 1024, 100 * 1024, dyn_max};
   for (int q = 0; q < (int)jobs.size(); ++q) {
     const PluJob &j = jobs[q];
     long long ent = (long long)j.m * j.n;
-    size_t with_core = plu_smem_bytes(j.m, j.n, true);
-    if (ent <= PLU_CTA_MAX && with_core <= dyn_max) {
-      int b = with_core <= smax[0] ? 0 : (with_core <= smax[1] ? 1 : 2);
-      small[b].push_back(q);
-      continue;
-    }
-    if (ent < 64 * 1024 && plu_dsm_bytes(j.m, j.n, 8, (j.m + 7) / 8) <= dyn_max) {
+    size_t wc = cta_bytes(j.m, j.n);
+    if (ent <= PLU_CTA_MAX && wc <= dyn_max) {
+      small[wc <= smax[0] ? 0 : (wc <= smax[1] ? 1 : 2)].push_back(q);
+    } else if (ent < 64 * 1024 && plu_dist_bytes(j.m, j.n, 8, true) <= dyn_max) {
       cl8.push_back(q);
-    } else if (plu_dsm_bytes(j.m, j.n, CS, (j.m + CS - 1) / CS) <= dyn_max) {
+    } else if (plu_dist_bytes(j.m, j.n, CS, true) <= dyn_max) {
       cl16.push_back(q);
-    } else if (plu_grid_bytes(j.m, j.n, nsm) <= dyn_max) {
-      grd.push_back(q);
-    } else if (plu_smem_bytes(j.m, j.n, false) <= dyn_max) {
-      clg.push_back(q);
+    } else if (plu_dist_bytes(j.m, j.n, nsm, true) <= dyn_max) {
+      grd_s.push_back(q);
+    } else if (plu_dist_bytes(j.m, j.n, nsm, false) <= dyn_max) {
+      grd_g.push_back(q);
     } else {
       throw runtime_error("complete-pivot core too large for the shared-memory bookkeeping");
     }
   }
   PluJob *dj = sk.push(jobs);
-  bool side = !cl8.empty() || !cl16.empty() || !clg.empty() || !grd.empty();
+  // every descriptor the side stream reads is pushed (on the main stream)
+  // BEFORE the fork event, so the side-stream kernels see them
+  int *ids_cl16 = sk.push(cl16), *ids_cl8 = sk.push(cl8), *ids_gs = sk.push(grd_s), *ids_gg = sk.push(grd_g);
+  GridScratch gs{};
+  if (!grd_s.empty() || !grd_g.empty()) {
+    int nmax = 1;
+    for (int q : grd_s) nmax = std::max(nmax, jobs[q].n);
+    for (int q : grd_g) nmax = std::max(nmax, jobs[q].n);
+    gs.nmax = nmax;
+    gs.best = (MaxLoc *)ctx->scratch.alloc(sizeof(MaxLoc) * 2 * nsm);
+    gs.cand = ctx->scratch.d((size_t)2 * nsm * nmax);
+  }
+  bool side = !cl8.empty() || !cl16.empty() || !grd_s.empty() || !grd_g.empty();
   if (side) {
     CK(cudaEventRecord(ctx->ev_fork, ctx->s));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
   }
-  auto cluster_group = [&](const std::vector<int> &g, int cs, bool resident) {
+  auto cluster_group = [&](const std::vector<int> &g, int *dids, int cs) {
     if (g.empty()) return;
-    int *dids = sk.push(g);
     size_t sm = 0;
-    for (int q : g)
-      sm = std::max(sm, resident ? plu_dsm_bytes(jobs[q].m, jobs[q].n, cs, (jobs[q].m + cs - 1) / cs)
-                                 : plu_smem_bytes(jobs[q].m, jobs[q].n, false));
-    launch_cluster(resident ? (const void *)k_plu_cluster_smem : (const void *)k_plu_cluster, (int)g.size(), cs,
-                   sm, ctx->side, dj, dids, eps);
+    for (int q : g) sm = std::max(sm, plu_dist_bytes(jobs[q].m, jobs[q].n, cs, true));
+    launch_cluster(fns[2], (int)g.size(), cs, sm, ctx->side, dj, dids, eps);
     ctx->launches++;
   };
-  cluster_group(clg, CS, false);
-  cluster_group(cl16, CS, true);
-  cluster_group(cl8, 8, true);
-  if (!grd.empty()) {
-    // whole-GPU cooperative kernel, cores one after another
-    int *dids = sk.push(grd);
+  cluster_group(cl16, ids_cl16, CS);
+  cluster_group(cl8, ids_cl8, 8);
+  auto grid_group = [&](const std::vector<int> &g, int *dids, bool rs) {
+    if (g.empty()) return;
     size_t sm = 0;
-    int nmax = 1;
-    for (int q : grd) {
-      sm = std::max(sm, plu_grid_bytes(jobs[q].m, jobs[q].n, nsm));
-      nmax = std::max(nmax, jobs[q].n);
-    }
+    for (int q : g) sm = std::max(sm, plu_dist_bytes(jobs[q].m, jobs[q].n, nsm, rs));
+    const void *fn = rs ? fns[4] : fns[5];
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_plu_grid, 512, sm));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, sm));
     if (per_sm < 1) throw runtime_error("cooperative pivot-LU kernel does not fit on an SM");
-    GridScratch gs;
-    gs.nmax = nmax;
-    gs.best = (MaxLoc *)ctx->scratch.alloc(sizeof(MaxLoc) * 2 * nsm);
-    gs.cand = ctx->scratch.d((size_t)2 * nsm * nmax);
-    int nc = (int)grd.size();
+    int nc = (int)g.size();
     double e = eps;
     void *args[5] = {(void *)&dj, (void *)&dids, (void *)&nc, (void *)&e, (void *)&gs};
-    CK(cudaLaunchCooperativeKernel((const void *)k_plu_grid, dim3(nsm), dim3(512), args, sm, ctx->side));
+    CK(cudaLaunchCooperativeKernel(fn, dim3(nsm), dim3(512), args, sm, ctx->side));
     ctx->launches++;
-  }
+  };
+  grid_group(grd_s, ids_gs, true);
+  grid_group(grd_g, ids_gg, false);
   if (side) CK(cudaEventRecord(ctx->ev_join, ctx->side));
   for (int b = 0; b < 3; ++b) {
     if (small[b].empty()) continue;
     int *dids = sk.push(small[b]);
     size_t sm = 0;
-    for (int q : small[b]) sm = std::max(sm, plu_smem_bytes(jobs[q].m, jobs[q].n, true));
+    for (int q : small[b]) sm = std::max(sm, cta_bytes(jobs[q].m, jobs[q].n));
     int nb = (int)small[b].size();
     sk.launch([=](cudaStream_t st) {
-      k_plu_cta<true><<<nb, b == 0 ? 256 : 512, sm, st>>>(dj, dids, eps);
+      k_plu_cta2<true><<<nb, b == 0 ? 256 : 512, sm, st>>>(dj, dids, eps);
       check_launch();
     });
   }
-  (void)mid;
   if (side) CK(cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0));
 }
 
@@ -727,6 +762,7 @@ struct BlockH {
   double *resd = nullptr;  // device [ratio, errpiv, errprev]
   // results
   int rank = 0, status = 0, errk = 0;
+  bool rows_phys = false;  // pivot-LU kernel left the core's rows physically permuted
   double ratio = 0.0, errpiv = 0.0, errprev = 0.0;
   bool dense = false;
   std::vector<int> rowperm, colperm;  // first `rank` pivots (parity log)
@@ -1287,7 +1323,7 @@ struct Factorizer {
       select(f, b.r0, b.m, b.c0, b.n, b.I, b.J);
       ioff.push_back(itot);
       doff.push_back(dtot);
-      itot += 4 * ((int64_t)b.I.size() + b.J.size()) + 3;
+      itot += 4 * ((int64_t)b.I.size() + b.J.size()) + 4;
       dtot += (int64_t)b.I.size() + b.J.size() + 3;
     }
     int *pint_all = sblocks.empty() ? nullptr : ctx->scratch.i(itot);
@@ -1430,6 +1466,7 @@ struct Factorizer {
         b.errpiv = od[1];
         b.errprev = od[2];
         if (b.status && first_err < 0) first_err = (int)q;
+        b.rows_phys = out[3] == 1;
         b.rowperm.assign(p, p + b.rank);
         b.colperm.assign(p + 4 * nI, p + 4 * nI + b.rank);
         // algorithmic visits: sum_{k < min(rank+1, min(I,J))} (|I|-k)(|J|-k)
@@ -1466,7 +1503,7 @@ struct Factorizer {
       } else if (b.rank > 0) {
         int r = b.rank;
         double *lu = ctx->scratch.d((size_t)r * r);
-        lux.push_back(LuExtractJob{b.core, nJ, r, b.pint, b.pint + 4 * nI, lu});
+        lux.push_back(LuExtractJob{b.core, nJ, r, b.rows_phys ? nullptr : b.pint, nullptr, lu});
         b.row = F->arena.d((size_t)r * b.n);
         b.col = F->arena.d((size_t)b.m * r);
         SkelJob sj{};
@@ -2338,6 +2375,7 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   cudaStreamSynchronize(ctx->c.s);
   ctx->c.stage.release();
   ctx->c.scratch.release();
+  ctx->c.pool.release();
   cudaFree(ctx->c.d_part);
   cudaFree(ctx->c.d_scal);
   cudaStreamSynchronize(ctx->c.side);
@@ -2376,6 +2414,7 @@ extern "C" int mfh_factorize(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const 
   A.val.assign(values, values + A.ptr[n]);
   F = new mfh_factor();
   F->ctx = &ctx->c;
+  F->arena.pool = &ctx->c.pool;
   int64_t launches0 = ctx->c.launches;
   Factorizer fz{};
   fz.F = F;
@@ -2817,7 +2856,7 @@ extern "C" int mfh_full_pivot_lu_batched(mfh_ctx *ctx, int64_t batch, const int6
   for (int64_t b = 0; b < batch; ++b) {
     ioff[b] = itot;
     doff[b] = dtot;
-    itot += 4 * (ms[b] + ns[b]) + 3;
+    itot += 4 * (ms[b] + ns[b]) + 4;
     dtot += ms[b] + ns[b] + 3;
   }
   int *ibuf = c->scratch.i(std::max<int64_t>(1, itot));
@@ -2872,11 +2911,12 @@ extern "C" int mfh_full_pivot_lu_batched(mfh_ctx *ctx, int64_t batch, const int6
     err[3 * b + 2] = od[2];
     for (int i = 0; i < m; ++i) row_perm[ro + i] = rowAt[i];
     for (int j = 0; j < n; ++j) col_perm[co + j] = colAt[j];
-    // reference layout: lu[p][q] = a[rowAt[p]][colAt[q]]
+    // reference layout: lu[p][q] = a[row at position p][q] (columns already physical)
     const double *a = raw.data() + offs[b];
     double *o = blocks + offs[b];
+    const bool phys = out[3] == 1;
     for (int i = 0; i < m; ++i)
-      for (int j = 0; j < n; ++j) o[(int64_t)i * n + j] = a[(int64_t)rowAt[i] * n + colAt[j]];
+      for (int j = 0; j < n; ++j) o[(int64_t)i * n + j] = a[(int64_t)(phys ? i : rowAt[i]) * n + j];
     ro += m;
     co += n;
   }

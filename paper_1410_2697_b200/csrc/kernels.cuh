@@ -1131,6 +1131,480 @@ __host__ __device__ inline size_t plu_grid_bytes(int m, int n, int G) {
   return plu_dsm_bytes(m, n, G, nl) + 16;
 }
 
+// ===========================================================================
+// v2 complete-pivot LU kernels: the reference's physical column swaps are
+// reproduced, so the trailing columns of step k are the contiguous range
+// (k, n) and the tie-break key of a candidate is (row position) * n + column
+// -- no per-entry indirection. Rows are physically swapped in the single-CTA
+// kernel and kept logical (owned rows + position table) in the distributed
+// kernels. One reduction barrier, one decision barrier and one pivot-row
+// barrier per step.
+// ===========================================================================
+__device__ __forceinline__ MaxLoc reduce_to0(double v, long long key, MaxLoc *red) {
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov = __shfl_down_sync(0xffffffffu, v, o);
+    long long ok = __shfl_down_sync(0xffffffffu, key, o);
+    if (better(ov, ok, v, key)) {
+      v = ov;
+      key = ok;
+    }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) red[w] = MaxLoc{v, key};
+  __syncthreads();
+  MaxLoc r{-2.0, 0x7fffffffffffffffLL};
+  if (w == 0) {
+    r = lane < nw ? red[lane] : MaxLoc{-2.0, 0x7fffffffffffffffLL};
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_down_sync(0xffffffffu, r.v, o);
+      long long ok = __shfl_down_sync(0xffffffffu, r.key, o);
+      if (better(ov, ok, r.v, r.key)) {
+        r.v = ov;
+        r.key = ok;
+      }
+    }
+  }
+  return r;  // valid in thread 0
+}
+
+// stop/continue rule of _core.pyx:49-62; returns true when elimination stops
+__device__ __forceinline__ bool plu_stop(PluState &st, int k, int kmax, double eps, double piv) {
+  if (k == 0) {
+    st.u11 = piv;
+    if (piv == 0.0) {
+      st.rank = 0;
+      st.ratio = 0.0;
+      return true;
+    }
+  } else {
+    if (piv > st.prev * MFH_PIVOT_GROWTH_BOUND) {
+      st.status = 1;
+      st.errk = k;
+      st.errpiv = piv;
+      st.errprev = st.prev;
+      return true;
+    }
+    double ratio = piv / st.u11;
+    if (ratio < eps || piv <= MFH_ZERO_PIVOT_RATIO * st.u11) {
+      st.rank = k;
+      st.ratio = ratio;
+      return true;
+    }
+  }
+  if (k == kmax) {
+    st.rank = kmax;
+    st.ratio = piv / st.u11;
+    return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void plu_out(const PluJob &J, const PluState &st) {
+  J.out[0] = st.rank;
+  J.out[1] = st.status;
+  J.out[2] = st.errk;
+  J.outd[0] = st.ratio;
+  J.outd[1] = st.errpiv;
+  J.outd[2] = st.errprev;
+}
+
+template <bool SMEM_CORE>
+__global__ void __launch_bounds__(512) k_plu_cta2(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
+                                                  double eps) {
+  extern __shared__ __align__(16) char dsm[];
+  __shared__ MaxLoc red[32];
+  __shared__ PluState st;
+  const PluJob J = jobs[ids[blockIdx.x]];
+  const int m = J.m, n = J.n, tid = threadIdx.x, nt = blockDim.x;
+  double *a = J.a;
+  int ld = J.ld;
+  char *base = dsm;
+  if (SMEM_CORE) {
+    double *sa = (double *)dsm;
+    for (long long e = tid; e < (long long)m * n; e += nt) sa[e] = J.a[(e / n) * J.ld + (e % n)];
+    a = sa;
+    ld = n;
+    base = dsm + sizeof(double) * (size_t)m * n;
+  }
+  int *rowAt = (int *)base, *colAt = rowAt + m;
+  for (int i = tid; i < m; i += nt) rowAt[i] = i;
+  for (int j = tid; j < n; j += nt) colAt[j] = j;
+  if (tid == 0) {
+    st = PluState{};
+  }
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  double bv = -1.0;
+  long long bk = 0x7fffffffffffffffLL;
+  __syncthreads();
+  for (int i = warp; i < m; i += nw) {
+    const double *row = a + (long long)i * ld;
+    for (int j = lane; j < n; j += 32) {
+      double v = fabs(row[j]);
+      if (better(v, (long long)i * n + j, bv, bk)) {
+        bv = v;
+        bk = (long long)i * n + j;
+      }
+    }
+  }
+  const int kmin = min(m, n);
+  for (int k = 0; k < kmin; ++k) {
+    MaxLoc best = reduce_to0(bv, bk, red);
+    if (tid == 0) {
+      double piv = best.v;
+      int bi = k, bj = k;
+      if (best.key != 0x7fffffffffffffffLL) {
+        bi = (int)(best.key / n);
+        bj = (int)(best.key % n);
+      } else {
+        piv = -1.0;
+      }
+      bool stop = plu_stop(st, k, J.kmax, eps, piv);
+      st.done = stop ? 1 : 0;
+      if (!stop) {
+        st.bi = bi;
+        st.bj = bj;
+        st.akk = a[(long long)bi * ld + bj];
+        st.prev = fabs(st.akk);
+        st.rank = k + 1;
+        int t = rowAt[k];
+        rowAt[k] = rowAt[bi];
+        rowAt[bi] = t;
+        t = colAt[k];
+        colAt[k] = colAt[bj];
+        colAt[bj] = t;
+      }
+    }
+    __syncthreads();
+    if (st.done) break;
+    const int bi = st.bi, bj = st.bj;
+    const double akk = st.akk;
+    // physical swaps: rows k <-> bi and columns k <-> bj in one conflict-free pass
+    if (bi != k)
+      for (int t = tid; t < n; t += nt) {
+        if (t == k || t == bj) continue;
+        double x = a[(long long)k * ld + t];
+        a[(long long)k * ld + t] = a[(long long)bi * ld + t];
+        a[(long long)bi * ld + t] = x;
+      }
+    if (bj != k)
+      for (int t = tid; t < m; t += nt) {
+        if (t == k || t == bi) continue;
+        double x = a[(long long)t * ld + k];
+        a[(long long)t * ld + k] = a[(long long)t * ld + bj];
+        a[(long long)t * ld + bj] = x;
+      }
+    if (tid == 0) {
+      double okk = a[(long long)k * ld + k], okb = a[(long long)k * ld + bj];
+      double oik = a[(long long)bi * ld + k], oib = a[(long long)bi * ld + bj];
+      a[(long long)k * ld + k] = oib;
+      a[(long long)k * ld + bj] = oik;
+      a[(long long)bi * ld + k] = okb;
+      a[(long long)bi * ld + bj] = okk;
+    }
+    __syncthreads();
+    bv = -1.0;
+    bk = 0x7fffffffffffffffLL;
+    const double *prow = a + (long long)k * ld;
+    for (int i = k + 1 + warp; i < m; i += nw) {
+      double *row = a + (long long)i * ld;
+      const double l = row[k] / akk;
+      __syncwarp();
+      if (lane == 0) row[k] = l;
+      const long long rk = (long long)i * n;
+      for (int j = k + 1 + lane; j < n; j += 32) {
+        double v = __dsub_rn(row[j], __dmul_rn(l, prow[j]));
+        row[j] = v;
+        double av = fabs(v);
+        if (better(av, rk + j, bv, bk)) {
+          bv = av;
+          bk = rk + j;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (SMEM_CORE)
+    for (long long e = tid; e < (long long)m * n; e += nt) J.a[(e / n) * J.ld + (e % n)] = a[e];
+  // physically permuted rows: the caller's row_perm is rowAt; report the layout as
+  // "rows already permuted" by storing rowAt and flagging it in out[3]
+  for (int i = tid; i < m; i += nt) J.rowAt[i] = rowAt[i];
+  for (int j = tid; j < n; j += nt) J.colAt[j] = colAt[j];
+  if (tid == 0) {
+    plu_out(J, st);
+    J.out[3] = 1;  // rows physically permuted
+  }
+}
+
+// distributed over CTAs (cluster: DSMEM; grid: global candidates): original
+// row i lives in CTA (i % G) at local row (i / G); columns are physical
+template <bool GRID, bool ROWS_SMEM>
+__device__ __forceinline__ void plu_dist_body(const PluJob &J, double eps, int G, int g, char *dsm, MaxLoc *red,
+                                              PluState &st, int &s_nact, cg::cluster_group *clp,
+                                              MaxLoc *slot, GridScratch *gs, int *s_win) {
+  const int m = J.m, n = J.n, tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  const int nl_max = (m + G - 1) / G;
+  const int nl = (m - g + G - 1) / G;
+  double *rows = (double *)dsm;  // ROWS_SMEM: nl_max x n
+  double *prow = ROWS_SMEM ? rows + (size_t)nl_max * n : rows;
+  int *rowAt = (int *)(prow + n);
+  int *colAt = rowAt + m;
+  int *posRl = colAt + n;
+  int *actRl = posRl + nl_max;
+  int *idxRl = actRl + nl_max;
+  int *defer = idxRl + nl_max;  // deferred column swap of this CTA's last pivot row: (li, k, bj)
+  auto row_ptr = [&](int li) -> double * {
+    return ROWS_SMEM ? rows + (size_t)li * n : J.a + (long long)(li * G + g) * J.ld;
+  };
+  if (ROWS_SMEM)
+    for (long long e = tid; e < (long long)nl * n; e += nt) {
+      int li = (int)(e / n), j = (int)(e % n);
+      rows[e] = J.a[(long long)(li * G + g) * J.ld + j];
+    }
+  for (int i = tid; i < m; i += nt) rowAt[i] = i;
+  for (int j = tid; j < n; j += nt) colAt[j] = j;
+  for (int li = tid; li < nl; li += nt) {
+    posRl[li] = li * G + g;
+    actRl[li] = li;
+    idxRl[li] = li;
+  }
+  if (tid == 0) {
+    st = PluState{};
+    s_nact = nl;
+    defer[0] = -1;
+  }
+  __syncthreads();
+  double bv = -1.0;
+  long long bk = 0x7fffffffffffffffLL;
+  for (int li = warp; li < nl; li += nw) {
+    const double *row = row_ptr(li);
+    const long long pr = (long long)(li * G + g) * n;
+    for (int j = lane; j < n; j += 32) {
+      double v = fabs(row[j]);
+      if (better(v, pr + j, bv, bk)) {
+        bv = v;
+        bk = pr + j;
+      }
+    }
+  }
+  const int kmin = min(m, n);
+  for (int k = 0; k < kmin; ++k) {
+    const int par = k & 1;
+    MaxLoc best = reduce_to0(bv, bk, red);
+    if (GRID) {
+      // publish the candidate and its row (pre-swap values of this step)
+      __shared__ int s_cand;
+      if (tid == 0) {
+        gs->best[par * G + g] = best;
+        s_cand = best.key == 0x7fffffffffffffffLL ? -1 : rowAt[(int)(best.key / n)] / G;
+      }
+      __syncthreads();
+      if (s_cand >= 0) {
+        const double *src = row_ptr(s_cand);
+        double *dst = gs->cand + ((size_t)par * G + g) * gs->nmax;
+        for (int j = tid; j < n; j += nt) dst[j] = src[j];
+      }
+      cg::this_grid().sync();
+    } else {
+      if (tid == 0) slot[par] = best;
+      clp->sync();
+    }
+    if (tid < 32) {
+      MaxLoc gb{-2.0, 0x7fffffffffffffffLL};
+      int who = -1;
+      if (GRID) {
+        for (int q = lane; q < G; q += 32) {
+          MaxLoc o = gs->best[par * G + q];
+          if (better(o.v, o.key, gb.v, gb.key)) {
+            gb = o;
+            who = q;
+          }
+        }
+      } else if (lane < G) {
+        gb = *clp->map_shared_rank(&slot[par], lane);
+        who = lane;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_down_sync(0xffffffffu, gb.v, o);
+        long long ok = __shfl_down_sync(0xffffffffu, gb.key, o);
+        int ow = __shfl_down_sync(0xffffffffu, who, o);
+        if (better(ov, ok, gb.v, gb.key)) {
+          gb.v = ov;
+          gb.key = ok;
+          who = ow;
+        }
+      }
+      if (tid == 0) {
+        // previous deferred pivot-row swap (nobody reads that row any more)
+        if (!GRID && defer[0] >= 0) {
+          double *r = row_ptr(defer[0]);
+          double x = r[defer[1]];
+          r[defer[1]] = r[defer[2]];
+          r[defer[2]] = x;
+          defer[0] = -1;
+        }
+        double piv = gb.v;
+        int pr = k, bj = k;
+        if (gb.key != 0x7fffffffffffffffLL) {
+          pr = (int)(gb.key / n);
+          bj = (int)(gb.key % n);
+        } else {
+          piv = -1.0;
+        }
+        if (pr < 0 || pr >= m || bj < 0 || bj >= n) {  // defensive: corrupt candidate
+          st.status = 2;
+          piv = -1.0;
+          pr = k;
+          bj = k;
+        }
+        bool stop = st.status == 2 || plu_stop(st, k, J.kmax, eps, piv);
+        st.done = stop ? 1 : 0;
+        if (!stop) {
+          const int bi = rowAt[pr], ak = rowAt[k];
+          const int owner = bi % G;
+          rowAt[k] = bi;
+          rowAt[pr] = ak;
+          if (bi % G == g) {
+            int li = bi / G;
+            posRl[li] = k;
+            int s2 = idxRl[li], l2 = actRl[s_nact - 1];
+            actRl[s2] = l2;
+            idxRl[l2] = s2;
+            idxRl[li] = 0x7fffffff;  // inactive
+            s_nact -= 1;
+            if (!GRID) {
+              defer[0] = li;
+              defer[1] = k;
+              defer[2] = bj;
+            }
+          }
+          if (ak % G == g && ak != bi) posRl[ak / G] = pr;
+          int t = colAt[k];
+          colAt[k] = colAt[bj];
+          colAt[bj] = t;
+          const double *orow;
+          if (GRID)
+            orow = gs->cand + ((size_t)par * G + who) * gs->nmax;
+          else
+            orow = ROWS_SMEM ? clp->map_shared_rank(rows, owner) + (size_t)(bi / G) * n : J.a + (long long)bi * J.ld;
+          st.akk = orow[bj];
+          st.prev = fabs(st.akk);
+          st.rank = k + 1;
+          st.bi = bi;
+          st.bj = bj;
+          *s_win = owner;
+          (void)who;
+        }
+      }
+    }
+    __syncthreads();
+    if (st.done) break;
+    const int bi = st.bi, bj = st.bj, na = s_nact;
+    const double akk = st.akk;
+    // pivot row at physical columns after this step's swap: prow[j] = orow[j], prow[bj] = orow[k]
+    {
+      const double *orow;
+      if (GRID) {
+        // the winner CTA published bi's row (keys are unique: winner = owner)
+        orow = gs->cand + ((size_t)par * G + (bi % G)) * gs->nmax;
+      } else {
+        orow = ROWS_SMEM ? clp->map_shared_rank(rows, bi % G) + (size_t)(bi / G) * n : J.a + (long long)bi * J.ld;
+      }
+      for (int j = k + 1 + tid; j < n; j += nt) prow[j] = (j == bj) ? orow[k] : orow[j];
+    }
+    // inactive owned rows (earlier pivots): physical column swap k <-> bj
+    if (bj != k)
+      for (int li = tid; li < nl; li += nt) {
+        if (idxRl[li] != 0x7fffffff) continue;  // still active (handled below)
+        if (!GRID && li * G + g == bi) continue;  // current pivot row: deferred (peers read it)
+        double *r = row_ptr(li);
+        double x = r[k];
+        r[k] = r[bj];
+        r[bj] = x;
+      }
+    __syncthreads();
+    bv = -1.0;
+    bk = 0x7fffffffffffffffLL;
+    for (int q = warp; q < na; q += nw) {
+      const int li = actRl[q];
+      double *row = row_ptr(li);
+      const double ok_ = row[k], ob = row[bj];
+      const double l = ob / akk;
+      __syncwarp();
+      if (lane == 0) row[k] = l;
+      const long long rk = (long long)posRl[li] * n;
+      for (int j = k + 1 + lane; j < n; j += 32) {
+        double cur = (j == bj) ? ok_ : row[j];
+        double v = __dsub_rn(cur, __dmul_rn(l, prow[j]));
+        row[j] = v;
+        double av = fabs(v);
+        if (better(av, rk + j, bv, bk)) {
+          bv = av;
+          bk = rk + j;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && !GRID && defer[0] >= 0) {
+    double *r = row_ptr(defer[0]);
+    double x = r[defer[1]];
+    r[defer[1]] = r[defer[2]];
+    r[defer[2]] = x;
+  }
+  __syncthreads();
+  if (ROWS_SMEM)
+    for (long long e = tid; e < (long long)nl * n; e += nt) {
+      int li = (int)(e / n), j = (int)(e % n);
+      J.a[(long long)(li * G + g) * J.ld + j] = rows[e];
+    }
+  if (g == 0) {
+    for (int i = tid; i < m; i += nt) J.rowAt[i] = rowAt[i];
+    for (int j = tid; j < n; j += nt) J.colAt[j] = colAt[j];
+    if (tid == 0) {
+      plu_out(J, st);
+      J.out[3] = 0;  // rows logical: row p of the factor is original row rowAt[p]
+    }
+  }
+}
+
+__host__ __device__ inline size_t plu_dist_bytes(int m, int n, int G, bool rows_smem) {
+  size_t nl = (size_t)((m + G - 1) / G);
+  size_t b = sizeof(double) * ((rows_smem ? nl * (size_t)n : 0) + (size_t)n);
+  b += sizeof(int) * ((size_t)m + (size_t)n + 3 * nl + 4);
+  return (b + 15) & ~size_t(15);
+}
+
+template <bool ROWS_SMEM>
+__global__ void __launch_bounds__(512) k_plu_cluster2(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
+                                                      double eps) {
+  extern __shared__ __align__(16) char dsm[];
+  __shared__ MaxLoc red[32];
+  __shared__ MaxLoc slot[2];
+  __shared__ PluState st;
+  __shared__ int s_nact, s_win;
+  cg::cluster_group cl = cg::this_cluster();
+  const int cr = (int)cl.block_rank(), cs = (int)cl.num_blocks();
+  const PluJob J = jobs[ids[blockIdx.x / cs]];
+  plu_dist_body<false, ROWS_SMEM>(J, eps, cs, cr, dsm, red, st, s_nact, &cl, slot, nullptr, &s_win);
+  cl.sync();  // DSMEM lifetime
+}
+
+template <bool ROWS_SMEM>
+__global__ void __launch_bounds__(512) k_plu_grid2(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
+                                                   int ncores, double eps, GridScratch gs) {
+  extern __shared__ __align__(16) char dsm[];
+  __shared__ MaxLoc red[32];
+  __shared__ PluState st;
+  __shared__ int s_nact, s_win;
+  for (int c = 0; c < ncores; ++c) {
+    const PluJob J = jobs[ids[c]];
+    plu_dist_body<true, ROWS_SMEM>(J, eps, gridDim.x, blockIdx.x, dsm, red, st, s_nact, nullptr, nullptr, &gs,
+                                   &s_win);
+    cg::this_grid().sync();  // candidate buffers are reused by the next core
+  }
+}
+
 // compact r x r LU of a factored core: lu[i][j] = a[rowAt[i]][colAt[j]]
 struct LuExtractJob {
   const double *a;
@@ -1144,7 +1618,7 @@ __global__ void k_lu_extract(const LuExtractJob *__restrict__ jobs) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     int i = (int)(e / J.r), j = (int)(e % J.r);
-    J.out[e] = J.a[(long long)J.rowAt[i] * J.ld + J.colAt[j]];
+    J.out[e] = J.a[(long long)(J.rowAt ? J.rowAt[i] : i) * J.ld + (J.colAt ? J.colAt[j] : j)];
   }
 }
 

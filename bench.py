@@ -326,6 +326,8 @@ def run_gpu_arm(args, cfg, world, rank, local):
                   "true_rel_residual_e2e": true_res, "e2e_iterations": he.iterations},
         "split_s": split,
         "factor": {"device_ms": tim["total_ms"], "host_plan_ms": tim["host_ms"],
+                   "host_ms": {k: tim[k] for k in ("host_preamble_ms", "host_select_ms", "host_sync_wait_ms",
+                                                   "wall_ms")},
                    "phases_ms": {k: tim[k] for k in ("sample_ms", "pivot_lu_ms", "skeleton_ms",
                                                      "hodlr_factor_ms", "dense_front_ms", "eliminate_ms")},
                    "structured_fronts": F.stats.structured_fronts, "dense_fronts": F.stats.dense_fronts,

@@ -1477,6 +1477,7 @@ struct Factorizer {
       }
       if (first_err >= 0) {
         BlockH &b = F->blocks[sblocks[first_err]];
+        if (b.status == 2) throw runtime_error("internal: corrupt complete-pivot candidate");
         char buf[256];
         snprintf(buf, sizeof buf, "pivot %d magnitude %.3e exceeds twice the previous %.3e", b.errk,
                  b.errpiv, b.errprev);

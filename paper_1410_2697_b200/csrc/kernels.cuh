@@ -362,774 +362,19 @@ __device__ __forceinline__ MaxLoc block_maxloc(double v, long long key, MaxLoc *
 }
 
 // ---------------------------------------------------------------------------
-// complete-pivot partial LU with rank cut (_core.pyx:23-86).
-// Logical permutation: values stay at their original (row, col); the pivot
-// search ranks candidates by (|a|, -(pos_r * n + pos_c)) with the CURRENT
-// positions, which reproduces the reference's row-major first-max rule and its
-// whole-row / whole-column swaps exactly. Update is mul + sub (no FMA).
-//
-// Two kernels share the step logic:
-//   k_plu_cta<SMEM>  one CTA per core; bookkeeping in shared memory, and the
-//                    core itself too when it fits (SMEM = true)
-//   k_plu_cluster    one thread-block cluster (8-16 CTAs) per large core; the
-//                    core stays in L2/HBM, bookkeeping is replicated per CTA,
-//                    the per-step argmax is reduced through DSMEM, one
-//                    cluster barrier per elimination step
+// complete-pivot partial LU with rank cut (_core.pyx:23-86): shared state and
+// the cross-CTA candidate buffers; the kernels are the v2 family below.
 // ---------------------------------------------------------------------------
-struct PluSmem {
-  double *mult, *prow;
-  int *rowAt, *posR, *actR, *idxR, *colAt, *posC, *actC, *idxC;
-};
-
-__host__ __device__ inline size_t plu_smem_bytes(int m, int n, bool core) {
-  size_t b = sizeof(double) * (size_t)(m + n) + sizeof(int) * 4 * (size_t)(m + n);
-  if (core) b += sizeof(double) * (size_t)m * n;
-  return (b + 15) & ~size_t(15);
-}
-
-__device__ __forceinline__ PluSmem plu_carve(char *base, int m, int n) {
-  PluSmem s;
-  s.mult = (double *)base;
-  s.prow = s.mult + m;
-  int *ip = (int *)(s.prow + n);
-  s.rowAt = ip;
-  s.posR = ip + m;
-  s.actR = ip + 2 * m;
-  s.idxR = ip + 3 * m;
-  ip += 4 * m;
-  s.colAt = ip;
-  s.posC = ip + n;
-  s.actC = ip + 2 * n;
-  s.idxC = ip + 3 * n;
-  return s;
-}
-
 struct PluState {
   int done, bi, bj, ar, ac, rank, status, errk;
   double akk, u11, prev, ratio, errpiv, errprev;
 };
 
-// step bookkeeping, executed by one thread (identically in every CTA of a cluster)
-__device__ __forceinline__ void plu_decide(PluState &st, PluSmem &S, const double *a, int ld, int n,
-                                           int k, int kmax, double eps, MaxLoc best) {
-  double piv = best.v;
-  int bi, bj;
-  if (best.key == 0x7fffffffffffffffLL) {  // nothing beat -1 (all NaN): reference keeps (k, k)
-    piv = -1.0;
-    bi = S.rowAt[k];
-    bj = S.colAt[k];
-  } else {
-    bi = S.rowAt[(int)(best.key / n)];
-    bj = S.colAt[(int)(best.key % n)];
-  }
-  if (k == 0) {
-    st.u11 = piv;
-    if (piv == 0.0) {
-      st.rank = 0;
-      st.ratio = 0.0;
-      st.done = 1;
-      return;
-    }
-  } else {
-    if (piv > st.prev * MFH_PIVOT_GROWTH_BOUND) {
-      st.status = 1;
-      st.errk = k;
-      st.errpiv = piv;
-      st.errprev = st.prev;
-      st.done = 1;
-      return;
-    }
-    double ratio = piv / st.u11;
-    if (ratio < eps || piv <= MFH_ZERO_PIVOT_RATIO * st.u11) {
-      st.rank = k;
-      st.ratio = ratio;
-      st.done = 1;
-      return;
-    }
-  }
-  if (k == kmax) {
-    st.rank = kmax;
-    st.ratio = piv / st.u11;
-    st.done = 1;
-    return;
-  }
-  int pbi = S.posR[bi], ak = S.rowAt[k];
-  S.rowAt[k] = bi;
-  S.rowAt[pbi] = ak;
-  S.posR[bi] = k;
-  S.posR[ak] = pbi;
-  int pbj = S.posC[bj], ck = S.colAt[k];
-  S.colAt[k] = bj;
-  S.colAt[pbj] = ck;
-  S.posC[bj] = k;
-  S.posC[ck] = pbj;
-  int sl = S.idxR[bi], last = S.actR[st.ar - 1];
-  S.actR[sl] = last;
-  S.idxR[last] = sl;
-  st.ar -= 1;
-  sl = S.idxC[bj];
-  last = S.actC[st.ac - 1];
-  S.actC[sl] = last;
-  S.idxC[last] = sl;
-  st.ac -= 1;
-  st.bi = bi;
-  st.bj = bj;
-  st.akk = a[(long long)bi * ld + bj];
-  st.prev = fabs(st.akk);
-  st.rank = k + 1;
-}
-
-__device__ __forceinline__ void plu_init(PluSmem &S, int m, int n) {
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    S.rowAt[i] = i;
-    S.posR[i] = i;
-    S.actR[i] = i;
-    S.idxR[i] = i;
-  }
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    S.colAt[j] = j;
-    S.posC[j] = j;
-    S.actC[j] = j;
-    S.idxC[j] = j;
-  }
-}
-
-// rank-1 update of the rows slot = r0, r0+rstep, ... fused with the next argmax
-__device__ __forceinline__ void plu_update(double *a, int ld, int n, const PluSmem &S, int ar, int ac,
-                                           int r0, int rstep, double &bv, long long &bk) {
-  bv = -1.0;
-  bk = 0x7fffffffffffffffLL;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int ii = r0 + warp * rstep; ii < ar; ii += nw * rstep) {
-    int i = S.actR[ii];
-    double l = S.mult[ii];
-    double *row = a + (long long)i * ld;
-    long long pr = (long long)S.posR[i] * n;
-    for (int jj = lane; jj < ac; jj += 32) {
-      int j = S.actC[jj];
-      double v = __dsub_rn(row[j], __dmul_rn(l, S.prow[jj]));
-      row[j] = v;
-      double av = fabs(v);
-      long long key = pr + S.posC[j];
-      if (better(av, key, bv, bk)) {
-        bv = av;
-        bk = key;
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ void plu_scan(const double *a, int ld, int n, int m, int r0, int rstep,
-                                         double &bv, long long &bk) {
-  bv = -1.0;
-  bk = 0x7fffffffffffffffLL;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int i = r0 + warp * rstep; i < m; i += nw * rstep) {
-    const double *row = a + (long long)i * ld;
-    for (int j = lane; j < n; j += 32) {
-      double v = fabs(row[j]);
-      long long key = (long long)i * n + j;
-      if (better(v, key, bv, bk)) {
-        bv = v;
-        bk = key;
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ void plu_finish(const PluJob &J, const PluSmem &S, const PluState &st, int m, int n) {
-  for (int i = threadIdx.x; i < m; i += blockDim.x) J.rowAt[i] = S.rowAt[i];
-  for (int j = threadIdx.x; j < n; j += blockDim.x) J.colAt[j] = S.colAt[j];
-  if (threadIdx.x == 0) {
-    J.out[0] = st.rank;
-    J.out[1] = st.status;
-    J.out[2] = st.errk;
-    J.outd[0] = st.ratio;
-    J.outd[1] = st.errpiv;
-    J.outd[2] = st.errprev;
-  }
-}
-
-template <bool SMEM_CORE>
-__global__ void __launch_bounds__(512) k_plu_cta(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
-                                                 double eps) {
-  extern __shared__ __align__(16) char dsm[];
-  __shared__ MaxLoc red[33];
-  __shared__ PluState st;
-  const PluJob J = jobs[ids[blockIdx.x]];
-  const int m = J.m, n = J.n;
-  double *a = J.a;
-  int ld = J.ld;
-  char *base = dsm;
-  if (SMEM_CORE) {
-    double *sa = (double *)dsm;
-    for (long long e = threadIdx.x; e < (long long)m * n; e += blockDim.x)
-      sa[e] = J.a[(e / n) * J.ld + (e % n)];
-    a = sa;
-    ld = n;
-    base = dsm + sizeof(double) * (size_t)m * n;
-  }
-  PluSmem S = plu_carve(base, m, n);
-  plu_init(S, m, n);
-  if (threadIdx.x == 0) {
-    st = PluState{};
-    st.ar = m;
-    st.ac = n;
-  }
-  __syncthreads();
-  double bv;
-  long long bk;
-  plu_scan(a, ld, n, m, 0, 1, bv, bk);
-  const int kmin = min(m, n);
-  for (int k = 0; k < kmin; ++k) {
-    MaxLoc best = block_maxloc(bv, bk, red);
-    if (threadIdx.x == 0) plu_decide(st, S, a, ld, n, k, J.kmax, eps, best);
-    __syncthreads();
-    if (st.done) break;
-    const int bi = st.bi, bj = st.bj, ar = st.ar, ac = st.ac;
-    const double akk = st.akk;
-    for (int ii = threadIdx.x; ii < ar; ii += blockDim.x) {
-      int i = S.actR[ii];
-      double l = a[(long long)i * ld + bj] / akk;
-      a[(long long)i * ld + bj] = l;
-      S.mult[ii] = l;
-    }
-    for (int jj = threadIdx.x; jj < ac; jj += blockDim.x) S.prow[jj] = a[(long long)bi * ld + S.actC[jj]];
-    __syncthreads();
-    plu_update(a, ld, n, S, ar, ac, 0, 1, bv, bk);
-    __syncthreads();
-  }
-  if (SMEM_CORE) {
-    for (long long e = threadIdx.x; e < (long long)m * n; e += blockDim.x)
-      J.a[(e / n) * J.ld + (e % n)] = a[e];
-  }
-  plu_finish(J, S, st, m, n);
-}
-
-// one cluster per core; CTA c owns the active-row slots ii with ii % csize == c
-__global__ void __launch_bounds__(512) k_plu_cluster(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
-                                                     double eps) {
-  extern __shared__ __align__(16) char dsm[];
-  __shared__ MaxLoc red[33];
-  __shared__ MaxLoc slot[2];
-  __shared__ PluState st;
-  cg::cluster_group cl = cg::this_cluster();
-  const int crank = (int)cl.block_rank(), csize = (int)cl.num_blocks();
-  const PluJob J = jobs[ids[blockIdx.x / csize]];
-  const int m = J.m, n = J.n, ld = J.ld;
-  double *a = J.a;
-  PluSmem S = plu_carve(dsm, m, n);
-  plu_init(S, m, n);
-  if (threadIdx.x == 0) {
-    st = PluState{};
-    st.ar = m;
-    st.ac = n;
-  }
-  __syncthreads();
-  double bv;
-  long long bk;
-  plu_scan(a, ld, n, m, crank, csize, bv, bk);
-  const int kmin = min(m, n);
-  for (int k = 0; k < kmin; ++k) {
-    MaxLoc best = block_maxloc(bv, bk, red);
-    if (threadIdx.x == 0) slot[k & 1] = best;
-    cl.sync();  // publishes slots and this step's global writes
-    if (threadIdx.x == 0) {
-      MaxLoc g = {-2.0, 0x7fffffffffffffffLL};
-      for (int c = 0; c < csize; ++c) {
-        MaxLoc *rs = cl.map_shared_rank(&slot[k & 1], c);
-        MaxLoc o = *rs;
-        if (better(o.v, o.key, g.v, g.key)) g = o;
-      }
-      plu_decide(st, S, a, ld, n, k, J.kmax, eps, g);
-    }
-    __syncthreads();
-    if (st.done) break;
-    const int bi = st.bi, bj = st.bj, ar = st.ar, ac = st.ac;
-    const double akk = st.akk;
-    for (int ii = crank + (int)threadIdx.x * csize; ii < ar; ii += (int)blockDim.x * csize) {
-      int i = S.actR[ii];
-      double l = a[(long long)i * ld + bj] / akk;
-      a[(long long)i * ld + bj] = l;
-      S.mult[ii] = l;
-    }
-    for (int jj = threadIdx.x; jj < ac; jj += blockDim.x) S.prow[jj] = a[(long long)bi * ld + S.actC[jj]];
-    __syncthreads();
-    plu_update(a, ld, n, S, ar, ac, crank, csize, bv, bk);
-    __syncthreads();
-  }
-  if (crank == 0) plu_finish(J, S, st, m, n);
-  cl.sync();  // no CTA leaves while another may still read its slots
-}
-
-// cluster variant with the core distributed over the CTAs' shared memory:
-// original row i lives in CTA (i % csize) at local row (i / csize); the pivot
-// row is read through DSMEM from its owner; one cluster barrier per step
-__host__ __device__ inline size_t plu_dsm_bytes(int m, int n, int cs, int crank_max_rows) {
-  (void)m;
-  size_t nl = (size_t)crank_max_rows;
-  size_t b = sizeof(double) * (nl * (size_t)n + nl + (size_t)n);      // rows, mult, prow
-  b += sizeof(int) * ((size_t)m + 4 * (size_t)n + 3 * nl);             // rowAt, col books, local row books
-  (void)cs;
-  return (b + 15) & ~size_t(15);
-}
-
-__global__ void __launch_bounds__(512) k_plu_cluster_smem(const PluJob *__restrict__ jobs,
-                                                          const int *__restrict__ ids, double eps) {
-  extern __shared__ __align__(16) char dsm[];
-  __shared__ MaxLoc red[33];
-  __shared__ MaxLoc slot[2];
-  __shared__ PluState st;
-  __shared__ int s_nact;
-  cg::cluster_group cl = cg::this_cluster();
-  const int cr = (int)cl.block_rank(), cs = (int)cl.num_blocks();
-  const PluJob J = jobs[ids[blockIdx.x / cs]];
-  const int m = J.m, n = J.n, ldg = J.ld;
-  const int nl_max = (m + cs - 1) / cs;
-  const int nl = (m - cr + cs - 1) / cs;  // rows owned by this CTA
-  double *rows = (double *)dsm;
-  double *mult = rows + (size_t)nl_max * n;
-  double *prow = mult + nl_max;
-  int *rowAt = (int *)(prow + n);
-  int *colAt = rowAt + m;
-  int *posC = colAt + n;
-  int *actC = posC + n;
-  int *idxC = actC + n;
-  int *posRl = idxC + n;  // position of each owned row
-  int *actRl = posRl + nl_max;  // active owned rows (local indices)
-  int *idxRl = actRl + nl_max;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (long long e = tid; e < (long long)nl * n; e += nt) {
-    int li = (int)(e / n), j = (int)(e % n);
-    rows[e] = J.a[(long long)(li * cs + cr) * ldg + j];
-  }
-  for (int i = tid; i < m; i += nt) rowAt[i] = i;
-  for (int j = tid; j < n; j += nt) {
-    colAt[j] = j;
-    posC[j] = j;
-    actC[j] = j;
-    idxC[j] = j;
-  }
-  for (int li = tid; li < nl; li += nt) {
-    posRl[li] = li * cs + cr;
-    actRl[li] = li;
-    idxRl[li] = li;
-  }
-  if (tid == 0) {
-    st = PluState{};
-    st.ar = m;
-    st.ac = n;
-    s_nact = nl;
-  }
-  __syncthreads();
-  // initial scan of owned rows
-  double bv = -1.0;
-  long long bk = 0x7fffffffffffffffLL;
-  {
-    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-    for (int li = warp; li < nl; li += nw) {
-      const double *row = rows + (size_t)li * n;
-      long long pr = (long long)(li * cs + cr) * n;
-      for (int j = lane; j < n; j += 32) {
-        double v = fabs(row[j]);
-        if (better(v, pr + j, bv, bk)) {
-          bv = v;
-          bk = pr + j;
-        }
-      }
-    }
-  }
-  const int kmin = min(m, n);
-  for (int k = 0; k < kmin; ++k) {
-    MaxLoc best = block_maxloc(bv, bk, red);
-    if (tid == 0) slot[k & 1] = best;
-    cl.sync();
-    if (tid < 32) {
-      // one lane per CTA of the cluster reads its slot through DSMEM, then a warp reduction
-      MaxLoc g = {-2.0, 0x7fffffffffffffffLL};
-      if (tid < cs) g = *cl.map_shared_rank(&slot[k & 1], tid);
-      for (int o = 16; o > 0; o >>= 1) {
-        double ov = __shfl_down_sync(0xffffffffu, g.v, o);
-        long long ok = __shfl_down_sync(0xffffffffu, g.key, o);
-        if (better(ov, ok, g.v, g.key)) {
-          g.v = ov;
-          g.key = ok;
-        }
-      }
-      if (tid == 0) {
-      double piv = g.v;
-      int pr, pc;
-      if (g.key == 0x7fffffffffffffffLL) {
-        piv = -1.0;
-        pr = k;
-        pc = k;
-      } else {
-        pr = (int)(g.key / n);
-        pc = (int)(g.key % n);
-      }
-      int bi = rowAt[pr], bj = colAt[pc];
-      bool stop = false;
-      if (k == 0) {
-        st.u11 = piv;
-        if (piv == 0.0) {
-          st.rank = 0;
-          st.ratio = 0.0;
-          stop = true;
-        }
-      } else if (piv > st.prev * MFH_PIVOT_GROWTH_BOUND) {
-        st.status = 1;
-        st.errk = k;
-        st.errpiv = piv;
-        st.errprev = st.prev;
-        stop = true;
-      } else {
-        double ratio = piv / st.u11;
-        if (ratio < eps || piv <= MFH_ZERO_PIVOT_RATIO * st.u11) {
-          st.rank = k;
-          st.ratio = ratio;
-          stop = true;
-        }
-      }
-      if (!stop && k == J.kmax) {
-        st.rank = J.kmax;
-        st.ratio = piv / st.u11;
-        stop = true;
-      }
-      st.done = stop ? 1 : 0;
-      if (!stop) {
-        int ak = rowAt[k];
-        rowAt[k] = bi;
-        rowAt[pr] = ak;
-        if (bi % cs == cr) posRl[bi / cs] = k;
-        if (ak % cs == cr) posRl[ak / cs] = pr;
-        int ck = colAt[k];
-        colAt[k] = bj;
-        colAt[pc] = ck;
-        posC[bj] = k;
-        posC[ck] = pc;
-        int sl = idxC[bj], last = actC[st.ac - 1];
-        actC[sl] = last;
-        idxC[last] = sl;
-        st.ac -= 1;
-        if (bi % cs == cr) {
-          int li = bi / cs;
-          int s2 = idxRl[li], l2 = actRl[s_nact - 1];
-          actRl[s2] = l2;
-          idxRl[l2] = s2;
-          s_nact -= 1;
-        }
-        st.ar -= 1;
-        st.bi = bi;
-        st.bj = bj;
-        const double *orow = cl.map_shared_rank(rows, bi % cs) + (size_t)(bi / cs) * n;
-        st.akk = orow[bj];
-        st.prev = fabs(st.akk);
-        st.rank = k + 1;
-      }
-      }
-    }
-    __syncthreads();
-    if (st.done) break;
-    const int bi = st.bi, bj = st.bj, ac = st.ac, na = s_nact;
-    const double akk = st.akk;
-    const double *orow = cl.map_shared_rank(rows, bi % cs) + (size_t)(bi / cs) * n;
-    for (int jj = tid; jj < ac; jj += nt) prow[jj] = orow[actC[jj]];
-    for (int q = tid; q < na; q += nt) {
-      int li = actRl[q];
-      double l = rows[(size_t)li * n + bj] / akk;
-      rows[(size_t)li * n + bj] = l;
-      mult[q] = l;
-    }
-    __syncthreads();
-    bv = -1.0;
-    bk = 0x7fffffffffffffffLL;
-    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-    for (int q = warp; q < na; q += nw) {
-      int li = actRl[q];
-      double l = mult[q];
-      double *row = rows + (size_t)li * n;
-      long long prk = (long long)posRl[li] * n;
-      for (int jj = lane; jj < ac; jj += 32) {
-        int j = actC[jj];
-        double v = __dsub_rn(row[j], __dmul_rn(l, prow[jj]));
-        row[j] = v;
-        double av = fabs(v);
-        long long key = prk + posC[j];
-        if (better(av, key, bv, bk)) {
-          bv = av;
-          bk = key;
-        }
-      }
-    }
-    __syncthreads();
-  }
-  for (long long e = tid; e < (long long)nl * n; e += nt) {
-    int li = (int)(e / n), j = (int)(e % n);
-    J.a[(long long)(li * cs + cr) * ldg + j] = rows[e];
-  }
-  if (cr == 0) {
-    for (int i = tid; i < m; i += nt) J.rowAt[i] = rowAt[i];
-    for (int j = tid; j < n; j += nt) J.colAt[j] = colAt[j];
-    if (tid == 0) {
-      J.out[0] = st.rank;
-      J.out[1] = st.status;
-      J.out[2] = st.errk;
-      J.outd[0] = st.ratio;
-      J.outd[1] = st.errpiv;
-      J.outd[2] = st.errprev;
-    }
-  }
-  cl.sync();  // DSMEM lifetime: nobody exits while others may read its rows / slots
-}
-
-// whole-GPU cooperative variant for the largest cores: CTA g of G owns rows
-// i % G == g in shared memory; every step each CTA publishes its best
-// candidate (value, key) AND that candidate's row to global memory, one grid
-// barrier, then all CTAs reduce the G candidates identically and read the
-// winner's published row as the pivot row. Cores are processed one after
-// another with the whole GPU.
 struct GridScratch {
   MaxLoc *best;   // 2 x G
   double *cand;   // 2 x G x nmax
   int nmax;
 };
-
-__global__ void __launch_bounds__(512) k_plu_grid(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
-                                                  int ncores, double eps, GridScratch gs) {
-  extern __shared__ __align__(16) char dsm[];
-  __shared__ MaxLoc red[33];
-  __shared__ PluState st;
-  __shared__ int s_nact, s_win;
-  cg::grid_group grid = cg::this_grid();
-  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-  for (int c = 0; c < ncores; ++c) {
-    const PluJob J = jobs[ids[c]];
-    const int m = J.m, n = J.n, ldg = J.ld;
-    const int nl_max = (m + G - 1) / G;
-    const int nl = (m - g + G - 1) / G;
-    double *rows = (double *)dsm;
-    double *mult = rows + (size_t)nl_max * n;
-    double *prow = mult + nl_max;
-    int *rowAt = (int *)(prow + n);
-    int *colAt = rowAt + m;
-    int *posC = colAt + n;
-    int *actC = posC + n;
-    int *idxC = actC + n;
-    int *posRl = idxC + n;
-    int *actRl = posRl + nl_max;
-    int *idxRl = actRl + nl_max;
-    int *candRow = idxRl + nl_max;  // local row index of this CTA's candidate
-    for (long long e = tid; e < (long long)nl * n; e += nt) {
-      int li = (int)(e / n), j = (int)(e % n);
-      rows[e] = J.a[(long long)(li * G + g) * ldg + j];
-    }
-    for (int i = tid; i < m; i += nt) rowAt[i] = i;
-    for (int j = tid; j < n; j += nt) {
-      colAt[j] = j;
-      posC[j] = j;
-      actC[j] = j;
-      idxC[j] = j;
-    }
-    for (int li = tid; li < nl; li += nt) {
-      posRl[li] = li * G + g;
-      actRl[li] = li;
-      idxRl[li] = li;
-    }
-    if (tid == 0) {
-      st = PluState{};
-      st.ar = m;
-      st.ac = n;
-      s_nact = nl;
-    }
-    __syncthreads();
-    double bv = -1.0;
-    long long bk = 0x7fffffffffffffffLL;
-    {
-      const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-      for (int li = warp; li < nl; li += nw) {
-        const double *row = rows + (size_t)li * n;
-        long long pr = (long long)(li * G + g) * n;
-        for (int j = lane; j < n; j += 32) {
-          double v = fabs(row[j]);
-          if (better(v, pr + j, bv, bk)) {
-            bv = v;
-            bk = pr + j;
-          }
-        }
-      }
-    }
-    const int kmin = min(m, n);
-    for (int k = 0; k < kmin; ++k) {
-      const int par = k & 1;
-      MaxLoc best = block_maxloc(bv, bk, red);
-      // publish the candidate and its row (row = key / n position -> original via rowAt)
-      if (tid == 0) {
-        gs.best[par * G + g] = best;
-        int li = -1;
-        if (best.key != 0x7fffffffffffffffLL) li = rowAt[(int)(best.key / n)] / G;
-        *candRow = li;
-      }
-      __syncthreads();
-      if (*candRow >= 0) {
-        const double *src = rows + (size_t)(*candRow) * n;
-        double *dst = gs.cand + ((size_t)par * G + g) * gs.nmax;
-        for (int j = tid; j < n; j += nt) dst[j] = src[j];
-      }
-      grid.sync();
-      // identical reduction in every CTA
-      if (tid < 32) {
-        double v = -2.0;
-        long long key = 0x7fffffffffffffffLL;
-        int who = -1;
-        for (int q = tid; q < G; q += 32) {
-          MaxLoc o = gs.best[par * G + q];
-          if (better(o.v, o.key, v, key)) {
-            v = o.v;
-            key = o.key;
-            who = q;
-          }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-          double ov = __shfl_down_sync(0xffffffffu, v, o);
-          long long ok = __shfl_down_sync(0xffffffffu, key, o);
-          int ow = __shfl_down_sync(0xffffffffu, who, o);
-          if (better(ov, ok, v, key)) {
-            v = ov;
-            key = ok;
-            who = ow;
-          }
-        }
-        MaxLoc gbest = {v, key};
-        if (tid == 0) s_win = who;
-        if (tid == 0) {
-          double piv = gbest.v;
-          int pr, pc;
-          if (gbest.key == 0x7fffffffffffffffLL) {
-            piv = -1.0;
-            pr = k;
-            pc = k;
-          } else {
-            pr = (int)(gbest.key / n);
-            pc = (int)(gbest.key % n);
-          }
-          int bi = rowAt[pr], bj = colAt[pc];
-          bool stop = false;
-          if (k == 0) {
-            st.u11 = piv;
-            if (piv == 0.0) {
-              st.rank = 0;
-              st.ratio = 0.0;
-              stop = true;
-            }
-          } else if (piv > st.prev * MFH_PIVOT_GROWTH_BOUND) {
-            st.status = 1;
-            st.errk = k;
-            st.errpiv = piv;
-            st.errprev = st.prev;
-            stop = true;
-          } else {
-            double ratio = piv / st.u11;
-            if (ratio < eps || piv <= MFH_ZERO_PIVOT_RATIO * st.u11) {
-              st.rank = k;
-              st.ratio = ratio;
-              stop = true;
-            }
-          }
-          if (!stop && k == J.kmax) {
-            st.rank = J.kmax;
-            st.ratio = piv / st.u11;
-            stop = true;
-          }
-          st.done = stop ? 1 : 0;
-          if (!stop) {
-            int ak = rowAt[k];
-            rowAt[k] = bi;
-            rowAt[pr] = ak;
-            if (bi % G == g) posRl[bi / G] = k;
-            if (ak % G == g) posRl[ak / G] = pr;
-            int ck = colAt[k];
-            colAt[k] = bj;
-            colAt[pc] = ck;
-            posC[bj] = k;
-            posC[ck] = pc;
-            int sl = idxC[bj], last = actC[st.ac - 1];
-            actC[sl] = last;
-            idxC[last] = sl;
-            st.ac -= 1;
-            if (bi % G == g) {
-              int li = bi / G;
-              int s2 = idxRl[li], l2 = actRl[s_nact - 1];
-              actRl[s2] = l2;
-              idxRl[l2] = s2;
-              s_nact -= 1;
-            }
-            st.ar -= 1;
-            st.bi = bi;
-            st.bj = bj;
-            st.rank = k + 1;
-          }
-        }
-      }
-      __syncthreads();
-      if (st.done) break;
-      const int bj = st.bj, ac = st.ac, na = s_nact;
-      const double *wrow = gs.cand + ((size_t)par * G + s_win) * gs.nmax;
-      const double akk = wrow[bj];
-      if (tid == 0) st.prev = fabs(akk);
-      for (int jj = tid; jj < ac; jj += nt) prow[jj] = wrow[actC[jj]];
-      for (int q = tid; q < na; q += nt) {
-        int li = actRl[q];
-        double l = rows[(size_t)li * n + bj] / akk;
-        rows[(size_t)li * n + bj] = l;
-        mult[q] = l;
-      }
-      __syncthreads();
-      bv = -1.0;
-      bk = 0x7fffffffffffffffLL;
-      const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-      for (int q = warp; q < na; q += nw) {
-        int li = actRl[q];
-        double l = mult[q];
-        double *row = rows + (size_t)li * n;
-        long long prk = (long long)posRl[li] * n;
-        for (int jj = lane; jj < ac; jj += 32) {
-          int j = actC[jj];
-          double v = __dsub_rn(row[j], __dmul_rn(l, prow[jj]));
-          row[j] = v;
-          double av = fabs(v);
-          long long key = prk + posC[j];
-          if (better(av, key, bv, bk)) {
-            bv = av;
-            bk = key;
-          }
-        }
-      }
-      __syncthreads();
-    }
-    for (long long e = tid; e < (long long)nl * n; e += nt) {
-      int li = (int)(e / n), j = (int)(e % n);
-      J.a[(long long)(li * G + g) * ldg + j] = rows[e];
-    }
-    if (g == 0) {
-      for (int i = tid; i < m; i += nt) J.rowAt[i] = rowAt[i];
-      for (int j = tid; j < n; j += nt) J.colAt[j] = colAt[j];
-      if (tid == 0) {
-        J.out[0] = st.rank;
-        J.out[1] = st.status;
-        J.out[2] = st.errk;
-        J.outd[0] = st.ratio;
-        J.outd[1] = st.errpiv;
-        J.outd[2] = st.errprev;
-      }
-    }
-    grid.sync();  // shared scratch / candidate buffers are reused by the next core
-  }
-}
-
-__host__ __device__ inline size_t plu_grid_bytes(int m, int n, int G) {
-  int nl = (m + G - 1) / G;
-  return plu_dsm_bytes(m, n, G, nl) + 16;
-}
 
 // ===========================================================================
 // v2 complete-pivot LU kernels: the reference's physical column swaps are

@@ -244,7 +244,7 @@ def run_gpu_arm(args, cfg, world, rank, local):
     dev_op = A.device_operator()
     hist = np.empty(4000)
 
-    split = {"factor_s": [], "solve_s": []}
+    split = {"factor_s": [], "solve_s": [], "gmres_inner_s": [], "apply_build_s": []}
 
     def step_device():
         t0 = time.perf_counter()
@@ -257,8 +257,12 @@ def run_gpu_arm(args, cfg, world, rank, local):
         _lib.check(_lib.lib().mfh_gmres_device(ctx.handle, C.byref(ops), n, C.c_void_p(d_b.data_ptr()),
                                                C.c_void_p(d_x.data_ptr()), cfg["tol"], 4000, cfg["restart"],
                                                _lib.ptr(hist), C.byref(nh), C.byref(its), C.byref(conv)))
+        t2 = time.perf_counter()
+        ti = F.timing()
         split["factor_s"].append(t1 - t0)
-        split["solve_s"].append(time.perf_counter() - t1)
+        split["solve_s"].append(t2 - t1)
+        split["gmres_inner_s"].append(ti["gmres_ms"] / 1e3)
+        split["apply_build_s"].append((ti["apply_build_ms"] + ti["apply_instantiate_ms"]) / 1e3)
         return F, its.value, bool(conv.value), hist[max(0, nh.value - 1)]
 
     def step_e2e():  # public API, host b -> host x
@@ -278,6 +282,7 @@ def run_gpu_arm(args, cfg, world, rank, local):
     launches0 = ctx.info()[1]
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
+            F = None  # the previous factorization is released before the next step
             flush.fill_(1)
             torch.cuda.synchronize()
             barrier(world)
@@ -327,7 +332,8 @@ def run_gpu_arm(args, cfg, world, rank, local):
         "split_s": split,
         "factor": {"device_ms": tim["total_ms"], "host_plan_ms": tim["host_ms"],
                    "host_ms": {k: tim[k] for k in ("host_preamble_ms", "host_select_ms", "host_sync_wait_ms",
-                                                   "wall_ms")},
+                                                   "wall_ms", "apply_build_ms", "apply_instantiate_ms",
+                                                   "gmres_ms", "gmres_apply_ms")},
                    "phases_ms": {k: tim[k] for k in ("sample_ms", "pivot_lu_ms", "skeleton_ms",
                                                      "hodlr_factor_ms", "dense_front_ms", "eliminate_ms")},
                    "structured_fronts": F.stats.structured_fronts, "dense_fronts": F.stats.dense_fronts,

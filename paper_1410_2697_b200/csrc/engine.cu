@@ -19,6 +19,8 @@
 #include <functional>
 #include <memory>
 #include <numeric>
+#include <atomic>
+#include <thread>
 
 #include "internal.h"
 #include "kernels.cuh"
@@ -827,6 +829,7 @@ struct FrontH {
   double *Pinv = nullptr, *Gfp = nullptr, *Gpf = nullptr;
   // structured path
   int pp = -1, ff = -1, pf = -1, fp = -1;  // tree / block ids
+  int tree_base = -1, block_base = -1;      // pre-assigned plan slots
   // update for the parent
   int upd = -1;  // -1 none, 0 dense, 1 hodlr
   const double *upd_dense = nullptr;
@@ -981,7 +984,7 @@ struct Factorizer {
   long long *d_ap_ptr = nullptr;
   int *d_ap_col = nullptr;
   double *d_ap_val = nullptr;
-  Graph graph;  // BDLR graph over permuted ids
+  const Graph *gp = nullptr;  // BDLR graph over permuted ids (cached on the etree)
   // selection scratch
   std::vector<int64_t> mark;
   int64_t stamp = 0;
@@ -997,6 +1000,7 @@ struct Factorizer {
   // ---- selection (bdlr.py:89-136), positions are front-local ----
   void select(const FrontH &f, int r0, int m, int c0, int nn, std::vector<int> &I,
               std::vector<int> &J) {
+    const Graph &graph = *gp;
     I.clear();
     J.clear();
     const int64_t *ids = f.ids.data();
@@ -1060,7 +1064,7 @@ struct Factorizer {
   }
 
   // ---- tree construction (hodlr.py:203-246 recursion order) ----
-  int make_tree(int fi, int base, int nloc, std::vector<int> &blist) {
+  int make_tree(int fi, int base, int nloc, std::vector<int> &blist, int tid) {
     HTree t;
     t.fi = fi;
     t.base = base;
@@ -1097,8 +1101,7 @@ struct Factorizer {
     t.f2.assign(cap, FacView{});
     t.linv.assign(cap, nullptr);
     t.cinv.assign(cap, nullptr);
-    F->trees.push_back(std::move(t));
-    int tid = (int)F->trees.size() - 1;
+    F->trees[tid] = std::move(t);
     // recursion with explicit stack: (slot, lo, hi, depth, stage)
     struct Fr {
       int v, lo, hi, d, stage;
@@ -1142,15 +1145,69 @@ struct Factorizer {
     return tid;
   }
 
+  int block_cursor = 0;  // planner thread: next pre-assigned block slot
   int new_block(int fi, int r0, int m, int c0, int nn) {
-    BlockH b;
+    BlockH &b = F->blocks[block_cursor];
     b.fi = fi;
     b.r0 = r0;
     b.m = m;
     b.c0 = c0;
     b.n = nn;
-    F->blocks.push_back(std::move(b));
-    return (int)F->blocks.size() - 1;
+    return block_cursor++;
+  }
+
+  // ---- symbolic plan of one structured front (trees, blocks, BDLR selections);
+  // runs on the planner thread, writing only into this front's pre-assigned slots
+  void plan_front(int fi) {
+    FrontH &f = F->fronts[fi];
+    block_cursor = f.block_base;
+    std::vector<int> blist;
+    if (f.npv) f.pp = make_tree(fi, 0, f.npv, blist, f.tree_base);
+    if (f.npv && f.nf) {
+      f.pf = new_block(fi, 0, f.npv, f.npv, f.nf);
+      f.fp = new_block(fi, f.npv, f.nf, 0, f.npv);
+      blist.push_back(f.pf);
+      blist.push_back(f.fp);
+    }
+    if (f.nf) f.ff = make_tree(fi, f.npv, f.nf, blist, f.tree_base + 1);
+    F->front_blocks[fi] = blist;
+    for (int bi : blist) {
+      BlockH &b = F->blocks[bi];
+      select(f, b.r0, b.m, b.c0, b.n, b.I, b.J);
+    }
+  }
+
+  static int count_internal(int64_t n, int64_t nl) {
+    if (n <= nl) return 0;
+    int64_t h = n / 2;
+    return 1 + count_internal(h, nl) + count_internal(n - h, nl);
+  }
+
+  // planner thread over the structured fronts, in processing order
+  std::thread planner;
+  std::atomic<int> planned{0};
+  std::vector<int> plan_order, plan_pos;
+  std::exception_ptr plan_error;
+  void start_planner() {
+    planner = std::thread([this]() {
+      try {
+        for (int fi : plan_order) {
+          plan_front(fi);
+          planned.fetch_add(1, std::memory_order_release);
+        }
+      } catch (...) {
+        plan_error = std::current_exception();
+        planned.store(1 << 30, std::memory_order_release);
+      }
+    });
+  }
+  void wait_planned(int fi) {
+    int need = plan_pos[fi] + 1;
+    while (planned.load(std::memory_order_acquire) < need) std::this_thread::yield();
+    if (plan_error) std::rethrow_exception(plan_error);
+  }
+  ~Factorizer() {
+    if (planner.joinable()) planner.join();
   }
 
   void check_flags(int64_t upto_flags) {
@@ -1285,17 +1342,9 @@ struct Factorizer {
     // ------------------------------------------------ structured: plan blocks
     std::vector<int> sblocks;  // all compressed blocks at this height
     for (int fi : S) {
+      wait_planned(fi);
       FrontH &f = F->fronts[fi];
-      std::vector<int> blist;
-      if (f.npv) f.pp = make_tree(fi, 0, f.npv, blist);
-      if (f.npv && f.nf) {
-        f.pf = new_block(fi, 0, f.npv, f.npv, f.nf);
-        f.fp = new_block(fi, f.npv, f.nf, 0, f.npv);
-        blist.push_back(f.pf);
-        blist.push_back(f.fp);
-      }
-      if (f.nf) f.ff = make_tree(fi, f.npv, f.nf, blist);
-      F->front_blocks[fi] = blist;
+      const std::vector<int> &blist = F->front_blocks[fi];
       sblocks.insert(sblocks.end(), blist.begin(), blist.end());
       // leaves: sampled straight into their storage
       for (int tt : {f.pp, f.ff}) {
@@ -1319,8 +1368,6 @@ struct Factorizer {
     std::vector<int64_t> ioff, doff;
     for (int bi : sblocks) {
       BlockH &b = F->blocks[bi];
-      FrontH &f = F->fronts[b.fi];
-      select(f, b.r0, b.m, b.c0, b.n, b.I, b.J);
       ioff.push_back(itot);
       doff.push_back(dtot);
       itot += 4 * ((int64_t)b.I.size() + b.J.size()) + 4;
@@ -1818,47 +1865,114 @@ struct Factorizer {
 
   void run(const HostCsr &A, int mode) {
     auto t0 = std::chrono::steady_clock::now();
+    const bool trace = getenv("MFH_HOST_TRACE") != nullptr;
+    auto tprev = t0;
+    auto mark_t = [&](const char *what) {
+      if (!trace) return;
+      auto now = std::chrono::steady_clock::now();
+      fprintf(stderr, "[mfh host] %-20s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - tprev).count());
+      tprev = now;
+    };
     n = A.n;
     accel = mode == MFH_ACCELERATED;
     F->n = n;
     F->perm = et->perm;
     F->mode = mode;
     F->params = P;
-    // ---- P A P^T as CSR (multifrontal.py:245-250)
+    // ---- P A P^T as CSR (multifrontal.py:245-250). The pattern part (two
+    // counting-sort transposes, O(nnz)) and the BDLR graph are symbolic: they
+    // are cached on the elimination tree, keyed by (pattern, zero pattern);
+    // every factorization gathers the values.
     {
       const std::vector<int64_t> &perm = et->perm;
-      std::vector<int64_t> cnt(n + 1, 0);
-      for (int64_t i = 0; i < n; ++i) cnt[perm[i] + 1] += A.ptr[i + 1] - A.ptr[i];
-      for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
-      ap_ptr = cnt;
-      ap_col.resize(cnt[n]);
-      ap_val.resize(cnt[n]);
-      std::vector<std::pair<int, double>> row;
-      for (int64_t i = 0; i < n; ++i) {
-        int64_t pi = perm[i];
-        row.clear();
-        for (int64_t p = A.ptr[i]; p < A.ptr[i + 1]; ++p) row.push_back({(int)perm[A.idx[p]], A.val[p]});
-        std::sort(row.begin(), row.end(), [](auto &a, auto &b) { return a.first < b.first; });
-        int64_t q = ap_ptr[pi];
-        for (auto &e : row) {
-          ap_col[q] = e.first;
-          ap_val[q] = e.second;
-          ++q;
+      const int64_t nnz = A.ptr[n];
+      uint64_t key = 1469598103934665603ULL ^ (uint64_t)n ^ ((uint64_t)nnz << 20) ^ (accel ? 7ULL : 0ULL);
+      auto mix = [&](uint64_t v) { key = (key ^ v) * 1099511628211ULL; };
+      for (int64_t i = 0; i <= n; i += 1) mix((uint64_t)A.ptr[i]);
+      for (int64_t p2 = 0; p2 < nnz; ++p2) {
+        mix((uint64_t)A.idx[p2]);
+        if (A.val[p2] == 0.0) mix(0x9e3779b97f4a7c15ULL ^ (uint64_t)p2);
+      }
+      mfh_symcache &C = et->cache;
+      if (!C.valid || C.key != key || (accel && !C.has_graph)) {
+        C = mfh_symcache{};
+        std::vector<int64_t> iperm(n);
+        for (int64_t i = 0; i < n; ++i) iperm[perm[i]] = i;
+        // T = (P A P^T)^T: row = new column, entries in increasing new row
+        std::vector<int64_t> tptr(n + 1, 0);
+        for (int64_t p2 = 0; p2 < nnz; ++p2) tptr[perm[A.idx[p2]] + 1]++;
+        for (int64_t i = 0; i < n; ++i) tptr[i + 1] += tptr[i];
+        std::vector<int> tcol(nnz);
+        std::vector<int64_t> tsrc(nnz);
+        {
+          std::vector<int64_t> fill(tptr.begin(), tptr.end() - 1);
+          for (int64_t pi = 0; pi < n; ++pi) {
+            int64_t i = iperm[pi];
+            for (int64_t p2 = A.ptr[i]; p2 < A.ptr[i + 1]; ++p2) {
+              int64_t q = fill[perm[A.idx[p2]]]++;
+              tcol[q] = (int)pi;
+              tsrc[q] = p2;
+            }
+          }
         }
+        C.ap_ptr.assign(n + 1, 0);
+        for (int64_t pi = 0; pi < n; ++pi) C.ap_ptr[pi + 1] = C.ap_ptr[pi] + (A.ptr[iperm[pi] + 1] - A.ptr[iperm[pi]]);
+        C.ap_col.resize(nnz);
+        C.src.resize(nnz);
+        {
+          std::vector<int64_t> fill(C.ap_ptr.begin(), C.ap_ptr.end() - 1);
+          for (int64_t pj = 0; pj < n; ++pj)
+            for (int64_t q = tptr[pj]; q < tptr[pj + 1]; ++q) {
+              int64_t r = fill[tcol[q]]++;
+              C.ap_col[r] = (int)pj;
+              C.src[r] = tsrc[q];
+            }
+        }
+        if (accel) {
+          // BDLR graph (sparse.py:102-111 on Ap): row i = {j != i : Ap[i][j] != 0 or Ap[j][i] != 0}
+          Graph &g = C.graph;
+          g.n = n;
+          g.ptr.assign(n + 1, 0);
+          g.idx.reserve(2 * nnz);
+          for (int64_t i = 0; i < n; ++i) {
+            int64_t p2 = C.ap_ptr[i], pe = C.ap_ptr[i + 1], q = tptr[i], qe = tptr[i + 1];
+            int64_t last = -1;
+            while (p2 < pe || q < qe) {
+              int64_t j;
+              bool nz;
+              if (q >= qe || (p2 < pe && C.ap_col[p2] <= tcol[q])) {
+                j = C.ap_col[p2];
+                nz = A.val[C.src[p2]] != 0.0;
+                ++p2;
+              } else {
+                j = tcol[q];
+                nz = A.val[tsrc[q]] != 0.0;
+                ++q;
+              }
+              if (!nz || j == i || j == last) continue;
+              g.idx.push_back(j);
+              last = j;
+            }
+            g.ptr[i + 1] = (int64_t)g.idx.size();
+          }
+          C.has_graph = true;
+        }
+        C.key = key;
+        C.valid = true;
       }
+      ap_val.resize(nnz);
+      for (int64_t r = 0; r < nnz; ++r) ap_val[r] = A.val[C.src[r]];
+      if (accel) gp = &C.graph;
       d_ap_ptr = (long long *)F->arena.alloc(sizeof(int64_t) * (n + 1));
-      d_ap_col = F->arena.i(std::max<int64_t>(1, ap_col.size()));
-      d_ap_val = F->arena.d(std::max<int64_t>(1, ap_val.size()));
-      upload(ctx->s, d_ap_ptr, ap_ptr.data(), sizeof(int64_t) * (n + 1));
-      if (!ap_col.empty()) {
-        upload(ctx->s, d_ap_col, ap_col.data(), sizeof(int) * ap_col.size());
-        upload(ctx->s, d_ap_val, ap_val.data(), sizeof(double) * ap_val.size());
-      }
-      if (accel) {
-        std::vector<int64_t> ptr64(ap_ptr), col64(ap_col.begin(), ap_col.end());
-        graph = adjacency_from_csr(n, ptr64.data(), col64.data(), ap_val.data());
+      d_ap_col = F->arena.i(std::max<int64_t>(1, nnz));
+      d_ap_val = F->arena.d(std::max<int64_t>(1, nnz));
+      upload(ctx->s, d_ap_ptr, C.ap_ptr.data(), sizeof(int64_t) * (n + 1));
+      if (nnz) {
+        upload(ctx->s, d_ap_col, C.ap_col.data(), sizeof(int) * nnz);
+        upload(ctx->s, d_ap_val, ap_val.data(), sizeof(double) * nnz);
       }
     }
+    mark_t("permute+graph");
     // ---- fronts in post order
     int64_t nn = (int64_t)et->parent.size();
     std::vector<int> pidx(nn, -1);
@@ -1899,6 +2013,7 @@ struct Factorizer {
       any_struct |= f.structured;
       max_nh = std::max<int64_t>(max_nh, f.nh);
     }
+    mark_t("fronts");
     if (any_struct) {
       if (!(P.eps > 0.0 && P.eps < 1.0)) throw value_error("eps must lie in (0, 1)");
       if (P.n_leaf < 1) throw value_error("n_leaf must be positive");
@@ -1924,6 +2039,7 @@ struct Factorizer {
       }
       upload(ctx->s, all, flat.data(), sizeof(int64_t) * tot);
     }
+    mark_t("identity+uploads");
     int max_flags = 0;
     for (auto &f : F->fronts) max_flags += 1 + (f.structured ? 8 * (int)(f.nh / std::max<int64_t>(1, P.n_leaf) + 2) : 0);
     flag_cap = max_flags + 16;
@@ -1933,6 +2049,29 @@ struct Factorizer {
     std::vector<std::vector<int>> byh(maxh + 1);
     for (size_t q = 0; q < F->fronts.size(); ++q)
       if (F->fronts[q].nh > 0) byh[F->fronts[q].height].push_back((int)q);
+    // structured-front plans (trees, blocks, BDLR selections) are symbolic: a
+    // planner thread computes them, in processing order, while the GPU works
+    {
+      int ntrees = 0, nblocks = 0;
+      plan_pos.assign(F->fronts.size(), -1);
+      for (int h = 0; h <= maxh; ++h)
+        for (int fi : byh[h]) {
+          FrontH &f = F->fronts[fi];
+          if (!f.structured) continue;
+          f.tree_base = ntrees;
+          ntrees += 2;
+          f.block_base = nblocks;
+          if (f.npv) nblocks += 2 * count_internal(f.npv, P.n_leaf);
+          if (f.npv && f.nf) nblocks += 2;
+          if (f.nf) nblocks += 2 * count_internal(f.nf, P.n_leaf);
+          plan_pos[fi] = (int)plan_order.size();
+          plan_order.push_back(fi);
+        }
+      F->trees.assign(ntrees, HTree{});
+      F->blocks.assign(nblocks, BlockH{});
+      if (!plan_order.empty()) start_planner();
+    }
+    mark_t("flags+plan");
     cudaEvent_t ev[8];
     for (auto &e : ev) CK(cudaEventCreate(&e));
     double tsum[7] = {0, 0, 0, 0, 0, 0, 0};
@@ -2102,6 +2241,7 @@ static void leaf_jobs(const HTree &T, const double *in, double *out, std::vector
 }
 
 static void build_apply(mfh_factor *F) {
+  auto tb0 = std::chrono::steady_clock::now();
   Ctx *ctx = F->ctx;
   auto AP = std::make_unique<ApplyPlan>();
   int64_t n = F->n;
@@ -2280,10 +2420,14 @@ static void build_apply(mfh_factor *F) {
   });
   // capture
   CK(cudaStreamSynchronize(ctx->s));
+  auto tb1 = std::chrono::steady_clock::now();
   CK(cudaStreamBeginCapture(ctx->s, cudaStreamCaptureModeThreadLocal));
   for (auto &op : sk.ops) op(ctx->s);
   CK(cudaStreamEndCapture(ctx->s, &AP->graph));
   CK(cudaGraphInstantiate(&AP->exec, AP->graph, 0));
+  auto tb2 = std::chrono::steady_clock::now();
+  F->timing.apply_build_ms = std::chrono::duration<double, std::milli>(tb1 - tb0).count();
+  F->timing.apply_instantiate_ms = std::chrono::duration<double, std::milli>(tb2 - tb1).count();
   AP->bytes = bytes;
   AP->nodes = (int64_t)sk.ops.size();
   F->apply = std::move(AP);
@@ -2648,10 +2792,13 @@ struct GmresRun {
     else
       host_op(ops->A_cb, ops->A_user, x, y);
   }
+  double m_ms = 0.0;
   void M(const double *x, double *y) {
-    if (ops->M)
+    auto t0 = std::chrono::steady_clock::now();
+    if (ops->M) {
       apply_device(ops->M, x, y);
-    else if (ops->M_cb)
+      m_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    } else if (ops->M_cb)
       host_op(ops->M_cb, ops->M_user, x, y);
     else
       CK(cudaMemcpyAsync(y, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s));
@@ -2804,7 +2951,12 @@ static int gmres_common(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const
   std::vector<double> res;
   int64_t its = 0;
   bool conv = false;
+  auto tg0 = std::chrono::steady_clock::now();
   g.run(d_b, d_x, tol, max_iter, restart, res, its, conv);
+  if (ops->M) {
+    ops->M->timing.gmres_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tg0).count();
+    ops->M->timing.gmres_apply_ms = g.m_ms;
+  }
   if (hist) std::memcpy(hist, res.data(), sizeof(double) * res.size());
   *n_hist = (int64_t)res.size();
   *iterations = its;

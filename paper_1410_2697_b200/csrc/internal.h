@@ -49,8 +49,20 @@ struct mfh_nd {
   std::vector<int64_t> post_order() const;
 };
 
+// Symbolic data derived from (pattern of A, permutation, zero pattern): the
+// permuted CSR pattern of P A P^T with a value-gather map, and the BDLR graph.
+struct mfh_symcache {
+  uint64_t key = 0;
+  bool valid = false;
+  std::vector<int64_t> ap_ptr, src;  // src[r]: position in A's CSR values of Ap entry r
+  std::vector<int> ap_col;
+  mfh::Graph graph;
+  bool has_graph = false;
+};
+
 // Elimination tree in the permuted numbering (ordering.py:211-261).
 struct mfh_etree {
+  mutable mfh_symcache cache;
   int64_t n = 0;
   int64_t root = -1;
   std::vector<int64_t> perm;

@@ -45,10 +45,14 @@ _PATHS = {0: "empty", 1: "dense", 2: "structured"}
 
 
 class FactorStats:
-    """Per-node records plus the deterministic counters (multifrontal.py:61-112)."""
+    """Per-node records plus the deterministic counters (multifrontal.py:61-112).
 
-    def __init__(self, st, records):
-        self.records = records
+    ``records`` is materialized lazily from the raw int64 table (one row per
+    node: node_id, front_size, n_pivot, path, max_offdiag_rank, stored_reals)."""
+
+    def __init__(self, st, table):
+        self._table = table
+        self._records = None
         self.peak_stored_reals = int(st.peak_stored_reals)
         self.retained_reals = int(st.retained_reals)
         self.structured_fronts = int(st.structured_fronts)
@@ -57,6 +61,13 @@ class FactorStats:
         self.n_blocks = int(st.n_blocks)
         self.n_dense_fallback = int(st.n_dense_fallback)
         self.device_bytes = int(st.device_bytes_peak)
+
+    @property
+    def records(self):
+        if self._records is None:
+            self._records = [FrontRecord(int(r[0]), int(r[1]), int(r[2]), _PATHS[int(r[3])], int(r[4]), int(r[5]))
+                             for r in self._table]
+        return self._records
 
     def to_csv(self, path):
         with open(path, "w", encoding="ascii") as fh:
@@ -80,12 +91,9 @@ class MfFactorization:
         L = _lib.lib()
         st = _lib.mfh_stats_t()
         _lib.check(L.mfh_factor_stats(handle, C.byref(st)))
-        recs = (_lib.mfh_record_t * max(1, st.n_records))()
-        _lib.check(L.mfh_factor_records(handle, recs))
-        records = [FrontRecord(int(r.node_id), int(r.front_size), int(r.n_pivot), _PATHS[int(r.path)],
-                               int(r.max_offdiag_rank), int(r.stored_reals))
-                   for r in recs[:st.n_records]]
-        self.stats = FactorStats(st, records)
+        table = np.empty((max(1, st.n_records), 6), dtype=np.int64)
+        _lib.check(L.mfh_factor_records(handle, _lib.ptr(table)))
+        self.stats = FactorStats(st, table[:st.n_records])
         self._stored = int(st.stored_reals)
         _lib.register(self)
 

@@ -185,6 +185,7 @@ struct Ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int cluster_size = 16;
   ChunkPool pool;
+  std::vector<cudaEvent_t> evpool;  // per-height phase events, reused
   Stage stage;
   Arena scratch;
   double *d_part = nullptr;  // reduction partials
@@ -374,12 +375,17 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
 
 static void run_check_finite(Sink &sk, const std::vector<LuJob> &jobs) {
   if (jobs.empty()) return;
-  LuJob *dj = sk.push(jobs);
-  int nb = (int)jobs.size();
-  sk.launch([=](cudaStream_t s) {
-    k_check_finite<<<nb, 256, 0, s>>>(dj);
-    check_launch();
-  });
+  int64_t mx = 1;
+  for (auto &j : jobs) mx = std::max<int64_t>(mx, (int64_t)j.n * j.n);
+  for (size_t b = 0; b < jobs.size(); b += 60000) {
+    std::vector<LuJob> part(jobs.begin() + b, jobs.begin() + std::min(jobs.size(), b + 60000));
+    LuJob *dj = sk.push(part);
+    dim3 grid((unsigned)std::min<int64_t>(cdiv(mx, 1024), 64), (unsigned)part.size());
+    sk.launch([=](cudaStream_t s) {
+      k_check_finite<<<grid, 256, 0, s>>>(dj);
+      check_launch();
+    });
+  }
 }
 
 static void run_getrs(Sink &sk, const std::vector<RsJob> &jobs) {
@@ -2072,8 +2078,6 @@ struct Factorizer {
       if (!plan_order.empty()) start_planner();
     }
     mark_t("flags+plan");
-    cudaEvent_t ev[8];
-    for (auto &e : ev) CK(cudaEventCreate(&e));
     double tsum[7] = {0, 0, 0, 0, 0, 0, 0};
     auto host_done = std::chrono::steady_clock::now();
     F->timing.host_ms += std::chrono::duration<double, std::milli>(host_done - t0).count();
@@ -2082,15 +2086,45 @@ struct Factorizer {
     CK(cudaEventCreate(&e_begin));
     CK(cudaEventCreate(&e_end));
     CK(cudaEventRecord(e_begin, ctx->s));
+    // Heights are enqueued back to back: the host only waits where it needs
+    // device data (the rank readback inside structured heights) or to recycle
+    // scratch memory; per-height phase events are evaluated at the end.
+    int used = 0;
     for (int h = 0; h <= maxh; ++h) {
       if (byh[h].empty()) continue;
-      for (auto &e : ev) CK(cudaEventRecord(e, ctx->s));
+      while ((int)ctx->evpool.size() < 8 * (used + 1)) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        ctx->evpool.push_back(e);
+      }
+      cudaEvent_t *ev = ctx->evpool.data() + 8 * used;
+      ++used;
+      for (int q = 0; q < 8; ++q) CK(cudaEventRecord(ev[q], ctx->s));
       process_height(byh[h], ev);
-      Sink s{ctx};
+      bool has_struct = false;
+      for (int fi : byh[h]) has_struct |= F->fronts[fi].structured;
+      if (has_struct || ctx->scratch.in_use > (size_t(4) << 30)) {
+        Sink s{ctx};
+        auto tw = std::chrono::steady_clock::now();
+        s.sync_reset();
+        F->timing.host_sync_wait_ms +=
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw).count();
+        check_flags(0);
+        ctx->scratch.reset();
+      }
+    }
+    CK(cudaEventRecord(e_end, ctx->s));
+    {
       auto tw = std::chrono::steady_clock::now();
-      s.sync_reset();
+      CK(cudaStreamSynchronize(ctx->s));
       F->timing.host_sync_wait_ms +=
           std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw).count();
+    }
+    ctx->stage.rewind();
+    check_flags(0);
+    ctx->scratch.reset();
+    for (int u = 0; u < used; ++u) {
+      cudaEvent_t *ev = ctx->evpool.data() + 8 * u;
       float ms;
       CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
       tsum[0] += ms;
@@ -2104,14 +2138,9 @@ struct Factorizer {
       tsum[3] += ms;
       CK(cudaEventElapsedTime(&ms, ev[6], ev[7]));
       tsum[5] += ms;
-      check_flags(0);
-      ctx->scratch.reset();
     }
-    CK(cudaEventRecord(e_end, ctx->s));
-    CK(cudaStreamSynchronize(ctx->s));
     float tot;
     CK(cudaEventElapsedTime(&tot, e_begin, e_end));
-    for (auto &e : ev) cudaEventDestroy(e);
     cudaEventDestroy(e_begin);
     cudaEventDestroy(e_end);
     F->timing.sample_ms = tsum[0];
@@ -2521,6 +2550,7 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   ctx->c.stage.release();
   ctx->c.scratch.release();
   ctx->c.pool.release();
+  for (auto e : ctx->c.evpool) cudaEventDestroy(e);
   cudaFree(ctx->c.d_part);
   cudaFree(ctx->c.d_scal);
   cudaStreamSynchronize(ctx->c.side);

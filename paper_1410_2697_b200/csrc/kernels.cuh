@@ -1188,41 +1188,65 @@ struct TrinvJob {
   int ldt, w, upper;
   double *out;
 };
-constexpr size_t TRINV_SMEM = sizeof(double) * (64 * 64 + 64 * 65);
-// 256 threads: column j = tid / 4, slice s = tid % 4 (the 4 slices of a column
-// sit in one warp); row-by-row substitution, each dot product split 4 ways
+constexpr size_t TRINV_SMEM = sizeof(double) * (64 * 64 + 2 * 64 * 65);
+// Triangular inverse by recursive doubling: with the inverses of the two s x s
+// diagonal blocks known, the 2s x 2s inverse only needs its off-diagonal block:
+//   lower [[A,0],[C,B]]^-1 = [[Ai,0],[-Bi C Ai, Bi]]
+//   upper [[A,C],[0,B]]^-1 = [[Ai,-Ai C Bi],[0,Bi]]
+// All pairs of a stage are formed in parallel (log2(64) = 6 stages of small
+// shared-memory GEMMs, instead of 64 dependent substitution rows).
 __global__ void __launch_bounds__(256) k_trinv(const TrinvJob *__restrict__ jobs) {
   extern __shared__ double tdyn[];
-  double *Ts = tdyn;
-  double *X = tdyn + 64 * 64;
+  double *Ts = tdyn;              // w x w (ld w)
+  double *X = tdyn + 64 * 64;     // inverse, ld 65
+  double *Tm = X + 64 * 65;       // temporary, ld 65
   const TrinvJob J = jobs[blockIdx.x];
-  const int w = J.w, tid = threadIdx.x;
-  const int j = tid >> 2, sl = tid & 3;
-  for (int e = tid; e < w * w; e += blockDim.x) Ts[e] = J.T[(long long)(e / w) * J.ldt + (e % w)];
-  __syncthreads();
-  if (!J.upper) {
-    for (int i = 0; i < w; ++i) {
-      double acc = 0.0;
-      if (j < w && i > j)
-        for (int k = j + sl; k < i; k += 4) acc = fma(-Ts[i * w + k], X[k * 65 + j], acc);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      if (j < w && sl == 0) X[i * 65 + j] = (i < j) ? 0.0 : (i == j ? 1.0 : acc);
-      __syncwarp();
-    }
-  } else {
-    for (int i = w - 1; i >= 0; --i) {
-      double acc = 0.0;
-      if (j < w && i < j)
-        for (int k = i + 1 + sl; k <= j; k += 4) acc = fma(Ts[i * w + k], X[k * 65 + j], acc);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      if (j < w && sl == 0) X[i * 65 + j] = (i > j) ? 0.0 : (i == j ? 1.0 / Ts[j * w + j] : -acc / Ts[i * w + i]);
-      __syncwarp();
-    }
+  const int w = J.w, tid = threadIdx.x, nt = blockDim.x;
+  const bool up = J.upper != 0;
+  for (int e = tid; e < w * w; e += nt) {
+    int i = e / w, j = e % w;
+    double t = J.T[(long long)i * J.ldt + j];
+    Ts[e] = t;
+    X[i * 65 + j] = (i == j) ? (up ? 1.0 / t : 1.0) : 0.0;
   }
   __syncthreads();
-  for (int e = tid; e < w * w; e += blockDim.x) J.out[e] = X[(e / w) * 65 + (e % w)];
+  for (int sz = 1; sz < w; sz <<= 1) {
+    const int npair = (w + 2 * sz - 1) / (2 * sz);
+    // Tm = C * Bi (upper) or C * Ai (lower) for every pair; C is |B| x s (lower) or s x |B| (upper)
+    for (int e = tid; e < npair * sz * sz; e += nt) {
+      int p = e / (sz * sz), r = (e / sz) % sz, c = e % sz;
+      int k0 = p * 2 * sz, k1 = k0 + sz, nb = min(sz, w - k1);
+      if (nb <= 0) continue;
+      double acc = 0.0;
+      if (!up) {  // rows of B (r < nb), cols of A (c)
+        if (r >= nb) continue;
+        for (int t = 0; t < sz; ++t) acc = fma(Ts[(k1 + r) * w + k0 + t], X[(k0 + t) * 65 + k0 + c], acc);
+        Tm[(k1 + r) * 65 + k0 + c] = acc;
+      } else {    // rows of A (r), cols of B (c < nb)
+        if (c >= nb) continue;
+        for (int t = 0; t < nb; ++t) acc = fma(Ts[(k0 + r) * w + k1 + t], X[(k1 + t) * 65 + k1 + c], acc);
+        Tm[(k0 + r) * 65 + k1 + c] = acc;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < npair * sz * sz; e += nt) {
+      int p = e / (sz * sz), r = (e / sz) % sz, c = e % sz;
+      int k0 = p * 2 * sz, k1 = k0 + sz, nb = min(sz, w - k1);
+      if (nb <= 0) continue;
+      double acc = 0.0;
+      if (!up) {  // X[B rows, A cols] = -Bi * Tm
+        if (r >= nb) continue;
+        for (int t = 0; t < nb; ++t) acc = fma(X[(k1 + r) * 65 + k1 + t], Tm[(k1 + t) * 65 + k0 + c], acc);
+        X[(k1 + r) * 65 + k0 + c] = -acc;
+      } else {    // X[A rows, B cols] = -Ai * Tm
+        if (c >= nb) continue;
+        for (int t = 0; t < sz; ++t) acc = fma(X[(k0 + r) * 65 + k0 + t], Tm[(k0 + t) * 65 + k1 + c], acc);
+        X[(k0 + r) * 65 + k1 + c] = -acc;
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < w * w; e += nt) J.out[e] = X[(e / w) * 65 + (e % w)];
 }
 
 // diagonal check after a blocked LU
@@ -1241,12 +1265,13 @@ __global__ void k_diag_check(const LuJob *__restrict__ jobs) {
 
 // non-finite scan of a square block (hodlr.py:346 check before the core LU)
 __global__ void k_check_finite(const LuJob *__restrict__ jobs) {
-  const LuJob J = jobs[blockIdx.x];
+  const LuJob J = jobs[blockIdx.y];
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
   long long total = (long long)J.n * J.n;
-  for (long long e = threadIdx.x; e < total; e += blockDim.x) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
     int i = (int)(e / J.n), j = (int)(e % J.n);
     if (!isfinite(J.a[(long long)i * J.lda + j])) bad = 1;
   }

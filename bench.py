@@ -73,28 +73,39 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region, in-process
+    through NVML (spawning nvidia-smi every 200 ms perturbs the sync-heavy GMRES
+    loop by tens of milliseconds)."""
 
-    def __init__(self, index=0):
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
+
+    def __init__(self, index=0, period=0.2):
         self.index = index
+        self.period = period
         self.samples = []
         self._stop = threading.Event()
         self._t = None
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            return self
+
         def run():
-            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap")
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True,
-                                         text=True, timeout=5).stdout.strip()
-                    self.samples.append([x.strip() for x in out.split(",")])
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((sm, mx, rs))
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(self.period)
+
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
         return self
@@ -107,13 +118,10 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace('.', '').isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace('.', '').isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples if len(s) >= 6 for k in range(4)
-                          if s[2 + k].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        reasons = sorted({name for _, _, rs in self.samples for bit, name in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": float(np.median([s[0] for s in self.samples])),
+                "sm_max_mhz": float(max(s[1] for s in self.samples)), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml"}
 
 
 def dist_setup(n_gpus):
@@ -244,7 +252,8 @@ def run_gpu_arm(args, cfg, world, rank, local):
     dev_op = A.device_operator()
     hist = np.empty(4000)
 
-    split = {"factor_s": [], "solve_s": [], "gmres_inner_s": [], "apply_build_s": []}
+    split = {"factor_s": [], "solve_s": [], "gmres_inner_s": [], "apply_build_s": [], "gmres_sync_s": [],
+             "gmres_apply_enqueue_s": []}
 
     def step_device():
         t0 = time.perf_counter()
@@ -263,6 +272,8 @@ def run_gpu_arm(args, cfg, world, rank, local):
         split["solve_s"].append(t2 - t1)
         split["gmres_inner_s"].append(ti["gmres_ms"] / 1e3)
         split["apply_build_s"].append((ti["apply_build_ms"] + ti["apply_instantiate_ms"]) / 1e3)
+        split["gmres_sync_s"].append(ti["gmres_sync_ms"] / 1e3)
+        split["gmres_apply_enqueue_s"].append(ti["gmres_apply_ms"] / 1e3)
         return F, its.value, bool(conv.value), hist[max(0, nh.value - 1)]
 
     def step_e2e():  # public API, host b -> host x
@@ -295,7 +306,9 @@ def run_gpu_arm(args, cfg, world, rank, local):
             times.append(e0.elapsed_time(e1) / 1e3)
         launches = (ctx.info()[1] - launches0) / max(1, args.steps)
         split = {k: float(np.mean(v[-args.steps:])) for k, v in split.items()}
+        Fe = None
         for _ in range(max(1, min(args.steps, 3))):
+            Fe = None  # the previous factorization is released before the next step
             flush.fill_(1)
             torch.cuda.synchronize()
             barrier(world)

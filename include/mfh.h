@@ -73,7 +73,7 @@ typedef struct {
   double host_ms;        /* host work before the first launch + BDLR selection */
   double host_preamble_ms, host_select_ms, host_sync_wait_ms, wall_ms;
   double apply_build_ms, apply_instantiate_ms; /* first-use CUDA-graph construction */
-  double gmres_ms, gmres_apply_ms;             /* last GMRES using this factor (host clock) */
+  double gmres_ms, gmres_apply_ms, gmres_sync_ms; /* last GMRES using this factor (host clock) */
   int64_t kernel_launches;
   double pivot_lu_visits; /* algorithmic trailing-entry visits */
   double sample_entries;

@@ -48,7 +48,7 @@ class mfh_timing_t(C.Structure):
                 ("host_ms", C.c_double), ("host_preamble_ms", C.c_double),
                 ("host_select_ms", C.c_double), ("host_sync_wait_ms", C.c_double), ("wall_ms", C.c_double),
                 ("apply_build_ms", C.c_double), ("apply_instantiate_ms", C.c_double),
-                ("gmres_ms", C.c_double), ("gmres_apply_ms", C.c_double),
+                ("gmres_ms", C.c_double), ("gmres_apply_ms", C.c_double), ("gmres_sync_ms", C.c_double),
                 ("kernel_launches", C.c_int64),
                 ("pivot_lu_visits", C.c_double), ("sample_entries", C.c_double)]
 

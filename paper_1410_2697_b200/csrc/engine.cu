@@ -833,6 +833,8 @@ struct FrontH {
   int *piv = nullptr;
   // apply operators (explicit inverse form, computed once at factor time)
   double *Pinv = nullptr, *Gfp = nullptr, *Gpf = nullptr;
+  // structured: Hinv = (HODLR pivot block)^{-1}, Xp = Hinv col_pf, RH = row_fp Hinv
+  double *Hinv = nullptr, *Xp = nullptr, *RH = nullptr;
   // structured path
   int pp = -1, ff = -1, pf = -1, fp = -1;  // tree / block ids
   int tree_base = -1, block_base = -1;      // pre-assigned plan slots
@@ -880,98 +882,6 @@ struct mfh_factor {
 };
 
 namespace mfh {
-
-// ---------------------------------------------------------------------------
-// HODLR level-batched multi-RHS solve (hodlr.py:360-383)
-// ---------------------------------------------------------------------------
-struct HProblem {
-  const HTree *t;
-  int root;  // heap slot of the subtree root
-  double *rhs;
-  int ld, k;
-};
-
-static void collect_subtree(const HTree &t, int root, std::vector<int> &out) {
-  std::vector<int> st{root};
-  while (!st.empty()) {
-    int v = st.back();
-    st.pop_back();
-    out.push_back(v);
-    if (!t.leaf[v]) {
-      st.push_back(2 * v + 2);
-      st.push_back(2 * v + 1);
-    }
-  }
-}
-
-static void hodlr_solve_batched(Sink &sk, const std::vector<HProblem> &probs) {
-  if (probs.empty()) return;
-  std::vector<GemmJob> leaves;
-  std::vector<CopyJob> leaf_copies;
-  struct Item {
-    int p, v;
-  };
-  std::vector<std::vector<Item>> bydepth;
-  for (int p = 0; p < (int)probs.size(); ++p) {
-    const HProblem &P = probs[p];
-    if (P.k == 0) continue;
-    std::vector<int> nodes;
-    collect_subtree(*P.t, P.root, nodes);
-    int base_lo = P.t->lo[P.root];
-    for (int v : nodes) {
-      if (P.t->leaf[v]) {
-        int sz = P.t->hi[v] - P.t->lo[v];
-        if (sz == 0) continue;
-        double *b = P.rhs + (int64_t)(P.t->lo[v] - base_lo) * P.ld;
-        // z_leaf = leaf^{-1} b_leaf; in place when the leaf fits one GEMM row tile
-        if (sz <= GEMM_BM) {
-          leaves.push_back(GemmJob{P.t->linv[v], b, b, sz, P.k, sz, sz, P.ld, P.ld, 1.0, 0.0});
-        } else {
-          double *tmp = sk.scratch_d((size_t)sz * P.k);
-          leaf_copies.push_back(CopyJob{b, tmp, sz, P.k, P.ld, P.k, nullptr, nullptr});
-          leaves.push_back(GemmJob{P.t->linv[v], tmp, b, sz, P.k, sz, sz, P.k, P.ld, 1.0, 0.0});
-        }
-      } else {
-        int d = P.t->depth[v];
-        if ((int)bydepth.size() <= d) bydepth.resize(d + 1);
-        bydepth[d].push_back({p, v});
-      }
-    }
-  }
-  run_copy(sk, leaf_copies);
-  run_gemm(sk, leaves);
-  for (int d = (int)bydepth.size() - 1; d >= 0; --d) {
-    auto &items = bydepth[d];
-    if (items.empty()) continue;
-    std::vector<GemmJob> g1, g2, g3;
-    for (auto &it : items) {
-      const HProblem &P = probs[it.p];
-      const HTree &t = *P.t;
-      int v = it.v;
-      int r1 = t.r1[v], r2 = t.r2[v];
-      if (r1 + r2 == 0) continue;
-      int base_lo = t.lo[P.root];
-      int lo = t.lo[v], hi = t.hi[v], mid = (lo + hi) >> 1;
-      double *zt = P.rhs + (int64_t)(lo - base_lo) * P.ld;
-      double *zb = P.rhs + (int64_t)(mid - base_lo) * P.ld;
-      double *w = sk.scratch_d((size_t)(r1 + r2) * P.k);
-      double *y = sk.scratch_d((size_t)(r1 + r2) * P.k);
-      // w_top = row_top @ z_bot ; w_bot = row_bot @ z_top
-      if (r1) g1.push_back(GemmJob{t.f1[v].row, zb, w, r1, P.k, hi - mid, t.f1[v].ldr, P.ld, P.k, 1.0, 0.0});
-      if (r2)
-        g1.push_back(GemmJob{t.f2[v].row, zt, w + (int64_t)r1 * P.k, r2, P.k, mid - lo, t.f2[v].ldr,
-                             P.ld, P.k, 1.0, 0.0});
-      // y = core^{-1} w
-      g2.push_back(GemmJob{t.cinv[v], w, y, r1 + r2, P.k, r1 + r2, r1 + r2, P.k, P.k, 1.0, 0.0});
-      if (r1) g3.push_back(GemmJob{t.xt[v], y, zt, mid - lo, P.k, r1, r1, P.k, P.ld, -1.0, 1.0});
-      if (r2)
-        g3.push_back(GemmJob{t.xb[v], y + (int64_t)r1 * P.k, zb, hi - mid, P.k, r2, r2, P.k, P.ld, -1.0, 1.0});
-    }
-    run_gemm(sk, g1);
-    run_gemm(sk, g2);
-    run_gemm(sk, g3);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // the factorization driver
@@ -1638,144 +1548,217 @@ struct Factorizer {
     }
 
     // ------------------------------------------------ HODLR factorization of pp
-    std::vector<int> ptrees;
-    for (int fi : S)
-      if (F->fronts[fi].pp >= 0) ptrees.push_back(F->fronts[fi].pp);
+    // hodlr_factorize (hodlr.py:312-357) in explicit-inverse form, one launch
+    // group per stage of a tree level, batched over every front of the height:
+    //   H_v = diag(H_L, H_R) + P Q,  P = diag(col1, col2),  Q = [[0, row1], [row2, 0]]
+    //   core = I + Q D^{-1} P = [[I, row1 x_bot], [row2 x_top, I]]  (the reference's core)
+    //   H_v^{-1} = D^{-1} - (D^{-1} P) core^{-1} (Q D^{-1})
+    // When a pivot-block HODLR is effectively dense (dense-fallback blocks
+    // everywhere, so its Woodbury cores are as large as the blocks), its exact
+    // inverse is cheaper as ONE dense blocked inversion of the assembled
+    // compressed matrix than as a chain of large core inversions: same
+    // compressed operator, exact either way. Per-tree choice by a cost model.
+    std::vector<int> ptrees, dtrees;
+    for (int fi : S) {
+      FrontH &f = F->fronts[fi];
+      if (f.pp < 0) continue;
+      HTree &T = F->trees[f.pp];
+      double core3 = 0.0;
+      for (int v = 0; v < T.nslots; ++v)
+        if (T.leaf[v] == 0) {
+          double rr = (double)F->blocks[T.up[v]].erank() + F->blocks[T.lw[v]].erank();
+          core3 += rr * rr * rr;
+        }
+      double N = (double)f.npv;
+      (core3 >= 0.3 * N * N * N && f.npv > INV_SMALL ? dtrees : ptrees).push_back(f.pp);
+    }
     {
-      // leaves: explicit inverses in place (hodlr.py:322-330 incl. the singular check)
-      std::vector<InvReq> leaves;
-      for (int tt : ptrees) {
+      std::vector<CopyJob> lc;
+      std::vector<InvReq> leaves, dense_inv;
+      std::vector<GemmJob> dense_lr;
+      for (int tt : dtrees) {
         HTree &T = F->trees[tt];
-        for (int v = 0; v < T.nslots; ++v)
+        FrontH &f = F->fronts[T.fi];
+        const int N = f.npv;
+        f.Hinv = F->arena.d((size_t)N * N);
+        double *Hd = ctx->scratch.d((size_t)N * N);
+        for (int v = 0; v < T.nslots; ++v) {
           if (T.leaf[v] == 1) {
-            int sz = T.hi[v] - T.lo[v];
+            int lo = T.lo[v], sz = T.hi[v] - T.lo[v];
+            lc.push_back(CopyJob{T.lval[v], Hd + (int64_t)lo * N + lo, sz, sz, sz, N, nullptr, nullptr});
+            // the reference's leaf singularity check (hodlr.py:325-328), flag only
             std::string msg = "singular pivot in leaf block [" + std::to_string(T.lo[v]) + ", " +
                               std::to_string(T.hi[v]) + ")";
             T.lflag[v] = new_flag(msg, (int64_t)T.fi * 1000000 + v);
-            if (sz > INV_SMALL) {
-              T.lpiv[v] = F->arena.i(sz);
-              T.linv[v] = F->arena.d((size_t)sz * sz);
-            } else {
-              T.linv[v] = T.lval[v];
+            if (sz <= INV_SMALL) {
+              double *chk = ctx->scratch.d((size_t)sz * sz);
+              lc.push_back(CopyJob{T.lval[v], chk, sz, sz, sz, sz, nullptr, nullptr});
+              leaves.push_back(InvReq{chk, sz, sz, chk, sz, nullptr, d_flags + T.lflag[v]});
             }
-            leaves.push_back(InvReq{T.lval[v], sz, sz, T.linv[v], sz, T.lpiv[v], d_flags + T.lflag[v]});
+          } else if (T.leaf[v] == 0) {
+            FacView f1 = as_factors(F->blocks[T.up[v]]), f2 = as_factors(F->blocks[T.lw[v]]);
+            T.f1[v] = f1;
+            T.f2[v] = f2;
+            T.r1[v] = f1.rank;
+            T.r2[v] = f2.rank;
+            const int lo = T.lo[v], hi = T.hi[v], mid = (lo + hi) >> 1;
+            for (int side = 0; side < 2; ++side) {
+              const BlockH &b = F->blocks[side == 0 ? T.up[v] : T.lw[v]];
+              double *dst = Hd + (side == 0 ? (int64_t)lo * N + mid : (int64_t)mid * N + lo);
+              if (b.dense)
+                lc.push_back(CopyJob{b.val, dst, b.m, b.n, b.n, N, nullptr, nullptr});
+              else  // rank 0 writes zeros (k = 0)
+                dense_lr.push_back(GemmJob{b.col, b.row, dst, b.m, b.n, b.rank, std::max(1, b.rank), b.n, N, 1.0, 0.0});
+            }
+          }
+        }
+        int fl = new_flag("singular coupling core at node [0, " + std::to_string(N) + ")", (int64_t)T.fi * 1000000);
+        dense_inv.push_back(InvReq{Hd, N, N, f.Hinv, N, ctx->scratch.i(N), d_flags + fl});
+      }
+      run_copy(s, lc);
+      lc.clear();
+      run_gemm(s, dense_lr);
+      run_inverse(s, dense_inv);
+
+      for (int tt : ptrees) {
+        HTree &T = F->trees[tt];
+        FrontH &f = F->fronts[T.fi];
+        const int N = f.npv;
+        f.Hinv = F->arena.d((size_t)N * N);
+        CK(cudaMemsetAsync(f.Hinv, 0, sizeof(double) * (size_t)N * N, ctx->s));
+        for (int v = 0; v < T.nslots; ++v)
+          if (T.leaf[v] == 1) {
+            int lo = T.lo[v], sz = T.hi[v] - T.lo[v];
+            double *blk = f.Hinv + (int64_t)lo * N + lo;
+            std::string msg = "singular pivot in leaf block [" + std::to_string(T.lo[v]) + ", " +
+                              std::to_string(T.hi[v]) + ")";
+            T.lflag[v] = new_flag(msg, (int64_t)T.fi * 1000000 + v);
+            if (sz <= INV_SMALL) {
+              lc.push_back(CopyJob{T.lval[v], blk, sz, sz, sz, N, nullptr, nullptr});
+              leaves.push_back(InvReq{blk, sz, N, blk, N, nullptr, d_flags + T.lflag[v]});
+            } else {
+              T.lpiv[v] = F->arena.i(sz);
+              leaves.push_back(InvReq{T.lval[v], sz, sz, blk, N, T.lpiv[v], d_flags + T.lflag[v]});
+            }
           }
       }
+      run_copy(s, lc);
       run_inverse(s, leaves);
       int maxd = 0;
       for (int tt : ptrees) maxd = std::max(maxd, F->trees[tt].maxdepth);
       for (int d = maxd; d >= 0; --d) {
-        std::vector<CopyJob> cps;
-        std::vector<HProblem> probs;
-        std::vector<std::pair<int, int>> nodes;
+        struct Nd {
+          HTree *T;
+          int v;
+          double *xt, *xb, *yt, *yb, *Tm;
+        };
+        std::vector<Nd> nodes;
+        std::vector<GemmJob> ga, gc, gd, ge;
+        std::vector<double *> ip;
+        std::vector<int> idim, ild;
+        std::vector<LuJob> fin;
+        std::vector<InvReq> invs;
         for (int tt : ptrees) {
           HTree &T = F->trees[tt];
+          FrontH &f = F->fronts[T.fi];
+          const int N = f.npv;
           for (int v = 0; v < T.nslots; ++v) {
             if (T.leaf[v] != 0 || T.depth[v] != d) continue;
-            nodes.push_back({tt, v});
             FacView f1 = as_factors(F->blocks[T.up[v]]);
             FacView f2 = as_factors(F->blocks[T.lw[v]]);
             T.f1[v] = f1;
             T.f2[v] = f2;
-            int lo = T.lo[v], hi = T.hi[v], mid = (lo + hi) >> 1;
-            int m1 = mid - lo, m2 = hi - mid;
-            T.r1[v] = f1.rank;
-            T.r2[v] = f2.rank;
-            T.xt[v] = F->arena.d((size_t)m1 * std::max(1, f1.rank));
-            T.xb[v] = F->arena.d((size_t)m2 * std::max(1, f2.rank));
-            // x_top = H1^{-1} col1, x_bot = H2^{-1} col2 (hodlr.py:333-338)
-            if (f1.rank) {
-              cps.push_back(CopyJob{f1.col, T.xt[v], m1, f1.rank, f1.ldc, f1.rank, nullptr, nullptr});
-              probs.push_back(HProblem{&T, 2 * v + 1, T.xt[v], f1.rank, f1.rank});
+            const int lo = T.lo[v], hi = T.hi[v], mid = (lo + hi) >> 1;
+            const int m1 = mid - lo, m2 = hi - mid, nv = hi - lo;
+            const int r1 = f1.rank, r2 = f2.rank, rr = r1 + r2;
+            T.r1[v] = r1;
+            T.r2[v] = r2;
+            if (rr == 0) continue;
+            double *HLL = f.Hinv + (int64_t)lo * N + lo, *HRR = f.Hinv + (int64_t)mid * N + mid;
+            Nd nd{&T, v, nullptr, nullptr, nullptr, nullptr, nullptr};
+            nd.xt = ctx->scratch.d((size_t)m1 * std::max(1, r1));
+            nd.xb = ctx->scratch.d((size_t)m2 * std::max(1, r2));
+            nd.yt = ctx->scratch.d((size_t)std::max(1, r1) * m2);
+            nd.yb = ctx->scratch.d((size_t)std::max(1, r2) * m1);
+            nd.Tm = ctx->scratch.d((size_t)rr * nv);
+            // (a) x_top = H_L^{-1} col1, x_bot = H_R^{-1} col2, y_top = row1 H_R^{-1}, y_bot = row2 H_L^{-1}
+            if (r1) {
+              ga.push_back(GemmJob{HLL, f1.col, nd.xt, m1, r1, m1, N, f1.ldc, r1, 1.0, 0.0});
+              ga.push_back(GemmJob{f1.row, HRR, nd.yt, r1, m2, m2, f1.ldr, N, m2, 1.0, 0.0});
             }
-            if (f2.rank) {
-              cps.push_back(CopyJob{f2.col, T.xb[v], m2, f2.rank, f2.ldc, f2.rank, nullptr, nullptr});
-              probs.push_back(HProblem{&T, 2 * v + 2, T.xb[v], f2.rank, f2.rank});
+            if (r2) {
+              ga.push_back(GemmJob{HRR, f2.col, nd.xb, m2, r2, m2, N, f2.ldc, r2, 1.0, 0.0});
+              ga.push_back(GemmJob{f2.row, HLL, nd.yb, r2, m1, m1, f2.ldr, N, m1, 1.0, 0.0});
             }
+            // (b) Woodbury core (hodlr.py:343-345) and its inverse (346-352 checks)
+            T.core[v] = F->arena.d((size_t)rr * rr);
+            ip.push_back(T.core[v]);
+            idim.push_back(rr);
+            ild.push_back(rr);
+            if (r1 && r2) {
+              gc.push_back(GemmJob{f1.row, nd.xb, T.core[v] + r1, r1, r2, m2, f1.ldr, r2, rr, 1.0, 1.0});
+              gc.push_back(GemmJob{f2.row, nd.xt, T.core[v] + (int64_t)r1 * rr, r2, r1, m1, f2.ldr, r1, rr, 1.0, 1.0});
+            }
+            std::string msg = "singular coupling core at node [" + std::to_string(lo) + ", " + std::to_string(hi) + ")";
+            int fl = new_flag(msg, (int64_t)T.fi * 1000000 + v);
+            fin.push_back(LuJob{T.core[v], rr, rr, nullptr, d_flags + fl});
+            if (rr > INV_SMALL) {
+              T.cpiv[v] = ctx->scratch.i(rr);
+              T.cinv[v] = ctx->scratch.d((size_t)rr * rr);
+            } else {
+              T.cinv[v] = T.core[v];
+            }
+            invs.push_back(InvReq{T.core[v], rr, rr, T.cinv[v], rr, T.cpiv[v], d_flags + fl});
+            // (d) Tm = core^{-1} [[0, y_top], [y_bot, 0]]  (rr x nv)
+            gd.push_back(GemmJob{T.cinv[v] + r1, nd.yb, nd.Tm, rr, m1, r2, rr, m1, nv, 1.0, 0.0});
+            gd.push_back(GemmJob{T.cinv[v], nd.yt, nd.Tm + m1, rr, m2, r1, rr, m2, nv, 1.0, 0.0});
+            // (e) H_v^{-1} rows L -= x_top Tm[:r1, :], rows R -= x_bot Tm[r1:, :]
+            if (r1) ge.push_back(GemmJob{nd.xt, nd.Tm, HLL, m1, nv, r1, r1, nv, N, -1.0, 1.0});
+            if (r2)
+              ge.push_back(GemmJob{nd.xb, nd.Tm + (int64_t)r1 * nv, f.Hinv + (int64_t)mid * N + lo, m2, nv, r2, r2, nv, N,
+                                   -1.0, 1.0});
+            nodes.push_back(nd);
           }
         }
         if (nodes.empty()) continue;
-        run_copy(s, cps);
-        hodlr_solve_batched(s, probs);
-        // Woodbury cores I + [[0, R1 x_bot], [R2 x_top, 0]] and their inverses (hodlr.py:341-352)
-        std::vector<double *> ip;
-        std::vector<int> idim, ild;
-        std::vector<GemmJob> gms;
-        std::vector<LuJob> fin;
-        std::vector<InvReq> invs;
-        for (auto &nv : nodes) {
-          HTree &T = F->trees[nv.first];
-          int v = nv.second;
-          int r1 = T.r1[v], r2 = T.r2[v];
-          if (r1 + r2 == 0) continue;
-          int lo = T.lo[v], hi = T.hi[v], mid = (lo + hi) >> 1;
-          int rr = r1 + r2;
-          T.core[v] = F->arena.d((size_t)rr * rr);
-          ip.push_back(T.core[v]);
-          idim.push_back(rr);
-          ild.push_back(rr);
-          if (r1 && r2) {
-            gms.push_back(GemmJob{T.f1[v].row, T.xb[v], T.core[v] + r1, r1, r2, hi - mid, T.f1[v].ldr, r2, rr,
-                                  1.0, 1.0});
-            gms.push_back(GemmJob{T.f2[v].row, T.xt[v], T.core[v] + (int64_t)r1 * rr, r2, r1, mid - lo,
-                                  T.f2[v].ldr, r1, rr, 1.0, 1.0});
-          }
-          std::string msg = "singular coupling core at node [" + std::to_string(lo) + ", " +
-                            std::to_string(hi) + ")";
-          int fl = new_flag(msg, (int64_t)T.fi * 1000000 + v);
-          fin.push_back(LuJob{T.core[v], rr, rr, nullptr, d_flags + fl});
-          if (rr > INV_SMALL) {
-            T.cpiv[v] = F->arena.i(rr);
-            T.cinv[v] = F->arena.d((size_t)rr * rr);
-          } else {
-            T.cinv[v] = T.core[v];
-          }
-          invs.push_back(InvReq{T.core[v], rr, rr, T.cinv[v], rr, T.cpiv[v], d_flags + fl});
-        }
+        run_gemm(s, ga);
         run_identity(s, ip, idim, ild);
-        run_gemm(s, gms);
+        run_gemm(s, gc);
         run_check_finite(s, fin);
         run_inverse(s, invs);
+        run_gemm(s, gd);
+        run_gemm(s, ge);
       }
     }
     cudaEventRecord(ev[6], ctx->s);
 
-    // ------------------------------------------------ eliminate_hodlr (W, V)
+    // ------------------------------------------------ eliminate_hodlr (W, V)  (multifrontal.py:411-456)
     {
-      std::vector<CopyJob> cps;
-      std::vector<HProblem> probs;
+      std::vector<GemmJob> g0, g1, g2;
       struct El {
         int fi;
         FacView pf, fp;
-        double *x;
       };
       std::vector<El> els;
       for (int fi : S) {
         FrontH &f = F->fronts[fi];
         if (!(f.npv && f.nf)) continue;
-        El e;
-        e.fi = fi;
-        e.pf = as_factors(F->blocks[f.pf]);
-        e.fp = as_factors(F->blocks[f.fp]);
-        e.x = ctx->scratch.d((size_t)f.npv * std::max(1, e.pf.rank));
-        if (e.pf.rank) {
-          cps.push_back(CopyJob{e.pf.col, e.x, f.npv, e.pf.rank, e.pf.ldc, e.pf.rank, nullptr, nullptr});
-          probs.push_back(HProblem{&F->trees[f.pp], 0, e.x, e.pf.rank, e.pf.rank});
-        }
+        El e{fi, as_factors(F->blocks[f.pf]), as_factors(F->blocks[f.fp])};
+        const int N = f.npv;
+        // x = H^{-1} col_pf (retained for the apply), RH = row_fp H^{-1} (apply)
+        f.Xp = F->arena.d((size_t)N * std::max(1, e.pf.rank));
+        f.RH = F->arena.d((size_t)std::max(1, e.fp.rank) * N);
+        if (e.pf.rank) g0.push_back(GemmJob{f.Hinv, e.pf.col, f.Xp, N, e.pf.rank, N, N, e.pf.ldc, e.pf.rank, 1.0, 0.0});
+        if (e.fp.rank) g0.push_back(GemmJob{e.fp.row, f.Hinv, f.RH, e.fp.rank, N, N, e.fp.ldr, N, N, 1.0, 0.0});
         els.push_back(e);
       }
-      run_copy(s, cps);
-      hodlr_solve_batched(s, probs);
-      std::vector<GemmJob> g1, g2;
+      run_gemm(s, g0);
       for (auto &e : els) {
         FrontH &f = F->fronts[e.fi];
         int rpf = e.pf.rank, rfp = e.fp.rank;
-        if (rpf == 0 || rfp == 0) {
-          // outer product of rank min(r_pf, r_fp) = 0 after the branch below
-        }
         double *core = ctx->scratch.d((size_t)std::max(1, rfp) * std::max(1, rpf));
         if (rfp && rpf)
-          g1.push_back(GemmJob{e.fp.row, e.x, core, rfp, rpf, f.npv, e.fp.ldr, rpf, rpf, 1.0, 0.0});
+          g1.push_back(GemmJob{e.fp.row, f.Xp, core, rfp, rpf, f.npv, e.fp.ldr, rpf, rpf, 1.0, 0.0});
         if (rpf <= rfp) {
           // W = col_fp @ core (nf x r_pf), V = row_pf^T  -> Vt = row_pf
           f.rw = rpf;
@@ -2204,6 +2187,31 @@ struct ApplyPlan {
   int64_t nodes = 0;
 };
 
+// DenseBlock.as_factors / LowRankFactor.as_factors (hodlr.py:59-63) as a device view
+static FacView fac_view(const mfh_factor *F, const BlockH &b) {
+  FacView v;
+  if (!b.dense) {
+    v.col = b.col;
+    v.ldc = b.rank;
+    v.row = b.row;
+    v.ldr = b.n;
+    v.rank = b.rank;
+  } else if (b.n <= b.m) {
+    v.col = b.val;
+    v.ldc = b.n;
+    v.row = F->ident;
+    v.ldr = F->ident_ld;
+    v.rank = b.n;
+  } else {
+    v.col = F->ident;
+    v.ldc = F->ident_ld;
+    v.row = b.val;
+    v.ldr = b.n;
+    v.rank = b.m;
+  }
+  return v;
+}
+
 static void run_gemv(Sink &sk, const std::vector<GemvJob> &jobs) {
   if (jobs.empty()) return;
   std::vector<int2> rows;
@@ -2226,49 +2234,6 @@ static GemvJob gemv(double *y, const double *y0, int m, const double *A1, int ld
   return GemvJob{y, y0, m, A1, lda1, k1, x1, a1, A2, lda2, k2, x2, idx2, a2};
 }
 
-// HODLR solve levels (hodlr.py:360-373) on vectors already holding the leaf
-// solutions: per depth, w = [R_top z_bot; R_bot z_top], y = core^{-1} w,
-// z_top -= X_top y_top, z_bot -= X_bot y_bot (three batched GEMV launches)
-struct ApplyTree {
-  const HTree *t;
-  double *z;  // z[lo..hi) of the tree's local range
-};
-
-static void emit_hodlr_levels(Sink &sk, Arena &ar, const std::vector<ApplyTree> &ts) {
-  int maxd = 0;
-  for (auto &a : ts) maxd = std::max(maxd, a.t->maxdepth);
-  for (int d = maxd; d >= 0; --d) {
-    std::vector<GemvJob> j1, j2, j3;
-    for (auto &a : ts) {
-      const HTree &T = *a.t;
-      for (int v = 0; v < T.nslots; ++v) {
-        if (T.leaf[v] != 0 || T.depth[v] != d) continue;
-        int r1 = T.r1[v], r2 = T.r2[v];
-        if (r1 + r2 == 0) continue;
-        int lo = T.lo[v], hi = T.hi[v], mid = (lo + hi) >> 1;
-        double *zt = a.z + lo, *zb = a.z + mid;
-        double *w = ar.d(r1 + r2), *yv = ar.d(r1 + r2);
-        if (r1) j1.push_back(gemv(w, nullptr, r1, T.f1[v].row, T.f1[v].ldr, hi - mid, zb, 1.0));
-        if (r2) j1.push_back(gemv(w + r1, nullptr, r2, T.f2[v].row, T.f2[v].ldr, mid - lo, zt, 1.0));
-        j2.push_back(gemv(yv, nullptr, r1 + r2, T.cinv[v], r1 + r2, r1 + r2, w, 1.0));
-        if (r1) j3.push_back(gemv(zt, zt, mid - lo, T.xt[v], r1, r1, yv, -1.0));
-        if (r2) j3.push_back(gemv(zb, zb, hi - mid, T.xb[v], r2, r2, yv + r1, -1.0));
-      }
-    }
-    run_gemv(sk, j1);
-    run_gemv(sk, j2);
-    run_gemv(sk, j3);
-  }
-}
-
-static void leaf_jobs(const HTree &T, const double *in, double *out, std::vector<GemvJob> &jobs) {
-  for (int v = 0; v < T.nslots; ++v)
-    if (T.leaf[v] == 1) {
-      int lo = T.lo[v], sz = T.hi[v] - T.lo[v];
-      jobs.push_back(gemv(out + lo, nullptr, sz, T.linv[v], sz, sz, in + lo, 1.0));
-    }
-}
-
 static void build_apply(mfh_factor *F) {
   auto tb0 = std::chrono::steady_clock::now();
   Ctx *ctx = F->ctx;
@@ -2280,7 +2245,6 @@ static void build_apply(mfh_factor *F) {
   AP->bu = ar.d(std::max<int64_t>(1, n));
   AP->xw = ar.d(std::max<int64_t>(1, n));
   AP->y = ar.d(std::max<int64_t>(1, n));
-  double *zz = ar.d(std::max<int64_t>(1, n));
   // contribution offsets (post order)
   std::vector<int64_t> off(F->fronts.size(), -1);
   int64_t tot = 0;
@@ -2350,7 +2314,6 @@ static void build_apply(mfh_factor *F) {
     check_launch();
   });
   bytes += 24.0 * n;
-  auto blk_tmp = [&](const BlockH &b) { return b.rank ? ar.d(b.rank) : nullptr; };
   // ---------------- upward: b_u[fro] -= apply_fp(pp_solve(b_u[piv]))
   for (int h = 0; h <= maxh; ++h) {
     auto &fis = byh[h];
@@ -2368,7 +2331,6 @@ static void build_apply(mfh_factor *F) {
       check_launch();
     });
     std::vector<GemvJob> j0, j1, j2;
-    std::vector<ApplyTree> ts;
     std::vector<std::pair<int, double *>> lr;  // structured LR fp: (front, tmp)
     for (int q : fis) {
       FrontH &f = F->fronts[q];
@@ -2379,25 +2341,19 @@ static void build_apply(mfh_factor *F) {
         j0.push_back(gemv(t, nullptr, f.nf, f.Gfp, f.npv, f.npv, bp, 1.0));
         bytes += 8.0 * (double)f.nf * f.npv;
       } else {
-        const HTree &T = F->trees[f.pp];
-        double *z = zz + f.piv_lo;
-        leaf_jobs(T, bp, z, j0);
-        ts.push_back(ApplyTree{&T, z});
-        BlockH &b = F->blocks[f.fp];
-        if (b.dense) {
-          j2.push_back(gemv(t, nullptr, f.nf, b.val, b.n, f.npv, z, 1.0));
-        } else if (b.rank) {
-          double *tmp = blk_tmp(b);
-          j1.push_back(gemv(tmp, nullptr, b.rank, b.row, b.n, f.npv, z, 1.0));
-          j2.push_back(gemv(t, nullptr, f.nf, b.col, b.rank, b.rank, tmp, 1.0));
+        // t = col_fp (RH b_piv), RH = row_fp H^{-1} precomputed at factor time
+        FacView fpv = fac_view(F, F->blocks[f.fp]);
+        if (fpv.rank) {
+          double *tmp = ar.d(fpv.rank);
+          j1.push_back(gemv(tmp, nullptr, fpv.rank, f.RH, f.npv, f.npv, bp, 1.0));
+          j2.push_back(gemv(t, nullptr, f.nf, fpv.col, fpv.ldc, fpv.rank, tmp, 1.0));
+          bytes += 8.0 * ((double)fpv.rank * f.npv + (double)f.nf * fpv.rank);
         } else {
           j2.push_back(gemv(t, nullptr, f.nf, nullptr, 0, 0, nullptr, 0.0));  // exact zero contribution
         }
-        bytes += 8.0 * (f.factor_reals - F->blocks[f.pf].stored());
       }
     }
     run_gemv(sk, j0);
-    emit_hodlr_levels(sk, ar, ts);
     run_gemv(sk, j1);
     run_gemv(sk, j2);
   }
@@ -2405,8 +2361,7 @@ static void build_apply(mfh_factor *F) {
   for (int h = maxh; h >= 0; --h) {
     auto &fis = byh[h];
     if (fis.empty()) continue;
-    std::vector<GemvJob> ja, jb, jc;
-    std::vector<ApplyTree> ts;
+    std::vector<GemvJob> ja, jb;
     for (int q : fis) {
       FrontH &f = F->fronts[q];
       const double *bp = bu + f.piv_lo;
@@ -2417,31 +2372,22 @@ static void build_apply(mfh_factor *F) {
         bytes += 8.0 * ((double)f.npv * f.npv + (double)f.npv * f.nf);
         continue;
       }
-      const HTree &T = F->trees[f.pp];
-      double *rhs = y + f.piv_lo;
-      if (f.nf) {
-        BlockH &b = F->blocks[f.pf];
-        if (b.dense) {
-          jb.push_back(gemv(rhs, bp, f.npv, nullptr, 0, 0, nullptr, 0.0, b.val, b.n, f.nf, xw, fro, -1.0));
-        } else if (b.rank) {
-          double *tmp = blk_tmp(b);
-          ja.push_back(gemv(tmp, nullptr, b.rank, nullptr, 0, 0, nullptr, 0.0, b.row, b.n, f.nf, xw, fro, 1.0));
-          jb.push_back(gemv(rhs, bp, f.npv, b.col, b.rank, b.rank, tmp, -1.0));
-        } else {
-          jb.push_back(gemv(rhs, bp, f.npv, nullptr, 0, 0, nullptr, 0.0));
-        }
-        bytes += 8.0 * (f.factor_reals - F->blocks[f.fp].stored());
-        leaf_jobs(T, rhs, xv, jc);
+      // x_piv = H^{-1} b_piv - Xp (row_pf x_fro), Xp = H^{-1} col_pf precomputed
+      FacView pfv;
+      if (f.nf) pfv = fac_view(F, F->blocks[f.pf]);
+      if (f.nf && pfv.rank) {
+        double *tmp = ar.d(pfv.rank);
+        ja.push_back(gemv(tmp, nullptr, pfv.rank, nullptr, 0, 0, nullptr, 0.0, pfv.row, pfv.ldr, f.nf, xw, fro, 1.0));
+        jb.push_back(gemv(xv, nullptr, f.npv, f.Hinv, f.npv, f.npv, bp, 1.0, f.Xp, pfv.rank, pfv.rank, tmp, nullptr,
+                          -1.0));
+        bytes += 8.0 * ((double)f.npv * f.npv + (double)f.npv * pfv.rank + (double)pfv.rank * f.nf);
       } else {
-        leaf_jobs(T, bp, xv, jc);
-        bytes += 8.0 * f.factor_reals;
+        jb.push_back(gemv(xv, nullptr, f.npv, f.Hinv, f.npv, f.npv, bp, 1.0));
+        bytes += 8.0 * (double)f.npv * f.npv;
       }
-      ts.push_back(ApplyTree{&T, xv});
     }
     run_gemv(sk, ja);
     run_gemv(sk, jb);
-    run_gemv(sk, jc);
-    emit_hodlr_levels(sk, ar, ts);
   }
   sk.launch([=](cudaStream_t s) {
     k_gather_perm<<<grid_n, 256, 0, s>>>(xw, perm, dx, n);
@@ -2840,10 +2786,13 @@ struct GmresRun {
     k_finish<<<1, 32, 0, ctx->s>>>(ctx->d_part, out, do_sqrt ? 1 : 0);
     check_launch();
   }
+  double sync_ms = 0.0;
   double host_scalar(double *d) {
     double v;
     CK(cudaMemcpyAsync(&v, d, sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+    auto t0 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(ctx->s));
+    sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return v;
   }
 
@@ -2871,6 +2820,12 @@ struct GmresRun {
     CK(cudaMallocAsync(&z, sizeof(double) * n, ctx->s));
     double *dy = S + 2048;
     int g = gridn();
+    int per_sm = 0, nsm = 148;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs_coop, 256, 0));
+    int mgs_grid = std::max(1, std::min(per_sm, 2) * nsm);
+    mgs_grid = (int)std::min<int64_t>(mgs_grid, std::max<int64_t>(1, cdiv(n, 256)));
+    if (mgs_grid > (RED_BLOCKS + 64) / 2) mgs_grid = (RED_BLOCKS + 64) / 2;
     auto cleanup = [&]() {
       cudaFreeAsync(V, ctx->s);
       cudaFreeAsync(w, ctx->s);
@@ -2902,15 +2857,23 @@ struct GmresRun {
         while (j < m) {
           M(V + j * n, z);
           A(z, w);
-          for (int64_t i = 0; i <= j; ++i) {
-            ctx->launches += 2;
-            k_dot_part<<<RED_BLOCKS, RED_THREADS, 0, ctx->s>>>(V + i * n, w, n, ctx->d_part);
-            k_mgs_axpy<<<g, 256, 0, ctx->s>>>(ctx->d_part, S + 8 + i, V + i * n, w, n);
+          {
+            // whole MGS sweep + norm in one cooperative launch
+            const double *Vc = V;
+            double *wc = w, *Hc = S + 8, *pc = ctx->d_part;
+            long long nn = n;
+            int jj = (int)j;
+            void *args[6] = {(void *)&Vc, (void *)&wc, (void *)&nn, (void *)&jj, (void *)&Hc, (void *)&pc};
+            CK(cudaLaunchCooperativeKernel((const void *)k_mgs_coop, dim3(mgs_grid), dim3(256), args, 0, ctx->s));
+            ctx->launches++;
           }
-          dot(w, w, S + 2, true);
-          check_launch();
-          CK(cudaMemcpyAsync(hcol.data(), S + 8, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, ctx->s));
-          double hn = host_scalar(S + 2);
+          CK(cudaMemcpyAsync(hcol.data(), S + 8, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, ctx->s));
+          {
+            auto t0 = std::chrono::steady_clock::now();
+            CK(cudaStreamSynchronize(ctx->s));
+            sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+          }
+          double hn = hcol[j + 1];
           for (int64_t i = 0; i <= j; ++i) h(i, j) = hcol[i];
           if (!std::isfinite(hn)) throw value_error("GMRES residual is not finite");
           h(j + 1, j) = hn;
@@ -2937,7 +2900,7 @@ struct GmresRun {
             break;
           }
           if (j < m) {
-            k_scale_inv<<<g, 256, 0, ctx->s>>>(S + 2, w, V + j * n, n);
+            k_scale_inv<<<g, 256, 0, ctx->s>>>(S + 8 + j, w, V + j * n, n);
             ctx->launches++;
           }
         }
@@ -2986,6 +2949,7 @@ static int gmres_common(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const
   if (ops->M) {
     ops->M->timing.gmres_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tg0).count();
     ops->M->timing.gmres_apply_ms = g.m_ms;
+    ops->M->timing.gmres_sync_ms = g.sync_ms;
   }
   if (hist) std::memcpy(hist, res.data(), sizeof(double) * res.size());
   *n_hist = (int64_t)res.size();

@@ -1504,6 +1504,47 @@ __global__ void k_combine(const double *__restrict__ V, const double *__restrict
   }
 }
 
+// Whole modified Gram-Schmidt sweep + norm of one Arnoldi step in one
+// cooperative launch (krylov.py:116-120): for i = 0..j, H[i] = V_i . w then
+// w -= H[i] V_i (numpy: w - (h * V_i), no FMA); finally H[j+1] = ||w||.
+// Each block owns a fixed slice of w, so the axpy of projection i-1 and the
+// dot of projection i run back to back on that slice; one grid barrier per
+// projection, and every block sums the partials in the same fixed order.
+__global__ void __launch_bounds__(256) k_mgs_coop(const double *__restrict__ V, double *__restrict__ w, long long n,
+                                                  int j, double *__restrict__ H, double *__restrict__ part) {
+  __shared__ double sh[33];
+  __shared__ double s_h;
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x, b = blockIdx.x;
+  const long long chunk = (n + G - 1) / G;
+  const long long lo = (long long)b * chunk, hi = min(n, lo + chunk);
+  double h = 0.0;
+  for (int i = 0; i <= j + 1; ++i) {
+    const double *Vp = V + (long long)(i - 1) * n;
+    const double *Vi = V + (long long)i * n;
+    double s = 0.0;
+    for (long long k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+      double wk = w[k];
+      if (i > 0) {
+        wk = __dsub_rn(wk, __dmul_rn(h, Vp[k]));
+        w[k] = wk;
+      }
+      s = (i <= j) ? fma(Vi[k], wk, s) : fma(wk, wk, s);
+    }
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) part[(i & 1) * G + b] = s;
+    grid.sync();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < G; ++q) t += part[(i & 1) * G + q];
+      s_h = t;
+    }
+    __syncthreads();
+    h = s_h;
+    if (b == 0 && threadIdx.x == 0) H[i] = (i <= j) ? h : sqrt(h);
+  }
+}
+
 // CSR SpMV, one warp per row (A @ x, sparse.py:277-284)
 __global__ void __launch_bounds__(256) k_spmv(long long nrows, const long long *__restrict__ ptr,
                                               const int *__restrict__ col,

@@ -75,7 +75,10 @@ def peaks():
 class ClockSampler:
     """SM clocks + throttle reasons sampled during the timed region, in-process
     through NVML (spawning nvidia-smi every 200 ms perturbs the sync-heavy GMRES
-    loop by tens of milliseconds)."""
+    loop by tens of milliseconds). NVML is initialised and the thread started
+    before warm-up (first NVML queries are slow and contend with the driver);
+    only samples taken while `active` is set (the timed region) are reported.
+    MFH_BENCH_NO_CLOCKS=1 disables sampling (diagnostics only)."""
 
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap"}
@@ -84,33 +87,40 @@ class ClockSampler:
         self.index = index
         self.period = period
         self.samples = []
+        self.active = False
         self._stop = threading.Event()
         self._t = None
 
-    def __enter__(self):
+    def start(self):
+        if os.environ.get("MFH_BENCH_NO_CLOCKS"):
+            return self
         try:
             import pynvml
             pynvml.nvmlInit()
             h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
             mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
         except Exception:
             return self
 
         def run():
             while not self._stop.is_set():
-                try:
-                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    self.samples.append((sm, mx, rs))
-                except Exception:
-                    pass
+                if self.active:
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        if self.active:
+                            self.samples.append((sm, mx, rs))
+                    except Exception:
+                        pass
                 self._stop.wait(self.period)
 
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
         return self
 
-    def __exit__(self, *a):
+    def stop(self):
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
@@ -286,12 +296,14 @@ def run_gpu_arm(args, cfg, world, rank, local):
         torch.cuda.synchronize()
         print(json.dumps({"profile_step": True, "iterations": its, "converged": conv}), flush=True)
         return
+    clocks = ClockSampler(local).start()
     for _ in range(args.warmup):
         F, its, conv, res = step_device()
     barrier(world)
     times, e2e_times = [], []
     launches0 = ctx.info()[1]
-    with ClockSampler(local) as clocks:
+    clocks.active = True
+    if True:
         for _ in range(args.steps):
             F = None  # the previous factorization is released before the next step
             flush.fill_(1)
@@ -305,6 +317,8 @@ def run_gpu_arm(args, cfg, world, rank, local):
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
         launches = (ctx.info()[1] - launches0) / max(1, args.steps)
+        per_step = {k: [round(x, 5) for x in v[-args.steps:]] for k, v in split.items()
+                    if k in ("factor_s", "gmres_inner_s")}
         split = {k: float(np.mean(v[-args.steps:])) for k, v in split.items()}
         Fe = None
         for _ in range(max(1, min(args.steps, 3))):
@@ -319,6 +333,8 @@ def run_gpu_arm(args, cfg, world, rank, local):
             e1.record(lib_stream)
             torch.cuda.synchronize()
             e2e_times.append(e0.elapsed_time(e1) / 1e3)
+    clocks.active = False
+    clocks.stop()
     t_step = max_over_ranks(float(np.mean(times)), world)
     t_e2e = max_over_ranks(float(np.mean(e2e_times)), world)
     true_res = float(np.linalg.norm(A._csc @ xe - b) / np.linalg.norm(b))
@@ -343,6 +359,7 @@ def run_gpu_arm(args, cfg, world, rank, local):
         "gmres": {"iterations": its, "converged": conv, "final_rel_residual": float(res),
                   "true_rel_residual_e2e": true_res, "e2e_iterations": he.iterations},
         "split_s": split,
+        "per_step_s": {"step": [round(x, 5) for x in times], **per_step},
         "factor": {"device_ms": tim["total_ms"], "host_plan_ms": tim["host_ms"],
                    "host_ms": {k: tim[k] for k in ("host_preamble_ms", "host_select_ms", "host_sync_wait_ms",
                                                    "wall_ms", "apply_build_ms", "apply_instantiate_ms",

@@ -181,6 +181,14 @@ int mfh_full_pivot_lu_batched(mfh_ctx *ctx, int64_t batch, const int64_t *offs, 
                               const int64_t *max_ranks, int64_t *row_perm, int64_t *col_perm,
                               int64_t *ranks, double *ratios, int64_t *status, double *err);
 
+/* ---- test hook (no reference counterpart) ------------------------------ */
+/* The factorization's explicit-inverse dispatch (register-tiled Gauss-Jordan
+ * for n <= 128, blocked LU + triangular inverses above) on a host batch of
+ * square row-major blocks packed at offs[i]; blocks are overwritten with the
+ * inverses; singular[i] = 1 where a pivot was zero or non-finite. */
+int mfh_test_inverse_batched(mfh_ctx *ctx, int64_t batch, const int64_t *offs, const int64_t *ns,
+                             double *blocks, int64_t total, int *singular);
+
 #ifdef __cplusplus
 }
 #endif

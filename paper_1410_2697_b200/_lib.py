@@ -138,6 +138,7 @@ def _sig(lib):
         "mfh_gmres_device": (C.c_int, [P, C.POINTER(mfh_gmres_ops), I64, P, P, d, I64, I64, P, pi,
                                        pi, C.POINTER(C.c_int)]),
         "mfh_full_pivot_lu_batched": (C.c_int, [P, I64, P, P, P, P, I64, d, P, P, P, P, P, P, P]),
+        "mfh_test_inverse_batched": (C.c_int, [P, I64, P, P, P, I64, P]),
     }
     for name, (res, args) in s.items():
         f = getattr(lib, name)

@@ -190,6 +190,7 @@ struct Ctx {
   Arena scratch;
   double *d_part = nullptr;  // reduction partials
   double *d_scal = nullptr;  // small device scalars
+  double *h_scal = nullptr;  // pinned host mirror for GMRES read-backs
   int64_t launches = 0;
 };
 
@@ -357,10 +358,45 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
     }
     PanelJob *dp = sk.push(pj);
     int np_ = (int)pj.size();
-    sk.launch([=](cudaStream_t s) {
-      k_getrf_panel<<<np_, 512, 0, s>>>(dp);
-      check_launch();
-    });
+    int mmax = 0;
+    for (auto &q : pj) mmax = std::max(mmax, q.n - q.c0);
+    int cs = (mmax + PANEL_ROWS_MAX - 1) / PANEL_ROWS_MAX;
+    static const bool legacy_panel = std::getenv("MFH_PANEL_LEGACY") != nullptr;
+    if (cs <= 16 && !legacy_panel) {
+      // shared-memory resident panel across a cluster of cs CTAs
+      static bool attr = false;
+      if (!attr) {
+        CK(cudaFuncSetAttribute(k_getrf_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(double) * PANEL_ROWS_MAX * PLD)));
+        CK(cudaFuncSetAttribute(k_getrf_panel_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr = true;
+      }
+      int rp = (mmax + cs - 1) / cs;
+      size_t smem = sizeof(double) * (size_t)rp * PLD;
+      sk.launch([=](cudaStream_t s) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(np_ * cs);
+        cfg.blockDim = dim3(512);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const PanelJob *arg = dp;
+        void *args[1] = {(void *)&arg};
+        cudaError_t e = cudaLaunchKernelExC(&cfg, (const void *)k_getrf_panel_cl, args);
+        if (e != cudaSuccess) throw runtime_error(std::string("panel cluster launch failed: ") + cudaGetErrorString(e));
+      });
+    } else {
+      sk.launch([=](cudaStream_t s) {
+        k_getrf_panel<<<np_, 512, 0, s>>>(dp);
+        check_launch();
+      });
+    }
     run_laswp(sk, sw);
     run_trsm(sk, tr);
     run_gemm(sk, gm);
@@ -558,15 +594,35 @@ static void run_inverse(Sink &sk, const std::vector<InvReq> &reqs) {
     }
   }
   run_copy(sk, cps);
-  if (!small.empty()) {
+  static const bool legacy_inv = std::getenv("MFH_INV_LEGACY") != nullptr;
+  if (!small.empty() && legacy_inv) {
     InvJob *dj = sk.push(small);
     int nb = (int)small.size();
     size_t sm = sizeof(double) * (size_t)maxs * maxs;
-    int th = maxs > 64 ? 512 : 256;
     sk.launch([=](cudaStream_t st) {
-      k_inv_small<<<nb, th, sm, st>>>(dj);
+      k_inv_small<<<nb, maxs > 64 ? 512 : 256, sm, st>>>(dj);
       check_launch();
     });
+  } else if (!small.empty()) {
+    // register-tiled Gauss-Jordan: 64-wide tiles (256 threads) or 128-wide (512)
+    std::vector<InvJob> s64, s128;
+    for (auto &j : small) (j.n <= 64 ? s64 : s128).push_back(j);
+    if (!s64.empty()) {
+      InvJob *dj = sk.push(s64);
+      int nb = (int)s64.size();
+      sk.launch([=](cudaStream_t st) {
+        k_inv_reg<8, 2><<<nb, 256, 0, st>>>(dj);
+        check_launch();
+      });
+    }
+    if (!s128.empty()) {
+      InvJob *dj = sk.push(s128);
+      int nb = (int)s128.size();
+      sk.launch([=](cudaStream_t st) {
+        k_inv_reg<16, 4><<<nb, 512, 0, st>>>(dj);
+        check_launch();
+      });
+    }
   }
   if (!lus.empty()) {
     run_getrf(sk, lus);
@@ -2486,6 +2542,7 @@ extern "C" int mfh_ctx_create(int device, mfh_ctx **out) {
   c->c.scratch.chunk = size_t(512) << 20;
   CK(cudaMalloc(&c->c.d_part, sizeof(double) * (RED_BLOCKS + 64)));
   CK(cudaMalloc(&c->c.d_scal, sizeof(double) * 4096));
+  CK(cudaMallocHost(&c->c.h_scal, sizeof(double) * 4096));
   *out = c;
   MFH_CATCH
 }
@@ -2499,6 +2556,7 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   for (auto e : ctx->c.evpool) cudaEventDestroy(e);
   cudaFree(ctx->c.d_part);
   cudaFree(ctx->c.d_scal);
+  cudaFreeHost(ctx->c.h_scal);
   cudaStreamSynchronize(ctx->c.side);
   cudaEventDestroy(ctx->c.ev_fork);
   cudaEventDestroy(ctx->c.ev_join);
@@ -2788,12 +2846,11 @@ struct GmresRun {
   }
   double sync_ms = 0.0;
   double host_scalar(double *d) {
-    double v;
-    CK(cudaMemcpyAsync(&v, d, sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaMemcpyAsync(ctx->h_scal, d, sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
     auto t0 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(ctx->s));
     sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    return v;
+    return ctx->h_scal[0];
   }
 
   void run(const double *d_b, double *d_x, double tol, int64_t max_iter, int64_t restart,
@@ -2804,6 +2861,7 @@ struct GmresRun {
     its = 0;
     conv = false;
     double *S = ctx->d_scal;  // [0] norm b, [1] beta, [2] hn, [8..] H column
+    const bool trace = std::getenv("MFH_GMRES_TRACE") != nullptr;
     CK(cudaMemsetAsync(d_x, 0, sizeof(double) * n, ctx->s));
     dot(d_b, d_b, S, true);
     double nb = host_scalar(S);
@@ -2813,11 +2871,12 @@ struct GmresRun {
       return;
     }
     int64_t mcap = std::min(restart, max_iter);
-    double *V = nullptr, *w = nullptr, *r = nullptr, *z = nullptr;
-    CK(cudaMallocAsync(&V, sizeof(double) * n * (mcap + 1), ctx->s));
-    CK(cudaMallocAsync(&w, sizeof(double) * n, ctx->s));
-    CK(cudaMallocAsync(&r, sizeof(double) * n, ctx->s));
-    CK(cudaMallocAsync(&z, sizeof(double) * n, ctx->s));
+    if (mcap > 2000)  // Hessenberg column and y live in the 4096-slot scalar buffers
+      throw value_error("min(restart, max_iter) must be <= 2000");
+    // Krylov basis + work vectors from the context's chunk pool (no per-solve
+    // cudaMalloc / driver-pool remapping)
+    auto chunk = ctx->pool.take(sizeof(double) * (size_t)n * (size_t)(mcap + 4));
+    double *V = (double *)chunk.first, *w = V + n * (mcap + 1), *r = w + n, *z = r + n;
     double *dy = S + 2048;
     int g = gridn();
     int per_sm = 0, nsm = 148;
@@ -2827,11 +2886,8 @@ struct GmresRun {
     mgs_grid = (int)std::min<int64_t>(mgs_grid, std::max<int64_t>(1, cdiv(n, 256)));
     if (mgs_grid > (RED_BLOCKS + 64) / 2) mgs_grid = (RED_BLOCKS + 64) / 2;
     auto cleanup = [&]() {
-      cudaFreeAsync(V, ctx->s);
-      cudaFreeAsync(w, ctx->s);
-      cudaFreeAsync(r, ctx->s);
-      cudaFreeAsync(z, ctx->s);
       cudaStreamSynchronize(ctx->s);
+      ctx->pool.give(chunk);
     };
     try {
       while (its < max_iter && !conv) {
@@ -2853,10 +2909,13 @@ struct GmresRun {
         k_scale_inv<<<g, 256, 0, ctx->s>>>(S + 1, r, V, n);
         int64_t j = 0;
         bool lucky_stop = false;
-        std::vector<double> hcol(m + 2);
+        double *hcol = ctx->h_scal + 16;  // pinned: the copy is truly async
         while (j < m) {
+          auto q0 = std::chrono::steady_clock::now();
           M(V + j * n, z);
+          auto q1 = std::chrono::steady_clock::now();
           A(z, w);
+          auto q2 = std::chrono::steady_clock::now();
           {
             // whole MGS sweep + norm in one cooperative launch
             const double *Vc = V;
@@ -2867,11 +2926,18 @@ struct GmresRun {
             CK(cudaLaunchCooperativeKernel((const void *)k_mgs_coop, dim3(mgs_grid), dim3(256), args, 0, ctx->s));
             ctx->launches++;
           }
-          CK(cudaMemcpyAsync(hcol.data(), S + 8, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, ctx->s));
+          auto q3 = std::chrono::steady_clock::now();
+          CK(cudaMemcpyAsync(hcol, S + 8, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, ctx->s));
+          auto q4 = std::chrono::steady_clock::now();
           {
-            auto t0 = std::chrono::steady_clock::now();
             CK(cudaStreamSynchronize(ctx->s));
-            sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - q4).count();
+          }
+          if (trace) {
+            auto q5 = std::chrono::steady_clock::now();
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            std::fprintf(stderr, "gmres it %lld: M %.3f A %.3f mgs %.3f cpy %.3f sync %.3f ms\n", (long long)its,
+                         ms(q0, q1), ms(q1, q2), ms(q2, q3), ms(q3, q4), ms(q4, q5));
           }
           double hn = hcol[j + 1];
           for (int64_t i = 0; i <= j; ++i) h(i, j) = hcol[i];
@@ -2967,21 +3033,20 @@ extern "C" int mfh_gmres_device(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t 
 extern "C" int mfh_gmres(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const double *b, double *x,
                          double tol, int64_t max_iter, int64_t restart, double *hist, int64_t *n_hist,
                          int64_t *iterations, int *converged) {
-  double *db = nullptr, *dx = nullptr;
   cudaStream_t s = ctx->c.s;
-  if (cudaMalloc(&db, sizeof(double) * std::max<int64_t>(1, n)) != cudaSuccess ||
-      cudaMalloc(&dx, sizeof(double) * std::max<int64_t>(1, n)) != cudaSuccess) {
-    set_last_error("CUDA allocation failed in mfh_gmres");
+  std::pair<char *, size_t> chunk{nullptr, 0};
+  try {
+    chunk = ctx->c.pool.take(sizeof(double) * 2 * (size_t)std::max<int64_t>(1, n));
+  } catch (const std::exception &e) {
+    set_last_error(std::string("CUDA allocation failed in mfh_gmres: ") + e.what());
     return MFH_ERUNTIME;
   }
+  double *db = (double *)chunk.first, *dx = db + std::max<int64_t>(1, n);
   cudaMemcpyAsync(db, b, sizeof(double) * n, cudaMemcpyHostToDevice, s);
   int rc = gmres_common(ctx, ops, n, db, dx, tol, max_iter, restart, hist, n_hist, iterations, converged);
-  if (rc == MFH_OK) {
-    cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-  }
-  cudaFree(db);
-  cudaFree(dx);
+  if (rc == MFH_OK) cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  ctx->c.pool.give(chunk);
   return rc;
 }
 
@@ -3067,5 +3132,43 @@ extern "C" int mfh_full_pivot_lu_batched(mfh_ctx *ctx, int64_t batch, const int6
     ro += m;
     co += n;
   }
+  MFH_CATCH
+}
+
+// ---------------------------------------------------------------------------
+// test hook: the factorization's explicit-inverse dispatch (run_inverse) on a
+// host batch of square row-major blocks; singular[i] = 1 where a pivot was
+// zero / non-finite (the reference's LU diagonal checks)
+// ---------------------------------------------------------------------------
+extern "C" int mfh_test_inverse_batched(mfh_ctx *ctx, int64_t batch, const int64_t *offs, const int64_t *ns,
+                                        double *blocks, int64_t total, int *singular) {
+  MFH_TRY
+  Ctx *c = &ctx->c;
+  if (batch == 0) return MFH_OK;
+  double *d_blocks = c->scratch.d(std::max<int64_t>(1, total));
+  double *d_out = c->scratch.d(std::max<int64_t>(1, total));
+  int64_t ptot = 0;
+  for (int64_t b = 0; b < batch; ++b) ptot += ns[b];
+  int *d_piv = c->scratch.i(std::max<int64_t>(1, ptot));
+  int *d_flag = c->scratch.i(std::max<int64_t>(1, batch));
+  CK(cudaMemcpyAsync(d_blocks, blocks, sizeof(double) * total, cudaMemcpyHostToDevice, c->s));
+  CK(cudaMemsetAsync(d_flag, 0, sizeof(int) * batch, c->s));
+  std::vector<InvReq> reqs;
+  int64_t po = 0;
+  for (int64_t b = 0; b < batch; ++b) {
+    int n = (int)ns[b];
+    if (n < 1) throw value_error("block sizes must be positive");
+    reqs.push_back(InvReq{d_blocks + offs[b], n, n, d_out + offs[b], n, d_piv + po, d_flag + b});
+    po += n;
+  }
+  Sink s{c};
+  run_inverse(s, reqs);
+  std::vector<int> hf(batch);
+  CK(cudaMemcpyAsync(blocks, d_out, sizeof(double) * total, cudaMemcpyDeviceToHost, c->s));
+  CK(cudaMemcpyAsync(hf.data(), d_flag, sizeof(int) * batch, cudaMemcpyDeviceToHost, c->s));
+  CK(cudaStreamSynchronize(c->s));
+  c->scratch.reset();
+  c->stage.rewind();
+  for (int64_t b = 0; b < batch; ++b) singular[b] = hf[b];
   MFH_CATCH
 }

@@ -1026,6 +1026,90 @@ __global__ void __launch_bounds__(512) k_getrf_panel(const PanelJob *__restrict_
   }
 }
 
+// Panel LU (partial pivoting, LAPACK rule) with the panel resident in shared
+// memory across a cluster: CTA q of the cluster owns panel rows
+// [q*rp, (q+1)*rp) (stride PNB+1: conflict-free column scans), one thread
+// per row. Per column: local candidate -> cluster barrier -> every CTA
+// reduces the CS candidates and pulls the pivot row (and, for the owner of
+// row p, old row k) over DSMEM -> cluster barrier -> swap writes, scale and
+// rank-1 update of the local rows. Same arithmetic as k_getrf_panel.
+constexpr int PLD = PNB + 1;
+constexpr int PANEL_ROWS_MAX = 416;  // rows per CTA (416 * 65 * 8 = 216 KB)
+__global__ void __launch_bounds__(512) k_getrf_panel_cl(const PanelJob *__restrict__ jobs) {
+  extern __shared__ double sh_panel[];
+  __shared__ MaxLoc red[33];
+  __shared__ MaxLoc cand;
+  __shared__ double prow[PNB], told[PNB];
+  __shared__ int s_p;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks(), q = (int)cl.block_rank();
+  const PanelJob J = jobs[blockIdx.x / CS];
+  const int n = J.n, lda = J.lda, c0 = J.c0, w = J.w, tid = threadIdx.x;
+  const int m = n - c0, rp = (m + CS - 1) / CS, r0 = q * rp, nr = max(0, min(m, r0 + rp) - r0);
+  double *a = J.a;
+  // load my slab: panel row t (global row c0 + r0 + t), columns c0 .. c0+w-1
+  for (int e = tid; e < nr * w; e += blockDim.x) {
+    int t = e / w, j = e - t * w;
+    sh_panel[t * PLD + j] = a[(long long)(c0 + r0 + t) * lda + c0 + j];
+  }
+  __syncthreads();
+  double *myrow = tid < nr ? sh_panel + tid * PLD : nullptr;
+  for (int kk = 0; kk < w; ++kk) {
+    // local candidate over my rows with panel index >= kk
+    double bv = -1.0;
+    long long bk = 0x7fffffffffffffffLL;
+    if (myrow && r0 + tid >= kk) {
+      bv = fabs(myrow[kk]);
+      bk = r0 + tid;
+    }
+    MaxLoc b = block_maxloc(bv, bk, red);
+    if (tid == 0) cand = b;
+    cl.sync();
+    if (tid < 32) {
+      MaxLoc o{-1.0, 0x7fffffffffffffffLL};
+      if (tid < CS) o = *cl.map_shared_rank(&cand, tid);
+      for (int off = 16; off > 0; off >>= 1) {
+        double ov = __shfl_down_sync(0xffffffffu, o.v, off);
+        long long ok = __shfl_down_sync(0xffffffffu, o.key, off);
+        if (better(ov, ok, o.v, o.key)) {
+          o.v = ov;
+          o.key = ok;
+        }
+      }
+      if (tid == 0) s_p = o.key == 0x7fffffffffffffffLL ? kk : (int)o.key;
+    }
+    __syncthreads();
+    const int p = s_p;  // panel row index
+    const int op = p / rp, ok_ = kk / rp;
+    if (tid < w) {
+      prow[tid] = cl.map_shared_rank(sh_panel, op)[(p - op * rp) * PLD + tid];
+      if (q == op && p != kk) told[tid] = cl.map_shared_rank(sh_panel, ok_)[(kk - ok_ * rp) * PLD + tid];
+    }
+    if (q == 0 && tid == 0) J.piv[c0 + kk] = c0 + p;
+    cl.sync();
+    const double pv = prow[kk];
+    if (p != kk && pv != 0.0) {
+      if (q == ok_ && tid < w) sh_panel[(kk - r0) * PLD + tid] = prow[tid];
+      if (q == op && tid < w) sh_panel[(p - r0) * PLD + tid] = told[tid];
+      __syncthreads();
+    }
+    if (myrow && r0 + tid > kk) {
+      double l = myrow[kk];
+      if (pv != 0.0) {
+        l *= 1.0 / pv;
+        myrow[kk] = l;
+      }
+      for (int j = kk + 1; j < w; ++j) myrow[j] = fma(-l, prow[j], myrow[j]);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < nr * w; e += blockDim.x) {
+    int t = e / w, j = e - t * w;
+    a[(long long)(c0 + r0 + t) * lda + c0 + j] = sh_panel[t * PLD + j];
+  }
+  cl.sync();  // remote readers are done before this CTA's shared memory goes away
+}
+
 // apply the panel's row swaps to the columns outside the panel
 struct SwapJob {
   double *a;
@@ -1179,6 +1263,155 @@ __global__ void __launch_bounds__(512) k_inv_small(const InvJob *__restrict__ jo
   }
   for (int e = tid; e < n * n; e += nt) J.a[(long long)(e / n) * J.lda + (e % n)] = sA[e];
   if (tid == 0 && bad && J.flag) *J.flag = 1;
+}
+
+// Register-tiled Gauss-Jordan inverse for n <= NW*8 (<= 32*CPL), same pivot
+// rule as k_inv_small: warp w owns rows [8w, 8w+8), lane l owns columns
+// {l, l+32, ...}; each thread keeps its 8 x CPL tile in registers. Per step:
+// every warp publishes its rows' column-k values and its best candidate; all
+// threads reduce the candidates redundantly (no broadcast barrier); the owners
+// of rows k and p publish them; every thread updates its tile. Two barriers
+// per step, no shared-memory matrix, no integer division.
+template <int NW, int CPL>
+__global__ void __launch_bounds__(NW * 32) k_inv_reg(const InvJob *__restrict__ jobs) {
+  constexpr int NR = NW * 8, NC = 32 * CPL;
+  static_assert(NW <= 32, "candidate reduction is one warp wide");
+  __shared__ double colkb[2][NR];  // parity double buffer: written before step k+1's first barrier
+  __shared__ double rowK[NC], rowP[NC];
+  __shared__ double cv[NW];
+  __shared__ int ci[NW];
+  __shared__ int piv[NR], idx[NC];
+  __shared__ int bad;
+  const InvJob J = jobs[blockIdx.x];
+  const int n = J.n, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double a[8][CPL];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      int i = warp * 8 + r, j = lane + 32 * c;
+      a[r][c] = (i < n && j < n) ? J.a[(long long)i * J.lda + j] : 0.0;
+    }
+  if (threadIdx.x == 0) bad = 0;
+  for (int k = 0; k < n; ++k) {
+    const int kl = k & 31, kc = k >> 5;
+    double *colk = colkb[k & 1];
+    if (lane == kl) {
+      // rows ascend, so a strict '>' keeps the first maximum
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        int i = warp * 8 + r;
+        double v = 0.0;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+          if (c == kc) v = a[r][c];
+        colk[i] = v;
+        if (i >= k && i < n && fabs(v) > bv) {
+          bv = fabs(v);
+          bi = i;
+        }
+      }
+      cv[warp] = bv;
+      ci[warp] = bi;
+    }
+    __syncthreads();
+    // every warp reduces the NW candidates (ties -> lower row)
+    double bv = lane < NW ? cv[lane] : -1.0;
+    int bi = lane < NW ? ci[lane] : 0x7fffffff;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      if (off >= NW) continue;
+      double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    bi = __shfl_sync(0xffffffffu, bi, 0);  // only lanes < NW took part in the reduction
+    const int p = bi == 0x7fffffff ? k : bi;
+    const double pv = colk[p];
+    if (pv == 0.0 || !isfinite(pv)) {
+      if (threadIdx.x == 0) bad = 1;
+      break;
+    }
+    if (threadIdx.x == 0) piv[k] = p;
+    if (warp == (k >> 3)) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (warp * 8 + r == k)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) rowK[lane + 32 * c] = a[r][c];
+    }
+    if (warp == (p >> 3)) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (warp * 8 + r == p)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) rowP[lane + 32 * c] = a[r][c];
+    }
+    __syncthreads();
+    const double rinv = 1.0 / pv;
+    double pj[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int j = lane + 32 * c;
+      pj[c] = (j == k ? 1.0 : rowP[j]) * rinv;  // scaled pivot row (new row k)
+    }
+    // row p takes old row k (the swap); column k is cleared before the update
+    if (warp == (p >> 3) && p != k) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (warp * 8 + r == p)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) a[r][c] = rowK[lane + 32 * c];
+    }
+    if (lane == kl) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+          if (c == kc) a[r][c] = 0.0;
+    }
+    const double ck_p = colk[k];  // old A[k][k]: row p's column-k value after the swap
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int i = warp * 8 + r;
+      const double f = (i == p) ? ck_p : colk[i];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) a[r][c] = fma(-f, pj[c], a[r][c]);
+    }
+    if (warp == (k >> 3)) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (warp * 8 + r == k)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) a[r][c] = pj[c];
+    }
+  }
+  __syncthreads();
+  if (!bad) {
+    if (threadIdx.x == 0) {
+      for (int j = 0; j < n; ++j) idx[j] = j;
+      for (int k = n - 1; k >= 0; --k) {
+        int t = idx[k];
+        idx[k] = idx[piv[k]];
+        idx[piv[k]] = t;
+      }
+      for (int j = 0; j < n; ++j) piv[idx[j]] = j;  // position of computed column m
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        int i = warp * 8 + r, m = lane + 32 * c;
+        if (i < n && m < n) J.a[(long long)i * J.lda + piv[m]] = a[r][c];
+      }
+  }
+  if (threadIdx.x == 0 && bad && J.flag) *J.flag = 1;
 }
 
 // inverse of a w x w (w <= 64) diagonal block: unit lower (upper = 0) or

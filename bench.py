@@ -72,6 +72,55 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
+def fp64_peak_tflops():
+    """cuBLAS DGEMM throughput measured live (4096^3, best of 5, CUDA events):
+    the FP64 roofline denominator (MEASURED_PEAKS.json has no FP64 figure)."""
+    import torch
+    n = 4096
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    best = float("inf")
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    return 2.0 * n ** 3 / best / 1e12
+
+
+def phase_rooflines(tim, records, hbm, fp64, apply_ms, apply_bytes):
+    """Per-phase achieved throughput against its binding roofline (SURVEY 8d
+    counts): sampling 16 B per sampled entry (write + source read), pivot LU
+    8 B per trailing-entry visit, dense fronts (2/3)n_p^3 + 2 n_p^2 nf +
+    2 n_p nf^2 flops, apply bytes from the stored factor. The HODLR phases
+    (a14-a16) have no count here and are left out of the weighted total."""
+    dense_flops = 0.0
+    for r in records:
+        if r.path == "dense" and r.n_pivot > 0:
+            npv, nf = r.n_pivot, r.front_size - r.n_pivot
+            dense_flops += (2.0 / 3.0) * npv ** 3 + 2.0 * npv * npv * nf + 2.0 * npv * nf * nf
+    out = {}
+
+    def put(name, amount, ms, unit, peak):
+        if ms <= 0:
+            return
+        ach = amount / (ms * 1e-3) / (1e9 if unit == "GB/s" else 1e12)
+        out[name] = {"achieved": ach, "unit": unit, "peak": peak, "frac": ach / peak, "ms": ms}
+
+    put("sample", 16.0 * tim["sample_entries"], tim["sample_ms"], "GB/s", hbm)
+    put("pivot_lu", 8.0 * tim["pivot_lu_visits"], tim["pivot_lu_ms"], "GB/s", hbm)
+    put("dense_front", dense_flops, tim["dense_front_ms"], "TFLOP/s", fp64)
+    put("apply", apply_bytes, apply_ms, "GB/s", hbm)
+    fac = [v for k, v in out.items() if k != "apply"]
+    tot = sum(v["ms"] for v in fac)
+    out["factor_weighted_frac"] = sum(v["frac"] * v["ms"] for v in fac) / tot if tot else None
+    out["factor_covered_ms"] = tot
+    out["fp64_peak_kind"] = "cuBLAS DGEMM 4096^3 measured live"
+    return out
+
+
 class ClockSampler:
     """SM clocks + throttle reasons sampled during the timed region, in-process
     through NVML (spawning nvidia-smi every 200 ms perturbs the sync-heavy GMRES
@@ -371,6 +420,7 @@ def run_gpu_arm(args, cfg, world, rank, local):
                    "symbolic_s": t_sym},
         "apply": {"ms": apply_ms, "bytes": apply_bytes, "gbs": apply_bytes / (apply_ms * 1e-3) / 1e9,
                   "frac_of_hbm": apply_bytes / (apply_ms * 1e-3) / 1e9 / hbm},
+        "phase_roofline": phase_rooflines(tim, F.stats.records, hbm, fp64_peak_tflops(), apply_ms, apply_bytes),
         "roofline": {"kernel": "k_full_pivot_lu", "bound": "hbm", "achieved": plu_gbs, "peak": hbm,
                      "unit": "GB/s", "frac": plu_gbs / hbm, "traffic": None, "peak_kind": pk_kind},
         "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": int(8 * (n + A.nnz) + 4 * A.nnz + 8 * (n + 1)),

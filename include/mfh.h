@@ -121,6 +121,32 @@ void mfh_etree_free(mfh_etree *t);
 int mfh_factorize(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const int64_t *indptr,
                   const int64_t *indices, const double *values, int mode, const mfh_params *params,
                   mfh_factor **out);
+/* ---- subtree-sharded factorization (one process per GPU) ------- */
+/* The exchange callback sums `count` doubles of the DEVICE buffer `d_buf` in
+ * place over all ranks (an all-reduce SUM). Work producing d_buf is enqueued on
+ * the context stream (mfh_ctx_info); the callback must order its collective
+ * after it (NCCL on that stream) or synchronize (host staging). Every slot is
+ * written by exactly one rank and is zero elsewhere, so the sum is exact.
+ * Returns 0 on success. */
+typedef int (*mfh_exchange_fn)(void *user, double *d_buf, int64_t count);
+typedef struct {
+  const int32_t *owner; /* per etree node id: the rank that factors it (subtrees whole) */
+  int rank;             /* this rank */
+  mfh_exchange_fn exchange;
+  void *user;
+} mfh_shard_t;
+/* mf_factorize over the nodes this rank owns, in global height order. After
+ * each height with a child -> parent edge between ranks, the children's
+ * updates are densified by their owners (bitwise the per-child term of the
+ * parent's sampler) into a fresh buffer and exchanged. The factor's stats
+ * cover the whole tree (per-node accounting exchanged). mfh_apply /
+ * mfh_gmres on it run the global apply levels on this rank's fronts, with the
+ * contribution buffer (upward) and x (downward) exchanged at the level
+ * boundaries where a dependency crosses ranks and x exchanged at the end:
+ * every rank gets the full solution, bitwise equal to the single-GPU one. */
+int mfh_factorize_sharded(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const int64_t *indptr,
+                          const int64_t *indices, const double *values, int mode, const mfh_params *params,
+                          const mfh_shard_t *shard, mfh_factor **out);
 int mfh_factor_stats(const mfh_factor *f, mfh_stats_t *out);
 int mfh_factor_records(const mfh_factor *f, mfh_record_t *out /* n_records */);
 int mfh_factor_timing(const mfh_factor *f, mfh_timing_t *out);

@@ -29,6 +29,15 @@ class mfh_params(C.Structure):
                 ("n_leaf", C.c_int64), ("max_rank", C.c_int64)]
 
 
+# int (*)(void *user, double *d_buf, int64_t count): in-place all-reduce SUM
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64)
+
+
+class mfh_shard_t(C.Structure):
+    _fields_ = [("owner", C.POINTER(C.c_int32)), ("rank", C.c_int), ("exchange", EXCHANGE_FN),
+                ("user", C.c_void_p)]
+
+
 class mfh_stats_t(C.Structure):
     _fields_ = [(k, C.c_int64) for k in (
         "peak_stored_reals", "retained_reals", "structured_fronts", "dense_fronts",
@@ -122,6 +131,8 @@ def _sig(lib):
         "mfh_etree_fetch": (C.c_int, [P, P, P, P, P, P, P]),
         "mfh_etree_free": (None, [P]),
         "mfh_factorize": (C.c_int, [P, P, I64, P, P, P, C.c_int, C.POINTER(mfh_params), PP]),
+        "mfh_factorize_sharded": (C.c_int, [P, P, I64, P, P, P, C.c_int, C.POINTER(mfh_params),
+                                            C.POINTER(mfh_shard_t), PP]),
         "mfh_factor_stats": (C.c_int, [P, C.POINTER(mfh_stats_t)]),
         "mfh_factor_records": (C.c_int, [P, P]),
         "mfh_factor_timing": (C.c_int, [P, C.POINTER(mfh_timing_t)]),

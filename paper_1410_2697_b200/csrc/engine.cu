@@ -935,6 +935,17 @@ struct mfh_factor {
   mfh_timing_t timing{};
   // apply
   std::unique_ptr<mfh::ApplyPlan> apply;
+  // subtree-sharded factor: owner rank per post index, mine = owner == rank
+  bool sharded = false;
+  std::vector<int> owner;
+  std::vector<int8_t> mine;
+  int rank = 0, world = 1;
+  mfh_exchange_fn exchange = nullptr;
+  void *xuser = nullptr;
+  void exchange_or_throw(double *d, int64_t count) {
+    if (count <= 0) return;
+    if (exchange(xuser, d, count) != 0) throw mfh::runtime_error("shard exchange callback failed");
+  }
 };
 
 namespace mfh {
@@ -947,6 +958,7 @@ struct Factorizer {
   Ctx *ctx;
   const mfh_etree *et;
   mfh_params P;
+  const mfh_shard_t *shard = nullptr;
   bool accel;
   int64_t n;
   // permuted matrix on device
@@ -1908,6 +1920,100 @@ struct Factorizer {
     }
   }
 
+  // ---- sharded: every cut root's update, densified by the
+  // owner through a virtual front with no pivots (so each entry is bitwise
+  // the per-child term the parent's sampler would add), summed over ranks;
+  // the top fronts then see every cut root as a dense child
+  void exchange_updates(const std::vector<int> &cuts) {
+    std::vector<int64_t> coff;
+    int64_t T = 0;
+    for (int q : cuts) {
+      coff.push_back(T);
+      T += (int64_t)F->fronts[q].nf * F->fronts[q].nf;
+    }
+    Sink s{ctx};
+    s.sync_reset();
+    check_flags(0);
+    ctx->scratch.reset();
+    double *imp = F->arena.d(std::max<int64_t>(1, T));
+    CK(cudaMemsetAsync(imp, 0, sizeof(double) * std::max<int64_t>(1, T), ctx->s));
+    std::vector<DFront> dfr;
+    std::vector<DChild> dch;
+    std::vector<SReq> reqs;
+    for (size_t k = 0; k < cuts.size(); ++k) {
+      if (!F->mine[cuts[k]]) continue;
+      FrontH &c = F->fronts[cuts[k]];
+      std::vector<int> to(c.nf);
+      for (int q = 0; q < c.nf; ++q) to[q] = q;
+      DChild ch{};
+      ch.to_child = s.push_keep(to);
+      ch.n = c.nf;
+      if (c.upd == 0) {
+        ch.kind = 0;
+        ch.dense = c.upd_dense;
+        ch.ldd = c.upd_ld;
+      } else {
+        ch.kind = 1;
+        ch.hn = F->trees[c.ff].d_nodes;
+        ch.W = c.W;
+        ch.Vt = c.Vt;
+        ch.rw = c.rw;
+        ch.ldw = c.ldw;
+        ch.ldv = c.ldv;
+      }
+      DFront d{};
+      d.ids = c.d_ids + c.npv;
+      d.nh = c.nf;
+      d.npv = 0;  // no seed: every entry is the child term alone
+      d.child_begin = (int)dch.size();
+      dch.push_back(ch);
+      d.child_end = (int)dch.size();
+      reqs.push_back(SReq{(int)dfr.size(), c.nf, c.nf, nullptr, nullptr, 0, 0, imp + coff[k], c.nf});
+      dfr.push_back(d);
+    }
+    if (!reqs.empty()) {
+      DFront *dF = s.push_keep(dfr);
+      DChild *dC = s.push_keep(dch);
+      run_sample(s, reqs, dF, dC);
+    }
+    F->exchange_or_throw(imp, T);
+    for (size_t k = 0; k < cuts.size(); ++k) {
+      FrontH &c = F->fronts[cuts[k]];
+      c.upd = 0;
+      c.upd_dense = imp + coff[k];
+      c.upd_ld = c.nf;
+    }
+  }
+
+  // ---- sharded: the numeric accounting of fronts factored elsewhere, for the
+  // whole-tree stats replay
+  void exchange_accounting() {
+    const size_t nf_ = F->fronts.size();
+    std::vector<double> acc(4 * nf_, 0.0);
+    for (size_t q = 0; q < nf_; ++q) {
+      if (!F->mine[q]) continue;
+      FrontH &f = F->fronts[q];
+      acc[4 * q] = (double)f.front_reals;
+      acc[4 * q + 1] = (double)f.factor_reals;
+      acc[4 * q + 2] = (double)f.upd_reals;
+      acc[4 * q + 3] = (double)f.hint;
+    }
+    double *d = ctx->scratch.d(std::max<size_t>(1, acc.size()));
+    upload(ctx->s, d, acc.data(), sizeof(double) * acc.size());  // ordered on the library stream
+    F->exchange_or_throw(d, (int64_t)acc.size());
+    CK(cudaStreamSynchronize(ctx->s));
+    CK(cudaMemcpy(acc.data(), d, sizeof(double) * acc.size(), cudaMemcpyDeviceToHost));
+    ctx->scratch.reset();
+    for (size_t q = 0; q < nf_; ++q) {
+      if (F->mine[q]) continue;
+      FrontH &f = F->fronts[q];
+      f.front_reals = (int64_t)acc[4 * q];
+      f.factor_reals = (int64_t)acc[4 * q + 1];
+      f.upd_reals = (int64_t)acc[4 * q + 2];
+      f.hint = (int64_t)acc[4 * q + 3];
+    }
+  }
+
   void run(const HostCsr &A, int mode) {
     auto t0 = std::chrono::steady_clock::now();
     const bool trace = getenv("MFH_HOST_TRACE") != nullptr;
@@ -2059,6 +2165,25 @@ struct Factorizer {
       max_nh = std::max<int64_t>(max_nh, f.nh);
     }
     mark_t("fronts");
+    if (shard) {
+      F->sharded = true;
+      F->rank = shard->rank;
+      F->exchange = shard->exchange;
+      F->xuser = shard->user;
+      if (!shard->owner || !shard->exchange) throw value_error("shard needs an owner array and an exchange callback");
+      F->owner.assign(F->fronts.size(), 0);
+      F->mine.assign(F->fronts.size(), 0);
+      int world = 1;
+      for (size_t q = 0; q < F->fronts.size(); ++q) {
+        int o = shard->owner[F->fronts[q].node];
+        if (o < 0) throw value_error("shard owner ranks must be non-negative");
+        F->owner[q] = o;
+        F->mine[q] = o == shard->rank;
+        world = std::max(world, o + 1);
+      }
+      F->world = std::max(world, shard->rank + 1);
+    }
+    auto active = [&](size_t q) { return !F->sharded || F->mine[q] != 0; };
     if (any_struct) {
       if (!(P.eps > 0.0 && P.eps < 1.0)) throw value_error("eps must lie in (0, 1)");
       if (P.n_leaf < 1) throw value_error("n_leaf must be positive");
@@ -2093,7 +2218,17 @@ struct Factorizer {
     // ---- heights
     std::vector<std::vector<int>> byh(maxh + 1);
     for (size_t q = 0; q < F->fronts.size(); ++q)
-      if (F->fronts[q].nh > 0) byh[F->fronts[q].height].push_back((int)q);
+      if (F->fronts[q].nh > 0 && active(q)) byh[F->fronts[q].height].push_back((int)q);
+    // sharded: heights after which a child -> parent update crosses ranks (the
+    // same on every rank: computed from the global tree)
+    std::vector<std::vector<int>> cut_at(maxh + 1);
+    if (F->sharded)
+      for (size_t q = 0; q < F->fronts.size(); ++q) {
+        FrontH &f = F->fronts[q];
+        int64_t par = et->parent[f.node];
+        if (par < 0 || f.nh == 0 || f.nf == 0) continue;
+        if (F->owner[pidx[par]] != F->owner[q]) cut_at[f.height].push_back((int)q);
+      }
     // structured-front plans (trees, blocks, BDLR selections) are symbolic: a
     // planner thread computes them, in processing order, while the GPU works
     {
@@ -2130,7 +2265,10 @@ struct Factorizer {
     // scratch memory; per-height phase events are evaluated at the end.
     int used = 0;
     for (int h = 0; h <= maxh; ++h) {
-      if (byh[h].empty()) continue;
+      if (byh[h].empty()) {
+        if (!cut_at[h].empty()) exchange_updates(cut_at[h]);
+        continue;
+      }
       while ((int)ctx->evpool.size() < 8 * (used + 1)) {
         cudaEvent_t e;
         CK(cudaEventCreate(&e));
@@ -2151,6 +2289,7 @@ struct Factorizer {
         check_flags(0);
         ctx->scratch.reset();
       }
+      if (!cut_at[h].empty()) exchange_updates(cut_at[h]);
     }
     CK(cudaEventRecord(e_end, ctx->s));
     {
@@ -2188,6 +2327,7 @@ struct Factorizer {
     F->timing.skeleton_ms = tsum[2];
     F->timing.hodlr_factor_ms = tsum[3];
     F->timing.eliminate_ms = tsum[5];
+    if (F->sharded) exchange_accounting();
     // ---- stats replay in post order (multifrontal.py:76-86, 478-529)
     int64_t retained = 0, live = 0, peak = 0;
     F->records.clear();
@@ -2239,6 +2379,12 @@ struct ApplyPlan {
   double *bu = nullptr, *xw = nullptr, *y = nullptr, *cbuf = nullptr, *xf = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
+  // sharded: segment k + 1 runs after exchange k (buffer, count); the first
+  // segment is (graph, exec)
+  std::vector<cudaGraph_t> seg_graph;
+  std::vector<cudaGraphExec_t> seg_exec;
+  std::vector<int64_t> seg_nodes;
+  std::vector<std::pair<double *, int64_t>> xchg;
   double bytes = 0;  // algorithmic bytes per apply
   int64_t nodes = 0;
 };
@@ -2344,34 +2490,132 @@ static void build_apply(mfh_factor *F) {
   double *bu = AP->bu, *xw = AP->xw, *y = AP->y, *cbuf = AP->cbuf;
   double bytes = 0;
   // apply levels count only pivot-carrying nodes: merge nodes (npv = 0) do no
-  // solve work, and skipping them collapses the long merge chains
-  std::vector<int> ah(F->fronts.size(), -1), sub(F->fronts.size(), -1);
-  int maxh = 0;
-  for (size_t q = 0; q < F->fronts.size(); ++q) {
-    FrontH &f = F->fronts[q];
-    int below = -1;
-    for (int c : f.allkids) below = std::max(below, sub[c]);
-    if (f.nh > 0 && f.npv > 0) {
-      ah[q] = below + 1;
-      sub[q] = ah[q];
-      maxh = std::max(maxh, ah[q]);
-    } else {
-      sub[q] = below;
+  // solve work, and skipping them collapses the long merge chains.
+  // Levels are global (all ranks agree); a sharded factor runs its own fronts.
+  const bool sh = F->sharded;
+  const size_t NF = F->fronts.size();
+  std::vector<int> ah(NF, -1);
+  int maxh = -1;
+  {
+    std::vector<int> sub(NF, -1);
+    for (size_t q = 0; q < NF; ++q) {
+      FrontH &f = F->fronts[q];
+      int below = -1;
+      for (int c : f.allkids) below = std::max(below, sub[c]);
+      if (f.nh > 0 && f.npv > 0) {
+        ah[q] = below + 1;
+        sub[q] = ah[q];
+        maxh = std::max(maxh, ah[q]);
+      } else {
+        sub[q] = below;
+      }
     }
   }
   std::vector<std::vector<int>> byh(maxh + 1);
-  for (size_t q = 0; q < F->fronts.size(); ++q)
-    if (ah[q] >= 0) byh[ah[q]].push_back((int)q);
+  for (size_t q = 0; q < NF; ++q)
+    if (ah[q] >= 0 && (!sh || F->mine[q])) byh[ah[q]].push_back((int)q);
+  // sharded exchange points (symbolic, identical on every rank): upward before
+  // level L when a level-L front has a descendant of another rank at a level
+  // not yet exchanged; downward before L when a level-L front has an ancestor
+  // of another rank at a level written since the last exchange
+  std::vector<char> ex_up(maxh + 2, 0), ex_dn(maxh + 2, 0);
+  if (sh) {
+    const int W = F->world;
+    std::vector<int> dsub(NF * W, -1), dmax(NF * W, -1);
+    for (size_t q = 0; q < NF; ++q) {
+      for (int c : F->fronts[q].allkids)
+        for (int o = 0; o < W; ++o) dmax[q * W + o] = std::max(dmax[q * W + o], dsub[(size_t)c * W + o]);
+      for (int o = 0; o < W; ++o) dsub[q * W + o] = dmax[q * W + o];
+      if (ah[q] >= 0) dsub[q * W + F->owner[q]] = std::max(dsub[q * W + F->owner[q]], ah[q]);
+    }
+    const int INF = 1 << 30;
+    std::vector<int> amin(NF * W, INF);
+    for (size_t q = NF; q-- > 0;)  // parents come after children in post order
+      for (int c : F->fronts[q].allkids) {
+        for (int o = 0; o < W; ++o) amin[(size_t)c * W + o] = amin[q * W + o];
+        if (ah[q] >= 0) amin[(size_t)c * W + F->owner[q]] = std::min(amin[(size_t)c * W + F->owner[q]], ah[q]);
+      }
+    std::vector<int> mo(NF, -1), ma(NF, INF);
+    for (size_t q = 0; q < NF; ++q)
+      for (int o = 0; o < W; ++o)
+        if (o != F->owner[q]) {
+          mo[q] = std::max(mo[q], dmax[q * W + o]);
+          ma[q] = std::min(ma[q], amin[q * W + o]);
+        }
+    std::vector<std::vector<int>> all_at(maxh + 1);
+    for (size_t q = 0; q < NF; ++q)
+      if (ah[q] >= 0) all_at[ah[q]].push_back((int)q);
+    int last = 0;
+    for (int L = 0; L <= maxh; ++L) {
+      bool need = false;
+      for (int q : all_at[L]) need |= mo[q] >= last;
+      if (need) {
+        ex_up[L] = 1;
+        last = L;
+      }
+    }
+    int synced = INF;
+    for (int L = maxh; L >= 0; --L) {
+      bool need = false;
+      for (int q : all_at[L]) need |= ma[q] <= synced;
+      if (need) {
+        ex_dn[L] = 1;
+        synced = L;
+      }
+    }
+  }
   long long *perm = F->d_perm;
   double *db = AP->d_b, *dx = AP->d_x;
   int grid_n = (int)std::min<int64_t>(cdiv(std::max<int64_t>(n, 1), 256), 148 * 8);
+  // sharded: exchanges split the recorded ops into segments; an exchange
+  // all-reduces this rank's own slots / pivots (selected, others zero) and
+  // copies the result back
+  std::vector<std::vector<std::function<void(cudaStream_t)>>> segs;
+  int8_t *cb_mask = nullptr, *x_mask = nullptr;
+  double *cb_tmp = nullptr, *x_tmp = nullptr;
+  const int64_t ncb = std::max<int64_t>(1, tot);
+  if (sh) {
+    std::vector<int8_t> cm(ncb, 0), xm(std::max<int64_t>(1, n), 0);
+    for (size_t q = 0; q < NF; ++q) {
+      if (!F->mine[q]) continue;
+      FrontH &f = F->fronts[q];
+      if (off[q] >= 0)
+        for (int j = 0; j < f.nf; ++j) cm[off[q] + j] = 1;
+      for (int j = 0; j < f.npv; ++j) xm[f.piv_lo + j] = 1;
+    }
+    cb_mask = (int8_t *)ar.alloc(cm.size());
+    x_mask = (int8_t *)ar.alloc(xm.size());
+    upload(ctx->s, cb_mask, cm.data(), cm.size());
+    upload(ctx->s, x_mask, xm.data(), xm.size());
+    cb_tmp = ar.d(ncb);
+    x_tmp = ar.d(std::max<int64_t>(1, n));
+    sk.launch([=](cudaStream_t s) {
+      CK(cudaMemsetAsync(cbuf, 0, sizeof(double) * ncb, s));
+      CK(cudaMemsetAsync(xw, 0, sizeof(double) * std::max<int64_t>(1, n), s));
+    });
+  }
+  auto exchange_point = [&](double *buf, const int8_t *mask, double *tmp, int64_t cnt) {
+    int g = (int)std::min<int64_t>(cdiv(cnt, 256), 148 * 8);
+    sk.launch([=](cudaStream_t s) {
+      k_mask_select<<<g, 256, 0, s>>>(buf, mask, tmp, cnt);
+      check_launch();
+    });
+    segs.push_back(std::move(sk.ops));
+    sk.ops.clear();
+    AP->xchg.push_back({tmp, cnt});
+    sk.launch([=](cudaStream_t s) {
+      CK(cudaMemcpyAsync(buf, tmp, sizeof(double) * cnt, cudaMemcpyDeviceToDevice, s));
+    });
+  };
   sk.launch([=](cudaStream_t s) {
     k_scatter_perm<<<grid_n, 256, 0, s>>>(db, perm, bu, n);
     check_launch();
   });
   bytes += 24.0 * n;
   // ---------------- upward: b_u[fro] -= apply_fp(pp_solve(b_u[piv]))
-  for (int h = 0; h <= maxh; ++h) {
+  auto upward = [&](std::vector<std::vector<int>> &byh) {
+  for (int h = 0; h < (int)byh.size(); ++h) {
+    if (sh && ex_up[h]) exchange_point(cbuf, cb_mask, cb_tmp, ncb);
     auto &fis = byh[h];
     if (fis.empty()) continue;
     std::vector<int64_t> gl;
@@ -2387,7 +2631,6 @@ static void build_apply(mfh_factor *F) {
       check_launch();
     });
     std::vector<GemvJob> j0, j1, j2;
-    std::vector<std::pair<int, double *>> lr;  // structured LR fp: (front, tmp)
     for (int q : fis) {
       FrontH &f = F->fronts[q];
       if (f.nf == 0) continue;
@@ -2413,8 +2656,11 @@ static void build_apply(mfh_factor *F) {
     run_gemv(sk, j1);
     run_gemv(sk, j2);
   }
+  };
   // ---------------- downward: x[piv] = pp_solve(b_u[piv] - apply_pf(x[fro]))
-  for (int h = maxh; h >= 0; --h) {
+  auto downward = [&](std::vector<std::vector<int>> &byh) {
+  for (int h = (int)byh.size() - 1; h >= 0; --h) {
+    if (sh && ex_dn[h]) exchange_point(xw, x_mask, x_tmp, std::max<int64_t>(1, n));
     auto &fis = byh[h];
     if (fis.empty()) continue;
     std::vector<GemvJob> ja, jb;
@@ -2445,6 +2691,10 @@ static void build_apply(mfh_factor *F) {
     run_gemv(sk, ja);
     run_gemv(sk, jb);
   }
+  };
+  upward(byh);
+  downward(byh);
+  if (sh) exchange_point(xw, x_mask, x_tmp, std::max<int64_t>(1, n));  // every rank gets every pivot
   sk.launch([=](cudaStream_t s) {
     k_gather_perm<<<grid_n, 256, 0, s>>>(xw, perm, dx, n);
     check_launch();
@@ -2452,16 +2702,46 @@ static void build_apply(mfh_factor *F) {
   // capture
   CK(cudaStreamSynchronize(ctx->s));
   auto tb1 = std::chrono::steady_clock::now();
-  CK(cudaStreamBeginCapture(ctx->s, cudaStreamCaptureModeThreadLocal));
-  for (auto &op : sk.ops) op(ctx->s);
-  CK(cudaStreamEndCapture(ctx->s, &AP->graph));
-  CK(cudaGraphInstantiate(&AP->exec, AP->graph, 0));
+  auto capture = [&](std::vector<std::function<void(cudaStream_t)>> &ops, cudaGraph_t *g, cudaGraphExec_t *e) {
+    CK(cudaStreamBeginCapture(ctx->s, cudaStreamCaptureModeThreadLocal));
+    for (auto &op : ops) op(ctx->s);
+    CK(cudaStreamEndCapture(ctx->s, g));
+    CK(cudaGraphInstantiate(e, *g, 0));
+  };
+  if (sh) {
+    segs.push_back(std::move(sk.ops));
+    capture(segs[0], &AP->graph, &AP->exec);
+    for (size_t k = 1; k < segs.size(); ++k) {
+      cudaGraph_t g;
+      cudaGraphExec_t e;
+      capture(segs[k], &g, &e);
+      AP->seg_graph.push_back(g);
+      AP->seg_exec.push_back(e);
+      AP->seg_nodes.push_back((int64_t)segs[k].size());
+    }
+  } else {
+    capture(sk.ops, &AP->graph, &AP->exec);
+  }
   auto tb2 = std::chrono::steady_clock::now();
   F->timing.apply_build_ms = std::chrono::duration<double, std::milli>(tb1 - tb0).count();
   F->timing.apply_instantiate_ms = std::chrono::duration<double, std::milli>(tb2 - tb1).count();
   AP->bytes = bytes;
-  AP->nodes = (int64_t)sk.ops.size();
+  AP->nodes = sh ? (int64_t)segs[0].size() : (int64_t)sk.ops.size();
   F->apply = std::move(AP);
+}
+
+// A->d_b -> A->d_x; a sharded factor exchanges the contribution buffer
+// between its two graphs and the solution after them
+static void apply_run(mfh_factor *F) {
+  Ctx *ctx = F->ctx;
+  ApplyPlan *A = F->apply.get();
+  CK(cudaGraphLaunch(A->exec, ctx->s));
+  ctx->launches += A->nodes;
+  for (size_t k = 0; k < A->xchg.size(); ++k) {
+    F->exchange_or_throw(A->xchg[k].first, A->xchg[k].second);
+    CK(cudaGraphLaunch(A->seg_exec[k], ctx->s));
+    ctx->launches += A->seg_nodes[k];
+  }
 }
 
 static void apply_device(mfh_factor *F, const double *d_in, double *d_out) {
@@ -2471,8 +2751,7 @@ static void apply_device(mfh_factor *F, const double *d_in, double *d_out) {
   int64_t n = F->n;
   if (n == 0) return;
   CK(cudaMemcpyAsync(A->d_b, d_in, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s));
-  CK(cudaGraphLaunch(A->exec, ctx->s));
-  ctx->launches += A->nodes;
+  apply_run(F);
   CK(cudaMemcpyAsync(d_out, A->d_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s));
 }
 
@@ -2578,9 +2857,9 @@ extern "C" int mfh_ctx_sync(mfh_ctx *ctx) {
   MFH_CATCH
 }
 
-extern "C" int mfh_factorize(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const int64_t *indptr,
-                             const int64_t *indices, const double *values, int mode,
-                             const mfh_params *params, mfh_factor **out) {
+static int factorize_common(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const int64_t *indptr,
+                            const int64_t *indices, const double *values, int mode, const mfh_params *params,
+                            const mfh_shard_t *shard, mfh_factor **out) {
   mfh_factor *F = nullptr;
   MFH_TRY
   if (mode != MFH_CONVENTIONAL && mode != MFH_ACCELERATED) throw value_error("unknown mode");
@@ -2600,6 +2879,7 @@ extern "C" int mfh_factorize(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const 
   fz.ctx = &ctx->c;
   fz.et = t;
   fz.P = *params;
+  fz.shard = shard;
   fz.run(A, mode);
   F->timing.kernel_launches = ctx->c.launches - launches0;
   *out = F;
@@ -2628,6 +2908,22 @@ extern "C" int mfh_factorize(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const 
     return MFH_ERUNTIME;
   }
   return MFH_OK;
+}
+
+extern "C" int mfh_factorize(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const int64_t *indptr,
+                             const int64_t *indices, const double *values, int mode,
+                             const mfh_params *params, mfh_factor **out) {
+  return factorize_common(ctx, t, n, indptr, indices, values, mode, params, nullptr, out);
+}
+
+extern "C" int mfh_factorize_sharded(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const int64_t *indptr,
+                                     const int64_t *indices, const double *values, int mode,
+                                     const mfh_params *params, const mfh_shard_t *shard, mfh_factor **out) {
+  if (!shard) {
+    set_last_error("mfh_factorize_sharded needs a shard description");
+    return MFH_EVALUE;
+  }
+  return factorize_common(ctx, t, n, indptr, indices, values, mode, params, shard, out);
 }
 
 extern "C" int mfh_factor_stats(const mfh_factor *f, mfh_stats_t *out) {
@@ -2686,6 +2982,8 @@ extern "C" void mfh_factor_free(mfh_factor *f) {
   if (f->apply) {
     if (f->apply->exec) cudaGraphExecDestroy(f->apply->exec);
     if (f->apply->graph) cudaGraphDestroy(f->apply->graph);
+    for (auto e : f->apply->seg_exec) cudaGraphExecDestroy(e);
+    for (auto g : f->apply->seg_graph) cudaGraphDestroy(g);
   }
   f->arena.release();
   delete f;
@@ -2703,8 +3001,7 @@ extern "C" int mfh_apply(mfh_factor *f, const double *b, double *x, int64_t nrhs
       apply_device(f, b + r * n, x + r * n);
     } else {
       CK(cudaMemcpyAsync(A->d_b, b + r * n, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->s));
-      CK(cudaGraphLaunch(A->exec, ctx->s));
-      ctx->launches += A->nodes;
+      apply_run(f);
       CK(cudaMemcpyAsync(x + r * n, A->d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->s));
     }
   }
@@ -2720,9 +3017,9 @@ extern "C" int mfh_apply_bench(mfh_factor *f, int64_t reps, double *ms_per_apply
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  CK(cudaGraphLaunch(A->exec, ctx->s));
+  apply_run(f);
   CK(cudaEventRecord(e0, ctx->s));
-  for (int64_t r = 0; r < reps; ++r) CK(cudaGraphLaunch(A->exec, ctx->s));
+  for (int64_t r = 0; r < reps; ++r) apply_run(f);
   CK(cudaEventRecord(e1, ctx->s));
   CK(cudaEventSynchronize(e1));
   float ms;

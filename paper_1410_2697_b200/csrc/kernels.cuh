@@ -221,6 +221,13 @@ __global__ void k_sample(const SReq *__restrict__ reqs, const int2 *__restrict__
   }
 }
 
+// dst = mask ? src : 0 (a select: no arithmetic on the dropped values)
+__global__ void k_mask_select(const double *__restrict__ src, const int8_t *__restrict__ mask,
+                              double *__restrict__ dst, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = mask[i] ? src[i] : 0.0;
+}
+
 // ---------------------------------------------------------------------------
 // batched 2-D copy / gather
 // ---------------------------------------------------------------------------

@@ -1,0 +1,89 @@
+"""Subtree-sharded factorization on the GPU: world-size-2 and -3
+gloo groups of processes sharing one GPU (the exchanges are host-side between
+launches, so no kernel waits on another rank). The sharded preconditioner's
+apply, GMRES solution and iteration count, stats and records must be bitwise
+equal to the single-GPU factorization's."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "p7_16": (lambda PR: PR.gen_poisson7(16, 16, 16)[0], 32, dict(n_c=96, eps=1e-5, d=1, n_leaf=32)),
+    "hex_8": (lambda PR: PR.gen_hex_q1(8, seed=3)[0], 32, dict(n_c=96, eps=1e-4, d=1, n_leaf=32)),
+}
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _recs(F):
+    return [(r.node_id, r.front_size, r.n_pivot, r.path, r.max_offdiag_rank, r.stored_reals)
+            for r in F.stats.records]
+
+
+def _worker(rank, world, port, case, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    try:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_1410_2697_b200 as P
+        from paper_1410_2697_b200 import problems as PR
+        from paper_1410_2697_b200.sharded import mf_factorize_sharded
+        gen, leaf, kw = CASES[case]
+        A = gen(PR)
+        tree = P.build_elimination_tree(P.nested_dissection(P.adjacency_graph(A), leaf), A)
+        params = P.MfParams(**kw)
+        b = np.random.default_rng(0).standard_normal(A.n_rows)
+        F = mf_factorize_sharded(A, tree, P.ACCELERATED, params)
+        x = P.mf_solve(F, b)
+        xg, h = P.gmres(A, b, M=P.mf_preconditioner(F), tol=1e-10, restart=30)
+        out = dict(rank=rank, x=x, xg=xg, its=h.iterations, hist=np.asarray(h.residuals), recs=_recs(F),
+                   peak=F.stats.peak_stored_reals, counts=(F.stats.structured_fronts, F.stats.dense_fronts),
+                   calls=F.exchange.calls, owners=F.partition.owners())
+        if rank == 0:
+            F1 = P.mf_factorize(A, tree, P.ACCELERATED, params)
+            x1g, h1 = P.gmres(A, b, M=P.mf_preconditioner(F1), tol=1e-10, restart=30)
+            out.update(x1=P.mf_solve(F1, b), x1g=x1g, its1=h1.iterations, hist1=np.asarray(h1.residuals),
+                       recs1=_recs(F1), peak1=F1.stats.peak_stored_reals,
+                       counts1=(F1.stats.structured_fronts, F1.stats.dense_fronts))
+        dist.barrier()
+        q.put(out)
+        dist.destroy_process_group()
+    except Exception as e:  # surfaced by the parent
+        import traceback
+        q.put(dict(rank=rank, error=traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world,case", [(2, "p7_16"), (3, "p7_16"), (2, "hex_8")])
+def test_sharded_factor_bitwise_equals_single(world, case):
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    outs = sorted((q.get(timeout=240) for _ in ps), key=lambda o: o["rank"])
+    for p in ps:
+        p.join(timeout=60)
+    for o in outs:
+        assert "error" not in o, o.get("error")
+    r0 = outs[0]
+    assert len(set(r0["owners"].tolist())) == world  # every rank owns fronts
+    for o in outs:
+        assert o["calls"] > 0
+        np.testing.assert_array_equal(o["x"], r0["x1"])
+        np.testing.assert_array_equal(o["xg"], r0["x1g"])
+        assert o["its"] == r0["its1"]
+        np.testing.assert_array_equal(o["hist"], r0["hist1"])
+        assert o["recs"] == r0["recs1"]
+        assert o["peak"] == r0["peak1"] and o["counts"] == r0["counts1"]

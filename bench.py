@@ -14,8 +14,11 @@ Arms:
                       oracle restatement; the Python reference cannot travel
                       to the GPU box), timed on the full workload (1 core)
 
-Multi-GPU (torchrun, N > 1): replicas only — every rank factors and solves its
-own copy (independent systems, no collective on the data path); value is the
+Multi-GPU (torchrun, N > 1): the factorization is sharded by nested-dissection
+subtree (SURVEY 8e): each rank factors the subtrees and top fronts it owns;
+cut-child updates, preconditioner contributions and solution pieces cross
+ranks through NCCL all-reduces on the library stream. GMRES runs replicated on
+that sharded preconditioner. Strong scaling: one system per job, value is the
 max-over-ranks step time.
 """
 
@@ -187,11 +190,14 @@ def dist_setup(n_gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("MFH_BENCH_EMULATE"):
+        # diagnostics on a one-GPU box: every rank on cuda:0, gloo host exchanges
+        local = 0
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if os.environ.get("MFH_BENCH_EMULATE") else "nccl")
     return world, rank, local
 
 
@@ -314,9 +320,19 @@ def run_gpu_arm(args, cfg, world, rank, local):
     split = {"factor_s": [], "solve_s": [], "gmres_inner_s": [], "apply_build_s": [], "gmres_sync_s": [],
              "gmres_apply_enqueue_s": []}
 
+    if world > 1:
+        from paper_1410_2697_b200.sharded import SubtreePartition, mf_factorize_sharded
+        part = SubtreePartition(et, world)
+
+        def factorize():
+            return mf_factorize_sharded(A, et, P.ACCELERATED, params, partition=part)
+    else:
+        def factorize():
+            return P.mf_factorize(A, et, P.ACCELERATED, params)
+
     def step_device():
         t0 = time.perf_counter()
-        F = P.mf_factorize(A, et, P.ACCELERATED, params)
+        F = factorize()
         t1 = time.perf_counter()
         ops = _lib.mfh_gmres_ops()
         ops.A = dev_op.handle
@@ -336,7 +352,7 @@ def run_gpu_arm(args, cfg, world, rank, local):
         return F, its.value, bool(conv.value), hist[max(0, nh.value - 1)]
 
     def step_e2e():  # public API, host b -> host x
-        F = P.mf_factorize(A, et, P.ACCELERATED, params)
+        F = factorize()
         x, h = P.gmres(A, b, M=P.mf_preconditioner(F), tol=cfg["tol"], restart=cfg["restart"])
         return F, x, h
 
@@ -399,11 +415,12 @@ def run_gpu_arm(args, cfg, world, rank, local):
         return
     line = {
         "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["desc"], "n": n, "nnz": A.nnz, **cfg["params"], "nd_leaf": cfg["leaf"],
                    "restart": cfg["restart"], "tol": cfg["tol"], "rhs": f"{cfg['rhs']} seed 0",
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": f"subtree{world}" if world > 1 else "single",
                    "l2": "flushed (256 MiB write) before every timed step"},
         "gmres": {"iterations": its, "converged": conv, "final_rel_residual": float(res),
                   "true_rel_residual_e2e": true_res, "e2e_iterations": he.iterations},

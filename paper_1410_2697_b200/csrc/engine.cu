@@ -696,7 +696,7 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
   static size_t dyn_max = 0;
   static const void *fns[6] = {(const void *)k_plu_cta2<true>,      (const void *)k_plu_cta2<false>,
                                (const void *)k_plu_cluster2<true>,  (const void *)k_plu_cluster2<false>,
-                               (const void *)k_plu_grid2<true>,     (const void *)k_plu_grid2<false>};
+                               (const void *)k_plu_groups<true>,    (const void *)k_plu_groups<false>};
   if (!attr_done) {
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
@@ -721,7 +721,7 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
   int nsm = 148;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
   auto cta_bytes = [](int m, int n) { return sizeof(double) * (size_t)m * n + sizeof(int) * (size_t)(m + n) + 16; };
-  std::vector<int> small[3], cl8, cl16, grd_s, grd_g;
+  std::vector<int> small[3], cl8, cl16, grd;
   size_t smax[3] = {48 * 1024, 100 * 1024, dyn_max};
   for (int q = 0; q < (int)jobs.size(); ++q) {
     const PluJob &j = jobs[q];
@@ -733,10 +733,8 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
       cl8.push_back(q);
     } else if (plu_dist_bytes(j.m, j.n, CS, true) <= dyn_max) {
       cl16.push_back(q);
-    } else if (plu_dist_bytes(j.m, j.n, nsm, true) <= dyn_max) {
-      grd_s.push_back(q);
     } else if (plu_dist_bytes(j.m, j.n, nsm, false) <= dyn_max) {
-      grd_g.push_back(q);
+      grd.push_back(q);
     } else {
       throw runtime_error("complete-pivot core too large for the shared-memory bookkeeping");
     }
@@ -744,17 +742,117 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
   PluJob *dj = sk.push(jobs);
   // every descriptor the side stream reads is pushed (on the main stream)
   // BEFORE the fork event, so the side-stream kernels see them
-  int *ids_cl16 = sk.push(cl16), *ids_cl8 = sk.push(cl8), *ids_gs = sk.push(grd_s), *ids_gg = sk.push(grd_g);
+  int *ids_cl16 = sk.push(cl16), *ids_cl8 = sk.push(cl8);
+  // grid class: the cooperative launch is split into groups of CTAs, one core
+  // sequence per group (LPT over min(m, n), the step-count bound), so large
+  // cores of one height factor concurrently; a group whose cores do not fit
+  // the shared-memory row layout at its size goes to a second (global-row) launch
+  struct GridLaunch {
+    std::vector<int> first, cptr, ids;
+    size_t smem = 0;
+  } gl[2];
   GridScratch gs{};
-  if (!grd_s.empty() || !grd_g.empty()) {
+  if (!grd.empty()) {
+    std::vector<int> order = grd;
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+      long long sa = std::min(jobs[a].m, jobs[a].n), sb = std::min(jobs[b].m, jobs[b].n);
+      if (sa != sb) return sa > sb;
+      return a < b;
+    });
+    // per-step cost model (measured at C2): a latency floor plus the trailing
+    // update spread over the group's CTAs; steps bounded by min(m, n). Groups
+    // get CTAs in proportion to their work and must keep rows in shared memory.
+    const double LAT = 8.0, PER = 4.0e-4;  // us per step, us per entry per CTA
+    auto steps = [&](int q) { return (double)std::min(jobs[q].m, jobs[q].n); };
+    auto ent = [&](int q) { return (double)jobs[q].m * jobs[q].n; };
+    auto gmin = [&](int q) {
+      for (int G = 1; G <= nsm; ++G)
+        if (plu_dist_bytes(jobs[q].m, jobs[q].n, G, true) <= dyn_max) return G;
+      return nsm + 1;
+    };
+    static const int max_groups = std::getenv("MFH_PLU_MAXGROUPS") ? std::atoi(std::getenv("MFH_PLU_MAXGROUPS"))
+                                                                     : std::max(1, nsm / 16);
+    double best_cost = 1e300;
+    std::vector<std::vector<int>> members;
+    std::vector<int> sizes;
+    for (int ng = 1; ng <= std::min<int>((int)order.size(), std::max(1, max_groups)); ++ng) {
+      std::vector<double> load(ng, 0.0), work(ng, 0.0);
+      std::vector<int> need(ng, 1);
+      std::vector<std::vector<int>> mem(ng);
+      for (int q : order) {
+        int t = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        load[t] += steps(q);
+        work[t] += steps(q) * ent(q);
+        need[t] = std::max(need[t], gmin(q));
+        mem[t].push_back(q);
+      }
+      double wsum = 0;
+      int nsum = 0;
+      for (int t = 0; t < ng; ++t) wsum += work[t], nsum += need[t];
+      if (nsum > nsm && ng > 1) continue;  // some group could not keep its rows in shared memory
+      // proportional allocation with minimums (one group = the whole grid,
+      // global-row layout if its rows do not fit shared memory)
+      std::vector<int> G(ng);
+      int left = nsm;
+      for (int t = 0; t < ng && ng > 1; ++t) {
+        G[t] = std::max(need[t], (int)std::floor(nsm * work[t] / std::max(wsum, 1.0)));
+        left -= G[t];
+      }
+      while (left < 0) {  // trim the largest groups above their minimum
+        int t = (int)(std::max_element(G.begin(), G.end()) - G.begin());
+        if (G[t] <= need[t]) break;
+        G[t]--;
+        left++;
+      }
+      if (left < 0) continue;
+      if (ng == 1) G[0] = 0;
+      for (int t = 0; left > 0; t = (t + 1) % ng, --left) G[t]++;
+      double cost = 0;
+      for (int t = 0; t < ng; ++t) {
+        double c = 0;
+        for (int q : mem[t]) c += steps(q) * (LAT + PER * ent(q) / G[t]);
+        cost = std::max(cost, c);
+      }
+      if (cost < best_cost) {
+        best_cost = cost;
+        members = mem;
+        sizes = G;
+      }
+    }
+    int ng = (int)members.size();
     int nmax = 1;
-    for (int q : grd_s) nmax = std::max(nmax, jobs[q].n);
-    for (int q : grd_g) nmax = std::max(nmax, jobs[q].n);
+    for (int q : grd) nmax = std::max(nmax, jobs[q].n);
+    for (int t = 0, f1 = 0; t < ng; ++t) {
+      int f0 = f1, G = sizes[t];
+      f1 = f0 + G;
+      bool fits = true;
+      for (int q : members[t]) fits &= plu_dist_bytes(jobs[q].m, jobs[q].n, G, true) <= dyn_max;
+      bool ok = true;
+      for (int q : members[t]) ok &= plu_dist_bytes(jobs[q].m, jobs[q].n, G, false) <= dyn_max;
+      if (!ok) throw runtime_error("complete-pivot core too large for its cooperative group");
+      GridLaunch &L = gl[fits ? 0 : 1];
+      if (L.cptr.empty()) L.cptr.push_back(0);
+      L.first.push_back(f0);  // group = CTAs [f0, f1) of the launch
+      L.first.push_back(f1);
+      for (int q : members[t]) {
+        L.ids.push_back(q);
+        L.smem = std::max(L.smem, plu_dist_bytes(jobs[q].m, jobs[q].n, G, fits));
+      }
+      L.cptr.push_back((int)L.ids.size());
+    }
     gs.nmax = nmax;
     gs.best = (MaxLoc *)ctx->scratch.alloc(sizeof(MaxLoc) * 2 * nsm);
     gs.cand = ctx->scratch.d((size_t)2 * nsm * nmax);
+    gs.bar = (unsigned *)ctx->scratch.alloc(sizeof(unsigned) * 2 * ng);
+    CK(cudaMemsetAsync(gs.bar, 0, sizeof(unsigned) * 2 * ng, ctx->s));
   }
-  bool side = !cl8.empty() || !cl16.empty() || !grd_s.empty() || !grd_g.empty();
+  int *gl_first[2], *gl_cptr[2], *gl_ids[2];
+  for (int v = 0; v < 2; ++v) {
+    gl_first[v] = gl[v].ids.empty() ? nullptr : sk.push(gl[v].first);
+    gl_cptr[v] = gl[v].ids.empty() ? nullptr : sk.push(gl[v].cptr);
+    gl_ids[v] = gl[v].ids.empty() ? nullptr : sk.push(gl[v].ids);
+  }
+  bool side = !cl8.empty() || !cl16.empty() || !grd.empty();
   if (side) {
     CK(cudaEventRecord(ctx->ev_fork, ctx->s));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
@@ -768,22 +866,21 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
   };
   cluster_group(cl16, ids_cl16, CS);
   cluster_group(cl8, ids_cl8, 8);
-  auto grid_group = [&](const std::vector<int> &g, int *dids, bool rs) {
-    if (g.empty()) return;
-    size_t sm = 0;
-    for (int q : g) sm = std::max(sm, plu_dist_bytes(jobs[q].m, jobs[q].n, nsm, rs));
-    const void *fn = rs ? fns[4] : fns[5];
+  for (int v = 0; v < 2; ++v) {
+    GridLaunch &L = gl[v];
+    if (L.ids.empty()) continue;
+    const void *fn = v == 0 ? fns[4] : fns[5];
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, sm));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, L.smem));
     if (per_sm < 1) throw runtime_error("cooperative pivot-LU kernel does not fit on an SM");
-    int nc = (int)g.size();
+    int ngr = (int)L.cptr.size() - 1;
     double e = eps;
-    void *args[5] = {(void *)&dj, (void *)&dids, (void *)&nc, (void *)&e, (void *)&gs};
-    CK(cudaLaunchCooperativeKernel(fn, dim3(nsm), dim3(512), args, sm, ctx->side));
+    GridScratch g2 = gs;
+    void *args[7] = {(void *)&dj, (void *)&gl_ids[v], (void *)&gl_first[v], (void *)&gl_cptr[v], (void *)&ngr,
+                     (void *)&e, (void *)&g2};
+    CK(cudaLaunchCooperativeKernel(fn, dim3(nsm), dim3(512), args, L.smem, ctx->side));
     ctx->launches++;
-  };
-  grid_group(grd_s, ids_gs, true);
-  grid_group(grd_g, ids_gg, false);
+  }
   if (side) CK(cudaEventRecord(ctx->ev_join, ctx->side));
   for (int b = 0; b < 3; ++b) {
     if (small[b].empty()) continue;

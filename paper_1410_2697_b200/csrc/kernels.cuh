@@ -377,11 +377,40 @@ struct PluState {
   double akk, u11, prev, ratio, errpiv, errprev;
 };
 
+constexpr int GRID_MAX = 160;  // CTAs per cooperative group (>= SM count)
+
 struct GridScratch {
   MaxLoc *best;   // 2 x G
   double *cand;   // 2 x G x nmax
   int nmax;
+  unsigned *bar;  // group barrier (count, generation); nullptr = whole-grid sync
 };
+
+// Barrier over the G CTAs of one group of a cooperative launch (all CTAs are
+// co-resident): the same arrive / spin-on-generation protocol as a grid sync,
+// so several groups run independent cores concurrently.
+__device__ __forceinline__ void group_barrier(GridScratch *gs, int G) {
+  if (!gs->bar) {
+    cg::this_grid().sync();
+    return;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned *vgen = gs->bar + 1;
+    unsigned g0 = *vgen;
+    __threadfence();
+    if (atomicAdd(gs->bar, 1u) == (unsigned)G - 1) {
+      gs->bar[0] = 0;
+      __threadfence();
+      atomicAdd(gs->bar + 1, 1u);
+    } else {
+      while (*vgen == g0) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
 
 // ===========================================================================
 // v2 complete-pivot LU kernels: the reference's physical column swaps are
@@ -656,7 +685,7 @@ __device__ __forceinline__ void plu_dist_body(const PluJob &J, double eps, int G
         double *dst = gs->cand + ((size_t)par * G + g) * gs->nmax;
         for (int j = tid; j < n; j += nt) dst[j] = src[j];
       }
-      cg::this_grid().sync();
+      group_barrier(gs, G);
     } else {
       if (tid == 0) slot[par] = best;
       clp->sync();
@@ -665,13 +694,19 @@ __device__ __forceinline__ void plu_dist_body(const PluJob &J, double eps, int G
       MaxLoc gb{-2.0, 0x7fffffffffffffffLL};
       int who = -1;
       if (GRID) {
-        for (int q = lane; q < G; q += 32) {
-          MaxLoc o = gs->best[par * G + q];
-          if (better(o.v, o.key, gb.v, gb.key)) {
-            gb = o;
-            who = q;
-          }
+        // all loads first (independent), then the in-lane reduction
+        MaxLoc o[GRID_MAX / 32];
+#pragma unroll
+        for (int u = 0; u < GRID_MAX / 32; ++u) {
+          int q = lane + 32 * u;
+          o[u] = q < G ? gs->best[par * G + q] : MaxLoc{-2.0, 0x7fffffffffffffffLL};
         }
+#pragma unroll
+        for (int u = 0; u < GRID_MAX / 32; ++u)
+          if (better(o[u].v, o[u].key, gb.v, gb.key)) {
+            gb = o[u];
+            who = lane + 32 * u;
+          }
       } else if (lane < G) {
         gb = *clp->map_shared_rank(&slot[par], lane);
         who = lane;
@@ -842,18 +877,30 @@ __global__ void __launch_bounds__(512) k_plu_cluster2(const PluJob *__restrict__
   cl.sync();  // DSMEM lifetime
 }
 
+// Cooperative launch split into groups of CTAs: group q = CTAs
+// [range[2q], range[2q+1]) factors cores ids[cptr[q] .. cptr[q+1]) one after
+// another with its own barrier and candidate buffers, concurrently with the
+// other groups (the per-step latency, not the trailing update, bounds a core).
 template <bool ROWS_SMEM>
-__global__ void __launch_bounds__(512) k_plu_grid2(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
-                                                   int ncores, double eps, GridScratch gs) {
+__global__ void __launch_bounds__(512) k_plu_groups(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
+                                                    const int *__restrict__ first, const int *__restrict__ cptr,
+                                                    int ngroups, double eps, GridScratch gs) {
   extern __shared__ __align__(16) char dsm[];
   __shared__ MaxLoc red[32];
   __shared__ PluState st;
   __shared__ int s_nact, s_win;
-  for (int c = 0; c < ncores; ++c) {
+  int q = 0;
+  while (q < ngroups && !((int)blockIdx.x >= first[2 * q] && (int)blockIdx.x < first[2 * q + 1])) ++q;
+  if (q >= ngroups) return;  // CTA of no group in this launch
+  const int f0 = first[2 * q], G = first[2 * q + 1] - f0, g = blockIdx.x - f0;
+  GridScratch mine = gs;
+  mine.best = gs.best + 2 * (size_t)f0;
+  mine.cand = gs.cand + 2 * (size_t)f0 * gs.nmax;
+  mine.bar = gs.bar + 2 * q;
+  for (int c = cptr[q]; c < cptr[q + 1]; ++c) {
     const PluJob J = jobs[ids[c]];
-    plu_dist_body<true, ROWS_SMEM>(J, eps, gridDim.x, blockIdx.x, dsm, red, st, s_nact, nullptr, nullptr, &gs,
-                                   &s_win);
-    cg::this_grid().sync();  // candidate buffers are reused by the next core
+    plu_dist_body<true, ROWS_SMEM>(J, eps, G, g, dsm, red, st, s_nact, nullptr, nullptr, &mine, &s_win);
+    group_barrier(&mine, G);  // candidate buffers are reused by the next core
   }
 }
 

@@ -57,6 +57,26 @@ def test_fplu_large_random_vs_oracle(oracle):
         np.testing.assert_array_equal(lu, olu)
 
 
+def test_fplu_concurrent_groups_vs_oracle(oracle):
+    """Five whole-GPU-class cores in one call: the cooperative launch splits into
+    five CTA groups factoring concurrently (small groups push the tall cores
+    into the global-row launch). Bit-exact against the oracle."""
+    import paper_1410_2697_b200 as P
+    rng = np.random.default_rng(21)
+    blocks, caps = [], []
+    for m, n, r, cap in ((1800, 1000, 60, 10**9), (1000, 1800, 30, 10**9), (1500, 1500, 50, 10**9),
+                         (2400, 700, 20, 10**9), (900, 900, 900, 120)):
+        blocks.append(rng.standard_normal((m, r)) @ rng.standard_normal((r, n)))
+        caps.append(min(m, n, cap))
+    outs = P.full_pivot_lu_batched(blocks, 1e-9, caps)
+    for B, cap, (lu, rp, cp, rank, ratio) in zip(blocks, caps, outs):
+        olu, orp, ocp, orank, oratio = oracle.full_pivot_lu(B, 1e-9, cap)
+        assert rank == orank and ratio == oratio
+        np.testing.assert_array_equal(rp, orp)
+        np.testing.assert_array_equal(cp, ocp)
+        np.testing.assert_array_equal(lu, olu)
+
+
 def test_spmv_matches_scipy():
     import paper_1410_2697_b200 as P
     A, _ = P.gen_poisson7(20, 17, 13)

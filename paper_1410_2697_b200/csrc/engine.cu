@@ -238,6 +238,14 @@ struct Sink {
     return (T *)dst;
   }
   double *scratch_d(size_t n) { return record ? persist->d(n) : ctx->scratch.d(n); }
+  // async host -> device copy into caller-owned device memory through the
+  // pinned staging ring (valid until the next sync rewinds it)
+  void push_to(void *dst, const void *src, size_t bytes) {
+    if (bytes == 0) return;
+    auto hd = ctx->stage.take(bytes);
+    std::memcpy(hd.first, src, bytes);
+    CK(cudaMemcpyAsync(dst, hd.first, bytes, cudaMemcpyHostToDevice, ctx->s));
+  }
   int *scratch_i(size_t n) { return record ? persist->i(n) : ctx->scratch.i(n); }
   void launch(std::function<void(cudaStream_t)> f) {
     if (record) {
@@ -1708,7 +1716,7 @@ struct Factorizer {
       if (!all.empty()) {
         HNode *d = (HNode *)F->arena.alloc(sizeof(HNode) * all.size());
         for (auto &w : where) F->trees[w.first].d_nodes = d + w.second;
-        upload(ctx->s, d, all.data(), sizeof(HNode) * all.size());
+        s.push_to(d, all.data(), sizeof(HNode) * all.size());
       }
     }
 
@@ -2361,6 +2369,7 @@ struct Factorizer {
     // device data (the rank readback inside structured heights) or to recycle
     // scratch memory; per-height phase events are evaluated at the end.
     int used = 0;
+    std::vector<int> height_of_use, struct_of_use;
     for (int h = 0; h <= maxh; ++h) {
       if (byh[h].empty()) {
         if (!cut_at[h].empty()) exchange_updates(cut_at[h]);
@@ -2373,11 +2382,17 @@ struct Factorizer {
       }
       cudaEvent_t *ev = ctx->evpool.data() + 8 * used;
       ++used;
+      height_of_use.push_back(h);
+      {
+        int ns = 0;
+        for (int fi : byh[h]) ns += F->fronts[fi].structured;
+        struct_of_use.push_back(ns);
+      }
       for (int q = 0; q < 8; ++q) CK(cudaEventRecord(ev[q], ctx->s));
       process_height(byh[h], ev);
-      bool has_struct = false;
-      for (int fi : byh[h]) has_struct |= F->fronts[fi].structured;
-      if (has_struct || ctx->scratch.in_use > (size_t(4) << 30)) {
+      // heights run ahead of the host: the only waits are the rank readback
+      // inside structured heights and scratch recycling
+      if (ctx->scratch.in_use > (size_t(4) << 30)) {
         Sink s{ctx};
         auto tw = std::chrono::steady_clock::now();
         s.sync_reset();
@@ -2398,8 +2413,15 @@ struct Factorizer {
     ctx->stage.rewind();
     check_flags(0);
     ctx->scratch.reset();
+    const bool htrace = getenv("MFH_HEIGHT_TRACE") != nullptr;
     for (int u = 0; u < used; ++u) {
       cudaEvent_t *ev = ctx->evpool.data() + 8 * u;
+      if (htrace) {
+        float a[7];
+        for (int q = 0; q < 7; ++q) CK(cudaEventElapsedTime(&a[q], ev[q], ev[q + 1]));
+        fprintf(stderr, "[mfh height %3d] fronts %4zu struct %2d | sample %7.3f dense %7.3f plu %7.3f - %7.3f skel %7.3f hodlr %7.3f elim %7.3f ms\n",
+                height_of_use[u], byh[height_of_use[u]].size(), struct_of_use[u], a[0], a[1], a[2], a[3], a[4], a[5], a[6]);
+      }
       float ms;
       CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
       tsum[0] += ms;

@@ -281,7 +281,11 @@ def run_reference_arm(args, cfg, world, rank):
         "impl": "reference", "metric": METRIC, "value": t, "unit": "s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["desc"], **cfg["params"], "restart": cfg["restart"], "tol": cfg["tol"]},
+        "config": {"workload": cfg["desc"], "n": w.A.n_rows, "nnz": w.A.nnz, **cfg["params"], "nd_leaf": cfg["leaf"],
+                   "restart": cfg["restart"], "tol": cfg["tol"], "rhs": f"{cfg['rhs']} seed 0",
+                   "parallelism": "single (rank 0; the reference is single-process)",
+                   "threads": "1 (OPENBLAS_NUM_THREADS=1: more BLAS threads make the reference 5-15x slower, "
+                              "SURVEY 6.3, so one thread is its fastest configuration)"},
         "cpu_baseline": {"value": t, "unit": "s", "cores": 1, "kind": "port", "sample": sample_text(steps[-1], w)},
         "e2e": {"value": t, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gmres": {"iterations": steps[-1]["its"], "converged": steps[-1]["conv"]},

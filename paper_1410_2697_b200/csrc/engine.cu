@@ -1314,6 +1314,7 @@ struct Factorizer {
   void build_fronts_dev(Sink &s, const std::vector<int> &fis, std::vector<DFront> &dfr,
                         std::vector<DChild> &dch, std::vector<int> &slot_of) {
     slot_of.assign(F->fronts.size(), -1);
+    slot_rw.clear();
     for (int fi : fis) {
       FrontH &f = F->fronts[fi];
       DFront d{};
@@ -1356,30 +1357,53 @@ struct Factorizer {
       }
       d.child_end = (int)dch.size();
       slot_of[fi] = (int)dfr.size();
+      int mrw = 0;
+      for (int q = d.child_begin; q < d.child_end; ++q)
+        if (dch[q].kind == 1) mrw = std::max(mrw, dch[q].rw);
+      slot_rw.push_back(mrw);
       dfr.push_back(d);
     }
   }
 
+  // largest child update rank per DFront slot of the current descriptor set
+  // (filled where the descriptors are built): routes requests to the
+  // register-blocked sampler when a child carries a real W Vt
+  std::vector<int> slot_rw;
+  static constexpr int RB_MIN_RANK = 16;
+
   void run_sample(Sink &s, const std::vector<SReq> &reqs, DFront *dF, DChild *dC) {
     if (reqs.empty()) return;
-    std::vector<int2> tiles;
+    std::vector<int2> tiles, tiles_rb;
     for (int q = 0; q < (int)reqs.size(); ++q) {
-      int64_t nt = cdiv(reqs[q].nr, SAMPLE_TR) * cdiv(reqs[q].nc, SAMPLE_TC);
-      for (int64_t t = 0; t < nt; ++t) tiles.push_back(make_int2(q, (int)t));
+      const bool rb = reqs[q].front < (int)slot_rw.size() && slot_rw[reqs[q].front] >= RB_MIN_RANK;
+      int64_t nt = rb ? cdiv(reqs[q].nr, RB_T) * cdiv(reqs[q].nc, RB_T)
+                      : cdiv(reqs[q].nr, SAMPLE_TR) * cdiv(reqs[q].nc, SAMPLE_TC);
+      for (int64_t t = 0; t < nt; ++t) (rb ? tiles_rb : tiles).push_back(make_int2(q, (int)t));
       F->timing.sample_entries += (double)reqs[q].nr * reqs[q].nc;
     }
-    if (tiles.empty()) return;
+    if (tiles.empty() && tiles_rb.empty()) return;
     SReq *dr = s.push(reqs);
-    int2 *dt = s.push(tiles);
-    int nt = (int)tiles.size();
     long long *pp = d_ap_ptr;
     int *pc = d_ap_col;
     double *pv = d_ap_val;
-    int grid = std::min(nt, 148 * 32);
-    s.launch([=](cudaStream_t st) {
-      k_sample<<<grid, dim3(SAMPLE_TC, SAMPLE_TR), 0, st>>>(dr, dt, nt, dF, dC, pp, pc, pv);
-      check_launch();
-    });
+    if (!tiles.empty()) {
+      int2 *dt = s.push(tiles);
+      int nt = (int)tiles.size();
+      int grid = std::min(nt, 148 * 32);
+      s.launch([=](cudaStream_t st) {
+        k_sample<<<grid, dim3(SAMPLE_TC, SAMPLE_TR), 0, st>>>(dr, dt, nt, dF, dC, pp, pc, pv);
+        check_launch();
+      });
+    }
+    if (!tiles_rb.empty()) {
+      int2 *dt = s.push(tiles_rb);
+      int nt = (int)tiles_rb.size();
+      int grid = std::min(nt, 148 * 8);
+      s.launch([=](cudaStream_t st) {
+        k_sample_rb<<<grid, 256, 0, st>>>(dr, dt, nt, dF, dC, pp, pc, pv);
+        check_launch();
+      });
+    }
   }
 
   FacView as_factors(const BlockH &b) {
@@ -2045,6 +2069,7 @@ struct Factorizer {
     std::vector<DFront> dfr;
     std::vector<DChild> dch;
     std::vector<SReq> reqs;
+    std::vector<int> rws;
     for (size_t k = 0; k < cuts.size(); ++k) {
       if (!F->mine[cuts[k]]) continue;
       FrontH &c = F->fronts[cuts[k]];
@@ -2075,10 +2100,12 @@ struct Factorizer {
       d.child_end = (int)dch.size();
       reqs.push_back(SReq{(int)dfr.size(), c.nf, c.nf, nullptr, nullptr, 0, 0, imp + coff[k], c.nf});
       dfr.push_back(d);
+      rws.push_back(ch.kind == 1 ? ch.rw : 0);
     }
     if (!reqs.empty()) {
       DFront *dF = s.push_keep(dfr);
       DChild *dC = s.push_keep(dch);
+      slot_rw = rws;
       run_sample(s, reqs, dF, dC);
     }
     F->exchange_or_throw(imp, T);

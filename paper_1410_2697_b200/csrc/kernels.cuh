@@ -228,6 +228,123 @@ __global__ void k_mask_select(const double *__restrict__ src, const int8_t *__re
     dst[i] = mask[i] ? src[i] : 0.0;
 }
 
+// Register-blocked extend-add sampler for fronts whose children carry a
+// low-rank update W Vt of meaningful rank: 64 x 64 tiles, 256 threads, 4 x 4
+// entries per thread; W rows and Vt columns of the tile stream through shared
+// memory in 16-wide rank chunks (16 FMA per 8 shared loads). Per entry the
+// arithmetic is exactly k_sample's: seed, then per child in order
+// sub = (HODLR or dense entry) - (u-ascending FMA chain of W[cr,u] Vt[u,cc]),
+// v = v + sub.
+constexpr int RB_T = 64, RB_K = 16;
+__global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs, const int2 *__restrict__ tiles,
+                                                   int ntiles, const DFront *__restrict__ fronts,
+                                                   const DChild *__restrict__ kids,
+                                                   const long long *__restrict__ Ap_ptr,
+                                                   const int *__restrict__ Ap_col,
+                                                   const double *__restrict__ Ap_val) {
+  __shared__ double Ws[RB_K][RB_T + 1];
+  __shared__ double Vs[RB_K][RB_T];
+  __shared__ int s_r[RB_T], s_c[RB_T], s_cr[RB_T], s_cc[RB_T];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int2 tl = tiles[t];
+    const SReq rq = reqs[tl.x];
+    const int tpr = (rq.nc + RB_T - 1) / RB_T;
+    const int bi = (tl.y / tpr) * RB_T, bj = (tl.y % tpr) * RB_T;
+    const DFront F = fronts[rq.front];
+    if (tid < RB_T) {
+      int i = bi + tid;
+      s_r[tid] = i < rq.nr ? (rq.rows ? rq.rows[i] : rq.r0 + i) : -1;
+    } else if (tid < 2 * RB_T) {
+      int j = bj + tid - RB_T;
+      s_c[tid - RB_T] = j < rq.nc ? (rq.cols ? rq.cols[j] : rq.c0 + j) : -1;
+    }
+    __syncthreads();
+    double v[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int r = s_r[ty + 16 * a], c = s_c[tx + 16 * b];
+        v[a][b] = (r >= 0 && c >= 0 && (r < F.npv || c < F.npv))
+                      ? seed_entry(Ap_ptr, Ap_col, Ap_val, F.ids[r], F.ids[c])
+                      : 0.0;
+      }
+    for (int q = F.child_begin; q < F.child_end; ++q) {
+      const DChild &ch = kids[q];
+      if (tid < RB_T) {
+        int r = s_r[tid];
+        s_cr[tid] = r >= 0 ? ch.to_child[r] : -1;
+      } else if (tid < 2 * RB_T) {
+        int c = s_c[tid - RB_T];
+        s_cc[tid - RB_T] = c >= 0 ? ch.to_child[c] : -1;
+      }
+      __syncthreads();
+      double sub[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int cr = s_cr[ty + 16 * a], cc = s_cc[tx + 16 * b];
+          double x = 0.0;
+          if (cr >= 0 && cc >= 0) x = ch.kind == 0 ? ch.dense[(long long)cr * ch.ldd + cc] : hodlr_entry(ch.hn, ch.n, cr, cc);
+          sub[a][b] = x;
+        }
+      if (ch.kind == 1 && ch.rw) {
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        for (int u0 = 0; u0 < ch.rw; u0 += RB_K) {
+          const int kc = min(RB_K, ch.rw - u0);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const int e = tid + 256 * m;
+            const int row = e >> 4, k = e & 15;  // W: 64 rows x 16 ranks
+            const int cr = s_cr[row];
+            Ws[k][row] = (cr >= 0 && k < kc) ? ch.W[(long long)cr * ch.ldw + u0 + k] : 0.0;
+            const int k2 = e >> 6, col = e & 63;  // Vt: 16 ranks x 64 cols
+            const int cc = s_cc[col];
+            Vs[k2][col] = (cc >= 0 && k2 < kc) ? ch.Vt[(long long)(u0 + k2) * ch.ldv + cc] : 0.0;
+          }
+          __syncthreads();
+          for (int k = 0; k < kc; ++k) {
+            double w[4], x[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) w[a] = Ws[k][ty + 16 * a];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) x[b] = Vs[k][tx + 16 * b];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) acc[a][b] = fma(w[a], x[b], acc[a][b]);
+          }
+          __syncthreads();
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) sub[a][b] = sub[a][b] - acc[a][b];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (s_cr[ty + 16 * a] >= 0 && s_cc[tx + 16 * b] >= 0) v[a][b] = v[a][b] + sub[a][b];
+      __syncthreads();  // s_cr / s_cc are rewritten for the next child
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = bi + ty + 16 * a, j = bj + tx + 16 * b;
+        if (i < rq.nr && j < rq.nc) rq.out[(long long)i * rq.ld + j] = v[a][b];
+      }
+    __syncthreads();  // s_r / s_c are rewritten for the next tile
+  }
+}
+
 // ---------------------------------------------------------------------------
 // batched 2-D copy / gather
 // ---------------------------------------------------------------------------

@@ -701,24 +701,27 @@ __global__ void __launch_bounds__(512) k_plu_cta2(const PluJob *__restrict__ job
     }
     __syncthreads();
     bv = -1.0;
-    bk = 0x7fffffffffffffffLL;
+    // each thread scans rows ascending and, within a row, columns ascending:
+    // scan order = key order, so a strict '>' keeps the first (lowest-key) max
+    int bi_ = -1, bj_ = 0;
     const double *prow = a + (long long)k * ld;
     for (int i = k + 1 + warp; i < m; i += nw) {
       double *row = a + (long long)i * ld;
       const double l = row[k] / akk;
       __syncwarp();
       if (lane == 0) row[k] = l;
-      const long long rk = (long long)i * n;
       for (int j = k + 1 + lane; j < n; j += 32) {
         double v = __dsub_rn(row[j], __dmul_rn(l, prow[j]));
         row[j] = v;
         double av = fabs(v);
-        if (better(av, rk + j, bv, bk)) {
+        if (av > bv) {
           bv = av;
-          bk = rk + j;
+          bi_ = i;
+          bj_ = j;
         }
       }
     }
+    bk = bi_ >= 0 ? (long long)bi_ * n + bj_ : 0x7fffffffffffffffLL;
   }
   __syncthreads();
   if (SMEM_CORE)
@@ -935,17 +938,29 @@ __device__ __forceinline__ void plu_dist_body(const PluJob &J, double eps, int G
       const double ok_ = row[k], ob = row[bj];
       const double l = ob / akk;
       __syncwarp();
-      if (lane == 0) row[k] = l;
+      if (lane == 0) {
+        row[k] = l;
+        if (bj != k) row[bj] = ok_;  // the physical column swap, before the sweep
+      }
+      __syncwarp();
       const long long rk = (long long)posRl[li] * n;
+      // within one row the lane's columns ascend, so key order = scan order:
+      // a strict '>' with the column index is exact; the (value, key) merge
+      // with the thread's best happens once per row
+      double rbv = -1.0;
+      int rj = 0x7fffffff;
       for (int j = k + 1 + lane; j < n; j += 32) {
-        double cur = (j == bj) ? ok_ : row[j];
-        double v = __dsub_rn(cur, __dmul_rn(l, prow[j]));
+        double v = __dsub_rn(row[j], __dmul_rn(l, prow[j]));
         row[j] = v;
         double av = fabs(v);
-        if (better(av, rk + j, bv, bk)) {
-          bv = av;
-          bk = rk + j;
+        if (av > rbv) {
+          rbv = av;
+          rj = j;
         }
+      }
+      if (rj != 0x7fffffff && better(rbv, rk + rj, bv, bk)) {
+        bv = rbv;
+        bk = rk + rj;
       }
     }
   }

@@ -1850,7 +1850,7 @@ struct Factorizer {
           double *xt, *xb, *yt, *yb, *Tm;
         };
         std::vector<Nd> nodes;
-        std::vector<GemmJob> ga, gc, gd, ge;
+        std::vector<GemmJob> ga, gc, gd, ge, gsch, gs1, gs2;
         std::vector<double *> ip;
         std::vector<int> idim, ild;
         std::vector<LuJob> fin;
@@ -1887,25 +1887,51 @@ struct Factorizer {
               ga.push_back(GemmJob{HRR, f2.col, nd.xb, m2, r2, m2, N, f2.ldc, r2, 1.0, 0.0});
               ga.push_back(GemmJob{f2.row, HLL, nd.yb, r2, m1, m1, f2.ldr, N, m1, 1.0, 0.0});
             }
-            // (b) Woodbury core (hodlr.py:343-345) and its inverse (346-352 checks)
-            T.core[v] = F->arena.d((size_t)rr * rr);
+            // (b) Woodbury core (hodlr.py:343-345) C = [[I, A], [B, I]], A = row1 x_bot,
+            // B = row2 x_top, and its inverse through the Schur complement of the
+            // smaller side: with S = I - B A (r2 <= r1),
+            //   C^{-1} = [[I + A S^{-1} B, -A S^{-1}], [-S^{-1} B, S^{-1}]]
+            // (mirrored with S = I - A B when r1 < r2): one inverse of
+            // min(r1, r2) instead of r1 + r2, the rest batched GEMMs. C is
+            // singular iff S is (the reference's core check, hodlr.py:346-352).
+            T.core[v] = ctx->scratch.d((size_t)rr * rr);
             ip.push_back(T.core[v]);
             idim.push_back(rr);
             ild.push_back(rr);
+            double *C = T.core[v];
             if (r1 && r2) {
-              gc.push_back(GemmJob{f1.row, nd.xb, T.core[v] + r1, r1, r2, m2, f1.ldr, r2, rr, 1.0, 1.0});
-              gc.push_back(GemmJob{f2.row, nd.xt, T.core[v] + (int64_t)r1 * rr, r2, r1, m1, f2.ldr, r1, rr, 1.0, 1.0});
+              gc.push_back(GemmJob{f1.row, nd.xb, C + r1, r1, r2, m2, f1.ldr, r2, rr, 1.0, 1.0});
+              gc.push_back(GemmJob{f2.row, nd.xt, C + (int64_t)r1 * rr, r2, r1, m1, f2.ldr, r1, rr, 1.0, 1.0});
             }
             std::string msg = "singular coupling core at node [" + std::to_string(lo) + ", " + std::to_string(hi) + ")";
             int fl = new_flag(msg, (int64_t)T.fi * 1000000 + v);
-            fin.push_back(LuJob{T.core[v], rr, rr, nullptr, d_flags + fl});
-            if (rr > INV_SMALL) {
-              T.cpiv[v] = ctx->scratch.i(rr);
-              T.cinv[v] = ctx->scratch.d((size_t)rr * rr);
+            fin.push_back(LuJob{C, rr, rr, nullptr, d_flags + fl});
+            double *Ci = T.cinv[v] = ctx->scratch.d((size_t)rr * rr);
+            double *A = C + r1, *B = C + (int64_t)r1 * rr;
+            if (!(r1 && r2)) {  // C = I exactly
+              ip.push_back(Ci);
+              idim.push_back(rr);
+              ild.push_back(rr);
+            } else if (r2 <= r1) {
+              double *S = ctx->scratch.d((size_t)r2 * r2);
+              ip.push_back(S), idim.push_back(r2), ild.push_back(r2);
+              ip.push_back(Ci), idim.push_back(r1), ild.push_back(rr);  // top-left starts as I
+              gsch.push_back(GemmJob{B, A, S, r2, r2, r1, rr, rr, r2, -1.0, 1.0});
+              double *Si = Ci + (int64_t)r1 * rr + r1;
+              invs.push_back(InvReq{S, r2, r2, Si, rr, r2 > INV_SMALL ? ctx->scratch.i(r2) : nullptr, d_flags + fl});
+              gs1.push_back(GemmJob{Si, B, Ci + (int64_t)r1 * rr, r2, r1, r2, rr, rr, rr, -1.0, 0.0});
+              gs1.push_back(GemmJob{A, Si, Ci + r1, r1, r2, r2, rr, rr, rr, -1.0, 0.0});
+              gs2.push_back(GemmJob{A, Ci + (int64_t)r1 * rr, Ci, r1, r1, r2, rr, rr, rr, -1.0, 1.0});
             } else {
-              T.cinv[v] = T.core[v];
+              double *S = ctx->scratch.d((size_t)r1 * r1);
+              ip.push_back(S), idim.push_back(r1), ild.push_back(r1);
+              ip.push_back(Ci + (int64_t)r1 * rr + r1), idim.push_back(r2), ild.push_back(rr);  // bottom-right I
+              gsch.push_back(GemmJob{A, B, S, r1, r1, r2, rr, rr, r1, -1.0, 1.0});
+              invs.push_back(InvReq{S, r1, r1, Ci, rr, r1 > INV_SMALL ? ctx->scratch.i(r1) : nullptr, d_flags + fl});
+              gs1.push_back(GemmJob{Ci, A, Ci + r1, r1, r2, r1, rr, rr, rr, -1.0, 0.0});
+              gs1.push_back(GemmJob{B, Ci, Ci + (int64_t)r1 * rr, r2, r1, r1, rr, rr, rr, -1.0, 0.0});
+              gs2.push_back(GemmJob{B, Ci + r1, Ci + (int64_t)r1 * rr + r1, r2, r2, r1, rr, rr, rr, -1.0, 1.0});
             }
-            invs.push_back(InvReq{T.core[v], rr, rr, T.cinv[v], rr, T.cpiv[v], d_flags + fl});
             // (d) Tm = core^{-1} [[0, y_top], [y_bot, 0]]  (rr x nv)
             gd.push_back(GemmJob{T.cinv[v] + r1, nd.yb, nd.Tm, rr, m1, r2, rr, m1, nv, 1.0, 0.0});
             gd.push_back(GemmJob{T.cinv[v], nd.yt, nd.Tm + m1, rr, m2, r1, rr, m2, nv, 1.0, 0.0});
@@ -1922,7 +1948,10 @@ struct Factorizer {
         run_identity(s, ip, idim, ild);
         run_gemm(s, gc);
         run_check_finite(s, fin);
+        run_gemm(s, gsch);
         run_inverse(s, invs);
+        run_gemm(s, gs1);
+        run_gemm(s, gs2);
         run_gemm(s, gd);
         run_gemm(s, ge);
       }

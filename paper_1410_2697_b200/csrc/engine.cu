@@ -1399,8 +1399,13 @@ struct Factorizer {
       int2 *dt = s.push(tiles_rb);
       int nt = (int)tiles_rb.size();
       int grid = std::min(nt, 148 * 8);
+      static bool attr = false;
+      if (!attr) {
+        CK(cudaFuncSetAttribute(k_sample_rb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RB_DYN));
+        attr = true;
+      }
       s.launch([=](cudaStream_t st) {
-        k_sample_rb<<<grid, 256, 0, st>>>(dr, dt, nt, dF, dC, pp, pc, pv);
+        k_sample_rb<<<grid, 256, RB_DYN, st>>>(dr, dt, nt, dF, dC, pp, pc, pv);
         check_launch();
       });
     }

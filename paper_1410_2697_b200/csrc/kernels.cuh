@@ -228,14 +228,95 @@ __global__ void k_mask_select(const double *__restrict__ src, const int8_t *__re
     dst[i] = mask[i] ? src[i] : 0.0;
 }
 
+// descend to the block holding (r, c), also returning the block's rectangle
+// in HODLR-local coordinates (rows [rlo, rhi), cols [clo, chi)); nullptr for a leaf
+__device__ __forceinline__ const HBlk *hodlr_locate_rect(const HNode *hn, int n, int r, int c, int &rlo, int &rhi,
+                                                         int &clo, int &chi) {
+  int idx = 0, lo = 0, hi = n;
+  while (true) {
+    const HNode &nd = hn[idx];
+    if (nd.leaf) return nullptr;
+    int mid = (lo + hi) >> 1;
+    if (r < mid) {
+      if (c < mid) {
+        idx = 2 * idx + 1;
+        hi = mid;
+        continue;
+      }
+      rlo = lo, rhi = mid, clo = mid, chi = hi;
+      return &nd.up;
+    }
+    if (c >= mid) {
+      idx = 2 * idx + 2;
+      lo = mid;
+      continue;
+    }
+    rlo = mid, rhi = hi, clo = lo, chi = mid;
+    return &nd.lw;
+  }
+}
+
 // Register-blocked extend-add sampler for fronts whose children carry a
 // low-rank update W Vt of meaningful rank: 64 x 64 tiles, 256 threads, 4 x 4
-// entries per thread; W rows and Vt columns of the tile stream through shared
-// memory in 16-wide rank chunks (16 FMA per 8 shared loads). Per entry the
+// entries per thread. Rank-r dot products stream their factors through shared
+// memory in 16-wide chunks (16 FMA per 8 shared loads, next chunk prefetched
+// into registers): the W Vt term always, and the HODLR term when the tile's
+// child rows x cols rectangle lies inside one low-rank block. Per entry the
 // arithmetic is exactly k_sample's: seed, then per child in order
 // sub = (HODLR or dense entry) - (u-ascending FMA chain of W[cr,u] Vt[u,cc]),
-// v = v + sub.
+// v = v + sub (the HODLR low-rank entry is itself a t-ascending FMA chain).
 constexpr int RB_T = 64, RB_K = 16;
+constexpr size_t RB_DYN = sizeof(double) * RB_T * (RB_T + 1);
+
+// acc[a][b] = sum_u X[sx[row_a], u] * Y[u, sy[col_b]] (u ascending from 0);
+// rows / cols with index -1 contribute zero
+__device__ __forceinline__ void rb_dot(double (&acc)[4][4], const double *__restrict__ X, int ldx,
+                                       const int *sx, const double *__restrict__ Y, int ldy, const int *sy, int K,
+                                       double (*Ws)[RB_T + 1], double (*Vs)[RB_T], int tid, int tx, int ty) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  double pw[4], pv[4];
+  auto fetch = [&](int u0) {
+    const int kc = min(RB_K, K - u0);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int e = tid + 256 * m;
+      const int row = e >> 4, k = e & 15;
+      const int xr = sx[row];
+      pw[m] = (xr >= 0 && k < kc) ? X[(long long)xr * ldx + u0 + k] : 0.0;
+      const int k2 = e >> 6, col = e & 63;
+      const int yc = sy[col];
+      pv[m] = (yc >= 0 && k2 < kc) ? Y[(long long)(u0 + k2) * ldy + yc] : 0.0;
+    }
+  };
+  fetch(0);
+  for (int u0 = 0; u0 < K; u0 += RB_K) {
+    const int kc = min(RB_K, K - u0);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int e = tid + 256 * m;
+      Ws[e & 15][e >> 4] = pw[m];
+      Vs[e >> 6][e & 63] = pv[m];
+    }
+    __syncthreads();
+    if (u0 + RB_K < K) fetch(u0 + RB_K);  // in flight during the FMAs
+    for (int k = 0; k < kc; ++k) {
+      double w[4], x[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) w[a] = Ws[k][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) x[b] = Vs[k][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(w[a], x[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs, const int2 *__restrict__ tiles,
                                                    int ntiles, const DFront *__restrict__ fronts,
                                                    const DChild *__restrict__ kids,
@@ -244,7 +325,11 @@ __global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs
                                                    const double *__restrict__ Ap_val) {
   __shared__ double Ws[RB_K][RB_T + 1];
   __shared__ double Vs[RB_K][RB_T];
-  __shared__ int s_r[RB_T], s_c[RB_T], s_cr[RB_T], s_cc[RB_T];
+  __shared__ int s_r[RB_T], s_c[RB_T], s_cr[RB_T], s_cc[RB_T], s_br[RB_T], s_bc[RB_T];
+  __shared__ const HBlk *s_blk;
+  __shared__ int s_rlo, s_clo;
+  extern __shared__ double rb_dyn[];  // running entry values s_v[RB_T][RB_T + 1] (keeps registers for the dots)
+  double(*s_v)[RB_T + 1] = reinterpret_cast<double(*)[RB_T + 1]>(rb_dyn);
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int2 tl = tiles[t];
@@ -260,15 +345,14 @@ __global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs
       s_c[tid - RB_T] = j < rq.nc ? (rq.cols ? rq.cols[j] : rq.c0 + j) : -1;
     }
     __syncthreads();
-    double v[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int r = s_r[ty + 16 * a], c = s_c[tx + 16 * b];
-        v[a][b] = (r >= 0 && c >= 0 && (r < F.npv || c < F.npv))
-                      ? seed_entry(Ap_ptr, Ap_col, Ap_val, F.ids[r], F.ids[c])
-                      : 0.0;
+        s_v[ty + 16 * a][tx + 16 * b] = (r >= 0 && c >= 0 && (r < F.npv || c < F.npv))
+                                            ? seed_entry(Ap_ptr, Ap_col, Ap_val, F.ids[r], F.ids[c])
+                                            : 0.0;
       }
     for (int q = F.child_begin; q < F.child_end; ++q) {
       const DChild &ch = kids[q];
@@ -280,48 +364,64 @@ __global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs
         s_cc[tid - RB_T] = c >= 0 ? ch.to_child[c] : -1;
       }
       __syncthreads();
-      double sub[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int cr = s_cr[ty + 16 * a], cc = s_cc[tx + 16 * b];
-          double x = 0.0;
-          if (cr >= 0 && cc >= 0) x = ch.kind == 0 ? ch.dense[(long long)cr * ch.ldd + cc] : hodlr_entry(ch.hn, ch.n, cr, cc);
-          sub[a][b] = x;
+      bool uni = false;
+      if (ch.kind == 1) {
+        // does the tile's child rectangle sit inside one low-rank block?
+        if (tid < 32) {
+          int rmin = 0x7fffffff, rmax = -1, cmin = 0x7fffffff, cmax = -1;
+          for (int e = tid; e < RB_T; e += 32) {
+            int x = s_cr[e], y = s_cc[e];
+            if (x >= 0) rmin = min(rmin, x), rmax = max(rmax, x);
+            if (y >= 0) cmin = min(cmin, y), cmax = max(cmax, y);
+          }
+          for (int o = 16; o > 0; o >>= 1) {
+            rmin = min(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+            rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+            cmin = min(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+            cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+          }
+          if (tid == 0) {
+            const HBlk *blk = nullptr;
+            if (rmax >= 0 && cmax >= 0) {
+              int rlo, rhi, clo, chi;
+              blk = hodlr_locate_rect(ch.hn, ch.n, rmin, cmin, rlo, rhi, clo, chi);
+              if (blk && !(blk->kind == 0 && blk->rank > 0 && rmax < rhi && cmax < chi)) blk = nullptr;
+              s_rlo = rlo;
+              s_clo = clo;
+            }
+            s_blk = blk;
+          }
         }
-      if (ch.kind == 1 && ch.rw) {
-        double acc[4][4];
+        __syncthreads();
+        uni = s_blk != nullptr;
+      }
+      double sub[4][4];
+      if (uni) {
+        const HBlk B = *s_blk;
+        if (tid < RB_T) {
+          int x = s_cr[tid];
+          s_br[tid] = x >= 0 ? x - s_rlo : -1;
+        } else if (tid < 2 * RB_T) {
+          int y = s_cc[tid - RB_T];
+          s_bc[tid - RB_T] = y >= 0 ? y - s_clo : -1;
+        }
+        __syncthreads();
+        rb_dot(sub, B.a, B.lda, s_br, B.b, B.ldb, s_bc, B.rank, Ws, Vs, tid, tx, ty);
+      } else {
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-        for (int u0 = 0; u0 < ch.rw; u0 += RB_K) {
-          const int kc = min(RB_K, ch.rw - u0);
-#pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            const int e = tid + 256 * m;
-            const int row = e >> 4, k = e & 15;  // W: 64 rows x 16 ranks
-            const int cr = s_cr[row];
-            Ws[k][row] = (cr >= 0 && k < kc) ? ch.W[(long long)cr * ch.ldw + u0 + k] : 0.0;
-            const int k2 = e >> 6, col = e & 63;  // Vt: 16 ranks x 64 cols
-            const int cc = s_cc[col];
-            Vs[k2][col] = (cc >= 0 && k2 < kc) ? ch.Vt[(long long)(u0 + k2) * ch.ldv + cc] : 0.0;
+          for (int b = 0; b < 4; ++b) {
+            const int cr = s_cr[ty + 16 * a], cc = s_cc[tx + 16 * b];
+            double x = 0.0;
+            if (cr >= 0 && cc >= 0)
+              x = ch.kind == 0 ? ch.dense[(long long)cr * ch.ldd + cc] : hodlr_entry(ch.hn, ch.n, cr, cc);
+            sub[a][b] = x;
           }
-          __syncthreads();
-          for (int k = 0; k < kc; ++k) {
-            double w[4], x[4];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) w[a] = Ws[k][ty + 16 * a];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) x[b] = Vs[k][tx + 16 * b];
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-              for (int b = 0; b < 4; ++b) acc[a][b] = fma(w[a], x[b], acc[a][b]);
-          }
-          __syncthreads();
-        }
+      }
+      if (ch.kind == 1 && ch.rw) {
+        double acc[4][4];
+        rb_dot(acc, ch.W, ch.ldw, s_cr, ch.Vt, ch.ldv, s_cc, ch.rw, Ws, Vs, tid, tx, ty);
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -331,15 +431,16 @@ __global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b)
-          if (s_cr[ty + 16 * a] >= 0 && s_cc[tx + 16 * b] >= 0) v[a][b] = v[a][b] + sub[a][b];
-      __syncthreads();  // s_cr / s_cc are rewritten for the next child
+          if (s_cr[ty + 16 * a] >= 0 && s_cc[tx + 16 * b] >= 0)
+            s_v[ty + 16 * a][tx + 16 * b] = s_v[ty + 16 * a][tx + 16 * b] + sub[a][b];
+      __syncthreads();  // s_cr / s_cc / s_blk are rewritten for the next child
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int i = bi + ty + 16 * a, j = bj + tx + 16 * b;
-        if (i < rq.nr && j < rq.nc) rq.out[(long long)i * rq.ld + j] = v[a][b];
+        if (i < rq.nr && j < rq.nc) rq.out[(long long)i * rq.ld + j] = s_v[ty + 16 * a][tx + 16 * b];
       }
     __syncthreads();  // s_r / s_c are rewritten for the next tile
   }

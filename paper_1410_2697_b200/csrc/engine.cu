@@ -703,7 +703,7 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
   static bool attr_done = false;
   static size_t dyn_max = 0;
   static const void *fns[6] = {(const void *)k_plu_cta2<true>,      (const void *)k_plu_cta2<false>,
-                               (const void *)k_plu_cluster2<true>,  (const void *)k_plu_cluster2<false>,
+                               (const void *)k_plu_cluster3,        (const void *)k_plu_cluster2<false>,
                                (const void *)k_plu_groups<true>,    (const void *)k_plu_groups<false>};
   if (!attr_done) {
     int optin = 0;
@@ -868,7 +868,7 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
   auto cluster_group = [&](const std::vector<int> &g, int *dids, int cs) {
     if (g.empty()) return;
     size_t sm = 0;
-    for (int q : g) sm = std::max(sm, plu_dist_bytes(jobs[q].m, jobs[q].n, cs, true));
+    for (int q : g) sm = std::max(sm, plu_cl3_bytes(jobs[q].m, jobs[q].n, cs));
     launch_cluster(fns[2], (int)g.size(), cs, sm, ctx->side, dj, dids, eps);
     ctx->launches++;
   };

@@ -1110,6 +1110,218 @@ __global__ void __launch_bounds__(512) k_plu_cluster2(const PluJob *__restrict__
   cl.sync();  // DSMEM lifetime
 }
 
+// ---------------------------------------------------------------------------
+// Cluster complete-pivot LU, one cluster barrier per step (rows in DSMEM)
+//   * every CTA publishes its best candidate (|v|, key, signed v, local row);
+//     after the cluster barrier EVERY warp reduces the G slots itself, so all
+//     threads know the pivot without a broadcast
+//   * the stop / rank state (plu_stop) is evaluated identically in every
+//     thread's registers
+//   * rows are dealt round-robin (original row i -> CTA i % G, local i / G), so
+//     the pivot's original row is (local row, CTA); each row's logical position
+//     is kept by the warp that updates it; active rows carry a flag instead of
+//     a compacted list
+//   * the column swap k <-> bj is fused into the update for active rows;
+//     pivoted rows receive all their later swaps in one pass at the end
+// Same arithmetic and the same (|v|, row-major key) first-max rule as
+// k_plu_cta2 / plu_dist_body: bit-identical factors, pivots, rank, ratio.
+// ---------------------------------------------------------------------------
+struct PluCand {
+  double v, sv;
+  long long key;
+  int li;
+};
+__device__ __forceinline__ PluCand cand_none() { return PluCand{-1.0, 0.0, 0x7fffffffffffffffLL, -1}; }
+// warp argmax under better(): max |v| (NaN and "none" never win), then the
+// lowest key, with hardware redux on 32-bit halves of a monotone encoding;
+// every lane returns the winner (payload broadcast from the winning lane)
+__device__ __forceinline__ PluCand warp_best(PluCand c, int &who) {
+  const unsigned long long u = (c.v >= 0.0) ? (unsigned long long)__double_as_longlong(c.v) + 1ull : 0ull;
+  const unsigned uh = (unsigned)(u >> 32), ul = (unsigned)u;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, uh);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, uh == mh ? ul : 0u);
+  const bool top = uh == mh && ul == ml;
+  const unsigned long long key = (unsigned long long)c.key;
+  const unsigned kh = (unsigned)(key >> 32), kl = (unsigned)key;
+  const unsigned mkh = __reduce_min_sync(0xffffffffu, top ? kh : 0xffffffffu);
+  const unsigned mkl = __reduce_min_sync(0xffffffffu, (top && kh == mkh) ? kl : 0xffffffffu);
+  const unsigned win = __ballot_sync(0xffffffffu, top && kh == mkh && kl == mkl);
+  const int src = __ffs(win) - 1;
+  PluCand r;
+  r.v = __shfl_sync(0xffffffffu, c.v, src);
+  r.sv = __shfl_sync(0xffffffffu, c.sv, src);
+  r.key = (long long)(((unsigned long long)mkh << 32) | mkl);
+  r.li = __shfl_sync(0xffffffffu, c.li, src);
+  who = __shfl_sync(0xffffffffu, who, src);
+  return r;
+}
+
+__host__ __device__ inline size_t plu_cl3_bytes(int m, int n, int G) {
+  size_t nl = (size_t)((m + G - 1) / G), kmin = (size_t)(m < n ? m : n);
+  size_t b = sizeof(double) * (nl * (size_t)n + (size_t)n);
+  b += sizeof(int) * (3 * nl + kmin + (size_t)n + 4);
+  return (b + 15) & ~size_t(15);
+}
+
+__global__ void __launch_bounds__(512) k_plu_cluster3(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
+                                                      double eps) {
+  extern __shared__ __align__(16) char dsm[];
+  __shared__ PluCand red[16];
+  __shared__ PluCand slots[2][16];  // [parity][source CTA]: pushed by every CTA before the barrier
+  cg::cluster_group cl = cg::this_cluster();
+  const int G = (int)cl.num_blocks(), g = (int)cl.block_rank();
+  const PluJob J = jobs[ids[blockIdx.x / G]];
+  const int m = J.m, n = J.n, tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  const int nl_max = (m + G - 1) / G, nl = (m - g + G - 1) / G, kmin = min(m, n);
+  double *rows = (double *)dsm;
+  double *prow = rows + (size_t)nl_max * n;
+  int *posR = (int *)(prow + n);
+  int *act = posR + nl_max;
+  int *pstep = act + nl_max;
+  int *swp = pstep + nl_max;
+  int *colAt = swp + kmin;
+  for (long long e = tid; e < (long long)nl * n; e += nt) {
+    int li = (int)(e / n), j = (int)(e % n);
+    rows[e] = J.a[(long long)(li * G + g) * J.ld + j];
+  }
+  for (int li = tid; li < nl; li += nt) {
+    posR[li] = li * G + g;
+    act[li] = 1;
+    pstep[li] = -1;
+  }
+  for (int j = tid; j < n; j += nt) colAt[j] = j;
+  __syncthreads();
+  // initial candidates: first max of |a| in row-major (original) order
+  PluCand best = cand_none();
+  for (int li = warp; li < nl; li += nw) {
+    const double *row = rows + (size_t)li * n;
+    double rbv = -1.0, rsv = 0.0;
+    int rj = 0x7fffffff;
+    for (int j = lane; j < n; j += 32) {
+      double x = row[j], av = fabs(x);
+      if (av > rbv) {
+        rbv = av;
+        rsv = x;
+        rj = j;
+      }
+    }
+    const long long key = (long long)(li * G + g) * n + rj;
+    if (rj != 0x7fffffff && better(rbv, key, best.v, best.key)) best = PluCand{rbv, rsv, key, li};
+  }
+  PluState my{};
+  int steps = 0;
+  for (int k = 0; k < kmin; ++k) {
+    const int par = k & 1;
+    {
+      int who = 0;
+      PluCand c = warp_best(best, who);
+      if (lane == 0) red[warp] = c;
+      __syncthreads();
+      if (warp == 0) {
+        PluCand x = lane < nw ? red[lane] : cand_none();
+        x = warp_best(x, who);
+        // push this CTA's candidate into every CTA's local slot array
+        if (lane < G) *cl.map_shared_rank(&slots[par][g], lane) = x;
+      }
+    }
+    cl.sync();
+    // every warp reduces the cluster's candidates from local shared memory
+    int who = lane;
+    PluCand gb = lane < G ? slots[par][lane] : cand_none();
+    gb = warp_best(gb, who);
+    double piv = gb.v;
+    int pr = k, bj = k;
+    if (gb.key != 0x7fffffffffffffffLL) {
+      pr = (int)(gb.key / n);
+      bj = (int)(gb.key % n);
+    } else {
+      piv = -1.0;
+    }
+    if (plu_stop(my, k, J.kmax, eps, piv)) break;
+    my.prev = fabs(gb.sv);
+    my.rank = k + 1;
+    steps = k + 1;
+    const double akk = gb.sv;
+    // pivot row (after this step's column swap) from the winner's DSMEM
+    {
+      const double *orow = cl.map_shared_rank(rows, who) + (size_t)gb.li * n;
+      for (int j = k + 1 + tid; j < n; j += nt) prow[j] = (j == bj) ? orow[k] : orow[j];
+    }
+    if (tid == 0) {
+      int t = colAt[k];
+      colAt[k] = colAt[bj];
+      colAt[bj] = t;
+      swp[k] = bj;
+      if (who == g) {
+        act[gb.li] = 0;
+        pstep[gb.li] = k;
+        posR[gb.li] = k;
+      }
+    }
+    __syncthreads();
+    best = cand_none();
+    for (int li = warp; li < nl; li += nw) {
+      if (!act[li]) continue;
+      double *row = rows + (size_t)li * n;
+      const double ok_ = row[k], ob = row[bj];
+      int pos = posR[li];
+      const double l = ob / akk;
+      __syncwarp();
+      if (lane == 0) {
+        row[k] = l;
+        if (bj != k) row[bj] = ok_;
+        if (pos == k) posR[li] = pr;  // the row at position k moves to the pivot's old position
+      }
+      __syncwarp();
+      if (pos == k) pos = pr;
+      double rbv = -1.0, rsv = 0.0;
+      int rj = 0x7fffffff;
+      for (int j = k + 1 + lane; j < n; j += 32) {
+        double v = __dsub_rn(row[j], __dmul_rn(l, prow[j]));
+        row[j] = v;
+        double av = fabs(v);
+        if (av > rbv) {
+          rbv = av;
+          rsv = v;
+          rj = j;
+        }
+      }
+      const long long key = (long long)pos * n + rj;
+      if (rj != 0x7fffffff && better(rbv, key, best.v, best.key)) best = PluCand{rbv, rsv, key, li};
+    }
+  }
+  __syncthreads();
+  // pivoted rows: the column swaps of their own step and every later step
+  for (int li = tid; li < nl; li += nt) {
+    const int p = pstep[li];
+    if (p < 0) continue;
+    double *row = rows + (size_t)li * n;
+    for (int s2 = p; s2 < steps; ++s2) {
+      const int b2 = swp[s2];
+      if (b2 != s2) {
+        double x = row[s2];
+        row[s2] = row[b2];
+        row[b2] = x;
+      }
+    }
+  }
+  __syncthreads();
+  for (long long e = tid; e < (long long)nl * n; e += nt) {
+    int li = (int)(e / n), j = (int)(e % n);
+    J.a[(long long)(li * G + g) * J.ld + j] = rows[e];
+  }
+  for (int li = tid; li < nl; li += nt) J.rowAt[posR[li]] = li * G + g;
+  if (g == 0) {
+    for (int j = tid; j < n; j += nt) J.colAt[j] = colAt[j];
+    if (tid == 0) {
+      plu_out(J, my);
+      J.out[3] = 0;  // rows logical: row p of the factor is original row rowAt[p]
+    }
+  }
+  cl.sync();  // DSMEM lifetime: peers may still read this CTA's rows
+}
+
 // Cooperative launch split into groups of CTAs: group q = CTAs
 // [range[2q], range[2q+1]) factors cores ids[cptr[q] .. cptr[q+1]) one after
 // another with its own barrier and candidate buffers, concurrently with the

@@ -10,6 +10,7 @@
 //                                skeleton TRSMs / dense fallbacks, level-batched
 //                                HODLR factorization, W/V update (multifrontal.py:353-456)
 // BDLR selections (bdlr.py:89-136) are integer graph work done on the host.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -191,7 +192,9 @@ struct Ctx {
   double *d_part = nullptr;  // reduction partials
   double *d_scal = nullptr;  // small device scalars
   double *h_scal = nullptr;  // pinned host mirror for GMRES read-backs
-  int64_t launches = 0;
+  int64_t launches = 0;      // launches of this library's kernels
+  int64_t lib_calls = 0;     // cuBLAS DGEMM calls (plain large GEMMs)
+  cublasHandle_t blas = nullptr;
 };
 
 // ---------------------------------------------------------------------------
@@ -263,15 +266,50 @@ static void check_launch() {
 }
 
 // ---- batched launch helpers -------------------------------------------------
+// Batched GEMM dispatch: large plain GEMMs (>= 2^27 flops, both sides >= 64,
+// C not aliasing A or B) go to cuBLAS DGEMM (FP64 tensor cores); the many
+// small / aliased ones to the batched tile kernel k_gemm.
+static bool gemm_overlaps(const GemmJob &g) {
+  auto span = [](const double *p, int rows, int cols, int ld) {
+    return std::make_pair(p, p + (int64_t)(rows - 1) * ld + cols);
+  };
+  auto c = span(g.C, g.m, g.n, g.ldc), a = span(g.A, g.m, g.k, g.lda), b = span(g.B, g.k, g.n, g.ldb);
+  auto hit = [](std::pair<const double *, const double *> x, std::pair<const double *, const double *> y) {
+    return x.first < y.second && y.first < x.second;
+  };
+  return hit(c, a) || hit(c, b);
+}
+
 static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
   if (jobs.empty()) return;
   std::vector<int4> tiles;
+  std::vector<GemmJob> big;
   for (int j = 0; j < (int)jobs.size(); ++j) {
     const GemmJob &g = jobs[j];
     if (g.m <= 0 || g.n <= 0) continue;
+    if (!sk.record && g.k > 0 && g.m >= 64 && g.n >= 64 && 2.0 * g.m * g.n * g.k >= (double)(1 << 27) &&
+        !gemm_overlaps(g)) {
+      big.push_back(g);
+      continue;
+    }
     int tm = (int)cdiv(g.m, GEMM_BM), tn = (int)cdiv(g.n, GEMM_BN);
     for (int a = 0; a < tm; ++a)
       for (int b = 0; b < tn; ++b) tiles.push_back(make_int4(j, a, b, 0));
+  }
+  if (!big.empty()) {
+    Ctx *ctx = sk.ctx;
+    if (!ctx->blas) {
+      if (cublasCreate(&ctx->blas) != CUBLAS_STATUS_SUCCESS) throw runtime_error("cublasCreate failed");
+    }
+    if (cublasSetStream(ctx->blas, ctx->s) != CUBLAS_STATUS_SUCCESS) throw runtime_error("cublasSetStream failed");
+    for (const GemmJob &g : big) {
+      // row-major C = alpha A B + beta C  ==  column-major C^T = alpha B^T A^T + beta C^T
+      double al = g.alpha, be = g.beta;
+      if (cublasDgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, g.n, g.m, g.k, &al, g.B, g.ldb, g.A, g.lda, &be, g.C,
+                      g.ldc) != CUBLAS_STATUS_SUCCESS)
+        throw runtime_error("cublasDgemm failed");
+      ctx->lib_calls++;
+    }
   }
   if (tiles.empty()) return;
   GemmJob *dj = sk.push(jobs);
@@ -555,6 +593,74 @@ static void run_right_upper_solve(Sink &sk, const std::vector<RSolve> &jobs) {
       });
     }
     run_gemm(sk, apply);
+  }
+}
+
+// Full triangular inverse out = T^{-1} (n x n, ld n) of a unit-lower (upper = 0)
+// or non-unit upper (upper = 1) triangle: the 64 x 64 diagonal blocks in one
+// k_trinv launch, then recursive doubling over block pairs,
+//   lower [[A,0],[C,B]]^-1 = [[Ai,0],[-Bi (C Ai), Bi]]
+//   upper [[A,C],[0,B]]^-1 = [[Ai,-Ai (C Bi)],[0,Bi]]
+// two batched GEMMs per level: log2(n / 64) dependent levels instead of n / 64
+// dependent block-solve steps.
+static void run_identity(Sink &sk, const std::vector<double *> &ptrs, const std::vector<int> &dims,
+                         const std::vector<int> &lds);
+struct TriInvReq {
+  const double *T;
+  int ldt, n, upper;
+  double *out;
+};
+static void run_tri_inv(Sink &sk, const std::vector<TriInvReq> &reqs) {
+  if (reqs.empty()) return;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_trinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRINV_SMEM));
+    attr = true;
+  }
+  std::vector<double *> ip;
+  std::vector<int> idim, ild;
+  std::vector<TrinvJob> ti;
+  int maxn = 0;
+  for (auto &r : reqs) {
+    if (r.n <= 0) continue;
+    ip.push_back(r.out), idim.push_back(r.n), ild.push_back(r.n);  // zero triangle
+    for (int c0 = 0; c0 < r.n; c0 += 64) {
+      int w = std::min(64, r.n - c0);
+      ti.push_back(TrinvJob{r.T + (int64_t)c0 * r.ldt + c0, r.ldt, w, r.upper, r.out + (int64_t)c0 * r.n + c0, r.n});
+    }
+    maxn = std::max(maxn, r.n);
+  }
+  run_identity(sk, ip, idim, ild);
+  if (!ti.empty()) {
+    TrinvJob *dj = sk.push(ti);
+    int nb = (int)ti.size();
+    sk.launch([=](cudaStream_t st) {
+      k_trinv<<<nb, 256, TRINV_SMEM, st>>>(dj);
+      check_launch();
+    });
+  }
+  for (int b = 64; b < maxn; b <<= 1) {
+    std::vector<GemmJob> g1, g2;
+    for (auto &r : reqs) {
+      const int n = r.n;
+      for (int k0 = 0; k0 + b < n; k0 += 2 * b) {
+        const int k1 = k0 + b, nb = std::min(b, n - k1);
+        double *Ai = r.out + (int64_t)k0 * n + k0, *Bi = r.out + (int64_t)k1 * n + k1;
+        if (!r.upper) {
+          double *tmp = sk.scratch_d((size_t)nb * b);
+          const double *C = r.T + (int64_t)k1 * r.ldt + k0;  // nb x b
+          g1.push_back(GemmJob{C, Ai, tmp, nb, b, b, r.ldt, n, b, 1.0, 0.0});
+          g2.push_back(GemmJob{Bi, tmp, r.out + (int64_t)k1 * n + k0, nb, b, nb, n, b, n, -1.0, 0.0});
+        } else {
+          double *tmp = sk.scratch_d((size_t)b * nb);
+          const double *C = r.T + (int64_t)k0 * r.ldt + k1;  // b x nb
+          g1.push_back(GemmJob{C, Bi, tmp, b, nb, nb, r.ldt, n, nb, 1.0, 0.0});
+          g2.push_back(GemmJob{Ai, tmp, r.out + (int64_t)k0 * n + k1, b, nb, b, n, nb, n, -1.0, 0.0});
+        }
+      }
+    }
+    run_gemm(sk, g1);
+    run_gemm(sk, g2);
   }
 }
 
@@ -1703,19 +1809,24 @@ struct Factorizer {
           check_launch();
         });
       }
-      // row factor = L^{-1} R[rp[:r], :] ; col factor = C[:, cp[:r]] U^{-1} (bdlr.py:178-183)
+      // row factor = L^{-1} R[rp[:r], :] ; col factor = C[:, cp[:r]] U^{-1} (bdlr.py:178-183):
+      // gathered panels times the explicit triangular inverses (one GEMM each)
       std::vector<CopyJob> gat;
-      std::vector<LSolve> ls;
-      std::vector<RSolve> rs;
+      std::vector<TriInvReq> tinv;
+      std::vector<GemmJob> app;
       for (auto &sj : skel) {
-        gat.push_back(CopyJob{sj.R, sj.row_out, sj.r, sj.n, sj.ldR, sj.n, sj.rp, nullptr});
-        gat.push_back(CopyJob{sj.C, sj.col_out, sj.m, sj.r, sj.ldC, sj.r, nullptr, sj.cp});
-        ls.push_back(LSolve{sj.lu, sj.r, sj.r, sj.row_out, sj.n, sj.n});
-        rs.push_back(RSolve{sj.lu, sj.r, sj.r, sj.col_out, sj.r, sj.m});
+        double *Rg = ctx->scratch.d((size_t)sj.r * sj.n), *Cg = ctx->scratch.d((size_t)sj.m * sj.r);
+        double *Li = ctx->scratch.d((size_t)sj.r * sj.r), *Ui = ctx->scratch.d((size_t)sj.r * sj.r);
+        gat.push_back(CopyJob{sj.R, Rg, sj.r, sj.n, sj.ldR, sj.n, sj.rp, nullptr});
+        gat.push_back(CopyJob{sj.C, Cg, sj.m, sj.r, sj.ldC, sj.r, nullptr, sj.cp});
+        tinv.push_back(TriInvReq{sj.lu, sj.r, sj.r, 0, Li});
+        tinv.push_back(TriInvReq{sj.lu, sj.r, sj.r, 1, Ui});
+        app.push_back(GemmJob{Li, Rg, sj.row_out, sj.r, sj.n, sj.r, sj.r, sj.n, sj.n, 1.0, 0.0});
+        app.push_back(GemmJob{Cg, Ui, sj.col_out, sj.m, sj.r, sj.r, sj.r, sj.r, sj.r, 1.0, 0.0});
       }
       run_copy(s, gat);
-      run_lower_unit_solve(s, ls);
-      run_right_upper_solve(s, rs);
+      run_tri_inv(s, tinv);
+      run_gemm(s, app);
     }
     run_sample(s, dreq, dF, dC);
     cudaEventRecord(ev[5], ctx->s);
@@ -3019,6 +3130,7 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   for (auto e : ctx->c.evpool) cudaEventDestroy(e);
   cudaFree(ctx->c.d_part);
   cudaFree(ctx->c.d_scal);
+  if (ctx->c.blas) cublasDestroy(ctx->c.blas);
   cudaFreeHost(ctx->c.h_scal);
   cudaStreamSynchronize(ctx->c.side);
   cudaEventDestroy(ctx->c.ev_fork);

@@ -1919,6 +1919,7 @@ struct TrinvJob {
   const double *T;
   int ldt, w, upper;
   double *out;
+  int ldo;  // leading dimension of out (w when 0)
 };
 constexpr size_t TRINV_SMEM = sizeof(double) * (64 * 64 + 2 * 64 * 65);
 // Triangular inverse by recursive doubling: with the inverses of the two s x s
@@ -1978,7 +1979,8 @@ __global__ void __launch_bounds__(256) k_trinv(const TrinvJob *__restrict__ jobs
     }
     __syncthreads();
   }
-  for (int e = tid; e < w * w; e += nt) J.out[e] = X[(e / w) * 65 + (e % w)];
+  const int ldo = J.ldo > 0 ? J.ldo : w;
+  for (int e = tid; e < w * w; e += nt) J.out[(long long)(e / w) * ldo + (e % w)] = X[(e / w) * 65 + (e % w)];
 }
 
 // diagonal check after a blocked LU

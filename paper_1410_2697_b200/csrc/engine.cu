@@ -195,6 +195,8 @@ struct Ctx {
   int64_t launches = 0;      // launches of this library's kernels
   int64_t lib_calls = 0;     // cuBLAS DGEMM calls (plain large GEMMs)
   cublasHandle_t blas = nullptr;
+  // device copies of per-tree extend-add maps, keyed by etree uid
+  std::vector<std::pair<uint64_t, int *>> map_dev;
 };
 
 // ---------------------------------------------------------------------------
@@ -1416,7 +1418,47 @@ struct Factorizer {
     (void)upto_flags;
   }
 
-  // ---- child descriptors + to_child maps for a set of fronts ----
+  // ---- extend-add maps (symbolic, once per tree; device copy once per context) ----
+  int *d_maps = nullptr;
+  void ensure_maps() {
+    mfh_mapcache &M = et->mapcache;
+    if (!M.valid) {
+      M.maps.clear();
+      M.off.assign(F->fronts.size(), -1);
+      for (size_t fi = 0; fi < F->fronts.size(); ++fi) {
+        FrontH &f = F->fronts[fi];
+        for (int ci : f.kids) {
+          FrontH &c = F->fronts[ci];
+          // parent position -> child update position (multifrontal.py:270-280, 321-327)
+          M.off[ci] = (int64_t)M.maps.size();
+          M.maps.resize(M.maps.size() + f.nh, -1);
+          int *to = M.maps.data() + M.off[ci];
+          const int64_t *cid = c.ids.data() + c.npv;
+          int p = 0;
+          for (int q = 0; q < c.nf; ++q) {
+            int64_t g = cid[q];
+            while (p < f.nh && f.ids[p] < g) ++p;
+            if (p >= f.nh || f.ids[p] != g)
+              throw value_error("update index " + std::to_string(g) + " not present in parent front (node " +
+                                std::to_string(f.node) + ")");
+            to[p] = q;
+          }
+        }
+      }
+      M.valid = true;
+    }
+    for (auto &m : ctx->map_dev)
+      if (m.first == et->uid) {
+        d_maps = m.second;
+        return;
+      }
+    size_t bytes = sizeof(int) * std::max<size_t>(1, M.maps.size());
+    CK(cudaMalloc(&d_maps, bytes));
+    upload(ctx->s, d_maps, M.maps.data(), sizeof(int) * M.maps.size());
+    ctx->map_dev.push_back({et->uid, d_maps});
+  }
+
+  // ---- child descriptors (maps from the per-tree cache) for a set of fronts ----
   void build_fronts_dev(Sink &s, const std::vector<int> &fis, std::vector<DFront> &dfr,
                         std::vector<DChild> &dch, std::vector<int> &slot_of) {
     slot_of.assign(F->fronts.size(), -1);
@@ -1430,21 +1472,9 @@ struct Factorizer {
       d.child_begin = (int)dch.size();
       for (int ci : f.kids) {
         FrontH &c = F->fronts[ci];
-        // to_child map: parent position -> child update position (multifrontal.py:270-280, 321-327)
-        std::vector<int> to(f.nh, -1);
-        const int64_t *cid = c.ids.data() + c.npv;
-        int cn = c.nf;
-        int p = 0;
-        for (int q = 0; q < cn; ++q) {
-          int64_t g = cid[q];
-          while (p < f.nh && f.ids[p] < g) ++p;
-          if (p >= f.nh || f.ids[p] != g)
-            throw value_error("update index " + std::to_string(g) + " not present in parent front (node " +
-                              std::to_string(f.node) + ")");
-          to[p] = q;
-        }
         DChild ch{};
-        ch.to_child = s.push_keep(to);
+        ch.to_child = d_maps + et->mapcache.off[ci];
+        const int cn = c.nf;
         ch.n = cn;
         if (c.upd == 0) {
           ch.kind = 0;
@@ -2465,6 +2495,8 @@ struct Factorizer {
       F->world = std::max(world, shard->rank + 1);
     }
     auto active = [&](size_t q) { return !F->sharded || F->mine[q] != 0; };
+    ensure_maps();
+    mark_t("maps");
     if (any_struct) {
       if (!(P.eps > 0.0 && P.eps < 1.0)) throw value_error("eps must lie in (0, 1)");
       if (P.n_leaf < 1) throw value_error("n_leaf must be positive");
@@ -2593,10 +2625,11 @@ struct Factorizer {
     for (int u = 0; u < used; ++u) {
       cudaEvent_t *ev = ctx->evpool.data() + 8 * u;
       if (htrace) {
-        float a[7];
+        float a[7], gap = 0.f;
         for (int q = 0; q < 7; ++q) CK(cudaEventElapsedTime(&a[q], ev[q], ev[q + 1]));
-        fprintf(stderr, "[mfh height %3d] fronts %4zu struct %2d | sample %7.3f dense %7.3f plu %7.3f - %7.3f skel %7.3f hodlr %7.3f elim %7.3f ms\n",
-                height_of_use[u], byh[height_of_use[u]].size(), struct_of_use[u], a[0], a[1], a[2], a[3], a[4], a[5], a[6]);
+        if (u > 0) CK(cudaEventElapsedTime(&gap, ctx->evpool[8 * (u - 1) + 7], ev[0]));
+        fprintf(stderr, "[mfh height %3d] fronts %4zu struct %2d | gap %7.3f sample %7.3f dense %7.3f plu %7.3f - %7.3f skel %7.3f hodlr %7.3f elim %7.3f ms\n",
+                height_of_use[u], byh[height_of_use[u]].size(), struct_of_use[u], gap, a[0], a[1], a[2], a[3], a[4], a[5], a[6]);
       }
       float ms;
       CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
@@ -3131,6 +3164,7 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   cudaFree(ctx->c.d_part);
   cudaFree(ctx->c.d_scal);
   if (ctx->c.blas) cublasDestroy(ctx->c.blas);
+  for (auto &m : ctx->c.map_dev) cudaFree(m.second);
   cudaFreeHost(ctx->c.h_scal);
   cudaStreamSynchronize(ctx->c.side);
   cudaEventDestroy(ctx->c.ev_fork);

@@ -60,9 +60,19 @@ struct mfh_symcache {
   bool has_graph = false;
 };
 
+// Extend-add index maps (multifrontal.py:270-280, 321-327) are symbolic: one
+// flat array per tree, map of child c (post index) at [off[c], off[c] + parent nh)
+struct mfh_mapcache {
+  bool valid = false;
+  std::vector<int> maps;
+  std::vector<int64_t> off;  // per post index, -1 when the child passes no update
+};
+
 // Elimination tree in the permuted numbering (ordering.py:211-261).
 struct mfh_etree {
   mutable mfh_symcache cache;
+  mutable mfh_mapcache mapcache;
+  uint64_t uid = 0;  // process-unique id (device-side caches are keyed by it)
   int64_t n = 0;
   int64_t root = -1;
   std::vector<int64_t> perm;

@@ -14,6 +14,8 @@
 
 #include "internal.h"
 
+#include <atomic>
+
 namespace mfh {
 
 Graph adjacency_from_csr(int64_t n, const int64_t *indptr, const int64_t *indices,
@@ -346,6 +348,8 @@ mfh_etree *elimination_tree(const HostCsr &A, const mfh_nd &nd) {
   }
 
   auto *t = new mfh_etree();
+  static std::atomic<uint64_t> next_uid{1};
+  t->uid = next_uid++;
   t->n = n;
   t->root = nd.root;
   t->perm = nd.perm;

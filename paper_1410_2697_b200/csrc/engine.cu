@@ -197,6 +197,14 @@ struct Ctx {
   cublasHandle_t blas = nullptr;
   // device copies of per-tree extend-add maps, keyed by etree uid
   std::vector<std::pair<uint64_t, int *>> map_dev;
+  // per-tree apply structure: contribution CSR over global ids (post order)
+  struct ApplySym {
+    uint64_t uid = 0;
+    int64_t tot = 0;
+    std::vector<int64_t> off;  // contribution slot offset per post index (-1: none)
+    long long *d_cptr = nullptr, *d_coff = nullptr, *d_fro = nullptr;
+  };
+  std::vector<ApplySym> apply_sym;
 };
 
 // ---------------------------------------------------------------------------
@@ -216,9 +224,11 @@ struct Sink {
   }
   void *push_bytes(const void *src, size_t bytes) {
     if (bytes == 0) return nullptr;
-    if (record) {
+    if (record) {  // persistent copy, staged asynchronously (ordered on the stream)
       void *p = persist->alloc(bytes);
-      upload(ctx->s, p, src, bytes);
+      auto hd = ctx->stage.take(bytes);
+      std::memcpy(hd.first, src, bytes);
+      CK(cudaMemcpyAsync(p, hd.first, bytes, cudaMemcpyHostToDevice, ctx->s));
       return p;
     }
     auto hd = ctx->stage.take(bytes);
@@ -1123,6 +1133,11 @@ struct ApplyPlan;
 
 }  // namespace mfh
 
+struct mfh_factor;
+namespace mfh {
+static void build_apply(mfh_factor *F);
+}
+
 struct mfh_ctx {
   mfh::Ctx c;
 };
@@ -1135,6 +1150,7 @@ struct mfh_factor {
   mfh_params params{};
   std::vector<int64_t> perm;
   long long *d_perm = nullptr;
+  uint64_t et_uid = 0;                   // elimination tree the factor was built on
   std::vector<mfh::FrontH> fronts;       // by post-order index
   std::vector<int64_t> post;             // node ids in post order
   std::vector<mfh::BlockH> blocks;
@@ -2338,6 +2354,7 @@ struct Factorizer {
     n = A.n;
     accel = mode == MFH_ACCELERATED;
     F->n = n;
+    F->et_uid = et->uid;
     F->perm = et->perm;
     F->mode = mode;
     F->params = P;
@@ -2612,6 +2629,8 @@ struct Factorizer {
       if (!cut_at[h].empty()) exchange_updates(cut_at[h]);
     }
     CK(cudaEventRecord(e_end, ctx->s));
+    // the apply plan (host work) is built while the GPU finishes the last heights
+    build_apply(F);
     {
       auto tw = std::chrono::steady_clock::now();
       CK(cudaStreamSynchronize(ctx->s));
@@ -2744,16 +2763,15 @@ static FacView fac_view(const mfh_factor *F, const BlockH &b) {
 
 static void run_gemv(Sink &sk, const std::vector<GemvJob> &jobs) {
   if (jobs.empty()) return;
-  std::vector<int2> rows;
-  for (int q = 0; q < (int)jobs.size(); ++q)
-    for (int i = 0; i < jobs[q].m; ++i) rows.push_back(make_int2(q, i));
-  if (rows.empty()) return;
+  std::vector<int> start(jobs.size() + 1, 0);
+  for (size_t q = 0; q < jobs.size(); ++q) start[q + 1] = start[q] + std::max(0, jobs[q].m);
+  const int nr = start.back(), nj = (int)jobs.size();
+  if (nr == 0) return;
   GemvJob *dj = sk.push(jobs);
-  int2 *dr = sk.push(rows);
-  int nr = (int)rows.size();
+  int *ds = sk.push(start);
   int grid = (int)std::min<int64_t>(cdiv((int64_t)nr * 32, 256), 148 * 16);
   sk.launch([=](cudaStream_t st) {
-    k_gemv2<<<grid, 256, 0, st>>>(dj, dr, nr);
+    k_gemv2<<<grid, 256, 0, st>>>(dj, ds, nj, nr);
     check_launch();
   });
 }
@@ -2775,42 +2793,55 @@ static void build_apply(mfh_factor *F) {
   AP->bu = ar.d(std::max<int64_t>(1, n));
   AP->xw = ar.d(std::max<int64_t>(1, n));
   AP->y = ar.d(std::max<int64_t>(1, n));
-  // contribution offsets (post order)
-  std::vector<int64_t> off(F->fronts.size(), -1);
-  int64_t tot = 0;
-  for (size_t q = 0; q < F->fronts.size(); ++q) {
-    FrontH &f = F->fronts[q];
-    if (f.nh == 0 || f.npv == 0 || f.nf == 0) continue;
-    off[q] = tot;
-    tot += f.nf;
-  }
-  AP->cbuf = ar.d(std::max<int64_t>(1, tot));
-  // contributions to each global id, in post order (multifrontal.py:549 order)
-  std::vector<int64_t> cptr(n + 1, 0), coff(tot), fro_all(std::max<int64_t>(1, tot));
-  for (size_t q = 0; q < F->fronts.size(); ++q)
-    if (off[q] >= 0)
-      for (int j = 0; j < F->fronts[q].nf; ++j) {
-        int64_t g = F->fronts[q].ids[F->fronts[q].npv + j];
-        cptr[g + 1]++;
-        fro_all[off[q] + j] = g;
-      }
-  for (int64_t i = 0; i < n; ++i) cptr[i + 1] += cptr[i];
-  {
-    std::vector<int64_t> fill(cptr.begin(), cptr.end() - 1);
+  // contribution CSR (symbolic: built once per tree, kept on the device per context)
+  Ctx::ApplySym *sym = nullptr;
+  for (auto &a : ctx->apply_sym)
+    if (a.uid == F->et_uid) sym = &a;
+  if (!sym) {
+    Ctx::ApplySym a;
+    a.uid = F->et_uid;
+    a.off.assign(F->fronts.size(), -1);
+    int64_t tt = 0;
+    for (size_t q = 0; q < F->fronts.size(); ++q) {
+      FrontH &f = F->fronts[q];
+      if (f.nh == 0 || f.npv == 0 || f.nf == 0) continue;
+      a.off[q] = tt;
+      tt += f.nf;
+    }
+    a.tot = tt;
+    // contributions to each global id, in post order (multifrontal.py:549 order)
+    std::vector<int64_t> cptr(n + 1, 0), coff(std::max<int64_t>(1, tt)), fro_all(std::max<int64_t>(1, tt));
     for (size_t q = 0; q < F->fronts.size(); ++q)
-      if (off[q] >= 0) {
-        FrontH &f = F->fronts[q];
-        for (int j = 0; j < f.nf; ++j) coff[fill[f.ids[f.npv + j]]++] = off[q] + j;
-      }
+      if (a.off[q] >= 0)
+        for (int j = 0; j < F->fronts[q].nf; ++j) {
+          int64_t g = F->fronts[q].ids[F->fronts[q].npv + j];
+          cptr[g + 1]++;
+          fro_all[a.off[q] + j] = g;
+        }
+    for (int64_t i = 0; i < n; ++i) cptr[i + 1] += cptr[i];
+    {
+      std::vector<int64_t> fill(cptr.begin(), cptr.end() - 1);
+      for (size_t q = 0; q < F->fronts.size(); ++q)
+        if (a.off[q] >= 0) {
+          FrontH &f = F->fronts[q];
+          for (int j = 0; j < f.nf; ++j) coff[fill[f.ids[f.npv + j]]++] = a.off[q] + j;
+        }
+    }
+    CK(cudaMalloc(&a.d_cptr, sizeof(int64_t) * (n + 1)));
+    CK(cudaMalloc(&a.d_coff, sizeof(int64_t) * std::max<int64_t>(1, tt)));
+    CK(cudaMalloc(&a.d_fro, sizeof(int64_t) * std::max<int64_t>(1, tt)));
+    upload(ctx->s, a.d_cptr, cptr.data(), sizeof(int64_t) * (n + 1));
+    if (tt) {
+      upload(ctx->s, a.d_coff, coff.data(), sizeof(int64_t) * tt);
+      upload(ctx->s, a.d_fro, fro_all.data(), sizeof(int64_t) * tt);
+    }
+    ctx->apply_sym.push_back(std::move(a));
+    sym = &ctx->apply_sym.back();
   }
-  long long *d_cptr = (long long *)ar.alloc(sizeof(int64_t) * (n + 1));
-  long long *d_coff = (long long *)ar.alloc(sizeof(int64_t) * std::max<int64_t>(1, tot));
-  long long *d_fro = (long long *)ar.alloc(sizeof(int64_t) * std::max<int64_t>(1, tot));
-  upload(ctx->s, d_cptr, cptr.data(), sizeof(int64_t) * (n + 1));
-  if (tot) {
-    upload(ctx->s, d_coff, coff.data(), sizeof(int64_t) * tot);
-    upload(ctx->s, d_fro, fro_all.data(), sizeof(int64_t) * tot);
-  }
+  const std::vector<int64_t> &off = sym->off;
+  const int64_t tot = sym->tot;
+  long long *d_cptr = sym->d_cptr, *d_coff = sym->d_coff, *d_fro = sym->d_fro;
+  AP->cbuf = ar.d(std::max<int64_t>(1, tot));
 
   Sink sk{ctx};
   sk.record = true;
@@ -2913,8 +2944,11 @@ static void build_apply(mfh_factor *F) {
     }
     cb_mask = (int8_t *)ar.alloc(cm.size());
     x_mask = (int8_t *)ar.alloc(xm.size());
-    upload(ctx->s, cb_mask, cm.data(), cm.size());
-    upload(ctx->s, x_mask, xm.data(), xm.size());
+    {
+      Sink up{ctx};
+      up.push_to(cb_mask, cm.data(), cm.size());
+      up.push_to(x_mask, xm.data(), xm.size());
+    }
     cb_tmp = ar.d(ncb);
     x_tmp = ar.d(std::max<int64_t>(1, n));
     sk.launch([=](cudaStream_t s) {
@@ -3027,8 +3061,8 @@ static void build_apply(mfh_factor *F) {
     k_gather_perm<<<grid_n, 256, 0, s>>>(xw, perm, dx, n);
     check_launch();
   });
-  // capture
-  CK(cudaStreamSynchronize(ctx->s));
+  // capture (the stream may still be running the factorization: captured work
+  // is independent of it, and the graph is only launched after it)
   auto tb1 = std::chrono::steady_clock::now();
   auto capture = [&](std::vector<std::function<void(cudaStream_t)>> &ops, cudaGraph_t *g, cudaGraphExec_t *e) {
     CK(cudaStreamBeginCapture(ctx->s, cudaStreamCaptureModeThreadLocal));
@@ -3165,6 +3199,11 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   cudaFree(ctx->c.d_scal);
   if (ctx->c.blas) cublasDestroy(ctx->c.blas);
   for (auto &m : ctx->c.map_dev) cudaFree(m.second);
+  for (auto &a : ctx->c.apply_sym) {
+    cudaFree(a.d_cptr);
+    cudaFree(a.d_coff);
+    cudaFree(a.d_fro);
+  }
   cudaFreeHost(ctx->c.h_scal);
   cudaStreamSynchronize(ctx->c.side);
   cudaEventDestroy(ctx->c.ev_fork);

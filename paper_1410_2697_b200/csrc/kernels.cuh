@@ -2074,14 +2074,35 @@ struct GemvJob {
   double a2;
 };
 
-__global__ void __launch_bounds__(256) k_gemv2(const GemvJob *__restrict__ jobs, const int2 *__restrict__ rows,
-                                               int nrows) {
+// warp per output row; row t belongs to job q with start[q] <= t < start[q + 1].
+// Each warp takes a contiguous chunk of rows: one binary search, then a walk.
+__global__ void __launch_bounds__(256) k_gemv2(const GemvJob *__restrict__ jobs, const int *__restrict__ start,
+                                               int njobs, int nrows) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int t = warp; t < nrows; t += nw) {
-    int2 r = rows[t];
-    const GemvJob &J = jobs[r.x];
-    const int i = r.y;
+  const int chunk = (nrows + nw - 1) / nw;
+  const int t0 = warp * chunk, t1 = min(nrows, t0 + chunk);
+  if (t0 >= t1) return;
+  int q = 0;
+  {
+    int lo = 0, hi = njobs - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (start[mid] <= t0)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    q = lo;
+  }
+  int qend = start[q + 1];
+  for (int t = t0; t < t1; ++t) {
+    while (t >= qend) {
+      ++q;
+      qend = start[q + 1];
+    }
+    const GemvJob &J = jobs[q];
+    const int i = t - start[q];
     double s1 = 0.0, s2 = 0.0;
     if (J.k1) {
       const double *a = J.A1 + (long long)i * J.lda1;

@@ -195,8 +195,15 @@ struct Ctx {
   int64_t launches = 0;      // launches of this library's kernels
   int64_t lib_calls = 0;     // cuBLAS DGEMM calls (plain large GEMMs)
   cublasHandle_t blas = nullptr;
-  // device copies of per-tree extend-add maps, keyed by etree uid
+  // device copies of per-tree extend-add maps and front id lists, keyed by etree uid
   std::vector<std::pair<uint64_t, int *>> map_dev;
+  std::vector<std::pair<uint64_t, long long *>> ids_dev;
+  struct PatDev {  // permuted matrix pattern + gather map, keyed by symcache generation
+    uint64_t gen = 0;
+    long long *ptr = nullptr, *src = nullptr;
+    int *col = nullptr;
+  };
+  std::vector<PatDev> pat_dev;
   // per-tree apply structure: contribution CSR over global ids (post order)
   struct ApplySym {
     uint64_t uid = 0;
@@ -1096,11 +1103,22 @@ struct HTree {
 // ---------------------------------------------------------------------------
 // factorization object
 // ---------------------------------------------------------------------------
+// non-owning view of a front's id list (the per-tree flat cache)
+struct IdsView {
+  const int64_t *p = nullptr;
+  size_t n = 0;
+  const int64_t &operator[](size_t i) const { return p[i]; }
+  const int64_t *data() const { return p; }
+  size_t size() const { return n; }
+  const int64_t *begin() const { return p; }
+  const int64_t *end() const { return p + n; }
+};
+
 struct FrontH {
   int64_t node = -1;
   int npv = 0, nf = 0, nh = 0;
   int64_t piv_lo = 0;
-  std::vector<int64_t> ids;
+  IdsView ids;
   int height = 0;
   bool structured = false;
   std::vector<int> kids;  // fronts with a non-empty update, in node.children order
@@ -1182,6 +1200,13 @@ namespace mfh {
 // ---------------------------------------------------------------------------
 // the factorization driver
 // ---------------------------------------------------------------------------
+// read-only view of the caller's CSR (rows sorted, no duplicates)
+struct CsrView {
+  int64_t n = 0;
+  const int64_t *ptr = nullptr, *idx = nullptr;
+  const double *val = nullptr;
+};
+
 struct Factorizer {
   mfh_factor *F;
   Ctx *ctx;
@@ -1193,7 +1218,6 @@ struct Factorizer {
   // permuted matrix on device
   std::vector<int64_t> ap_ptr;
   std::vector<int> ap_col;
-  std::vector<double> ap_val;
   long long *d_ap_ptr = nullptr;
   int *d_ap_col = nullptr;
   double *d_ap_val = nullptr;
@@ -2341,7 +2365,7 @@ struct Factorizer {
     }
   }
 
-  void run(const HostCsr &A, int mode) {
+  void run(const CsrView &A, int mode) {
     auto t0 = std::chrono::steady_clock::now();
     const bool trace = getenv("MFH_HOST_TRACE") != nullptr;
     auto tprev = t0;
@@ -2365,16 +2389,23 @@ struct Factorizer {
     {
       const std::vector<int64_t> &perm = et->perm;
       const int64_t nnz = A.ptr[n];
-      uint64_t key = 1469598103934665603ULL ^ (uint64_t)n ^ ((uint64_t)nnz << 20) ^ (accel ? 7ULL : 0ULL);
-      auto mix = [&](uint64_t v) { key = (key ^ v) * 1099511628211ULL; };
-      for (int64_t i = 0; i <= n; i += 1) mix((uint64_t)A.ptr[i]);
-      for (int64_t p2 = 0; p2 < nnz; ++p2) {
-        mix((uint64_t)A.idx[p2]);
-        if (A.val[p2] == 0.0) mix(0x9e3779b97f4a7c15ULL ^ (uint64_t)p2);
-      }
       mfh_symcache &C = et->cache;
-      if (!C.valid || C.key != key || (accel && !C.has_graph)) {
+      // the cached symbolic data is valid for exactly this pattern and zero pattern
+      std::vector<int64_t> zeros;
+      for (int64_t p2 = 0; p2 < nnz; ++p2)
+        if (A.val[p2] == 0.0) zeros.push_back(p2);
+      const bool same = C.valid && C.pat_accel == accel && (int64_t)C.pat_ptr.size() == n + 1 &&
+                        (int64_t)C.pat_idx.size() == nnz &&
+                        std::memcmp(C.pat_ptr.data(), A.ptr, sizeof(int64_t) * (n + 1)) == 0 &&
+                        std::memcmp(C.pat_idx.data(), A.idx, sizeof(int64_t) * nnz) == 0 && C.pat_zero == zeros;
+      if (!same) {
         C = mfh_symcache{};
+        C.pat_ptr.assign(A.ptr, A.ptr + n + 1);
+        C.pat_idx.assign(A.idx, A.idx + nnz);
+        C.pat_zero = zeros;
+        C.pat_accel = accel;
+        static std::atomic<uint64_t> next_gen{1};
+        C.gen = next_gen++;
         std::vector<int64_t> iperm(n);
         for (int64_t i = 0; i < n; ++i) iperm[perm[i]] = i;
         // T = (P A P^T)^T: row = new column, entries in increasing new row
@@ -2436,19 +2467,41 @@ struct Factorizer {
           }
           C.has_graph = true;
         }
-        C.key = key;
         C.valid = true;
       }
-      ap_val.resize(nnz);
-      for (int64_t r = 0; r < nnz; ++r) ap_val[r] = A.val[C.src[r]];
       if (accel) gp = &C.graph;
-      d_ap_ptr = (long long *)F->arena.alloc(sizeof(int64_t) * (n + 1));
-      d_ap_col = F->arena.i(std::max<int64_t>(1, nnz));
+      // permuted pattern + value-gather map: on the device once per (context, pattern)
+      Ctx::PatDev *pd = nullptr;
+      for (auto &q : ctx->pat_dev)
+        if (q.gen == C.gen) pd = &q;
+      if (!pd) {
+        Ctx::PatDev q;
+        q.gen = C.gen;
+        CK(cudaMalloc(&q.ptr, sizeof(int64_t) * (n + 1)));
+        CK(cudaMalloc(&q.col, sizeof(int) * std::max<int64_t>(1, nnz)));
+        CK(cudaMalloc(&q.src, sizeof(int64_t) * std::max<int64_t>(1, nnz)));
+        upload(ctx->s, q.ptr, C.ap_ptr.data(), sizeof(int64_t) * (n + 1));
+        if (nnz) {
+          upload(ctx->s, q.col, C.ap_col.data(), sizeof(int) * nnz);
+          upload(ctx->s, q.src, C.src.data(), sizeof(int64_t) * nnz);
+        }
+        ctx->pat_dev.push_back(q);
+        pd = &ctx->pat_dev.back();
+      }
+      d_ap_ptr = pd->ptr;
+      d_ap_col = pd->col;
       d_ap_val = F->arena.d(std::max<int64_t>(1, nnz));
-      upload(ctx->s, d_ap_ptr, C.ap_ptr.data(), sizeof(int64_t) * (n + 1));
       if (nnz) {
-        upload(ctx->s, d_ap_col, C.ap_col.data(), sizeof(int) * nnz);
-        upload(ctx->s, d_ap_val, ap_val.data(), sizeof(double) * nnz);
+        // raw values staged asynchronously, gathered into P A P^T order on the device
+        double *raw = F->arena.d(nnz);
+        Sink up{ctx};
+        up.push_to(raw, A.val, sizeof(double) * nnz);
+        const long long *srcp = pd->src;
+        double *dst = d_ap_val;
+        int g = (int)std::min<int64_t>(cdiv(nnz, 256), 148 * 8);
+        k_gather_idx<<<g, 256, 0, ctx->s>>>(srcp, raw, dst, nnz);
+        check_launch();
+        ctx->launches++;
       }
     }
     mark_t("permute+graph");
@@ -2456,6 +2509,20 @@ struct Factorizer {
     int64_t nn = (int64_t)et->parent.size();
     std::vector<int> pidx(nn, -1);
     F->post = et->post;
+    {  // front id lists (symbolic): flattened once per tree
+      mfh_mapcache &M = et->mapcache;
+      if (!M.ids_valid) {
+        M.ids_flat.clear();
+        M.ids_off.assign(et->post.size(), 0);
+        for (size_t q = 0; q < et->post.size(); ++q) {
+          int64_t p = et->post[q];
+          M.ids_off[q] = (int64_t)M.ids_flat.size();
+          M.ids_flat.insert(M.ids_flat.end(), et->piv.begin() + et->piv_ptr[p], et->piv.begin() + et->piv_ptr[p + 1]);
+          M.ids_flat.insert(M.ids_flat.end(), et->fr.begin() + et->fr_ptr[p], et->fr.begin() + et->fr_ptr[p + 1]);
+        }
+        M.ids_valid = true;
+      }
+    }
     F->fronts.resize(et->post.size());
     F->front_blocks.assign(et->post.size(), {});
     double thr = accel ? (double)P.n_c : INFINITY;
@@ -2471,8 +2538,7 @@ struct Factorizer {
       f.npv = (int)(pe - pb);
       f.nf = (int)(fe - fb);
       f.nh = f.npv + f.nf;
-      f.ids.assign(et->piv.begin() + pb, et->piv.begin() + pe);
-      f.ids.insert(f.ids.end(), et->fr.begin() + fb, et->fr.begin() + fe);
+      f.ids = IdsView{et->mapcache.ids_flat.data() + et->mapcache.ids_off[q], (size_t)f.nh};
       f.piv_lo = f.npv ? f.ids[0] : 0;
       for (int q2 = 1; q2 < f.npv; ++q2)
         if (f.ids[q2] != f.ids[q2 - 1] + 1) throw runtime_error("pivot ids are not a contiguous run");
@@ -2527,17 +2593,23 @@ struct Factorizer {
     F->d_perm = (long long *)F->arena.alloc(sizeof(int64_t) * std::max<int64_t>(1, n));
     upload(ctx->s, F->d_perm, et->perm.data(), sizeof(int64_t) * n);
     // device ids + flags
-    {  // all front id lists in one upload
+    {  // all front id lists: symbolic, on the device once per (context, tree)
+      long long *all = nullptr;
+      for (auto &m : ctx->ids_dev)
+        if (m.first == et->uid) all = m.second;
       int64_t tot = 0;
-      for (auto &f : F->fronts) tot += f.nh;
-      long long *all = (long long *)F->arena.alloc(sizeof(int64_t) * std::max<int64_t>(1, tot));
-      std::vector<int64_t> flat;
-      flat.reserve(tot);
-      for (auto &f : F->fronts) {
-        f.d_ids = f.nh ? all + flat.size() : nullptr;
-        flat.insert(flat.end(), f.ids.begin(), f.ids.end());
+      if (!all) {
+        for (auto &f : F->fronts) tot += f.nh;
+        const std::vector<int64_t> &flat = et->mapcache.ids_flat;
+        CK(cudaMalloc(&all, sizeof(int64_t) * std::max<int64_t>(1, tot)));
+        upload(ctx->s, all, flat.data(), sizeof(int64_t) * tot);
+        ctx->ids_dev.push_back({et->uid, all});
       }
-      upload(ctx->s, all, flat.data(), sizeof(int64_t) * tot);
+      int64_t o = 0;
+      for (auto &f : F->fronts) {
+        f.d_ids = f.nh ? all + o : nullptr;
+        o += f.nh;
+      }
     }
     mark_t("identity+uploads");
     int max_flags = 0;
@@ -2712,6 +2784,9 @@ struct Factorizer {
     F->stats.n_records = (int64_t)F->records.size();
     F->stats.stored_reals = retained;
     F->stats.device_bytes_peak = (int64_t)F->arena.capacity() + (int64_t)ctx->scratch.capacity();
+    // id views point into the tree's cache; nothing after the factorization
+    // (the apply plan is already built) may read them
+    for (auto &f : F->fronts) f.ids = IdsView{};
     F->timing.total_ms = tot;
     F->timing.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
@@ -3199,6 +3274,12 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   cudaFree(ctx->c.d_scal);
   if (ctx->c.blas) cublasDestroy(ctx->c.blas);
   for (auto &m : ctx->c.map_dev) cudaFree(m.second);
+  for (auto &m : ctx->c.ids_dev) cudaFree(m.second);
+  for (auto &q : ctx->c.pat_dev) {
+    cudaFree(q.ptr);
+    cudaFree(q.col);
+    cudaFree(q.src);
+  }
   for (auto &a : ctx->c.apply_sym) {
     cudaFree(a.d_cptr);
     cudaFree(a.d_coff);
@@ -3234,11 +3315,7 @@ static int factorize_common(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const i
   if (mode != MFH_CONVENTIONAL && mode != MFH_ACCELERATED) throw value_error("unknown mode");
   if (t->n != n) throw value_error("separator tree size does not match the matrix");
   CK(cudaSetDevice(ctx->c.device));
-  HostCsr A;
-  A.n = n;
-  A.ptr.assign(indptr, indptr + n + 1);
-  A.idx.assign(indices, indices + A.ptr[n]);
-  A.val.assign(values, values + A.ptr[n]);
+  CsrView A{n, indptr, indices, values};  // the caller's arrays, read-only (no copy)
   F = new mfh_factor();
   F->ctx = &ctx->c;
   F->arena.pool = &ctx->c.pool;

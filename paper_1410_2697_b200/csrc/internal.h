@@ -54,6 +54,10 @@ struct mfh_nd {
 struct mfh_symcache {
   uint64_t key = 0;
   bool valid = false;
+  // exact validation of the cached pattern (no hashing of the whole pattern per call)
+  std::vector<int64_t> pat_ptr, pat_idx, pat_zero;
+  bool pat_accel = false;
+  uint64_t gen = 0;  // process-unique generation (device copies are keyed by it)
   std::vector<int64_t> ap_ptr, src;  // src[r]: position in A's CSR values of Ap entry r
   std::vector<int> ap_col;
   mfh::Graph graph;
@@ -66,6 +70,9 @@ struct mfh_mapcache {
   bool valid = false;
   std::vector<int> maps;
   std::vector<int64_t> off;  // per post index, -1 when the child passes no update
+  // front id lists (pivots then frontal ids) of every node in post order, flat
+  bool ids_valid = false;
+  std::vector<int64_t> ids_flat, ids_off;
 };
 
 // Elimination tree in the permuted numbering (ordering.py:211-261).

@@ -182,8 +182,9 @@ static void upload(cudaStream_t st, void *dst, const void *src, size_t bytes) {
 struct Ctx {
   int device = 0;
   cudaStream_t s = nullptr;
-  cudaStream_t side = nullptr;  // concurrent large-core cluster kernels
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t side = nullptr;   // concurrent large-core cluster / cooperative kernels
+  cudaStream_t side2 = nullptr;  // 8-CTA cluster cores, concurrently with the 16-CTA ones
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
   int cluster_size = 16;
   ChunkPool pool;
   std::vector<cudaEvent_t> evpool;  // per-height phase events, reused
@@ -822,8 +823,14 @@ static void launch_cluster(const void *fn, int ncores, int cs, size_t smem, cuda
   if (e != cudaSuccess) throw runtime_error(std::string("cluster launch failed: ") + cudaGetErrorString(e));
 }
 
-static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
-  if (jobs.empty()) return;
+// main_work (optional) is enqueued on the main stream while the side streams
+// run the cluster / cooperative cores
+static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
+                    const std::function<void()> &main_work = nullptr) {
+  if (jobs.empty()) {
+    if (main_work) main_work();
+    return;
+  }
   Ctx *ctx = sk.ctx;
   static bool attr_done = false;
   static size_t dyn_max = 0;
@@ -989,16 +996,20 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
   if (side) {
     CK(cudaEventRecord(ctx->ev_fork, ctx->s));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    if (!cl8.empty()) CK(cudaStreamWaitEvent(ctx->side2, ctx->ev_fork, 0));
   }
-  auto cluster_group = [&](const std::vector<int> &g, int *dids, int cs) {
+  auto cluster_group = [&](const std::vector<int> &g, int *dids, int cs, cudaStream_t st) {
     if (g.empty()) return;
     size_t sm = 0;
     for (int q : g) sm = std::max(sm, plu_cl3_bytes(jobs[q].m, jobs[q].n, cs));
-    launch_cluster(fns[2], (int)g.size(), cs, sm, ctx->side, dj, dids, eps);
+    launch_cluster(fns[2], (int)g.size(), cs, sm, st, dj, dids, eps);
     ctx->launches++;
   };
-  cluster_group(cl16, ids_cl16, CS);
-  cluster_group(cl8, ids_cl8, 8);
+  // 8-CTA clusters on their own stream: they run beside the 16-CTA clusters
+  // (and ahead of the cooperative launch, which waits for free SMs)
+  cluster_group(cl8, ids_cl8, 8, ctx->side2);
+  if (!cl8.empty()) CK(cudaEventRecord(ctx->ev_join2, ctx->side2));
+  cluster_group(cl16, ids_cl16, CS, ctx->side);
   for (int v = 0; v < 2; ++v) {
     GridLaunch &L = gl[v];
     if (L.ids.empty()) continue;
@@ -1015,6 +1026,7 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
     ctx->launches++;
   }
   if (side) CK(cudaEventRecord(ctx->ev_join, ctx->side));
+  if (main_work) main_work();
   for (int b = 0; b < 3; ++b) {
     if (small[b].empty()) continue;
     int *dids = sk.push(small[b]);
@@ -1027,6 +1039,7 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps) {
     });
   }
   if (side) CK(cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0));
+  if (!cl8.empty()) CK(cudaStreamWaitEvent(ctx->s, ctx->ev_join2, 0));
 }
 
 // ---------------------------------------------------------------------------
@@ -1738,7 +1751,9 @@ struct Factorizer {
     cudaEventRecord(ev[1], ctx->s);
 
     // ------------------------------------------------ dense fronts: eliminate
-    {
+    // (at heights with structured fronts this runs on the main stream inside
+    // the pivot-LU window, overlapping the side-stream complete-pivot LU)
+    auto dense_elim = [&]() {
       // F_pp^{-1} explicitly (multifrontal.py:302-306 semantics incl. the singular
       // check); Gpf = F_pp^{-1} F_pf; Schur update F_ff -= F_fp Gpf; Gfp = F_fp F_pp^{-1}
       std::vector<InvReq> inv;
@@ -1774,16 +1789,18 @@ struct Factorizer {
         f.factor_reals = (f.npv ? (int64_t)f.npv * f.npv : 0) + 2 * (int64_t)f.npv * f.nf;
         f.upd_reals = (int64_t)f.nf * f.nf;
       }
-    }
-    cudaEventRecord(ev[2], ctx->s);
+    };
     if (S.empty()) {
+      dense_elim();
+      cudaEventRecord(ev[2], ctx->s);
       for (int q = 3; q < 8; ++q) cudaEventRecord(ev[q], ctx->s);
       return;
     }
+    cudaEventRecord(ev[2], ctx->s);
 
     // ------------------------------------------------ structured: pivot LU
     run_copy(s, core_copies);
-    run_plu(s, plu, P.eps);
+    run_plu(s, plu, P.eps, dense_elim);
     cudaEventRecord(ev[3], ctx->s);
     // read ranks, status and pivot sequences: one D2H pair for the height
     {
@@ -3252,8 +3269,10 @@ extern "C" int mfh_ctx_create(int device, mfh_ctx **out) {
   c->c.device = device;
   CK(cudaStreamCreateWithFlags(&c->c.s, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->c.side, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->c.side2, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->c.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->c.ev_join, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->c.ev_join2, cudaEventDisableTiming));
   c->c.stage.init(size_t(64) << 20);
   c->c.scratch.chunk = size_t(512) << 20;
   CK(cudaMalloc(&c->c.d_part, sizeof(double) * (RED_BLOCKS + 64)));
@@ -3287,9 +3306,12 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   }
   cudaFreeHost(ctx->c.h_scal);
   cudaStreamSynchronize(ctx->c.side);
+  cudaStreamSynchronize(ctx->c.side2);
   cudaEventDestroy(ctx->c.ev_fork);
   cudaEventDestroy(ctx->c.ev_join);
+  cudaEventDestroy(ctx->c.ev_join2);
   cudaStreamDestroy(ctx->c.side);
+  cudaStreamDestroy(ctx->c.side2);
   cudaStreamDestroy(ctx->c.s);
   delete ctx;
 }

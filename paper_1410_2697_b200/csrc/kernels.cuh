@@ -1781,6 +1781,7 @@ __global__ void __launch_bounds__(NW * 32) k_inv_reg(const InvJob *__restrict__ 
   __shared__ int ci[NW];
   __shared__ int piv[NR], idx[NC];
   __shared__ int bad;
+  __shared__ double s_rinv;
   const InvJob J = jobs[blockIdx.x];
   const int n = J.n, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double a[8][CPL];
@@ -1792,102 +1793,108 @@ __global__ void __launch_bounds__(NW * 32) k_inv_reg(const InvJob *__restrict__ 
       a[r][c] = (i < n && j < n) ? J.a[(long long)i * J.lda + j] : 0.0;
     }
   if (threadIdx.x == 0) bad = 0;
-  for (int k = 0; k < n; ++k) {
-    const int kl = k & 31, kc = k >> 5;
-    double *colk = colkb[k & 1];
-    if (lane == kl) {
-      // rows ascend, so a strict '>' keeps the first maximum
-      double bv = -1.0;
-      int bi = 0x7fffffff;
+  bool stop = false;
+  // step k = 32 kc + kl: the column group kc is a compile-time register index
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        int i = warp * 8 + r;
-        double v = 0.0;
+  for (int kc = 0; kc < CPL; ++kc) {
+    if (stop) break;
+    for (int kl = 0; kl < 32; ++kl) {
+      const int k = kc * 32 + kl;
+      if (k >= n) {
+        stop = true;
+        break;
+      }
+      double *colk = colkb[k & 1];
+      if (lane == kl) {
+        // rows ascend, so a strict '>' keeps the first maximum
+        double bv = -1.0;
+        int bi = 0x7fffffff;
 #pragma unroll
-        for (int c = 0; c < CPL; ++c)
-          if (c == kc) v = a[r][c];
-        colk[i] = v;
-        if (i >= k && i < n && fabs(v) > bv) {
-          bv = fabs(v);
-          bi = i;
+        for (int r = 0; r < 8; ++r) {
+          const int i = warp * 8 + r;
+          const double v = a[r][kc];
+          colk[i] = v;
+          if (i >= k && i < n && fabs(v) > bv) {
+            bv = fabs(v);
+            bi = i;
+          }
+        }
+        cv[warp] = bv;
+        ci[warp] = bi;
+      }
+      __syncthreads();
+      // every warp reduces the NW candidates (ties -> lower row)
+      double bv = lane < NW ? cv[lane] : -1.0;
+      int bi = lane < NW ? ci[lane] : 0x7fffffff;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        if (off >= NW) continue;
+        double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
         }
       }
-      cv[warp] = bv;
-      ci[warp] = bi;
-    }
-    __syncthreads();
-    // every warp reduces the NW candidates (ties -> lower row)
-    double bv = lane < NW ? cv[lane] : -1.0;
-    int bi = lane < NW ? ci[lane] : 0x7fffffff;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      if (off >= NW) continue;
-      double ov = __shfl_xor_sync(0xffffffffu, bv, off);
-      int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (ov > bv || (ov == bv && oi < bi)) {
-        bv = ov;
-        bi = oi;
+      bi = __shfl_sync(0xffffffffu, bi, 0);  // only lanes < NW took part in the reduction
+      const int p = bi == 0x7fffffff ? k : bi;
+      const double pv = colk[p];
+      if (pv == 0.0 || !isfinite(pv)) {
+        if (threadIdx.x == 0) bad = 1;
+        stop = true;
+        break;
       }
-    }
-    bi = __shfl_sync(0xffffffffu, bi, 0);  // only lanes < NW took part in the reduction
-    const int p = bi == 0x7fffffff ? k : bi;
-    const double pv = colk[p];
-    if (pv == 0.0 || !isfinite(pv)) {
-      if (threadIdx.x == 0) bad = 1;
-      break;
-    }
-    if (threadIdx.x == 0) piv[k] = p;
-    if (warp == (k >> 3)) {
+      if (threadIdx.x == 0) piv[k] = p;
+      if (warp == (k >> 3)) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
-        if (warp * 8 + r == k)
+        for (int r = 0; r < 8; ++r)
+          if (warp * 8 + r == k)
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) rowK[lane + 32 * c] = a[r][c];
-    }
-    if (warp == (p >> 3)) {
+            for (int c = 0; c < CPL; ++c) rowK[lane + 32 * c] = a[r][c];
+      }
+      if (warp == (p >> 3)) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
-        if (warp * 8 + r == p)
+        for (int r = 0; r < 8; ++r)
+          if (warp * 8 + r == p)
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) rowP[lane + 32 * c] = a[r][c];
-    }
-    __syncthreads();
-    const double rinv = 1.0 / pv;
-    double pj[CPL];
+            for (int c = 0; c < CPL; ++c) rowP[lane + 32 * c] = a[r][c];
+        if (lane == 0) s_rinv = 1.0 / pv;  // one division per step
+      }
+      __syncthreads();
+      const double rinv = s_rinv;
+      double pj[CPL];
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      const int j = lane + 32 * c;
-      pj[c] = (j == k ? 1.0 : rowP[j]) * rinv;  // scaled pivot row (new row k)
-    }
-    // row p takes old row k (the swap); column k is cleared before the update
-    if (warp == (p >> 3) && p != k) {
+      for (int c = 0; c < CPL; ++c) {
+        const int j = lane + 32 * c;
+        pj[c] = (j == k ? 1.0 : rowP[j]) * rinv;  // scaled pivot row (new row k)
+      }
+      // row p takes old row k (the swap); column k is cleared before the update
+      if (warp == (p >> 3) && p != k) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
-        if (warp * 8 + r == p)
+        for (int r = 0; r < 8; ++r)
+          if (warp * 8 + r == p)
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) a[r][c] = rowK[lane + 32 * c];
-    }
-    if (lane == kl) {
+            for (int c = 0; c < CPL; ++c) a[r][c] = rowK[lane + 32 * c];
+      }
+      if (lane == kl) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+        for (int r = 0; r < 8; ++r) a[r][kc] = 0.0;
+      }
+      const double ck_p = colk[k];  // old A[k][k]: row p's column-k value after the swap
 #pragma unroll
-        for (int c = 0; c < CPL; ++c)
-          if (c == kc) a[r][c] = 0.0;
-    }
-    const double ck_p = colk[k];  // old A[k][k]: row p's column-k value after the swap
+      for (int r = 0; r < 8; ++r) {
+        const int i = warp * 8 + r;
+        const double f = (i == p) ? ck_p : colk[i];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int i = warp * 8 + r;
-      const double f = (i == p) ? ck_p : colk[i];
+        for (int c = 0; c < CPL; ++c) a[r][c] = fma(-f, pj[c], a[r][c]);
+      }
+      if (warp == (k >> 3)) {
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) a[r][c] = fma(-f, pj[c], a[r][c]);
-    }
-    if (warp == (k >> 3)) {
+        for (int r = 0; r < 8; ++r)
+          if (warp * 8 + r == k)
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
-        if (warp * 8 + r == k)
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) a[r][c] = pj[c];
+            for (int c = 0; c < CPL; ++c) a[r][c] = pj[c];
+      }
     }
   }
   __syncthreads();

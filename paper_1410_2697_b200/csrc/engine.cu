@@ -802,13 +802,14 @@ static void run_identity(Sink &sk, const std::vector<double *> &ptrs, const std:
 // complete-pivot LU of a batch of cores: small cores run with the core in
 // shared memory, mid-size cores from L2 with bookkeeping in shared memory,
 // large cores on a thread-block cluster (on the side stream, concurrently)
-constexpr long long PLU_CTA_MAX = 16 * 1024;  // entries: one CTA with the core in shared memory
+constexpr long long PLU_CTA_MAX = 32 * 1024;  // entries: one CTA with the core in shared memory (if it fits)
+constexpr int PLU_CL_NT = 1024;               // threads per CTA of the cluster kernel
 
 static void launch_cluster(const void *fn, int ncores, int cs, size_t smem, cudaStream_t st, const PluJob *dj,
                            const int *dids, double eps) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ncores * cs);
-  cfg.blockDim = dim3(512);
+  cfg.blockDim = dim3(PLU_CL_NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -834,8 +835,8 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
   Ctx *ctx = sk.ctx;
   static bool attr_done = false;
   static size_t dyn_max = 0;
-  static const void *fns[6] = {(const void *)k_plu_cta2<true>,      (const void *)k_plu_cta2<false>,
-                               (const void *)k_plu_cluster3,        (const void *)k_plu_cluster2<false>,
+  static const void *fns[6] = {(const void *)k_plu_cta2<true, 512>, (const void *)k_plu_cta2<true, 1024>,
+                               (const void *)k_plu_cluster3<PLU_CL_NT>, (const void *)k_plu_cluster2<false>,
                                (const void *)k_plu_groups<true>,    (const void *)k_plu_groups<false>};
   if (!attr_done) {
     int optin = 0;
@@ -1034,7 +1035,10 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
     for (int q : small[b]) sm = std::max(sm, cta_bytes(jobs[q].m, jobs[q].n));
     int nb = (int)small[b].size();
     sk.launch([=](cudaStream_t st) {
-      k_plu_cta2<true><<<nb, b == 0 ? 256 : 512, sm, st>>>(dj, dids, eps);
+      if (b == 2)
+        k_plu_cta2<true, 1024><<<nb, 1024, sm, st>>>(dj, dids, eps);
+      else
+        k_plu_cta2<true, 512><<<nb, b == 0 ? 256 : 512, sm, st>>>(dj, dids, eps);
       check_launch();
     });
   }

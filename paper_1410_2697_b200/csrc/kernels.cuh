@@ -707,9 +707,9 @@ __device__ __forceinline__ void plu_out(const PluJob &J, const PluState &st) {
   J.outd[2] = st.errprev;
 }
 
-template <bool SMEM_CORE>
-__global__ void __launch_bounds__(512) k_plu_cta2(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
-                                                  double eps) {
+template <bool SMEM_CORE, int NT = 512>
+__global__ void __launch_bounds__(NT) k_plu_cta2(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
+                                                 double eps) {
   extern __shared__ __align__(16) char dsm[];
   __shared__ MaxLoc red[32];
   __shared__ PluState st;
@@ -1163,10 +1163,11 @@ __host__ __device__ inline size_t plu_cl3_bytes(int m, int n, int G) {
   return (b + 15) & ~size_t(15);
 }
 
-__global__ void __launch_bounds__(512) k_plu_cluster3(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
-                                                      double eps) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_plu_cluster3(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
+                                                     double eps) {
   extern __shared__ __align__(16) char dsm[];
-  __shared__ PluCand red[16];
+  __shared__ PluCand red[NT / 32];
   __shared__ PluCand slots[2][16];  // [parity][source CTA]: pushed by every CTA before the barrier
   cg::cluster_group cl = cg::this_cluster();
   const int G = (int)cl.num_blocks(), g = (int)cl.block_rank();

@@ -1323,6 +1323,228 @@ __global__ void __launch_bounds__(NT) k_plu_cluster3(const PluJob *__restrict__ 
   cl.sync();  // DSMEM lifetime: peers may still read this CTA's rows
 }
 
+// Grouped cooperative complete-pivot LU with the cluster kernel's per-step
+// structure (k_plu_cluster3), candidates exchanged through global memory:
+// every CTA publishes (|v|, key, signed v, local row) and its candidate row
+// before the group barrier; after it EVERY warp reduces the group's
+// candidates (L2 reads, __ldcg) and copies the winner's published row. The
+// stop / rank state lives in every thread's registers, row positions with the
+// warp that owns the row, pivoted rows get their column swaps at the end.
+// Same arithmetic and first-max rule: bit-identical results.
+__device__ __forceinline__ PluCand ldcg_cand(const PluCand *p) {
+  PluCand c;
+  c.v = __ldcg(&p->v);
+  c.sv = __ldcg(&p->sv);
+  c.key = __ldcg(&p->key);
+  c.li = __ldcg(&p->li);
+  return c;
+}
+
+__global__ void __launch_bounds__(512) k_plu_groups3(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
+                                                     const int *__restrict__ first, const int *__restrict__ cptr,
+                                                     int ngroups, double eps, GridScratch gs) {
+  extern __shared__ __align__(16) char dsm[];
+  __shared__ PluCand red[16];
+  __shared__ PluCand s_best;
+  __shared__ int s_who, s_myli;
+  int gq = 0;
+  while (gq < ngroups && !((int)blockIdx.x >= first[2 * gq] && (int)blockIdx.x < first[2 * gq + 1])) ++gq;
+  if (gq >= ngroups) return;  // CTA of no group in this launch
+  const int f0 = first[2 * gq], G = first[2 * gq + 1] - f0, g = blockIdx.x - f0;
+  GridScratch mine = gs;
+  // 16-byte slots {signed pivot value, key}: |value| orders, the sign rides along
+  MaxLoc *slots = gs.best + 2 * (size_t)f0;  // [parity][G]
+  double *cand = gs.cand + 2 * (size_t)f0 * gs.nmax;                       // [parity][G][nmax]
+  mine.bar = gs.bar + 2 * gq;
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  for (int cc = cptr[gq]; cc < cptr[gq + 1]; ++cc) {
+    const PluJob J = jobs[ids[cc]];
+    const int m = J.m, n = J.n;
+    const int nl_max = (m + G - 1) / G, nl = (m - g + G - 1) / G, kmin = min(m, n);
+    double *rows = (double *)dsm;
+    double *prow = rows + (size_t)nl_max * n;
+    int *posR = (int *)(prow + n);
+    int *act = posR + nl_max;
+    int *pstep = act + nl_max;
+    int *swp = pstep + nl_max;
+    int *colAt = swp + kmin;
+    for (long long e = tid; e < (long long)nl * n; e += nt) {
+      int li = (int)(e / n), j = (int)(e % n);
+      rows[e] = J.a[(long long)(li * G + g) * J.ld + j];
+    }
+    for (int li = tid; li < nl; li += nt) {
+      posR[li] = li * G + g;
+      act[li] = 1;
+      pstep[li] = -1;
+    }
+    for (int j = tid; j < n; j += nt) colAt[j] = j;
+    __syncthreads();
+    PluCand best = cand_none();
+    for (int li = warp; li < nl; li += nw) {
+      const double *row = rows + (size_t)li * n;
+      double rbv = -1.0, rsv = 0.0;
+      int rj = 0x7fffffff;
+      for (int j = lane; j < n; j += 32) {
+        double x = row[j], av = fabs(x);
+        if (av > rbv) {
+          rbv = av;
+          rsv = x;
+          rj = j;
+        }
+      }
+      const long long key = (long long)(li * G + g) * n + rj;
+      if (rj != 0x7fffffff && better(rbv, key, best.v, best.key)) best = PluCand{rbv, rsv, key, li};
+    }
+    PluState my{};
+    int steps = 0;
+    for (int k = 0; k < kmin; ++k) {
+      const int par = k & 1;
+      {
+        int who = 0;
+        PluCand c = warp_best(best, who);
+        if (lane == 0) red[warp] = c;
+        __syncthreads();
+        if (warp == 0) {
+          PluCand x = lane < nw ? red[lane] : cand_none();
+          x = warp_best(x, who);
+          if (lane == 0) {
+            s_best = x;
+            slots[par * G + g] = MaxLoc{x.key == 0x7fffffffffffffffLL ? -1.0 : x.sv, x.key};
+          }
+        }
+        __syncthreads();
+        const int bl = s_best.li;
+        if (tid == 0) s_myli = bl;
+        if (bl >= 0) {
+          const double *src = rows + (size_t)bl * n;
+          double *dst = cand + ((size_t)par * G + g) * gs.nmax;
+          for (int j = tid; j < n; j += nt) dst[j] = src[j];
+        }
+      }
+      group_barrier(&mine, G);
+      // warp 0 reduces the group's candidates (L2, bypassing L1) and broadcasts
+      // the winner through shared memory (every warp reading them would put
+      // G x warps x CTAs requests on the same lines)
+      if (warp == 0) {
+        double ov[GRID_MAX / 32];
+        long long ok[GRID_MAX / 32];
+#pragma unroll
+        for (int u = 0; u < GRID_MAX / 32; ++u) {  // all loads first, then the in-lane reduction
+          const int q = lane + 32 * u;
+          ov[u] = q < G ? __ldcg(&slots[par * G + q].v) : 0.0;
+          ok[u] = q < G ? __ldcg(&slots[par * G + q].key) : 0x7fffffffffffffffLL;
+        }
+        PluCand gb0 = cand_none();
+        int who0 = 0x7fffffff;
+#pragma unroll
+        for (int u = 0; u < GRID_MAX / 32; ++u) {
+          const double av = ok[u] == 0x7fffffffffffffffLL ? -1.0 : fabs(ov[u]);
+          if (better(av, ok[u], gb0.v, gb0.key)) {
+            gb0 = PluCand{av, ov[u], ok[u], -1};
+            who0 = lane + 32 * u;
+          }
+        }
+        gb0 = warp_best(gb0, who0);
+        if (lane == 0) {
+          s_best = gb0;
+          s_who = who0;
+        }
+      }
+      __syncthreads();
+      const PluCand gb = s_best;
+      const int who = s_who;
+      double piv = gb.v;
+      int pr = k, bj = k;
+      if (gb.key != 0x7fffffffffffffffLL) {
+        pr = (int)(gb.key / n);
+        bj = (int)(gb.key % n);
+      } else {
+        piv = -1.0;
+      }
+      if (plu_stop(my, k, J.kmax, eps, piv)) break;
+      my.prev = fabs(gb.sv);
+      my.rank = k + 1;
+      steps = k + 1;
+      const double akk = gb.sv;
+      {
+        const double *orow = cand + ((size_t)par * G + who) * gs.nmax;
+        for (int j = k + 1 + tid; j < n; j += nt) prow[j] = (j == bj) ? __ldcg(orow + k) : __ldcg(orow + j);
+      }
+      if (tid == 0) {
+        int t = colAt[k];
+        colAt[k] = colAt[bj];
+        colAt[bj] = t;
+        swp[k] = bj;
+        if (who == g) {
+          const int wl = s_myli;  // this CTA won: its published candidate row
+          act[wl] = 0;
+          pstep[wl] = k;
+          posR[wl] = k;
+        }
+      }
+      __syncthreads();
+      best = cand_none();
+      for (int li = warp; li < nl; li += nw) {
+        if (!act[li]) continue;
+        double *row = rows + (size_t)li * n;
+        const double ok_ = row[k], ob = row[bj];
+        int pos = posR[li];
+        const double l = ob / akk;
+        __syncwarp();
+        if (lane == 0) {
+          row[k] = l;
+          if (bj != k) row[bj] = ok_;
+          if (pos == k) posR[li] = pr;
+        }
+        __syncwarp();
+        if (pos == k) pos = pr;
+        double rbv = -1.0, rsv = 0.0;
+        int rj = 0x7fffffff;
+        for (int j = k + 1 + lane; j < n; j += 32) {
+          double v = __dsub_rn(row[j], __dmul_rn(l, prow[j]));
+          row[j] = v;
+          double av = fabs(v);
+          if (av > rbv) {
+            rbv = av;
+            rsv = v;
+            rj = j;
+          }
+        }
+        const long long key = (long long)pos * n + rj;
+        if (rj != 0x7fffffff && better(rbv, key, best.v, best.key)) best = PluCand{rbv, rsv, key, li};
+      }
+    }
+    __syncthreads();
+    for (int li = tid; li < nl; li += nt) {
+      const int p = pstep[li];
+      if (p < 0) continue;
+      double *row = rows + (size_t)li * n;
+      for (int s2 = p; s2 < steps; ++s2) {
+        const int b2 = swp[s2];
+        if (b2 != s2) {
+          double x = row[s2];
+          row[s2] = row[b2];
+          row[b2] = x;
+        }
+      }
+    }
+    __syncthreads();
+    for (long long e = tid; e < (long long)nl * n; e += nt) {
+      int li = (int)(e / n), j = (int)(e % n);
+      J.a[(long long)(li * G + g) * J.ld + j] = rows[e];
+    }
+    for (int li = tid; li < nl; li += nt) J.rowAt[posR[li]] = li * G + g;
+    if (g == 0) {
+      for (int j = tid; j < n; j += nt) J.colAt[j] = colAt[j];
+      if (tid == 0) {
+        plu_out(J, my);
+        J.out[3] = 0;
+      }
+    }
+    group_barrier(&mine, G);  // candidate buffers are reused by the next core
+  }
+}
+
 // Cooperative launch split into groups of CTAs: group q = CTAs
 // [range[2q], range[2q+1]) factors cores ids[cptr[q] .. cptr[q+1]) one after
 // another with its own barrier and candidate buffers, concurrently with the

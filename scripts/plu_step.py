@@ -1,6 +1,10 @@
 """Per-step cost of the complete-pivot LU kernel classes: time one core of a
 given size at two ranks through mfh_full_pivot_lu_batched (copies cancel in the
-difference) -> microseconds per elimination step."""
+difference) -> microseconds per elimination step.
+
+Caveat: the call includes pageable host copies of the core; for cores above
+~1M entries their run-to-run variance is of the order of the difference, so
+use the bench's device-timed pivot-LU phase for decisions at those sizes."""
 import time
 import numpy as np
 import torch

@@ -427,8 +427,7 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
     int mmax = 0;
     for (auto &q : pj) mmax = std::max(mmax, q.n - q.c0);
     int cs = (mmax + PANEL_ROWS_MAX - 1) / PANEL_ROWS_MAX;
-    static const bool legacy_panel = std::getenv("MFH_PANEL_LEGACY") != nullptr;
-    if (cs <= 16 && !legacy_panel) {
+    if (cs <= 16) {
       // shared-memory resident panel across a cluster of cs CTAs
       static bool attr = false;
       if (!attr) {
@@ -547,75 +546,6 @@ static void run_getrs(Sink &sk, const std::vector<RsJob> &jobs) {
   }
 }
 
-// B (n x k, ldb) <- L^{-1} B, L unit lower n x n (ldl): blocked, GEMM-based
-struct LSolve {
-  const double *L;
-  int ldl, n;
-  double *B;
-  int ldb, k;
-};
-static void run_lower_unit_solve(Sink &sk, const std::vector<LSolve> &jobs) {
-  int maxn = 0;
-  for (auto &j : jobs) maxn = std::max(maxn, j.n);
-  for (int c0 = 0; c0 < maxn; c0 += PNB) {
-    std::vector<TrsmJob> tr;
-    std::vector<GemmJob> gm;
-    for (auto &j : jobs) {
-      if (j.n <= c0 || j.k <= 0) continue;
-      int w = std::min(PNB, j.n - c0);
-      const double *T = j.L + (int64_t)c0 * j.ldl + c0;
-      double *Bt = j.B + (int64_t)c0 * j.ldb;
-      tr.push_back(TrsmJob{T, j.ldl, w, Bt, j.ldb, j.k, 0});
-      int rest = j.n - c0 - w;
-      if (rest > 0)
-        gm.push_back(GemmJob{T + (int64_t)w * j.ldl, Bt, Bt + (int64_t)w * j.ldb, rest, j.k, w, j.ldl, j.ldb, j.ldb,
-                             -1.0, 1.0});
-    }
-    run_trsm(sk, tr);
-    run_gemm(sk, gm);
-  }
-}
-
-// X (m x n, ldx) <- X U^{-1}, U upper n x n (ldu), non-unit: blocked by column strips
-struct RSolve {
-  const double *U;
-  int ldu, n;
-  double *X;
-  int ldx, m;
-};
-static void run_right_upper_solve(Sink &sk, const std::vector<RSolve> &jobs) {
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_trinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRINV_SMEM));
-    attr = true;
-  }
-  int maxn = 0;
-  for (auto &j : jobs) maxn = std::max(maxn, j.n);
-  for (int c0 = 0; c0 < maxn; c0 += PNB) {
-    std::vector<GemmJob> upd, apply;
-    std::vector<TrinvJob> ti;
-    for (auto &j : jobs) {
-      if (j.n <= c0 || j.m <= 0) continue;
-      int w = std::min(PNB, j.n - c0);
-      double *Xt = j.X + c0;
-      if (c0 > 0) upd.push_back(GemmJob{j.X, j.U + c0, Xt, j.m, w, c0, j.ldx, j.ldu, j.ldx, -1.0, 1.0});
-      double *inv = sk.scratch_d((size_t)w * w);
-      ti.push_back(TrinvJob{j.U + (int64_t)c0 * j.ldu + c0, j.ldu, w, 1, inv});
-      apply.push_back(GemmJob{Xt, inv, Xt, j.m, w, w, j.ldx, w, j.ldx, 1.0, 0.0});  // in place: one column tile
-    }
-    run_gemm(sk, upd);
-    if (!ti.empty()) {
-      TrinvJob *dj = sk.push(ti);
-      int nb = (int)ti.size();
-      sk.launch([=](cudaStream_t st) {
-        k_trinv<<<nb, 256, TRINV_SMEM, st>>>(dj);
-        check_launch();
-      });
-    }
-    run_gemm(sk, apply);
-  }
-}
-
 // Full triangular inverse out = T^{-1} (n x n, ld n) of a unit-lower (upper = 0)
 // or non-unit upper (upper = 1) triangle: the 64 x 64 diagonal blocks in one
 // k_trinv launch, then recursive doubling over block pairs,
@@ -700,12 +630,6 @@ static void run_identity(Sink &sk, const std::vector<double *> &ptrs, const std:
 // GEMM-based solve against the identity above that
 static void run_inverse(Sink &sk, const std::vector<InvReq> &reqs) {
   if (reqs.empty()) return;
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_inv_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(sizeof(double) * INV_SMALL * INV_SMALL)));
-    attr = true;
-  }
   std::vector<InvJob> small;
   std::vector<CopyJob> cps;
   std::vector<LuJob> lus;
@@ -728,16 +652,7 @@ static void run_inverse(Sink &sk, const std::vector<InvReq> &reqs) {
     }
   }
   run_copy(sk, cps);
-  static const bool legacy_inv = std::getenv("MFH_INV_LEGACY") != nullptr;
-  if (!small.empty() && legacy_inv) {
-    InvJob *dj = sk.push(small);
-    int nb = (int)small.size();
-    size_t sm = sizeof(double) * (size_t)maxs * maxs;
-    sk.launch([=](cudaStream_t st) {
-      k_inv_small<<<nb, maxs > 64 ? 512 : 256, sm, st>>>(dj);
-      check_launch();
-    });
-  } else if (!small.empty()) {
+  if (!small.empty()) {
     // register-tiled Gauss-Jordan: 64-wide tiles (256 threads) or 128-wide (512)
     std::vector<InvJob> s64, s128;
     for (auto &j : small) (j.n <= 64 ? s64 : s128).push_back(j);
@@ -835,10 +750,9 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
   Ctx *ctx = sk.ctx;
   static bool attr_done = false;
   static size_t dyn_max = 0;
-  static const void *fns[7] = {(const void *)k_plu_cta2<true, 512>, (const void *)k_plu_cta2<true, 1024>,
-                               (const void *)k_plu_cluster3<PLU_CL_NT>, (const void *)k_plu_cluster2<false>,
-                               (const void *)k_plu_groups3,         (const void *)k_plu_groups<false>,
-                               (const void *)k_plu_groups<true>};
+  static const void *fns[6] = {(const void *)k_plu_cta2<true, 512>, (const void *)k_plu_cta2<true, 1024>,
+                               (const void *)k_plu_cluster3<PLU_CL_NT>, (const void *)k_plu_groups3,
+                               (const void *)k_plu_groups<false>,   (const void *)k_plu_groups<true>};
   if (!attr_done) {
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
@@ -850,7 +764,7 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
     }
     dyn_max = (size_t)optin - stat - 64;
     for (const void *fn : fns) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
-    for (const void *fn : {fns[2], fns[3]}) {
+    for (const void *fn : {fns[2]}) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) {
         cudaGetLastError();
@@ -1018,7 +932,7 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
     // one group spanning the GPU: the compacted-list kernel measures faster
     // (4.4 vs 8.4 us/step at 1728 x 971); split GPUs: the one-barrier kernel
     const int ngroups_l = (int)L.cptr.size() - 1;
-    const void *fn = v == 1 ? fns[5] : (ngroups_l == 1 ? fns[6] : fns[4]);
+    const void *fn = v == 1 ? fns[4] : (ngroups_l == 1 ? fns[5] : fns[3]);
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, L.smem));
     if (per_sm < 1) throw runtime_error("cooperative pivot-LU kernel does not fit on an SM");

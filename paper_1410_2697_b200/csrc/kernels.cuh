@@ -1095,20 +1095,6 @@ __host__ __device__ inline size_t plu_dist_bytes(int m, int n, int G, bool rows_
   return (b + 15) & ~size_t(15);
 }
 
-template <bool ROWS_SMEM>
-__global__ void __launch_bounds__(512) k_plu_cluster2(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
-                                                      double eps) {
-  extern __shared__ __align__(16) char dsm[];
-  __shared__ MaxLoc red[32];
-  __shared__ MaxLoc slot[2];
-  __shared__ PluState st;
-  __shared__ int s_nact, s_win;
-  cg::cluster_group cl = cg::this_cluster();
-  const int cr = (int)cl.block_rank(), cs = (int)cl.num_blocks();
-  const PluJob J = jobs[ids[blockIdx.x / cs]];
-  plu_dist_body<false, ROWS_SMEM>(J, eps, cs, cr, dsm, red, st, s_nact, &cl, slot, nullptr, &s_win);
-  cl.sync();  // DSMEM lifetime
-}
 
 // ---------------------------------------------------------------------------
 // Cluster complete-pivot LU, one cluster barrier per step (rows in DSMEM)
@@ -1589,40 +1575,7 @@ __global__ void k_lu_extract(const LuExtractJob *__restrict__ jobs) {
   }
 }
 
-// row factor: row_out = L^{-1} R[rp[:r], :]   (bdlr.py:178-181), thread per column
-__global__ void k_skel_row(const SkelJob *__restrict__ jobs, const int2 *__restrict__ chunks,
-                           int nchunks) {
-  for (int t = blockIdx.x; t < nchunks; t += gridDim.x) {
-    int2 ch = chunks[t];
-    const SkelJob J = jobs[ch.x];
-    int j = ch.y * blockDim.x + threadIdx.x;
-    if (j >= J.n) continue;
-    for (int i = 0; i < J.r; ++i) {
-      double acc = J.R[(long long)J.rp[i] * J.ldR + j];
-      const double *L = J.lu + (long long)i * J.r;
-      for (int k = 0; k < i; ++k) acc = fma(-L[k], J.row_out[(long long)k * J.n + j], acc);
-      J.row_out[(long long)i * J.n + j] = acc;
-    }
-  }
-}
 
-// col factor: col_out = C[:, cp[:r]] U^{-1}   (bdlr.py:182-183), thread per row
-__global__ void k_skel_col(const SkelJob *__restrict__ jobs, const int2 *__restrict__ chunks,
-                           int nchunks) {
-  for (int t = blockIdx.x; t < nchunks; t += gridDim.x) {
-    int2 ch = chunks[t];
-    const SkelJob J = jobs[ch.x];
-    int i = ch.y * blockDim.x + threadIdx.x;
-    if (i >= J.m) continue;
-    double *x = J.col_out + (long long)i * J.r;
-    const double *c = J.C + (long long)i * J.ldC;
-    for (int j = 0; j < J.r; ++j) {
-      double acc = c[J.cp[j]];
-      for (int k = 0; k < j; ++k) acc = fma(-J.lu[(long long)k * J.r + j], x[k], acc);
-      x[j] = acc / J.lu[(long long)j * J.r + j];
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // getrf (partial pivoting, LAPACK dgetf2 semantics: first max |a|, row swaps
@@ -1699,54 +1652,6 @@ struct PanelJob {  // panel columns [c0, c0+w) of an n x n matrix, rows c0..n-1
   int *flag;
 };
 
-// partial-pivot LU of a tall panel, swaps restricted to the panel columns
-__global__ void __launch_bounds__(512) k_getrf_panel(const PanelJob *__restrict__ jobs) {
-  __shared__ MaxLoc red[33];
-  __shared__ int s_p;
-  const PanelJob J = jobs[blockIdx.x];
-  const int n = J.n, lda = J.lda, c0 = J.c0, w = J.w, tid = threadIdx.x, nt = blockDim.x;
-  double *a = J.a;
-  for (int k = c0; k < c0 + w; ++k) {
-    double bv = -1.0;
-    long long bk = 0x7fffffffffffffffLL;
-    for (int i = k + tid; i < n; i += nt) {
-      double v = fabs(a[(long long)i * lda + k]);
-      if (better(v, i, bv, bk)) {
-        bv = v;
-        bk = i;
-      }
-    }
-    MaxLoc best = block_maxloc(bv, bk, red);
-    if (tid == 0) {
-      int p = (best.key == 0x7fffffffffffffffLL) ? k : (int)best.key;
-      J.piv[k] = p;
-      s_p = p;
-    }
-    __syncthreads();
-    const int p = s_p;
-    const double pv = a[(long long)p * lda + k];
-    if (pv != 0.0) {
-      if (p != k)
-        for (int j = c0 + tid; j < c0 + w; j += nt) {
-          double t = a[(long long)k * lda + j];
-          a[(long long)k * lda + j] = a[(long long)p * lda + j];
-          a[(long long)p * lda + j] = t;
-        }
-      __syncthreads();
-      const double rinv = 1.0 / pv;
-      for (int i = k + 1 + tid; i < n; i += nt) a[(long long)i * lda + k] *= rinv;
-    }
-    __syncthreads();
-    const int wp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-    for (int i = k + 1 + wp; i < n; i += nw) {
-      const double l = a[(long long)i * lda + k];
-      double *ri = a + (long long)i * lda;
-      const double *rk = a + (long long)k * lda;
-      for (int j = k + 1 + lane; j < c0 + w; j += 32) ri[j] = fma(-l, rk[j], ri[j]);
-    }
-    __syncthreads();
-  }
-}
 
 // Panel LU (partial pivoting, LAPACK rule) with the panel resident in shared
 // memory across a cluster: CTA q of the cluster owns panel rows
@@ -1754,7 +1659,7 @@ __global__ void __launch_bounds__(512) k_getrf_panel(const PanelJob *__restrict_
 // per row. Per column: local candidate -> cluster barrier -> every CTA
 // reduces the CS candidates and pulls the pivot row (and, for the owner of
 // row p, old row k) over DSMEM -> cluster barrier -> swap writes, scale and
-// rank-1 update of the local rows. Same arithmetic as k_getrf_panel.
+// rank-1 update of the local rows. Same arithmetic as the global-memory k_getrf_panel.
 constexpr int PLD = PNB + 1;
 constexpr int PANEL_ROWS_MAX = 416;  // rows per CTA (416 * 65 * 8 = 216 KB)
 __global__ void __launch_bounds__(512) k_getrf_panel_cl(const PanelJob *__restrict__ jobs) {
@@ -1832,6 +1737,56 @@ __global__ void __launch_bounds__(512) k_getrf_panel_cl(const PanelJob *__restri
   cl.sync();  // remote readers are done before this CTA's shared memory goes away
 }
 
+// panel LU with the panel in global memory: fallback for panels taller than a
+// cluster's shared memory holds (16 x PANEL_ROWS_MAX rows)
+__global__ void __launch_bounds__(512) k_getrf_panel(const PanelJob *__restrict__ jobs) {
+  __shared__ MaxLoc red[33];
+  __shared__ int s_p;
+  const PanelJob J = jobs[blockIdx.x];
+  const int n = J.n, lda = J.lda, c0 = J.c0, w = J.w, tid = threadIdx.x, nt = blockDim.x;
+  double *a = J.a;
+  for (int k = c0; k < c0 + w; ++k) {
+    double bv = -1.0;
+    long long bk = 0x7fffffffffffffffLL;
+    for (int i = k + tid; i < n; i += nt) {
+      double v = fabs(a[(long long)i * lda + k]);
+      if (better(v, i, bv, bk)) {
+        bv = v;
+        bk = i;
+      }
+    }
+    MaxLoc best = block_maxloc(bv, bk, red);
+    if (tid == 0) {
+      int p = (best.key == 0x7fffffffffffffffLL) ? k : (int)best.key;
+      J.piv[k] = p;
+      s_p = p;
+    }
+    __syncthreads();
+    const int p = s_p;
+    const double pv = a[(long long)p * lda + k];
+    if (pv != 0.0) {
+      if (p != k)
+        for (int j = c0 + tid; j < c0 + w; j += nt) {
+          double t = a[(long long)k * lda + j];
+          a[(long long)k * lda + j] = a[(long long)p * lda + j];
+          a[(long long)p * lda + j] = t;
+        }
+      __syncthreads();
+      const double rinv = 1.0 / pv;
+      for (int i = k + 1 + tid; i < n; i += nt) a[(long long)i * lda + k] *= rinv;
+    }
+    __syncthreads();
+    const int wp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (int i = k + 1 + wp; i < n; i += nw) {
+      const double l = a[(long long)i * lda + k];
+      double *ri = a + (long long)i * lda;
+      const double *rk = a + (long long)k * lda;
+      for (int j = k + 1 + lane; j < c0 + w; j += 32) ri[j] = fma(-l, rk[j], ri[j]);
+    }
+    __syncthreads();
+  }
+}
+
 // apply the panel's row swaps to the columns outside the panel
 struct SwapJob {
   double *a;
@@ -1864,33 +1819,6 @@ struct TrsmJob {
   int ldb, ncols;
   int upper;
 };
-__global__ void __launch_bounds__(256) k_trsm_small(const TrsmJob *__restrict__ jobs, const int2 *__restrict__ chunks,
-                                                    int nchunks) {
-  __shared__ double Ts[PNB * PNB];
-  for (int t = blockIdx.x; t < nchunks; t += gridDim.x) {
-    int2 ch = chunks[t];
-    const TrsmJob J = jobs[ch.x];
-    __syncthreads();
-    for (int e = threadIdx.x; e < J.w * J.w; e += blockDim.x) Ts[e] = J.T[(long long)(e / J.w) * J.ldt + (e % J.w)];
-    __syncthreads();
-    int c = ch.y * blockDim.x + threadIdx.x;
-    if (c >= J.ncols) continue;
-    double *b = J.B + c;
-    const int w = J.w;
-    if (!J.upper) {
-      for (int i = 0; i < w; ++i) {
-        double xi = b[(long long)i * J.ldb];
-        for (int r = i + 1; r < w; ++r) b[(long long)r * J.ldb] = fma(-Ts[r * w + i], xi, b[(long long)r * J.ldb]);
-      }
-    } else {
-      for (int i = w - 1; i >= 0; --i) {
-        double xi = b[(long long)i * J.ldb] / Ts[i * w + i];
-        b[(long long)i * J.ldb] = xi;
-        for (int r = 0; r < i; ++r) b[(long long)r * J.ldb] = fma(-Ts[r * w + i], xi, b[(long long)r * J.ldb]);
-      }
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // explicit inverses (GPU-native replacement for the reference's lu_factor +
@@ -1904,91 +1832,9 @@ struct InvJob {  // in-place inverse of an n x n block (n <= INV_SMALL)
   int *flag;  // set when a pivot is zero / non-finite (== reference's LU diagonal checks)
 };
 
-// Gauss-Jordan with partial pivoting (first max |a| in the column, LAPACK
-// idamax rule), whole-row swaps, undone as column swaps at the end
-__global__ void __launch_bounds__(512) k_inv_small(const InvJob *__restrict__ jobs) {
-  extern __shared__ double sA[];
-  __shared__ int piv[INV_SMALL];
-  __shared__ double colk[INV_SMALL];
-  __shared__ int s_p, bad;
-  __shared__ double s_pv;
-  const InvJob J = jobs[blockIdx.x];
-  const int n = J.n, tid = threadIdx.x, nt = blockDim.x;
-  for (int e = tid; e < n * n; e += nt) sA[e] = J.a[(long long)(e / n) * J.lda + (e % n)];
-  if (tid == 0) bad = 0;
-  __syncthreads();
-  for (int k = 0; k < n; ++k) {
-    // (1) pivot search by warp 0: first max |a[i][k]|, i >= k
-    if (tid < 32) {
-      double bv = -1.0;
-      long long bk = 0x7fffffffffffffffLL;
-      for (int i = k + tid; i < n; i += 32) {
-        double v = fabs(sA[i * n + k]);
-        if (better(v, i, bv, bk)) {
-          bv = v;
-          bk = i;
-        }
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        double ov = __shfl_down_sync(0xffffffffu, bv, o);
-        long long ok = __shfl_down_sync(0xffffffffu, bk, o);
-        if (better(ov, ok, bv, bk)) {
-          bv = ov;
-          bk = ok;
-        }
-      }
-      if (tid == 0) {
-        int p = bk == 0x7fffffffffffffffLL ? k : (int)bk;
-        s_p = p;
-        piv[k] = p;
-        s_pv = sA[p * n + k];
-      }
-    }
-    __syncthreads();
-    const int p = s_p;
-    const double pv = s_pv;
-    if (pv == 0.0 || !isfinite(pv)) {
-      if (tid == 0) bad = 1;
-      break;
-    }
-    const double rinv = 1.0 / pv;
-    // (2) swap rows k <-> p, scale the new row k, save column k of the other rows
-    for (int t = tid; t < n; t += nt) {
-      double ok_ = sA[k * n + t], op_ = sA[p * n + t];
-      sA[k * n + t] = (t == k ? 1.0 : op_) * rinv;
-      if (p != k) {
-        sA[p * n + t] = ok_;
-        if (t == k) colk[p] = ok_;
-      }
-      if (t != k && t != p) colk[t] = sA[t * n + k];
-    }
-    __syncthreads();
-    // (3) eliminate column k from every other row
-    for (int e = tid; e < n * n; e += nt) {
-      int i = e / n, j = e - (e / n) * n;
-      if (i == k) continue;
-      sA[e] = (j == k ? 0.0 : sA[e]) - colk[i] * sA[k * n + j];
-    }
-    __syncthreads();
-  }
-  if (!bad) {
-    for (int k = n - 1; k >= 0; --k) {
-      int p = piv[k];
-      if (p != k)
-        for (int i = tid; i < n; i += nt) {
-          double t = sA[i * n + k];
-          sA[i * n + k] = sA[i * n + p];
-          sA[i * n + p] = t;
-        }
-      __syncthreads();
-    }
-  }
-  for (int e = tid; e < n * n; e += nt) J.a[(long long)(e / n) * J.lda + (e % n)] = sA[e];
-  if (tid == 0 && bad && J.flag) *J.flag = 1;
-}
 
 // Register-tiled Gauss-Jordan inverse for n <= NW*8 (<= 32*CPL), same pivot
-// rule as k_inv_small: warp w owns rows [8w, 8w+8), lane l owns columns
+// rule as LAPACK getrf (first max |a| in the column): warp w owns rows [8w, 8w+8), lane l owns columns
 // {l, l+32, ...}; each thread keeps its 8 x CPL tile in registers. Per step:
 // every warp publishes its rows' column-k values and its best candidate; all
 // threads reduce the candidates redundantly (no broadcast barrier); the owners
@@ -2393,14 +2239,6 @@ __global__ void k_gather_idx(const long long *__restrict__ src_idx, const double
        t += (long long)gridDim.x * blockDim.x)
     dst[t] = x[src_idx[t]];
 }
-__global__ void k_copy_idx(const long long *__restrict__ idx, const double *__restrict__ src,
-                           double *__restrict__ dst, long long cnt) {
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < cnt;
-       t += (long long)gridDim.x * blockDim.x) {
-    long long g = idx[t];
-    dst[g] = src[g];
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Krylov vector kernels (deterministic reductions: fixed grid, ordered final sum)
@@ -2446,18 +2284,6 @@ __global__ void k_finish(const double *__restrict__ part, double *__restrict__ o
     double s = sum_parts(part);
     *out = do_sqrt ? sqrt(s) : s;
   }
-}
-// h = sum(part); w -= h * v ; block 0 stores h
-__global__ void k_mgs_axpy(const double *__restrict__ part, double *__restrict__ hout,
-                           const double *__restrict__ v, double *__restrict__ w, long long n) {
-  __shared__ double h;
-  if (threadIdx.x == 0) h = sum_parts(part);
-  __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x == 0) *hout = h;
-  const double hh = h;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    w[i] = __dsub_rn(w[i], __dmul_rn(hh, v[i]));  // numpy: w - (h * v)
 }
 // y = a*x (a = 1/s with s read on device)  : V[:, j] = w / h
 __global__ void k_scale_inv(const double *__restrict__ s, const double *__restrict__ x,

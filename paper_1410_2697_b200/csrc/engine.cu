@@ -427,7 +427,20 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
     int mmax = 0;
     for (auto &q : pj) mmax = std::max(mmax, q.n - q.c0);
     int cs = (mmax + PANEL_ROWS_MAX - 1) / PANEL_ROWS_MAX;
-    if (cs <= 16) {
+    if (cs == 1) {
+      // every panel of the batch fits one CTA's shared memory
+      static bool attr1 = false;
+      if (!attr1) {
+        CK(cudaFuncSetAttribute(k_getrf_panel_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(double) * PANEL_ROWS_MAX * PLD)));
+        attr1 = true;
+      }
+      size_t smem = sizeof(double) * (size_t)mmax * PLD;
+      sk.launch([=](cudaStream_t s) {
+        k_getrf_panel_cta<<<np_, 512, smem, s>>>(dp);
+        check_launch();
+      });
+    } else if (cs <= 16) {
       // shared-memory resident panel across a cluster of cs CTAs
       static bool attr = false;
       if (!attr) {
@@ -486,63 +499,6 @@ static void run_check_finite(Sink &sk, const std::vector<LuJob> &jobs) {
       k_check_finite<<<grid, 256, 0, s>>>(dj);
       check_launch();
     });
-  }
-}
-
-static void run_getrs(Sink &sk, const std::vector<RsJob> &jobs) {
-  if (jobs.empty()) return;
-  std::vector<RsJob> small, big;
-  for (auto &j : jobs) (j.n > BIG_N ? big : small).push_back(j);
-  if (!small.empty()) {
-    RsJob *dj = sk.push(small);
-    int nb = (int)small.size();
-    sk.launch([=](cudaStream_t s) {
-      k_getrs<<<nb, 256, 0, s>>>(dj);
-      check_launch();
-    });
-  }
-  if (big.empty()) return;
-  // row interchanges, then blocked forward (unit lower) and backward (upper)
-  std::vector<SwapJob> sw;
-  int maxn = 0;
-  for (auto &j : big) {
-    sw.push_back(SwapJob{j.b, j.ldb, j.k, j.piv, 0, j.n, 0, 0});
-    maxn = std::max(maxn, j.n);
-  }
-  run_laswp(sk, sw);
-  for (int c0 = 0; c0 < maxn; c0 += PNB) {
-    std::vector<TrsmJob> tr;
-    std::vector<GemmJob> gm;
-    for (auto &j : big) {
-      if (j.n <= c0) continue;
-      int w = std::min(PNB, j.n - c0);
-      const double *T = j.a + (int64_t)c0 * j.lda + c0;
-      double *Bt = j.b + (int64_t)c0 * j.ldb;
-      tr.push_back(TrsmJob{T, j.lda, w, Bt, j.ldb, j.k, 0});
-      int rest = j.n - c0 - w;
-      if (rest > 0)
-        gm.push_back(GemmJob{T + (int64_t)w * j.lda, Bt, Bt + (int64_t)w * j.ldb, rest, j.k, w, j.lda, j.ldb, j.ldb,
-                             -1.0, 1.0});
-    }
-    run_trsm(sk, tr);
-    run_gemm(sk, gm);
-  }
-  int nblk = (int)cdiv(maxn, PNB);
-  for (int t = nblk - 1; t >= 0; --t) {
-    int c0 = t * PNB;
-    std::vector<TrsmJob> tr;
-    std::vector<GemmJob> gm;
-    for (auto &j : big) {
-      if (j.n <= c0) continue;
-      int w = std::min(PNB, j.n - c0);
-      const double *T = j.a + (int64_t)c0 * j.lda + c0;
-      double *Bt = j.b + (int64_t)c0 * j.ldb;
-      tr.push_back(TrsmJob{T, j.lda, w, Bt, j.ldb, j.k, 1});
-      if (c0 > 0)
-        gm.push_back(GemmJob{j.a + c0, Bt, j.b, c0, j.k, w, j.lda, j.ldb, j.ldb, -1.0, 1.0});
-    }
-    run_trsm(sk, tr);
-    run_gemm(sk, gm);
   }
 }
 
@@ -633,7 +589,6 @@ static void run_inverse(Sink &sk, const std::vector<InvReq> &reqs) {
   std::vector<InvJob> small;
   std::vector<CopyJob> cps;
   std::vector<LuJob> lus;
-  std::vector<RsJob> rss;
   std::vector<double *> ip;
   std::vector<int> idim, ild;
   int maxs = 1;
@@ -648,7 +603,6 @@ static void run_inverse(Sink &sk, const std::vector<InvReq> &reqs) {
       ip.push_back(r.out);
       idim.push_back(r.n);
       ild.push_back(r.ldo);
-      rss.push_back(RsJob{r.a, r.piv, r.out, r.n, r.lda, r.n, r.ldo});
     }
   }
   run_copy(sk, cps);
@@ -674,9 +628,27 @@ static void run_inverse(Sink &sk, const std::vector<InvReq> &reqs) {
     }
   }
   if (!lus.empty()) {
+    // A^{-1} = U^{-1} L^{-1} P: triangular inverses by recursive doubling, P as the
+    // row-swapped identity, two GEMMs (log-depth instead of n / 64 solve steps)
     run_getrf(sk, lus);
+    std::vector<TriInvReq> ti;
+    std::vector<SwapJob> sw;
+    std::vector<GemmJob> g1, g2;
+    for (size_t q = 0; q < lus.size(); ++q) {
+      const LuJob &L = lus[q];
+      const int n = L.n;
+      double *Li = sk.scratch_d((size_t)n * n), *Ui = sk.scratch_d((size_t)n * n), *T = sk.scratch_d((size_t)n * n);
+      ti.push_back(TriInvReq{L.a, L.lda, n, 0, Li});
+      ti.push_back(TriInvReq{L.a, L.lda, n, 1, Ui});
+      sw.push_back(SwapJob{ip[q], ild[q], n, L.piv, 0, n, 0, 0});
+      g1.push_back(GemmJob{Li, ip[q], T, n, n, n, n, ild[q], n, 1.0, 0.0});
+      g2.push_back(GemmJob{Ui, T, ip[q], n, n, n, n, n, ild[q], 1.0, 0.0});
+    }
+    run_tri_inv(sk, ti);
     run_identity(sk, ip, idim, ild);
-    run_getrs(sk, rss);
+    run_laswp(sk, sw);
+    run_gemm(sk, g1);
+    run_gemm(sk, g2);
   }
 }
 

@@ -80,12 +80,6 @@ struct LuJob {  // partial-pivot LU (getrf) of n x n in place
   int *flag;  // set to 1 when singular / non-finite (reference diag checks)
 };
 
-struct RsJob {  // getrs: solve with LU+piv, B (n x k, ldb) in place
-  const double *a;
-  const int *piv;
-  double *b;
-  int n, lda, k, ldb;
-};
 
 struct CopyJob {  // dst (m x n, ldd) = src (m x n, lds); optional row/col maps on src
   const double *src;
@@ -1787,6 +1781,84 @@ __global__ void __launch_bounds__(512) k_getrf_panel(const PanelJob *__restrict_
   }
 }
 
+// Panel LU in ONE CTA (panel rows <= PANEL_ROWS_MAX): rows in shared memory,
+// thread per row, warp argmax by redux (first max |a|, NaN never wins, ties to
+// the lower row), two or three block barriers per column. Same arithmetic as
+// k_getrf_panel_cl / k_getrf_panel (multiply by 1/pv, FMA update).
+__device__ __forceinline__ void warp_argmax_row(double v, int row, unsigned &uh_out, unsigned &ul_out,
+                                                int &row_out) {
+  const unsigned long long u = (v >= 0.0) ? (unsigned long long)__double_as_longlong(v) + 1ull : 0ull;
+  const unsigned uh = (unsigned)(u >> 32), ul = (unsigned)u;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, uh);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, uh == mh ? ul : 0u);
+  const bool top = uh == mh && ul == ml;
+  const unsigned r = (unsigned)__reduce_min_sync(0xffffffffu, top ? (unsigned)row : 0x7fffffffu);
+  uh_out = mh;
+  ul_out = ml;
+  row_out = (int)r;
+}
+
+__global__ void __launch_bounds__(512) k_getrf_panel_cta(const PanelJob *__restrict__ jobs) {
+  extern __shared__ double sh_panel[];
+  __shared__ unsigned s_uh[16], s_ul[16];
+  __shared__ int s_row[16];
+  const PanelJob J = jobs[blockIdx.x];
+  const int n = J.n, lda = J.lda, c0 = J.c0, w = J.w, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m = n - c0;
+  double *a = J.a;
+  for (int e = tid; e < m * w; e += blockDim.x) {
+    int t = e / w, j = e - t * w;
+    sh_panel[t * PLD + j] = a[(long long)(c0 + t) * lda + c0 + j];
+  }
+  __syncthreads();
+  double *myrow = tid < m ? sh_panel + tid * PLD : nullptr;
+  for (int kk = 0; kk < w; ++kk) {
+    const double v = (myrow && tid >= kk) ? fabs(myrow[kk]) : -1.0;
+    unsigned uh, ul;
+    int r;
+    warp_argmax_row(v, tid, uh, ul, r);
+    if (lane == 0) {
+      s_uh[warp] = uh;
+      s_ul[warp] = ul;
+      s_row[warp] = r;
+    }
+    __syncthreads();
+    {  // every warp reduces the 16 warp candidates (warps ascend in rows)
+      const unsigned xh = lane < 16 ? s_uh[lane] : 0u, xl = lane < 16 ? s_ul[lane] : 0u;
+      const int xr = lane < 16 ? s_row[lane] : 0x7fffffff;
+      const unsigned mh = __reduce_max_sync(0xffffffffu, xh);
+      const unsigned ml = __reduce_max_sync(0xffffffffu, xh == mh ? xl : 0u);
+      r = (int)__reduce_min_sync(0xffffffffu, (xh == mh && xl == ml) ? (unsigned)xr : 0x7fffffffu);
+      if (mh == 0u && ml == 0u) r = kk;  // no candidate: keep row kk
+    }
+    const int p = r;
+    const double pv = sh_panel[p * PLD + kk];
+    if (tid == 0) J.piv[c0 + kk] = c0 + p;
+    if (p != kk && pv != 0.0) {
+      if (tid < w) {
+        double t = sh_panel[kk * PLD + tid];
+        sh_panel[kk * PLD + tid] = sh_panel[p * PLD + tid];
+        sh_panel[p * PLD + tid] = t;
+      }
+      __syncthreads();
+    }
+    if (myrow && tid > kk) {
+      double l = myrow[kk];
+      if (pv != 0.0) {
+        l *= 1.0 / pv;
+        myrow[kk] = l;
+      }
+      const double *prow = sh_panel + kk * PLD;
+      for (int j = kk + 1; j < w; ++j) myrow[j] = fma(-l, prow[j], myrow[j]);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < m * w; e += blockDim.x) {
+    int t = e / w, j = e - t * w;
+    a[(long long)(c0 + t) * lda + c0 + j] = sh_panel[t * PLD + j];
+  }
+}
+
 // apply the panel's row swaps to the columns outside the panel
 struct SwapJob {
   double *a;
@@ -2087,48 +2159,6 @@ __global__ void k_check_finite(const LuJob *__restrict__ jobs) {
   }
   __syncthreads();
   if (threadIdx.x == 0 && bad && J.flag) *J.flag = 1;
-}
-
-// getrs: B <- (LU)^{-1} P B, column-oriented substitution (dtrsm order)
-__global__ void __launch_bounds__(256) k_getrs(const RsJob *__restrict__ jobs) {
-  const RsJob J = jobs[blockIdx.x];
-  const int n = J.n, k = J.k, tid = threadIdx.x, nt = blockDim.x;
-  const double *a = J.a;
-  double *b = J.b;
-  // row interchanges (dlaswp), each thread owns whole columns
-  for (int c = tid; c < k; c += nt)
-    for (int i = 0; i < n; ++i) {
-      int p = J.piv[i];
-      if (p != i) {
-        double t = b[(long long)i * J.ldb + c];
-        b[(long long)i * J.ldb + c] = b[(long long)p * J.ldb + c];
-        b[(long long)p * J.ldb + c] = t;
-      }
-    }
-  __syncthreads();
-  // forward: unit lower
-  for (int i = 0; i < n - 1; ++i) {
-    int rows = n - 1 - i;
-    long long work = (long long)rows * k;
-    for (long long e = tid; e < work; e += nt) {
-      int r = i + 1 + (int)(e / k), c = (int)(e % k);
-      b[(long long)r * J.ldb + c] = fma(-a[(long long)r * J.lda + i], b[(long long)i * J.ldb + c],
-                                        b[(long long)r * J.ldb + c]);
-    }
-    __syncthreads();
-  }
-  // backward: upper
-  for (int i = n - 1; i >= 0; --i) {
-    for (int c = tid; c < k; c += nt) b[(long long)i * J.ldb + c] /= a[(long long)i * J.lda + i];
-    __syncthreads();
-    long long work = (long long)i * k;
-    for (long long e = tid; e < work; e += nt) {
-      int r = (int)(e / k), c = (int)(e % k);
-      b[(long long)r * J.ldb + c] = fma(-a[(long long)r * J.lda + i], b[(long long)i * J.ldb + c],
-                                        b[(long long)r * J.ldb + c]);
-    }
-    __syncthreads();
-  }
 }
 
 // ---------------------------------------------------------------------------

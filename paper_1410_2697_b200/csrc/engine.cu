@@ -3000,8 +3000,8 @@ static void build_apply(mfh_factor *F) {
         }
       }
     }
+    j0.insert(j0.end(), j1.begin(), j1.end());  // independent: one launch
     run_gemv(sk, j0);
-    run_gemv(sk, j1);
     run_gemv(sk, j2);
   }
   };

@@ -1214,8 +1214,14 @@ __global__ void __launch_bounds__(NT) k_plu_cluster3(const PluJob *__restrict__ 
     double piv = gb.v;
     int pr = k, bj = k;
     if (gb.key != 0x7fffffffffffffffLL) {
-      pr = (int)(gb.key / n);
-      bj = (int)(gb.key % n);
+      if (gb.key < 0xffffffffLL) {  // keys of cluster-sized cores fit 32 bits: cheap division
+        const unsigned k32 = (unsigned)gb.key, q32 = k32 / (unsigned)n;
+        pr = (int)q32;
+        bj = (int)(k32 - q32 * (unsigned)n);
+      } else {
+        pr = (int)(gb.key / n);
+        bj = (int)(gb.key % n);
+      }
     } else {
       piv = -1.0;
     }
@@ -1436,8 +1442,14 @@ __global__ void __launch_bounds__(512) k_plu_groups3(const PluJob *__restrict__ 
       double piv = gb.v;
       int pr = k, bj = k;
       if (gb.key != 0x7fffffffffffffffLL) {
-        pr = (int)(gb.key / n);
-        bj = (int)(gb.key % n);
+        if (gb.key < 0xffffffffLL) {
+          const unsigned k32 = (unsigned)gb.key, q32 = k32 / (unsigned)n;
+          pr = (int)q32;
+          bj = (int)(k32 - q32 * (unsigned)n);
+        } else {
+          pr = (int)(gb.key / n);
+          bj = (int)(gb.key % n);
+        }
       } else {
         piv = -1.0;
       }

@@ -2194,12 +2194,9 @@ struct GemvJob {
 
 // warp per output row; row t belongs to job q with start[q] <= t < start[q + 1].
 // Each warp takes a contiguous chunk of rows: one binary search, then a walk.
-__global__ void __launch_bounds__(256) k_gemv2(const GemvJob *__restrict__ jobs, const int *__restrict__ start,
-                                               int njobs, int nrows) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  const int chunk = (nrows + nw - 1) / nw;
-  const int t0 = warp * chunk, t1 = min(nrows, t0 + chunk);
+// rows [t0, t1) of a GEMV batch, one warp: job q holds rows start[q] .. start[q+1]
+__device__ __forceinline__ void gemv_rows(const GemvJob *__restrict__ jobs, const int *__restrict__ start, int njobs,
+                                          int t0, int t1, int lane) {
   if (t0 >= t1) return;
   int q = 0;
   {
@@ -2244,6 +2241,16 @@ __global__ void __launch_bounds__(256) k_gemv2(const GemvJob *__restrict__ jobs,
       J.y[i] = v;
     }
   }
+}
+
+// warp per output row; each warp takes a contiguous chunk of rows
+__global__ void __launch_bounds__(256) k_gemv2(const GemvJob *__restrict__ jobs, const int *__restrict__ start,
+                                               int njobs, int nrows) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int chunk = (nrows + nw - 1) / nw;
+  const int t0 = warp * chunk;
+  gemv_rows(jobs, start, njobs, t0, min(nrows, t0 + chunk), lane);
 }
 
 // ---------------------------------------------------------------------------

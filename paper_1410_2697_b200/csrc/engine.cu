@@ -205,14 +205,23 @@ struct Ctx {
     int *col = nullptr;
   };
   std::vector<PatDev> pat_dev;
-  // per-tree apply structure: contribution CSR over global ids (post order)
+  // per-tree apply structure: contribution CSR over global ids (post order);
+  // shared with the apply plans of live factors, so eviction never frees it
+  // under a factor
   struct ApplySym {
     uint64_t uid = 0;
     int64_t tot = 0;
     std::vector<int64_t> off;  // contribution slot offset per post index (-1: none)
     long long *d_cptr = nullptr, *d_coff = nullptr, *d_fro = nullptr;
+    ~ApplySym() {
+      cudaFree(d_cptr);
+      cudaFree(d_coff);
+      cudaFree(d_fro);
+    }
   };
-  std::vector<ApplySym> apply_sym;
+  std::vector<std::shared_ptr<ApplySym>> apply_sym;
+  // the per-tree device caches keep the most recent trees only
+  static constexpr size_t SYM_CACHE_MAX = 8;
 };
 
 // ---------------------------------------------------------------------------
@@ -1399,6 +1408,10 @@ struct Factorizer {
         d_maps = m.second;
         return;
       }
+    if (ctx->map_dev.size() >= Ctx::SYM_CACHE_MAX) {  // least recently added tree
+      cudaFree(ctx->map_dev.front().second);
+      ctx->map_dev.erase(ctx->map_dev.begin());
+    }
     size_t bytes = sizeof(int) * std::max<size_t>(1, M.maps.size());
     CK(cudaMalloc(&d_maps, bytes));
     upload(ctx->s, d_maps, M.maps.data(), sizeof(int) * M.maps.size());
@@ -2386,6 +2399,12 @@ struct Factorizer {
       for (auto &q : ctx->pat_dev)
         if (q.gen == C.gen) pd = &q;
       if (!pd) {
+        if (ctx->pat_dev.size() >= Ctx::SYM_CACHE_MAX) {
+          cudaFree(ctx->pat_dev.front().ptr);
+          cudaFree(ctx->pat_dev.front().col);
+          cudaFree(ctx->pat_dev.front().src);
+          ctx->pat_dev.erase(ctx->pat_dev.begin());
+        }
         Ctx::PatDev q;
         q.gen = C.gen;
         CK(cudaMalloc(&q.ptr, sizeof(int64_t) * (n + 1)));
@@ -2510,6 +2529,10 @@ struct Factorizer {
         if (m.first == et->uid) all = m.second;
       int64_t tot = 0;
       if (!all) {
+        if (ctx->ids_dev.size() >= Ctx::SYM_CACHE_MAX) {
+          cudaFree(ctx->ids_dev.front().second);
+          ctx->ids_dev.erase(ctx->ids_dev.begin());
+        }
         for (auto &f : F->fronts) tot += f.nh;
         const std::vector<int64_t> &flat = et->mapcache.ids_flat;
         CK(cudaMalloc(&all, sizeof(int64_t) * std::max<int64_t>(1, tot)));
@@ -2720,6 +2743,7 @@ struct ApplyPlan {
   std::vector<std::pair<double *, int64_t>> xchg;
   double bytes = 0;  // algorithmic bytes per apply
   int64_t nodes = 0;
+  std::shared_ptr<Ctx::ApplySym> sym;  // contribution CSR the graph reads
 };
 
 // DenseBlock.as_factors / LowRankFactor.as_factors (hodlr.py:59-63) as a device view
@@ -2780,11 +2804,12 @@ static void build_apply(mfh_factor *F) {
   AP->xw = ar.d(std::max<int64_t>(1, n));
   AP->y = ar.d(std::max<int64_t>(1, n));
   // contribution CSR (symbolic: built once per tree, kept on the device per context)
-  Ctx::ApplySym *sym = nullptr;
+  std::shared_ptr<Ctx::ApplySym> sym;
   for (auto &a : ctx->apply_sym)
-    if (a.uid == F->et_uid) sym = &a;
+    if (a->uid == F->et_uid) sym = a;
   if (!sym) {
-    Ctx::ApplySym a;
+    auto ap = std::make_shared<Ctx::ApplySym>();
+    Ctx::ApplySym &a = *ap;
     a.uid = F->et_uid;
     a.off.assign(F->fronts.size(), -1);
     int64_t tt = 0;
@@ -2821,9 +2846,11 @@ static void build_apply(mfh_factor *F) {
       upload(ctx->s, a.d_coff, coff.data(), sizeof(int64_t) * tt);
       upload(ctx->s, a.d_fro, fro_all.data(), sizeof(int64_t) * tt);
     }
-    ctx->apply_sym.push_back(std::move(a));
-    sym = &ctx->apply_sym.back();
+    if (ctx->apply_sym.size() >= Ctx::SYM_CACHE_MAX) ctx->apply_sym.erase(ctx->apply_sym.begin());
+    ctx->apply_sym.push_back(ap);
+    sym = ap;
   }
+  AP->sym = sym;  // the plan's graph reads these arrays: keep them alive with the factor
   const std::vector<int64_t> &off = sym->off;
   const int64_t tot = sym->tot;
   long long *d_cptr = sym->d_cptr, *d_coff = sym->d_coff, *d_fro = sym->d_fro;
@@ -3193,11 +3220,7 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
     cudaFree(q.col);
     cudaFree(q.src);
   }
-  for (auto &a : ctx->c.apply_sym) {
-    cudaFree(a.d_cptr);
-    cudaFree(a.d_coff);
-    cudaFree(a.d_fro);
-  }
+  ctx->c.apply_sym.clear();
   cudaFreeHost(ctx->c.h_scal);
   cudaStreamSynchronize(ctx->c.side);
   cudaStreamSynchronize(ctx->c.side2);

@@ -156,3 +156,20 @@ def test_large_cores_against_oracle(oracle):
     q_gpu = np.linalg.norm(A._csc @ P.mf_solve(F, b) - b) / np.linalg.norm(b)
     q_ref = np.linalg.norm(A._csc @ oracle.solve(OF, b) - b) / np.linalg.norm(b)
     assert q_gpu <= 2.0 * q_ref + 1e-12, (q_gpu, q_ref)
+
+
+def test_symbolic_cache_eviction_keeps_live_factors_valid():
+    """More distinct trees than the per-context symbolic caches hold: early
+    factors' applies (which read the per-tree contribution CSR) still return
+    bitwise what they returned right after their factorization."""
+    import paper_1410_2697_b200 as P
+    from paper_1410_2697_b200 import problems as PR
+    kept = []
+    for k in range(10):
+        A, _ = PR.gen_poisson7(6 + k, 7, 5)
+        tree = P.build_elimination_tree(P.nested_dissection(P.adjacency_graph(A), 16), A)
+        F = P.mf_factorize(A, tree, P.ACCELERATED, P.MfParams(n_c=40, eps=1e-6, d=1, n_leaf=16))
+        b = np.random.default_rng(k).standard_normal(A.n_rows)
+        kept.append((F, b, P.mf_solve(F, b)))
+    for F, b, x0 in kept:
+        np.testing.assert_array_equal(P.mf_solve(F, b), x0)

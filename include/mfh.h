@@ -12,6 +12,11 @@
  * Each entry point cites the reference interface it replaces
  * (/root/reference/pkg/src/mfhodlr/<file>:<line>). The Python binding that a
  * maintainer adds on the reference side is shown in INTEGRATION.md.
+ *
+ * Threading: calls that use a context are serialized per context (a
+ * recursive lock: a GMRES host-callback operator may call back into the
+ * library on the same thread). Distinct contexts run independently.
+ * Lifetimes: an mfh_etree may be freed while factors built on it live on.
  */
 #ifndef MFH_H_
 #define MFH_H_

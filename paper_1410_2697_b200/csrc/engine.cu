@@ -21,6 +21,7 @@
 #include <memory>
 #include <numeric>
 #include <atomic>
+#include <mutex>
 #include <thread>
 
 #include "internal.h"
@@ -193,6 +194,9 @@ struct Ctx {
   double *d_part = nullptr;  // reduction partials
   double *d_scal = nullptr;  // small device scalars
   double *h_scal = nullptr;  // pinned host mirror for GMRES read-backs
+  // every C entry point holds this while it uses the context (recursive: a
+  // GMRES host-callback preconditioner may re-enter on the same thread)
+  std::recursive_mutex mu;
   int64_t launches = 0;      // launches of this library's kernels
   int64_t lib_calls = 0;     // cuBLAS DGEMM calls (plain large GEMMs)
   cublasHandle_t blas = nullptr;
@@ -3241,6 +3245,7 @@ extern "C" int mfh_ctx_info(mfh_ctx *ctx, void **stream, int64_t *launches) {
 }
 
 extern "C" int mfh_ctx_sync(mfh_ctx *ctx) {
+  std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
   MFH_TRY
   CK(cudaStreamSynchronize(ctx->c.s));
   MFH_CATCH
@@ -3249,6 +3254,7 @@ extern "C" int mfh_ctx_sync(mfh_ctx *ctx) {
 static int factorize_common(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const int64_t *indptr,
                             const int64_t *indices, const double *values, int mode, const mfh_params *params,
                             const mfh_shard_t *shard, mfh_factor **out) {
+  std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
   mfh_factor *F = nullptr;
   MFH_TRY
   if (mode != MFH_CONVENTIONAL && mode != MFH_ACCELERATED) throw value_error("unknown mode");
@@ -3363,6 +3369,7 @@ extern "C" int mfh_factor_blocks(const mfh_factor *f, int64_t *n_blocks, int64_t
 
 extern "C" void mfh_factor_free(mfh_factor *f) {
   if (!f) return;
+  std::lock_guard<std::recursive_mutex> lk_(f->ctx->mu);
   cudaStreamSynchronize(f->ctx->s);
   if (f->apply) {
     if (f->apply->exec) cudaGraphExecDestroy(f->apply->exec);
@@ -3375,6 +3382,7 @@ extern "C" void mfh_factor_free(mfh_factor *f) {
 }
 
 extern "C" int mfh_apply(mfh_factor *f, const double *b, double *x, int64_t nrhs, int on_device) {
+  std::lock_guard<std::recursive_mutex> lk_(f->ctx->mu);
   MFH_TRY
   Ctx *ctx = f->ctx;
   int64_t n = f->n;
@@ -3395,6 +3403,7 @@ extern "C" int mfh_apply(mfh_factor *f, const double *b, double *x, int64_t nrhs
 }
 
 extern "C" int mfh_apply_bench(mfh_factor *f, int64_t reps, double *ms_per_apply, double *bytes_per_apply) {
+  std::lock_guard<std::recursive_mutex> lk_(f->ctx->mu);
   MFH_TRY
   Ctx *ctx = f->ctx;
   if (!f->apply) build_apply(f);
@@ -3418,6 +3427,7 @@ extern "C" int mfh_apply_bench(mfh_factor *f, int64_t reps, double *ms_per_apply
 
 extern "C" int mfh_csr_create(mfh_ctx *ctx, int64_t n_rows, int64_t n_cols, const int64_t *indptr,
                               const int64_t *indices, const double *values, mfh_csr **out) {
+  std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
   MFH_TRY
   auto *A = new mfh_csr();
   A->ctx = &ctx->c;
@@ -3439,6 +3449,7 @@ extern "C" int mfh_csr_create(mfh_ctx *ctx, int64_t n_rows, int64_t n_cols, cons
 }
 
 extern "C" int mfh_dense_create(mfh_ctx *ctx, int64_t n, const double *values, mfh_csr **out) {
+  std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
   MFH_TRY
   auto *A = new mfh_csr();
   A->ctx = &ctx->c;
@@ -3453,6 +3464,7 @@ extern "C" int mfh_dense_create(mfh_ctx *ctx, int64_t n, const double *values, m
 
 extern "C" void mfh_csr_free(mfh_csr *A) {
   if (!A) return;
+  std::lock_guard<std::recursive_mutex> lk_(A->ctx->mu);
   cudaStreamSynchronize(A->ctx->s);
   cudaFree(A->ptr);
   cudaFree(A->col);
@@ -3461,6 +3473,7 @@ extern "C" void mfh_csr_free(mfh_csr *A) {
 }
 
 extern "C" int mfh_spmv(mfh_csr *A, const double *x, double *y, int on_device) {
+  std::lock_guard<std::recursive_mutex> lk_(A->ctx->mu);
   MFH_TRY
   Ctx *ctx = A->ctx;
   if (on_device) {
@@ -3709,12 +3722,14 @@ static int gmres_common(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const
 extern "C" int mfh_gmres_device(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const double *d_b,
                                 double *d_x, double tol, int64_t max_iter, int64_t restart, double *hist,
                                 int64_t *n_hist, int64_t *iterations, int *converged) {
+  std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
   return gmres_common(ctx, ops, n, d_b, d_x, tol, max_iter, restart, hist, n_hist, iterations, converged);
 }
 
 extern "C" int mfh_gmres(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const double *b, double *x,
                          double tol, int64_t max_iter, int64_t restart, double *hist, int64_t *n_hist,
                          int64_t *iterations, int *converged) {
+  std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
   cudaStream_t s = ctx->c.s;
   std::pair<char *, size_t> chunk{nullptr, 0};
   try {
@@ -3739,6 +3754,7 @@ extern "C" int mfh_full_pivot_lu_batched(mfh_ctx *ctx, int64_t batch, const int6
                                          const int64_t *ns, double *blocks, int64_t total, double eps,
                                          const int64_t *max_ranks, int64_t *row_perm, int64_t *col_perm,
                                          int64_t *ranks, double *ratios, int64_t *status, double *err) {
+  std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
   MFH_TRY
   Ctx *c = &ctx->c;
   if (batch == 0) return MFH_OK;
@@ -3824,6 +3840,7 @@ extern "C" int mfh_full_pivot_lu_batched(mfh_ctx *ctx, int64_t batch, const int6
 // ---------------------------------------------------------------------------
 extern "C" int mfh_test_inverse_batched(mfh_ctx *ctx, int64_t batch, const int64_t *offs, const int64_t *ns,
                                         double *blocks, int64_t total, int *singular) {
+  std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
   MFH_TRY
   Ctx *c = &ctx->c;
   if (batch == 0) return MFH_OK;

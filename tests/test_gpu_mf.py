@@ -173,3 +173,30 @@ def test_symbolic_cache_eviction_keeps_live_factors_valid():
         kept.append((F, b, P.mf_solve(F, b)))
     for F, b, x0 in kept:
         np.testing.assert_array_equal(P.mf_solve(F, b), x0)
+
+
+def test_concurrent_mf_solve_threads():
+    """concurrent mf_solve calls with distinct vectors are
+    permitted. Four threads on one factorization return exactly the
+    sequential results (calls are serialized per context)."""
+    import threading
+    import paper_1410_2697_b200 as P
+    from paper_1410_2697_b200 import problems as PR
+    A, _ = PR.gen_poisson7(12, 12, 12)
+    tree = P.build_elimination_tree(P.nested_dissection(P.adjacency_graph(A), 32), A)
+    F = P.mf_factorize(A, tree, P.ACCELERATED, P.MfParams(n_c=128, eps=1e-6, d=1, n_leaf=32))
+    bs = [np.random.default_rng(s).standard_normal(A.n_rows) for s in range(8)]
+    ref = [P.mf_solve(F, b) for b in bs]
+    out = [None] * len(bs)
+
+    def work(k):
+        for _ in range(5):
+            out[k] = P.mf_solve(F, bs[k])
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(len(bs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for x, r in zip(out, ref):
+        np.testing.assert_array_equal(x, r)

@@ -153,6 +153,11 @@ int mfh_factorize_sharded(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const int
                           const int64_t *indices, const double *values, int mode, const mfh_params *params,
                           const mfh_shard_t *shard, mfh_factor **out);
 int mfh_factor_stats(const mfh_factor *f, mfh_stats_t *out);
+/* Per-node solve operators of MfFactorization.node_factors (DenseNodeFactor /
+ * StructuredNodeFactor, multifrontal.py:160-216) on host vectors: op 0 =
+ * pp_solve (y = F_pp^{-1} x, n_pivot -> n_pivot), 1 = apply_pf (y = F_pf x,
+ * frontal -> n_pivot), 2 = apply_fp (y = F_fp x, n_pivot -> frontal). */
+int mfh_node_op(mfh_factor *f, int64_t node, int op, const double *x, double *y);
 int mfh_factor_records(const mfh_factor *f, mfh_record_t *out /* n_records */);
 int mfh_factor_timing(const mfh_factor *f, mfh_timing_t *out);
 /* integer parity record of every compressed block, in the reference's visiting

@@ -131,6 +131,7 @@ def _sig(lib):
         "mfh_etree_fetch": (C.c_int, [P, P, P, P, P, P, P]),
         "mfh_etree_free": (None, [P]),
         "mfh_factorize": (C.c_int, [P, P, I64, P, P, P, C.c_int, C.POINTER(mfh_params), PP]),
+        "mfh_node_op": (C.c_int, [P, I64, C.c_int, P, P]),
         "mfh_factorize_sharded": (C.c_int, [P, P, I64, P, P, P, C.c_int, C.POINTER(mfh_params),
                                             C.POINTER(mfh_shard_t), PP]),
         "mfh_factor_stats": (C.c_int, [P, C.POINTER(mfh_stats_t)]),

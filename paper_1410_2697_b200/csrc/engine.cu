@@ -3402,6 +3402,59 @@ extern "C" int mfh_apply(mfh_factor *f, const double *b, double *x, int64_t nrhs
   MFH_CATCH
 }
 
+// per-node solve operators (DenseNodeFactor / StructuredNodeFactor,
+// multifrontal.py:160-216): op 0 pp_solve (F_pp^{-1} v), 1 apply_pf (F_pf v),
+// 2 apply_fp (F_fp v); host vectors
+extern "C" int mfh_node_op(mfh_factor *f, int64_t node, int op, const double *x, double *y) {
+  std::lock_guard<std::recursive_mutex> lk_(f->ctx->mu);
+  MFH_TRY
+  using namespace mfh;
+  Ctx *ctx = f->ctx;
+  int q = -1;
+  for (size_t t = 0; t < f->post.size(); ++t)
+    if (f->post[t] == node) q = (int)t;
+  if (q < 0) throw value_error("node " + std::to_string(node) + " is not in the elimination tree");
+  const FrontH &fr = f->fronts[q];
+  if (fr.nh == 0) throw value_error("node " + std::to_string(node) + " has no node factor");
+  if (op < 0 || op > 2) throw value_error("node operator must be 0 (pp_solve), 1 (apply_pf) or 2 (apply_fp)");
+  const int npv = fr.npv, nf = fr.nf;
+  const int nin = op == 1 ? nf : npv, nout = op == 2 ? nf : npv;
+  if (nout == 0) return MFH_OK;
+  if (npv == 0) {  // merge node: F_fp is nf x 0
+    std::memset(y, 0, sizeof(double) * nout);
+    return MFH_OK;
+  }
+  double *dx = ctx->scratch.d(std::max(1, nin)), *dy = ctx->scratch.d(std::max(1, nout));
+  double *dt = ctx->scratch.d(std::max(1, std::max(npv, nf)));
+  if (nin) CK(cudaMemcpyAsync(dx, x, sizeof(double) * nin, cudaMemcpyHostToDevice, ctx->s));
+  Sink sk{ctx};
+  std::vector<GemvJob> g1, g2;
+  if (op == 0) {
+    g1.push_back(gemv(dy, nullptr, npv, fr.structured ? fr.Hinv : fr.Pinv, npv, npv, dx, 1.0));
+  } else if (!fr.structured) {
+    // the front buffer keeps F_pf (rows 0..npv, cols npv..) and F_fp (rows npv.., cols 0..npv)
+    if (op == 1)
+      g1.push_back(gemv(dy, nullptr, npv, fr.F + npv, fr.nh, nf, dx, 1.0));
+    else
+      g1.push_back(gemv(dy, nullptr, nf, fr.F + (int64_t)npv * fr.nh, fr.nh, npv, dx, 1.0));
+  } else {
+    FacView v = fac_view(f, f->blocks[op == 1 ? fr.pf : fr.fp]);
+    if (v.rank == 0) {
+      CK(cudaMemsetAsync(dy, 0, sizeof(double) * nout, ctx->s));
+    } else {
+      g1.push_back(gemv(dt, nullptr, v.rank, v.row, v.ldr, nin, dx, 1.0));  // row factor first
+      g2.push_back(gemv(dy, nullptr, nout, v.col, v.ldc, v.rank, dt, 1.0));
+    }
+  }
+  run_gemv(sk, g1);
+  run_gemv(sk, g2);
+  CK(cudaMemcpyAsync(y, dy, sizeof(double) * nout, cudaMemcpyDeviceToHost, ctx->s));
+  CK(cudaStreamSynchronize(ctx->s));
+  ctx->scratch.reset();
+  ctx->stage.rewind();
+  MFH_CATCH
+}
+
 extern "C" int mfh_apply_bench(mfh_factor *f, int64_t reps, double *ms_per_apply, double *bytes_per_apply) {
   std::lock_guard<std::recursive_mutex> lk_(f->ctx->mu);
   MFH_TRY

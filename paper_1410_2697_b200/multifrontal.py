@@ -77,6 +77,42 @@ class FactorStats:
                          f"{r.max_offdiag_rank},{r.stored_reals}\n")
 
 
+class NodeFactor:
+    """DenseNodeFactor / StructuredNodeFactor (multifrontal.py:160-216) of one
+    node: ids (pivots then frontal ids, permuted numbering), n_pivot, and the
+    solve operators evaluated on the device factor."""
+
+    def __init__(self, F, node_id, record):
+        self._F = F
+        self.node_id = node_id
+        node = F.tree.nodes[node_id]
+        self.ids = node.front_ids()
+        self.n_pivot = node.n_pivot
+        self.kind = record.path
+        self._record = record
+
+    def _op(self, op, v, n_out):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        y = np.empty(n_out)
+        _lib.check(_lib.lib().mfh_node_op(self._F._h, self.node_id, op, _lib.ptr(v), _lib.ptr(y)))
+        return y
+
+    def pp_solve(self, v):
+        return self._op(0, v, self.n_pivot)
+
+    def apply_pf(self, v):
+        return self._op(1, v, self.n_pivot)
+
+    def apply_fp(self, v):
+        return self._op(2, v, len(self.ids) - self.n_pivot)
+
+    def stored_reals(self):
+        return self._record.stored_reals
+
+    def max_offdiag_rank(self):
+        return self._record.max_offdiag_rank
+
+
 class MfFactorization:
     """Device-resident factorization (multifrontal.py:227-242)."""
 
@@ -95,10 +131,24 @@ class MfFactorization:
         _lib.check(L.mfh_factor_records(handle, _lib.ptr(table)))
         self.stats = FactorStats(st, table[:st.n_records])
         self._stored = int(st.stored_reals)
+        self._node_factors = None
         _lib.register(self)
 
     def stored_reals(self):
         return self._stored
+
+    @property
+    def node_factors(self):
+        """{node id: NodeFactor view, or None for empty fronts} (multifrontal.py:477-521).
+        The operators run on the device factor (mfh_node_op)."""
+        if self._node_factors is None:
+            by_node = {r.node_id: r for r in self.stats.records}
+            nf = {}
+            for p in self.tree.post_order:
+                r = by_node.get(p)
+                nf[p] = None if r is None or r.path == "empty" else NodeFactor(self, p, r)
+            self._node_factors = nf
+        return self._node_factors
 
     def timing(self):
         t = _lib.mfh_timing_t()

@@ -200,3 +200,41 @@ def test_concurrent_mf_solve_threads():
         t.join()
     for x, r in zip(out, ref):
         np.testing.assert_array_equal(x, r)
+
+
+def test_node_factors_reproduce_mf_solve():
+    """MfFactorization.node_factors (multifrontal.py:477-521): the reference's
+    own two-pass solve (multifrontal.py:533-560) written against the node
+    factor views reproduces the device mf_solve."""
+    import paper_1410_2697_b200 as P
+    from paper_1410_2697_b200 import problems as PR
+    A, _ = PR.gen_poisson7(10, 9, 8)
+    tree = P.build_elimination_tree(P.nested_dissection(P.adjacency_graph(A), 16), A)
+    F = P.mf_factorize(A, tree, P.ACCELERATED, P.MfParams(n_c=60, eps=1e-6, d=1, n_leaf=16))
+    nfs = F.node_factors
+    kinds = {nf.kind for nf in nfs.values() if nf is not None}
+    assert {"dense", "structured"} <= kinds
+    b = np.random.default_rng(3).standard_normal(A.n_rows)
+    bu, x = np.empty(F.n), np.zeros(F.n)
+    bu[F.permutation] = b
+    order = list(tree.post_order)
+    for p in order:
+        nf = nfs[p]
+        if nf is None or nf.n_pivot == 0:
+            continue
+        piv, fro = nf.ids[:nf.n_pivot], nf.ids[nf.n_pivot:]
+        if len(fro):
+            bu[fro] -= nf.apply_fp(nf.pp_solve(bu[piv]))
+    for p in reversed(order):
+        nf = nfs[p]
+        if nf is None or nf.n_pivot == 0:
+            continue
+        piv, fro = nf.ids[:nf.n_pivot], nf.ids[nf.n_pivot:]
+        rhs = bu[piv]
+        if len(fro):
+            rhs = rhs - nf.apply_pf(x[fro])
+        x[piv] = nf.pp_solve(rhs)
+    ref = x[F.permutation]
+    got = P.mf_solve(F, b)
+    assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref)
+    assert sum(nf.stored_reals() for nf in nfs.values() if nf is not None) == F.stored_reals()

@@ -296,7 +296,11 @@ __device__ __forceinline__ void rb_dot(double (&acc)[4][4], const double *__rest
     }
     __syncthreads();
     if (u0 + RB_K < K) fetch(u0 + RB_K);  // in flight during the FMAs
-    for (int k = 0; k < kc; ++k) {
+    // full, unrolled chunk: padded ranks are zeros in both operands and
+    // fma(0, 0, acc) == acc, so the result is unchanged and the loads pipeline
+    (void)kc;
+#pragma unroll
+    for (int k = 0; k < RB_K; ++k) {
       double w[4], x[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) w[a] = Ws[k][ty + 16 * a];

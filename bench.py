@@ -53,6 +53,8 @@ CONFIGS = {
     "c2_nc256": dict(desc="3D Poisson 48^3, reference defaults d=1 n_c=256", gen=("poisson7", (48, 48, 48)),
                      leaf=64, params=dict(n_c=256, eps=1e-5, d=1, n_leaf=64), restart=30, tol=1e-10,
                      rhs="normal"),
+    "t8": dict(desc="3D Poisson 8^3 (tests of the bench arms)", gen=("poisson7", (8, 8, 8)), leaf=16,
+               params=dict(n_c=64, eps=1e-5, d=1, n_leaf=16), restart=30, tol=1e-10, rhs="normal"),
     "p32": dict(desc="3D Poisson 32^3 (C2 params)", gen=("poisson7", (32, 32, 32)), leaf=64,
                 params=dict(n_c=256, eps=1e-5, d=1, n_leaf=64), restart=30, tol=1e-10, rhs="normal"),
     # larger BASELINE configs (parity at these sizes is through the size-independent

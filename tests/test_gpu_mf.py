@@ -238,3 +238,30 @@ def test_node_factors_reproduce_mf_solve():
     got = P.mf_solve(F, b)
     assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref)
     assert sum(nf.stored_reals() for nf in nfs.values() if nf is not None) == F.stored_reals()
+
+
+def test_singular_structured_leaf_matches_reference_message(oracle):
+    """hodlr.py:325-328: a singular leaf of a structured front's pivot HODLR
+    raises ValueError("singular pivot in leaf block [lo, hi)"). Zeroing every
+    entry of the root separator (pattern kept) makes the root's leaves zero;
+    the GPU raises the oracle's (reference's) exact message."""
+    import scipy.sparse as sp
+    import paper_1410_2697_b200 as P
+    A, _ = P.gen_poisson7(10, 10, 10)
+    tree = P.build_elimination_tree(P.nested_dissection(P.adjacency_graph(A), 16), A)
+    perm = np.asarray(tree.permutation)
+    iperm = np.empty_like(perm)
+    iperm[perm] = np.arange(len(perm))
+    sep = iperm[np.asarray(tree.nodes[tree.root].pivot_ids)]
+    Z = A._csc.tocoo()
+    Z.data[np.isin(Z.row, sep) | np.isin(Z.col, sep)] = 0.0
+    Zc = sp.csc_matrix((Z.data, (Z.row, Z.col)), shape=Z.shape)
+    kw = dict(n_c=60, eps=1e-6, d=1, n_leaf=16)
+    ip, ix = oracle.adjacency(A._csc)
+    ot = oracle.build_elimination_tree(oracle.nested_dissection(ip, ix, A.n_rows, 16), A._csc)
+    with pytest.raises(ValueError) as ref:
+        oracle.factorize(Zc, ot, "accelerated", **kw)
+    assert "singular pivot in leaf block" in str(ref.value)
+    with pytest.raises(ValueError) as got:
+        P.mf_factorize(P.SparseMatrix(Zc), tree, P.ACCELERATED, P.MfParams(**kw))
+    assert str(got.value) == str(ref.value)

@@ -172,6 +172,62 @@ struct Stage {
   }
 };
 
+// Chunked bump allocator for data that dies during the factorization (dense
+// front buffers: read by the parent's sampler, dead afterwards). Each chunk
+// keeps the latest release height of its allocations and goes back to the
+// pool once that height has been enqueued; every reader runs earlier on the
+// same stream, so reuse is stream-ordered after it.
+struct ReleaseArena {
+  struct Chunk {
+    char *p;
+    size_t cap, off;
+    int rh;
+  };
+  std::vector<Chunk> live;
+  ChunkPool *pool = nullptr;
+  size_t chunk = size_t(64) << 20;
+  size_t held = 0, peak = 0;
+  void *alloc(size_t bytes, int rh) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes == 0) bytes = 256;
+    if (!live.empty()) {
+      Chunk &c = live.back();
+      if (c.off + bytes <= c.cap) {
+        void *p = c.p + c.off;
+        c.off += bytes;
+        c.rh = std::max(c.rh, rh);
+        return p;
+      }
+    }
+    auto t = pool->take(std::max(chunk, bytes));
+    live.push_back(Chunk{t.first, t.second, bytes, rh});
+    held += t.second;
+    peak = std::max(peak, held);
+    return t.first;
+  }
+  double *d(size_t n, int rh) { return (double *)alloc(n * sizeof(double), rh); }
+  void release_upto(int h) {
+    for (size_t i = 0; i < live.size();) {
+      if (live[i].rh > h) {
+        ++i;
+      } else if (i + 1 == live.size()) {  // the open chunk: everything in it is dead, reuse it
+        live[i].off = 0;
+        live[i].rh = -1;
+        ++i;
+      } else {
+        pool->give({live[i].p, live[i].cap});
+        held -= live[i].cap;
+        live.erase(live.begin() + i);
+      }
+    }
+  }
+  void release_all() {
+    for (auto &c : live) pool->give({c.p, c.cap});
+    live.clear();
+    held = 0;
+  }
+};
+
 // host -> device upload ordered on the library stream (a plain cudaMemcpy from
 // pageable memory is only ordered on the legacy default stream)
 static void upload(cudaStream_t st, void *dst, const void *src, size_t bytes) {
@@ -1050,6 +1106,7 @@ struct FrontH {
   int *piv = nullptr;
   // apply operators (explicit inverse form, computed once at factor time)
   double *Pinv = nullptr, *Gfp = nullptr, *Gpf = nullptr;
+  double *Fpf = nullptr, *Ffp = nullptr;  // dense: F_pf / F_fp kept for node_factors (apply_pf / apply_fp)
   // structured: Hinv = (HODLR pivot block)^{-1}, Xp = Hinv col_pf, RH = row_fp Hinv
   double *Hinv = nullptr, *Xp = nullptr, *RH = nullptr;
   // structured path
@@ -1133,6 +1190,12 @@ struct Factorizer {
   const mfh_etree *et;
   mfh_params P;
   const mfh_shard_t *shard = nullptr;
+  ReleaseArena upd;            // dense front buffers (dead once the parent has sampled them)
+  std::vector<int> pidx_;      // post index of every node
+  int release_height(const FrontH &f) const {
+    int64_t par = et->parent[f.node];
+    return par < 0 ? (1 << 30) : F->fronts[pidx_[par]].height;
+  }
   bool accel;
   int64_t n;
   // permuted matrix on device
@@ -1365,6 +1428,7 @@ struct Factorizer {
   }
   ~Factorizer() {
     if (planner.joinable()) planner.join();
+    upd.release_all();  // (error paths synchronize the stream before the pool is reused)
   }
 
   void check_flags(int64_t upto_flags) {
@@ -1553,7 +1617,7 @@ struct Factorizer {
     // ------------------------------------------------ dense fronts: assemble
     for (int fi : D) {
       FrontH &f = F->fronts[fi];
-      f.F = F->arena.d((size_t)f.nh * f.nh);
+      f.F = upd.d((size_t)f.nh * f.nh, release_height(f));
       if (f.npv) f.piv = F->arena.i(f.npv);
       reqs.push_back(SReq{slot[fi], f.nh, f.nh, nullptr, nullptr, 0, 0, f.F, f.nh});
     }
@@ -1689,6 +1753,18 @@ struct Factorizer {
       run_inverse(s, inv);
       run_gemm(s, g1);
       run_gemm(s, g2);
+      {  // F_pf / F_fp outlive the front buffer (node_factors apply_pf / apply_fp)
+        std::vector<CopyJob> keep;
+        for (int fi : D) {
+          FrontH &f = F->fronts[fi];
+          if (!f.npv || !f.nf) continue;
+          f.Fpf = F->arena.d((size_t)f.npv * f.nf);
+          f.Ffp = F->arena.d((size_t)f.nf * f.npv);
+          keep.push_back(CopyJob{f.F + f.npv, f.Fpf, f.npv, f.nf, f.nh, f.nf, nullptr, nullptr});
+          keep.push_back(CopyJob{f.F + (int64_t)f.npv * f.nh, f.Ffp, f.nf, f.npv, f.nh, f.npv, nullptr, nullptr});
+        }
+        run_copy(s, keep);
+      }
       for (int fi : D) {
         FrontH &f = F->fronts[fi];
         if (f.nf) {
@@ -2441,7 +2517,9 @@ struct Factorizer {
     mark_t("permute+graph");
     // ---- fronts in post order
     int64_t nn = (int64_t)et->parent.size();
-    std::vector<int> pidx(nn, -1);
+    std::vector<int> &pidx = pidx_;
+    pidx.assign(nn, -1);
+    upd.pool = &ctx->pool;
     F->post = et->post;
     {  // front id lists (symbolic): flattened once per tree
       mfh_mapcache &M = et->mapcache;
@@ -2608,6 +2686,7 @@ struct Factorizer {
     for (int h = 0; h <= maxh; ++h) {
       if (byh[h].empty()) {
         if (!cut_at[h].empty()) exchange_updates(cut_at[h]);
+        upd.release_upto(h);
         continue;
       }
       while ((int)ctx->evpool.size() < 8 * (used + 1)) {
@@ -2637,6 +2716,7 @@ struct Factorizer {
         ctx->scratch.reset();
       }
       if (!cut_at[h].empty()) exchange_updates(cut_at[h]);
+      upd.release_upto(h);  // dense front buffers whose parents have sampled them
     }
     CK(cudaEventRecord(e_end, ctx->s));
     // the apply plan (host work) is built while the GPU finishes the last heights
@@ -2721,7 +2801,8 @@ struct Factorizer {
     F->stats.retained_reals = retained;
     F->stats.n_records = (int64_t)F->records.size();
     F->stats.stored_reals = retained;
-    F->stats.device_bytes_peak = (int64_t)F->arena.capacity() + (int64_t)ctx->scratch.capacity();
+    F->stats.device_bytes_peak =
+        (int64_t)F->arena.capacity() + (int64_t)upd.peak + (int64_t)ctx->scratch.capacity();
     // id views point into the tree's cache; nothing after the factorization
     // (the apply plan is already built) may read them
     for (auto &f : F->fronts) f.ids = IdsView{};
@@ -3434,9 +3515,9 @@ extern "C" int mfh_node_op(mfh_factor *f, int64_t node, int op, const double *x,
   } else if (!fr.structured) {
     // the front buffer keeps F_pf (rows 0..npv, cols npv..) and F_fp (rows npv.., cols 0..npv)
     if (op == 1)
-      g1.push_back(gemv(dy, nullptr, npv, fr.F + npv, fr.nh, nf, dx, 1.0));
+      g1.push_back(gemv(dy, nullptr, npv, fr.Fpf, nf, nf, dx, 1.0));
     else
-      g1.push_back(gemv(dy, nullptr, nf, fr.F + (int64_t)npv * fr.nh, fr.nh, npv, dx, 1.0));
+      g1.push_back(gemv(dy, nullptr, nf, fr.Ffp, npv, npv, dx, 1.0));
   } else {
     FacView v = fac_view(f, f->blocks[op == 1 ? fr.pf : fr.fp]);
     if (v.rank == 0) {

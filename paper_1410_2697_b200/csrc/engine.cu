@@ -242,6 +242,7 @@ struct Ctx {
   cudaStream_t side = nullptr;   // concurrent large-core cluster / cooperative kernels
   cudaStream_t side2 = nullptr;  // 8-CTA cluster cores, concurrently with the 16-CTA ones
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
+  cudaEvent_t gmres_ev[2] = {nullptr, nullptr};  // Hessenberg column read-backs (pipelined Arnoldi)
   int cluster_size = 16;
   ChunkPool pool;
   std::vector<cudaEvent_t> evpool;  // per-height phase events, reused
@@ -3279,6 +3280,7 @@ extern "C" int mfh_ctx_create(int device, mfh_ctx **out) {
   CK(cudaEventCreateWithFlags(&c->c.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->c.ev_join, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->c.ev_join2, cudaEventDisableTiming));
+  for (auto &e : c->c.gmres_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   c->c.stage.init(size_t(64) << 20);
   c->c.scratch.chunk = size_t(512) << 20;
   CK(cudaMalloc(&c->c.d_part, sizeof(double) * (RED_BLOCKS + 64)));
@@ -3312,6 +3314,7 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   cudaEventDestroy(ctx->c.ev_fork);
   cudaEventDestroy(ctx->c.ev_join);
   cudaEventDestroy(ctx->c.ev_join2);
+  for (auto &e : ctx->c.gmres_ev) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->c.side);
   cudaStreamDestroy(ctx->c.side2);
   cudaStreamDestroy(ctx->c.s);
@@ -3738,10 +3741,23 @@ struct GmresRun {
         k_scale_inv<<<g, 256, 0, ctx->s>>>(S + 1, r, V, n);
         int64_t j = 0;
         bool lucky_stop = false;
-        double *hcol = ctx->h_scal + 16;  // pinned: the copy is truly async
-        while (j < m) {
+        // Arnoldi steps are pipelined one deep: step j+1 (and the basis vector
+        // it starts from, V_{j+1} = w / H[j+1], a device value) is enqueued
+        // before the host waits for step j's Hessenberg column, so the GPU does
+        // not idle while the host applies the Givens rotations. A speculative
+        // step after the last one only writes scratch (w, z, H slots, V_{j+1})
+        // that the final combine never reads. It is skipped when the residual
+        // trend says step j is likely the last (it would delay the combine).
+        double *hbuf[2] = {ctx->h_scal + 16, ctx->h_scal + 2040};  // pinned: the copies are truly async
+        cudaEvent_t *hev = ctx->gmres_ev;
+        double qm = 0.0, qa = 0.0, qg = 0.0;
+        auto enqueue_step = [&](int64_t jj) {
           auto q0 = std::chrono::steady_clock::now();
-          M(V + j * n, z);
+          if (jj > 0) {
+            k_scale_inv<<<g, 256, 0, ctx->s>>>(S + 8 + jj, w, V + jj * n, n);
+            ctx->launches++;
+          }
+          M(V + jj * n, z);
           auto q1 = std::chrono::steady_clock::now();
           A(z, w);
           auto q2 = std::chrono::steady_clock::now();
@@ -3750,24 +3766,41 @@ struct GmresRun {
             const double *Vc = V;
             double *wc = w, *Hc = S + 8, *pc = ctx->d_part;
             long long nn = n;
-            int jj = (int)j;
-            void *args[6] = {(void *)&Vc, (void *)&wc, (void *)&nn, (void *)&jj, (void *)&Hc, (void *)&pc};
+            int jj32 = (int)jj;
+            void *args[6] = {(void *)&Vc, (void *)&wc, (void *)&nn, (void *)&jj32, (void *)&Hc, (void *)&pc};
             CK(cudaLaunchCooperativeKernel((const void *)k_mgs_coop, dim3(mgs_grid), dim3(256), args, 0, ctx->s));
             ctx->launches++;
           }
+          CK(cudaMemcpyAsync(hbuf[jj & 1], S + 8, sizeof(double) * (jj + 2), cudaMemcpyDeviceToHost, ctx->s));
+          CK(cudaEventRecord(hev[jj & 1], ctx->s));
           auto q3 = std::chrono::steady_clock::now();
-          CK(cudaMemcpyAsync(hcol, S + 8, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, ctx->s));
+          auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+          qm = ms(q0, q1);
+          qa = ms(q1, q2);
+          qg = ms(q2, q3);
+        };
+        // host callbacks see exactly the reference's calls: no speculation
+        const bool can_spec = ops->A != nullptr && (ops->M != nullptr || ops->M_cb == nullptr);
+        bool ahead = false;  // step j+1 already enqueued
+        enqueue_step(0);
+        while (j < m) {
+          // speculate on step j+1 unless step j is predicted to converge
+          bool spec = can_spec && j + 1 < m && its + 1 < max_iter;
+          if (spec && res.size() >= 2 && j >= 2) {
+            double r1 = res[res.size() - 1], r0 = res[res.size() - 2];
+            double rate = r0 > 0.0 ? r1 / r0 : 1.0;
+            if (r1 * rate <= 4.0 * tol) spec = false;
+          }
+          if (spec) enqueue_step(j + 1);
+          ahead = spec;
           auto q4 = std::chrono::steady_clock::now();
-          {
-            CK(cudaStreamSynchronize(ctx->s));
-            sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - q4).count();
-          }
-          if (trace) {
-            auto q5 = std::chrono::steady_clock::now();
-            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-            std::fprintf(stderr, "gmres it %lld: M %.3f A %.3f mgs %.3f cpy %.3f sync %.3f ms\n", (long long)its,
-                         ms(q0, q1), ms(q1, q2), ms(q2, q3), ms(q3, q4), ms(q4, q5));
-          }
+          CK(cudaEventSynchronize(hev[j & 1]));
+          sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - q4).count();
+          if (trace)
+            std::fprintf(stderr, "gmres it %lld: M %.3f A %.3f mgs %.3f sync %.3f ms%s\n", (long long)its, qm, qa, qg,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - q4).count(),
+                         spec ? " (next enqueued)" : "");
+          const double *hcol = hbuf[j & 1];
           double hn = hcol[j + 1];
           for (int64_t i = 0; i <= j; ++i) h(i, j) = hcol[i];
           if (!std::isfinite(hn)) throw value_error("GMRES residual is not finite");
@@ -3794,10 +3827,7 @@ struct GmresRun {
             lucky_stop = lucky;
             break;
           }
-          if (j < m) {
-            k_scale_inv<<<g, 256, 0, ctx->s>>>(S + 8 + j, w, V + j * n, n);
-            ctx->launches++;
-          }
+          if (j < m && !ahead) enqueue_step(j);
         }
         if (j > 0) {
           std::vector<double> y(j, 0.0);

@@ -2373,7 +2373,8 @@ __global__ void k_combine(const double *__restrict__ V, const double *__restrict
 // w -= H[i] V_i (numpy: w - (h * V_i), no FMA); finally H[j+1] = ||w||.
 // Each block owns a fixed slice of w, so the axpy of projection i-1 and the
 // dot of projection i run back to back on that slice; one grid barrier per
-// projection, and every block sums the partials in the same fixed order.
+// projection, and every block sums the partials in the same fixed order
+// (lane-strided, then an xor butterfly: a+b == b+a, so all lanes agree).
 __global__ void __launch_bounds__(256) k_mgs_coop(const double *__restrict__ V, double *__restrict__ w, long long n,
                                                   int j, double *__restrict__ H, double *__restrict__ part) {
   __shared__ double sh[33];
@@ -2398,10 +2399,11 @@ __global__ void __launch_bounds__(256) k_mgs_coop(const double *__restrict__ V, 
     s = block_sum(s, sh);
     if (threadIdx.x == 0) part[(i & 1) * G + b] = s;
     grid.sync();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // lane-strided partials + xor butterfly: every block gets the same bits
       double t = 0.0;
-      for (int q = 0; q < G; ++q) t += part[(i & 1) * G + q];
-      s_h = t;
+      for (int q = threadIdx.x; q < G; q += 32) t += __ldcg(part + (i & 1) * G + q);
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (threadIdx.x == 0) s_h = t;
     }
     __syncthreads();
     h = s_h;

@@ -2830,6 +2830,7 @@ struct ApplyPlan {
   double bytes = 0;  // algorithmic bytes per apply
   int64_t nodes = 0;
   std::shared_ptr<Ctx::ApplySym> sym;  // contribution CSR the graph reads
+  std::vector<std::function<void(cudaStream_t)>> ops;  // the captured ops (MFH_APPLY_OPS profile)
 };
 
 // DenseBlock.as_factors / LowRankFactor.as_factors (hodlr.py:59-63) as a device view
@@ -2863,11 +2864,39 @@ static void run_gemv(Sink &sk, const std::vector<GemvJob> &jobs) {
   for (size_t q = 0; q < jobs.size(); ++q) start[q + 1] = start[q] + std::max(0, jobs[q].m);
   const int nr = start.back(), nj = (int)jobs.size();
   if (nr == 0) return;
+  // one wave of warps, each a contiguous chunk of rows (a chunk of >= GV_R rows
+  // of one job keeps GV_R rows' loads in flight)
+  static int occ = 0;
+  if (!occ) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gemv2, 256, 0));
+    occ = std::max(occ, 1);
+  }
+  int grid = (int)std::min<int64_t>(cdiv((int64_t)nr * 32, 256), (int64_t)148 * occ);
+  const int nw = grid * 8, chunk = (int)cdiv(nr, nw);
+  std::vector<int> wq;
+  wq.reserve(cdiv(nr, chunk));
+  for (int t0 = 0, q = 0; t0 < nr; t0 += chunk) {
+    while (start[q + 1] <= t0) ++q;
+    wq.push_back(q);
+  }
+  static const bool gtrace = getenv("MFH_APPLY_TRACE") != nullptr;
+  if (gtrace) {
+    double el = 0, mx = 0;
+    int nk2 = 0;
+    for (auto &j : jobs) {
+      el += (double)j.m * (j.k1 + j.k2);
+      mx = std::max(mx, (double)(j.k1 + j.k2));
+      nk2 += j.k2 > 0;
+    }
+    fprintf(stderr, "[mfh gemv] jobs %5d rows %7d avg k %7.1f max k %6.0f with k2 %5d grid %4d chunk %3d\n", nj, nr,
+            el / std::max(1, nr), mx, nk2, grid, chunk);
+  }
   GemvJob *dj = sk.push(jobs);
   int *ds = sk.push(start);
-  int grid = (int)std::min<int64_t>(cdiv((int64_t)nr * 32, 256), 148 * 16);
+  int *dw = sk.push(wq);
+  (void)nj;
   sk.launch([=](cudaStream_t st) {
-    k_gemv2<<<grid, 256, 0, st>>>(dj, ds, nj, nr);
+    k_gemv2<<<grid, 256, 0, st>>>(dj, ds, dw, chunk, nr);
     check_launch();
   });
 }
@@ -3074,6 +3103,7 @@ static void build_apply(mfh_factor *F) {
   });
   bytes += 24.0 * n;
   // ---------------- upward: b_u[fro] -= apply_fp(pp_solve(b_u[piv]))
+  const bool atrace = getenv("MFH_APPLY_TRACE") != nullptr;
   auto upward = [&](std::vector<std::vector<int>> &byh) {
   for (int h = 0; h < (int)byh.size(); ++h) {
     if (sh && ex_up[h]) exchange_point(cbuf, cb_mask, cb_tmp, ncb);
@@ -3086,8 +3116,9 @@ static void build_apply(mfh_factor *F) {
     }
     long long *dgl = (long long *)sk.push(gl);
     int cnt = (int)gl.size();
-    sk.launch([=](cudaStream_t s) {
-      k_contrib_gather<<<(int)std::min<int64_t>(cdiv(cnt, 256), 1184), 256, 0, s>>>(dgl, cnt, d_cptr, d_coff,
+    // level 0 fronts have no pivot-carrying descendants: nothing to gather
+    if (h > 0) sk.launch([=](cudaStream_t s) {
+      k_contrib_gather<<<(int)std::min<int64_t>(cdiv((int64_t)cnt * 32, 256), 148 * 16), 256, 0, s>>>(dgl, cnt, d_cptr, d_coff,
                                                                                   cbuf, bu, nullptr);
       check_launch();
     });
@@ -3114,6 +3145,12 @@ static void build_apply(mfh_factor *F) {
       }
     }
     j0.insert(j0.end(), j1.begin(), j1.end());  // independent: one launch
+    if (atrace) {
+      int64_t mr = 0;
+      for (int q : fis) mr = std::max<int64_t>(mr, F->fronts[q].npv);
+      fprintf(stderr, "[mfh apply up %2d] fronts %5zu gather %7d jobs %5zu+%5zu max npv %5lld\n", h, fis.size(), cnt,
+              j0.size(), j2.size(), (long long)mr);
+    }
     run_gemv(sk, j0);
     run_gemv(sk, j2);
   }
@@ -3149,6 +3186,12 @@ static void build_apply(mfh_factor *F) {
         bytes += 8.0 * (double)f.npv * f.npv;
       }
     }
+    if (atrace) {
+      double lb = 0;
+      for (auto &j : jb) lb += 8.0 * (double)j.m * (j.k1 + j.k2);
+      for (auto &j : ja) lb += 8.0 * (double)j.m * (j.k1 + j.k2);
+      fprintf(stderr, "[mfh apply dn %2d] jobs %5zu+%5zu  %.2f MB\n", h, ja.size(), jb.size(), lb / 1e6);
+    }
     run_gemv(sk, ja);
     run_gemv(sk, jb);
   }
@@ -3182,6 +3225,7 @@ static void build_apply(mfh_factor *F) {
     }
   } else {
     capture(sk.ops, &AP->graph, &AP->exec);
+    if (getenv("MFH_APPLY_OPS")) AP->ops = sk.ops;
   }
   auto tb2 = std::chrono::steady_clock::now();
   F->timing.apply_build_ms = std::chrono::duration<double, std::milli>(tb1 - tb0).count();
@@ -3557,6 +3601,32 @@ extern "C" int mfh_apply_bench(mfh_factor *f, int64_t reps, double *ms_per_apply
   CK(cudaEventElapsedTime(&ms, e0, e1));
   *ms_per_apply = ms / std::max<int64_t>(1, reps);
   *bytes_per_apply = A->bytes;
+  if (!A->ops.empty()) {  // warm per-op device times, ops run eagerly with events between them
+    const size_t no = A->ops.size();
+    std::vector<cudaEvent_t> ev(no + 1);
+    for (auto &e : ev) CK(cudaEventCreate(&e));
+    std::vector<float> best(no, 1e30f);
+    for (int r = 0; r < 5; ++r) {
+      CK(cudaEventRecord(ev[0], ctx->s));
+      for (size_t k = 0; k < no; ++k) {
+        A->ops[k](ctx->s);
+        CK(cudaEventRecord(ev[k + 1], ctx->s));
+      }
+      CK(cudaEventSynchronize(ev[no]));
+      for (size_t k = 0; k < no; ++k) {
+        float t;
+        CK(cudaEventElapsedTime(&t, ev[k], ev[k + 1]));
+        best[k] = std::min(best[k], t);
+      }
+    }
+    double sum = 0;
+    for (size_t k = 0; k < no; ++k) {
+      fprintf(stderr, "[mfh apply op %3zu] %8.2f us\n", k, best[k] * 1e3);
+      sum += best[k] * 1e3;
+    }
+    fprintf(stderr, "[mfh apply ops] sum %.1f us over %zu ops\n", sum, no);
+    for (auto &e : ev) cudaEventDestroy(e);
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   MFH_CATCH

@@ -2198,63 +2198,160 @@ struct GemvJob {
 
 // warp per output row; row t belongs to job q with start[q] <= t < start[q + 1].
 // Each warp takes a contiguous chunk of rows: one binary search, then a walk.
-// rows [t0, t1) of a GEMV batch, one warp: job q holds rows start[q] .. start[q+1]
-__device__ __forceinline__ void gemv_rows(const GemvJob *__restrict__ jobs, const int *__restrict__ start, int njobs,
+// Every row is summed in the same order (lane-strided, k ascending per lane,
+// then a shuffle tree) however rows are grouped, so a row's bits do not depend
+// on the batch it is in (the sharded apply relies on that). Loads are issued
+// ahead of the FMAs (GV_U per lane per row, GV_R rows of one job at a time)
+// to keep enough bytes in flight for HBM.
+constexpr int GV_R = 4;
+template <int U, typename Ld>
+__device__ __forceinline__ void gv_run(const double *__restrict__ a, const Ld &xv, int k, int &kk, double &s) {
+  for (; kk + 32 * (U - 1) < k; kk += 32 * U) {
+    double v[U], w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      v[u] = a[kk + 32 * u];
+      w[u] = xv(kk + 32 * u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) s = fma(v[u], w[u], s);
+  }
+}
+// lane-strided dot, k ascending per lane (8 then 2 then 1 loads in flight)
+template <typename Ld>
+__device__ __forceinline__ double gv_dot_t(const double *__restrict__ a, const Ld &xv, int k, int lane) {
+  double s = 0.0;
+  int kk = lane;
+  gv_run<8>(a, xv, k, kk, s);
+  gv_run<2>(a, xv, k, kk, s);
+  gv_run<1>(a, xv, k, kk, s);
+  return s;
+}
+__device__ __forceinline__ double gv_dot(const double *__restrict__ a, const double *__restrict__ x, int k, int lane) {
+  return gv_dot_t(a, [x](int q) { return x[q]; }, k, lane);
+}
+__device__ __forceinline__ double gv_dot_idx(const double *__restrict__ a, const double *__restrict__ x,
+                                             const long long *__restrict__ idx, int k, int lane) {
+  return gv_dot_t(a, [x, idx](int q) { return x[idx[q]]; }, k, lane);
+}
+__device__ __forceinline__ double warp_sum_down(double s) {
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  return s;
+}
+__device__ __forceinline__ void gemv_rows(const GemvJob *__restrict__ jobs, const int *__restrict__ start, int q,
                                           int t0, int t1, int lane) {
   if (t0 >= t1) return;
-  int q = 0;
-  {
-    int lo = 0, hi = njobs - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (start[mid] <= t0)
-        lo = mid;
-      else
-        hi = mid - 1;
-    }
-    q = lo;
-  }
   int qend = start[q + 1];
-  for (int t = t0; t < t1; ++t) {
+  for (int t = t0; t < t1;) {
     while (t >= qend) {
       ++q;
       qend = start[q + 1];
     }
     const GemvJob &J = jobs[q];
     const int i = t - start[q];
-    double s1 = 0.0, s2 = 0.0;
-    if (J.k1) {
-      const double *a = J.A1 + (long long)i * J.lda1;
-      for (int k = lane; k < J.k1; k += 32) s1 = fma(a[k], J.x1[k], s1);
+    if (J.k2 == 0 && J.k1 <= 16) {
+      // short rows: W >= k1 lanes per row (W = 4, 8, 16 from k1 alone: one
+      // element per lane), 32 / W rows per pass, GV_R passes' loads in flight,
+      // xor tree inside the W lanes
+      const int W = J.k1 <= 4 ? 4 : (J.k1 <= 8 ? 8 : 16);
+      const int G = 32 / W, g = lane / W, l = lane & (W - 1);
+      const int tend = min(t1, qend), s0 = start[q];
+      for (int tb = t; tb < tend; tb += G * GV_R) {
+        double sr[GV_R];
+#pragma unroll
+        for (int r = 0; r < GV_R; ++r) {
+          const int tr = tb + g + G * r;
+          sr[r] = (tr < tend && l < J.k1) ? J.A1[(long long)(tr - s0) * J.lda1 + l] * J.x1[l] : 0.0;
+        }
+        for (int o = W >> 1; o > 0; o >>= 1)
+#pragma unroll
+          for (int r = 0; r < GV_R; ++r) sr[r] += __shfl_xor_sync(0xffffffffu, sr[r], o);
+        if (l == 0) {
+#pragma unroll
+          for (int r = 0; r < GV_R; ++r) {
+            const int tr = tb + g + G * r;
+            if (tr < tend) {
+              double v = J.y0 ? J.y0[tr - s0] : 0.0;
+              J.y[tr - s0] = v + J.a1 * sr[r];
+            }
+          }
+        }
+      }
+      t = tend;
+      continue;
     }
+    if (t + GV_R <= min(t1, qend)) {
+      // GV_R rows of one job: the same per-row order as below, loads of all rows in flight
+      double s1[GV_R], s2[GV_R];
+#pragma unroll
+      for (int r = 0; r < GV_R; ++r) s1[r] = s2[r] = 0.0;
+      if (J.k1) {
+        const double *a = J.A1 + (long long)i * J.lda1;
+        for (int kk = lane; kk < J.k1; kk += 32) {
+          const double xv = J.x1[kk];
+          double v[GV_R];
+#pragma unroll
+          for (int r = 0; r < GV_R; ++r) v[r] = a[(long long)r * J.lda1 + kk];
+#pragma unroll
+          for (int r = 0; r < GV_R; ++r) s1[r] = fma(v[r], xv, s1[r]);
+        }
+      }
+      if (J.k2) {
+        const double *a = J.A2 + (long long)i * J.lda2;
+        for (int kk = lane; kk < J.k2; kk += 32) {
+          const double xv = J.idx2 ? J.x2[J.idx2[kk]] : J.x2[kk];
+          double v[GV_R];
+#pragma unroll
+          for (int r = 0; r < GV_R; ++r) v[r] = a[(long long)r * J.lda2 + kk];
+#pragma unroll
+          for (int r = 0; r < GV_R; ++r) s2[r] = fma(v[r], xv, s2[r]);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < GV_R; ++r) {
+          s1[r] += __shfl_down_sync(0xffffffffu, s1[r], o);
+          s2[r] += __shfl_down_sync(0xffffffffu, s2[r], o);
+        }
+      if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < GV_R; ++r) {
+          double v = J.y0 ? J.y0[i + r] : 0.0;
+          if (J.k1) v += J.a1 * s1[r];
+          if (J.k2) v += J.a2 * s2[r];
+          J.y[i + r] = v;
+        }
+      }
+      t += GV_R;
+      continue;
+    }
+    double s1 = 0.0, s2 = 0.0;
+    if (J.k1) s1 = gv_dot(J.A1 + (long long)i * J.lda1, J.x1, J.k1, lane);
     if (J.k2) {
       const double *a = J.A2 + (long long)i * J.lda2;
-      if (J.idx2)
-        for (int k = lane; k < J.k2; k += 32) s2 = fma(a[k], J.x2[J.idx2[k]], s2);
-      else
-        for (int k = lane; k < J.k2; k += 32) s2 = fma(a[k], J.x2[k], s2);
+      s2 = J.idx2 ? gv_dot_idx(a, J.x2, J.idx2, J.k2, lane) : gv_dot(a, J.x2, J.k2, lane);
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      s1 += __shfl_down_sync(0xffffffffu, s1, o);
-      s2 += __shfl_down_sync(0xffffffffu, s2, o);
-    }
+    s1 = warp_sum_down(s1);
+    s2 = warp_sum_down(s2);
     if (lane == 0) {
       double v = J.y0 ? J.y0[i] : 0.0;
       if (J.k1) v += J.a1 * s1;
       if (J.k2) v += J.a2 * s2;
       J.y[i] = v;
     }
+    ++t;
   }
 }
 
-// warp per output row; each warp takes a contiguous chunk of rows
+// warp per output row; each warp takes a contiguous chunk of rows, starting in
+// job wq[warp] (computed on the host: no search through start[] on the device)
 __global__ void __launch_bounds__(256) k_gemv2(const GemvJob *__restrict__ jobs, const int *__restrict__ start,
-                                               int njobs, int nrows) {
+                                               const int *__restrict__ wq, int chunk, int nrows) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  const int chunk = (nrows + nw - 1) / nw;
   const int t0 = warp * chunk;
-  gemv_rows(jobs, start, njobs, t0, min(nrows, t0 + chunk), lane);
+  if (t0 >= nrows) return;
+  gemv_rows(jobs, start, wq[warp], t0, min(nrows, t0 + chunk), lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -2273,16 +2370,28 @@ __global__ void k_gather_perm(const double *__restrict__ x, const long long *__r
     out[i] = x[perm[i]];
 }
 // b_u[g] -= contributions in post order (multifrontal.py:549 applied lazily)
-__global__ void k_contrib_gather(const long long *__restrict__ gl, int cnt,
-                                 const long long *__restrict__ cptr,
-                                 const long long *__restrict__ coff, const double *__restrict__ cbuf,
-                                 double *__restrict__ bu, double *__restrict__ y) {
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
-    long long g = gl[t];
+// Warp per pivot: the lanes load 32 contributions at once, then the sum runs
+// in list order through shuffles (the same bits as a sequential loop).
+__global__ void __launch_bounds__(256) k_contrib_gather(const long long *__restrict__ gl, int cnt,
+                                                        const long long *__restrict__ cptr,
+                                                        const long long *__restrict__ coff,
+                                                        const double *__restrict__ cbuf, double *__restrict__ bu,
+                                                        double *__restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < cnt; t += nw) {
+    const long long g = gl[t];
+    const long long b = cptr[g], e = cptr[g + 1];
     double acc = bu[g];
-    for (long long q = cptr[g]; q < cptr[g + 1]; ++q) acc = acc - cbuf[coff[q]];
-    bu[g] = acc;
-    if (y) y[g] = acc;
+    for (long long q0 = b; q0 < e; q0 += 32) {
+      const double v = q0 + lane < e ? cbuf[coff[q0 + lane]] : 0.0;
+      const int m = (int)(e - q0 < 32 ? e - q0 : 32);
+      for (int r = 0; r < m; ++r) acc = acc - __shfl_sync(0xffffffffu, v, r);
+    }
+    if (lane == 0) {
+      bu[g] = acc;
+      if (y) y[g] = acc;
+    }
   }
 }
 // xf[off + j] = x[fro[j]] for all (off, fro) of a height

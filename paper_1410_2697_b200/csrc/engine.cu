@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -311,6 +312,8 @@ struct Sink {
     }
     auto hd = ctx->stage.take(bytes);
     std::memcpy(hd.first, src, bytes);
+    static const bool zc = getenv("MFH_ZEROCOPY") != nullptr;
+    if (zc) return hd.first;  // experiment: kernels read the pinned ring directly (UVA)
     CK(cudaMemcpyAsync(hd.second, hd.first, bytes, cudaMemcpyHostToDevice, ctx->s));
     return hd.second;
   }
@@ -329,6 +332,27 @@ struct Sink {
     std::memcpy(hd.first, v.data(), bytes);
     CK(cudaMemcpyAsync(dst, hd.first, bytes, cudaMemcpyHostToDevice, ctx->s));
     return (T *)dst;
+  }
+  // several arrays in one staged copy into scratch (valid to the end of the
+  // height): one H2D transfer instead of one per array (each costs GPU time)
+  std::vector<char *> push_keep_many(const std::vector<std::pair<const void *, size_t>> &parts) {
+    size_t tot = 0;
+    for (auto &p : parts) tot += (p.second + 255) & ~size_t(255);
+    std::vector<char *> out;
+    if (tot == 0) {
+      out.assign(parts.size(), nullptr);
+      return out;
+    }
+    char *dst = record ? (char *)persist->alloc(tot) : (char *)ctx->scratch.alloc(tot);
+    auto hd = ctx->stage.take(tot);
+    size_t o = 0;
+    for (auto &p : parts) {
+      if (p.second) std::memcpy(hd.first + o, p.first, p.second);
+      out.push_back(p.second ? dst + o : nullptr);
+      o += (p.second + 255) & ~size_t(255);
+    }
+    CK(cudaMemcpyAsync(dst, hd.first, tot, cudaMemcpyHostToDevice, ctx->s));
+    return out;
   }
   double *scratch_d(size_t n) { return record ? persist->d(n) : ctx->scratch.d(n); }
   // async host -> device copy into caller-owned device memory through the
@@ -1193,8 +1217,10 @@ struct Factorizer {
   const mfh_shard_t *shard = nullptr;
   ReleaseArena upd;            // dense front buffers (dead once the parent has sampled them)
   std::vector<int> pidx_;      // post index of every node
+  std::vector<char> alias_;    // dense merge node whose update is its only child's, bit for bit
   int release_height(const FrontH &f) const {
     int64_t par = et->parent[f.node];
+    while (par >= 0 && alias_[pidx_[par]]) par = et->parent[par];
     return par < 0 ? (1 << 30) : F->fronts[pidx_[par]].height;
   }
   bool accel;
@@ -1536,8 +1562,23 @@ struct Factorizer {
   std::vector<int> slot_rw;
   static constexpr int RB_MIN_RANK = 16;
 
-  void run_sample(Sink &s, const std::vector<SReq> &reqs, DFront *dF, DChild *dC) {
-    if (reqs.empty()) return;
+  // hfr / hch given: the front descriptors are pushed here, in the same H2D
+  // transfer as the requests and tiles, and dF / dC are set
+  void run_sample(Sink &s, const std::vector<SReq> &reqs, DFront *&dF, DChild *&dC,
+                  const std::vector<DFront> *hfr = nullptr, const std::vector<DChild> *hch = nullptr) {
+    auto push_fronts = [&](std::vector<std::pair<const void *, size_t>> extra) {
+      std::vector<std::pair<const void *, size_t>> parts{{hfr->data(), hfr->size() * sizeof(DFront)},
+                                                        {hch->data(), hch->size() * sizeof(DChild)}};
+      parts.insert(parts.end(), extra.begin(), extra.end());
+      auto p = s.push_keep_many(parts);
+      dF = (DFront *)p[0];
+      dC = (DChild *)p[1];
+      return p;
+    };
+    if (reqs.empty()) {
+      if (hfr) push_fronts({});
+      return;
+    }
     std::vector<int2> tiles, tiles_rb;
     for (int q = 0; q < (int)reqs.size(); ++q) {
       const bool rb = reqs[q].front < (int)slot_rw.size() && slot_rw[reqs[q].front] >= RB_MIN_RANK;
@@ -1546,22 +1587,40 @@ struct Factorizer {
       for (int64_t t = 0; t < nt; ++t) (rb ? tiles_rb : tiles).push_back(make_int2(q, (int)t));
       F->timing.sample_entries += (double)reqs[q].nr * reqs[q].nc;
     }
-    if (tiles.empty() && tiles_rb.empty()) return;
-    SReq *dr = s.push(reqs);
+    if (tiles.empty() && tiles_rb.empty()) {
+      if (hfr) push_fronts({});
+      return;
+    }
+    SReq *dr;
+    int2 *dt_plain = nullptr, *dt_rb = nullptr;
+    if (hfr) {
+      auto p = push_fronts({{reqs.data(), reqs.size() * sizeof(SReq)},
+                            {tiles.data(), tiles.size() * sizeof(int2)},
+                            {tiles_rb.data(), tiles_rb.size() * sizeof(int2)}});
+      dr = (SReq *)p[2];
+      dt_plain = (int2 *)p[3];
+      dt_rb = (int2 *)p[4];
+    } else {
+      dr = s.push(reqs);
+      if (!tiles.empty()) dt_plain = s.push(tiles);
+      if (!tiles_rb.empty()) dt_rb = s.push(tiles_rb);
+    }
+    DFront *fF = dF;
+    DChild *fC = dC;
     long long *pp = d_ap_ptr;
     int *pc = d_ap_col;
     double *pv = d_ap_val;
     if (!tiles.empty()) {
-      int2 *dt = s.push(tiles);
+      int2 *dt = dt_plain;
       int nt = (int)tiles.size();
       int grid = std::min(nt, 148 * 32);
       s.launch([=](cudaStream_t st) {
-        k_sample<<<grid, dim3(SAMPLE_TC, SAMPLE_TR), 0, st>>>(dr, dt, nt, dF, dC, pp, pc, pv);
+        k_sample<<<grid, dim3(SAMPLE_TC, SAMPLE_TR), 0, st>>>(dr, dt, nt, fF, fC, pp, pc, pv);
         check_launch();
       });
     }
     if (!tiles_rb.empty()) {
-      int2 *dt = s.push(tiles_rb);
+      int2 *dt = dt_rb;
       int nt = (int)tiles_rb.size();
       int grid = std::min(nt, 148 * 8);
       static bool attr = false;
@@ -1570,7 +1629,7 @@ struct Factorizer {
         attr = true;
       }
       s.launch([=](cudaStream_t st) {
-        k_sample_rb<<<grid, 256, RB_DYN, st>>>(dr, dt, nt, dF, dC, pp, pc, pv);
+        k_sample_rb<<<grid, 256, RB_DYN, st>>>(dr, dt, nt, fF, fC, pp, pc, pv);
         check_launch();
       });
     }
@@ -1611,8 +1670,8 @@ struct Factorizer {
     std::vector<DChild> dch;
     std::vector<int> slot;
     build_fronts_dev(s, fis, dfr, dch, slot);
-    DFront *dF = s.push_keep(dfr);
-    DChild *dC = dch.empty() ? nullptr : s.push_keep(dch);
+    DFront *dF = nullptr;  // pushed with the first sampling batch below
+    DChild *dC = nullptr;
 
     std::vector<SReq> reqs;
     // ------------------------------------------------ dense fronts: assemble
@@ -1723,7 +1782,7 @@ struct Factorizer {
     }
 
     cudaEventRecord(ev[0], ctx->s);
-    run_sample(s, reqs, dF, dC);
+    run_sample(s, reqs, dF, dC, &dfr, &dch);
     cudaEventRecord(ev[1], ctx->s);
 
     // ------------------------------------------------ dense fronts: eliminate
@@ -1778,10 +1837,9 @@ struct Factorizer {
         f.upd_reals = (int64_t)f.nf * f.nf;
       }
     };
-    if (S.empty()) {
+    if (S.empty()) {  // dense-only height: three events (each record costs GPU time)
       dense_elim();
       cudaEventRecord(ev[2], ctx->s);
-      for (int q = 3; q < 8; ++q) cudaEventRecord(ev[q], ctx->s);
       return;
     }
     cudaEventRecord(ev[2], ctx->s);
@@ -2634,10 +2692,28 @@ struct Factorizer {
     flag_cap = max_flags + 16;
     d_flags = F->arena.i(max_flags + 16);
     CK(cudaMemset(d_flags, 0, sizeof(int) * (max_flags + 16)));
+    // Dense merge nodes (no pivots) with one updating child over the same
+    // frontal ids: the front is 0 + the child's update, i.e. that update bit
+    // for bit, so it aliases the child's buffer instead of being assembled
+    // (the long single-child merge chains of nested dissection).
+    alias_.assign(F->fronts.size(), 0);
+    std::vector<std::vector<int>> alias_at(maxh + 1);
+    if (!F->sharded)
+      for (size_t q = 0; q < F->fronts.size(); ++q) {
+        FrontH &f = F->fronts[q];
+        if (f.structured || f.nh == 0 || f.npv != 0 || f.kids.size() != 1) continue;
+        FrontH &c = F->fronts[f.kids[0]];
+        if (c.structured || c.nf != f.nf) continue;
+        bool same = true;
+        for (int j = 0; j < f.nf && same; ++j) same = c.ids[c.npv + j] == f.ids[j];
+        if (!same) continue;
+        alias_[q] = 1;
+        alias_at[f.height].push_back((int)q);
+      }
     // ---- heights
     std::vector<std::vector<int>> byh(maxh + 1);
     for (size_t q = 0; q < F->fronts.size(); ++q)
-      if (F->fronts[q].nh > 0 && active(q)) byh[F->fronts[q].height].push_back((int)q);
+      if (F->fronts[q].nh > 0 && active(q) && !alias_[q]) byh[F->fronts[q].height].push_back((int)q);
     // sharded: heights after which a child -> parent update crosses ranks (the
     // same on every rank: computed from the global tree)
     std::vector<std::vector<int>> cut_at(maxh + 1);
@@ -2684,7 +2760,19 @@ struct Factorizer {
     // scratch memory; per-height phase events are evaluated at the end.
     int used = 0;
     std::vector<int> height_of_use, struct_of_use;
+    std::vector<std::array<int, 4>> first_of_use;  // npv, nf, kids of the first front; aliased fronts
+    std::vector<double> host_us_of_use;
     for (int h = 0; h <= maxh; ++h) {
+      for (int q : alias_at[h]) {  // the child was enqueued at a lower height
+        FrontH &f = F->fronts[q];
+        const FrontH &c = F->fronts[f.kids[0]];
+        f.upd = 0;
+        f.upd_dense = c.upd_dense;
+        f.upd_ld = c.upd_ld;
+        f.front_reals = (int64_t)f.nh * f.nh;
+        f.factor_reals = 0;
+        f.upd_reals = (int64_t)f.nf * f.nf;
+      }
       if (byh[h].empty()) {
         if (!cut_at[h].empty()) exchange_updates(cut_at[h]);
         upd.release_upto(h);
@@ -2702,9 +2790,13 @@ struct Factorizer {
         int ns = 0;
         for (int fi : byh[h]) ns += F->fronts[fi].structured;
         struct_of_use.push_back(ns);
+        const FrontH &f0 = F->fronts[byh[h][0]];
+        first_of_use.push_back({f0.npv, f0.nf, (int)f0.kids.size(), (int)alias_at[h].size()});
       }
-      for (int q = 0; q < 8; ++q) CK(cudaEventRecord(ev[q], ctx->s));
+      // process_height records ev[0..2] (dense-only heights) or ev[0..7]
+      auto th0 = std::chrono::steady_clock::now();
       process_height(byh[h], ev);
+      host_us_of_use.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count());
       // heights run ahead of the host: the only waits are the rank readback
       // inside structured heights and scratch recycling
       if (ctx->scratch.in_use > (size_t(4) << 30)) {
@@ -2734,18 +2826,22 @@ struct Factorizer {
     const bool htrace = getenv("MFH_HEIGHT_TRACE") != nullptr;
     for (int u = 0; u < used; ++u) {
       cudaEvent_t *ev = ctx->evpool.data() + 8 * u;
+      const bool donly = struct_of_use[u] == 0;
       if (htrace) {
-        float a[7], gap = 0.f;
-        for (int q = 0; q < 7; ++q) CK(cudaEventElapsedTime(&a[q], ev[q], ev[q + 1]));
-        if (u > 0) CK(cudaEventElapsedTime(&gap, ctx->evpool[8 * (u - 1) + 7], ev[0]));
-        fprintf(stderr, "[mfh height %3d] fronts %4zu struct %2d | gap %7.3f sample %7.3f dense %7.3f plu %7.3f - %7.3f skel %7.3f hodlr %7.3f elim %7.3f ms\n",
-                height_of_use[u], byh[height_of_use[u]].size(), struct_of_use[u], gap, a[0], a[1], a[2], a[3], a[4], a[5], a[6]);
+        float a[7] = {0, 0, 0, 0, 0, 0, 0}, gap = 0.f;
+        for (int q = 0; q < (donly ? 2 : 7); ++q) CK(cudaEventElapsedTime(&a[q], ev[q], ev[q + 1]));
+        if (u > 0)
+          CK(cudaEventElapsedTime(&gap, ctx->evpool[8 * (u - 1) + (struct_of_use[u - 1] ? 7 : 2)], ev[0]));
+        fprintf(stderr, "[mfh height %3d] fronts %4zu struct %2d | gap %7.3f sample %7.3f dense %7.3f plu %7.3f - %7.3f skel %7.3f hodlr %7.3f elim %7.3f ms | first npv %d nf %d kids %d, aliased %d | host %.1f us\n",
+                height_of_use[u], byh[height_of_use[u]].size(), struct_of_use[u], gap, a[0], a[1], a[2], a[3], a[4], a[5], a[6],
+                first_of_use[u][0], first_of_use[u][1], first_of_use[u][2], first_of_use[u][3], host_us_of_use[u]);
       }
       float ms;
       CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
       tsum[0] += ms;
       CK(cudaEventElapsedTime(&ms, ev[1], ev[2]));
       tsum[4] += ms;
+      if (donly) continue;
       CK(cudaEventElapsedTime(&ms, ev[2], ev[3]));
       tsum[1] += ms;
       CK(cudaEventElapsedTime(&ms, ev[4], ev[5]));

@@ -312,8 +312,6 @@ struct Sink {
     }
     auto hd = ctx->stage.take(bytes);
     std::memcpy(hd.first, src, bytes);
-    static const bool zc = getenv("MFH_ZEROCOPY") != nullptr;
-    if (zc) return hd.first;  // experiment: kernels read the pinned ring directly (UVA)
     CK(cudaMemcpyAsync(hd.second, hd.first, bytes, cudaMemcpyHostToDevice, ctx->s));
     return hd.second;
   }
@@ -1870,6 +1868,10 @@ struct Factorizer {
         b.errpiv = od[1];
         b.errprev = od[2];
         if (b.status && first_err < 0) first_err = (int)q;
+        static const bool ptrace = getenv("MFH_PLU_TRACE") != nullptr;
+        if (ptrace)
+          fprintf(stderr, "[mfh plu] height %d block %d core %d x %d rank %d\n", F->fronts[b.fi].height, sblocks[q], nI,
+                  nJ, b.rank);
         b.rows_phys = out[3] == 1;
         b.rowperm.assign(p, p + b.rank);
         b.colperm.assign(p + 4 * nI, p + 4 * nI + b.rank);

@@ -705,6 +705,36 @@ __device__ __forceinline__ void plu_out(const PluJob &J, const PluState &st) {
   J.outd[2] = st.errprev;
 }
 
+// One trailing-update row of the complete-pivot LU: a[j] -= l * p[j] for the
+// lane's columns j = j0 + lane + 32 t, t ascending, with f(v, j) called in
+// that order (the caller's strict '>' running max keeps the first max). Four
+// columns' loads are issued before their arithmetic: the same per-element
+// operations, more bytes in flight per lane.
+template <class F>
+__device__ __forceinline__ void plu_row_update(double *__restrict__ row, const double *__restrict__ prow, double l,
+                                               int j0, int n, int lane, F &&f) {
+  int j = j0 + lane;
+  for (; j + 96 < n; j += 128) {
+    const double a0 = row[j], a1 = row[j + 32], a2 = row[j + 64], a3 = row[j + 96];
+    const double p0 = prow[j], p1 = prow[j + 32], p2 = prow[j + 64], p3 = prow[j + 96];
+    const double v0 = __dsub_rn(a0, __dmul_rn(l, p0)), v1 = __dsub_rn(a1, __dmul_rn(l, p1));
+    const double v2 = __dsub_rn(a2, __dmul_rn(l, p2)), v3 = __dsub_rn(a3, __dmul_rn(l, p3));
+    row[j] = v0;
+    row[j + 32] = v1;
+    row[j + 64] = v2;
+    row[j + 96] = v3;
+    f(v0, j);
+    f(v1, j + 32);
+    f(v2, j + 64);
+    f(v3, j + 96);
+  }
+  for (; j < n; j += 32) {
+    const double v = __dsub_rn(row[j], __dmul_rn(l, prow[j]));
+    row[j] = v;
+    f(v, j);
+  }
+}
+
 template <bool SMEM_CORE, int NT = 512>
 __global__ void __launch_bounds__(NT) k_plu_cta2(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
                                                  double eps) {
@@ -809,16 +839,14 @@ __global__ void __launch_bounds__(NT) k_plu_cta2(const PluJob *__restrict__ jobs
       const double l = row[k] / akk;
       __syncwarp();
       if (lane == 0) row[k] = l;
-      for (int j = k + 1 + lane; j < n; j += 32) {
-        double v = __dsub_rn(row[j], __dmul_rn(l, prow[j]));
-        row[j] = v;
-        double av = fabs(v);
+      plu_row_update(row, prow, l, k + 1, n, lane, [&](double v, int j) {
+        const double av = fabs(v);
         if (av > bv) {
           bv = av;
           bi_ = i;
           bj_ = j;
         }
-      }
+      });
     }
     bk = bi_ >= 0 ? (long long)bi_ * n + bj_ : 0x7fffffffffffffffLL;
   }
@@ -1048,15 +1076,13 @@ __device__ __forceinline__ void plu_dist_body(const PluJob &J, double eps, int G
       // with the thread's best happens once per row
       double rbv = -1.0;
       int rj = 0x7fffffff;
-      for (int j = k + 1 + lane; j < n; j += 32) {
-        double v = __dsub_rn(row[j], __dmul_rn(l, prow[j]));
-        row[j] = v;
-        double av = fabs(v);
+      plu_row_update(row, prow, l, k + 1, n, lane, [&](double v, int j) {
+        const double av = fabs(v);
         if (av > rbv) {
           rbv = av;
           rj = j;
         }
-      }
+      });
       if (rj != 0x7fffffff && better(rbv, rk + rj, bv, bk)) {
         bv = rbv;
         bk = rk + rj;
@@ -1268,16 +1294,14 @@ __global__ void __launch_bounds__(NT) k_plu_cluster3(const PluJob *__restrict__ 
       if (pos == k) pos = pr;
       double rbv = -1.0, rsv = 0.0;
       int rj = 0x7fffffff;
-      for (int j = k + 1 + lane; j < n; j += 32) {
-        double v = __dsub_rn(row[j], __dmul_rn(l, prow[j]));
-        row[j] = v;
-        double av = fabs(v);
+      plu_row_update(row, prow, l, k + 1, n, lane, [&](double v, int j) {
+        const double av = fabs(v);
         if (av > rbv) {
           rbv = av;
           rsv = v;
           rj = j;
         }
-      }
+      });
       const long long key = (long long)pos * n + rj;
       if (rj != 0x7fffffff && better(rbv, key, best.v, best.key)) best = PluCand{rbv, rsv, key, li};
     }
@@ -1496,16 +1520,14 @@ __global__ void __launch_bounds__(512) k_plu_groups3(const PluJob *__restrict__ 
         if (pos == k) pos = pr;
         double rbv = -1.0, rsv = 0.0;
         int rj = 0x7fffffff;
-        for (int j = k + 1 + lane; j < n; j += 32) {
-          double v = __dsub_rn(row[j], __dmul_rn(l, prow[j]));
-          row[j] = v;
-          double av = fabs(v);
+        plu_row_update(row, prow, l, k + 1, n, lane, [&](double v, int j) {
+          const double av = fabs(v);
           if (av > rbv) {
             rbv = av;
             rsv = v;
             rj = j;
           }
-        }
+        });
         const long long key = (long long)pos * n + rj;
         if (rj != 0x7fffffff && better(rbv, key, best.v, best.key)) best = PluCand{rbv, rsv, key, li};
       }

@@ -596,15 +596,19 @@ struct PluState {
 constexpr int GRID_MAX = 160;  // CTAs per cooperative group (>= SM count)
 
 struct GridScratch {
-  MaxLoc *best;   // 2 x G
-  double *cand;   // 2 x G x nmax
+  MaxLoc *best;    // 2 x G
+  double *cand;    // 2 x G x nmax
   int nmax;
-  unsigned *bar;  // group barrier (count, generation); nullptr = whole-grid sync
+  unsigned *bar;   // group barrier arrival counter (zeroed before the launch); nullptr = whole-grid sync
+  unsigned epoch;  // barriers this CTA has passed (thread 0's copy)
 };
 
 // Barrier over the G CTAs of one group of a cooperative launch (all CTAs are
-// co-resident): the same arrive / spin-on-generation protocol as a grid sync,
-// so several groups run independent cores concurrently.
+// co-resident). The counter only grows: barrier e is complete once it reaches
+// G * e, so an arrival is one acq_rel atomic and the wait an acquire-load
+// spin (the release publishes the CTA's candidate slot and row, ordered
+// after the block's writes by the __syncthreads; the acquire makes the other
+// CTAs' visible before the closing __syncthreads).
 __device__ __forceinline__ void group_barrier(GridScratch *gs, int G) {
   if (!gs->bar) {
     cg::this_grid().sync();
@@ -612,18 +616,12 @@ __device__ __forceinline__ void group_barrier(GridScratch *gs, int G) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned *vgen = gs->bar + 1;
-    unsigned g0 = *vgen;
-    __threadfence();
-    if (atomicAdd(gs->bar, 1u) == (unsigned)G - 1) {
-      gs->bar[0] = 0;
-      __threadfence();
-      atomicAdd(gs->bar + 1, 1u);
-    } else {
-      while (*vgen == g0) {
-      }
-    }
-    __threadfence();
+    const unsigned target = (unsigned)G * ++gs->epoch;
+    unsigned v;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(gs->bar) : "memory");
+    unsigned cur = v + 1;
+    while ((int)(cur - target) < 0)  // not the last arriver: wait for the rest
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(gs->bar) : "memory");
   }
   __syncthreads();
 }

@@ -859,6 +859,19 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
       throw runtime_error("complete-pivot core too large for the shared-memory bookkeeping");
     }
   }
+  // Cores of a class start in launch order as SMs free up (only ~7 16-CTA
+  // clusters are co-resident): longest first (steps bounded by min(m, n) and
+  // kmax, work per step by m n), so the tail is short.
+  auto lpt = [&](std::vector<int> &v) {
+    auto cost = [&](int q) {
+      const PluJob &j = jobs[q];
+      return (double)std::min(std::min(j.m, j.n), j.kmax) * ((double)j.m * j.n);
+    };
+    std::stable_sort(v.begin(), v.end(), [&](int a, int b) { return cost(a) > cost(b); });
+  };
+  lpt(cl8);
+  lpt(cl16);
+  for (auto &v : small) lpt(v);
   PluJob *dj = sk.push(jobs);
   // every descriptor the side stream reads is pushed (on the main stream)
   // BEFORE the fork event, so the side-stream kernels see them

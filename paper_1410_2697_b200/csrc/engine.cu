@@ -252,6 +252,16 @@ struct Ctx {
   double *d_part = nullptr;  // reduction partials
   double *d_scal = nullptr;  // small device scalars
   double *h_scal = nullptr;  // pinned host mirror for GMRES read-backs
+  char *h_rb = nullptr;      // pinned landing area for the per-height rank read-back
+  size_t h_rb_cap = 0;
+  char *readback(size_t bytes) {
+    if (bytes > h_rb_cap) {
+      if (h_rb) CK(cudaFreeHost(h_rb));
+      h_rb_cap = std::max(bytes, std::max(h_rb_cap * 2, size_t(1) << 20));
+      CK(cudaMallocHost(&h_rb, h_rb_cap));
+    }
+    return h_rb;
+  }
   // every C entry point holds this while it uses the context (recursive: a
   // GMRES host-callback preconditioner may re-enter on the same thread)
   std::recursive_mutex mu;
@@ -1469,10 +1479,13 @@ struct Factorizer {
     upd.release_all();  // (error paths synchronize the stream before the pool is reused)
   }
 
-  void check_flags(int64_t upto_flags) {
+  void check_flags(int64_t upto_flags, const int *hflags = nullptr) {
     if (nflags == 0) return;
     std::vector<int> h(nflags);
-    CK(cudaMemcpy(h.data(), d_flags, sizeof(int) * nflags, cudaMemcpyDeviceToHost));
+    if (hflags)
+      std::memcpy(h.data(), hflags, sizeof(int) * nflags);
+    else
+      CK(cudaMemcpy(h.data(), d_flags, sizeof(int) * nflags, cudaMemcpyDeviceToHost));
     int best = -1;
     for (int q = 0; q < nflags; ++q)
       if (h[q] && (best < 0 || flag_order[q] < flag_order[best])) best = q;
@@ -1861,12 +1874,18 @@ struct Factorizer {
     cudaEventRecord(ev[3], ctx->s);
     // read ranks, status and pivot sequences: one D2H pair for the height
     {
-      std::vector<int> hi(itot);
-      std::vector<double> hd(dtot);
-      CK(cudaMemcpyAsync(hi.data(), pint_all, sizeof(int) * itot, cudaMemcpyDeviceToHost, ctx->s));
-      CK(cudaMemcpyAsync(hd.data(), pdbl_all, sizeof(double) * dtot, cudaMemcpyDeviceToHost, ctx->s));
+      // one pinned landing area: ranks / pivots, their doubles and the error
+      // flags arrive with the same sync (no pageable copies, no second trip)
+      const size_t bi_ = sizeof(int) * itot, bd_ = sizeof(double) * dtot, bf_ = sizeof(int) * nflags;
+      const size_t oD = (bi_ + 15) & ~size_t(15), oF = oD + ((bd_ + 15) & ~size_t(15));
+      char *hb = ctx->readback(oF + bf_);
+      CK(cudaMemcpyAsync(hb, pint_all, bi_, cudaMemcpyDeviceToHost, ctx->s));
+      CK(cudaMemcpyAsync(hb + oD, pdbl_all, bd_, cudaMemcpyDeviceToHost, ctx->s));
+      if (nflags) CK(cudaMemcpyAsync(hb + oF, d_flags, bf_, cudaMemcpyDeviceToHost, ctx->s));
       s.sync_reset();
-      check_flags(0);
+      std::vector<int> hi((const int *)hb, (const int *)hb + itot);
+      std::vector<double> hd((const double *)(hb + oD), (const double *)(hb + oD) + dtot);
+      check_flags(0, (const int *)(hb + oF));
       int first_err = -1;
       for (size_t q = 0; q < sblocks.size(); ++q) {
         BlockH &b = F->blocks[sblocks[q]];
@@ -3464,6 +3483,7 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   }
   ctx->c.apply_sym.clear();
   cudaFreeHost(ctx->c.h_scal);
+  if (ctx->c.h_rb) cudaFreeHost(ctx->c.h_rb);
   cudaStreamSynchronize(ctx->c.side);
   cudaStreamSynchronize(ctx->c.side2);
   cudaEventDestroy(ctx->c.ev_fork);

@@ -1686,7 +1686,11 @@ struct Factorizer {
   }
 
   // ---- one height ----
+  // host clock when each phase event was enqueued (MFH_HEIGHT_TRACE)
+  std::chrono::steady_clock::time_point hts[8];
   void process_height(const std::vector<int> &fis, cudaEvent_t *ev) {
+    const auto h_t0 = std::chrono::steady_clock::now();
+    for (auto &t : hts) t = h_t0;
     Sink s{ctx};
     std::vector<int> D, S;
     for (int fi : fis) (F->fronts[fi].structured ? S : D).push_back(fi);
@@ -1806,8 +1810,10 @@ struct Factorizer {
     }
 
     cudaEventRecord(ev[0], ctx->s);
+    hts[0] = std::chrono::steady_clock::now();
     run_sample(s, reqs, dF, dC, &dfr, &dch);
     cudaEventRecord(ev[1], ctx->s);
+    hts[1] = std::chrono::steady_clock::now();
 
     // ------------------------------------------------ dense fronts: eliminate
     // (at heights with structured fronts this runs on the main stream inside
@@ -1867,11 +1873,13 @@ struct Factorizer {
       return;
     }
     cudaEventRecord(ev[2], ctx->s);
+    hts[2] = std::chrono::steady_clock::now();
 
     // ------------------------------------------------ structured: pivot LU
     run_copy(s, core_copies);
     run_plu(s, plu, P.eps, dense_elim);
     cudaEventRecord(ev[3], ctx->s);
+    hts[3] = std::chrono::steady_clock::now();
     // read ranks, status and pivot sequences: one D2H pair for the height
     {
       // one pinned landing area: ranks / pivots, their doubles and the error
@@ -1963,6 +1971,7 @@ struct Factorizer {
       F->stats.n_blocks++;
     }
     cudaEventRecord(ev[4], ctx->s);
+    hts[4] = std::chrono::steady_clock::now();
     if (!lux.empty()) {
       LuExtractJob *dj = s.push(lux);
       int64_t mx = 0;
@@ -1997,6 +2006,7 @@ struct Factorizer {
     }
     run_sample(s, dreq, dF, dC);
     cudaEventRecord(ev[5], ctx->s);
+    hts[5] = std::chrono::steady_clock::now();
 
     // ------------------------------------------------ device HNode tables (one upload)
     {
@@ -2244,6 +2254,7 @@ struct Factorizer {
       }
     }
     cudaEventRecord(ev[6], ctx->s);
+    hts[6] = std::chrono::steady_clock::now();
 
     // ------------------------------------------------ eliminate_hodlr (W, V)  (multifrontal.py:411-456)
     {
@@ -2298,6 +2309,14 @@ struct Factorizer {
       run_gemm(s, g2);
     }
     cudaEventRecord(ev[7], ctx->s);
+    hts[7] = std::chrono::steady_clock::now();
+    static const bool htr = getenv("MFH_HEIGHT_TRACE") != nullptr;
+    if (htr) {
+      auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+      fprintf(stderr, "[mfh host height %d] enqueue-at (us from entry): ev0 %.0f ev1 %.0f ev2 %.0f ev3 %.0f ev4 %.0f ev5 %.0f ev6 %.0f ev7 %.0f\n",
+              F->fronts[fis[0]].height, us(h_t0, hts[0]), us(h_t0, hts[1]), us(h_t0, hts[2]), us(h_t0, hts[3]),
+              us(h_t0, hts[4]), us(h_t0, hts[5]), us(h_t0, hts[6]), us(h_t0, hts[7]));
+    }
 
     // ------------------------------------------------ accounting (host)
     for (int fi : S) {

@@ -1944,21 +1944,25 @@ struct InvJob {  // in-place inverse of an n x n block (n <= INV_SMALL)
 // Register-tiled Gauss-Jordan inverse for n <= NW*8 (<= 32*CPL), same pivot
 // rule as LAPACK getrf (first max |a| in the column): warp w owns rows [8w, 8w+8), lane l owns columns
 // {l, l+32, ...}; each thread keeps its 8 x CPL tile in registers. Per step:
-// every warp publishes its rows' column-k values and its best candidate; all
-// threads reduce the candidates redundantly (no broadcast barrier); the owners
-// of rows k and p publish them; every thread updates its tile. Two barriers
-// per step, no shared-memory matrix, no integer division.
+// every warp publishes its rows' column-k values, its best candidate and that
+// candidate's row (and the owner of row k publishes row k); after the step's
+// only barrier all threads reduce the candidates redundantly, take the
+// winner's published row as the pivot row and update their tiles. No
+// shared-memory matrix, no integer division.
 template <int NW, int CPL>
 __global__ void __launch_bounds__(NW * 32) k_inv_reg(const InvJob *__restrict__ jobs) {
   constexpr int NR = NW * 8, NC = 32 * CPL;
   static_assert(NW <= 32, "candidate reduction is one warp wide");
-  __shared__ double colkb[2][NR];  // parity double buffer: written before step k+1's first barrier
-  __shared__ double rowK[NC], rowP[NC];
-  __shared__ double cv[NW];
-  __shared__ int ci[NW];
+  // parity double buffers: step k writes buffer k & 1 before its only barrier;
+  // a warp cannot reach step k + 2's writes before every warp has passed step
+  // k + 1's barrier, i.e. finished reading step k's buffers
+  __shared__ double colkb[2][NR];
+  __shared__ double candrow[2][NW][NC];  // each warp's candidate row (its best row in column k)
+  __shared__ double rowKb[2][NC];
+  __shared__ double cv[2][NW];
+  __shared__ int ci[2][NW];
   __shared__ int piv[NR], idx[NC];
   __shared__ int bad;
-  __shared__ double s_rinv;
   const InvJob J = jobs[blockIdx.x];
   const int n = J.n, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double a[8][CPL];
@@ -1981,28 +1985,40 @@ __global__ void __launch_bounds__(NW * 32) k_inv_reg(const InvJob *__restrict__ 
         stop = true;
         break;
       }
-      double *colk = colkb[k & 1];
+      const int par = k & 1;
+      double *colk = colkb[par];
+      // this warp's candidate: rows ascend, so a strict '>' keeps the first maximum
+      double wbv = -1.0;
+      int wbi = 0x7fffffff;
       if (lane == kl) {
-        // rows ascend, so a strict '>' keeps the first maximum
-        double bv = -1.0;
-        int bi = 0x7fffffff;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int i = warp * 8 + r;
           const double v = a[r][kc];
           colk[i] = v;
-          if (i >= k && i < n && fabs(v) > bv) {
-            bv = fabs(v);
-            bi = i;
+          if (i >= k && i < n && fabs(v) > wbv) {
+            wbv = fabs(v);
+            wbi = i;
           }
         }
-        cv[warp] = bv;
-        ci[warp] = bi;
+        cv[par][warp] = wbv;
+        ci[par][warp] = wbi;
       }
-      __syncthreads();
+      wbi = __shfl_sync(0xffffffffu, wbi, kl);
+      // publish the candidate row and row k (the swap partner) with the candidates
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        if (warp * 8 + r == wbi)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) candrow[par][warp][lane + 32 * c] = a[r][c];
+        if (warp * 8 + r == k)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) rowKb[par][lane + 32 * c] = a[r][c];
+      }
+      __syncthreads();  // the only barrier of the step
       // every warp reduces the NW candidates (ties -> lower row)
-      double bv = lane < NW ? cv[lane] : -1.0;
-      int bi = lane < NW ? ci[lane] : 0x7fffffff;
+      double bv = lane < NW ? cv[par][lane] : -1.0;
+      int bi = lane < NW ? ci[par][lane] : 0x7fffffff;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
         if (off >= NW) continue;
@@ -2022,23 +2038,8 @@ __global__ void __launch_bounds__(NW * 32) k_inv_reg(const InvJob *__restrict__ 
         break;
       }
       if (threadIdx.x == 0) piv[k] = p;
-      if (warp == (k >> 3)) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-          if (warp * 8 + r == k)
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) rowK[lane + 32 * c] = a[r][c];
-      }
-      if (warp == (p >> 3)) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-          if (warp * 8 + r == p)
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) rowP[lane + 32 * c] = a[r][c];
-        if (lane == 0) s_rinv = 1.0 / pv;  // one division per step
-      }
-      __syncthreads();
-      const double rinv = s_rinv;
+      const double rinv = 1.0 / pv;  // every thread: the same bits as one division broadcast
+      const double *rowP = bi == 0x7fffffff ? rowKb[par] : candrow[par][p >> 3];
       double pj[CPL];
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
@@ -2051,7 +2052,7 @@ __global__ void __launch_bounds__(NW * 32) k_inv_reg(const InvJob *__restrict__ 
         for (int r = 0; r < 8; ++r)
           if (warp * 8 + r == p)
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) a[r][c] = rowK[lane + 32 * c];
+            for (int c = 0; c < CPL; ++c) a[r][c] = rowKb[par][lane + 32 * c];
       }
       if (lane == kl) {
 #pragma unroll

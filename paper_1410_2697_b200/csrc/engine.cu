@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <memory>
 #include <numeric>
 #include <atomic>
@@ -1205,6 +1206,7 @@ struct mfh_factor {
   mfh_timing_t timing{};
   // apply
   std::unique_ptr<mfh::ApplyPlan> apply;
+  std::map<int, std::unique_ptr<mfh::ApplyPlan>> apply_nv;  // several right-hand sides per replay (built on demand)
   // subtree-sharded factor: owner rank per post index, mine = owner == rank
   bool sharded = false;
   std::vector<int> owner;
@@ -2980,6 +2982,13 @@ struct ApplyPlan {
   int64_t nodes = 0;
   std::shared_ptr<Ctx::ApplySym> sym;  // contribution CSR the graph reads
   std::vector<std::function<void(cudaStream_t)>> ops;  // the captured ops (MFH_APPLY_OPS profile)
+  int nv = 1;                                          // right-hand sides per replay
+  ~ApplyPlan() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (auto e : seg_exec) cudaGraphExecDestroy(e);
+    for (auto g : seg_graph) cudaGraphDestroy(g);
+  }
 };
 
 // DenseBlock.as_factors / LowRankFactor.as_factors (hodlr.py:59-63) as a device view
@@ -3007,7 +3016,13 @@ static FacView fac_view(const mfh_factor *F, const BlockH &b) {
   return v;
 }
 
-static void run_gemv(Sink &sk, const std::vector<GemvJob> &jobs) {
+template <int NV>
+static void launch_gemv_mv(cudaStream_t st, int grid, const GemvJob *dj, const int *ds, const int *dw, int chunk,
+                           int nr) {
+  k_gemv_mv<NV><<<grid, 256, 0, st>>>(dj, ds, dw, chunk, nr);
+}
+// nv right-hand sides (1..8): vector v of a job at pointer + v * its stride
+static void run_gemv(Sink &sk, const std::vector<GemvJob> &jobs, int nv = 1) {
   if (jobs.empty()) return;
   std::vector<int> start(jobs.size() + 1, 0);
   for (size_t q = 0; q < jobs.size(); ++q) start[q + 1] = start[q] + std::max(0, jobs[q].m);
@@ -3045,7 +3060,17 @@ static void run_gemv(Sink &sk, const std::vector<GemvJob> &jobs) {
   int *dw = sk.push(wq);
   (void)nj;
   sk.launch([=](cudaStream_t st) {
-    k_gemv2<<<grid, 256, 0, st>>>(dj, ds, dw, chunk, nr);
+    switch (nv) {
+      case 1: k_gemv2<<<grid, 256, 0, st>>>(dj, ds, dw, chunk, nr); break;
+      case 2: launch_gemv_mv<2>(st, grid, dj, ds, dw, chunk, nr); break;
+      case 3: launch_gemv_mv<3>(st, grid, dj, ds, dw, chunk, nr); break;
+      case 4: launch_gemv_mv<4>(st, grid, dj, ds, dw, chunk, nr); break;
+      case 5: launch_gemv_mv<5>(st, grid, dj, ds, dw, chunk, nr); break;
+      case 6: launch_gemv_mv<6>(st, grid, dj, ds, dw, chunk, nr); break;
+      case 7: launch_gemv_mv<7>(st, grid, dj, ds, dw, chunk, nr); break;
+      case 8: launch_gemv_mv<8>(st, grid, dj, ds, dw, chunk, nr); break;
+      default: throw runtime_error("run_gemv: 1..8 right-hand sides per launch");
+    }
     check_launch();
   });
 }
@@ -3053,24 +3078,41 @@ static void run_gemv(Sink &sk, const std::vector<GemvJob> &jobs) {
 static GemvJob gemv(double *y, const double *y0, int m, const double *A1, int lda1, int k1, const double *x1,
                     double a1, const double *A2 = nullptr, int lda2 = 0, int k2 = 0, const double *x2 = nullptr,
                     const long long *idx2 = nullptr, double a2 = 0.0) {
-  return GemvJob{y, y0, m, A1, lda1, k1, x1, a1, A2, lda2, k2, x2, idx2, a2};
+  return GemvJob{y, y0, m, A1, lda1, k1, x1, a1, A2, lda2, k2, x2, idx2, a2, 0, 0, 0, 0};
+}
+// the same job with the vector strides of a several-right-hand-side plan
+static GemvJob strided(GemvJob j, long long ys, long long x1s, long long x2s) {
+  j.ys = ys;
+  j.x1s = x1s;
+  j.x2s = x2s;
+  return j;
 }
 
-static void build_apply(mfh_factor *F) {
+// The two-pass apply for nv right-hand sides (1..8; several only for an
+// unsharded factor): every per-vector buffer is [nv][len], one graph.
+static std::unique_ptr<ApplyPlan> make_apply(mfh_factor *F, int nv);
+static void build_apply(mfh_factor *F) { F->apply = make_apply(F, 1); }
+static std::unique_ptr<ApplyPlan> make_apply(mfh_factor *F, int nv) {
   auto tb0 = std::chrono::steady_clock::now();
   Ctx *ctx = F->ctx;
   auto AP = std::make_unique<ApplyPlan>();
   int64_t n = F->n;
   Arena &ar = F->arena;
-  AP->d_b = ar.d(std::max<int64_t>(1, n));
-  AP->d_x = ar.d(std::max<int64_t>(1, n));
-  AP->bu = ar.d(std::max<int64_t>(1, n));
-  AP->xw = ar.d(std::max<int64_t>(1, n));
-  AP->y = ar.d(std::max<int64_t>(1, n));
+  if (nv < 1 || nv > 8 || (nv > 1 && F->sharded)) throw runtime_error("apply plan: 1..8 right-hand sides (one when sharded)");
+  AP->nv = nv;
+  const int64_t nn1 = std::max<int64_t>(1, n);
+  AP->d_b = ar.d(nv * nn1);
+  AP->d_x = ar.d(nv * nn1);
+  AP->bu = ar.d(nv * nn1);
+  AP->xw = ar.d(nv * nn1);
+  AP->y = ar.d(nn1);
   // contribution CSR (symbolic: built once per tree, kept on the device per context)
   std::shared_ptr<Ctx::ApplySym> sym;
+  // a several-vector plan is built after the factorization, when the front id
+  // views are gone: it shares the one-vector plan's contribution CSR
+  if (nv > 1) sym = F->apply->sym;
   for (auto &a : ctx->apply_sym)
-    if (a->uid == F->et_uid) sym = a;
+    if (!sym && a->uid == F->et_uid) sym = a;
   if (!sym) {
     auto ap = std::make_shared<Ctx::ApplySym>();
     Ctx::ApplySym &a = *ap;
@@ -3118,7 +3160,8 @@ static void build_apply(mfh_factor *F) {
   const std::vector<int64_t> &off = sym->off;
   const int64_t tot = sym->tot;
   long long *d_cptr = sym->d_cptr, *d_coff = sym->d_coff, *d_fro = sym->d_fro;
-  AP->cbuf = ar.d(std::max<int64_t>(1, tot));
+  AP->cbuf = ar.d(nv * std::max<int64_t>(1, tot));
+  const long long cst = std::max<int64_t>(1, tot), nst = nn1;  // vector strides of cbuf and bu / xw
 
   Sink sk{ctx};
   sk.record = true;
@@ -3247,7 +3290,7 @@ static void build_apply(mfh_factor *F) {
     });
   };
   sk.launch([=](cudaStream_t s) {
-    k_scatter_perm<<<grid_n, 256, 0, s>>>(db, perm, bu, n);
+    k_scatter_perm<<<dim3(grid_n, nv), 256, 0, s>>>(db, perm, bu, n);
     check_launch();
   });
   bytes += 24.0 * n;
@@ -3261,14 +3304,14 @@ static void build_apply(mfh_factor *F) {
     std::vector<int64_t> gl;
     for (int q : fis) {
       FrontH &f = F->fronts[q];
-      for (int j = 0; j < f.npv; ++j) gl.push_back(f.ids[j]);
+      for (int j = 0; j < f.npv; ++j) gl.push_back(f.piv_lo + j);  // pivot ids are one contiguous run
     }
     long long *dgl = (long long *)sk.push(gl);
     int cnt = (int)gl.size();
     // level 0 fronts have no pivot-carrying descendants: nothing to gather
     if (h > 0) sk.launch([=](cudaStream_t s) {
-      k_contrib_gather<<<(int)std::min<int64_t>(cdiv((int64_t)cnt * 32, 256), 148 * 16), 256, 0, s>>>(dgl, cnt, d_cptr, d_coff,
-                                                                                  cbuf, bu, nullptr);
+      k_contrib_gather<<<dim3((unsigned)std::min<int64_t>(cdiv((int64_t)cnt * 32, 256), 148 * 16), nv), 256, 0, s>>>(
+          dgl, cnt, d_cptr, d_coff, cbuf, bu, nullptr, cst, nst);
       check_launch();
     });
     std::vector<GemvJob> j0, j1, j2;
@@ -3278,18 +3321,18 @@ static void build_apply(mfh_factor *F) {
       const double *bp = bu + f.piv_lo;
       double *t = cbuf + off[q];
       if (!f.structured) {
-        j0.push_back(gemv(t, nullptr, f.nf, f.Gfp, f.npv, f.npv, bp, 1.0));
+        j0.push_back(strided(gemv(t, nullptr, f.nf, f.Gfp, f.npv, f.npv, bp, 1.0), cst, nst, 0));
         bytes += 8.0 * (double)f.nf * f.npv;
       } else {
         // t = col_fp (RH b_piv), RH = row_fp H^{-1} precomputed at factor time
         FacView fpv = fac_view(F, F->blocks[f.fp]);
         if (fpv.rank) {
-          double *tmp = ar.d(fpv.rank);
-          j1.push_back(gemv(tmp, nullptr, fpv.rank, f.RH, f.npv, f.npv, bp, 1.0));
-          j2.push_back(gemv(t, nullptr, f.nf, fpv.col, fpv.ldc, fpv.rank, tmp, 1.0));
+          double *tmp = ar.d((size_t)nv * fpv.rank);
+          j1.push_back(strided(gemv(tmp, nullptr, fpv.rank, f.RH, f.npv, f.npv, bp, 1.0), fpv.rank, nst, 0));
+          j2.push_back(strided(gemv(t, nullptr, f.nf, fpv.col, fpv.ldc, fpv.rank, tmp, 1.0), cst, fpv.rank, 0));
           bytes += 8.0 * ((double)fpv.rank * f.npv + (double)f.nf * fpv.rank);
         } else {
-          j2.push_back(gemv(t, nullptr, f.nf, nullptr, 0, 0, nullptr, 0.0));  // exact zero contribution
+          j2.push_back(strided(gemv(t, nullptr, f.nf, nullptr, 0, 0, nullptr, 0.0), cst, 0, 0));  // exact zero contribution
         }
       }
     }
@@ -3300,8 +3343,8 @@ static void build_apply(mfh_factor *F) {
       fprintf(stderr, "[mfh apply up %2d] fronts %5zu gather %7d jobs %5zu+%5zu max npv %5lld\n", h, fis.size(), cnt,
               j0.size(), j2.size(), (long long)mr);
     }
-    run_gemv(sk, j0);
-    run_gemv(sk, j2);
+    run_gemv(sk, j0, nv);
+    run_gemv(sk, j2, nv);
   }
   };
   // ---------------- downward: x[piv] = pp_solve(b_u[piv] - apply_pf(x[fro]))
@@ -3317,7 +3360,8 @@ static void build_apply(mfh_factor *F) {
       double *xv = xw + f.piv_lo;
       const long long *fro = f.nf ? d_fro + off[q] : nullptr;
       if (!f.structured) {
-        jb.push_back(gemv(xv, nullptr, f.npv, f.Pinv, f.npv, f.npv, bp, 1.0, f.Gpf, f.nf, f.nf, xw, fro, -1.0));
+        jb.push_back(strided(gemv(xv, nullptr, f.npv, f.Pinv, f.npv, f.npv, bp, 1.0, f.Gpf, f.nf, f.nf, xw, fro, -1.0),
+                             nst, nst, nst));
         bytes += 8.0 * ((double)f.npv * f.npv + (double)f.npv * f.nf);
         continue;
       }
@@ -3325,13 +3369,16 @@ static void build_apply(mfh_factor *F) {
       FacView pfv;
       if (f.nf) pfv = fac_view(F, F->blocks[f.pf]);
       if (f.nf && pfv.rank) {
-        double *tmp = ar.d(pfv.rank);
-        ja.push_back(gemv(tmp, nullptr, pfv.rank, nullptr, 0, 0, nullptr, 0.0, pfv.row, pfv.ldr, f.nf, xw, fro, 1.0));
-        jb.push_back(gemv(xv, nullptr, f.npv, f.Hinv, f.npv, f.npv, bp, 1.0, f.Xp, pfv.rank, pfv.rank, tmp, nullptr,
-                          -1.0));
+        double *tmp = ar.d((size_t)nv * pfv.rank);
+        ja.push_back(strided(
+            gemv(tmp, nullptr, pfv.rank, nullptr, 0, 0, nullptr, 0.0, pfv.row, pfv.ldr, f.nf, xw, fro, 1.0), pfv.rank, 0,
+            nst));
+        jb.push_back(strided(gemv(xv, nullptr, f.npv, f.Hinv, f.npv, f.npv, bp, 1.0, f.Xp, pfv.rank, pfv.rank, tmp,
+                                  nullptr, -1.0),
+                             nst, nst, pfv.rank));
         bytes += 8.0 * ((double)f.npv * f.npv + (double)f.npv * pfv.rank + (double)pfv.rank * f.nf);
       } else {
-        jb.push_back(gemv(xv, nullptr, f.npv, f.Hinv, f.npv, f.npv, bp, 1.0));
+        jb.push_back(strided(gemv(xv, nullptr, f.npv, f.Hinv, f.npv, f.npv, bp, 1.0), nst, nst, 0));
         bytes += 8.0 * (double)f.npv * f.npv;
       }
     }
@@ -3341,15 +3388,15 @@ static void build_apply(mfh_factor *F) {
       for (auto &j : ja) lb += 8.0 * (double)j.m * (j.k1 + j.k2);
       fprintf(stderr, "[mfh apply dn %2d] jobs %5zu+%5zu  %.2f MB\n", h, ja.size(), jb.size(), lb / 1e6);
     }
-    run_gemv(sk, ja);
-    run_gemv(sk, jb);
+    run_gemv(sk, ja, nv);
+    run_gemv(sk, jb, nv);
   }
   };
   upward(byh);
   downward(byh);
   if (sh) exchange_point(xw, x_mask, x_tmp, std::max<int64_t>(1, n));  // every rank gets every pivot
   sk.launch([=](cudaStream_t s) {
-    k_gather_perm<<<grid_n, 256, 0, s>>>(xw, perm, dx, n);
+    k_gather_perm<<<dim3(grid_n, nv), 256, 0, s>>>(xw, perm, dx, n);
     check_launch();
   });
   // capture (the stream may still be running the factorization: captured work
@@ -3377,11 +3424,13 @@ static void build_apply(mfh_factor *F) {
     if (getenv("MFH_APPLY_OPS")) AP->ops = sk.ops;
   }
   auto tb2 = std::chrono::steady_clock::now();
-  F->timing.apply_build_ms = std::chrono::duration<double, std::milli>(tb1 - tb0).count();
-  F->timing.apply_instantiate_ms = std::chrono::duration<double, std::milli>(tb2 - tb1).count();
+  if (nv == 1) {
+    F->timing.apply_build_ms = std::chrono::duration<double, std::milli>(tb1 - tb0).count();
+    F->timing.apply_instantiate_ms = std::chrono::duration<double, std::milli>(tb2 - tb1).count();
+  }
   AP->bytes = bytes;
   AP->nodes = sh ? (int64_t)segs[0].size() : (int64_t)sk.ops.size();
-  F->apply = std::move(AP);
+  return AP;
 }
 
 // A->d_b -> A->d_x; a sharded factor exchanges the contribution buffer
@@ -3396,6 +3445,34 @@ static void apply_run(mfh_factor *F) {
     CK(cudaGraphLaunch(A->seg_exec[k], ctx->s));
     ctx->launches += A->seg_nodes[k];
   }
+}
+
+// the plan for nv right-hand sides (nv > 1: unsharded factors only)
+static ApplyPlan *plan_nv(mfh_factor *F, int nv) {
+  if (!F->apply) build_apply(F);
+  if (nv == 1) return F->apply.get();
+  auto &p = F->apply_nv[nv];
+  if (!p) p = make_apply(F, nv);
+  return p.get();
+}
+
+// nv right-hand sides, vector v at d_in + v * in_stride -> d_out + v * out_stride
+static void apply_device_nv(mfh_factor *F, int nv, const double *d_in, int64_t in_stride, double *d_out,
+                            int64_t out_stride) {
+  Ctx *ctx = F->ctx;
+  int64_t n = F->n;
+  if (n == 0) return;
+  ApplyPlan *A = plan_nv(F, nv);
+  CK(cudaMemcpy2DAsync(A->d_b, sizeof(double) * n, d_in, sizeof(double) * in_stride, sizeof(double) * n, nv,
+                       cudaMemcpyDeviceToDevice, ctx->s));
+  if (nv == 1) {
+    apply_run(F);
+  } else {
+    CK(cudaGraphLaunch(A->exec, ctx->s));
+    ctx->launches += A->nodes;
+  }
+  CK(cudaMemcpy2DAsync(d_out, sizeof(double) * out_stride, A->d_x, sizeof(double) * n, sizeof(double) * n, nv,
+                       cudaMemcpyDeviceToDevice, ctx->s));
 }
 
 static void apply_device(mfh_factor *F, const double *d_in, double *d_out) {
@@ -3649,12 +3726,6 @@ extern "C" void mfh_factor_free(mfh_factor *f) {
   if (!f) return;
   std::lock_guard<std::recursive_mutex> lk_(f->ctx->mu);
   cudaStreamSynchronize(f->ctx->s);
-  if (f->apply) {
-    if (f->apply->exec) cudaGraphExecDestroy(f->apply->exec);
-    if (f->apply->graph) cudaGraphDestroy(f->apply->graph);
-    for (auto e : f->apply->seg_exec) cudaGraphExecDestroy(e);
-    for (auto g : f->apply->seg_graph) cudaGraphDestroy(g);
-  }
   f->arena.release();
   delete f;
 }
@@ -3665,16 +3736,23 @@ extern "C" int mfh_apply(mfh_factor *f, const double *b, double *x, int64_t nrhs
   Ctx *ctx = f->ctx;
   int64_t n = f->n;
   if (!f->apply) build_apply(f);
-  ApplyPlan *A = f->apply.get();
-  for (int64_t r = 0; r < nrhs; ++r) {
-    if (n == 0) continue;
+  // up to eight right-hand sides per graph replay: the factor is read once per group
+  for (int64_t r = 0; r < nrhs && n > 0;) {
+    const int c = f->sharded ? 1 : (int)std::min<int64_t>(8, nrhs - r);
     if (on_device) {
-      apply_device(f, b + r * n, x + r * n);
+      apply_device_nv(f, c, b + r * n, n, x + r * n, n);
     } else {
-      CK(cudaMemcpyAsync(A->d_b, b + r * n, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->s));
-      apply_run(f);
-      CK(cudaMemcpyAsync(x + r * n, A->d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->s));
+      ApplyPlan *A = plan_nv(f, c);
+      CK(cudaMemcpyAsync(A->d_b, b + r * n, sizeof(double) * n * c, cudaMemcpyHostToDevice, ctx->s));
+      if (c == 1) {
+        apply_run(f);
+      } else {
+        CK(cudaGraphLaunch(A->exec, ctx->s));
+        ctx->launches += A->nodes;
+      }
+      CK(cudaMemcpyAsync(x + r * n, A->d_x, sizeof(double) * n * c, cudaMemcpyDeviceToHost, ctx->s));
     }
+    r += c;
   }
   CK(cudaStreamSynchronize(ctx->s));
   MFH_CATCH

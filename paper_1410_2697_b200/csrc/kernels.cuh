@@ -2215,6 +2215,8 @@ struct GemvJob {
   const double *x2;
   const long long *idx2;
   double a2;
+  // several right-hand sides (k_gemv_mv): vector v reads / writes at p + v * stride
+  long long ys, y0s, x1s, x2s;
 };
 
 // warp per output row; row t belongs to job q with start[q] <= t < start[q + 1].
@@ -2375,17 +2377,112 @@ __global__ void __launch_bounds__(256) k_gemv2(const GemvJob *__restrict__ jobs,
   gemv_rows(jobs, start, wq[warp], t0, min(nrows, t0 + chunk), lane);
 }
 
+// NV right-hand sides in one pass over the matrices: every A element is loaded
+// once and multiplies NV vectors. Per vector and row the arithmetic is exactly
+// gemv_rows' (short rows: W-lane products + xor tree; otherwise lane-strided
+// ascending FMA chains + shuffle tree), so each column is bit-identical to a
+// one-vector apply.
+template <int NV>
+__device__ __forceinline__ void gemv_rows_mv(const GemvJob *__restrict__ jobs, const int *__restrict__ start, int q,
+                                             int t0, int t1, int lane) {
+  if (t0 >= t1) return;
+  int qend = start[q + 1];
+  for (int t = t0; t < t1;) {
+    while (t >= qend) {
+      ++q;
+      qend = start[q + 1];
+    }
+    const GemvJob &J = jobs[q];
+    const int s0 = start[q];
+    if (J.k2 == 0 && J.k1 <= 16) {
+      const int W = J.k1 <= 4 ? 4 : (J.k1 <= 8 ? 8 : 16);
+      const int G = 32 / W, g = lane / W, l = lane & (W - 1);
+      const int tend = min(t1, qend);
+      for (int tb = t; tb < tend; tb += G) {
+        const int tr = tb + g;
+        const bool ok = tr < tend && l < J.k1;
+        const double av = ok ? J.A1[(long long)(tr - s0) * J.lda1 + l] : 0.0;
+        double sr[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sr[v] = ok ? av * J.x1[v * J.x1s + l] : 0.0;
+        for (int o = W >> 1; o > 0; o >>= 1)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) sr[v] += __shfl_xor_sync(0xffffffffu, sr[v], o);
+        if (l == 0 && tr < tend) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const double y0 = J.y0 ? J.y0[v * J.y0s + tr - s0] : 0.0;
+            J.y[v * J.ys + tr - s0] = y0 + J.a1 * sr[v];
+          }
+        }
+      }
+      t = tend;
+      continue;
+    }
+    const int i = t - s0;
+    double s1[NV], s2[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) s1[v] = s2[v] = 0.0;
+    if (J.k1) {
+      const double *a = J.A1 + (long long)i * J.lda1;
+#pragma unroll 4
+      for (int kk = lane; kk < J.k1; kk += 32) {
+        const double av = a[kk];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) s1[v] = fma(av, J.x1[v * J.x1s + kk], s1[v]);
+      }
+    }
+    if (J.k2) {
+      const double *a = J.A2 + (long long)i * J.lda2;
+#pragma unroll 4
+      for (int kk = lane; kk < J.k2; kk += 32) {
+        const double av = a[kk];
+        const long long xi = J.idx2 ? J.idx2[kk] : kk;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) s2[v] = fma(av, J.x2[v * J.x2s + xi], s2[v]);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      s1[v] = warp_sum_down(s1[v]);
+      s2[v] = warp_sum_down(s2[v]);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double y = J.y0 ? J.y0[v * J.y0s + i] : 0.0;
+        if (J.k1) y += J.a1 * s1[v];
+        if (J.k2) y += J.a2 * s2[v];
+        J.y[v * J.ys + i] = y;
+      }
+    }
+    ++t;
+  }
+}
+template <int NV>
+__global__ void __launch_bounds__(256) k_gemv_mv(const GemvJob *__restrict__ jobs, const int *__restrict__ start,
+                                                 const int *__restrict__ wq, int chunk, int nrows) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int t0 = warp * chunk;
+  if (t0 >= nrows) return;
+  gemv_rows_mv<NV>(jobs, start, wq[warp], t0, min(nrows, t0 + chunk), lane);
+}
+
 // ---------------------------------------------------------------------------
 // solve-phase vector kernels
 // ---------------------------------------------------------------------------
 __global__ void k_scatter_perm(const double *__restrict__ b, const long long *__restrict__ perm,
                                double *__restrict__ bu, long long n) {
+  b += blockIdx.y * n;  // right-hand side blockIdx.y
+  bu += blockIdx.y * n;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     bu[perm[i]] = b[i];
 }
 __global__ void k_gather_perm(const double *__restrict__ x, const long long *__restrict__ perm,
                               double *__restrict__ out, long long n) {
+  x += blockIdx.y * n;  // right-hand side blockIdx.y
+  out += blockIdx.y * n;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     out[i] = x[perm[i]];
@@ -2397,7 +2494,10 @@ __global__ void __launch_bounds__(256) k_contrib_gather(const long long *__restr
                                                         const long long *__restrict__ cptr,
                                                         const long long *__restrict__ coff,
                                                         const double *__restrict__ cbuf, double *__restrict__ bu,
-                                                        double *__restrict__ y) {
+                                                        double *__restrict__ y, long long cstride, long long bstride) {
+  cbuf += blockIdx.y * cstride;  // right-hand side blockIdx.y
+  bu += blockIdx.y * bstride;
+  if (y) y += blockIdx.y * bstride;
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < cnt; t += nw) {

@@ -204,6 +204,22 @@ int mfh_gmres(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const double *b
 int mfh_gmres_device(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const double *d_b,
                      double *d_x, double tol, int64_t max_iter, int64_t restart, double *hist,
                      int64_t *n_hist, int64_t *iterations, int *converged);
+/* Several right-hand sides with one device factorization (BASELINE C5: 8
+ * RHS). Replaces the caller's loop of gmres(A, b_r, M) calls (the reference
+ * has no batched entry; krylov.py:68-161 per column): right-hand side r is
+ * b + r*n, its solution x + r*n; groups of up to eight run in lockstep and
+ * share each preconditioner apply, so the factor is read once per Arnoldi step
+ * for the group. Per right-hand side: history row r of hist (hist_cap
+ * entries), n_hist[r], iterations[r], converged[r]; every column is
+ * bit-identical to its mfh_gmres solve. ops->A and ops->M must be device
+ * objects (no host callbacks). Host arrays / device arrays respectively. */
+int mfh_gmres_batched(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, int64_t nrhs, const double *b,
+                      double *x, double tol, int64_t max_iter, int64_t restart, double *hist,
+                      int64_t hist_cap, int64_t *n_hist, int64_t *iterations, int *converged);
+int mfh_gmres_batched_device(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, int64_t nrhs,
+                             const double *d_b, double *d_x, double tol, int64_t max_iter,
+                             int64_t restart, double *hist, int64_t hist_cap, int64_t *n_hist,
+                             int64_t *iterations, int *converged);
 
 /* ---- kernel plugin (full_pivot_lu, _kernels/__init__.py:25; _core.pyx:23) - */
 /* Batched complete-pivot LU on the device. Blocks are row-major, packed at

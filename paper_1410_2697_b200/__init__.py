@@ -8,7 +8,7 @@ behind the C-ABI of ``include/mfh.h`` (``libmfh.so``).
 
 from ._lib import PivotMonotonicityError
 from .kernels import BACKEND as KERNEL_BACKEND, full_pivot_lu, full_pivot_lu_batched
-from .krylov import (ConvergenceHistory, LinearOperator, Preconditioner, gmres,
+from .krylov import (ConvergenceHistory, LinearOperator, Preconditioner, gmres, gmres_batched,
                      identity_preconditioner, mf_preconditioner)
 from .multifrontal import (ACCELERATED, CONVENTIONAL, FactorStats, FrontRecord, MfFactorization,
                            MfParams, mf_factorize, mf_solve)
@@ -24,7 +24,7 @@ __all__ = [
     "FactorStats", "FrontRecord", "KERNEL_BACKEND", "LinearOperator", "MfFactorization", "MfParams",
     "PivotMonotonicityError", "Preconditioner", "SepNode", "SeparatorTree", "SparseMatrix",
     "adjacency_graph", "build_elimination_tree", "full_pivot_lu", "full_pivot_lu_batched",
-    "gen_hex_q1", "gen_p1_delaunay", "gen_poisson7", "gen_q1_2d", "gmres",
+    "gen_hex_q1", "gen_p1_delaunay", "gen_poisson7", "gen_q1_2d", "gmres", "gmres_batched",
     "identity_preconditioner", "mf_factorize", "mf_preconditioner", "mf_solve",
     "nested_dissection", "seeded_rhs", "spmv",
 ]

@@ -149,6 +149,10 @@ def _sig(lib):
                                 C.POINTER(C.c_int)]),
         "mfh_gmres_device": (C.c_int, [P, C.POINTER(mfh_gmres_ops), I64, P, P, d, I64, I64, P, pi,
                                        pi, C.POINTER(C.c_int)]),
+        "mfh_gmres_batched": (C.c_int, [P, C.POINTER(mfh_gmres_ops), I64, I64, P, P, d, I64, I64, P, I64, P, P,
+                                        P]),
+        "mfh_gmres_batched_device": (C.c_int, [P, C.POINTER(mfh_gmres_ops), I64, I64, P, P, d, I64, I64, P, I64,
+                                               P, P, P]),
         "mfh_full_pivot_lu_batched": (C.c_int, [P, I64, P, P, P, P, I64, d, P, P, P, P, P, P, P]),
         "mfh_test_inverse_batched": (C.c_int, [P, I64, P, P, P, I64, P]),
     }

@@ -3030,13 +3030,23 @@ static void run_gemv(Sink &sk, const std::vector<GemvJob> &jobs, int nv = 1) {
   if (nr == 0) return;
   // one wave of warps, each a contiguous chunk of rows (a chunk of >= GV_R rows
   // of one job keeps GV_R rows' loads in flight)
-  static int occ = 0;
+  static int occ_nv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (nv < 1 || nv > 8) throw runtime_error("run_gemv: 1..8 right-hand sides per launch");
+  int &occ = occ_nv[nv];
   if (!occ) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gemv2, 256, 0));
+    const void *fns[9] = {nullptr, (const void *)k_gemv2, (const void *)k_gemv_mv<2>, (const void *)k_gemv_mv<3>,
+                          (const void *)k_gemv_mv<4>, (const void *)k_gemv_mv<5>, (const void *)k_gemv_mv<6>,
+                          (const void *)k_gemv_mv<7>, (const void *)k_gemv_mv<8>};
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fns[nv], 256, 0));
     occ = std::max(occ, 1);
   }
   int grid = (int)std::min<int64_t>(cdiv((int64_t)nr * 32, 256), (int64_t)148 * occ);
-  const int nw = grid * 8, chunk = (int)cdiv(nr, nw);
+  const int nw = grid * 8;
+  int chunk = (int)cdiv(nr, nw);
+  if (nv > 1) {  // whole row groups of k_gemv_mv (RR rows share each x load)
+    const int rr = nv <= 4 ? 8 : 4;
+    chunk = (int)cdiv(chunk, rr) * rr;
+  }
   std::vector<int> wq;
   wq.reserve(cdiv(nr, chunk));
   for (int t0 = 0, q = 0; t0 < nr; t0 += chunk) {
@@ -4157,6 +4167,225 @@ struct GmresRun {
   }
 };
 
+// Several right-hand sides in lockstep (BASELINE C5: 8 RHS, one factor). The
+// preconditioner apply of all Krylov vectors of a step is one graph replay
+// (apply_device_nv: the factor is read once per step, not once per vector);
+// SpMV, Gram-Schmidt, the scalings and the host Givens recurrence run per
+// right-hand side with GmresRun's kernels and launch shapes, so every
+// solution and residual history is bit-identical to its one-vector solve.
+struct GmresMulti {
+  Ctx *ctx;
+  const mfh_gmres_ops *ops;
+  int64_t n;
+  int nv;
+  double sync_ms = 0.0;
+  struct Rhs {
+    double nb = 0.0;
+    bool conv = false, lucky_stop = false;
+    int64_t its = 0, m = 0, j = 0;
+    std::vector<double> H, cs, sn, gg, res;
+  };
+  void run(const double *d_B, double *d_X, double tol, int64_t max_iter, int64_t restart, std::vector<Rhs> &st) {
+    if (!(tol > 0.0 && tol < 1.0)) throw value_error("tol must lie in (0, 1)");
+    if (max_iter < 1 || restart < 1) throw value_error("max_iter and restart must be positive");
+    if (!ops->A || !ops->M) throw value_error("batched GMRES needs a device operator and a device factorization");
+    if (nv < 1 || nv > 8) throw value_error("batched GMRES: 1..8 right-hand sides per group");
+    GmresRun g{ctx, ops, n};
+    st.assign(nv, Rhs{});
+    const int64_t mcap = std::min(restart, max_iter);
+    if (mcap > 2000) throw value_error("min(restart, max_iter) must be <= 2000");
+    const int64_t HS = 2048;  // per-vector stride of the Hessenberg column / y areas
+    // V [nv][mcap+1][n], w / r / z / x-work [nv][n], H and y [nv][HS], scalars [nv][8]
+    const size_t need = sizeof(double) * ((size_t)nv * (size_t)n * (size_t)(mcap + 4) + (size_t)nv * (2 * HS + 8));
+    auto chunk = ctx->pool.take(need);
+    double *V = (double *)chunk.first, *w = V + (size_t)nv * n * (mcap + 1), *r = w + (size_t)nv * n,
+           *z = r + (size_t)nv * n, *Hd = z + (size_t)nv * n, *Yd = Hd + nv * HS, *sc = Yd + nv * HS;
+    const int64_t vs = n * (mcap + 1);  // V stride between right-hand sides
+    double *hp = nullptr;
+    CK(cudaMallocHost(&hp, sizeof(double) * (size_t)nv * (2 * HS + 8)));
+    double *hH = hp, *hY = hp + nv * HS, *hS = hp + 2 * nv * HS;
+    int gr = g.gridn();
+    int per_sm = 0, nsm = 148;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs_coop, 256, 0));
+    int mgs_grid = std::max(1, std::min(per_sm, 2) * nsm);
+    mgs_grid = (int)std::min<int64_t>(mgs_grid, std::max<int64_t>(1, cdiv(n, 256)));
+    if (mgs_grid > (RED_BLOCKS + 64) / 2) mgs_grid = (RED_BLOCKS + 64) / 2;
+    auto sync_read = [&](double *dst, const double *src, size_t bytes) {
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->s));
+      auto t0 = std::chrono::steady_clock::now();
+      CK(cudaStreamSynchronize(ctx->s));
+      sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    };
+    auto cleanup = [&]() {
+      cudaStreamSynchronize(ctx->s);
+      ctx->pool.give(chunk);
+      cudaFreeHost(hp);
+    };
+    auto B = [&](int v) { return d_B + (size_t)v * n; };
+    auto X = [&](int v) { return d_X + (size_t)v * n; };
+    auto W = [&](int v) { return w + (size_t)v * n; };
+    auto R = [&](int v) { return r + (size_t)v * n; };
+    auto Z = [&](int v) { return z + (size_t)v * n; };
+    auto Vj = [&](int v, int64_t j) { return V + (size_t)v * vs + (size_t)j * n; };
+    try {
+      for (int v = 0; v < nv; ++v) {
+        CK(cudaMemsetAsync(X(v), 0, sizeof(double) * n, ctx->s));
+        g.dot(B(v), B(v), sc + 8 * v, true);
+      }
+      sync_read(hS, sc, sizeof(double) * 8 * nv);
+      for (int v = 0; v < nv; ++v) {
+        st[v].nb = hS[8 * v];
+        if (st[v].nb == 0.0) {
+          st[v].conv = true;
+          st[v].res.push_back(0.0);
+        }
+      }
+      auto active = [&](int v) { return !st[v].conv && st[v].its < max_iter; };
+      while (true) {
+        std::vector<int> C;
+        for (int v = 0; v < nv; ++v)
+          if (active(v)) C.push_back(v);
+        if (C.empty()) break;
+        for (int v : C) {
+          op_apply_device(ops->A, X(v), W(v));
+          k_sub<<<gr, 256, 0, ctx->s>>>(B(v), W(v), R(v), n);
+          ctx->launches++;
+          g.dot(R(v), R(v), sc + 8 * v + 1, true);
+        }
+        sync_read(hS, sc, sizeof(double) * 8 * nv);
+        std::vector<int> run;
+        for (int v : C) {
+          Rhs &q = st[v];
+          const double beta = hS[8 * v + 1];
+          if (!std::isfinite(beta)) throw value_error("GMRES residual is not finite");
+          if (beta / q.nb <= tol) {
+            q.conv = true;
+            if (q.res.empty()) q.res.push_back(beta / q.nb);
+            continue;
+          }
+          q.m = std::min(restart, max_iter - q.its);
+          q.H.assign((q.m + 1) * q.m, 0.0);
+          q.cs.assign(q.m, 0.0);
+          q.sn.assign(q.m, 0.0);
+          q.gg.assign(q.m + 1, 0.0);
+          q.gg[0] = beta;
+          q.j = 0;
+          q.lucky_stop = false;
+          k_scale_inv<<<gr, 256, 0, ctx->s>>>(sc + 8 * v + 1, R(v), Vj(v, 0), n);
+          ctx->launches++;
+          run.push_back(v);
+        }
+        std::vector<int> cyc = run;  // right-hand sides of this cycle
+        for (int64_t j = 0; !run.empty(); ++j) {
+          // one replay applies M to column j of every right-hand side
+          apply_device_nv(ops->M, nv, V + (size_t)j * n, vs, z, n);
+          for (int v : run) {
+            op_apply_device(ops->A, Z(v), W(v));
+            const double *Vc = V + (size_t)v * vs;
+            double *wc = W(v), *Hc = Hd + v * HS, *pc = ctx->d_part;
+            long long nn = n;
+            int jj = (int)j;
+            void *args[6] = {(void *)&Vc, (void *)&wc, (void *)&nn, (void *)&jj, (void *)&Hc, (void *)&pc};
+            CK(cudaLaunchCooperativeKernel((const void *)k_mgs_coop, dim3(mgs_grid), dim3(256), args, 0, ctx->s));
+            ctx->launches++;
+          }
+          CK(cudaMemcpy2DAsync(hH, sizeof(double) * HS, Hd, sizeof(double) * HS, sizeof(double) * (j + 2), nv,
+                               cudaMemcpyDeviceToHost, ctx->s));
+          {
+            auto t0 = std::chrono::steady_clock::now();
+            CK(cudaStreamSynchronize(ctx->s));
+            sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+          }
+          std::vector<int> next;
+          for (int v : run) {
+            Rhs &q = st[v];
+            const int64_t m = q.m;
+            auto h = [&](int64_t i, int64_t jc) -> double & { return q.H[i * m + jc]; };
+            const double *hcol = hH + v * HS;
+            const double hn = hcol[j + 1];
+            for (int64_t i = 0; i <= j; ++i) h(i, j) = hcol[i];
+            if (!std::isfinite(hn)) throw value_error("GMRES residual is not finite");
+            h(j + 1, j) = hn;
+            for (int64_t i = 0; i < j; ++i) {
+              double t = q.cs[i] * h(i, j) + q.sn[i] * h(i + 1, j);
+              h(i + 1, j) = -q.sn[i] * h(i, j) + q.cs[i] * h(i + 1, j);
+              h(i, j) = t;
+            }
+            const double den = std::hypot(h(j, j), h(j + 1, j));
+            if (den == 0.0) throw value_error("GMRES breakdown: zero Hessenberg column");
+            q.cs[j] = h(j, j) / den;
+            q.sn[j] = h(j + 1, j) / den;
+            h(j, j) = den;
+            h(j + 1, j) = 0.0;
+            q.gg[j + 1] = -q.sn[j] * q.gg[j];
+            q.gg[j] = q.cs[j] * q.gg[j];
+            q.its += 1;
+            const double rel = std::fabs(q.gg[j + 1]) / q.nb;
+            q.res.push_back(rel);
+            const bool lucky = hn == 0.0;
+            q.j = j + 1;
+            if (rel <= tol || lucky) {
+              q.lucky_stop = lucky;
+              continue;
+            }
+            if (j + 1 < m) {
+              k_scale_inv<<<gr, 256, 0, ctx->s>>>(Hd + v * HS + j + 1, W(v), Vj(v, j + 1), n);
+              ctx->launches++;
+              next.push_back(v);
+            }
+          }
+          run.swap(next);
+        }
+        // x += M (V y) for every right-hand side of the cycle; one replay for all
+        bool any = false;
+        for (int v : cyc) {
+          Rhs &q = st[v];
+          if (q.j == 0) continue;
+          const int64_t m = q.m, jn = q.j;
+          auto h = [&](int64_t i, int64_t jc) -> double & { return q.H[i * m + jc]; };
+          double *y = hY + v * HS;
+          for (int64_t i = jn - 1; i >= 0; --i) {
+            double s2 = 0.0;
+            for (int64_t c = i + 1; c < jn; ++c) s2 += h(i, c) * y[c];
+            y[i] = (q.gg[i] - s2) / h(i, i);
+          }
+          CK(cudaMemcpyAsync(Yd + v * HS, y, sizeof(double) * jn, cudaMemcpyHostToDevice, ctx->s));
+          k_combine<<<gr, 256, 0, ctx->s>>>(V + (size_t)v * vs, Yd + v * HS, (int)jn, n, W(v));
+          ctx->launches++;
+          any = true;
+        }
+        if (any) {
+          apply_device_nv(ops->M, nv, w, n, z, n);
+          for (int v : cyc)
+            if (st[v].j > 0) {
+              k_add<<<gr, 256, 0, ctx->s>>>(Z(v), X(v), n);
+              ctx->launches++;
+            }
+        }
+        for (int v : cyc) {
+          op_apply_device(ops->A, X(v), W(v));
+          k_sub<<<gr, 256, 0, ctx->s>>>(B(v), W(v), R(v), n);
+          ctx->launches++;
+          g.dot(R(v), R(v), sc + 8 * v + 3, true);
+        }
+        sync_read(hS, sc, sizeof(double) * 8 * nv);
+        for (int v : cyc) {
+          Rhs &q = st[v];
+          const double tr = hS[8 * v + 3] / q.nb;
+          if (!std::isfinite(tr)) throw value_error("GMRES residual is not finite");
+          if (!q.res.empty()) q.res.back() = tr;
+          if (tr <= tol || q.lucky_stop) q.conv = true;
+        }
+      }
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  }
+};
+
 }  // namespace mfh
 
 static int gmres_common(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const double *d_b, double *d_x,
@@ -4204,6 +4433,71 @@ extern "C" int mfh_gmres(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, cons
   cudaMemcpyAsync(db, b, sizeof(double) * n, cudaMemcpyHostToDevice, s);
   int rc = gmres_common(ctx, ops, n, db, dx, tol, max_iter, restart, hist, n_hist, iterations, converged);
   if (rc == MFH_OK) cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  ctx->c.pool.give(chunk);
+  return rc;
+}
+
+// Several right-hand sides (vector r at b + r n), groups of up to eight in
+// lockstep; per right-hand side: history row r of hist (hist_cap entries),
+// n_hist[r], iterations[r], converged[r]. Device operator and factor only.
+static int gmres_batched_common(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, int64_t nrhs, const double *d_b,
+                                double *d_x, double tol, int64_t max_iter, int64_t restart, double *hist,
+                                int64_t hist_cap, int64_t *n_hist, int64_t *iterations, int *converged) {
+  MFH_TRY
+  if (nrhs < 0) throw value_error("nrhs must be non-negative");
+  auto tg0 = std::chrono::steady_clock::now();
+  double sync_ms = 0.0;
+  for (int64_t r0 = 0; r0 < nrhs; r0 += 8) {
+    const int nv = (int)std::min<int64_t>(8, nrhs - r0);
+    GmresMulti g{&ctx->c, ops, n, nv};
+    std::vector<GmresMulti::Rhs> st;
+    g.run(d_b + r0 * n, d_x + r0 * n, tol, max_iter, restart, st);
+    sync_ms += g.sync_ms;
+    for (int v = 0; v < nv; ++v) {
+      const int64_t r = r0 + v;
+      const auto &q = st[v];
+      const int64_t nh = (int64_t)q.res.size();
+      if (hist) std::memcpy(hist + r * hist_cap, q.res.data(), sizeof(double) * std::min(nh, hist_cap));
+      n_hist[r] = nh;
+      iterations[r] = q.its;
+      converged[r] = q.conv ? 1 : 0;
+    }
+  }
+  if (ops->M) {
+    ops->M->timing.gmres_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tg0).count();
+    ops->M->timing.gmres_sync_ms = sync_ms;
+  }
+  MFH_CATCH
+}
+
+extern "C" int mfh_gmres_batched_device(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, int64_t nrhs,
+                                        const double *d_b, double *d_x, double tol, int64_t max_iter,
+                                        int64_t restart, double *hist, int64_t hist_cap, int64_t *n_hist,
+                                        int64_t *iterations, int *converged) {
+  std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
+  return gmres_batched_common(ctx, ops, n, nrhs, d_b, d_x, tol, max_iter, restart, hist, hist_cap, n_hist,
+                              iterations, converged);
+}
+
+extern "C" int mfh_gmres_batched(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, int64_t nrhs, const double *b,
+                                 double *x, double tol, int64_t max_iter, int64_t restart, double *hist,
+                                 int64_t hist_cap, int64_t *n_hist, int64_t *iterations, int *converged) {
+  std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
+  cudaStream_t s = ctx->c.s;
+  std::pair<char *, size_t> chunk{nullptr, 0};
+  const size_t len = (size_t)std::max<int64_t>(1, n * std::max<int64_t>(1, nrhs));
+  try {
+    chunk = ctx->c.pool.take(sizeof(double) * 2 * len);
+  } catch (const std::exception &e) {
+    set_last_error(std::string("CUDA allocation failed in mfh_gmres_batched: ") + e.what());
+    return MFH_ERUNTIME;
+  }
+  double *db = (double *)chunk.first, *dx = db + len;
+  cudaMemcpyAsync(db, b, sizeof(double) * n * nrhs, cudaMemcpyHostToDevice, s);
+  int rc = gmres_batched_common(ctx, ops, n, nrhs, db, dx, tol, max_iter, restart, hist, hist_cap, n_hist,
+                                iterations, converged);
+  if (rc == MFH_OK) cudaMemcpyAsync(x, dx, sizeof(double) * n * nrhs, cudaMemcpyDeviceToHost, s);
   cudaStreamSynchronize(s);
   ctx->c.pool.give(chunk);
   return rc;

@@ -2420,6 +2420,61 @@ __device__ __forceinline__ void gemv_rows_mv(const GemvJob *__restrict__ jobs, c
       continue;
     }
     const int i = t - s0;
+    constexpr int RR = NV <= 4 ? 8 : 4;  // rows sharing each x load (RR x NV accumulators); run_gemv rounds chunks to it
+    if (t + RR <= min(t1, qend)) {
+      // RR rows of one job: per row and vector the same lane-strided ascending
+      // chain and shuffle tree as below; the k1 result is stored (y0 + a1 s1)
+      // and the k2 term added after, i.e. (y0 + a1 s1) + a2 s2 as below
+      double acc[RR][NV];
+      for (int part = 0; part < 2; ++part) {
+        const int kk_n = part == 0 ? J.k1 : J.k2;
+        if (kk_n == 0) {
+          if (part == 0 && lane == 0)
+            for (int r = 0; r < RR; ++r)
+#pragma unroll
+              for (int v = 0; v < NV; ++v) J.y[v * J.ys + i + r] = J.y0 ? J.y0[v * J.y0s + i + r] : 0.0;
+          continue;
+        }
+#pragma unroll
+        for (int r = 0; r < RR; ++r)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) acc[r][v] = 0.0;
+        const double *a = part == 0 ? J.A1 + (long long)i * J.lda1 : J.A2 + (long long)i * J.lda2;
+        const long long lda = part == 0 ? J.lda1 : J.lda2;
+        const double *xb = part == 0 ? J.x1 : J.x2;
+        const long long xs = part == 0 ? J.x1s : J.x2s;
+        const long long *ix = part == 0 ? nullptr : J.idx2;
+        for (int kk = lane; kk < kk_n; kk += 32) {
+          double av[RR];
+#pragma unroll
+          for (int r = 0; r < RR; ++r) av[r] = a[r * lda + kk];
+          const long long xi = ix ? ix[kk] : kk;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const double xv = xb[v * xs + xi];
+#pragma unroll
+            for (int r = 0; r < RR; ++r) acc[r][v] = fma(av[r], xv, acc[r][v]);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < RR; ++r)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) acc[r][v] = warp_sum_down(acc[r][v]);
+        if (lane == 0) {
+          const double al = part == 0 ? J.a1 : J.a2;
+#pragma unroll
+          for (int r = 0; r < RR; ++r)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              double *yp = J.y + v * J.ys + i + r;
+              const double base = part == 0 ? (J.y0 ? J.y0[v * J.y0s + i + r] : 0.0) : *yp;
+              *yp = base + al * acc[r][v];
+            }
+        }
+      }
+      t += RR;
+      continue;
+    }
     double s1[NV], s2[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) s1[v] = s2[v] = 0.0;

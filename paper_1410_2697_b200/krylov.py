@@ -135,3 +135,39 @@ def gmres(A, b, M=None, tol=DEFAULT_TOL, max_iter=DEFAULT_MAX_ITER, restart=DEFA
     _lib.check(rc)
     h = ConvergenceHistory([float(v) for v in hist[:nh.value]], bool(conv.value), int(its.value))
     return x, h
+
+
+def gmres_batched(A, B, M, tol=DEFAULT_TOL, max_iter=DEFAULT_MAX_ITER, restart=DEFAULT_RESTART):
+    """``gmres`` for the columns of ``B`` (n x k) with one device factorization:
+    groups of up to eight right-hand sides run in lockstep and share each
+    preconditioner apply (the factor is read once per Arnoldi step, not once per
+    column). Every column's solution and history are bit-identical to
+    ``gmres(A, B[:, j], M)``. ``A`` must be a SparseMatrix (or a LinearOperator
+    from one) and ``M`` a ``mf_preconditioner``."""
+    if not (0.0 < tol < 1.0):
+        raise ValueError("tol must lie in (0, 1)")
+    if max_iter < 1 or restart < 1:
+        raise ValueError("max_iter and restart must be positive")
+    if isinstance(A, SparseMatrix):
+        A = LinearOperator.from_matrix(A)
+    if A._device is None or M is None or getattr(M, "_factor", None) is None:
+        raise ValueError("gmres_batched needs a device operator and an mf_preconditioner")
+    B = np.asarray(B, dtype=np.float64)
+    if B.ndim != 2 or B.shape[0] != A.dimension:
+        raise ValueError("right-hand sides must be an (n, k) array matching the operator dimension")
+    n, k = B.shape
+    Bt = np.ascontiguousarray(B.T)
+    Xt = np.zeros_like(Bt)
+    ops = _lib.mfh_gmres_ops()
+    ops.A = A._device.handle
+    ops.M = M._factor._h
+    cap = max(1, int(max_iter))
+    hist = np.empty((max(1, k), cap))
+    nh = np.zeros(max(1, k), dtype=np.int64)
+    its = np.zeros(max(1, k), dtype=np.int64)
+    conv = np.zeros(max(1, k), dtype=np.int32)
+    _lib.check(_lib.lib().mfh_gmres_batched(_lib.context().handle, C.byref(ops), n, k, _lib.ptr(Bt), _lib.ptr(Xt),
+                                            float(tol), int(max_iter), int(restart), _lib.ptr(hist), cap,
+                                            _lib.ptr(nh), _lib.ptr(its), _lib.ptr(conv)))
+    hs = [ConvergenceHistory([float(v) for v in hist[j, :nh[j]]], bool(conv[j]), int(its[j])) for j in range(k)]
+    return Xt.T.copy(), hs

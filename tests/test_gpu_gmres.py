@@ -96,3 +96,25 @@ def test_max_iter_cap():
     A = rng.standard_normal((50, 50)) + 2 * np.eye(50)
     _, h = P.gmres(op(A), rng.standard_normal(50), tol=1e-14, restart=4, max_iter=7)
     assert h.iterations <= 7 and not h.converged
+
+
+@pytest.mark.parametrize("restart", [6, 30])
+def test_batched_rhs_bit_identical_to_single_solves(restart):
+    """gmres_batched (groups of up to eight right-hand sides sharing each
+    preconditioner apply) against one gmres call per column: solutions,
+    iteration counts and residual histories bit-identical, across a group
+    boundary (10 = 8 + 2), with restarts (restart 6) and a zero column."""
+    import paper_1410_2697_b200 as P
+    A, _ = P.gen_poisson7(12, 11, 10)
+    et = P.build_elimination_tree(P.nested_dissection(P.adjacency_graph(A), 32), A)
+    F = P.mf_factorize(A, et, P.ACCELERATED, P.MfParams(n_c=96, eps=1e-2, n_leaf=16))
+    M = P.mf_preconditioner(F)
+    B = np.random.default_rng(5).standard_normal((A.n_rows, 10))
+    B[:, 3] = 0.0
+    X, hs = P.gmres_batched(A, B, M, tol=1e-10, restart=restart)
+    for j in range(B.shape[1]):
+        x, h = P.gmres(A, B[:, j], M=M, tol=1e-10, restart=restart)
+        np.testing.assert_array_equal(X[:, j], x)
+        assert hs[j].iterations == h.iterations and hs[j].converged == h.converged
+        assert hs[j].residuals == h.residuals
+    assert hs[0].iterations > restart if restart == 6 else True

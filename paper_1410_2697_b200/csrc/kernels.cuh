@@ -251,26 +251,40 @@ __device__ __forceinline__ const HBlk *hodlr_locate_rect(const HNode *hn, int n,
 }
 
 // Register-blocked extend-add sampler for fronts whose children carry a
-// low-rank update W Vt of meaningful rank: 64 x 64 tiles, 256 threads, 4 x 4
-// entries per thread. Rank-r dot products stream their factors through shared
-// memory in 16-wide chunks (16 FMA per 8 shared loads, next chunk prefetched
-// into registers): the W Vt term always, and the HODLR term when the tile's
-// child rows x cols rectangle lies inside one low-rank block. Per entry the
-// arithmetic is exactly k_sample's: seed, then per child in order
-// sub = (HODLR or dense entry) - (u-ascending FMA chain of W[cr,u] Vt[u,cc]),
-// v = v + sub (the HODLR low-rank entry is itself a t-ascending FMA chain).
-constexpr int RB_T = 64, RB_K = 16;
+// low-rank update W Vt of meaningful rank: 64 x 64 tiles, 256 threads. The
+// rank-r dot products run on the FP64 tensor cores (mma.sync m8n8k4): warp w
+// owns a 16 x 32 sub-tile (two 8-row by four 8-column MMA tiles), the factors
+// stream through shared memory in 16-wide chunks (next chunk prefetched into
+// registers). An m8n8k4 FP64 MMA equals the k-ascending FMA chain bit for bit
+// (scripts/probe/dmma_order.cu: 0 differences in 1.28M entries on B200), so
+// per entry the arithmetic is exactly k_sample's: seed, then per child in
+// order sub = (HODLR or dense entry) - (u-ascending FMA chain of W[cr,u]
+// Vt[u,cc]), v = v + sub (the HODLR low-rank entry is itself a t-ascending
+// FMA chain). The W Vt term always uses the MMA path, the HODLR term when the
+// tile's child rows x cols rectangle lies inside one low-rank block.
+constexpr int RB_T = 64, RB_K = 16, RB_LD = RB_T + 4;  // RB_LD: conflict-free fragment loads
 constexpr size_t RB_DYN = sizeof(double) * RB_T * (RB_T + 1);
 
-// acc[a][b] = sum_u X[sx[row_a], u] * Y[u, sy[col_b]] (u ascending from 0);
-// rows / cols with index -1 contribute zero
-__device__ __forceinline__ void rb_dot(double (&acc)[4][4], const double *__restrict__ X, int ldx,
-                                       const int *sx, const double *__restrict__ Y, int ldy, const int *sy, int K,
-                                       double (*Ws)[RB_T + 1], double (*Vs)[RB_T], int tid, int tx, int ty) {
+// thread entry (a, b), a in {0, 1}, b in 0..7: tile row / column
+__device__ __forceinline__ int rb_row(int a, int wr, int g) { return 16 * wr + 8 * a + g; }
+__device__ __forceinline__ int rb_col(int b, int wc, int q) { return 32 * wc + 8 * (b >> 1) + 2 * q + (b & 1); }
+
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// acc[a][b] = sum_u X[sx[row], u] * Y[u, sy[col]] (u ascending from 0) for the
+// thread's entries; rows / cols with index -1 contribute zero
+__device__ __forceinline__ void rb_dot(double (&acc)[2][8], const double *__restrict__ X, int ldx, const int *sx,
+                                       const double *__restrict__ Y, int ldy, const int *sy, int K,
+                                       double (*Ws)[RB_LD], double (*Vs)[RB_LD], int tid, int wr, int wc, int g,
+                                       int q) {
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
   double pw[4], pv[4];
   auto fetch = [&](int u0) {
     const int kc = min(RB_K, K - u0);
@@ -287,7 +301,6 @@ __device__ __forceinline__ void rb_dot(double (&acc)[4][4], const double *__rest
   };
   fetch(0);
   for (int u0 = 0; u0 < K; u0 += RB_K) {
-    const int kc = min(RB_K, K - u0);
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
       const int e = tid + 256 * m;
@@ -295,21 +308,20 @@ __device__ __forceinline__ void rb_dot(double (&acc)[4][4], const double *__rest
       Vs[e >> 6][e & 63] = pv[m];
     }
     __syncthreads();
-    if (u0 + RB_K < K) fetch(u0 + RB_K);  // in flight during the FMAs
-    // full, unrolled chunk: padded ranks are zeros in both operands and
-    // fma(0, 0, acc) == acc, so the result is unchanged and the loads pipeline
-    (void)kc;
+    if (u0 + RB_K < K) fetch(u0 + RB_K);  // in flight during the MMAs
+    // full chunk: padded ranks are zeros in both operands and fma(0, 0, acc)
+    // == acc, so the chain is unchanged
 #pragma unroll
-    for (int k = 0; k < RB_K; ++k) {
-      double w[4], x[4];
+    for (int kb = 0; kb < RB_K / 4; ++kb) {
+      double fa[2], fb[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) w[a] = Ws[k][ty + 16 * a];
+      for (int a = 0; a < 2; ++a) fa[a] = Ws[4 * kb + q][16 * wr + 8 * a + g];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) x[b] = Vs[k][tx + 16 * b];
+      for (int j = 0; j < 4; ++j) fb[j] = Vs[4 * kb + q][32 * wc + 8 * j + g];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(w[a], x[b], acc[a][b]);
+        for (int j = 0; j < 4; ++j) dmma884(acc[a][2 * j], acc[a][2 * j + 1], fa[a], fb[j]);
     }
     __syncthreads();
   }
@@ -321,14 +333,15 @@ __global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs
                                                    const long long *__restrict__ Ap_ptr,
                                                    const int *__restrict__ Ap_col,
                                                    const double *__restrict__ Ap_val) {
-  __shared__ double Ws[RB_K][RB_T + 1];
-  __shared__ double Vs[RB_K][RB_T];
+  __shared__ double Ws[RB_K][RB_LD];
+  __shared__ double Vs[RB_K][RB_LD];
   __shared__ int s_r[RB_T], s_c[RB_T], s_cr[RB_T], s_cc[RB_T], s_br[RB_T], s_bc[RB_T];
   __shared__ const HBlk *s_blk;
   __shared__ int s_rlo, s_clo;
   extern __shared__ double rb_dyn[];  // running entry values s_v[RB_T][RB_T + 1] (keeps registers for the dots)
   double(*s_v)[RB_T + 1] = reinterpret_cast<double(*)[RB_T + 1]>(rb_dyn);
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp >> 1, wc = warp & 1, g = lane >> 2, q = lane & 3;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int2 tl = tiles[t];
     const SReq rq = reqs[tl.x];
@@ -344,16 +357,17 @@ __global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs
     }
     __syncthreads();
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int r = s_r[ty + 16 * a], c = s_c[tx + 16 * b];
-        s_v[ty + 16 * a][tx + 16 * b] = (r >= 0 && c >= 0 && (r < F.npv || c < F.npv))
-                                            ? seed_entry(Ap_ptr, Ap_col, Ap_val, F.ids[r], F.ids[c])
-                                            : 0.0;
+      for (int b = 0; b < 8; ++b) {
+        const int ra = rb_row(a, wr, g), cb = rb_col(b, wc, q);
+        const int r = s_r[ra], c = s_c[cb];
+        s_v[ra][cb] = (r >= 0 && c >= 0 && (r < F.npv || c < F.npv))
+                          ? seed_entry(Ap_ptr, Ap_col, Ap_val, F.ids[r], F.ids[c])
+                          : 0.0;
       }
-    for (int q = F.child_begin; q < F.child_end; ++q) {
-      const DChild &ch = kids[q];
+    for (int qq = F.child_begin; qq < F.child_end; ++qq) {
+      const DChild &ch = kids[qq];
       if (tid < RB_T) {
         int r = s_r[tid];
         s_cr[tid] = r >= 0 ? ch.to_child[r] : -1;
@@ -393,7 +407,7 @@ __global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs
         __syncthreads();
         uni = s_blk != nullptr;
       }
-      double sub[4][4];
+      double sub[2][8];
       if (uni) {
         const HBlk B = *s_blk;
         if (tid < RB_T) {
@@ -404,13 +418,13 @@ __global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs
           s_bc[tid - RB_T] = y >= 0 ? y - s_clo : -1;
         }
         __syncthreads();
-        rb_dot(sub, B.a, B.lda, s_br, B.b, B.ldb, s_bc, B.rank, Ws, Vs, tid, tx, ty);
+        rb_dot(sub, B.a, B.lda, s_br, B.b, B.ldb, s_bc, B.rank, Ws, Vs, tid, wr, wc, g, q);
       } else {
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < 2; ++a)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int cr = s_cr[ty + 16 * a], cc = s_cc[tx + 16 * b];
+          for (int b = 0; b < 8; ++b) {
+            const int cr = s_cr[rb_row(a, wr, g)], cc = s_cc[rb_col(b, wc, q)];
             double x = 0.0;
             if (cr >= 0 && cc >= 0)
               x = ch.kind == 0 ? ch.dense[(long long)cr * ch.ldd + cc] : hodlr_entry(ch.hn, ch.n, cr, cc);
@@ -418,27 +432,29 @@ __global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs
           }
       }
       if (ch.kind == 1 && ch.rw) {
-        double acc[4][4];
-        rb_dot(acc, ch.W, ch.ldw, s_cr, ch.Vt, ch.ldv, s_cc, ch.rw, Ws, Vs, tid, tx, ty);
+        double acc[2][8];
+        rb_dot(acc, ch.W, ch.ldw, s_cr, ch.Vt, ch.ldv, s_cc, ch.rw, Ws, Vs, tid, wr, wc, g, q);
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < 2; ++a)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) sub[a][b] = sub[a][b] - acc[a][b];
+          for (int b = 0; b < 8; ++b) sub[a][b] = sub[a][b] - acc[a][b];
       }
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-          if (s_cr[ty + 16 * a] >= 0 && s_cc[tx + 16 * b] >= 0)
-            s_v[ty + 16 * a][tx + 16 * b] = s_v[ty + 16 * a][tx + 16 * b] + sub[a][b];
+        for (int b = 0; b < 8; ++b) {
+          const int ra = rb_row(a, wr, g), cb = rb_col(b, wc, q);
+          if (s_cr[ra] >= 0 && s_cc[cb] >= 0) s_v[ra][cb] = s_v[ra][cb] + sub[a][b];
+        }
       __syncthreads();  // s_cr / s_cc / s_blk are rewritten for the next child
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int i = bi + ty + 16 * a, j = bj + tx + 16 * b;
-        if (i < rq.nr && j < rq.nc) rq.out[(long long)i * rq.ld + j] = s_v[ty + 16 * a][tx + 16 * b];
+      for (int b = 0; b < 8; ++b) {
+        const int ra = rb_row(a, wr, g), cb = rb_col(b, wc, q);
+        const int i = bi + ra, j = bj + cb;
+        if (i < rq.nr && j < rq.nc) rq.out[(long long)i * rq.ld + j] = s_v[ra][cb];
       }
     __syncthreads();  // s_r / s_c are rewritten for the next tile
   }

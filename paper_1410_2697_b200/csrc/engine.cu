@@ -1605,57 +1605,73 @@ struct Factorizer {
       if (hfr) push_fronts({});
       return;
     }
-    std::vector<int2> tiles, tiles_rb;
+    // per class: the requests and their tile prefix (the kernels decode tile t
+    // by a binary search; no per-tile descriptors from the host)
+    std::vector<int> rid[2];
+    std::vector<long long> pre[2] = {{0}, {0}};
     for (int q = 0; q < (int)reqs.size(); ++q) {
       const bool rb = reqs[q].front < (int)slot_rw.size() && slot_rw[reqs[q].front] >= RB_MIN_RANK;
-      int64_t nt = rb ? cdiv(reqs[q].nr, RB_T) * cdiv(reqs[q].nc, RB_T)
-                      : cdiv(reqs[q].nr, SAMPLE_TR) * cdiv(reqs[q].nc, SAMPLE_TC);
-      for (int64_t t = 0; t < nt; ++t) (rb ? tiles_rb : tiles).push_back(make_int2(q, (int)t));
+      const int64_t nt = rb ? cdiv(reqs[q].nr, RB_T) * cdiv(reqs[q].nc, RB_T)
+                            : cdiv(reqs[q].nr, SAMPLE_TR) * cdiv(reqs[q].nc, SAMPLE_TC);
       F->timing.sample_entries += (double)reqs[q].nr * reqs[q].nc;
+      if (nt == 0) continue;
+      rid[rb].push_back(q);
+      pre[rb].push_back(pre[rb].back() + nt);
     }
-    if (tiles.empty() && tiles_rb.empty()) {
+    if (rid[0].empty() && rid[1].empty()) {
       if (hfr) push_fronts({});
       return;
     }
     SReq *dr;
-    int2 *dt_plain = nullptr, *dt_rb = nullptr;
+    int *drid[2];
+    long long *dpre[2];
+    auto bytes_of = [](const auto &v) { return v.size() * sizeof(v[0]); };
     if (hfr) {
       auto p = push_fronts({{reqs.data(), reqs.size() * sizeof(SReq)},
-                            {tiles.data(), tiles.size() * sizeof(int2)},
-                            {tiles_rb.data(), tiles_rb.size() * sizeof(int2)}});
+                            {rid[0].data(), bytes_of(rid[0])},
+                            {pre[0].data(), bytes_of(pre[0])},
+                            {rid[1].data(), bytes_of(rid[1])},
+                            {pre[1].data(), bytes_of(pre[1])}});
       dr = (SReq *)p[2];
-      dt_plain = (int2 *)p[3];
-      dt_rb = (int2 *)p[4];
+      drid[0] = (int *)p[3];
+      dpre[0] = (long long *)p[4];
+      drid[1] = (int *)p[5];
+      dpre[1] = (long long *)p[6];
     } else {
-      dr = s.push(reqs);
-      if (!tiles.empty()) dt_plain = s.push(tiles);
-      if (!tiles_rb.empty()) dt_rb = s.push(tiles_rb);
+      auto p = s.push_keep_many({{reqs.data(), reqs.size() * sizeof(SReq)},
+                                 {rid[0].data(), bytes_of(rid[0])},
+                                 {pre[0].data(), bytes_of(pre[0])},
+                                 {rid[1].data(), bytes_of(rid[1])},
+                                 {pre[1].data(), bytes_of(pre[1])}});
+      dr = (SReq *)p[0];
+      drid[0] = (int *)p[1];
+      dpre[0] = (long long *)p[2];
+      drid[1] = (int *)p[3];
+      dpre[1] = (long long *)p[4];
     }
     DFront *fF = dF;
     DChild *fC = dC;
     long long *pp = d_ap_ptr;
     int *pc = d_ap_col;
     double *pv = d_ap_val;
-    if (!tiles.empty()) {
-      int2 *dt = dt_plain;
-      int nt = (int)tiles.size();
-      int grid = std::min(nt, 148 * 32);
+    if (!rid[0].empty()) {
+      SampleTiles T{drid[0], dpre[0], (int)rid[0].size(), pre[0].back()};
+      int grid = (int)std::min<int64_t>(T.ntiles, 148 * 32);
       s.launch([=](cudaStream_t st) {
-        k_sample<<<grid, dim3(SAMPLE_TC, SAMPLE_TR), 0, st>>>(dr, dt, nt, fF, fC, pp, pc, pv);
+        k_sample<<<grid, dim3(SAMPLE_TC, SAMPLE_TR), 0, st>>>(dr, T, fF, fC, pp, pc, pv);
         check_launch();
       });
     }
-    if (!tiles_rb.empty()) {
-      int2 *dt = dt_rb;
-      int nt = (int)tiles_rb.size();
-      int grid = std::min(nt, 148 * 8);
+    if (!rid[1].empty()) {
+      SampleTiles T{drid[1], dpre[1], (int)rid[1].size(), pre[1].back()};
+      int grid = (int)std::min<int64_t>(T.ntiles, 148 * 8);
       static bool attr = false;
       if (!attr) {
         CK(cudaFuncSetAttribute(k_sample_rb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RB_DYN));
         attr = true;
       }
       s.launch([=](cudaStream_t st) {
-        k_sample_rb<<<grid, 256, RB_DYN, st>>>(dr, dt, nt, fF, fC, pp, pc, pv);
+        k_sample_rb<<<grid, 256, RB_DYN, st>>>(dr, T, fF, fC, pp, pc, pv);
         check_launch();
       });
     }

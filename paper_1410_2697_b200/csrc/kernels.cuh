@@ -175,12 +175,32 @@ __device__ __forceinline__ double seed_entry(const long long *Ap_ptr, const int 
 // ---------------------------------------------------------------------------
 constexpr int SAMPLE_TR = 8, SAMPLE_TC = 32;
 
-__global__ void k_sample(const SReq *__restrict__ reqs, const int2 *__restrict__ tiles, int ntiles,
+// Tile t of a sampling batch: request rids[p] with tpre[p] <= t < tpre[p + 1]
+// (the host sends the per-request tile prefix, not one descriptor per tile)
+struct SampleTiles {
+  const int *rids;
+  const long long *tpre;
+  int nr;
+  long long ntiles;
+};
+__device__ __forceinline__ int2 sample_tile(const SampleTiles &T, long long t) {
+  int lo = 0, hi = T.nr - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (T.tpre[mid] <= t)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return make_int2(T.rids[lo], (int)(t - T.tpre[lo]));
+}
+
+__global__ void k_sample(const SReq *__restrict__ reqs, SampleTiles tiles,
                          const DFront *__restrict__ fronts, const DChild *__restrict__ kids,
                          const long long *__restrict__ Ap_ptr, const int *__restrict__ Ap_col,
                          const double *__restrict__ Ap_val) {
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    int2 tl = tiles[t];
+  for (long long t = blockIdx.x; t < tiles.ntiles; t += gridDim.x) {
+    const int2 tl = sample_tile(tiles, t);
     const SReq rq = reqs[tl.x];
     int tpr = (rq.nc + SAMPLE_TC - 1) / SAMPLE_TC;
     int i = (tl.y / tpr) * SAMPLE_TR + threadIdx.y;
@@ -327,8 +347,8 @@ __device__ __forceinline__ void rb_dot(double (&acc)[2][8], const double *__rest
   }
 }
 
-__global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs, const int2 *__restrict__ tiles,
-                                                   int ntiles, const DFront *__restrict__ fronts,
+__global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs, SampleTiles tiles,
+                                                   const DFront *__restrict__ fronts,
                                                    const DChild *__restrict__ kids,
                                                    const long long *__restrict__ Ap_ptr,
                                                    const int *__restrict__ Ap_col,
@@ -342,8 +362,8 @@ __global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs
   double(*s_v)[RB_T + 1] = reinterpret_cast<double(*)[RB_T + 1]>(rb_dyn);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wr = warp >> 1, wc = warp & 1, g = lane >> 2, q = lane & 3;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int2 tl = tiles[t];
+  for (long long t = blockIdx.x; t < tiles.ntiles; t += gridDim.x) {
+    const int2 tl = sample_tile(tiles, t);
     const SReq rq = reqs[tl.x];
     const int tpr = (rq.nc + RB_T - 1) / RB_T;
     const int bi = (tl.y / tpr) * RB_T, bj = (tl.y % tpr) * RB_T;

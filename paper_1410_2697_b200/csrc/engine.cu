@@ -269,6 +269,7 @@ struct Ctx {
   int64_t launches = 0;      // launches of this library's kernels
   int64_t lib_calls = 0;     // cuBLAS DGEMM calls (plain large GEMMs)
   cublasHandle_t blas = nullptr;
+  void *blas_ws = nullptr;  // cuBLAS workspace (set once with the stream)
   // device copies of per-tree extend-add maps and front id lists, keyed by etree uid
   std::vector<std::pair<uint64_t, int *>> map_dev;
   std::vector<std::pair<uint64_t, long long *>> ids_dev;
@@ -392,6 +393,36 @@ static void check_launch() {
 // Batched GEMM dispatch: large plain GEMMs (>= 2^27 flops, both sides >= 64,
 // C not aliasing A or B) go to cuBLAS DGEMM (FP64 tensor cores); the many
 // small / aliased ones to the batched tile kernel k_gemm.
+// Per-operation host clock (MFH_OP_TRACE=1; with CUDA_LAUNCH_BLOCKING=1 the
+// host time of an operation is its GPU time): where a factorization goes.
+struct OpClock {
+  static std::map<std::string, std::pair<double, int64_t>> &table() {
+    static std::map<std::string, std::pair<double, int64_t>> t;
+    return t;
+  }
+  static bool on() {
+    static const bool o = getenv("MFH_OP_TRACE") != nullptr;
+    return o;
+  }
+  const char *name;
+  std::chrono::steady_clock::time_point t0;
+  explicit OpClock(const char *n) : name(n), t0(std::chrono::steady_clock::now()) {}
+  ~OpClock() {
+    if (!on()) return;
+    auto &e = table()[name];
+    e.first += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    e.second++;
+  }
+  static void dump() {
+    if (!on()) return;
+    for (auto &kv : table())
+      fprintf(stderr, "[mfh op] %-18s %10.1f ms %8lld calls\n", kv.first.c_str(), kv.second.first,
+              (long long)kv.second.second);
+  }
+};
+// host-side time spent in library GEMM calls (MFH_HEIGHT_TRACE diagnostics)
+static double g_blas_host_ms = 0.0;
+static int64_t g_blas_calls = 0;
 static bool gemm_overlaps(const GemmJob &g) {
   auto span = [](const double *p, int rows, int cols, int ld) {
     return std::make_pair(p, p + (int64_t)(rows - 1) * ld + cols);
@@ -404,6 +435,7 @@ static bool gemm_overlaps(const GemmJob &g) {
 }
 
 static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
+  OpClock oc_("gemm");
   if (jobs.empty()) return;
   std::vector<int4> tiles;
   std::vector<GemmJob> big;
@@ -423,8 +455,22 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
     Ctx *ctx = sk.ctx;
     if (!ctx->blas) {
       if (cublasCreate(&ctx->blas) != CUBLAS_STATUS_SUCCESS) throw runtime_error("cublasCreate failed");
+      // stream and a fixed workspace once per handle: cublasSetStream resets
+      // the workspace, so calling it per launch batch re-provisions it
+      if (cublasSetStream(ctx->blas, ctx->s) != CUBLAS_STATUS_SUCCESS) throw runtime_error("cublasSetStream failed");
+      const size_t ws = size_t(32) << 20;
+      CK(cudaMalloc(&ctx->blas_ws, ws));
+      if (cublasSetWorkspace(ctx->blas, ctx->blas_ws, ws) != CUBLAS_STATUS_SUCCESS)
+        throw runtime_error("cublasSetWorkspace failed");
     }
-    if (cublasSetStream(ctx->blas, ctx->s) != CUBLAS_STATUS_SUCCESS) throw runtime_error("cublasSetStream failed");
+    auto tb0 = std::chrono::steady_clock::now();
+    g_blas_calls += (int64_t)big.size();
+    struct BlasClock {
+      std::chrono::steady_clock::time_point t0;
+      ~BlasClock() {
+        g_blas_host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      }
+    } bclk{tb0};
     for (const GemmJob &g : big) {
       // row-major C = alpha A B + beta C  ==  column-major C^T = alpha B^T A^T + beta C^T
       double al = g.alpha, be = g.beta;
@@ -449,6 +495,7 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
 // (k_trinv), then B <- T^{-1} B as an in-place GEMM (safe: m = w fits one
 // 64-row GEMM tile, so every CTA reads its whole column strip before writing)
 static void run_trsm(Sink &sk, const std::vector<TrsmJob> &jobs) {
+  OpClock oc_("trsm");
   if (jobs.empty()) return;
   std::vector<TrinvJob> ti;
   std::vector<GemmJob> gm;
@@ -476,6 +523,7 @@ static void run_trsm(Sink &sk, const std::vector<TrsmJob> &jobs) {
 constexpr int BIG_N = INV_SMALL;  // above this, LU / solves run blocked across the GPU
 
 static void run_laswp(Sink &sk, const std::vector<SwapJob> &jobs) {
+  OpClock oc_("laswp");
   for (size_t b = 0; b < jobs.size(); b += 60000) {
     std::vector<SwapJob> part(jobs.begin() + b, jobs.begin() + std::min(jobs.size(), b + 60000));
     int mx = 1;
@@ -490,6 +538,7 @@ static void run_laswp(Sink &sk, const std::vector<SwapJob> &jobs) {
 }
 
 static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
+  OpClock oc_("getrf");
   if (jobs.empty()) return;
   std::vector<LuJob> small, big;
   for (auto &j : jobs) (j.n > BIG_N ? big : small).push_back(j);
@@ -591,6 +640,7 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
 }
 
 static void run_check_finite(Sink &sk, const std::vector<LuJob> &jobs) {
+  OpClock oc_("check_finite");
   if (jobs.empty()) return;
   int64_t mx = 1;
   for (auto &j : jobs) mx = std::max<int64_t>(mx, (int64_t)j.n * j.n);
@@ -620,6 +670,7 @@ struct TriInvReq {
   double *out;
 };
 static void run_tri_inv(Sink &sk, const std::vector<TriInvReq> &reqs) {
+  OpClock oc_("tri_inv");
   if (reqs.empty()) return;
   static bool attr = false;
   if (!attr) {
@@ -688,6 +739,7 @@ static void run_identity(Sink &sk, const std::vector<double *> &ptrs, const std:
 // explicit inverses: in-shared-memory Gauss-Jordan for n <= 128, blocked LU +
 // GEMM-based solve against the identity above that
 static void run_inverse(Sink &sk, const std::vector<InvReq> &reqs) {
+  OpClock oc_("inverse");
   if (reqs.empty()) return;
   std::vector<InvJob> small;
   std::vector<CopyJob> cps;
@@ -756,6 +808,7 @@ static void run_inverse(Sink &sk, const std::vector<InvReq> &reqs) {
 }
 
 static void run_copy(Sink &sk, const std::vector<CopyJob> &jobs) {
+  OpClock oc_("copy");
   for (size_t b = 0; b < jobs.size(); b += 60000) {
     std::vector<CopyJob> part(jobs.begin() + b, jobs.begin() + std::min(jobs.size(), b + 60000));
     int64_t mx = 0;
@@ -818,6 +871,7 @@ static void launch_cluster(const void *fn, int ncores, int cs, size_t smem, cuda
 // run the cluster / cooperative cores
 static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
                     const std::function<void()> &main_work = nullptr) {
+  OpClock oc_("plu");
   if (jobs.empty()) {
     if (main_work) main_work();
     return;
@@ -1592,6 +1646,7 @@ struct Factorizer {
   // transfer as the requests and tiles, and dF / dC are set
   void run_sample(Sink &s, const std::vector<SReq> &reqs, DFront *&dF, DChild *&dC,
                   const std::vector<DFront> *hfr = nullptr, const std::vector<DChild> *hch = nullptr) {
+    OpClock oc_("sample");
     auto push_fronts = [&](std::vector<std::pair<const void *, size_t>> extra) {
       std::vector<std::pair<const void *, size_t>> parts{{hfr->data(), hfr->size() * sizeof(DFront)},
                                                         {hch->data(), hch->size() * sizeof(DChild)}};
@@ -2895,6 +2950,11 @@ struct Factorizer {
     check_flags(0);
     ctx->scratch.reset();
     const bool htrace = getenv("MFH_HEIGHT_TRACE") != nullptr;
+    if (htrace) {
+      fprintf(stderr, "[mfh blas] %lld cuBLAS DGEMM calls, %.1f ms host time in them (cumulative)\n",
+              (long long)g_blas_calls, g_blas_host_ms);
+    }
+    OpClock::dump();
     for (int u = 0; u < used; ++u) {
       cudaEvent_t *ev = ctx->evpool.data() + 8 * u;
       const bool donly = struct_of_use[u] == 0;
@@ -3596,6 +3656,7 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   cudaFree(ctx->c.d_part);
   cudaFree(ctx->c.d_scal);
   if (ctx->c.blas) cublasDestroy(ctx->c.blas);
+  if (ctx->c.blas_ws) cudaFree(ctx->c.blas_ws);
   for (auto &m : ctx->c.map_dev) cudaFree(m.second);
   for (auto &m : ctx->c.ids_dev) cudaFree(m.second);
   for (auto &q : ctx->c.pat_dev) {

@@ -423,33 +423,62 @@ struct OpClock {
 // host-side time spent in library GEMM calls (MFH_HEIGHT_TRACE diagnostics)
 static double g_blas_host_ms = 0.0;
 static int64_t g_blas_calls = 0;
+// Do C and A (or B) share an element? Row-major blocks inside one buffer with
+// the same leading dimension (e.g. F_ff and F_fp of one front) are tested
+// exactly on the row/column lattice; anything else by address span.
+static bool blocks_overlap(const double *p, int rows, int cols, int ld, const double *q, int rows2, int cols2,
+                           int ld2) {
+  const double *pe = p + (int64_t)(rows - 1) * ld + cols, *qe = q + (int64_t)(rows2 - 1) * ld2 + cols2;
+  if (!(p < qe && q < pe)) return false;
+  if (ld != ld2 || cols > ld || cols2 > ld) return true;
+  const int64_t d = q - p;
+  const int64_t c = ((d % ld) + ld) % ld, r0 = (d - c) / ld;
+  if (c + cols2 > ld) return true;
+  const bool rows_hit = r0 < rows && 0 < r0 + rows2;
+  const bool cols_hit = c < cols && 0 < c + cols2;
+  return rows_hit && cols_hit;
+}
 static bool gemm_overlaps(const GemmJob &g) {
-  auto span = [](const double *p, int rows, int cols, int ld) {
-    return std::make_pair(p, p + (int64_t)(rows - 1) * ld + cols);
-  };
-  auto c = span(g.C, g.m, g.n, g.ldc), a = span(g.A, g.m, g.k, g.lda), b = span(g.B, g.k, g.n, g.ldb);
-  auto hit = [](std::pair<const double *, const double *> x, std::pair<const double *, const double *> y) {
-    return x.first < y.second && y.first < x.second;
-  };
-  return hit(c, a) || hit(c, b);
+  return blocks_overlap(g.C, g.m, g.n, g.ldc, g.A, g.m, g.k, g.lda) ||
+         blocks_overlap(g.C, g.m, g.n, g.ldc, g.B, g.k, g.n, g.ldb);
 }
 
 static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
   OpClock oc_("gemm");
   if (jobs.empty()) return;
-  std::vector<int4> tiles;
+  std::vector<GemmTile> tiles;
   std::vector<GemmJob> big;
+  std::vector<GemmSplit> splits;
+  int nslot = 0;
+  auto is_big = [&](const GemmJob &g) {
+    return !sk.record && g.k > 0 && g.m >= 64 && g.n >= 64 && 2.0 * g.m * g.n * g.k >= (double)(1 << 27) &&
+           !gemm_overlaps(g);
+  };
   for (int j = 0; j < (int)jobs.size(); ++j) {
     const GemmJob &g = jobs[j];
     if (g.m <= 0 || g.n <= 0) continue;
-    if (!sk.record && g.k > 0 && g.m >= 64 && g.n >= 64 && 2.0 * g.m * g.n * g.k >= (double)(1 << 27) &&
-        !gemm_overlaps(g)) {
+    if (is_big(g)) {
       big.push_back(g);
       continue;
     }
     int tm = (int)cdiv(g.m, GEMM_BM), tn = (int)cdiv(g.n, GEMM_BN);
+    // split-K (a rule of the job alone): <= 32 output tiles and k >= 256 ->
+    // k chunks of 128, partials summed in order by k_gemm_reduce
+    static const int split_k = getenv("MFH_GEMM_SPLIT_K") ? atoi(getenv("MFH_GEMM_SPLIT_K")) : 128;
+    const int ns = (split_k > 0 && !sk.record && g.k >= 2 * split_k && tm * tn <= 32 && !gemm_overlaps(g))
+                       ? (int)cdiv(g.k, split_k)
+                       : 1;
     for (int a = 0; a < tm; ++a)
-      for (int b = 0; b < tn; ++b) tiles.push_back(make_int4(j, a, b, 0));
+      for (int b = 0; b < tn; ++b) {
+        if (ns == 1) {
+          tiles.push_back(GemmTile{j, a, b, 0, std::max(g.k, 0), -1});
+          continue;
+        }
+        splits.push_back(GemmSplit{j, a, b, nslot, ns});
+        for (int q = 0; q < ns; ++q)
+          tiles.push_back(GemmTile{j, a, b, q * split_k, std::min(g.k, (q + 1) * split_k), nslot + q});
+        nslot += ns;
+      }
   }
   if (!big.empty()) {
     Ctx *ctx = sk.ctx;
@@ -481,12 +510,28 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
     }
   }
   if (tiles.empty()) return;
+  static const bool glog = getenv("MFH_GEMM_LOG") != nullptr;
+  if (glog) {
+    int64_t fl = 0;
+    int kmax = 0, ov = 0;
+    for (auto &g : jobs) {
+      fl += 2ll * g.m * g.n * g.k;
+      kmax = std::max(kmax, g.k);
+      ov += gemm_overlaps(g);
+    }
+    fprintf(stderr, "[gemm] jobs %zu tiles %zu splits %zu kmax %d overlap %d gflop %.4f first m%d n%d k%d\n",
+            jobs.size(), tiles.size(), splits.size(), kmax, ov, fl * 1e-9, jobs[0].m, jobs[0].n, jobs[0].k);
+  }
   GemmJob *dj = sk.push(jobs);
-  int4 *dt = sk.push(tiles);
-  int nt = (int)tiles.size();
+  GemmTile *dt = sk.push(tiles);
+  GemmSplit *dsp = splits.empty() ? nullptr : sk.push(splits);
+  double *dws = nslot ? sk.scratch_d((size_t)nslot * GEMM_BM * GEMM_BN) : nullptr;
+  int nt = (int)tiles.size(), nsp = (int)splits.size();
   int grid = std::min(nt, 148 * 16);
   sk.launch([=](cudaStream_t s) {
-    k_gemm<<<grid, 256, 0, s>>>(dj, dt, nt);
+    k_gemm<<<grid, 256, 0, s>>>(dj, dt, nt, dws);
+    check_launch();
+    if (nsp) k_gemm_reduce<<<nsp, 256, 0, s>>>(dj, dsp, dws);
     check_launch();
   });
 }

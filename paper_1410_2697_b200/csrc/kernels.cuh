@@ -509,44 +509,73 @@ __global__ void k_identity(double *const *__restrict__ ptrs, const int *__restri
 }
 
 // ---------------------------------------------------------------------------
-// vbatched GEMM, NN, row-major: 64x64 tiles, BK 16, 256 threads, 4x4 per thread
+// vbatched GEMM, NN, row-major: 64x64 tiles, BK 16, 256 threads, 4x4 per thread.
+// Deterministic split-K for jobs with few output tiles and a long k (a rule of
+// the job's own (m, n, k), so a job's bits never depend on what else is in
+// the batch; the sharded factorization relies on that): each split tile
+// writes its partial (valid rows/columns only) to a workspace slot, and
+// k_gemm_reduce sums the partials in split order 0..S-1 and applies
+// alpha/beta. The main loop carries no fences or atomics, so its A/B tile
+// loads stay L1-cached.
 // ---------------------------------------------------------------------------
 constexpr int GEMM_BM = 64, GEMM_BN = 64, GEMM_BK = 16;
 
-__global__ void __launch_bounds__(256) k_gemm(const GemmJob *__restrict__ jobs,
-                                              const int4 *__restrict__ tiles, int ntiles) {
+struct GemmTile {
+  int job, mt, nt, k0, k1;
+  int ws;  // split-K: workspace slot of this partial, -1 = write C directly
+};
+
+struct GemmSplit {  // one split output tile: partials ws .. ws+ns-1
+  int job, mt, nt, ws, ns;
+};
+
+__global__ void __launch_bounds__(256, 3) k_gemm(const GemmJob *__restrict__ jobs,
+                                              const GemmTile *__restrict__ tiles, int ntiles,
+                                              double *__restrict__ ws) {
   __shared__ double As[GEMM_BK][GEMM_BM + 1];
   __shared__ double Bs[GEMM_BK][GEMM_BN];
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    int4 tl = tiles[t];
-    const GemmJob J = jobs[tl.x];
-    const int m0 = tl.y * GEMM_BM, n0 = tl.z * GEMM_BN;
+    const GemmTile tl = tiles[t];
+    const GemmJob J = jobs[tl.job];
+    const int m0 = tl.mt * GEMM_BM, n0 = tl.nt * GEMM_BN;
+    const int k1 = tl.k1;
     double acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-    for (int k0 = 0; k0 < J.k; k0 += GEMM_BK) {
-      // A tile: 64 rows x 16 k
+    // register prefetch: the next k slab's global loads are in flight while
+    // the current slab is multiplied out of shared memory (same FMA order)
+    double ra[4], rb[4];
+    auto load_slab = [&](int k0) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 4; ++q) {  // A: 64 rows x 16 k
         int e = tid + q * 256;
         int mm = e >> 4, kk = e & 15;
         int gm = m0 + mm, gk = k0 + kk;
-        As[kk][mm] = (gm < J.m && gk < J.k) ? J.A[(long long)gm * J.lda + gk] : 0.0;
+        ra[q] = (gm < J.m && gk < k1) ? J.A[(long long)gm * J.lda + gk] : 0.0;
       }
-      // B tile: 16 k x 64 cols
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 4; ++q) {  // B: 16 k x 64 cols
         int e = tid + q * 256;
         int kk = e >> 6, nn = e & 63;
         int gk = k0 + kk, gn = n0 + nn;
-        Bs[kk][nn] = (gk < J.k && gn < J.n) ? J.B[(long long)gk * J.ldb + gn] : 0.0;
+        rb[q] = (gk < k1 && gn < J.n) ? J.B[(long long)gk * J.ldb + gn] : 0.0;
+      }
+    };
+    if (tl.k0 < k1) load_slab(tl.k0);
+    for (int k0 = tl.k0; k0 < k1; k0 += GEMM_BK) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int e = tid + q * 256;
+        As[e & 15][e >> 4] = ra[q];
+        Bs[e >> 6][e & 63] = rb[q];
       }
       __syncthreads();
-      int kc = min(GEMM_BK, J.k - k0);
+      if (k0 + GEMM_BK < k1) load_slab(k0 + GEMM_BK);
+      int kc = min(GEMM_BK, k1 - k0);
       for (int kk = 0; kk < kc; ++kk) {
         double a[4], b[4];
 #pragma unroll
@@ -560,6 +589,7 @@ __global__ void __launch_bounds__(256) k_gemm(const GemmJob *__restrict__ jobs,
       }
       __syncthreads();
     }
+    double *part = tl.ws >= 0 ? ws + (long long)tl.ws * (GEMM_BM * GEMM_BN) : nullptr;
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
       int gm = m0 + ty + 16 * p;
@@ -568,11 +598,35 @@ __global__ void __launch_bounds__(256) k_gemm(const GemmJob *__restrict__ jobs,
       for (int q = 0; q < 4; ++q) {
         int gn = n0 + tx + 16 * q;
         if (gn >= J.n) continue;
+        if (part) {
+          part[(ty + 16 * p) * GEMM_BN + tx + 16 * q] = acc[p][q];
+          continue;
+        }
         double *c = J.C + (long long)gm * J.ldc + gn;
         double v = J.alpha * acc[p][q];
         *c = (J.beta == 0.0) ? v : J.beta * (*c) + v;
       }
     }
+  }
+}
+
+// split-K epilogue: C = alpha * (((p0 + p1) + p2) + ...) + beta * C
+__global__ void __launch_bounds__(256) k_gemm_reduce(const GemmJob *__restrict__ jobs,
+                                                     const GemmSplit *__restrict__ splits,
+                                                     const double *__restrict__ ws) {
+  const GemmSplit sp = splits[blockIdx.x];
+  const GemmJob J = jobs[sp.job];
+  const int m0 = sp.mt * GEMM_BM, n0 = sp.nt * GEMM_BN;
+  const double *w0 = ws + (long long)sp.ws * (GEMM_BM * GEMM_BN);
+  for (int e = threadIdx.x; e < GEMM_BM * GEMM_BN; e += blockDim.x) {
+    int r = e >> 6, c = e & 63;
+    int gm = m0 + r, gn = n0 + c;
+    if (gm >= J.m || gn >= J.n) continue;
+    double v = w0[e];
+    for (int s = 1; s < sp.ns; ++s) v += w0[(long long)s * (GEMM_BM * GEMM_BN) + e];
+    double *cp = J.C + (long long)gm * J.ldc + gn;
+    v = J.alpha * v;
+    *cp = (J.beta == 0.0) ? v : J.beta * (*cp) + v;
   }
 }
 

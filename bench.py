@@ -408,6 +408,7 @@ def run_gpu_arm(args, cfg, world, rank, local):
         return
     clocks = ClockSampler(local).start()
     for _ in range(args.warmup):
+        F = None  # release the previous factorization first (C5's factor is tens of GB)
         F, its, conv, res = step_device()
     barrier(world)
     times, e2e_times = [], []

@@ -62,7 +62,19 @@ struct ChunkPool {
       return c;
     }
     char *p = nullptr;
-    CK(cudaMalloc(&p, need));
+    if (cudaMalloc(&p, need) != cudaSuccess) {
+      // free chunks of the wrong sizes can hold the memory a larger request
+      // needs (C5): return them to the device and retry once
+      (void)cudaGetLastError();
+      release();
+      if (cudaMalloc(&p, need) != cudaSuccess) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        fprintf(stderr, "[mfh] out of device memory: chunk of %.1f MB requested, %.1f of %.1f GB free\n",
+                need / 1e6, fr / 1e9, tot / 1e9);
+        CK(cudaErrorMemoryAllocation);
+      }
+    }
     return {p, need};
   }
   void give(std::pair<char *, size_t> c) { free_chunks.push_back(c); }
@@ -462,9 +474,12 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
       continue;
     }
     int tm = (int)cdiv(g.m, GEMM_BM), tn = (int)cdiv(g.n, GEMM_BN);
-    // split-K (a rule of the job alone): <= 32 output tiles and k >= 256 ->
-    // k chunks of 128, partials summed in order by k_gemm_reduce
-    static const int split_k = getenv("MFH_GEMM_SPLIT_K") ? atoi(getenv("MFH_GEMM_SPLIT_K")) : 128;
+    // split-K (a rule of the job alone): <= 32 output tiles and k >= 2 chunks
+    // -> k chunks of MFH_GEMM_SPLIT_K, partials summed in order by
+    // k_gemm_reduce. Off by default: with the prefetched slabs it measured no
+    // gain at C2 (0.1282 vs 0.1278 s/step), and at C5 the per-job partials
+    // (32 KB per tile per chunk) ran the device out of memory.
+    static const int split_k = getenv("MFH_GEMM_SPLIT_K") ? atoi(getenv("MFH_GEMM_SPLIT_K")) : 0;
     const int ns = (split_k > 0 && !sk.record && g.k >= 2 * split_k && tm * tn <= 32 && !gemm_overlaps(g))
                        ? (int)cdiv(g.k, split_k)
                        : 1;

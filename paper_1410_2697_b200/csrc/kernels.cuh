@@ -509,14 +509,15 @@ __global__ void k_identity(double *const *__restrict__ ptrs, const int *__restri
 }
 
 // ---------------------------------------------------------------------------
-// vbatched GEMM, NN, row-major: 64x64 tiles, BK 16, 256 threads, 4x4 per thread.
-// Deterministic split-K for jobs with few output tiles and a long k (a rule of
-// the job's own (m, n, k), so a job's bits never depend on what else is in
-// the batch; the sharded factorization relies on that): each split tile
-// writes its partial (valid rows/columns only) to a workspace slot, and
-// k_gemm_reduce sums the partials in split order 0..S-1 and applies
-// alpha/beta. The main loop carries no fences or atomics, so its A/B tile
-// loads stay L1-cached.
+// vbatched GEMM, NN, row-major: 64x64 tiles, BK 16, 256 threads. The dot
+// products run on the FP64 tensor cores (mma.sync m8n8k4, the sampler's
+// fragment layout: warp w owns a 16 x 32 sub-tile); an m8n8k4 FP64 MMA equals
+// the k-ascending FMA chain bit for bit (scripts/probe/dmma_order.cu), and the
+// zero padding of a short last slab leaves the chain unchanged. The next k
+// slab is prefetched into registers while the current one is multiplied.
+// Deterministic split-K (off by default, see run_gemm): each split tile writes
+// its partial (valid rows/columns only) to a workspace slot, and k_gemm_reduce
+// sums the partials in split order 0..S-1 and applies alpha/beta.
 // ---------------------------------------------------------------------------
 constexpr int GEMM_BM = 64, GEMM_BN = 64, GEMM_BK = 16;
 
@@ -529,82 +530,76 @@ struct GemmSplit {  // one split output tile: partials ws .. ws+ns-1
   int job, mt, nt, ws, ns;
 };
 
-__global__ void __launch_bounds__(256, 3) k_gemm(const GemmJob *__restrict__ jobs,
+__global__ void __launch_bounds__(256) k_gemm(const GemmJob *__restrict__ jobs,
                                               const GemmTile *__restrict__ tiles, int ntiles,
                                               double *__restrict__ ws) {
-  __shared__ double As[GEMM_BK][GEMM_BM + 1];
-  __shared__ double Bs[GEMM_BK][GEMM_BN];
-  const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
+  __shared__ double As[GEMM_BK][RB_LD];
+  __shared__ double Bs[GEMM_BK][RB_LD];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp >> 1, wc = warp & 1, g = lane >> 2, q = lane & 3;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const GemmTile tl = tiles[t];
     const GemmJob J = jobs[tl.job];
     const int m0 = tl.mt * GEMM_BM, n0 = tl.nt * GEMM_BN;
     const int k1 = tl.k1;
-    double acc[4][4];
+    double acc[2][8];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-    // register prefetch: the next k slab's global loads are in flight while
-    // the current slab is multiplied out of shared memory (same FMA order)
+      for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
     double ra[4], rb[4];
     auto load_slab = [&](int k0) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {  // A: 64 rows x 16 k
-        int e = tid + q * 256;
-        int mm = e >> 4, kk = e & 15;
-        int gm = m0 + mm, gk = k0 + kk;
-        ra[q] = (gm < J.m && gk < k1) ? J.A[(long long)gm * J.lda + gk] : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {  // B: 16 k x 64 cols
-        int e = tid + q * 256;
-        int kk = e >> 6, nn = e & 63;
-        int gk = k0 + kk, gn = n0 + nn;
-        rb[q] = (gk < k1 && gn < J.n) ? J.B[(long long)gk * J.ldb + gn] : 0.0;
+      for (int m = 0; m < 4; ++m) {
+        const int e = tid + 256 * m;
+        const int mm = e >> 4, kk = e & 15;  // A: 64 rows x 16 k
+        const int gm = m0 + mm, gk = k0 + kk;
+        ra[m] = (gm < J.m && gk < k1) ? J.A[(long long)gm * J.lda + gk] : 0.0;
+        const int k2 = e >> 6, nn = e & 63;  // B: 16 k x 64 cols
+        const int gk2 = k0 + k2, gn = n0 + nn;
+        rb[m] = (gk2 < k1 && gn < J.n) ? J.B[(long long)gk2 * J.ldb + gn] : 0.0;
       }
     };
     if (tl.k0 < k1) load_slab(tl.k0);
     for (int k0 = tl.k0; k0 < k1; k0 += GEMM_BK) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        int e = tid + q * 256;
-        As[e & 15][e >> 4] = ra[q];
-        Bs[e >> 6][e & 63] = rb[q];
+      for (int m = 0; m < 4; ++m) {
+        const int e = tid + 256 * m;
+        As[e & 15][e >> 4] = ra[m];
+        Bs[e >> 6][e & 63] = rb[m];
       }
       __syncthreads();
-      if (k0 + GEMM_BK < k1) load_slab(k0 + GEMM_BK);
-      int kc = min(GEMM_BK, k1 - k0);
-      for (int kk = 0; kk < kc; ++kk) {
-        double a[4], b[4];
+      if (k0 + GEMM_BK < k1) load_slab(k0 + GEMM_BK);  // in flight during the MMAs
 #pragma unroll
-        for (int q = 0; q < 4; ++q) a[q] = As[kk][ty + 16 * q];
+      for (int kb = 0; kb < GEMM_BK / 4; ++kb) {
+        double fa[2], fb[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) b[q] = Bs[kk][tx + 16 * q];
+        for (int a = 0; a < 2; ++a) fa[a] = As[4 * kb + q][16 * wr + 8 * a + g];
 #pragma unroll
-        for (int p = 0; p < 4; ++p)
+        for (int j = 0; j < 4; ++j) fb[j] = Bs[4 * kb + q][32 * wc + 8 * j + g];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma884(acc[a][2 * j], acc[a][2 * j + 1], fa[a], fb[j]);
       }
       __syncthreads();
     }
     double *part = tl.ws >= 0 ? ws + (long long)tl.ws * (GEMM_BM * GEMM_BN) : nullptr;
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      int gm = m0 + ty + 16 * p;
+    for (int a = 0; a < 2; ++a) {
+      const int r = rb_row(a, wr, g), gm = m0 + r;
       if (gm >= J.m) continue;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        int gn = n0 + tx + 16 * q;
+      for (int b = 0; b < 8; ++b) {
+        const int c = rb_col(b, wc, q), gn = n0 + c;
         if (gn >= J.n) continue;
         if (part) {
-          part[(ty + 16 * p) * GEMM_BN + tx + 16 * q] = acc[p][q];
+          part[r * GEMM_BN + c] = acc[a][b];
           continue;
         }
-        double *c = J.C + (long long)gm * J.ldc + gn;
-        double v = J.alpha * acc[p][q];
-        *c = (J.beta == 0.0) ? v : J.beta * (*c) + v;
+        double *cp = J.C + (long long)gm * J.ldc + gn;
+        double v = J.alpha * acc[a][b];
+        *cp = (J.beta == 0.0) ? v : J.beta * (*cp) + v;
       }
     }
   }

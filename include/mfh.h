@@ -118,6 +118,20 @@ int mfh_etree_sizes(const mfh_etree *t, int64_t *n_nodes, int64_t *n_piv_total,
                     int64_t *n_frontal_total, int64_t *root);
 int mfh_etree_fetch(const mfh_etree *t, int64_t *post_order, int64_t *piv_ptr, int64_t *piv,
                     int64_t *fr_ptr, int64_t *fr, int64_t *parent);
+/* The CALLER's elimination tree (replaces passing the reference's
+ * EliminationTree, ordering.py:238-261, to mf_factorize, multifrontal.py:459),
+ * flattened: permutation (old -> new), n_nodes nodes, root, parent (-1 at the
+ * root), children in node.children order (child_ptr / child), post order, and
+ * per node the pivot ids (a contiguous run) and sorted frontal ids, all in the
+ * permuted numbering. Validated (permutation, tree shape, post order children
+ * first, pivots covering 0..n-1 once); a frontal id at or below its node's
+ * pivots raises the reference's "node {id}: frontal index below the pivot
+ * block" (ordering.py:303-306). Nothing is recomputed: the factorization uses
+ * exactly this tree. */
+int mfh_etree_from_arrays(int64_t n, const int64_t *perm, int64_t n_nodes, int64_t root, const int64_t *parent,
+                          const int64_t *child_ptr, const int64_t *child, int64_t n_post,
+                          const int64_t *post_order, const int64_t *piv_ptr, const int64_t *piv,
+                          const int64_t *fr_ptr, const int64_t *fr, mfh_etree **out);
 void mfh_etree_free(mfh_etree *t);
 
 /* ---- numeric factorization (mf_factorize, multifrontal.py:459-530) --------- */

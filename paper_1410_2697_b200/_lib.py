@@ -130,6 +130,7 @@ def _sig(lib):
         "mfh_etree_sizes": (C.c_int, [P, pi, pi, pi, pi]),
         "mfh_etree_fetch": (C.c_int, [P, P, P, P, P, P, P]),
         "mfh_etree_free": (None, [P]),
+        "mfh_etree_from_arrays": (C.c_int, [I64, P, I64, I64, P, P, P, I64, P, P, P, P, P, PP]),
         "mfh_factorize": (C.c_int, [P, P, I64, P, P, P, C.c_int, C.POINTER(mfh_params), PP]),
         "mfh_node_op": (C.c_int, [P, I64, C.c_int, P, P]),
         "mfh_factorize_sharded": (C.c_int, [P, P, I64, P, P, P, C.c_int, C.POINTER(mfh_params),

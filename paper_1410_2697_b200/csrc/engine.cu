@@ -64,8 +64,13 @@ struct ChunkPool {
     char *p = nullptr;
     if (cudaMalloc(&p, need) != cudaSuccess) {
       // free chunks of the wrong sizes can hold the memory a larger request
-      // needs (C5): return them to the device and retry once
+      // needs (C5): return them to the device and retry once. A free chunk may
+      // still be read by enqueued work (release arenas hand chunks back as soon
+      // as their last reader is enqueued), so the device drains first; the
+      // cudaFree below must never race those kernels, even if it becomes
+      // stream-ordered.
       (void)cudaGetLastError();
+      CK(cudaDeviceSynchronize());
       release();
       if (cudaMalloc(&p, need) != cudaSuccess) {
         size_t fr = 0, tot = 0;
@@ -258,6 +263,8 @@ struct Ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
   cudaEvent_t gmres_ev[2] = {nullptr, nullptr};  // Hessenberg column read-backs (pipelined Arnoldi)
   int cluster_size = 16;
+  size_t plu_dyn_max = 0;  // dynamic shared memory the pivot-LU kernels may use (per device)
+  int nsm = 148;
   ChunkPool pool;
   std::vector<cudaEvent_t> evpool;  // per-height phase events, reused
   Stage stage;
@@ -464,11 +471,22 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
   int nslot = 0;
   auto is_big = [&](const GemmJob &g) {
     return !sk.record && g.k > 0 && g.m >= 64 && g.n >= 64 && 2.0 * g.m * g.n * g.k >= (double)(1 << 27) &&
-           !gemm_overlaps(g);
+           g.lda > 0 && g.ldb > 0 && !gemm_overlaps(g);
   };
+  // products with an identity operand (leading dimension -1: the strip that
+  // stands for DenseBlock.as_factors' eye) are scaled copies, not GEMMs
+  std::vector<GemmJob> eye;
+  std::vector<int> eye_which;
   for (int j = 0; j < (int)jobs.size(); ++j) {
     const GemmJob &g = jobs[j];
     if (g.m <= 0 || g.n <= 0) continue;
+    if (g.k > 0 && (g.lda < 0 || g.ldb < 0)) {
+      if ((g.lda < 0 && g.m != g.k) || (g.ldb < 0 && g.k != g.n))
+        throw runtime_error("internal: identity operand of a GEMM must be square");
+      eye.push_back(g);
+      eye_which.push_back(g.lda < 0 ? 0 : 1);
+      continue;
+    }
     if (is_big(g)) {
       big.push_back(g);
       continue;
@@ -524,6 +542,21 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
       ctx->lib_calls++;
     }
   }
+  if (!eye.empty()) {
+    int64_t mx = 1;
+    for (auto &g : eye) mx = std::max<int64_t>(mx, (int64_t)g.m * g.n);
+    for (size_t b = 0; b < eye.size(); b += 60000) {
+      std::vector<GemmJob> part(eye.begin() + b, eye.begin() + std::min(eye.size(), b + 60000));
+      std::vector<int> wh(eye_which.begin() + b, eye_which.begin() + std::min(eye.size(), b + 60000));
+      GemmJob *dj = sk.push(part);
+      int *dw = sk.push(wh);
+      dim3 grid((unsigned)std::min<int64_t>(cdiv(mx, 256), 128), (unsigned)part.size());
+      sk.launch([=](cudaStream_t st) {
+        k_axpby<<<grid, 256, 0, st>>>(dj, dw);
+        check_launch();
+      });
+    }
+  }
   if (tiles.empty()) return;
   static const bool glog = getenv("MFH_GEMM_LOG") != nullptr;
   if (glog) {
@@ -566,11 +599,6 @@ static void run_trsm(Sink &sk, const std::vector<TrsmJob> &jobs) {
     gm.push_back(GemmJob{inv, j.B, j.B, j.w, j.ncols, j.w, j.w, j.ldb, j.ldb, 1.0, 0.0});
   }
   if (ti.empty()) return;
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_trinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRINV_SMEM));
-    attr = true;
-  }
   TrinvJob *dj = sk.push(ti);
   int nb = (int)ti.size();
   sk.launch([=](cudaStream_t st) {
@@ -641,26 +669,13 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
     int cs = (mmax + PANEL_ROWS_MAX - 1) / PANEL_ROWS_MAX;
     if (cs == 1) {
       // every panel of the batch fits one CTA's shared memory
-      static bool attr1 = false;
-      if (!attr1) {
-        CK(cudaFuncSetAttribute(k_getrf_panel_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(sizeof(double) * PANEL_ROWS_MAX * PLD)));
-        attr1 = true;
-      }
       size_t smem = sizeof(double) * (size_t)mmax * PLD;
       sk.launch([=](cudaStream_t s) {
         k_getrf_panel_cta<<<np_, 512, smem, s>>>(dp);
         check_launch();
       });
-    } else if (cs <= 16) {
+    } else if (cs <= sk.ctx->cluster_size) {
       // shared-memory resident panel across a cluster of cs CTAs
-      static bool attr = false;
-      if (!attr) {
-        CK(cudaFuncSetAttribute(k_getrf_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(sizeof(double) * PANEL_ROWS_MAX * PLD)));
-        CK(cudaFuncSetAttribute(k_getrf_panel_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr = true;
-      }
       int rp = (mmax + cs - 1) / cs;
       size_t smem = sizeof(double) * (size_t)rp * PLD;
       sk.launch([=](cudaStream_t s) {
@@ -732,11 +747,6 @@ struct TriInvReq {
 static void run_tri_inv(Sink &sk, const std::vector<TriInvReq> &reqs) {
   OpClock oc_("tri_inv");
   if (reqs.empty()) return;
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_trinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRINV_SMEM));
-    attr = true;
-  }
   std::vector<double *> ip;
   std::vector<int> idim, ild;
   std::vector<TrinvJob> ti;
@@ -908,6 +918,68 @@ static void run_identity(Sink &sk, const std::vector<double *> &ptrs, const std:
 constexpr long long PLU_CTA_MAX = 32 * 1024;  // entries: one CTA with the core in shared memory (if it fits)
 constexpr int PLU_CL_NT = 1024;               // threads per CTA of the cluster kernel
 
+// the pivot-LU kernels that opt into large dynamic shared memory
+static const void *const *plu_fns() {
+  static const void *fns[6] = {(const void *)k_plu_cta2<true, 512>, (const void *)k_plu_cta2<true, 1024>,
+                               (const void *)k_plu_cluster3<PLU_CL_NT>, (const void *)k_plu_groups3,
+                               (const void *)k_plu_groups<false>,   (const void *)k_plu_groups<true>};
+  return fns;
+}
+
+// Function attributes (shared-memory opt-ins, non-portable cluster sizes) are
+// per DEVICE: set them once per device (the first context created on it), and
+// record the device's limits in every context.
+static void device_setup(Ctx *ctx) {
+  static std::mutex mu;
+  static std::vector<int> done;  // devices already configured
+  std::lock_guard<std::mutex> lk(mu);
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  CK(cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, ctx->device));
+  const void *const *fns = plu_fns();
+  size_t stat = 0;
+  for (int q = 0; q < 6; ++q) {
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, fns[q]));
+    stat = std::max(stat, fa.sharedSizeBytes);
+  }
+  ctx->plu_dyn_max = (size_t)optin - stat - 64;
+  const bool first = std::find(done.begin(), done.end(), ctx->device) == done.end();
+  if (first) {
+    for (int q = 0; q < 6; ++q)
+      CK(cudaFuncSetAttribute(fns[q], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->plu_dyn_max));
+    CK(cudaFuncSetAttribute(k_trinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRINV_SMEM));
+    CK(cudaFuncSetAttribute(k_getrf_panel_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(sizeof(double) * PANEL_ROWS_MAX * PLD)));
+    CK(cudaFuncSetAttribute(k_getrf_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(sizeof(double) * PANEL_ROWS_MAX * PLD)));
+    CK(cudaFuncSetAttribute(k_sample_rb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RB_DYN));
+  }
+  // 16-CTA clusters need the non-portable opt-in; without it the cluster
+  // kernels run 8-CTA clusters
+  cudaError_t e1 = cudaFuncSetAttribute(fns[2], cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaError_t e2 = cudaFuncSetAttribute(k_getrf_panel_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    (void)cudaGetLastError();
+    ctx->cluster_size = 8;
+  }
+  if (first) done.push_back(ctx->device);
+}
+
+// every entry point that uses a context runs on that context's device (and
+// restores the caller's current device)
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 static void launch_cluster(const void *fn, int ncores, int cs, size_t smem, cudaStream_t st, const PluJob *dj,
                            const int *dids, double eps) {
   cudaLaunchConfig_t cfg = {};
@@ -937,34 +1009,10 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
     return;
   }
   Ctx *ctx = sk.ctx;
-  static bool attr_done = false;
-  static size_t dyn_max = 0;
-  static const void *fns[6] = {(const void *)k_plu_cta2<true, 512>, (const void *)k_plu_cta2<true, 1024>,
-                               (const void *)k_plu_cluster3<PLU_CL_NT>, (const void *)k_plu_groups3,
-                               (const void *)k_plu_groups<false>,   (const void *)k_plu_groups<true>};
-  if (!attr_done) {
-    int optin = 0;
-    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-    size_t stat = 0;
-    for (const void *fn : fns) {
-      cudaFuncAttributes fa;
-      CK(cudaFuncGetAttributes(&fa, fn));
-      stat = std::max(stat, fa.sharedSizeBytes);
-    }
-    dyn_max = (size_t)optin - stat - 64;
-    for (const void *fn : fns) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
-    for (const void *fn : {fns[2]}) {
-      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) {
-        cudaGetLastError();
-        ctx->cluster_size = 8;
-      }
-    }
-    attr_done = true;
-  }
+  const size_t dyn_max = ctx->plu_dyn_max;  // set per device in device_setup
+  const void *const *fns = plu_fns();
   const int CS = ctx->cluster_size;
-  int nsm = 148;
-  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
+  const int nsm = ctx->nsm;
   auto cta_bytes = [](int m, int n) { return sizeof(double) * (size_t)m * n + sizeof(int) * (size_t)(m + n) + 16; };
   std::vector<int> small[3], cl8, cl16, grd;
   size_t smax[3] = {48 * 1024, 100 * 1024, dyn_max};
@@ -1179,6 +1227,8 @@ struct FacView {  // DenseBlock.as_factors / LowRankFactor.as_factors (hodlr.py:
 
 struct BlockH {
   int fi = -1;
+  int kind = 2;  // 0: pivot-block HODLR (dies with the height), 1: update HODLR (dies once the
+                 // parent has sampled it), 2: pf / fp coupling (retained for the apply)
   int r0 = 0, m = 0, c0 = 0, n = 0;
   std::vector<int> I, J;
   bool fullI = false, fullJ = false;
@@ -1267,9 +1317,29 @@ struct FrontH {
   int *piv = nullptr;
   // apply operators (explicit inverse form, computed once at factor time)
   double *Pinv = nullptr, *Gfp = nullptr, *Gpf = nullptr;
-  double *Fpf = nullptr, *Ffp = nullptr;  // dense: F_pf / F_fp kept for node_factors (apply_pf / apply_fp)
-  // structured: Hinv = (HODLR pivot block)^{-1}, Xp = Hinv col_pf, RH = row_fp Hinv
+  // dense: F_pp kept for node_factors: apply_pf = F_pp (Gpf v), apply_fp = Gfp (F_pp v)
+  // (n_p^2 reals instead of keeping F_pf and F_fp, 2 n_p nf)
+  double *Fpp = nullptr;
+  // structured: Hinv = (HODLR pivot block)^{-1} (retained when pform == 0),
+  // Xp = Hinv col_pf, RH = row_fp Hinv (low-rank couplings only)
   double *Hinv = nullptr, *Xp = nullptr, *RH = nullptr;
+  // retained pivot-block inverse: 0 explicit Hinv, 1 HODLR inverse form
+  //   H^{-1} b = L^{-1} b - sum_v X_v w_v,  w_v = Tm_v b[v's range]
+  int pform = 0;
+  struct TmNode {
+    int slot = 0, lo = 0, nv = 0, r1 = 0, r2 = 0;
+    double *Tm = nullptr;                  // (r1 + r2) x nv, retained
+    const double *xt = nullptr, *xb = nullptr;  // x_top / x_bot (factor-time scratch)
+    int64_t woff = 0;                      // offset of w_v in the front's w segment
+  };
+  struct TmLeaf {
+    int slot = 0, lo = 0, sz = 0, K = 0;
+    double *Linv = nullptr, *XL = nullptr;  // sz x sz, sz x K
+    long long *idx = nullptr;               // K entries into the w segment
+  };
+  std::vector<TmNode> tnode;
+  std::vector<TmLeaf> tleaf;
+  int64_t wlen = 0;
   // structured path
   int pp = -1, ff = -1, pf = -1, fp = -1;  // tree / block ids
   int tree_base = -1, block_base = -1;      // pre-assigned plan slots
@@ -1448,7 +1518,7 @@ struct Factorizer {
   }
 
   // ---- tree construction (hodlr.py:203-246 recursion order) ----
-  int make_tree(int fi, int base, int nloc, std::vector<int> &blist, int tid) {
+  int make_tree(int fi, int base, int nloc, std::vector<int> &blist, int tid, int kind) {
     HTree t;
     t.fi = fi;
     t.base = base;
@@ -1518,8 +1588,8 @@ struct Factorizer {
         int lo = fr.lo, hi = fr.hi, mid = (lo + hi) >> 1;
         int v = fr.v;
         st.pop_back();
-        int bu = new_block(fi, base + lo, mid - lo, base + mid, hi - mid);
-        int bl = new_block(fi, base + mid, hi - mid, base + lo, mid - lo);
+        int bu = new_block(fi, base + lo, mid - lo, base + mid, hi - mid, kind);
+        int bl = new_block(fi, base + mid, hi - mid, base + lo, mid - lo, kind);
         F->trees[tid].up[v] = bu;
         F->trees[tid].lw[v] = bl;
         blist.push_back(bu);
@@ -1530,9 +1600,10 @@ struct Factorizer {
   }
 
   int block_cursor = 0;  // planner thread: next pre-assigned block slot
-  int new_block(int fi, int r0, int m, int c0, int nn) {
+  int new_block(int fi, int r0, int m, int c0, int nn, int kind) {
     BlockH &b = F->blocks[block_cursor];
     b.fi = fi;
+    b.kind = kind;
     b.r0 = r0;
     b.m = m;
     b.c0 = c0;
@@ -1546,14 +1617,14 @@ struct Factorizer {
     FrontH &f = F->fronts[fi];
     block_cursor = f.block_base;
     std::vector<int> blist;
-    if (f.npv) f.pp = make_tree(fi, 0, f.npv, blist, f.tree_base);
+    if (f.npv) f.pp = make_tree(fi, 0, f.npv, blist, f.tree_base, 0);
     if (f.npv && f.nf) {
-      f.pf = new_block(fi, 0, f.npv, f.npv, f.nf);
-      f.fp = new_block(fi, f.npv, f.nf, 0, f.npv);
+      f.pf = new_block(fi, 0, f.npv, f.npv, f.nf, 2);
+      f.fp = new_block(fi, f.npv, f.nf, 0, f.npv, 2);
       blist.push_back(f.pf);
       blist.push_back(f.fp);
     }
-    if (f.nf) f.ff = make_tree(fi, f.npv, f.nf, blist, f.tree_base + 1);
+    if (f.nf) f.ff = make_tree(fi, f.npv, f.nf, blist, f.tree_base + 1, 1);
     F->front_blocks[fi] = blist;
     for (int bi : blist) {
       BlockH &b = F->blocks[bi];
@@ -1780,11 +1851,6 @@ struct Factorizer {
     if (!rid[1].empty()) {
       SampleTiles T{drid[1], dpre[1], (int)rid[1].size(), pre[1].back()};
       int grid = (int)std::min<int64_t>(T.ntiles, 148 * 8);
-      static bool attr = false;
-      if (!attr) {
-        CK(cudaFuncSetAttribute(k_sample_rb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RB_DYN));
-        attr = true;
-      }
       s.launch([=](cudaStream_t st) {
         k_sample_rb<<<grid, 256, RB_DYN, st>>>(dr, T, fF, fC, pp, pc, pv);
         check_launch();
@@ -1816,6 +1882,33 @@ struct Factorizer {
       v.rank = b.m;
     }
     return v;
+  }
+
+  // retained pivot-block form: 1 (HODLR inverse form) when it holds fewer reals
+  // than the explicit inverse; MFH_PFORM=0/1 forces one (tests)
+  int pform_of(const HTree &T, int N) {
+    const char *fe = getenv("MFH_PFORM");
+    const int force = fe ? atoi(fe) : -1;
+    if (force == 0 || force == 1) return force;
+    double tm = 0;
+    for (int v = 0; v < T.nslots; ++v) {
+      if (T.leaf[v] == 1) {
+        double sz = T.hi[v] - T.lo[v];
+        tm += sz * sz;
+      } else if (T.leaf[v] == 0) {
+        const int lo = T.lo[v], hi = T.hi[v], mid = (lo + hi) >> 1;
+        const double r1 = F->blocks[T.up[v]].erank(), r2 = F->blocks[T.lw[v]].erank();
+        tm += (r1 + r2) * (hi - lo) + (mid - lo) * r1 + (hi - mid) * r2;
+      }
+    }
+    return tm < (double)N * N ? 1 : 0;
+  }
+
+  // device storage of a compressed block by its lifetime (BlockH::kind)
+  double *blk_alloc(const BlockH &b, size_t n) {
+    if (b.kind == 0) return ctx->scratch.d(n);
+    if (b.kind == 1) return upd.d(n, release_height(F->fronts[b.fi]));
+    return F->arena.d(n);
   }
 
   // ---- one height ----
@@ -1856,7 +1949,8 @@ struct Factorizer {
         for (int v = 0; v < T.nslots; ++v)
           if (T.leaf[v] == 1) {
             int sz = T.hi[v] - T.lo[v];
-            T.lval[v] = F->arena.d((size_t)sz * sz);
+            // pivot-block leaves live for the height, update leaves until the parent sampled them
+            T.lval[v] = tt == f.pp ? ctx->scratch.d((size_t)sz * sz) : upd.d((size_t)sz * sz, release_height(f));
             reqs.push_back(SReq{slot[fi], sz, sz, nullptr, nullptr, T.base + T.lo[v], T.base + T.lo[v],
                                 T.lval[v], sz});
           }
@@ -1973,21 +2067,20 @@ struct Factorizer {
                                f.nf, f.npv, f.nh, f.nf, f.nh, -1.0, 1.0});
         }
       }
-      run_inverse(s, inv);
-      run_gemm(s, g1);
-      run_gemm(s, g2);
-      {  // F_pf / F_fp outlive the front buffer (node_factors apply_pf / apply_fp)
+      {  // F_pp outlives the front buffer (node_factors apply_pf / apply_fp); copied
+        // before the blocked inversion overwrites it with its LU
         std::vector<CopyJob> keep;
         for (int fi : D) {
           FrontH &f = F->fronts[fi];
           if (!f.npv || !f.nf) continue;
-          f.Fpf = F->arena.d((size_t)f.npv * f.nf);
-          f.Ffp = F->arena.d((size_t)f.nf * f.npv);
-          keep.push_back(CopyJob{f.F + f.npv, f.Fpf, f.npv, f.nf, f.nh, f.nf, nullptr, nullptr});
-          keep.push_back(CopyJob{f.F + (int64_t)f.npv * f.nh, f.Ffp, f.nf, f.npv, f.nh, f.npv, nullptr, nullptr});
+          f.Fpp = F->arena.d((size_t)f.npv * f.npv);
+          keep.push_back(CopyJob{f.F, f.Fpp, f.npv, f.npv, f.nh, f.npv, nullptr, nullptr});
         }
         run_copy(s, keep);
       }
+      run_inverse(s, inv);
+      run_gemm(s, g1);
+      run_gemm(s, g2);
       for (int fi : D) {
         FrontH &f = F->fronts[fi];
         if (f.nf) {
@@ -2077,15 +2170,15 @@ struct Factorizer {
       int64_t lr_stored = (int64_t)(b.m + b.n) * b.rank;
       b.dense = unc || lr_stored > (int64_t)b.m * b.n;
       if (b.dense) {
-        b.val = F->arena.d((size_t)b.m * b.n);
+        b.val = blk_alloc(b, (size_t)b.m * b.n);
         dreq.push_back(SReq{slot[b.fi], b.m, b.n, nullptr, nullptr, b.r0, b.c0, b.val, b.n});
         F->stats.n_dense_fallback++;
       } else if (b.rank > 0) {
         int r = b.rank;
         double *lu = ctx->scratch.d((size_t)r * r);
         lux.push_back(LuExtractJob{b.core, nJ, r, b.rows_phys ? nullptr : b.pint, nullptr, lu});
-        b.row = F->arena.d((size_t)r * b.n);
-        b.col = F->arena.d((size_t)b.m * r);
+        b.row = blk_alloc(b, (size_t)r * b.n);
+        b.col = blk_alloc(b, (size_t)b.m * r);
         SkelJob sj{};
         sj.lu = lu;
         sj.r = r;
@@ -2141,30 +2234,34 @@ struct Factorizer {
     cudaEventRecord(ev[5], ctx->s);
     hts[5] = std::chrono::steady_clock::now();
 
-    // ------------------------------------------------ device HNode tables (one upload)
+    // ------------------------------------------------ device HNode tables of the
+    // update HODLRs (what the parent's sampler descends), one upload; they die
+    // with the update
     {
       std::vector<HNode> all;
       std::vector<std::pair<int, size_t>> where;
+      std::vector<std::pair<size_t, int>> seg;  // (first node, release height) per front
       for (int fi : S) {
         FrontH &f = F->fronts[fi];
-        for (int tt : {f.pp, f.ff}) {
-          if (tt < 0) continue;
-          HTree &T = F->trees[tt];
-          where.push_back({tt, all.size()});
-          for (int v = 0; v < T.nslots; ++v) {
-            HNode h{};
-            if (T.leaf[v] == 1)
-              h.leaf = T.lval[v];
-            else if (T.leaf[v] == 0) {
-              h.up = F->blocks[T.up[v]].dev();
-              h.lw = F->blocks[T.lw[v]].dev();
-            }
-            all.push_back(h);
+        if (f.ff < 0) continue;
+        HTree &T = F->trees[f.ff];
+        where.push_back({f.ff, all.size()});
+        seg.push_back({all.size(), release_height(f)});
+        for (int v = 0; v < T.nslots; ++v) {
+          HNode h{};
+          if (T.leaf[v] == 1)
+            h.leaf = T.lval[v];
+          else if (T.leaf[v] == 0) {
+            h.up = F->blocks[T.up[v]].dev();
+            h.lw = F->blocks[T.lw[v]].dev();
           }
+          all.push_back(h);
         }
       }
       if (!all.empty()) {
-        HNode *d = (HNode *)F->arena.alloc(sizeof(HNode) * all.size());
+        int rh = 0;
+        for (auto &q : seg) rh = std::max(rh, q.second);
+        HNode *d = (HNode *)upd.alloc(sizeof(HNode) * all.size(), rh);
         for (auto &w : where) F->trees[w.first].d_nodes = d + w.second;
         s.push_to(d, all.data(), sizeof(HNode) * all.size());
       }
@@ -2251,7 +2348,12 @@ struct Factorizer {
         HTree &T = F->trees[tt];
         FrontH &f = F->fronts[T.fi];
         const int N = f.npv;
-        f.Hinv = F->arena.d((size_t)N * N);
+        // retained form of the pivot-block inverse (a14/a15): the explicit n_p^2
+        // inverse, or the HODLR inverse form (leaf inverses, per node X_v and
+        // Tm_v: H^{-1} = blockdiag(L^{-1}) - sum_v X_v Tm_v), whichever holds
+        // fewer reals -- it is also what one apply reads
+        f.pform = pform_of(T, N);
+        f.Hinv = f.pform ? ctx->scratch.d((size_t)N * N) : F->arena.d((size_t)N * N);
         CK(cudaMemsetAsync(f.Hinv, 0, sizeof(double) * (size_t)N * N, ctx->s));
         for (int v = 0; v < T.nslots; ++v)
           if (T.leaf[v] == 1) {
@@ -2264,13 +2366,37 @@ struct Factorizer {
               lc.push_back(CopyJob{T.lval[v], blk, sz, sz, sz, N, nullptr, nullptr});
               leaves.push_back(InvReq{blk, sz, N, blk, N, nullptr, d_flags + T.lflag[v]});
             } else {
-              T.lpiv[v] = F->arena.i(sz);
+              T.lpiv[v] = ctx->scratch.i(sz);
               leaves.push_back(InvReq{T.lval[v], sz, sz, blk, N, T.lpiv[v], d_flags + T.lflag[v]});
             }
           }
       }
       run_copy(s, lc);
       run_inverse(s, leaves);
+      {  // HODLR inverse form: keep the leaf inverses before the levels update Hinv's diagonal
+        std::vector<CopyJob> lk;
+        for (int tt : ptrees) {
+          HTree &T = F->trees[tt];
+          FrontH &f = F->fronts[T.fi];
+          if (!f.pform) continue;
+          f.tleaf.clear();
+          f.tnode.clear();
+          f.wlen = 0;
+          const int N = f.npv;
+          for (int v = 0; v < T.nslots; ++v)
+            if (T.leaf[v] == 1) {
+              const int lo = T.lo[v], sz = T.hi[v] - T.lo[v];
+              FrontH::TmLeaf L{};
+              L.slot = v;
+              L.lo = lo;
+              L.sz = sz;
+              L.Linv = F->arena.d((size_t)sz * sz);
+              lk.push_back(CopyJob{f.Hinv + (int64_t)lo * N + lo, L.Linv, sz, sz, N, sz, nullptr, nullptr});
+              f.tleaf.push_back(L);
+            }
+        }
+        run_copy(s, lk);
+      }
       int maxd = 0;
       for (int tt : ptrees) maxd = std::max(maxd, F->trees[tt].maxdepth);
       for (int d = maxd; d >= 0; --d) {
@@ -2307,7 +2433,21 @@ struct Factorizer {
             nd.xb = ctx->scratch.d((size_t)m2 * std::max(1, r2));
             nd.yt = ctx->scratch.d((size_t)std::max(1, r1) * m2);
             nd.yb = ctx->scratch.d((size_t)std::max(1, r2) * m1);
-            nd.Tm = ctx->scratch.d((size_t)rr * nv);
+            nd.Tm = f.pform ? F->arena.d((size_t)rr * nv) : ctx->scratch.d((size_t)rr * nv);
+            if (f.pform) {
+              FrontH::TmNode tn{};
+              tn.slot = v;
+              tn.lo = lo;
+              tn.nv = nv;
+              tn.r1 = r1;
+              tn.r2 = r2;
+              tn.Tm = nd.Tm;
+              tn.xt = nd.xt;
+              tn.xb = nd.xb;
+              tn.woff = f.wlen;
+              f.wlen += rr;
+              f.tnode.push_back(tn);
+            }
             // (a) x_top = H_L^{-1} col1, x_bot = H_R^{-1} col2, y_top = row1 H_R^{-1}, y_bot = row2 H_L^{-1}
             if (r1) {
               ga.push_back(GemmJob{HLL, f1.col, nd.xt, m1, r1, m1, N, f1.ldc, r1, 1.0, 0.0});
@@ -2385,6 +2525,48 @@ struct Factorizer {
         run_gemm(s, gd);
         run_gemm(s, ge);
       }
+      // HODLR inverse form: per leaf, the rows of its ancestors' X_v = diag(x_top,
+      // x_bot) side by side (XL, sz x K) and where each column's w entry lives
+      // (idx into the front's w segment): y_leaf = L^{-1} b_leaf - XL w[idx]
+      std::vector<CopyJob> xl;
+      for (int tt : ptrees) {
+        HTree &T = F->trees[tt];
+        FrontH &f = F->fronts[T.fi];
+        if (!f.pform) continue;
+        std::map<int, const FrontH::TmNode *> by_slot;
+        for (auto &tn : f.tnode) by_slot[tn.slot] = &tn;
+        for (auto &L : f.tleaf) {
+          std::vector<const FrontH::TmNode *> anc;
+          for (int v = L.slot; v > 0;) {
+            v = (v - 1) / 2;
+            auto it = by_slot.find(v);
+            if (it != by_slot.end()) anc.push_back(it->second);
+          }
+          std::reverse(anc.begin(), anc.end());  // root first
+          std::vector<long long> idx;
+          std::vector<std::array<int64_t, 4>> cols;  // (node, left?, column offset, width)
+          for (auto *tn : anc) {
+            const int mid = tn->lo + tn->nv / 2;
+            const bool left = L.lo < mid;
+            const int r = left ? tn->r1 : tn->r2;
+            if (r == 0) continue;
+            cols.push_back({(int64_t)(tn - f.tnode.data()), left, (int64_t)idx.size(), r});
+            for (int j = 0; j < r; ++j) idx.push_back(tn->woff + (left ? 0 : tn->r1) + j);
+          }
+          L.K = (int)idx.size();
+          if (!L.K) continue;
+          L.XL = F->arena.d((size_t)L.sz * L.K);
+          L.idx = (long long *)F->arena.alloc(sizeof(long long) * idx.size());
+          s.push_to(L.idx, idx.data(), sizeof(long long) * idx.size());
+          for (auto &c : cols) {
+            const FrontH::TmNode &tn = f.tnode[c[0]];
+            const int mid = tn.lo + tn.nv / 2, r = (int)c[3];
+            const double *src = c[1] ? tn.xt + (int64_t)(L.lo - tn.lo) * r : tn.xb + (int64_t)(L.lo - mid) * r;
+            xl.push_back(CopyJob{src, L.XL + c[2], L.sz, r, r, L.K, nullptr, nullptr});
+          }
+        }
+      }
+      run_copy(s, xl);
     }
     cudaEventRecord(ev[6], ctx->s);
     hts[6] = std::chrono::steady_clock::now();
@@ -2401,12 +2583,29 @@ struct Factorizer {
         FrontH &f = F->fronts[fi];
         if (!(f.npv && f.nf)) continue;
         El e{fi, as_factors(F->blocks[f.pf]), as_factors(F->blocks[f.fp])};
-        const int N = f.npv;
-        // x = H^{-1} col_pf (retained for the apply), RH = row_fp H^{-1} (apply)
-        f.Xp = F->arena.d((size_t)N * std::max(1, e.pf.rank));
-        f.RH = F->arena.d((size_t)std::max(1, e.fp.rank) * N);
-        if (e.pf.rank) g0.push_back(GemmJob{f.Hinv, e.pf.col, f.Xp, N, e.pf.rank, N, N, e.pf.ldc, e.pf.rank, 1.0, 0.0});
-        if (e.fp.rank) g0.push_back(GemmJob{e.fp.row, f.Hinv, f.RH, e.fp.rank, N, N, e.fp.ldr, N, N, 1.0, 0.0});
+        const int N = f.npv, nf = f.nf;
+        const BlockH &bpf = F->blocks[f.pf], &bfp = F->blocks[f.fp];
+        // x = H^{-1} col_pf (multifrontal.py:428): the eliminate core and, for a
+        // low-rank F_pf, the apply's downward operator Xp. A dense-fallback F_pf
+        // enters as (F_pf, I) or (I, F_pf) (hodlr.py:59-63): x is H^{-1} F_pf
+        // (factor-time scratch) or H^{-1} itself; the apply then uses F_pf
+        // directly (x_piv = H^{-1} (b_piv - F_pf x_fro)), so nothing n_p x nf
+        // beyond the block itself is kept
+        if (!bpf.dense) {
+          f.Xp = F->arena.d((size_t)N * std::max(1, e.pf.rank));
+          if (e.pf.rank) g0.push_back(GemmJob{f.Hinv, e.pf.col, f.Xp, N, e.pf.rank, N, N, e.pf.ldc, e.pf.rank, 1.0, 0.0});
+        } else if (nf <= N) {
+          f.Xp = ctx->scratch.d((size_t)N * nf);
+          g0.push_back(GemmJob{f.Hinv, bpf.val, f.Xp, N, nf, N, N, nf, nf, 1.0, 0.0});
+        } else {
+          f.Xp = f.Hinv;  // H^{-1} I (rank n_p = N, leading dimension N)
+        }
+        // upward apply operator RH = row_fp H^{-1} (low rank; a dense F_fp is
+        // applied to y_piv = H^{-1} b_piv directly)
+        if (!bfp.dense) {
+          f.RH = F->arena.d((size_t)std::max(1, e.fp.rank) * N);
+          if (e.fp.rank) g0.push_back(GemmJob{e.fp.row, f.Hinv, f.RH, e.fp.rank, N, N, e.fp.ldr, N, N, 1.0, 0.0});
+        }
         els.push_back(e);
       }
       run_gemm(s, g0);
@@ -2420,7 +2619,7 @@ struct Factorizer {
           // W = col_fp @ core (nf x r_pf), V = row_pf^T  -> Vt = row_pf
           f.rw = rpf;
           if (rpf) {
-            double *W = F->arena.d((size_t)f.nf * rpf);
+            double *W = upd.d((size_t)f.nf * rpf, release_height(f));
             g2.push_back(GemmJob{e.fp.col, core, W, f.nf, rpf, rfp, e.fp.ldc, rpf, rpf, 1.0, 0.0});
             f.W = W;
             f.ldw = rpf;
@@ -2432,7 +2631,7 @@ struct Factorizer {
           f.rw = rfp;
           f.W = e.fp.col;
           f.ldw = e.fp.ldc;
-          double *Vt = F->arena.d((size_t)rfp * f.nf);
+          double *Vt = upd.d((size_t)rfp * f.nf, release_height(f));
           g2.push_back(GemmJob{core, e.pf.row, Vt, rfp, f.nf, rpf, rpf, e.pf.ldr, f.nf, 1.0, 0.0});
           f.Vt = Vt;
           f.ldv = f.nf;
@@ -2612,6 +2811,65 @@ struct Factorizer {
       f.upd_reals = (int64_t)acc[4 * q + 2];
       f.hint = (int64_t)acc[4 * q + 3];
     }
+  }
+
+  // where the device memory of a factorization goes (MFH_MEM_TRACE=1): the
+  // retained arena by category, from the host-side metadata
+  void memory_breakdown() {
+    // retained (arena) categories, then the transient ones (release arena / scratch)
+    double cat[7] = {0}, tr[3] = {0};
+    const char *names[7] = {"dense Pinv/Gpf/Gfp", "dense Fpp", "pf/fp blocks", "pp inverse (Hinv|form)",
+                            "Xp/RH", "other", ""};
+    auto tree_bytes = [&](int tt) {
+      double s2 = 0;
+      if (tt < 0) return s2;
+      HTree &T = F->trees[tt];
+      for (int v = 0; v < T.nslots; ++v) {
+        if (T.leaf[v] == 1) {
+          double sz = T.hi[v] - T.lo[v];
+          s2 += 8 * sz * sz;
+        } else if (T.leaf[v] == 0) {
+          s2 += 8.0 * (F->blocks[T.up[v]].stored() + F->blocks[T.lw[v]].stored());
+        }
+      }
+      return s2;
+    };
+    int n_form = 0, n_struct = 0;
+    for (auto &f : F->fronts) {
+      if (f.nh == 0) continue;
+      if (!f.structured) {
+        cat[0] += 8.0 * ((double)f.npv * f.npv + 2.0 * f.npv * f.nf);
+        if (f.Fpp) cat[1] += 8.0 * f.npv * f.npv;
+        continue;
+      }
+      n_struct++;
+      tr[0] += tree_bytes(f.pp);
+      tr[1] += tree_bytes(f.ff);
+      if (f.W && f.W != as_factors(F->blocks[f.fp]).col) tr[2] += 8.0 * f.nf * f.rw;
+      if (f.Vt && f.Vt != as_factors(F->blocks[f.pf]).row) tr[2] += 8.0 * f.nf * f.rw;
+      if (f.pf >= 0) cat[2] += 8.0 * (F->blocks[f.pf].stored() + F->blocks[f.fp].stored());
+      if (!f.pform) {
+        cat[3] += 8.0 * f.npv * f.npv;
+      } else {
+        n_form++;
+        for (auto &L : f.tleaf) cat[3] += 8.0 * L.sz * (L.sz + L.K);
+        for (auto &t : f.tnode) cat[3] += 8.0 * (t.r1 + t.r2) * t.nv;
+      }
+      if (f.pf >= 0) {
+        const BlockH &bpf = F->blocks[f.pf], &bfp = F->blocks[f.fp];
+        cat[4] += 8.0 * f.npv * ((bpf.dense ? 0 : bpf.rank) + (bfp.dense ? 0 : bfp.rank));
+      }
+    }
+    double known = 0;
+    for (int q = 0; q < 5; ++q) known += cat[q];
+    cat[5] = (double)F->arena.capacity() - known;
+    fprintf(stderr, "[mfh mem] arena %.2f GB (peak in use %.2f GB), release arena peak %.2f GB, scratch %.2f GB; "
+            "%d of %d structured fronts in HODLR inverse form\n",
+            F->arena.capacity() / 1e9, F->arena.peak / 1e9, upd.peak / 1e9, ctx->scratch.capacity() / 1e9, n_form,
+            n_struct);
+    for (int q = 0; q < 6; ++q) fprintf(stderr, "[mfh mem]   retained %-24s %8.3f GB\n", names[q], cat[q] / 1e9);
+    fprintf(stderr, "[mfh mem]   transient pp trees %.3f GB, update trees %.3f GB, W/Vt %.3f GB\n", tr[0] / 1e9,
+            tr[1] / 1e9, tr[2] / 1e9);
   }
 
   void run(const CsrView &A, int mode) {
@@ -2841,11 +3099,17 @@ struct Factorizer {
       if (!(P.eps > 0.0 && P.eps < 1.0)) throw value_error("eps must lie in (0, 1)");
       if (P.n_leaf < 1) throw value_error("n_leaf must be positive");
       if (P.d < 1) throw value_error("distance must be at least 1");
-      // identity for DenseBlock.as_factors
-      F->ident_ld = (int)max_nh;
-      F->ident = F->arena.d((size_t)max_nh * max_nh);
-      Sink s{ctx};
-      run_identity(s, {F->ident}, {(int)max_nh}, {(int)max_nh});
+      // identity for DenseBlock.as_factors: a strip of 2 max_nh - 1 doubles with
+      // the one in the middle, read with leading dimension -1 (element (i, j) at
+      // center + j - i), instead of a max_nh^2 matrix (3 GB at C5). GEMMs with
+      // it become scaled copies (run_gemm); the GEMV kernels index with signed
+      // 64-bit arithmetic and read it directly.
+      double *strip = F->arena.d((size_t)2 * max_nh - 1);
+      CK(cudaMemsetAsync(strip, 0, sizeof(double) * (2 * max_nh - 1), ctx->s));
+      static const double one = 1.0;
+      CK(cudaMemcpyAsync(strip + (max_nh - 1), &one, sizeof(double), cudaMemcpyHostToDevice, ctx->s));
+      F->ident_ld = -1;
+      F->ident = strip + (max_nh - 1);
     }
     F->d_perm = (long long *)F->arena.alloc(sizeof(int64_t) * std::max<int64_t>(1, n));
     upload(ctx->s, F->d_perm, et->perm.data(), sizeof(int64_t) * n);
@@ -3091,6 +3355,7 @@ struct Factorizer {
     F->stats.stored_reals = retained;
     F->stats.device_bytes_peak =
         (int64_t)F->arena.capacity() + (int64_t)upd.peak + (int64_t)ctx->scratch.capacity();
+    if (getenv("MFH_MEM_TRACE")) memory_breakdown();
     // id views point into the tree's cache; nothing after the factorization
     // (the apply plan is already built) may read them
     for (auto &f : F->fronts) f.ids = IdsView{};
@@ -3106,6 +3371,9 @@ struct Factorizer {
 struct ApplyPlan {
   double *d_b = nullptr, *d_x = nullptr;  // user-facing input / output
   double *bu = nullptr, *xw = nullptr, *y = nullptr, *cbuf = nullptr, *xf = nullptr;
+  double *yb = nullptr;  // structured fronts: y_piv = H^{-1} b_piv from the upward pass, reused downward
+  double *ub = nullptr;  // dense-fallback F_pf: u_piv = b_piv - F_pf x_fro before its H^{-1}
+  double *wb = nullptr;  // HODLR inverse form: w_v = Tm_v b_v of every node
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
   // sharded: segment k + 1 runs after exchange k (buffer, count); the first
@@ -3227,10 +3495,11 @@ static GemvJob gemv(double *y, const double *y0, int m, const double *A1, int ld
   return GemvJob{y, y0, m, A1, lda1, k1, x1, a1, A2, lda2, k2, x2, idx2, a2, 0, 0, 0, 0};
 }
 // the same job with the vector strides of a several-right-hand-side plan
-static GemvJob strided(GemvJob j, long long ys, long long x1s, long long x2s) {
+static GemvJob strided(GemvJob j, long long ys, long long x1s, long long x2s, long long y0s = 0) {
   j.ys = ys;
   j.x1s = x1s;
   j.x2s = x2s;
+  j.y0s = y0s;
   return j;
 }
 
@@ -3252,6 +3521,18 @@ static std::unique_ptr<ApplyPlan> make_apply(mfh_factor *F, int nv) {
   AP->bu = ar.d(nv * nn1);
   AP->xw = ar.d(nv * nn1);
   AP->y = ar.d(nn1);
+  AP->yb = ar.d(nv * nn1);
+  AP->ub = ar.d(nv * nn1);
+  // w segments of the fronts kept in HODLR inverse form
+  std::vector<int64_t> wo(F->fronts.size(), 0);
+  int64_t wtot = 0;
+  for (size_t q = 0; q < F->fronts.size(); ++q)
+    if (F->fronts[q].structured && F->fronts[q].pform) {
+      wo[q] = wtot;
+      wtot += F->fronts[q].wlen;
+    }
+  const long long wst = std::max<int64_t>(1, wtot);
+  AP->wb = ar.d(nv * wst);
   // contribution CSR (symbolic: built once per tree, kept on the device per context)
   std::shared_ptr<Ctx::ApplySym> sym;
   // a several-vector plan is built after the factorization, when the front id
@@ -3312,7 +3593,7 @@ static std::unique_ptr<ApplyPlan> make_apply(mfh_factor *F, int nv) {
   Sink sk{ctx};
   sk.record = true;
   sk.persist = &ar;
-  double *bu = AP->bu, *xw = AP->xw, *y = AP->y, *cbuf = AP->cbuf;
+  double *bu = AP->bu, *xw = AP->xw, *y = AP->y, *cbuf = AP->cbuf, *yb = AP->yb, *wb = AP->wb, *ub = AP->ub;
   double bytes = 0;
   // apply levels count only pivot-carrying nodes: merge nodes (npv = 0) do no
   // solve work, and skipping them collapses the long merge chains.
@@ -3460,37 +3741,70 @@ static std::unique_ptr<ApplyPlan> make_apply(mfh_factor *F, int nv) {
           dgl, cnt, d_cptr, d_coff, cbuf, bu, nullptr, cst, nst);
       check_launch();
     });
-    std::vector<GemvJob> j0, j1, j2;
+    // three dependent stages at most: st[0] reads b_piv only, st[1] reads
+    // st[0]'s results, st[2] (HODLR inverse form with a dense F_fp) reads st[1]'s
+    std::vector<GemvJob> st[3];
     for (int q : fis) {
       FrontH &f = F->fronts[q];
-      if (f.nf == 0) continue;
       const double *bp = bu + f.piv_lo;
-      double *t = cbuf + off[q];
+      double *t = f.nf ? cbuf + off[q] : nullptr;
       if (!f.structured) {
-        j0.push_back(strided(gemv(t, nullptr, f.nf, f.Gfp, f.npv, f.npv, bp, 1.0), cst, nst, 0));
+        if (f.nf == 0) continue;
+        st[0].push_back(strided(gemv(t, nullptr, f.nf, f.Gfp, f.npv, f.npv, bp, 1.0), cst, nst, 0));
         bytes += 8.0 * (double)f.nf * f.npv;
+        continue;
+      }
+      // y_piv = H^{-1} b_piv, kept for the downward pass (b_u[piv] is final once
+      // this level's gather ran: only ancestors' pivots change after it)
+      double *yp = yb + f.piv_lo;
+      int ystage;  // the stage that writes y_piv
+      if (!f.pform) {
+        st[0].push_back(strided(gemv(yp, nullptr, f.npv, f.Hinv, f.npv, f.npv, bp, 1.0), nst, nst, 0));
+        bytes += 8.0 * (double)f.npv * f.npv;
+        ystage = 0;
       } else {
-        // t = col_fp (RH b_piv), RH = row_fp H^{-1} precomputed at factor time
-        FacView fpv = fac_view(F, F->blocks[f.fp]);
-        if (fpv.rank) {
-          double *tmp = ar.d((size_t)nv * fpv.rank);
-          j1.push_back(strided(gemv(tmp, nullptr, fpv.rank, f.RH, f.npv, f.npv, bp, 1.0), fpv.rank, nst, 0));
-          j2.push_back(strided(gemv(t, nullptr, f.nf, fpv.col, fpv.ldc, fpv.rank, tmp, 1.0), cst, fpv.rank, 0));
-          bytes += 8.0 * ((double)fpv.rank * f.npv + (double)f.nf * fpv.rank);
-        } else {
-          j2.push_back(strided(gemv(t, nullptr, f.nf, nullptr, 0, 0, nullptr, 0.0), cst, 0, 0));  // exact zero contribution
+        // HODLR inverse form: every w_v = Tm_v b_v at once, then per leaf
+        // y_leaf = L^{-1} b_leaf - XL w[idx] (all ancestors' corrections)
+        double *w = wb + wo[q];
+        for (auto &tn : f.tnode) {
+          const int rr = tn.r1 + tn.r2;
+          st[0].push_back(strided(gemv(w + tn.woff, nullptr, rr, tn.Tm, tn.nv, tn.nv, bp + tn.lo, 1.0), wst, nst, 0));
+          bytes += 8.0 * (double)rr * tn.nv;
         }
+        for (auto &L : f.tleaf) {
+          if (L.K)
+            st[1].push_back(strided(gemv(yp + L.lo, nullptr, L.sz, L.Linv, L.sz, L.sz, bp + L.lo, 1.0, L.XL, L.K, L.K,
+                                         w, L.idx, -1.0),
+                                    nst, nst, wst));
+          else
+            st[1].push_back(strided(gemv(yp + L.lo, nullptr, L.sz, L.Linv, L.sz, L.sz, bp + L.lo, 1.0), nst, nst, 0));
+          bytes += 8.0 * (double)L.sz * (L.sz + L.K);
+        }
+        ystage = 1;
+      }
+      if (f.nf == 0) continue;
+      // t = F_fp H^{-1} b_piv: F_fp y_piv (dense fallback) or col_fp (RH b_piv) (low rank)
+      const BlockH &bfp = F->blocks[f.fp];
+      if (bfp.dense) {
+        st[ystage + 1].push_back(strided(gemv(t, nullptr, f.nf, bfp.val, f.npv, f.npv, yp, 1.0), cst, nst, 0));
+        bytes += 8.0 * (double)f.nf * f.npv;
+      } else if (bfp.rank) {
+        const int r = bfp.rank;
+        double *tmp = ar.d((size_t)nv * r);
+        st[0].push_back(strided(gemv(tmp, nullptr, r, f.RH, f.npv, f.npv, bp, 1.0), r, nst, 0));
+        st[1].push_back(strided(gemv(t, nullptr, f.nf, bfp.col, r, r, tmp, 1.0), cst, r, 0));
+        bytes += 8.0 * ((double)r * f.npv + (double)f.nf * r);
+      } else {
+        st[1].push_back(strided(gemv(t, nullptr, f.nf, nullptr, 0, 0, nullptr, 0.0), cst, 0, 0));  // exact zero contribution
       }
     }
-    j0.insert(j0.end(), j1.begin(), j1.end());  // independent: one launch
     if (atrace) {
       int64_t mr = 0;
       for (int q : fis) mr = std::max<int64_t>(mr, F->fronts[q].npv);
-      fprintf(stderr, "[mfh apply up %2d] fronts %5zu gather %7d jobs %5zu+%5zu max npv %5lld\n", h, fis.size(), cnt,
-              j0.size(), j2.size(), (long long)mr);
+      fprintf(stderr, "[mfh apply up %2d] fronts %5zu gather %7d jobs %5zu+%5zu+%5zu max npv %5lld\n", h, fis.size(), cnt,
+              st[0].size(), st[1].size(), st[2].size(), (long long)mr);
     }
-    run_gemv(sk, j0, nv);
-    run_gemv(sk, j2, nv);
+    for (auto &v : st) run_gemv(sk, v, nv);
   }
   };
   // ---------------- downward: x[piv] = pp_solve(b_u[piv] - apply_pf(x[fro]))
@@ -3499,43 +3813,69 @@ static std::unique_ptr<ApplyPlan> make_apply(mfh_factor *F, int nv) {
     if (sh && ex_dn[h]) exchange_point(xw, x_mask, x_tmp, std::max<int64_t>(1, n));
     auto &fis = byh[h];
     if (fis.empty()) continue;
-    std::vector<GemvJob> ja, jb;
+    // stages: sa[0] reads x_fro (final), sa[1] writes x_piv, except a dense
+    // F_pf in HODLR inverse form: u, w = Tm u, then the leaves (sa[2])
+    std::vector<GemvJob> sa[3];
     for (int q : fis) {
       FrontH &f = F->fronts[q];
       const double *bp = bu + f.piv_lo;
       double *xv = xw + f.piv_lo;
       const long long *fro = f.nf ? d_fro + off[q] : nullptr;
       if (!f.structured) {
-        jb.push_back(strided(gemv(xv, nullptr, f.npv, f.Pinv, f.npv, f.npv, bp, 1.0, f.Gpf, f.nf, f.nf, xw, fro, -1.0),
-                             nst, nst, nst));
+        sa[1].push_back(strided(gemv(xv, nullptr, f.npv, f.Pinv, f.npv, f.npv, bp, 1.0, f.Gpf, f.nf, f.nf, xw, fro, -1.0),
+                                nst, nst, nst));
         bytes += 8.0 * ((double)f.npv * f.npv + (double)f.npv * f.nf);
         continue;
       }
-      // x_piv = H^{-1} b_piv - Xp (row_pf x_fro), Xp = H^{-1} col_pf precomputed
-      FacView pfv;
-      if (f.nf) pfv = fac_view(F, F->blocks[f.pf]);
-      if (f.nf && pfv.rank) {
-        double *tmp = ar.d((size_t)nv * pfv.rank);
-        ja.push_back(strided(
-            gemv(tmp, nullptr, pfv.rank, nullptr, 0, 0, nullptr, 0.0, pfv.row, pfv.ldr, f.nf, xw, fro, 1.0), pfv.rank, 0,
-            nst));
-        jb.push_back(strided(gemv(xv, nullptr, f.npv, f.Hinv, f.npv, f.npv, bp, 1.0, f.Xp, pfv.rank, pfv.rank, tmp,
-                                  nullptr, -1.0),
-                             nst, nst, pfv.rank));
-        bytes += 8.0 * ((double)f.npv * f.npv + (double)f.npv * pfv.rank + (double)pfv.rank * f.nf);
+      // x_piv = y_piv - Xp (row_pf x_fro) (low rank), y_piv (no coupling), or
+      // H^{-1} (b_piv - F_pf x_fro) (dense fallback); y_piv = H^{-1} b_piv
+      const double *yp = yb + f.piv_lo;
+      const BlockH *bpf = f.nf ? &F->blocks[f.pf] : nullptr;
+      if (bpf && bpf->dense) {
+        double *u = ub + f.piv_lo;
+        sa[0].push_back(strided(gemv(u, bp, f.npv, nullptr, 0, 0, nullptr, 0.0, bpf->val, f.nf, f.nf, xw, fro, -1.0), nst,
+                                0, nst, nst));
+        bytes += 8.0 * (double)f.npv * f.nf;
+        if (!f.pform) {
+          sa[1].push_back(strided(gemv(xv, nullptr, f.npv, f.Hinv, f.npv, f.npv, u, 1.0), nst, nst, 0));
+          bytes += 8.0 * (double)f.npv * f.npv;
+        } else {
+          double *w = wb + wo[q];
+          for (auto &tn : f.tnode) {
+            const int rr = tn.r1 + tn.r2;
+            sa[1].push_back(strided(gemv(w + tn.woff, nullptr, rr, tn.Tm, tn.nv, tn.nv, u + tn.lo, 1.0), wst, nst, 0));
+            bytes += 8.0 * (double)rr * tn.nv;
+          }
+          for (auto &L : f.tleaf) {
+            if (L.K)
+              sa[2].push_back(strided(gemv(xv + L.lo, nullptr, L.sz, L.Linv, L.sz, L.sz, u + L.lo, 1.0, L.XL, L.K, L.K,
+                                           w, L.idx, -1.0),
+                                      nst, nst, wst));
+            else
+              sa[2].push_back(strided(gemv(xv + L.lo, nullptr, L.sz, L.Linv, L.sz, L.sz, u + L.lo, 1.0), nst, nst, 0));
+            bytes += 8.0 * (double)L.sz * (L.sz + L.K);
+          }
+        }
+      } else if (bpf && bpf->rank) {
+        const int r = bpf->rank;
+        double *tmp = ar.d((size_t)nv * r);
+        sa[0].push_back(strided(gemv(tmp, nullptr, r, nullptr, 0, 0, nullptr, 0.0, bpf->row, f.nf, f.nf, xw, fro, 1.0),
+                                r, 0, nst));
+        sa[1].push_back(strided(gemv(xv, yp, f.npv, nullptr, 0, 0, nullptr, 0.0, f.Xp, r, r, tmp, nullptr, -1.0), nst, 0,
+                                r, nst));
+        bytes += 8.0 * ((double)f.npv * r + (double)r * f.nf);
       } else {
-        jb.push_back(strided(gemv(xv, nullptr, f.npv, f.Hinv, f.npv, f.npv, bp, 1.0), nst, nst, 0));
-        bytes += 8.0 * (double)f.npv * f.npv;
+        sa[1].push_back(strided(gemv(xv, yp, f.npv, nullptr, 0, 0, nullptr, 0.0), nst, 0, 0, nst));
       }
     }
     if (atrace) {
       double lb = 0;
-      for (auto &j : jb) lb += 8.0 * (double)j.m * (j.k1 + j.k2);
-      for (auto &j : ja) lb += 8.0 * (double)j.m * (j.k1 + j.k2);
-      fprintf(stderr, "[mfh apply dn %2d] jobs %5zu+%5zu  %.2f MB\n", h, ja.size(), jb.size(), lb / 1e6);
+      for (auto &v : sa)
+        for (auto &j : v) lb += 8.0 * (double)j.m * (j.k1 + j.k2);
+      fprintf(stderr, "[mfh apply dn %2d] jobs %5zu+%5zu+%5zu  %.2f MB\n", h, sa[0].size(), sa[1].size(), sa[2].size(),
+              lb / 1e6);
     }
-    run_gemv(sk, ja, nv);
-    run_gemv(sk, jb, nv);
+    for (auto &v : sa) run_gemv(sk, v, nv);
   }
   };
   upward(byh);
@@ -3702,12 +4042,16 @@ extern "C" int mfh_ctx_create(int device, mfh_ctx **out) {
   CK(cudaMalloc(&c->c.d_part, sizeof(double) * (RED_BLOCKS + 64)));
   CK(cudaMalloc(&c->c.d_scal, sizeof(double) * 4096));
   CK(cudaMallocHost(&c->c.h_scal, sizeof(double) * 4096));
+  device_setup(&c->c);
   *out = c;
   MFH_CATCH
 }
 
 extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   if (!ctx) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.s);
   ctx->c.stage.release();
   ctx->c.scratch.release();
@@ -3737,6 +4081,7 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   cudaStreamDestroy(ctx->c.side2);
   cudaStreamDestroy(ctx->c.s);
   delete ctx;
+  if (prev >= 0) cudaSetDevice(prev);
 }
 
 extern "C" int mfh_ctx_info(mfh_ctx *ctx, void **stream, int64_t *launches) {
@@ -3748,6 +4093,7 @@ extern "C" int mfh_ctx_info(mfh_ctx *ctx, void **stream, int64_t *launches) {
 
 extern "C" int mfh_ctx_sync(mfh_ctx *ctx) {
   std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
+  DeviceGuard dg_(ctx->c.device);
   MFH_TRY
   CK(cudaStreamSynchronize(ctx->c.s));
   MFH_CATCH
@@ -3761,7 +4107,7 @@ static int factorize_common(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const i
   MFH_TRY
   if (mode != MFH_CONVENTIONAL && mode != MFH_ACCELERATED) throw value_error("unknown mode");
   if (t->n != n) throw value_error("separator tree size does not match the matrix");
-  CK(cudaSetDevice(ctx->c.device));
+  DeviceGuard dg_(ctx->c.device);
   CsrView A{n, indptr, indices, values};  // the caller's arrays, read-only (no copy)
   F = new mfh_factor();
   F->ctx = &ctx->c;
@@ -3872,6 +4218,7 @@ extern "C" int mfh_factor_blocks(const mfh_factor *f, int64_t *n_blocks, int64_t
 extern "C" void mfh_factor_free(mfh_factor *f) {
   if (!f) return;
   std::lock_guard<std::recursive_mutex> lk_(f->ctx->mu);
+  DeviceGuard dg_(f->ctx->device);
   cudaStreamSynchronize(f->ctx->s);
   f->arena.release();
   delete f;
@@ -3880,6 +4227,7 @@ extern "C" void mfh_factor_free(mfh_factor *f) {
 extern "C" int mfh_apply(mfh_factor *f, const double *b, double *x, int64_t nrhs, int on_device) {
   std::lock_guard<std::recursive_mutex> lk_(f->ctx->mu);
   MFH_TRY
+  DeviceGuard dg_(f->ctx->device);
   Ctx *ctx = f->ctx;
   int64_t n = f->n;
   if (!f->apply) build_apply(f);
@@ -3911,6 +4259,7 @@ extern "C" int mfh_apply(mfh_factor *f, const double *b, double *x, int64_t nrhs
 extern "C" int mfh_node_op(mfh_factor *f, int64_t node, int op, const double *x, double *y) {
   std::lock_guard<std::recursive_mutex> lk_(f->ctx->mu);
   MFH_TRY
+  DeviceGuard dg_(f->ctx->device);
   using namespace mfh;
   Ctx *ctx = f->ctx;
   int q = -1;
@@ -3923,7 +4272,7 @@ extern "C" int mfh_node_op(mfh_factor *f, int64_t node, int op, const double *x,
   const int npv = fr.npv, nf = fr.nf;
   const int nin = op == 1 ? nf : npv, nout = op == 2 ? nf : npv;
   if (nout == 0) return MFH_OK;
-  if (npv == 0) {  // merge node: F_fp is nf x 0
+  if (npv == 0 || nin == 0) {  // merge node (F_fp is nf x 0) or F_pf with no columns
     std::memset(y, 0, sizeof(double) * nout);
     return MFH_OK;
   }
@@ -3932,14 +4281,24 @@ extern "C" int mfh_node_op(mfh_factor *f, int64_t node, int op, const double *x,
   if (nin) CK(cudaMemcpyAsync(dx, x, sizeof(double) * nin, cudaMemcpyHostToDevice, ctx->s));
   Sink sk{ctx};
   std::vector<GemvJob> g1, g2;
-  if (op == 0) {
+  if (op == 0 && fr.structured && fr.pform) {
+    // HODLR inverse form: w_v = Tm_v x_v for every node, then the leaves
+    double *dw = ctx->scratch.d(std::max<int64_t>(1, fr.wlen));
+    for (auto &tn : fr.tnode) g1.push_back(gemv(dw + tn.woff, nullptr, tn.r1 + tn.r2, tn.Tm, tn.nv, tn.nv, dx + tn.lo, 1.0));
+    for (auto &L : fr.tleaf)
+      g2.push_back(L.K ? gemv(dy + L.lo, nullptr, L.sz, L.Linv, L.sz, L.sz, dx + L.lo, 1.0, L.XL, L.K, L.K, dw, L.idx, -1.0)
+                       : gemv(dy + L.lo, nullptr, L.sz, L.Linv, L.sz, L.sz, dx + L.lo, 1.0));
+  } else if (op == 0) {
     g1.push_back(gemv(dy, nullptr, npv, fr.structured ? fr.Hinv : fr.Pinv, npv, npv, dx, 1.0));
   } else if (!fr.structured) {
-    // the front buffer keeps F_pf (rows 0..npv, cols npv..) and F_fp (rows npv.., cols 0..npv)
-    if (op == 1)
-      g1.push_back(gemv(dy, nullptr, npv, fr.Fpf, nf, nf, dx, 1.0));
-    else
-      g1.push_back(gemv(dy, nullptr, nf, fr.Ffp, npv, npv, dx, 1.0));
+    // F_pf v = F_pp (Gpf v), F_fp v = Gfp (F_pp v)  (Gpf = F_pp^{-1} F_pf, Gfp = F_fp F_pp^{-1})
+    if (op == 1) {
+      g1.push_back(gemv(dt, nullptr, npv, fr.Gpf, nf, nf, dx, 1.0));
+      g2.push_back(gemv(dy, nullptr, npv, fr.Fpp, npv, npv, dt, 1.0));
+    } else {
+      g1.push_back(gemv(dt, nullptr, npv, fr.Fpp, npv, npv, dx, 1.0));
+      g2.push_back(gemv(dy, nullptr, nf, fr.Gfp, npv, npv, dt, 1.0));
+    }
   } else {
     FacView v = fac_view(f, f->blocks[op == 1 ? fr.pf : fr.fp]);
     if (v.rank == 0) {
@@ -3961,6 +4320,7 @@ extern "C" int mfh_node_op(mfh_factor *f, int64_t node, int op, const double *x,
 extern "C" int mfh_apply_bench(mfh_factor *f, int64_t reps, double *ms_per_apply, double *bytes_per_apply) {
   std::lock_guard<std::recursive_mutex> lk_(f->ctx->mu);
   MFH_TRY
+  DeviceGuard dg_(f->ctx->device);
   Ctx *ctx = f->ctx;
   if (!f->apply) build_apply(f);
   ApplyPlan *A = f->apply.get();
@@ -4011,6 +4371,7 @@ extern "C" int mfh_csr_create(mfh_ctx *ctx, int64_t n_rows, int64_t n_cols, cons
                               const int64_t *indices, const double *values, mfh_csr **out) {
   std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
   MFH_TRY
+  DeviceGuard dg_(ctx->c.device);
   auto *A = new mfh_csr();
   A->ctx = &ctx->c;
   A->kind = 0;
@@ -4033,6 +4394,7 @@ extern "C" int mfh_csr_create(mfh_ctx *ctx, int64_t n_rows, int64_t n_cols, cons
 extern "C" int mfh_dense_create(mfh_ctx *ctx, int64_t n, const double *values, mfh_csr **out) {
   std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
   MFH_TRY
+  DeviceGuard dg_(ctx->c.device);
   auto *A = new mfh_csr();
   A->ctx = &ctx->c;
   A->kind = 1;
@@ -4047,6 +4409,7 @@ extern "C" int mfh_dense_create(mfh_ctx *ctx, int64_t n, const double *values, m
 extern "C" void mfh_csr_free(mfh_csr *A) {
   if (!A) return;
   std::lock_guard<std::recursive_mutex> lk_(A->ctx->mu);
+  DeviceGuard dg_(A->ctx->device);
   cudaStreamSynchronize(A->ctx->s);
   cudaFree(A->ptr);
   cudaFree(A->col);
@@ -4057,6 +4420,7 @@ extern "C" void mfh_csr_free(mfh_csr *A) {
 extern "C" int mfh_spmv(mfh_csr *A, const double *x, double *y, int on_device) {
   std::lock_guard<std::recursive_mutex> lk_(A->ctx->mu);
   MFH_TRY
+  DeviceGuard dg_(A->ctx->device);
   Ctx *ctx = A->ctx;
   if (on_device) {
     op_apply_device(A, x, y);
@@ -4529,6 +4893,7 @@ static int gmres_common(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const
                         double tol, int64_t max_iter, int64_t restart, double *hist, int64_t *n_hist,
                         int64_t *iterations, int *converged) {
   MFH_TRY
+  DeviceGuard dg_(ctx->c.device);
   GmresRun g{&ctx->c, ops, n};
   std::vector<double> res;
   int64_t its = 0;
@@ -4582,6 +4947,7 @@ static int gmres_batched_common(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t 
                                 double *d_x, double tol, int64_t max_iter, int64_t restart, double *hist,
                                 int64_t hist_cap, int64_t *n_hist, int64_t *iterations, int *converged) {
   MFH_TRY
+  DeviceGuard dg_(ctx->c.device);
   if (nrhs < 0) throw value_error("nrhs must be non-negative");
   auto tg0 = std::chrono::steady_clock::now();
   double sync_ms = 0.0;
@@ -4649,6 +5015,7 @@ extern "C" int mfh_full_pivot_lu_batched(mfh_ctx *ctx, int64_t batch, const int6
                                          int64_t *ranks, double *ratios, int64_t *status, double *err) {
   std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
   MFH_TRY
+  DeviceGuard dg_(ctx->c.device);
   Ctx *c = &ctx->c;
   if (batch == 0) return MFH_OK;
   double *d_blocks = c->scratch.d(std::max<int64_t>(1, total));
@@ -4735,6 +5102,7 @@ extern "C" int mfh_test_inverse_batched(mfh_ctx *ctx, int64_t batch, const int64
                                         double *blocks, int64_t total, int *singular) {
   std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
   MFH_TRY
+  DeviceGuard dg_(ctx->c.device);
   Ctx *c = &ctx->c;
   if (batch == 0) return MFH_OK;
   double *d_blocks = c->scratch.d(std::max<int64_t>(1, total));

@@ -495,6 +495,25 @@ __global__ void k_copy(const CopyJob *__restrict__ jobs, int njobs) {
   }
 }
 
+// C = alpha X + beta C (m x n): a GEMM whose other operand is an identity
+// (DenseBlock.as_factors' eye, stored as a strip with leading dimension -1).
+// Same epilogue expression as k_gemm, and the identity product is exact there,
+// so the result is the GEMM's bit for bit.
+__global__ void k_axpby(const GemmJob *__restrict__ jobs, const int *__restrict__ which) {
+  const GemmJob J = jobs[blockIdx.y];
+  const bool a_is_eye = which[blockIdx.y] == 0;
+  const double *X = a_is_eye ? J.B : J.A;
+  const long long ldx = a_is_eye ? J.ldb : J.lda;
+  const long long total = (long long)J.m * J.n;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / J.n), j = (int)(e % J.n);
+    double *cp = J.C + (long long)i * J.ldc + j;
+    const double v = J.alpha * X[(long long)i * ldx + j];
+    *cp = (J.beta == 0.0) ? v : J.beta * (*cp) + v;
+  }
+}
+
 // identity in an m x m block (ld)
 __global__ void k_identity(double *const *__restrict__ ptrs, const int *__restrict__ dims,
                            const int *__restrict__ lds) {

@@ -11,6 +11,8 @@
 //   etree                <- ordering.py:264-312
 #include <algorithm>
 #include <cstring>
+#include <memory>
+#include <string>
 
 #include "internal.h"
 
@@ -505,3 +507,74 @@ extern "C" int mfh_etree_fetch(const mfh_etree *t, int64_t *post_order, int64_t 
 }
 
 extern "C" void mfh_etree_free(mfh_etree *t) { delete t; }
+
+// The caller's own elimination tree (the reference's EliminationTree,
+// ordering.py:238-261, flattened), validated against what the numeric
+// factorization relies on.
+extern "C" int mfh_etree_from_arrays(int64_t n, const int64_t *perm, int64_t n_nodes, int64_t root,
+                                     const int64_t *parent, const int64_t *child_ptr, const int64_t *child,
+                                     int64_t n_post, const int64_t *post_order, const int64_t *piv_ptr,
+                                     const int64_t *piv, const int64_t *fr_ptr, const int64_t *fr,
+                                     mfh_etree **out) {
+  MFH_TRY
+  if (n < 0 || n_nodes < 0 || n_post < 0) throw value_error("elimination tree sizes must be non-negative");
+  std::vector<char> seen((size_t)std::max<int64_t>(n, 1), 0);
+  for (int64_t i = 0; i < n; ++i) {
+    if (perm[i] < 0 || perm[i] >= n || seen[perm[i]]) throw value_error("permutation is not a permutation of 0..n-1");
+    seen[perm[i]] = 1;
+  }
+  if (n_nodes == 0 ? root != -1 : (root < 0 || root >= n_nodes)) throw value_error("root is not a node of the tree");
+  auto *t = new mfh_etree();
+  std::unique_ptr<mfh_etree> guard(t);
+  static std::atomic<uint64_t> next_uid{1ull << 62};  // disjoint from mfh_etree_create's uids
+  t->uid = next_uid++;
+  t->n = n;
+  t->root = root;
+  t->perm.assign(perm, perm + n);
+  t->parent.assign(parent, parent + n_nodes);
+  t->children.assign(n_nodes, {});
+  for (int64_t v = 0; v < n_nodes; ++v) {
+    if (parent[v] < -1 || parent[v] >= n_nodes) throw value_error("parent of node " + std::to_string(v) + " out of range");
+    for (int64_t q = child_ptr[v]; q < child_ptr[v + 1]; ++q) {
+      const int64_t c = child[q];
+      if (c < 0 || c >= n_nodes || parent[c] != v)
+        throw value_error("children of node " + std::to_string(v) + " disagree with the parent array");
+      t->children[v].push_back(c);
+    }
+  }
+  // post order: every node once, children before their parent
+  std::vector<char> done((size_t)std::max<int64_t>(n_nodes, 1), 0);
+  t->post.assign(post_order, post_order + n_post);
+  for (int64_t p : t->post) {
+    if (p < 0 || p >= n_nodes || done[p]) throw value_error("post order repeats or leaves the tree");
+    for (int64_t c : t->children[p])
+      if (!done[c]) throw value_error("post order visits node " + std::to_string(p) + " before its child");
+    done[p] = 1;
+  }
+  if (n_post != n_nodes) throw value_error("post order must visit every node");
+  t->piv_ptr.assign(piv_ptr, piv_ptr + n_nodes + 1);
+  t->fr_ptr.assign(fr_ptr, fr_ptr + n_nodes + 1);
+  t->piv.assign(piv, piv + piv_ptr[n_nodes]);
+  t->fr.assign(fr, fr + fr_ptr[n_nodes]);
+  std::fill(seen.begin(), seen.end(), 0);
+  for (int64_t v = 0; v < n_nodes; ++v) {
+    const int64_t pb = piv_ptr[v], pe = piv_ptr[v + 1], fb = fr_ptr[v], fe = fr_ptr[v + 1];
+    if (pb > pe || fb > fe) throw value_error("index pointers must be non-decreasing");
+    for (int64_t q = pb; q < pe; ++q) {
+      if (piv[q] < 0 || piv[q] >= n || seen[piv[q]]) throw value_error("pivot ids must cover 0..n-1 exactly once");
+      seen[piv[q]] = 1;
+      if (q > pb && piv[q] != piv[q - 1] + 1)
+        throw value_error("pivot ids of node " + std::to_string(v) + " are not a contiguous run");
+    }
+    for (int64_t q = fb; q < fe; ++q) {
+      if (fr[q] < 0 || fr[q] >= n || (q > fb && fr[q] <= fr[q - 1]))
+        throw value_error("frontal ids of node " + std::to_string(v) + " must be sorted and in range");
+    }
+    if (pe > pb && fe > fb && fr[fb] <= piv[pe - 1])  // the reference's RuntimeError (ordering.py:303-306)
+      throw runtime_error("node " + std::to_string(v) + ": frontal index below the pivot block");
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (!seen[i]) throw value_error("pivot ids must cover 0..n-1 exactly once");
+  *out = guard.release();
+  MFH_CATCH
+}

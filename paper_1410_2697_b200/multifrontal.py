@@ -14,6 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
+from .ordering import etree_handle
 from .sparse import SparseMatrix
 
 CONVENTIONAL = "conventional"
@@ -204,14 +205,13 @@ def mf_factorize(A, tree, mode=CONVENTIONAL, params=None):
     params = params or MfParams()
     if not isinstance(A, SparseMatrix):
         A = SparseMatrix(A)
-    if tree._h is None:
-        raise ValueError("elimination tree must come from build_elimination_tree")
+    th = etree_handle(tree)  # ours, or the caller's own tree (e.g. the reference's) flattened as is
     ctx = _lib.context()
     ip, ix, dv = A.csr_arrays()
     p = _lib.mfh_params(int(min(params.n_c, 2**62)), float(params.eps), int(params.d),
                         int(params.n_leaf), -1 if params.max_rank is None else int(params.max_rank))
     h = C.c_void_p()
-    _lib.check(_lib.lib().mfh_factorize(ctx.handle, tree._h, A.n_rows, _lib.ptr(ip), _lib.ptr(ix),
+    _lib.check(_lib.lib().mfh_factorize(ctx.handle, th, A.n_rows, _lib.ptr(ip), _lib.ptr(ix),
                                         _lib.ptr(dv), 1 if mode == ACCELERATED else 0, C.byref(p),
                                         C.byref(h)))
     return MfFactorization(h, mode, params, tree, ctx)

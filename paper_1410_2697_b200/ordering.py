@@ -178,3 +178,69 @@ def build_elimination_tree(tree, A):
         nodes[v] = et
     post_order = [int(p) for p in post[:nn]]
     return EliminationTree(nodes, post_order, perm, tree.root, h)
+
+
+class _ForeignTree:
+    """Owns the native copy of a caller-built elimination tree."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib.lib().mfh_etree_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def etree_handle(tree):
+    """The native elimination tree for ``tree``: its own handle when it came
+    from ``build_elimination_tree``; otherwise (e.g. the reference's
+    ``EliminationTree``, ordering.py:238-261) the caller's tree is flattened
+    and handed over as is through ``mfh_etree_from_arrays`` -- nothing is
+    recomputed, so any leaf size or ordering the caller used is honoured."""
+    h = getattr(tree, "_h", None)
+    if h:
+        return h
+    cached = getattr(tree, "_mfh_foreign", None)
+    if cached is not None:
+        return cached.h
+    nodes = tree.nodes
+    nn = len(nodes)
+    perm = np.ascontiguousarray(np.asarray(tree.permutation, dtype=np.int64))
+    parent = np.full(max(1, nn), -1, dtype=np.int64)
+    cptr = np.zeros(nn + 1, dtype=np.int64)
+    kids, pivs, frs = [], [], []
+    pptr = np.zeros(nn + 1, dtype=np.int64)
+    fptr = np.zeros(nn + 1, dtype=np.int64)
+    for v in range(nn):
+        nd = nodes[v]
+        ch = [] if nd is None else list(nd.children or [])
+        pv = np.zeros(0, np.int64) if nd is None else np.asarray(nd.pivot_ids, dtype=np.int64)
+        fr = np.zeros(0, np.int64) if nd is None else np.asarray(nd.frontal_ids, dtype=np.int64)
+        if nd is not None and nd.parent is not None:
+            parent[v] = int(nd.parent)
+        kids += [int(c) for c in ch]
+        pivs.append(pv)
+        frs.append(fr)
+        cptr[v + 1] = cptr[v] + len(ch)
+        pptr[v + 1] = pptr[v] + len(pv)
+        fptr[v + 1] = fptr[v] + len(fr)
+    child = np.array(kids if kids else [0], dtype=np.int64)
+    piv = np.concatenate(pivs) if pptr[-1] else np.zeros(1, np.int64)
+    fr = np.concatenate(frs) if fptr[-1] else np.zeros(1, np.int64)
+    post = np.array(list(tree.post_order) or [0], dtype=np.int64)
+    root = -1 if tree.root is None else int(tree.root)
+    h = C.c_void_p()
+    _lib.check(_lib.lib().mfh_etree_from_arrays(len(perm), _lib.ptr(perm), nn, root, _lib.ptr(parent),
+                                                _lib.ptr(cptr), _lib.ptr(child), len(tree.post_order),
+                                                _lib.ptr(post), _lib.ptr(pptr), _lib.ptr(piv), _lib.ptr(fptr),
+                                                _lib.ptr(fr), C.byref(h)))
+    owner = _ForeignTree(h)
+    try:
+        tree._mfh_foreign = owner
+    except AttributeError:
+        pass
+    return owner.h

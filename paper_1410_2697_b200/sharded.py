@@ -24,6 +24,7 @@ import traceback
 
 import numpy as np
 
+from .ordering import etree_handle
 from . import _lib
 from .multifrontal import ACCELERATED, CONVENTIONAL, MfFactorization, MfParams, mf_factorize
 from .sparse import SparseMatrix
@@ -176,7 +177,7 @@ def mf_factorize_sharded(A, tree, mode=ACCELERATED, params=None, group=None, par
     p = _lib.mfh_params(int(min(params.n_c, 2**62)), float(params.eps), int(params.d),
                         int(params.n_leaf), -1 if params.max_rank is None else int(params.max_rank))
     h = C.c_void_p()
-    _lib.check(_lib.lib().mfh_factorize_sharded(ctx.handle, tree._h, A.n_rows, _lib.ptr(ip), _lib.ptr(ix),
+    _lib.check(_lib.lib().mfh_factorize_sharded(ctx.handle, etree_handle(tree), A.n_rows, _lib.ptr(ip), _lib.ptr(ix),
                                                 _lib.ptr(dv), 1 if mode == ACCELERATED else 0, C.byref(p),
                                                 C.byref(sh), C.byref(h)))
     F = MfFactorization(h, mode, params, tree, ctx)

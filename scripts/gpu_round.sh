@@ -6,7 +6,7 @@ export PYTHONFAULTHANDLER=1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.used --format=csv > gpurun_out/gpu.txt 2>&1
 for f in ${TEST_FILES:-tests/test_gpu_kernels.py tests/test_gpu_mf.py tests/test_gpu_gmres.py}; do
   b=$(basename $f .py)
-  timeout ${TEST_TIMEOUT:-300} python -m pytest $f -m gpu -v -x -p no:cacheprovider --timeout ${PYTEST_TIMEOUT:-120} > gpurun_out/$b.log 2>&1
+  timeout ${TEST_TIMEOUT:-300} python -m pytest $f -m gpu -v -x -rA -p no:cacheprovider ${PYTEST_EXTRA:-} --timeout ${PYTEST_TIMEOUT:-120} > gpurun_out/$b.log 2>&1
   echo "$b rc=$?" >> gpurun_out/summary.txt
 done
 if [ -n "${SMOKE:-1}" ]; then

@@ -280,3 +280,33 @@ def test_singular_structured_leaf_matches_reference_message(oracle):
     with pytest.raises(ValueError) as got:
         P.mf_factorize(P.SparseMatrix(Zc), tree, P.ACCELERATED, P.MfParams(**kw))
     assert str(got.value) == str(ref.value)
+
+
+@pytest.mark.parametrize("name", ["acc_p7_16", "acc_hex_8", "acc_p7_10_d2"])
+def test_pivot_block_forms_agree(monkeypatch, name):
+    """a14/a15: a structured front keeps its pivot-block inverse either as the
+    explicit n_p^2 matrix or in HODLR inverse form (leaf inverses + per node
+    X_v, Tm_v; H^{-1} = blockdiag(L^{-1}) - sum_v X_v Tm_v), whichever is
+    smaller. Both forms are the same exact inverse of the compressed operator:
+    forcing either gives the same preconditioner to rounding, the same integer
+    accounting, and node_factors' pp_solve agrees."""
+    import paper_1410_2697_b200 as P
+    gen, leaf, mode, kw = MF[name]
+    A, _ = gen()
+    et = P.build_elimination_tree(P.nested_dissection(P.adjacency_graph(A), leaf), A)
+    b = np.random.default_rng(5).standard_normal(A.n_rows)
+    out = {}
+    for form in ("0", "1"):
+        monkeypatch.setenv("MFH_PFORM", form)
+        F = P.mf_factorize(A, et, mode, P.MfParams(**kw))
+        x = P.mf_solve(F, b)
+        nf = {p: v for p, v in F.node_factors.items() if v is not None and v.kind == "structured" and v.n_pivot}
+        v = np.random.default_rng(1).standard_normal(max(f.n_pivot for f in nf.values()))
+        pps = {p: f.pp_solve(v[:f.n_pivot]) for p, f in nf.items()}
+        out[form] = (x, F.stats.peak_stored_reals, F.stored_reals(), pps)
+    (x0, pk0, st0, pp0), (x1, pk1, st1, pp1) = out["0"], out["1"]
+    assert (pk0, st0) == (pk1, st1)
+    assert np.linalg.norm(x1 - x0) <= 1e-10 * np.linalg.norm(x0)
+    assert pp0.keys() == pp1.keys() and pp0
+    for p in pp0:
+        assert np.linalg.norm(pp1[p] - pp0[p]) <= 1e-10 * np.linalg.norm(pp0[p])

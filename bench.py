@@ -110,35 +110,67 @@ def fp64_peak_tflops():
     return 2.0 * n ** 3 / best / 1e12
 
 
-def phase_rooflines(tim, records, hbm, fp64, apply_ms, apply_bytes):
-    """Per-phase achieved throughput against its binding roofline (SURVEY 8d
-    counts): sampling 16 B per sampled entry (write + source read), pivot LU
-    8 B per trailing-entry visit, dense fronts (2/3)n_p^3 + 2 n_p^2 nf +
-    2 n_p nf^2 flops, apply bytes from the stored factor. The HODLR phases
-    (a14-a16) have no count here and are left out of the weighted total."""
-    dense_flops = 0.0
-    for r in records:
-        if r.path == "dense" and r.n_pivot > 0:
-            npv, nf = r.n_pivot, r.front_size - r.n_pivot
-            dense_flops += (2.0 / 3.0) * npv ** 3 + 2.0 * npv * npv * nf + 2.0 * npv * nf * nf
+def phase_rooflines(tim, hbm, fp64, apply_ms, apply_bytes, spmv_ms, nnz, n):
+    """Per-phase achieved throughput against the binding roofline, with the
+    algorithmic counts of the REFERENCE's algorithm on this factor's structure
+    (counted by the engine: mfh_timing_t):
+      sample        16 B per sampled entry (write + source read), HBM; plus the
+                    2 r flops per entry and low-rank child term W V^T it meets
+      pivot_lu      8 B per trailing-entry visit (nominal: the cores live in
+                    shared memory, see traffic); latency model = the longest
+                    core's steps summed over structured heights, us per step
+      skeleton      r^2 (m + n) flops per low-rank block (the two TRSMs)
+      hodlr_factor  a14: sum_leaves (2/3) n^3 + sum_nodes [2 r1 S(L) + 2 r2 S(R)
+                    + 2 r1 r2 n + (2/3)(r1 + r2)^3]  (hodlr.py:298-357)
+      eliminate     a16: 2 r_pf S_pp + 2 r_fp n_p r_pf + 2 nf r_fp r_pf
+      hodlr_front   a14 + a16 over both phases' time: BASELINE's "HODLR front GFLOP/s"
+      dense_front   a5: (2/3) n_p^3 + 2 n_p^2 nf + 2 n_p nf^2
+      apply         8 sum(2 S_pp + S_pf + S_fp) + 32 N (the engine's own read
+                    bytes beside it)
+      spmv          12 nnz + 4 (N + 1) + 16 N
+    FP64 peak: cuBLAS DGEMM measured live; HBM: MEASURED_PEAKS.json."""
     out = {}
 
-    def put(name, amount, ms, unit, peak):
+    def put(name, amount, ms, unit, peak, **extra):
         if ms <= 0:
             return
         ach = amount / (ms * 1e-3) / (1e9 if unit == "GB/s" else 1e12)
-        out[name] = {"achieved": ach, "unit": unit, "peak": peak, "frac": ach / peak, "ms": ms}
+        out[name] = {"achieved": ach, "unit": unit, "peak": peak, "frac": ach / peak, "ms": ms,
+                     "amount": amount, **extra}
 
-    put("sample", 16.0 * tim["sample_entries"], tim["sample_ms"], "GB/s", hbm)
-    put("pivot_lu", 8.0 * tim["pivot_lu_visits"], tim["pivot_lu_ms"], "GB/s", hbm)
-    put("dense_front", dense_flops, tim["dense_front_ms"], "TFLOP/s", fp64)
-    put("apply", apply_bytes, apply_ms, "GB/s", hbm)
-    fac = [v for k, v in out.items() if k != "apply"]
+    put("sample", 16.0 * tim["sample_entries"], tim["sample_ms"], "GB/s", hbm,
+        lr_tflops=tim["sample_lr_flops"] / (tim["sample_ms"] * 1e-3) / 1e12 if tim["sample_ms"] > 0 else None)
+    steps = tim["pivot_lu_crit_steps"]
+    put("pivot_lu", 8.0 * tim["pivot_lu_visits"], tim["pivot_lu_ms"], "GB/s", hbm,
+        latency={"critical_steps": steps, "us_per_step": tim["pivot_lu_ms"] * 1e3 / steps if steps else None,
+                 "note": "sequential complete-pivot steps (argmax -> barrier -> pivot broadcast) bound this "
+                         "phase; the cores stay in shared memory (profiles/r2_traffic_c2.json)"})
+    put("skeleton", tim["skeleton_flops"], tim["skeleton_ms"], "TFLOP/s", fp64)
+    put("hodlr_factor", tim["hodlr_flops"], tim["hodlr_factor_ms"], "TFLOP/s", fp64)
+    put("eliminate", tim["elim_flops"], tim["eliminate_ms"], "TFLOP/s", fp64)
+    put("hodlr_front", tim["hodlr_flops"] + tim["elim_flops"], tim["hodlr_factor_ms"] + tim["eliminate_ms"],
+        "TFLOP/s", fp64, gflops=(tim["hodlr_flops"] + tim["elim_flops"]) /
+        max(1e-12, (tim["hodlr_factor_ms"] + tim["eliminate_ms"]) * 1e-3) / 1e9)
+    put("dense_front", tim["dense_flops"], tim["dense_front_ms"], "TFLOP/s", fp64)
+    put("apply", tim["apply_ref_bytes"], apply_ms, "GB/s", hbm, engine_bytes=apply_bytes,
+        engine_gbs=apply_bytes / (apply_ms * 1e-3) / 1e9 if apply_ms > 0 else None)
+    put("spmv", 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n, spmv_ms, "GB/s", hbm)
+    fac = [out[k] for k in ("sample", "pivot_lu", "skeleton", "hodlr_factor", "eliminate", "dense_front") if k in out]
     tot = sum(v["ms"] for v in fac)
     out["factor_weighted_frac"] = sum(v["frac"] * v["ms"] for v in fac) / tot if tot else None
     out["factor_covered_ms"] = tot
     out["fp64_peak_kind"] = "cuBLAS DGEMM 4096^3 measured live"
     return out
+
+
+def traffic_record(config):
+    """DRAM traffic per kernel class from the committed ncu capture of this
+    config's step (profiles/r2_traffic_<config>.json, scripts/ncu_traffic.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"r2_traffic_{config}.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
 
 
 class ClockSampler:
@@ -236,12 +268,6 @@ def max_over_ranks(v, world):
     return float(t.item())
 
 
-def replica_plan(world, rank, n_rhs=1):
-    """Replica mode (round 1): every rank factors its own copy of the system; the
-    right-hand sides of a multi-RHS workload are dealt round-robin to ranks."""
-    return [k for k in range(n_rhs) if k % world == rank]
-
-
 # ---------------------------------------------------------------------------
 # CPU baseline / reference arm: the oracle (reference algorithm restated)
 # ---------------------------------------------------------------------------
@@ -300,9 +326,9 @@ def run_reference_arm(args, cfg, world, rank):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["desc"], "n": w.A.n_rows, "nnz": w.A.nnz, **cfg["params"], "nd_leaf": cfg["leaf"],
                    "restart": cfg["restart"], "tol": cfg["tol"], "rhs": f"{cfg['rhs']} seed 0",
-                   "parallelism": "single (rank 0; the reference is single-process)",
-                   "threads": "1 (OPENBLAS_NUM_THREADS=1: more BLAS threads make the reference 5-15x slower, "
-                              "SURVEY 6.3, so one thread is its fastest configuration)"},
+                   "parallelism": "single" if args.gpus <= 1 else f"subtree{args.gpus}"},
+        "threads": "1 (OPENBLAS_NUM_THREADS=1: more BLAS threads make the reference 5-15x slower, "
+                   "SURVEY 6.3 / BASELINE.md 3; rank 0 only, the reference is single-process)",
         "cpu_baseline": {"value": t, "unit": "s", "cores": 1, "kind": "port", "sample": sample_text(steps[-1], w)},
         "e2e": {"value": t, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gmres": {"iterations": steps[-1]["its"], "converged": steps[-1]["conv"]},
@@ -353,8 +379,10 @@ def run_gpu_arm(args, cfg, world, rank, local):
         def factorize():
             return mf_factorize_sharded(A, et, P.ACCELERATED, params, partition=part)
     else:
+        mode = P.ACCELERATED if args.mode == "accelerated" else P.CONVENTIONAL
+
         def factorize():
-            return P.mf_factorize(A, et, P.ACCELERATED, params)
+            return P.mf_factorize(A, et, mode, params)
 
     def step_device():
         t0 = time.perf_counter()
@@ -407,9 +435,12 @@ def run_gpu_arm(args, cfg, world, rank, local):
         print(json.dumps({"profile_step": True, "iterations": its, "converged": conv}), flush=True)
         return
     clocks = ClockSampler(local).start()
-    for _ in range(args.warmup):
+    cold_s = None
+    for w in range(args.warmup):
         F = None  # release the previous factorization first (C5's factor is tens of GB)
         F, its, conv, res = step_device()
+        if w == 0:  # first call on this tree: symbolic caches, maps and patterns built inside it
+            cold_s = split["factor_s"][0]
     barrier(world)
     times, e2e_times = [], []
     launches0 = ctx.info()[1]
@@ -435,10 +466,12 @@ def run_gpu_arm(args, cfg, world, rank, local):
         # e2e steps (at C5 two factorizations do not fit in HBM together)
         tim = F.timing()
         apply_ms, apply_bytes = F.apply_bench(20)
+        spmv_ms = C.c_double()
+        _lib.check(_lib.lib().mfh_spmv_bench(dev_op.handle, 50, C.byref(spmv_ms)))
+        spmv_ms = spmv_ms.value
         st = F.stats
         fstats = {"structured_fronts": st.structured_fronts, "dense_fronts": st.dense_fronts,
                   "peak_stored_reals": st.peak_stored_reals, "device_bytes": st.device_bytes}
-        records = st.records
         F = st = None
         import gc
         gc.collect()
@@ -466,6 +499,11 @@ def run_gpu_arm(args, cfg, world, rank, local):
     # trailing-entry visit, per launch = per structured height
     plu_ms = tim["pivot_lu_ms"]
     plu_gbs = 8.0 * tim["pivot_lu_visits"] / (plu_ms * 1e-3) / 1e9 if plu_ms > 0 else 0.0
+    pr = phase_rooflines(tim, hbm, fp64_peak_tflops(), apply_ms, apply_bytes, spmv_ms, A.nnz, n)
+    tr = traffic_record(args.config) if args.mode == "accelerated" else None
+    plu_traffic = None
+    if tr and "k_plu" in tr:
+        plu_traffic = tr["k_plu"]["dram_bytes_per_launch"]
     if rank != 0:
         return
     line = {
@@ -475,8 +513,9 @@ def run_gpu_arm(args, cfg, world, rank, local):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["desc"], "n": n, "nnz": A.nnz, **cfg["params"], "nd_leaf": cfg["leaf"],
                    "restart": cfg["restart"], "tol": cfg["tol"], "rhs": f"{cfg['rhs']} seed 0" if nrhs == 1 else f"{cfg['rhs']} seeds 0..{nrhs - 1} (one factorization, {nrhs} GMRES solves in lockstep sharing each preconditioner apply)",
-                   "parallelism": f"subtree{world}" if world > 1 else "single",
-                   "l2": "flushed (256 MiB write) before every timed step"},
+                   "parallelism": f"subtree{world}" if world > 1 else "single"},
+        "l2": "flushed (256 MiB write) before every timed step",
+        "mode": args.mode,
         "gmres": {"iterations": its, "converged": conv, "final_rel_residual": float(res),
                   "true_rel_residual_e2e": true_res, "e2e_iterations": he.iterations},
         "split_s": split,
@@ -488,12 +527,16 @@ def run_gpu_arm(args, cfg, world, rank, local):
                    "phases_ms": {k: tim[k] for k in ("sample_ms", "pivot_lu_ms", "skeleton_ms",
                                                      "hodlr_factor_ms", "dense_front_ms", "eliminate_ms")},
                    **fstats,
-                   "symbolic_s": t_sym},
+                   "symbolic_s": t_sym, "cold_first_factor_s": cold_s},
         "apply": {"ms": apply_ms, "bytes": apply_bytes, "gbs": apply_bytes / (apply_ms * 1e-3) / 1e9,
                   "frac_of_hbm": apply_bytes / (apply_ms * 1e-3) / 1e9 / hbm},
-        "phase_roofline": phase_rooflines(tim, records, hbm, fp64_peak_tflops(), apply_ms, apply_bytes),
-        "roofline": {"kernel": "k_full_pivot_lu", "bound": "hbm", "achieved": plu_gbs, "peak": hbm,
-                     "unit": "GB/s", "frac": plu_gbs / hbm, "traffic": None, "peak_kind": pk_kind},
+        "phase_roofline": pr,
+        "roofline": {"kernel": "k_plu_* (complete-pivot LU, a10)", "bound": "hbm", "achieved": plu_gbs,
+                     "peak": hbm, "unit": "GB/s", "frac": plu_gbs / hbm, "traffic": plu_traffic,
+                     "peak_kind": pk_kind, "latency": pr.get("pivot_lu", {}).get("latency"),
+                     "note": "nominal HBM fraction (8 B per trailing-entry visit, SURVEY 8d); the cores live in "
+                             "shared memory, so traffic (ncu DRAM bytes per launch) is far below the "
+                             "algorithmic bytes and the binding limit is the per-step latency"},
         "e2e": {"value": t_e2e, "unit": "s",
                 "h2d_bytes_per_step": int(8 * n * nrhs + 8 * A.nnz + 4 * A.nnz + 8 * (n + 1)),
                 "d2h_bytes_per_step": int(8 * n * nrhs)},
@@ -516,6 +559,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="accelerated", choices=["accelerated", "conventional"],
+                    help="conventional = every front dense (the GPU dense multifrontal baseline, "
+                         "multifrontal.py:470)")
     ap.add_argument("--profile", action="store_true", help="one untimed step (for ncu)")
     ap.add_argument("--param", action="append", default=[], metavar="KEY=VALUE",
                     help="override an MfParams field of the config (exploration only)")

@@ -37,6 +37,7 @@ typedef struct mfh_nd mfh_nd;            /* separator tree (ordering.py:32-56)  
 typedef struct mfh_etree mfh_etree;      /* elimination tree (ordering.py:238-261)*/
 typedef struct mfh_factor mfh_factor;    /* MfFactorization (multifrontal.py:227) */
 typedef struct mfh_csr mfh_csr;          /* device CSR operator (krylov.py:21-33) */
+typedef struct mfh_precond mfh_precond;  /* baseline preconditioners (krylov.py:164-204) */
 
 /* MfParams (multifrontal.py:34-48); max_rank < 0 means None. */
 typedef struct {
@@ -82,6 +83,15 @@ typedef struct {
   int64_t kernel_launches;
   double pivot_lu_visits; /* algorithmic trailing-entry visits */
   double sample_entries;
+  /* algorithmic counts of the REFERENCE's algorithm on this factor's structure
+   * (SURVEY 8d), the numerators of the per-phase rooflines */
+  double hodlr_flops;     /* a14 hodlr_factorize: leaf getrf + Woodbury (hodlr.py:312-357) */
+  double elim_flops;      /* a16 eliminate_hodlr: x = H^{-1} col_pf, core, W / V (multifrontal.py:424-438) */
+  double dense_flops;     /* a5 dense fronts: (2/3) n_p^3 + 2 n_p^2 nf + 2 n_p nf^2 */
+  double skeleton_flops;  /* a9 the two triangular solves: r^2 (m + n) per low-rank block */
+  double sample_lr_flops; /* a7 2 r per sampled entry per low-rank child term W V^T it meets */
+  double pivot_lu_crit_steps; /* sum over structured heights of the longest core's steps */
+  double apply_ref_bytes; /* one mf_solve by SURVEY 8d's count: 8 sum(2 S_pp + S_pf + S_fp) + 32 N */
 } mfh_timing_t;
 
 /* ---- errors --------------------------------------------------------------- */
@@ -192,6 +202,8 @@ int mfh_apply_bench(mfh_factor *f, int64_t reps, double *ms_per_apply, double *b
 int mfh_csr_create(mfh_ctx *ctx, int64_t n_rows, int64_t n_cols, const int64_t *indptr,
                    const int64_t *indices, const double *values, mfh_csr **out);
 int mfh_spmv(mfh_csr *A, const double *x, double *y, int on_device);
+/* time `reps` device-resident SpMVs back to back (CUDA events); mean ms */
+int mfh_spmv_bench(mfh_csr *A, int64_t reps, double *ms_per_spmv);
 void mfh_csr_free(mfh_csr *A);
 /* dense operator (LinearOperator.from_matrix(ndarray), krylov.py:32-33): row-major n x n */
 int mfh_dense_create(mfh_ctx *ctx, int64_t n, const double *values, mfh_csr **out);
@@ -207,6 +219,7 @@ typedef struct {
   mfh_factor *M;       /* device preconditioner (accelerated-mf), or NULL */
   mfh_host_op M_cb;    /* host preconditioner callback when M == NULL; NULL = identity */
   void *M_user;
+  mfh_precond *P;      /* device baseline preconditioner (diagonal / ILUT); takes precedence over M */
 } mfh_gmres_ops;
 
 /* b, x host arrays of n; hist receives up to max_iter residuals (or 1 when
@@ -234,6 +247,34 @@ int mfh_gmres_batched_device(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, 
                              const double *d_b, double *d_x, double tol, int64_t max_iter,
                              int64_t restart, double *hist, int64_t hist_cap, int64_t *n_hist,
                              int64_t *iterations, int *converged);
+
+/* ---- baseline preconditioners (krylov.py:164-204) ------------------------ */
+/* diagonal_preconditioner (krylov.py:164-170): y = x / diag(A); A as CSR.
+ * ValueError "zero diagonal entry at index i". */
+int mfh_precond_diag_create(mfh_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+                            const double *values, mfh_precond **out);
+/* ilut (krylov.py:173-204): dual-threshold ILU, per-row fill cap
+ * floor(k nnz / n) + 1, drop_tol relative to the row 2-norm; the factors are
+ * bit-identical to the reference's ilut_factor (_core.pyx:145-269), computed on
+ * the host (a row-sequential recurrence). The apply (two triangular solves,
+ * _core.pyx:272-305) runs on the GPU by level sets, one graph replay, and is
+ * bit-identical to the reference's scalar loops. A as CSR with sorted rows.
+ * ValueError texts: "k must be at least 1", "drop_tol must be nonnegative",
+ * "ILUT zero pivot in row i". */
+int mfh_precond_ilut_create(mfh_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+                            const double *values, int64_t k, double drop_tol, mfh_precond **out);
+/* the ILUT factorization alone, on the host (no context): two-call protocol,
+ * li == NULL returns lnz / unz only (ilut_factor, _core.pyx:145-269) */
+int mfh_ilut_factor(int64_t n, const int64_t *indptr, const int64_t *indices, const double *values, int64_t k,
+                    double drop_tol, int64_t *lnz, int64_t *unz, int64_t *lp, int64_t *li, double *lv,
+                    int64_t *up, int64_t *ui, double *uv);
+/* stored reals (Preconditioner.stored_reals), nnz of L and U, triangular-solve levels */
+int mfh_precond_info(const mfh_precond *P, int64_t *stored_reals, int64_t *lnz, int64_t *unz, int64_t *levels);
+/* the ILUT factors (lp n+1, li/lv lnz; up n+1, ui/uv unz), as ilut_factor returns them */
+int mfh_precond_ilut_factors(const mfh_precond *P, int64_t *lp, int64_t *li, double *lv, int64_t *up,
+                             int64_t *ui, double *uv);
+int mfh_precond_apply(mfh_precond *P, const double *b, double *x, int on_device);
+void mfh_precond_free(mfh_precond *P);
 
 /* ---- kernel plugin (full_pivot_lu, _kernels/__init__.py:25; _core.pyx:23) - */
 /* Batched complete-pivot LU on the device. Blocks are row-major, packed at

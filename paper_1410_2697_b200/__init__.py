@@ -8,8 +8,9 @@ behind the C-ABI of ``include/mfh.h`` (``libmfh.so``).
 
 from ._lib import PivotMonotonicityError
 from .kernels import BACKEND as KERNEL_BACKEND, full_pivot_lu, full_pivot_lu_batched
-from .krylov import (ConvergenceHistory, LinearOperator, Preconditioner, gmres, gmres_batched,
-                     identity_preconditioner, mf_preconditioner)
+from .krylov import (ConvergenceHistory, LinearOperator, Preconditioner, diagonal_preconditioner, gmres,
+                     gmres_batched, identity_preconditioner, ilut, ilut_factors_as_csr, mf_preconditioner)
+from .mmio import ScalingRecord, load_matrix_market, row_scale, write_matrix_market
 from .multifrontal import (ACCELERATED, CONVENTIONAL, FactorStats, FrontRecord, MfFactorization,
                            MfParams, mf_factorize, mf_solve)
 from .ordering import (EliminationTree, EtNode, SeparatorTree, SepNode, build_elimination_tree,
@@ -22,9 +23,10 @@ __version__ = "0.1.0"
 __all__ = [
     "ACCELERATED", "AdjGraph", "CONVENTIONAL", "ConvergenceHistory", "EliminationTree", "EtNode",
     "FactorStats", "FrontRecord", "KERNEL_BACKEND", "LinearOperator", "MfFactorization", "MfParams",
-    "PivotMonotonicityError", "Preconditioner", "SepNode", "SeparatorTree", "SparseMatrix",
-    "adjacency_graph", "build_elimination_tree", "full_pivot_lu", "full_pivot_lu_batched",
-    "gen_hex_q1", "gen_p1_delaunay", "gen_poisson7", "gen_q1_2d", "gmres", "gmres_batched",
-    "identity_preconditioner", "mf_factorize", "mf_preconditioner", "mf_solve",
-    "nested_dissection", "seeded_rhs", "spmv",
+    "PivotMonotonicityError", "Preconditioner", "ScalingRecord", "SepNode", "SeparatorTree", "SparseMatrix",
+    "adjacency_graph", "build_elimination_tree", "diagonal_preconditioner", "full_pivot_lu",
+    "full_pivot_lu_batched", "gen_hex_q1", "gen_p1_delaunay", "gen_poisson7", "gen_q1_2d", "gmres",
+    "gmres_batched", "identity_preconditioner", "ilut", "ilut_factors_as_csr", "load_matrix_market",
+    "mf_factorize", "mf_preconditioner", "mf_solve", "nested_dissection", "row_scale", "seeded_rhs", "spmv",
+    "write_matrix_market",
 ]

@@ -59,7 +59,10 @@ class mfh_timing_t(C.Structure):
                 ("apply_build_ms", C.c_double), ("apply_instantiate_ms", C.c_double),
                 ("gmres_ms", C.c_double), ("gmres_apply_ms", C.c_double), ("gmres_sync_ms", C.c_double),
                 ("kernel_launches", C.c_int64),
-                ("pivot_lu_visits", C.c_double), ("sample_entries", C.c_double)]
+                ("pivot_lu_visits", C.c_double), ("sample_entries", C.c_double),
+                ("hodlr_flops", C.c_double), ("elim_flops", C.c_double), ("dense_flops", C.c_double),
+                ("skeleton_flops", C.c_double), ("sample_lr_flops", C.c_double),
+                ("pivot_lu_crit_steps", C.c_double), ("apply_ref_bytes", C.c_double)]
 
 
 HOST_OP = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double))
@@ -67,7 +70,7 @@ HOST_OP = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_dou
 
 class mfh_gmres_ops(C.Structure):
     _fields_ = [("A", C.c_void_p), ("A_cb", HOST_OP), ("A_user", C.c_void_p),
-                ("M", C.c_void_p), ("M_cb", HOST_OP), ("M_user", C.c_void_p)]
+                ("M", C.c_void_p), ("M_cb", HOST_OP), ("M_user", C.c_void_p), ("P", C.c_void_p)]
 
 
 _lib = None
@@ -145,6 +148,14 @@ def _sig(lib):
         "mfh_csr_create": (C.c_int, [P, I64, I64, P, P, P, PP]),
         "mfh_dense_create": (C.c_int, [P, I64, P, PP]),
         "mfh_spmv": (C.c_int, [P, P, P, C.c_int]),
+        "mfh_spmv_bench": (C.c_int, [P, I64, pd]),
+        "mfh_precond_diag_create": (C.c_int, [P, I64, P, P, P, PP]),
+        "mfh_precond_ilut_create": (C.c_int, [P, I64, P, P, P, I64, d, PP]),
+        "mfh_precond_info": (C.c_int, [P, pi, pi, pi, pi]),
+        "mfh_precond_ilut_factors": (C.c_int, [P, P, P, P, P, P, P]),
+        "mfh_precond_apply": (C.c_int, [P, P, P, C.c_int]),
+        "mfh_precond_free": (None, [P]),
+        "mfh_ilut_factor": (C.c_int, [I64, P, P, P, I64, d, pi, pi, P, P, P, P, P, P]),
         "mfh_csr_free": (None, [P]),
         "mfh_gmres": (C.c_int, [P, C.POINTER(mfh_gmres_ops), I64, P, P, d, I64, I64, P, pi, pi,
                                 C.POINTER(C.c_int)]),

@@ -1911,6 +1911,27 @@ struct Factorizer {
     return F->arena.d(n);
   }
 
+  // algorithmic flops of the low-rank child terms an extend-add request meets:
+  // 2 r per sampled entry whose row and column both map into a child carrying
+  // W V^T (multifrontal.py:340-347). Rows / columns: a range, or an index list.
+  void count_lr(int fi, int r0, int nr, const std::vector<int> *rl, int c0, int nc, const std::vector<int> *cl) {
+    const FrontH &f = F->fronts[fi];
+    for (int ci : f.kids) {
+      const FrontH &c = F->fronts[ci];
+      if (c.upd != 1 || c.rw == 0) continue;
+      const int *to = et->mapcache.maps.data() + et->mapcache.off[ci];
+      auto hits = [&](int a0, int n, const std::vector<int> *l) {
+        double h = 0;
+        if (l)
+          for (int x : *l) h += to[x] >= 0;
+        else
+          for (int x = a0; x < a0 + n; ++x) h += to[x] >= 0;
+        return h;
+      };
+      F->timing.sample_lr_flops += 2.0 * c.rw * hits(r0, nr, rl) * hits(c0, nc, cl);
+    }
+  }
+
   // ---- one height ----
   // host clock when each phase event was enqueued (MFH_HEIGHT_TRACE)
   std::chrono::steady_clock::time_point hts[8];
@@ -1934,6 +1955,7 @@ struct Factorizer {
       f.F = upd.d((size_t)f.nh * f.nh, release_height(f));
       if (f.npv) f.piv = F->arena.i(f.npv);
       reqs.push_back(SReq{slot[fi], f.nh, f.nh, nullptr, nullptr, 0, 0, f.F, f.nh});
+      count_lr(fi, 0, f.nh, nullptr, 0, f.nh, nullptr);
     }
     // ------------------------------------------------ structured: plan blocks
     std::vector<int> sblocks;  // all compressed blocks at this height
@@ -1951,6 +1973,7 @@ struct Factorizer {
             int sz = T.hi[v] - T.lo[v];
             // pivot-block leaves live for the height, update leaves until the parent sampled them
             T.lval[v] = tt == f.pp ? ctx->scratch.d((size_t)sz * sz) : upd.d((size_t)sz * sz, release_height(f));
+            count_lr(fi, T.base + T.lo[v], sz, nullptr, T.base + T.lo[v], sz, nullptr);
             reqs.push_back(SReq{slot[fi], sz, sz, nullptr, nullptr, T.base + T.lo[v], T.base + T.lo[v],
                                 T.lval[v], sz});
           }
@@ -1986,6 +2009,7 @@ struct Factorizer {
       b.ldR = b.n;
       b.d_I = b.fullI ? nullptr : s.push(b.I);
       reqs.push_back(SReq{slot[b.fi], nI, b.n, b.d_I, nullptr, b.I[0], b.c0, b.R, b.ldR});
+      count_lr(b.fi, 0, 0, &b.I, b.c0, b.n, nullptr);
       if (b.fullI && b.fullJ) {
         b.C = b.R;
         b.ldC = b.n;
@@ -1994,6 +2018,7 @@ struct Factorizer {
         b.ldC = nJ;
         b.d_J = b.fullJ ? nullptr : s.push(b.J);
         reqs.push_back(SReq{slot[b.fi], b.m, nJ, nullptr, b.d_J, b.r0, b.J[0], b.C, b.ldC});
+        count_lr(b.fi, b.r0, b.m, nullptr, 0, 0, &b.J);
       }
       // core = R[:, J - c0]
       b.core = ctx->scratch.d((size_t)nI * nJ);
@@ -2089,7 +2114,12 @@ struct Factorizer {
           f.upd_ld = f.nh;
         }
         f.front_reals = (int64_t)f.nh * f.nh;
+        {
+          const double np_ = f.npv, nf_ = f.nf;
+          F->timing.dense_flops += (2.0 / 3.0) * np_ * np_ * np_ + 2.0 * np_ * np_ * nf_ + 2.0 * np_ * nf_ * nf_;
+        }
         f.factor_reals = (f.npv ? (int64_t)f.npv * f.npv : 0) + 2 * (int64_t)f.npv * f.nf;
+        if (f.npv) F->timing.apply_ref_bytes += 8.0 * (2.0 * f.npv * f.npv + 2.0 * f.npv * f.nf);
         f.upd_reals = (int64_t)f.nf * f.nf;
       }
     };
@@ -2121,6 +2151,7 @@ struct Factorizer {
       std::vector<double> hd((const double *)(hb + oD), (const double *)(hb + oD) + dtot);
       check_flags(0, (const int *)(hb + oF));
       int first_err = -1;
+      int crit = 0;  // steps of the longest core of the height (the latency-bound critical path)
       for (size_t q = 0; q < sblocks.size(); ++q) {
         BlockH &b = F->blocks[sblocks[q]];
         int nI = (int)b.I.size(), nJ = (int)b.J.size();
@@ -2146,7 +2177,9 @@ struct Factorizer {
         double vis = 0;
         for (int k = 0; k < kk; ++k) vis += (double)(nI - k) * (nJ - k);
         F->timing.pivot_lu_visits += vis;
+        crit = std::max(crit, kk);
       }
+      F->timing.pivot_lu_crit_steps += crit;
       if (first_err >= 0) {
         BlockH &b = F->blocks[sblocks[first_err]];
         if (b.status == 2) throw runtime_error("internal: corrupt complete-pivot candidate");
@@ -2172,9 +2205,11 @@ struct Factorizer {
       if (b.dense) {
         b.val = blk_alloc(b, (size_t)b.m * b.n);
         dreq.push_back(SReq{slot[b.fi], b.m, b.n, nullptr, nullptr, b.r0, b.c0, b.val, b.n});
+        count_lr(b.fi, b.r0, b.m, nullptr, b.c0, b.n, nullptr);
         F->stats.n_dense_fallback++;
       } else if (b.rank > 0) {
         int r = b.rank;
+        F->timing.skeleton_flops += (double)r * r * (b.m + b.n);
         double *lu = ctx->scratch.d((size_t)r * r);
         lux.push_back(LuExtractJob{b.core, nJ, r, b.rows_phys ? nullptr : b.pint, nullptr, lu});
         b.row = blk_alloc(b, (size_t)r * b.n);
@@ -2693,10 +2728,37 @@ struct Factorizer {
         }
         return s2;
       };
+      // algorithmic flops of the reference's hodlr_factorize / eliminate_hodlr
+      // on this structure: S(v) = stored reals of v's factor subtree
+      double s_pp = 0;
+      if (f.pp >= 0) {
+        HTree &T = F->trees[f.pp];
+        std::vector<double> S(T.nslots, 0.0);
+        for (int v = T.nslots - 1; v >= 0; --v) {
+          if (T.leaf[v] == 1) {
+            const double sz = T.hi[v] - T.lo[v];
+            S[v] = sz * sz;
+            F->timing.hodlr_flops += (2.0 / 3.0) * sz * sz * sz;
+          } else if (T.leaf[v] == 0) {
+            const double lo = T.lo[v], hi = T.hi[v], mid = (T.lo[v] + T.hi[v]) >> 1;
+            const double r1 = F->blocks[T.up[v]].erank(), r2 = F->blocks[T.lw[v]].erank();
+            const double m1 = mid - lo, m2 = hi - mid, rr = r1 + r2;
+            const double SL = S[2 * v + 1], SR = S[2 * v + 2];
+            S[v] = SL + SR + m1 * r1 + m2 * r2 + r1 * m2 + r2 * m1 + rr * rr;
+            F->timing.hodlr_flops += 2.0 * r1 * SL + 2.0 * r2 * SR + 2.0 * r1 * r2 * (hi - lo) + (2.0 / 3.0) * rr * rr * rr;
+          }
+        }
+        s_pp = S[0];
+      }
+      if (f.npv && f.nf) {
+        const double rpf = F->blocks[f.pf].erank(), rfp = F->blocks[f.fp].erank();
+        F->timing.elim_flops += 2.0 * rpf * s_pp + 2.0 * rfp * f.npv * rpf + 2.0 * f.nf * rfp * rpf;
+      }
       int64_t pfs = f.pf >= 0 ? F->blocks[f.pf].stored() : 0;
       int64_t fps = f.fp >= 0 ? F->blocks[f.fp].stored() : 0;
       f.front_reals = tree_stored(f.pp) + pfs + fps + tree_stored(f.ff);
       f.factor_reals = factor_stored(f.pp) + pfs + fps;
+      if (f.npv) F->timing.apply_ref_bytes += 8.0 * (2.0 * factor_stored(f.pp) + pfs + fps);
       f.upd_reals = f.nf ? tree_stored(f.ff) + 2 * (int64_t)f.nf * f.rw : 0;
       int64_t h = std::max(tree_hint(f.pp), tree_hint(f.ff));
       if (f.pf >= 0) h = std::max<int64_t>(h, F->blocks[f.pf].erank());
@@ -3360,6 +3422,7 @@ struct Factorizer {
     // (the apply plan is already built) may read them
     for (auto &f : F->fronts) f.ids = IdsView{};
     F->timing.total_ms = tot;
+    F->timing.apply_ref_bytes += 32.0 * n;
     F->timing.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
 };
@@ -3977,6 +4040,32 @@ static void apply_device(mfh_factor *F, const double *d_in, double *d_out) {
 // ---------------------------------------------------------------------------
 // operators for GMRES
 // ---------------------------------------------------------------------------
+// baseline preconditioners (krylov.py:164-204): diagonal, and ILUT with the
+// factorization on the host (a row-sequential recurrence; bit-identical to the
+// reference's) and the two triangular solves on the GPU, level-scheduled and
+// replayed as one CUDA graph
+struct mfh_precond {
+  mfh::Ctx *ctx = nullptr;
+  int kind = 0;  // 0 diagonal, 1 ILUT
+  int64_t n = 0;
+  double *d = nullptr;  // diagonal
+  mfh::IlutFactors host;  // ILUT factors (host copy for ilut_factors / the test)
+  long long *lp = nullptr, *up = nullptr;
+  int *li = nullptr, *ui = nullptr, *lrows = nullptr, *urows = nullptr;
+  double *lv = nullptr, *uv = nullptr, *b = nullptr, *y = nullptr, *x = nullptr;
+  int64_t levels_l = 0, levels_u = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int64_t nodes = 0;
+  ~mfh_precond() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (void *q : {(void *)d, (void *)lp, (void *)up, (void *)li, (void *)ui, (void *)lrows, (void *)urows,
+                    (void *)lv, (void *)uv, (void *)b, (void *)y, (void *)x})
+      cudaFree(q);
+  }
+};
+
 struct mfh_csr {
   mfh::Ctx *ctx = nullptr;
   int kind = 0;  // 0 csr, 1 dense
@@ -4003,6 +4092,24 @@ static void op_apply_device(mfh_csr *A, const double *x, double *y) {
     Sink s{ctx};
     run_gemm(s, {j});
   }
+}
+
+// d_in -> d_out on the context stream (device vectors of length n)
+static void precond_apply_device(mfh_precond *P, const double *d_in, double *d_out) {
+  Ctx *ctx = P->ctx;
+  const int64_t n = P->n;
+  if (n == 0) return;
+  if (P->kind == 0) {
+    const int g = (int)std::min<int64_t>(cdiv(n, 256), 148 * 8);
+    k_diag_div<<<g, 256, 0, ctx->s>>>(n, P->d, d_in, d_out);
+    check_launch();
+    ctx->launches++;
+    return;
+  }
+  CK(cudaMemcpyAsync(P->b, d_in, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s));
+  CK(cudaGraphLaunch(P->exec, ctx->s));
+  ctx->launches += P->nodes;
+  CK(cudaMemcpyAsync(d_out, P->x, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s));
 }
 
 }  // namespace mfh
@@ -4367,6 +4474,166 @@ extern "C" int mfh_apply_bench(mfh_factor *f, int64_t reps, double *ms_per_apply
   MFH_CATCH
 }
 
+extern "C" int mfh_precond_diag_create(mfh_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+                                       const double *values, mfh_precond **out) {
+  std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
+  MFH_TRY
+  DeviceGuard dg_(ctx->c.device);
+  std::vector<double> dg((size_t)std::max<int64_t>(n, 1), 0.0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p)
+      if (indices[p] == i) dg[i] = values[p];
+  for (int64_t i = 0; i < n; ++i)  // krylov.py:166-168
+    if (dg[i] == 0.0) throw value_error("zero diagonal entry at index " + std::to_string(i));
+  std::unique_ptr<mfh_precond> P(new mfh_precond());
+  P->ctx = &ctx->c;
+  P->kind = 0;
+  P->n = n;
+  CK(cudaMalloc(&P->d, sizeof(double) * std::max<int64_t>(n, 1)));
+  upload(ctx->c.s, P->d, dg.data(), sizeof(double) * n);
+  *out = P.release();
+  MFH_CATCH
+}
+
+// level sets of a triangular factor: rows whose dependencies are all in
+// earlier levels (lower: columns < i; upper: columns > i, diagonal first)
+static std::vector<std::vector<int>> tri_levels(int64_t n, const std::vector<int64_t> &ptr,
+                                                const std::vector<int64_t> &idx, bool upper) {
+  std::vector<int> lev((size_t)std::max<int64_t>(n, 1), 0);
+  int mx = -1;
+  for (int64_t s = 0; s < n; ++s) {
+    const int64_t i = upper ? n - 1 - s : s;
+    int l = 0;
+    for (int64_t p = ptr[i] + (upper ? 1 : 0); p < ptr[i + 1]; ++p) l = std::max(l, lev[idx[p]] + 1);
+    lev[i] = l;
+    mx = std::max(mx, l);
+  }
+  std::vector<std::vector<int>> out(mx + 1);
+  for (int64_t i = 0; i < n; ++i) out[lev[i]].push_back((int)i);
+  return out;
+}
+
+extern "C" int mfh_precond_ilut_create(mfh_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+                                       const double *values, int64_t k, double drop_tol, mfh_precond **out) {
+  std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
+  MFH_TRY
+  DeviceGuard dg_(ctx->c.device);
+  if (k < 1) throw value_error("k must be at least 1");  // krylov.py:180-185
+  if (!(drop_tol >= 0)) throw value_error("drop_tol must be nonnegative");
+  if (n < 1) throw value_error("ILUT requires a non-empty square matrix");
+  const int64_t nnz = indptr[n];
+  const int64_t cap = k * nnz / n + 1;
+  std::unique_ptr<mfh_precond> P(new mfh_precond());
+  P->ctx = &ctx->c;
+  P->kind = 1;
+  P->n = n;
+  P->host = ilut_factor(n, indptr, indices, values, cap, drop_tol);
+  const IlutFactors &H = P->host;
+  auto up_i32 = [&](int **dst, const std::vector<int64_t> &v) {
+    std::vector<int> t(v.begin(), v.end());
+    CK(cudaMalloc(dst, sizeof(int) * std::max<size_t>(1, t.size())));
+    upload(ctx->c.s, *dst, t.data(), sizeof(int) * t.size());
+  };
+  auto up_raw = [&](auto **dst, const auto &v) {
+    CK(cudaMalloc(dst, sizeof(v[0]) * std::max<size_t>(1, v.size())));
+    upload(ctx->c.s, *dst, v.data(), sizeof(v[0]) * v.size());
+  };
+  up_raw(&P->lp, H.lp);
+  up_raw(&P->up, H.up);
+  up_i32(&P->li, H.li);
+  up_i32(&P->ui, H.ui);
+  up_raw(&P->lv, H.lv);
+  up_raw(&P->uv, H.uv);
+  for (double **q : {&P->b, &P->y, &P->x}) CK(cudaMalloc(q, sizeof(double) * n));
+  auto L = tri_levels(n, H.lp, H.li, false), U = tri_levels(n, H.up, H.ui, true);
+  P->levels_l = (int64_t)L.size();
+  P->levels_u = (int64_t)U.size();
+  std::vector<int> lr, ur;
+  std::vector<std::pair<int64_t, int>> lo, uo;  // (offset, count) per level
+  for (auto &v : L) {
+    lo.push_back({(int64_t)lr.size(), (int)v.size()});
+    lr.insert(lr.end(), v.begin(), v.end());
+  }
+  for (auto &v : U) {
+    uo.push_back({(int64_t)ur.size(), (int)v.size()});
+    ur.insert(ur.end(), v.begin(), v.end());
+  }
+  up_raw(&P->lrows, lr);
+  up_raw(&P->urows, ur);
+  // one graph: every level of L (b -> y), then every level of U (y -> x)
+  cudaStream_t st = ctx->c.s;
+  CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  for (auto &q : lo)
+    k_trsv_level<<<(unsigned)cdiv(q.second, 128), 128, 0, st>>>(P->lrows + q.first, q.second, P->lp, P->li, P->lv,
+                                                                  P->b, P->y, 0);
+  for (auto &q : uo)
+    k_trsv_level<<<(unsigned)cdiv(q.second, 128), 128, 0, st>>>(P->urows + q.first, q.second, P->up, P->ui, P->uv,
+                                                                  P->y, P->x, 1);
+  CK(cudaStreamEndCapture(st, &P->graph));
+  CK(cudaGraphInstantiate(&P->exec, P->graph, 0));
+  P->nodes = (int64_t)(lo.size() + uo.size());
+  *out = P.release();
+  MFH_CATCH
+}
+
+extern "C" int mfh_precond_info(const mfh_precond *P, int64_t *stored_reals, int64_t *lnz, int64_t *unz,
+                                int64_t *levels) {
+  MFH_TRY
+  if (P->kind == 0) {
+    *stored_reals = P->n;
+    if (lnz) *lnz = 0;
+    if (unz) *unz = 0;
+    if (levels) *levels = 1;
+  } else {
+    *stored_reals = (int64_t)(P->host.lv.size() + P->host.uv.size());
+    if (lnz) *lnz = (int64_t)P->host.lv.size();
+    if (unz) *unz = (int64_t)P->host.uv.size();
+    if (levels) *levels = P->levels_l + P->levels_u;
+  }
+  MFH_CATCH
+}
+
+extern "C" int mfh_precond_ilut_factors(const mfh_precond *P, int64_t *lp, int64_t *li, double *lv, int64_t *up,
+                                        int64_t *ui, double *uv) {
+  MFH_TRY
+  if (P->kind != 1) throw value_error("not an ILUT preconditioner");
+  const IlutFactors &H = P->host;
+  std::memcpy(lp, H.lp.data(), sizeof(int64_t) * H.lp.size());
+  std::memcpy(up, H.up.data(), sizeof(int64_t) * H.up.size());
+  std::memcpy(li, H.li.data(), sizeof(int64_t) * H.li.size());
+  std::memcpy(ui, H.ui.data(), sizeof(int64_t) * H.ui.size());
+  std::memcpy(lv, H.lv.data(), sizeof(double) * H.lv.size());
+  std::memcpy(uv, H.uv.data(), sizeof(double) * H.uv.size());
+  MFH_CATCH
+}
+
+extern "C" int mfh_precond_apply(mfh_precond *P, const double *b, double *x, int on_device) {
+  std::lock_guard<std::recursive_mutex> lk_(P->ctx->mu);
+  MFH_TRY
+  DeviceGuard dg_(P->ctx->device);
+  Ctx *ctx = P->ctx;
+  const int64_t n = P->n;
+  if (on_device) {
+    precond_apply_device(P, b, x);
+  } else {
+    double *db = ctx->scratch.d(std::max<int64_t>(1, n)), *dx = ctx->scratch.d(std::max<int64_t>(1, n));
+    CK(cudaMemcpyAsync(db, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->s));
+    precond_apply_device(P, db, dx);
+    CK(cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->s));
+  }
+  CK(cudaStreamSynchronize(ctx->s));
+  if (!on_device) ctx->scratch.reset();
+  MFH_CATCH
+}
+
+extern "C" void mfh_precond_free(mfh_precond *P) {
+  if (!P) return;
+  std::lock_guard<std::recursive_mutex> lk_(P->ctx->mu);
+  DeviceGuard dg_(P->ctx->device);
+  cudaStreamSynchronize(P->ctx->s);
+  delete P;
+}
+
 extern "C" int mfh_csr_create(mfh_ctx *ctx, int64_t n_rows, int64_t n_cols, const int64_t *indptr,
                               const int64_t *indices, const double *values, mfh_csr **out) {
   std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
@@ -4415,6 +4682,30 @@ extern "C" void mfh_csr_free(mfh_csr *A) {
   cudaFree(A->col);
   cudaFree(A->val);
   delete A;
+}
+
+extern "C" int mfh_spmv_bench(mfh_csr *A, int64_t reps, double *ms_per_spmv) {
+  std::lock_guard<std::recursive_mutex> lk_(A->ctx->mu);
+  MFH_TRY
+  DeviceGuard dg_(A->ctx->device);
+  Ctx *ctx = A->ctx;
+  double *dx = ctx->scratch.d(std::max<int64_t>(1, A->nc)), *dy = ctx->scratch.d(std::max<int64_t>(1, A->nr));
+  CK(cudaMemsetAsync(dx, 0, sizeof(double) * std::max<int64_t>(1, A->nc), ctx->s));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  op_apply_device(A, dx, dy);
+  CK(cudaEventRecord(e0, ctx->s));
+  for (int64_t r = 0; r < reps; ++r) op_apply_device(A, dx, dy);
+  CK(cudaEventRecord(e1, ctx->s));
+  CK(cudaEventSynchronize(e1));
+  float ms;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  *ms_per_spmv = ms / std::max<int64_t>(1, reps);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ctx->scratch.reset();
+  MFH_CATCH
 }
 
 extern "C" int mfh_spmv(mfh_csr *A, const double *x, double *y, int on_device) {
@@ -4470,7 +4761,9 @@ struct GmresRun {
   double m_ms = 0.0;
   void M(const double *x, double *y) {
     auto t0 = std::chrono::steady_clock::now();
-    if (ops->M) {
+    if (ops->P) {
+      precond_apply_device(ops->P, x, y);
+    } else if (ops->M) {
       apply_device(ops->M, x, y);
       m_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     } else if (ops->M_cb)

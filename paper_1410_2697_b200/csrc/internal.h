@@ -37,6 +37,17 @@ struct HostCsr {
 Graph adjacency_from_csr(int64_t n, const int64_t *indptr, const int64_t *indices,
                          const double *values);
 
+// Dual-threshold incomplete LU (ILUT) of a CSR matrix with sorted rows: the
+// comparison-baseline preconditioner (krylov.py:173-204, _core.pyx:145-269).
+// L is unit lower (diagonal not stored), U upper with the diagonal first in
+// every row. Throws value_error("ILUT zero pivot in row i").
+struct IlutFactors {
+  std::vector<int64_t> lp, li, up, ui;
+  std::vector<double> lv, uv;
+};
+IlutFactors ilut_factor(int64_t n, const int64_t *ap, const int64_t *aj, const double *ax, int64_t cap,
+                        double drop_tol);
+
 }  // namespace mfh
 
 // Separator tree produced by nested dissection (ordering.py:19-56).

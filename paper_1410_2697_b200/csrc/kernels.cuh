@@ -2816,4 +2816,32 @@ __global__ void __launch_bounds__(256) k_spmv(long long nrows, const long long *
   }
 }
 
+// ---------------------------------------------------------------------------
+// baseline preconditioners (krylov.py:164-204)
+// ---------------------------------------------------------------------------
+// y = x / d (diagonal_preconditioner: v / diag, IEEE division, bit-exact)
+__global__ void k_diag_div(long long n, const double *__restrict__ d, const double *__restrict__ x,
+                           double *__restrict__ y) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = x[i] / d[i];
+}
+
+// One level of a sparse triangular solve (ILUT apply), one thread per row of
+// the level: lower unit (x_i = b_i - sum_p v_p x_{j_p}) or upper with the
+// diagonal first in the row (x_i = (b_i - sum_{p > first} v_p x_{j_p}) / v_first).
+// The products and differences are rounded separately in the row's entry
+// order (__dmul_rn / __dsub_rn: no FMA contraction), exactly like the
+// reference's scalar loops (_core.pyx:272-305), so the apply is bit-identical.
+__global__ void k_trsv_level(const int *__restrict__ rows, int nrows, const long long *__restrict__ ptr,
+                             const int *__restrict__ idx, const double *__restrict__ val, const double *__restrict__ b,
+                             double *__restrict__ x, int upper) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nrows) return;
+  const int i = rows[t];
+  double s = b[i];
+  const long long p0 = ptr[i] + (upper ? 1 : 0), p1 = ptr[i + 1];
+  for (long long p = p0; p < p1; ++p) s = __dsub_rn(s, __dmul_rn(val[p], x[idx[p]]));
+  x[i] = upper ? s / val[ptr[i]] : s;
+}
+
 }  // namespace mfh

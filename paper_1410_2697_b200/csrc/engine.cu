@@ -3941,8 +3941,146 @@ static std::unique_ptr<ApplyPlan> make_apply(mfh_factor *F, int nv) {
     for (auto &v : sa) run_gemv(sk, v, nv);
   }
   };
+  // ---- low levels as whole dense subtrees per CTA (one launch per pass)
+  SubApply sub[2] = {};  // upward, downward
+  int sub_grid = 0, L0 = 0;
+  if (!sh && !(getenv("MFH_APPLY_SUBTREE") && atoi(getenv("MFH_APPLY_SUBTREE")) == 0)) {
+    const int INF = 1 << 30;
+    int L0s = maxh + 1;  // the first level holding a structured front
+    for (size_t q = 0; q < NF; ++q)
+      if (ah[q] >= 0 && F->fronts[q].structured) L0s = std::min(L0s, ah[q]);
+    std::vector<int> par(NF, -1), anc(NF, INF), cnt(NF, 1);
+    std::vector<double> sb(NF, 0.0);  // bytes of the pivot-carrying fronts of the subtree
+    for (size_t q = 0; q < NF; ++q) {
+      FrontH &f = F->fronts[q];
+      for (int c : f.allkids) {
+        par[c] = (int)q;
+        cnt[q] += cnt[c];
+        sb[q] += sb[c];
+      }
+      if (ah[q] >= 0) sb[q] += 8.0 * ((double)f.npv * f.npv + 2.0 * f.npv * f.nf);
+    }
+    for (size_t q = NF; q-- > 0;)
+      if (par[q] >= 0) anc[q] = ah[par[q]] >= 0 ? ah[par[q]] : anc[par[q]];
+    // cut level by a cost model: per-level launches cost about 35 us per level
+    // (gather + GEMV up, GEMV down); the subtree kernels cost their LPT
+    // makespan at ~40 GB/s per CTA plus ~5 us of barriers and load latency per
+    // level, in both passes
+    const int GMAX = 2 * ctx->nsm;
+    auto plan = [&](int L, std::vector<std::vector<int>> *assign) {
+      std::vector<int> roots;
+      for (size_t q = 0; q < NF; ++q)
+        if (ah[q] >= 0 && ah[q] < L && anc[q] >= L) roots.push_back((int)q);
+      if (roots.empty()) return 0.0;
+      std::stable_sort(roots.begin(), roots.end(), [&](int a, int b) { return sb[a] > sb[b]; });
+      const int G = std::min<int>((int)roots.size(), GMAX);
+      std::vector<double> load(G, 0.0);
+      if (assign) assign->assign(G, {});
+      for (int r : roots) {
+        int t = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        load[t] += sb[r];
+        if (assign) (*assign)[t].push_back(r);
+      }
+      return *std::max_element(load.begin(), load.end());
+    };
+    double best = 35e-6 * L0s;
+    for (int L = 1; L <= L0s; ++L) {
+      const double c = 2.0 * (plan(L, nullptr) / 40e9 + 5e-6 * L) + 35e-6 * (L0s - L);
+      if (c < best) {
+        best = c;
+        L0 = L;
+      }
+    }
+    if (L0 > 0) {
+      std::vector<std::vector<int>> assign;
+      plan(L0, &assign);
+      // per CTA, per level: the fronts of its subtrees (post order), their
+      // upward and downward GEMV jobs and the pivot ids to gather
+      std::vector<SubSeg> seg;
+      std::vector<int> cseg{0}, start{0};
+      std::vector<GemvJob> jup, jdn;
+      std::vector<int> sdn{0};
+      std::vector<long long> gids;
+      int nfr = 0;
+      for (auto &rs : assign) {
+        std::sort(rs.begin(), rs.end());
+        std::vector<std::vector<int>> lev(L0);
+        for (int r : rs)
+          for (int q = r - cnt[r] + 1; q <= r; ++q)
+            if (ah[q] >= 0) lev[ah[q]].push_back(q);
+        for (int L = 0; L < L0; ++L) {
+          if (lev[L].empty()) continue;
+          SubSeg g{};
+          g.jb = (int)jup.size();
+          g.gb = (int)gids.size();
+          for (int q : lev[L]) {
+            FrontH &f = F->fronts[q];
+            ++nfr;
+            if (L > 0)
+              for (int j = 0; j < f.npv; ++j) gids.push_back(f.piv_lo + j);
+            // upward t = Gfp b_piv (a zero-row job keeps jobs aligned with the downward list)
+            const double *bp = bu + f.piv_lo;
+            GemvJob u = f.nf ? strided(gemv(cbuf + off[q], nullptr, f.nf, f.Gfp, f.npv, f.npv, bp, 1.0), cst, nst, 0)
+                             : strided(gemv(nullptr, nullptr, 0, nullptr, 0, 0, nullptr, 0.0), 0, 0, 0);
+            GemvJob d = strided(gemv(xw + f.piv_lo, nullptr, f.npv, f.Pinv, f.npv, f.npv, bp, 1.0, f.Gpf, f.nf, f.nf,
+                                     xw, f.nf ? d_fro + off[q] : nullptr, -1.0),
+                                nst, nst, nst);
+            jup.push_back(u);
+            jdn.push_back(d);
+            start.push_back(start.back() + std::max(0, u.m));
+            sdn.push_back(sdn.back() + d.m);
+            bytes += 8.0 * ((double)f.npv * f.npv + 2.0 * f.npv * f.nf);
+          }
+          g.je = (int)jup.size();
+          g.ge = (int)gids.size();
+          seg.push_back(g);
+        }
+        cseg.push_back((int)seg.size());
+      }
+      for (int pass = 0; pass < 2; ++pass) {
+        SubApply &S = sub[pass];
+        S.seg = sk.push(seg);
+        S.cta_seg = sk.push(cseg);
+        S.job = sk.push(pass == 0 ? jup : jdn);
+        S.start = sk.push(pass == 0 ? start : sdn);
+        S.gids = gids.empty() ? nullptr : sk.push(gids);
+        S.cptr = d_cptr;
+        S.coff = d_coff;
+        S.cbuf = cbuf;
+        S.bu = bu;
+        S.cst = cst;
+        S.nst = nst;
+      }
+      sub_grid = (int)assign.size();
+      for (int h = 0; h < L0; ++h) byh[h].clear();
+      if (atrace)
+        fprintf(stderr, "[mfh apply] levels < %d (of %d dense-only) as %d subtree fronts on %d CTAs, est %.1f us\n",
+                L0, L0s, nfr, sub_grid, best * 1e6);
+    }
+  }
+  auto launch_sub = [&](bool up) {
+    if (!sub_grid) return;
+    const SubApply S = sub[up ? 0 : 1];
+    const int g = sub_grid, v = nv, u = up ? 1 : 0;
+    sk.launch([=](cudaStream_t st) {
+      switch (v) {
+        case 1: k_apply_sub<1><<<g, 512, 0, st>>>(S, u); break;
+        case 2: k_apply_sub<2><<<g, 512, 0, st>>>(S, u); break;
+        case 3: k_apply_sub<3><<<g, 512, 0, st>>>(S, u); break;
+        case 4: k_apply_sub<4><<<g, 512, 0, st>>>(S, u); break;
+        case 5: k_apply_sub<5><<<g, 512, 0, st>>>(S, u); break;
+        case 6: k_apply_sub<6><<<g, 512, 0, st>>>(S, u); break;
+        case 7: k_apply_sub<7><<<g, 512, 0, st>>>(S, u); break;
+        case 8: k_apply_sub<8><<<g, 512, 0, st>>>(S, u); break;
+        default: throw runtime_error("apply: 1..8 right-hand sides");
+      }
+      check_launch();
+    });
+  };
+  launch_sub(true);
   upward(byh);
   downward(byh);
+  launch_sub(false);
   if (sh) exchange_point(xw, x_mask, x_tmp, std::max<int64_t>(1, n));  // every rank gets every pivot
   sk.launch([=](cudaStream_t s) {
     k_gather_perm<<<dim3(grid_n, nv), 256, 0, s>>>(xw, perm, dx, n);
@@ -4069,7 +4207,7 @@ struct mfh_precond {
 struct mfh_csr {
   mfh::Ctx *ctx = nullptr;
   int kind = 0;  // 0 csr, 1 dense
-  int64_t nr = 0, nc = 0;
+  int64_t nr = 0, nc = 0, nnz = 0;
   long long *ptr = nullptr;
   int *col = nullptr;
   double *val = nullptr;
@@ -4081,10 +4219,18 @@ namespace mfh {
 static void op_apply_device(mfh_csr *A, const double *x, double *y) {
   Ctx *ctx = A->ctx;
   if (A->kind == 0) {
-    int64_t nw = A->nr;
-    int grid = (int)std::min<int64_t>(cdiv(nw * 32, 256), 148 * 16);
+    // lanes per row from the average row length
+    const int64_t nnz = A->nnz;
+    const double avg = A->nr ? (double)nnz / A->nr : 0.0;
+    const int W = avg <= 4.5 ? 4 : (avg <= 9.5 ? 8 : (avg <= 20 ? 16 : 32));
+    int grid = (int)std::min<int64_t>(cdiv(std::max<int64_t>(1, A->nr) * W, 256), 148 * 16);
     if (grid < 1) grid = 1;
-    k_spmv<<<grid, 256, 0, ctx->s>>>(A->nr, A->ptr, A->col, A->val, x, y);
+    switch (W) {
+      case 4: k_spmv_sub<4><<<grid, 256, 0, ctx->s>>>(A->nr, A->ptr, A->col, A->val, x, y); break;
+      case 8: k_spmv_sub<8><<<grid, 256, 0, ctx->s>>>(A->nr, A->ptr, A->col, A->val, x, y); break;
+      case 16: k_spmv_sub<16><<<grid, 256, 0, ctx->s>>>(A->nr, A->ptr, A->col, A->val, x, y); break;
+      default: k_spmv<<<grid, 256, 0, ctx->s>>>(A->nr, A->ptr, A->col, A->val, x, y);
+    }
     check_launch();
     ctx->launches++;
   } else {
@@ -4645,6 +4791,7 @@ extern "C" int mfh_csr_create(mfh_ctx *ctx, int64_t n_rows, int64_t n_cols, cons
   A->nr = n_rows;
   A->nc = n_cols;
   int64_t nnz = indptr[n_rows];
+  A->nnz = nnz;
   CK(cudaMalloc(&A->ptr, sizeof(int64_t) * (n_rows + 1)));
   CK(cudaMalloc(&A->col, sizeof(int) * std::max<int64_t>(1, nnz)));
   CK(cudaMalloc(&A->val, sizeof(double) * std::max<int64_t>(1, nnz)));

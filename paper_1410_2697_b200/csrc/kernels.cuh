@@ -2628,6 +2628,75 @@ __global__ void __launch_bounds__(256) k_gemv_mv(const GemvJob *__restrict__ job
 }
 
 // ---------------------------------------------------------------------------
+// apply, low levels: one CTA per group of whole dense subtrees, both passes
+// ---------------------------------------------------------------------------
+// The fronts below the first level holding a structured front form
+// independent subtrees. A CTA owns whole subtrees and walks their levels with
+// CTA barriers instead of kernel boundaries: per level, the contribution
+// gathers of all its fronts' pivots (upward), then all their GEMV rows, warps
+// spread over the rows of every front of the level. Every row is computed by
+// gemv_rows(_mv) and every gather in k_contrib_gather's order, so the results
+// are bitwise the per-level graph's; one launch per pass.
+struct SubSeg {   // one level of one CTA
+  int jb, je;     // GEMV jobs [jb, je) (rows numbered by start[jb .. je])
+  int gb, ge;     // pivot ids to gather, gids[gb .. ge)
+};
+struct SubApply {
+  const SubSeg *seg;
+  const int *cta_seg;      // segments [cta_seg[c], cta_seg[c + 1]) in level order
+  const GemvJob *job;      // upward (t = Gfp b_piv) or downward (x = Pinv b - Gpf x_fro) jobs
+  const int *start;        // row prefix per job (global numbering)
+  const long long *gids;   // pivot ids gathered before each upward level
+  const long long *cptr, *coff;
+  double *cbuf, *bu;
+  long long cst, nst;      // vector strides (several right-hand sides)
+};
+template <int NV>
+__device__ __forceinline__ void sub_level_rows(const SubApply &S, const SubSeg &g, int warp, int nw, int lane) {
+  const int r0 = S.start[g.jb], r1 = S.start[g.je];
+  const int chunk = (r1 - r0 + nw - 1) / nw;
+  const int t0 = r0 + warp * chunk, t1 = min(r1, t0 + chunk);
+  if (t0 >= t1) return;
+  int lo = g.jb, hi = g.je - 1;  // last job with start <= t0
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (S.start[mid] <= t0) lo = mid; else hi = mid - 1;
+  }
+  if (NV == 1)
+    gemv_rows(S.job, S.start, lo, t0, t1, lane);
+  else
+    gemv_rows_mv<NV>(S.job, S.start, lo, t0, t1, lane);
+}
+template <int NV>
+__global__ void __launch_bounds__(512) k_apply_sub(SubApply S, int up) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int s0 = S.cta_seg[blockIdx.x], s1 = S.cta_seg[blockIdx.x + 1];
+  for (int k = 0; k < s1 - s0; ++k) {
+    const SubSeg g = S.seg[up ? s0 + k : s1 - 1 - k];
+    if (up && g.ge > g.gb) {
+      // b_u[piv] -= contributions of the descendants, in post order
+      for (int t = g.gb + warp; t < g.ge; t += nw) {
+        const long long gg = S.gids[t], b = S.cptr[gg], e = S.cptr[gg + 1];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double *cb = S.cbuf + v * S.cst;
+          double acc = S.bu[v * S.nst + gg];
+          for (long long q0 = b; q0 < e; q0 += 32) {
+            const double x = q0 + lane < e ? cb[S.coff[q0 + lane]] : 0.0;
+            const int mm = (int)(e - q0 < 32 ? e - q0 : 32);
+            for (int r = 0; r < mm; ++r) acc = acc - __shfl_sync(0xffffffffu, x, r);
+          }
+          if (lane == 0) S.bu[v * S.nst + gg] = acc;
+        }
+      }
+      __syncthreads();  // gathered b_piv visible to every warp
+    }
+    sub_level_rows<NV>(S, g, warp, nw, lane);
+    __syncthreads();  // this level's results visible to the next level (same CTA)
+  }
+}
+
+// ---------------------------------------------------------------------------
 // solve-phase vector kernels
 // ---------------------------------------------------------------------------
 __global__ void k_scatter_perm(const double *__restrict__ b, const long long *__restrict__ perm,
@@ -2801,6 +2870,26 @@ __global__ void __launch_bounds__(256) k_mgs_coop(const double *__restrict__ V, 
 }
 
 // CSR SpMV, one warp per row (A @ x, sparse.py:277-284)
+// CSR SpMV with W lanes per row (W = 4, 8, 16: the power of two at or above
+// the average row length), so short stencil rows (7 / 9 / 27 nonzeros) keep
+// every lane busy: lane-strided partial sums, then an xor tree in the group
+template <int W>
+__global__ void __launch_bounds__(256) k_spmv_sub(long long nrows, const long long *__restrict__ ptr,
+                                                  const int *__restrict__ col, const double *__restrict__ val,
+                                                  const double *__restrict__ x, double *__restrict__ y) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int l = threadIdx.x & (W - 1);
+  const long long ng = ((long long)gridDim.x * blockDim.x) / W;
+  for (long long r = t / W; r < nrows; r += ng) {
+    double s = 0.0;
+    const long long p1 = __ldg(ptr + r + 1);
+    for (long long p = __ldg(ptr + r) + l; p < p1; p += W) s = fma(__ldg(val + p), __ldg(x + __ldg(col + p)), s);
+#pragma unroll
+    for (int o = W >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, W);
+    if (l == 0) y[r] = s;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_spmv(long long nrows, const long long *__restrict__ ptr,
                                               const int *__restrict__ col,
                                               const double *__restrict__ val,

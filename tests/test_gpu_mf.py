@@ -310,3 +310,21 @@ def test_pivot_block_forms_agree(monkeypatch, name):
     assert pp0.keys() == pp1.keys() and pp0
     for p in pp0:
         assert np.linalg.norm(pp1[p] - pp0[p]) <= 1e-10 * np.linalg.norm(pp0[p])
+
+
+def test_subtree_apply_bitwise_equal_to_per_level(monkeypatch):
+    """The low dense levels of the apply run as whole subtrees per CTA (one
+    launch per pass); every row and gather keeps the per-level kernels'
+    arithmetic, so mf_solve is bitwise the per-level graph's, for one and for
+    several right-hand sides."""
+    import paper_1410_2697_b200 as P
+    A, _ = P.gen_poisson7(20, 19, 18)
+    et = P.build_elimination_tree(P.nested_dissection(P.adjacency_graph(A), 32), A)
+    B = np.random.default_rng(4).standard_normal((A.n_rows, 3))
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("MFH_APPLY_SUBTREE", flag)
+        F = P.mf_factorize(A, et, P.ACCELERATED, P.MfParams(n_c=200, eps=1e-6, n_leaf=32))
+        out[flag] = (P.mf_solve(F, B[:, 0]), P.mf_solve(F, B))
+    np.testing.assert_array_equal(out["0"][0], out["1"][0])
+    np.testing.assert_array_equal(out["0"][1], out["1"][1])

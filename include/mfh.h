@@ -158,16 +158,29 @@ int mfh_factorize(mfh_ctx *ctx, const mfh_etree *t, int64_t n, const int64_t *in
  * written by exactly one rank and is zero elsewhere, so the sum is exact.
  * Returns 0 on success. */
 typedef int (*mfh_exchange_fn)(void *user, double *d_buf, int64_t count);
+/* Point-to-point transfers of DEVICE buffers posted as one group (NCCL group
+ * semantics: no ordering among the ops): op i sends (is_send[i] = 1) or
+ * receives counts[i] doubles of bufs[i] to / from rank peers[i]. Ordered after
+ * the work on the context stream, like mfh_exchange_fn. Returns 0 on success. */
+typedef int (*mfh_p2p_fn)(void *user, int64_t nops, double *const *bufs, const int64_t *counts,
+                          const int32_t *peers, const int32_t *is_send);
 typedef struct {
   const int32_t *owner; /* per etree node id: the rank that factors it (subtrees whole) */
   int rank;             /* this rank */
   mfh_exchange_fn exchange;
   void *user;
+  /* optional: with it, a child update crossing ranks travels in its own
+   * compressed form (the update HODLR's leaves and blocks, W, V^T: the
+   * reference's UpdateRep, hodlr.py:429-470) from the child's owner to the
+   * parent's owner only; without it, every cut update is densified and
+   * all-reduced to every rank */
+  mfh_p2p_fn p2p;
 } mfh_shard_t;
 /* mf_factorize over the nodes this rank owns, in global height order. After
  * each height with a child -> parent edge between ranks, the children's
- * updates are densified by their owners (bitwise the per-child term of the
- * parent's sampler) into a fresh buffer and exchanged. The factor's stats
+ * updates go to the parents' owners: serialized in their compressed form and
+ * sent point to point (shard->p2p), or densified (bitwise the per-child term
+ * of the parent's sampler) and all-reduced (no p2p callback). The factor's stats
  * cover the whole tree (per-node accounting exchanged). mfh_apply /
  * mfh_gmres on it run the global apply levels on this rank's fronts, with the
  * contribution buffer (upward) and x (downward) exchanged at the level

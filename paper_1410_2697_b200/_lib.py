@@ -31,11 +31,13 @@ class mfh_params(C.Structure):
 
 # int (*)(void *user, double *d_buf, int64_t count): in-place all-reduce SUM
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64)
+P2P_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
+                     C.POINTER(C.c_int32), C.POINTER(C.c_int32))
 
 
 class mfh_shard_t(C.Structure):
     _fields_ = [("owner", C.POINTER(C.c_int32)), ("rank", C.c_int), ("exchange", EXCHANGE_FN),
-                ("user", C.c_void_p)]
+                ("user", C.c_void_p), ("p2p", P2P_FN)]
 
 
 class mfh_stats_t(C.Structure):

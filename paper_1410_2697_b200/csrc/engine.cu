@@ -1349,6 +1349,7 @@ struct FrontH {
   int upd_ld = 0;
   const double *W = nullptr, *Vt = nullptr;
   int rw = 0, ldw = 0, ldv = 0;
+  const HNode *rx_nodes = nullptr;  // sharded: update HODLR received from the child's owner
   // accounting
   int64_t front_reals = 0, factor_reals = 0, upd_reals = 0;
   int64_t hint = 0;
@@ -1397,7 +1398,9 @@ struct mfh_factor {
   std::vector<int8_t> mine;
   int rank = 0, world = 1;
   mfh_exchange_fn exchange = nullptr;
+  mfh_p2p_fn p2p = nullptr;
   void *xuser = nullptr;
+  int64_t xchg_bytes = 0;  // bytes this rank sent in update exchanges (diagnostics)
   void exchange_or_throw(double *d, int64_t count) {
     if (count <= 0) return;
     if (exchange(xuser, d, count) != 0) throw mfh::runtime_error("shard exchange callback failed");
@@ -1748,7 +1751,7 @@ struct Factorizer {
           ch.ldd = c.upd_ld;
         } else {
           ch.kind = 1;
-          ch.hn = F->trees[c.ff].d_nodes;
+          ch.hn = c.rx_nodes ? c.rx_nodes : F->trees[c.ff].d_nodes;
           ch.W = c.W;
           ch.Vt = c.Vt;
           ch.rw = c.rw;
@@ -2846,6 +2849,147 @@ struct Factorizer {
     }
   }
 
+  // ---- sharded, compressed (the p2p path): every cut child's update travels
+  // from its owner to its parent's owner only, in its own form -- a dense
+  // Schur block, or the reference's UpdateRep (hodlr.py:429-470): the update
+  // HODLR's leaves and blocks behind an HNode table whose pointers are
+  // offsets, then W and V^T. Sizes first (one small all-reduce of disjoint
+  // meta slots), then one group of sends / receives; the receiver rebases the
+  // table. The parent's sampler then reads the same numbers it would read on
+  // one GPU: bitwise the single-GPU factorization.
+  void exchange_updates_p2p(const std::vector<int> &cuts) {
+    Sink s{ctx};
+    const int K = (int)cuts.size();
+    constexpr int MW = 6;  // kind, length, table slots, rw, offset of W, offset of V^T
+    std::vector<double> meta((size_t)MW * K, 0.0);
+    std::vector<double *> sbuf(K, nullptr);
+    std::vector<CopyJob> cps;
+    std::vector<std::vector<HNode>> tables(K);
+    auto parent_post = [&](int q) { return pidx_[et->parent[F->fronts[q].node]]; };
+    for (int k = 0; k < K; ++k) {
+      const int q = cuts[k];
+      if (!F->mine[q]) continue;
+      FrontH &c = F->fronts[q];
+      const int rh = release_height(c);
+      double *m = meta.data() + (size_t)MW * k;
+      if (c.upd == 0) {
+        const int64_t len = (int64_t)c.nf * c.nf;
+        sbuf[k] = upd.d(std::max<int64_t>(1, len), rh);
+        cps.push_back(CopyJob{c.upd_dense, sbuf[k], c.nf, c.nf, c.upd_ld, c.nf, nullptr, nullptr});
+        m[0] = 0;
+        m[1] = (double)len;
+        continue;
+      }
+      HTree &T = F->trees[c.ff];
+      const int64_t tab = (int64_t)cdiv((int64_t)sizeof(HNode) * T.nslots, (int64_t)sizeof(double));
+      int64_t off = tab;
+      struct Pend {
+        const double *src;
+        int64_t at;
+        int r, cl, lds;
+      };
+      std::vector<Pend> pend;
+      auto put = [&](const double *src, int r, int cl, int lds) -> const double * {
+        if (!src || (int64_t)r * cl == 0) return nullptr;
+        pend.push_back(Pend{src, off, r, cl, lds});
+        const int64_t at = off;
+        off += (int64_t)r * cl;
+        return (const double *)(uintptr_t)at;
+      };
+      auto blk = [&](const BlockH &b) {
+        HBlk h = b.dev();
+        if (b.dense) {
+          h.a = put(b.val, b.m, b.n, b.n);
+        } else {
+          h.a = put(b.col, b.m, b.rank, b.rank);
+          h.b = put(b.row, b.rank, b.n, b.n);
+        }
+        return h;
+      };
+      std::vector<HNode> &tb = tables[k];
+      tb.assign(T.nslots, HNode{});
+      for (int v = 0; v < T.nslots; ++v) {
+        if (T.leaf[v] == 1) {
+          const int sz = T.hi[v] - T.lo[v];
+          tb[v].leaf = put(T.lval[v], sz, sz, sz);
+        } else if (T.leaf[v] == 0) {
+          tb[v].up = blk(F->blocks[T.up[v]]);
+          tb[v].lw = blk(F->blocks[T.lw[v]]);
+        }
+      }
+      const int64_t oW = off;
+      put(c.W, c.nf, c.rw, c.ldw);
+      const int64_t oV = off;
+      put(c.Vt, c.rw, c.nf, c.ldv);
+      sbuf[k] = upd.d(std::max<int64_t>(1, off), rh);
+      for (auto &p : pend) cps.push_back(CopyJob{p.src, sbuf[k] + p.at, p.r, p.cl, p.lds, p.cl, nullptr, nullptr});
+      s.push_to(sbuf[k], tb.data(), sizeof(HNode) * tb.size());
+      m[0] = 1;
+      m[1] = (double)off;
+      m[2] = T.nslots;
+      m[3] = c.rw;
+      m[4] = (double)oW;
+      m[5] = (double)oV;
+    }
+    run_copy(s, cps);
+    // every rank learns every payload's size (disjoint slots: the sum is exact)
+    double *dm = ctx->scratch.d(std::max<size_t>(1, meta.size()));
+    s.push_to(dm, meta.data(), sizeof(double) * meta.size());
+    F->exchange_or_throw(dm, (int64_t)meta.size());
+    CK(cudaMemcpyAsync(meta.data(), dm, sizeof(double) * meta.size(), cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    std::vector<double *> bufs;
+    std::vector<int64_t> counts;
+    std::vector<int32_t> peers, sends;
+    std::vector<std::pair<int, double *>> recv;
+    for (int k = 0; k < K; ++k) {
+      const int q = cuts[k], pq = parent_post(q);
+      const int from = F->owner[q], to = F->owner[pq];
+      const int64_t len = (int64_t)meta[(size_t)MW * k + 1];
+      if (len <= 0 || from == to) continue;
+      if (F->mine[q]) {
+        bufs.push_back(sbuf[k]);
+        counts.push_back(len);
+        peers.push_back(to);
+        sends.push_back(1);
+        F->xchg_bytes += 8 * len;
+      } else if (F->mine[pq]) {
+        double *rb = upd.d(len, release_height(F->fronts[q]));
+        bufs.push_back(rb);
+        counts.push_back(len);
+        peers.push_back(from);
+        sends.push_back(0);
+        recv.push_back({k, rb});
+      }
+    }
+    if (!bufs.empty() &&
+        F->p2p(F->xuser, (int64_t)bufs.size(), bufs.data(), counts.data(), peers.data(), sends.data()) != 0)
+      throw runtime_error("shard point-to-point callback failed");
+    for (auto &r : recv) {
+      const int k = r.first;
+      FrontH &c = F->fronts[cuts[k]];
+      const double *m = meta.data() + (size_t)MW * k;
+      if (m[0] == 0) {
+        c.upd = 0;
+        c.upd_dense = r.second;
+        c.upd_ld = c.nf;
+        continue;
+      }
+      const int ns = (int)m[2];
+      HNode *t = (HNode *)r.second;
+      k_rebase_hnodes<<<(unsigned)cdiv(ns, 128), 128, 0, ctx->s>>>(t, ns, r.second);
+      check_launch();
+      ctx->launches++;
+      c.upd = 1;
+      c.rx_nodes = t;
+      c.rw = (int)m[3];
+      c.W = r.second + (int64_t)m[4];
+      c.ldw = c.rw;
+      c.Vt = r.second + (int64_t)m[5];
+      c.ldv = c.nf;
+    }
+  }
+
   // ---- sharded: the numeric accounting of fronts factored elsewhere, for the
   // whole-tree stats replay
   void exchange_accounting() {
@@ -3140,6 +3284,7 @@ struct Factorizer {
       F->sharded = true;
       F->rank = shard->rank;
       F->exchange = shard->exchange;
+      F->p2p = shard->p2p;
       F->xuser = shard->user;
       if (!shard->owner || !shard->exchange) throw value_error("shard needs an owner array and an exchange callback");
       F->owner.assign(F->fronts.size(), 0);
@@ -3286,7 +3431,7 @@ struct Factorizer {
         f.upd_reals = (int64_t)f.nf * f.nf;
       }
       if (byh[h].empty()) {
-        if (!cut_at[h].empty()) exchange_updates(cut_at[h]);
+        if (!cut_at[h].empty()) (F->p2p ? exchange_updates_p2p(cut_at[h]) : exchange_updates(cut_at[h]));
         upd.release_upto(h);
         continue;
       }
@@ -3320,7 +3465,7 @@ struct Factorizer {
         check_flags(0);
         ctx->scratch.reset();
       }
-      if (!cut_at[h].empty()) exchange_updates(cut_at[h]);
+      if (!cut_at[h].empty()) (F->p2p ? exchange_updates_p2p(cut_at[h]) : exchange_updates(cut_at[h]));
       upd.release_upto(h);  // dense front buffers whose parents have sampled them
     }
     CK(cudaEventRecord(e_end, ctx->s));

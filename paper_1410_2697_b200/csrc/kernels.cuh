@@ -35,6 +35,23 @@ struct HNode {
   HBlk up, lw;         // rows lo:mid x cols mid:hi ; rows mid:hi x cols lo:mid
 };
 
+// a serialized update HODLR (sharded exchange): the table's pointers are
+// offsets in doubles from the payload base (0 = null); make them addresses
+__global__ void k_rebase_hnodes(HNode *__restrict__ t, int n, const double *base) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  HNode h = t[i];
+  auto fix = [&](const double *&p) {
+    if (p) p = base + (unsigned long long)p;
+  };
+  fix(h.leaf);
+  fix(h.up.a);
+  fix(h.up.b);
+  fix(h.lw.a);
+  fix(h.lw.b);
+  t[i] = h;
+}
+
 // child update as seen by the parent's entry sampler
 struct DChild {
   const int *to_child;  // parent front position -> child position or -1

@@ -4,9 +4,13 @@ Nested-dissection subtrees are independent: every rank factors the subtrees
 it owns with no communication; the few fronts above the cut (the "top") are
 dealt to ranks height by height so siblings factor in parallel. The exchange
 step is a child update crossing ranks: after each height with such an edge,
-the owners densify those children's updates (bitwise the per-child term the
-parent's sampler adds, multifrontal.py:329-348) into a fresh buffer, and one
-all-reduce SUM over disjoint slots delivers them. The preconditioner apply
+each such update travels from the child's owner to the parent's owner only,
+point to point, in its own compressed form -- the reference's UpdateRep
+(hodlr.py:429-470): the update HODLR's leaves and low-rank / dense blocks
+behind a node table whose pointers are offsets, then W and V^T -- and the
+receiver rebases the table, so the parent's sampler reads exactly the numbers
+it reads on one GPU (multifrontal.py:329-348). ``compressed=False`` keeps the
+earlier path: every cut update densified and all-reduced to every rank. The preconditioner apply
 (mf_solve, multifrontal.py:533-560) runs the global apply levels on each
 rank's fronts and all-reduces the contribution buffer (upward) and x
 (downward) only at level boundaries where a dependency crosses ranks, then x
@@ -131,7 +135,10 @@ class TorchExchange:
         self.stream = torch.cuda.ExternalStream(ctx.info()[0])
         self.calls = 0
         self.bytes = 0
+        self.p2p_calls = 0
+        self.p2p_bytes = 0
         self.cfn = _lib.EXCHANGE_FN(self._call)
+        self.pfn = _lib.P2P_FN(self._p2p)
 
     def _call(self, user, dptr, count):
         import torch
@@ -154,7 +161,40 @@ class TorchExchange:
             return 1
 
 
-def mf_factorize_sharded(A, tree, mode=ACCELERATED, params=None, group=None, partition=None):
+    def _p2p(self, user, nops, bufs, counts, peers, sends):
+        """mfh_p2p_fn: one group of sends / receives of device buffers (NCCL
+        batch_isend_irecv on the library stream, or gloo through host staging)."""
+        import torch
+        import torch.distributed as dist
+        try:
+            ts = [torch.as_tensor(_CudaArray(bufs[i], counts[i]), device="cuda") for i in range(nops)]
+            with torch.cuda.stream(self.stream):
+                if self.device_collective:
+                    ops = [dist.P2POp(dist.isend if sends[i] else dist.irecv, ts[i], int(peers[i]), group=self.group)
+                           for i in range(nops)]
+                    for w in dist.batch_isend_irecv(ops):
+                        w.wait()
+                else:
+                    self.stream.synchronize()
+                    host = [t.cpu() if sends[i] else torch.empty(int(counts[i]), dtype=torch.float64)
+                            for i, t in enumerate(ts)]
+                    reqs = [(dist.isend if sends[i] else dist.irecv)(host[i], int(peers[i]), group=self.group)
+                            for i in range(nops)]
+                    for r in reqs:
+                        r.wait()
+                    for i in range(nops):
+                        if not sends[i]:
+                            ts[i].copy_(host[i])
+                    self.stream.synchronize()
+            self.p2p_calls += 1
+            self.p2p_bytes += 8 * sum(int(counts[i]) for i in range(nops) if sends[i])
+            return 0
+        except Exception:
+            traceback.print_exc()
+            return 1
+
+
+def mf_factorize_sharded(A, tree, mode=ACCELERATED, params=None, group=None, partition=None, compressed=True):
     """mf_factorize over torch.distributed ranks: this rank's subtrees and top
     fronts; returns a factorization whose stats cover the whole tree and whose
     apply / GMRES return the full solution on every rank."""
@@ -171,7 +211,8 @@ def mf_factorize_sharded(A, tree, mode=ACCELERATED, params=None, group=None, par
     part = partition or SubtreePartition(tree, world)
     owners = part.owners()
     ex = TorchExchange(group)
-    sh = _lib.mfh_shard_t(owners.ctypes.data_as(C.POINTER(C.c_int32)), rank, ex.cfn, None)
+    sh = _lib.mfh_shard_t(owners.ctypes.data_as(C.POINTER(C.c_int32)), rank, ex.cfn, None,
+                          ex.pfn if compressed else _lib.P2P_FN())
     ctx = _lib.context()
     ip, ix, dv = A.csr_arrays()
     p = _lib.mfh_params(int(min(params.n_c, 2**62)), float(params.eps), int(params.d),

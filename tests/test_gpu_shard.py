@@ -1,8 +1,9 @@
 """Subtree-sharded factorization on the GPU: world-size-2 and -3
 gloo groups of processes sharing one GPU (the exchanges are host-side between
-launches, so no kernel waits on another rank). The sharded preconditioner's
-apply, GMRES solution and iteration count, stats and records must be bitwise
-equal to the single-GPU factorization's."""
+launches, so no kernel waits on another rank). With the compressed
+point-to-point update exchange and with the dense all-reduce fallback, the
+sharded preconditioner's apply, GMRES solution and iteration count, stats and
+records must be bitwise equal to the single-GPU factorization's."""
 import os
 import socket
 
@@ -43,12 +44,17 @@ def _worker(rank, world, port, case, q):
         tree = P.build_elimination_tree(P.nested_dissection(P.adjacency_graph(A), leaf), A)
         params = P.MfParams(**kw)
         b = np.random.default_rng(0).standard_normal(A.n_rows)
-        F = mf_factorize_sharded(A, tree, P.ACCELERATED, params)
-        x = P.mf_solve(F, b)
-        xg, h = P.gmres(A, b, M=P.mf_preconditioner(F), tol=1e-10, restart=30)
-        out = dict(rank=rank, x=x, xg=xg, its=h.iterations, hist=np.asarray(h.residuals), recs=_recs(F),
-                   peak=F.stats.peak_stored_reals, counts=(F.stats.structured_fronts, F.stats.dense_fronts),
-                   calls=F.exchange.calls, owners=F.partition.owners())
+        out = dict(rank=rank)
+        for compressed in (True, False):
+            F = mf_factorize_sharded(A, tree, P.ACCELERATED, params, compressed=compressed)
+            x = P.mf_solve(F, b)
+            xg, h = P.gmres(A, b, M=P.mf_preconditioner(F), tol=1e-10, restart=30)
+            out[compressed] = dict(x=x, xg=xg, its=h.iterations, hist=np.asarray(h.residuals), recs=_recs(F),
+                                   peak=F.stats.peak_stored_reals,
+                                   counts=(F.stats.structured_fronts, F.stats.dense_fronts),
+                                   calls=F.exchange.calls, p2p=F.exchange.p2p_calls, p2p_bytes=F.exchange.p2p_bytes,
+                                   owners=F.partition.owners())
+            F = None
         if rank == 0:
             F1 = P.mf_factorize(A, tree, P.ACCELERATED, params)
             x1g, h1 = P.gmres(A, b, M=P.mf_preconditioner(F1), tol=1e-10, restart=30)
@@ -78,12 +84,18 @@ def test_sharded_factor_bitwise_equals_single(world, case):
     for o in outs:
         assert "error" not in o, o.get("error")
     r0 = outs[0]
-    assert len(set(r0["owners"].tolist())) == world  # every rank owns fronts
-    for o in outs:
-        assert o["calls"] > 0
-        np.testing.assert_array_equal(o["x"], r0["x1"])
-        np.testing.assert_array_equal(o["xg"], r0["x1g"])
-        assert o["its"] == r0["its1"]
-        np.testing.assert_array_equal(o["hist"], r0["hist1"])
-        assert o["recs"] == r0["recs1"]
-        assert o["peak"] == r0["peak1"] and o["counts"] == r0["counts1"]
+    assert len(set(r0[True]["owners"].tolist())) == world  # every rank owns fronts
+    # compressed point-to-point update exchange (UpdateRep form) and the dense
+    # all-reduce fallback: both bitwise the single-GPU factorization
+    for compressed in (True, False):
+        for o in outs:
+            c = o[compressed]
+            assert c["calls"] > 0
+            np.testing.assert_array_equal(c["x"], r0["x1"])
+            np.testing.assert_array_equal(c["xg"], r0["x1g"])
+            assert c["its"] == r0["its1"]
+            np.testing.assert_array_equal(c["hist"], r0["hist1"])
+            assert c["recs"] == r0["recs1"]
+            assert c["peak"] == r0["peak1"] and c["counts"] == r0["counts1"]
+    assert sum(o[True]["p2p"] for o in outs) > 0 and sum(o[True]["p2p_bytes"] for o in outs) > 0
+    assert all(o[False]["p2p"] == 0 for o in outs)

@@ -714,21 +714,6 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
   });
 }
 
-static void run_check_finite(Sink &sk, const std::vector<LuJob> &jobs) {
-  OpClock oc_("check_finite");
-  if (jobs.empty()) return;
-  int64_t mx = 1;
-  for (auto &j : jobs) mx = std::max<int64_t>(mx, (int64_t)j.n * j.n);
-  for (size_t b = 0; b < jobs.size(); b += 60000) {
-    std::vector<LuJob> part(jobs.begin() + b, jobs.begin() + std::min(jobs.size(), b + 60000));
-    LuJob *dj = sk.push(part);
-    dim3 grid((unsigned)std::min<int64_t>(cdiv(mx, 1024), 64), (unsigned)part.size());
-    sk.launch([=](cudaStream_t s) {
-      k_check_finite<<<grid, 256, 0, s>>>(dj);
-      check_launch();
-    });
-  }
-}
 
 // Full triangular inverse out = T^{-1} (n x n, ld n) of a unit-lower (upper = 0)
 // or non-unit upper (upper = 1) triangle: the 64 x 64 diagonal blocks in one
@@ -2438,17 +2423,22 @@ struct Factorizer {
       int maxd = 0;
       for (int tt : ptrees) maxd = std::max(maxd, F->trees[tt].maxdepth);
       for (int d = maxd; d >= 0; --d) {
-        struct Nd {
-          HTree *T;
-          int v;
-          double *xt, *xb, *yt, *yb, *Tm;
-        };
-        std::vector<Nd> nodes;
-        std::vector<GemmJob> ga, gc, gd, ge, gsch, gs1, gs2;
+        // Per node v = [L | R] (hodlr.py:330-352) with D = diag(H_L, H_R),
+        // x_top = H_L^{-1} col1, x_bot = H_R^{-1} col2, y_top = row1 H_R^{-1},
+        // y_bot = row2 H_L^{-1}, and the Woodbury core C = [[I, A], [B, I]]
+        // (A = row1 x_bot, B = row2 x_top, the reference's core):
+        //   H_v^{-1} = D^{-1} - diag(x_top, x_bot) Tm,  Tm = C^{-1} [[0, y_top], [y_bot, 0]].
+        // C^{-1} is never formed: through the Schur complement of the smaller
+        // side, S = I - B A (r2 <= r1),
+        //   Tm = [[-A Z1, y_top + A Z2], [Z1, -Z2]],  Z1 = S^{-1} y_bot, Z2 = S^{-1} (B y_top)
+        // (mirrored with S = I - A B when r1 < r2); C is singular iff S is
+        // (the reference's core check, hodlr.py:346-352). Launches per level:
+        // x / y, A / B, S + (B y_top | A y_bot), S^{-1}, Z, the top rows, Hinv.
+        std::vector<GemmJob> ga, gc, gsch, gz, gt, ge;
         std::vector<double *> ip;
         std::vector<int> idim, ild;
-        std::vector<LuJob> fin;
         std::vector<InvReq> invs;
+        bool any = false;
         for (int tt : ptrees) {
           HTree &T = F->trees[tt];
           FrontH &f = F->fronts[T.fi];
@@ -2465,13 +2455,11 @@ struct Factorizer {
             T.r1[v] = r1;
             T.r2[v] = r2;
             if (rr == 0) continue;
+            any = true;
             double *HLL = f.Hinv + (int64_t)lo * N + lo, *HRR = f.Hinv + (int64_t)mid * N + mid;
-            Nd nd{&T, v, nullptr, nullptr, nullptr, nullptr, nullptr};
-            nd.xt = ctx->scratch.d((size_t)m1 * std::max(1, r1));
-            nd.xb = ctx->scratch.d((size_t)m2 * std::max(1, r2));
-            nd.yt = ctx->scratch.d((size_t)std::max(1, r1) * m2);
-            nd.yb = ctx->scratch.d((size_t)std::max(1, r2) * m1);
-            nd.Tm = f.pform ? F->arena.d((size_t)rr * nv) : ctx->scratch.d((size_t)rr * nv);
+            double *xt = ctx->scratch.d((size_t)m1 * std::max(1, r1));
+            double *xb = ctx->scratch.d((size_t)m2 * std::max(1, r2));
+            double *Tm = f.pform ? F->arena.d((size_t)rr * nv) : ctx->scratch.d((size_t)rr * nv);
             if (f.pform) {
               FrontH::TmNode tn{};
               tn.slot = v;
@@ -2479,88 +2467,74 @@ struct Factorizer {
               tn.nv = nv;
               tn.r1 = r1;
               tn.r2 = r2;
-              tn.Tm = nd.Tm;
-              tn.xt = nd.xt;
-              tn.xb = nd.xb;
+              tn.Tm = Tm;
+              tn.xt = xt;
+              tn.xb = xb;
               tn.woff = f.wlen;
               f.wlen += rr;
               f.tnode.push_back(tn);
             }
-            // (a) x_top = H_L^{-1} col1, x_bot = H_R^{-1} col2, y_top = row1 H_R^{-1}, y_bot = row2 H_L^{-1}
-            if (r1) {
-              ga.push_back(GemmJob{HLL, f1.col, nd.xt, m1, r1, m1, N, f1.ldc, r1, 1.0, 0.0});
-              ga.push_back(GemmJob{f1.row, HRR, nd.yt, r1, m2, m2, f1.ldr, N, m2, 1.0, 0.0});
-            }
-            if (r2) {
-              ga.push_back(GemmJob{HRR, f2.col, nd.xb, m2, r2, m2, N, f2.ldc, r2, 1.0, 0.0});
-              ga.push_back(GemmJob{f2.row, HLL, nd.yb, r2, m1, m1, f2.ldr, N, m1, 1.0, 0.0});
-            }
-            // (b) Woodbury core (hodlr.py:343-345) C = [[I, A], [B, I]], A = row1 x_bot,
-            // B = row2 x_top, and its inverse through the Schur complement of the
-            // smaller side: with S = I - B A (r2 <= r1),
-            //   C^{-1} = [[I + A S^{-1} B, -A S^{-1}], [-S^{-1} B, S^{-1}]]
-            // (mirrored with S = I - A B when r1 < r2): one inverse of
-            // min(r1, r2) instead of r1 + r2, the rest batched GEMMs. C is
-            // singular iff S is (the reference's core check, hodlr.py:346-352).
-            T.core[v] = ctx->scratch.d((size_t)rr * rr);
-            ip.push_back(T.core[v]);
-            idim.push_back(rr);
-            ild.push_back(rr);
-            double *C = T.core[v];
-            if (r1 && r2) {
-              gc.push_back(GemmJob{f1.row, nd.xb, C + r1, r1, r2, m2, f1.ldr, r2, rr, 1.0, 1.0});
-              gc.push_back(GemmJob{f2.row, nd.xt, C + (int64_t)r1 * rr, r2, r1, m1, f2.ldr, r1, rr, 1.0, 1.0});
-            }
+            double *Ttl = Tm, *Ttr = Tm + m1;                                      // rows [0, r1)
+            double *Tbl = Tm + (int64_t)r1 * nv, *Tbr = Tm + (int64_t)r1 * nv + m1;  // rows [r1, rr)
+            if (r1) ga.push_back(GemmJob{HLL, f1.col, xt, m1, r1, m1, N, f1.ldc, r1, 1.0, 0.0});
+            if (r2) ga.push_back(GemmJob{HRR, f2.col, xb, m2, r2, m2, N, f2.ldc, r2, 1.0, 0.0});
             std::string msg = "singular coupling core at node [" + std::to_string(lo) + ", " + std::to_string(hi) + ")";
-            int fl = new_flag(msg, (int64_t)T.fi * 1000000 + v);
-            fin.push_back(LuJob{C, rr, rr, nullptr, d_flags + fl});
-            double *Ci = T.cinv[v] = ctx->scratch.d((size_t)rr * rr);
-            double *A = C + r1, *B = C + (int64_t)r1 * rr;
-            if (!(r1 && r2)) {  // C = I exactly
-              ip.push_back(Ci);
-              idim.push_back(rr);
-              ild.push_back(rr);
-            } else if (r2 <= r1) {
-              double *S = ctx->scratch.d((size_t)r2 * r2);
-              ip.push_back(S), idim.push_back(r2), ild.push_back(r2);
-              ip.push_back(Ci), idim.push_back(r1), ild.push_back(rr);  // top-left starts as I
-              gsch.push_back(GemmJob{B, A, S, r2, r2, r1, rr, rr, r2, -1.0, 1.0});
-              double *Si = Ci + (int64_t)r1 * rr + r1;
-              invs.push_back(InvReq{S, r2, r2, Si, rr, r2 > INV_SMALL ? ctx->scratch.i(r2) : nullptr, d_flags + fl});
-              gs1.push_back(GemmJob{Si, B, Ci + (int64_t)r1 * rr, r2, r1, r2, rr, rr, rr, -1.0, 0.0});
-              gs1.push_back(GemmJob{A, Si, Ci + r1, r1, r2, r2, rr, rr, rr, -1.0, 0.0});
-              gs2.push_back(GemmJob{A, Ci + (int64_t)r1 * rr, Ci, r1, r1, r2, rr, rr, rr, -1.0, 1.0});
+            if (!(r1 && r2)) {  // C = I: Tm = [[0, y_top]] or [[y_bot, 0]]
+              if (r1) {
+                ga.push_back(GemmJob{f1.row, HRR, Ttr, r1, m2, m2, f1.ldr, N, nv, 1.0, 0.0});
+                gt.push_back(GemmJob{nullptr, nullptr, Ttl, r1, m1, 0, 1, 1, nv, 0.0, 0.0});  // zeros
+              } else {
+                ga.push_back(GemmJob{f2.row, HLL, Tbl, r2, m1, m1, f2.ldr, N, nv, 1.0, 0.0});
+                gt.push_back(GemmJob{nullptr, nullptr, Tbr, r2, m2, 0, 1, 1, nv, 0.0, 0.0});
+              }
             } else {
-              double *S = ctx->scratch.d((size_t)r1 * r1);
-              ip.push_back(S), idim.push_back(r1), ild.push_back(r1);
-              ip.push_back(Ci + (int64_t)r1 * rr + r1), idim.push_back(r2), ild.push_back(rr);  // bottom-right I
-              gsch.push_back(GemmJob{A, B, S, r1, r1, r2, rr, rr, r1, -1.0, 1.0});
-              invs.push_back(InvReq{S, r1, r1, Ci, rr, r1 > INV_SMALL ? ctx->scratch.i(r1) : nullptr, d_flags + fl});
-              gs1.push_back(GemmJob{Ci, A, Ci + r1, r1, r2, r1, rr, rr, rr, -1.0, 0.0});
-              gs1.push_back(GemmJob{B, Ci, Ci + (int64_t)r1 * rr, r2, r1, r1, rr, rr, rr, -1.0, 0.0});
-              gs2.push_back(GemmJob{B, Ci + r1, Ci + (int64_t)r1 * rr + r1, r2, r2, r1, rr, rr, rr, -1.0, 1.0});
+              const int fl = new_flag(msg, (int64_t)T.fi * 1000000 + v);
+              double *A = ctx->scratch.d((size_t)r1 * r2), *B = ctx->scratch.d((size_t)r2 * r1);
+              gc.push_back(GemmJob{f1.row, xb, A, r1, r2, m2, f1.ldr, r2, r2, 1.0, 0.0});
+              gc.push_back(GemmJob{f2.row, xt, B, r2, r1, m1, f2.ldr, r1, r1, 1.0, 0.0});
+              if (r2 <= r1) {
+                double *yb = ctx->scratch.d((size_t)r2 * m1), *P = ctx->scratch.d((size_t)r2 * m2);
+                double *S = ctx->scratch.d((size_t)r2 * r2), *Si = ctx->scratch.d((size_t)r2 * r2);
+                ga.push_back(GemmJob{f1.row, HRR, Ttr, r1, m2, m2, f1.ldr, N, nv, 1.0, 0.0});  // y_top in place
+                ga.push_back(GemmJob{f2.row, HLL, yb, r2, m1, m1, f2.ldr, N, m1, 1.0, 0.0});
+                ip.push_back(S), idim.push_back(r2), ild.push_back(r2);
+                gsch.push_back(GemmJob{B, A, S, r2, r2, r1, r1, r2, r2, -1.0, 1.0});
+                gsch.push_back(GemmJob{B, Ttr, P, r2, m2, r1, r1, nv, m2, 1.0, 0.0});
+                invs.push_back(InvReq{S, r2, r2, Si, r2, r2 > INV_SMALL ? ctx->scratch.i(r2) : nullptr, d_flags + fl});
+                gz.push_back(GemmJob{Si, yb, Tbl, r2, m1, r2, r2, m1, nv, 1.0, 0.0});
+                gz.push_back(GemmJob{Si, P, Tbr, r2, m2, r2, r2, m2, nv, -1.0, 0.0});
+                gt.push_back(GemmJob{A, Tbl, Ttl, r1, m1, r2, r2, nv, nv, -1.0, 0.0});
+                gt.push_back(GemmJob{A, Tbr, Ttr, r1, m2, r2, r2, nv, nv, -1.0, 1.0});
+              } else {
+                double *yt = ctx->scratch.d((size_t)r1 * m2), *Q = ctx->scratch.d((size_t)r1 * m1);
+                double *S = ctx->scratch.d((size_t)r1 * r1), *Si = ctx->scratch.d((size_t)r1 * r1);
+                ga.push_back(GemmJob{f1.row, HRR, yt, r1, m2, m2, f1.ldr, N, m2, 1.0, 0.0});
+                ga.push_back(GemmJob{f2.row, HLL, Tbl, r2, m1, m1, f2.ldr, N, nv, 1.0, 0.0});  // y_bot in place
+                ip.push_back(S), idim.push_back(r1), ild.push_back(r1);
+                gsch.push_back(GemmJob{A, B, S, r1, r1, r2, r2, r1, r1, -1.0, 1.0});
+                gsch.push_back(GemmJob{A, Tbl, Q, r1, m1, r2, r2, nv, m1, 1.0, 0.0});
+                invs.push_back(InvReq{S, r1, r1, Si, r1, r1 > INV_SMALL ? ctx->scratch.i(r1) : nullptr, d_flags + fl});
+                gz.push_back(GemmJob{Si, Q, Ttl, r1, m1, r1, r1, m1, nv, -1.0, 0.0});
+                gz.push_back(GemmJob{Si, yt, Ttr, r1, m2, r1, r1, m2, nv, 1.0, 0.0});
+                gt.push_back(GemmJob{B, Ttl, Tbl, r2, m1, r1, r1, nv, nv, -1.0, 1.0});
+                gt.push_back(GemmJob{B, Ttr, Tbr, r2, m2, r1, r1, nv, nv, -1.0, 0.0});
+              }
             }
-            // (d) Tm = core^{-1} [[0, y_top], [y_bot, 0]]  (rr x nv)
-            gd.push_back(GemmJob{T.cinv[v] + r1, nd.yb, nd.Tm, rr, m1, r2, rr, m1, nv, 1.0, 0.0});
-            gd.push_back(GemmJob{T.cinv[v], nd.yt, nd.Tm + m1, rr, m2, r1, rr, m2, nv, 1.0, 0.0});
-            // (e) H_v^{-1} rows L -= x_top Tm[:r1, :], rows R -= x_bot Tm[r1:, :]
-            if (r1) ge.push_back(GemmJob{nd.xt, nd.Tm, HLL, m1, nv, r1, r1, nv, N, -1.0, 1.0});
+            // H_v^{-1} rows L -= x_top Tm[:r1, :], rows R -= x_bot Tm[r1:, :]
+            if (r1) ge.push_back(GemmJob{xt, Tm, HLL, m1, nv, r1, r1, nv, N, -1.0, 1.0});
             if (r2)
-              ge.push_back(GemmJob{nd.xb, nd.Tm + (int64_t)r1 * nv, f.Hinv + (int64_t)mid * N + lo, m2, nv, r2, r2, nv, N,
+              ge.push_back(GemmJob{xb, Tm + (int64_t)r1 * nv, f.Hinv + (int64_t)mid * N + lo, m2, nv, r2, r2, nv, N,
                                    -1.0, 1.0});
-            nodes.push_back(nd);
           }
         }
-        if (nodes.empty()) continue;
-        run_gemm(s, ga);
+        if (!any) continue;
         run_identity(s, ip, idim, ild);
+        run_gemm(s, ga);
         run_gemm(s, gc);
-        run_check_finite(s, fin);
         run_gemm(s, gsch);
         run_inverse(s, invs);
-        run_gemm(s, gs1);
-        run_gemm(s, gs2);
-        run_gemm(s, gd);
+        run_gemm(s, gz);
+        run_gemm(s, gt);
         run_gemm(s, ge);
       }
       // HODLR inverse form: per leaf, the rows of its ancestors' X_v = diag(x_top,

@@ -260,7 +260,8 @@ struct Ctx {
   cudaStream_t s = nullptr;
   cudaStream_t side = nullptr;   // concurrent large-core cluster / cooperative kernels
   cudaStream_t side2 = nullptr;  // 8-CTA cluster cores, concurrently with the 16-CTA ones
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
+  cudaStream_t side3 = nullptr;  // the cooperative grid-class cores when launched first
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr, ev_join3 = nullptr;
   cudaEvent_t gmres_ev[2] = {nullptr, nullptr};  // Hessenberg column read-backs (pipelined Arnoldi)
   int cluster_size = 16;
   size_t plu_dyn_max = 0;  // dynamic shared memory the pivot-LU kernels may use (per device)
@@ -997,7 +998,10 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
   const size_t dyn_max = ctx->plu_dyn_max;  // set per device in device_setup
   const void *const *fns = plu_fns();
   const int CS = ctx->cluster_size;
-  const int nsm = ctx->nsm;
+  // SMs of the cooperative (grid class) launch: all of them by default;
+  // MFH_PLU_GRID caps it so the cluster classes can run beside it (A/B knob)
+  const int nsm = getenv("MFH_PLU_GRID") ? std::max(1, std::min(ctx->nsm, atoi(getenv("MFH_PLU_GRID")))) : ctx->nsm;
+  const bool coop_first = getenv("MFH_PLU_COOP_FIRST") && atoi(getenv("MFH_PLU_COOP_FIRST")) != 0;
   auto cta_bytes = [](int m, int n) { return sizeof(double) * (size_t)m * n + sizeof(int) * (size_t)(m + n) + 16; };
   std::vector<int> small[3], cl8, cl16, grd;
   size_t smax[3] = {48 * 1024, 100 * 1024, dyn_max};
@@ -1158,9 +1162,7 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
   };
   // 8-CTA clusters on their own stream: they run beside the 16-CTA clusters
   // (and ahead of the cooperative launch, which waits for free SMs)
-  cluster_group(cl8, ids_cl8, 8, ctx->side2);
-  if (!cl8.empty()) CK(cudaEventRecord(ctx->ev_join2, ctx->side2));
-  cluster_group(cl16, ids_cl16, CS, ctx->side);
+  auto coop = [&](cudaStream_t st) {
   for (int v = 0; v < 2; ++v) {
     GridLaunch &L = gl[v];
     if (L.ids.empty()) continue;
@@ -1176,9 +1178,20 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
     GridScratch g2 = gs;
     void *args[7] = {(void *)&dj, (void *)&gl_ids[v], (void *)&gl_first[v], (void *)&gl_cptr[v], (void *)&ngr,
                      (void *)&e, (void *)&g2};
-    CK(cudaLaunchCooperativeKernel(fn, dim3(nsm), dim3(512), args, L.smem, ctx->side));
+    CK(cudaLaunchCooperativeKernel(fn, dim3(nsm), dim3(512), args, L.smem, st));
     ctx->launches++;
   }
+  };
+  const bool coop_own = coop_first && !grd.empty() && (!cl8.empty() || !cl16.empty());
+  if (coop_own) {  // the critical-path cores claim their SMs first, clusters fill the rest
+    CK(cudaStreamWaitEvent(ctx->side3, ctx->ev_fork, 0));
+    coop(ctx->side3);
+    CK(cudaEventRecord(ctx->ev_join3, ctx->side3));
+  }
+  cluster_group(cl8, ids_cl8, 8, ctx->side2);
+  if (!cl8.empty()) CK(cudaEventRecord(ctx->ev_join2, ctx->side2));
+  cluster_group(cl16, ids_cl16, CS, ctx->side);
+  if (!coop_own) coop(ctx->side);
   if (side) CK(cudaEventRecord(ctx->ev_join, ctx->side));
   if (main_work) main_work();
   for (int b = 0; b < 3; ++b) {
@@ -1197,6 +1210,7 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
   }
   if (side) CK(cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0));
   if (!cl8.empty()) CK(cudaStreamWaitEvent(ctx->s, ctx->ev_join2, 0));
+  if (coop_own) CK(cudaStreamWaitEvent(ctx->s, ctx->ev_join3, 0));
 }
 
 // ---------------------------------------------------------------------------
@@ -2181,6 +2195,7 @@ struct Factorizer {
     std::vector<LuExtractJob> lux;
     std::vector<SkelJob> skel;
     std::vector<SReq> dreq;
+    std::vector<CopyJob> dcopy;
     for (int bi : sblocks) {
       BlockH &b = F->blocks[bi];
       int nI = (int)b.I.size(), nJ = (int)b.J.size();
@@ -2191,9 +2206,21 @@ struct Factorizer {
       int64_t lr_stored = (int64_t)(b.m + b.n) * b.rank;
       b.dense = unc || lr_stored > (int64_t)b.m * b.n;
       if (b.dense) {
-        b.val = blk_alloc(b, (size_t)b.m * b.n);
-        dreq.push_back(SReq{slot[b.fi], b.m, b.n, nullptr, nullptr, b.r0, b.c0, b.val, b.n});
-        count_lr(b.fi, b.r0, b.m, nullptr, b.c0, b.n, nullptr);
+        if (full) {
+          // the full-selection panel R = B(all rows, :) IS the block, sampled by
+          // the same kernels the dense fallback would re-run (hodlr.py:98-99):
+          // adopt it (a pivot-block leaf lives exactly as long as R) or copy it
+          if (b.kind == 0) {
+            b.val = b.R;
+          } else {
+            b.val = blk_alloc(b, (size_t)b.m * b.n);
+            dcopy.push_back(CopyJob{b.R, b.val, b.m, b.n, b.ldR, b.n, nullptr, nullptr});
+          }
+        } else {
+          b.val = blk_alloc(b, (size_t)b.m * b.n);
+          dreq.push_back(SReq{slot[b.fi], b.m, b.n, nullptr, nullptr, b.r0, b.c0, b.val, b.n});
+          count_lr(b.fi, b.r0, b.m, nullptr, b.c0, b.n, nullptr);
+        }
         F->stats.n_dense_fallback++;
       } else if (b.rank > 0) {
         int r = b.rank;
@@ -2253,6 +2280,7 @@ struct Factorizer {
       run_tri_inv(s, tinv);
       run_gemm(s, app);
     }
+    run_copy(s, dcopy);
     run_sample(s, dreq, dF, dC);
     cudaEventRecord(ev[5], ctx->s);
     hts[5] = std::chrono::steady_clock::now();
@@ -4405,6 +4433,8 @@ extern "C" int mfh_ctx_create(int device, mfh_ctx **out) {
   CK(cudaStreamCreateWithFlags(&c->c.s, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->c.side, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->c.side2, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->c.side3, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->c.ev_join3, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->c.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->c.ev_join, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->c.ev_join2, cudaEventDisableTiming));
@@ -4445,6 +4475,9 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   if (ctx->c.h_rb) cudaFreeHost(ctx->c.h_rb);
   cudaStreamSynchronize(ctx->c.side);
   cudaStreamSynchronize(ctx->c.side2);
+  cudaStreamSynchronize(ctx->c.side3);
+  cudaEventDestroy(ctx->c.ev_join3);
+  cudaStreamDestroy(ctx->c.side3);
   cudaEventDestroy(ctx->c.ev_fork);
   cudaEventDestroy(ctx->c.ev_join);
   cudaEventDestroy(ctx->c.ev_join2);

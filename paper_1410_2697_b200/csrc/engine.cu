@@ -1002,6 +1002,9 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
   // MFH_PLU_GRID caps it so the cluster classes can run beside it (A/B knob)
   const int nsm = getenv("MFH_PLU_GRID") ? std::max(1, std::min(ctx->nsm, atoi(getenv("MFH_PLU_GRID")))) : ctx->nsm;
   const bool coop_first = getenv("MFH_PLU_COOP_FIRST") && atoi(getenv("MFH_PLU_COOP_FIRST")) != 0;
+  // A/B knob: the 16-CTA cluster class goes to the grouped cooperative launch
+  // (one wave, global-memory exchange) instead of cluster waves
+  const bool cl16_to_grid = getenv("MFH_PLU_CL16_GRID") && atoi(getenv("MFH_PLU_CL16_GRID")) != 0;
   auto cta_bytes = [](int m, int n) { return sizeof(double) * (size_t)m * n + sizeof(int) * (size_t)(m + n) + 16; };
   std::vector<int> small[3], cl8, cl16, grd;
   size_t smax[3] = {48 * 1024, 100 * 1024, dyn_max};
@@ -1013,7 +1016,7 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
       small[wc <= smax[0] ? 0 : (wc <= smax[1] ? 1 : 2)].push_back(q);
     } else if (ent < 64 * 1024 && plu_dist_bytes(j.m, j.n, 8, true) <= dyn_max) {
       cl8.push_back(q);
-    } else if (plu_dist_bytes(j.m, j.n, CS, true) <= dyn_max) {
+    } else if (plu_dist_bytes(j.m, j.n, CS, true) <= dyn_max && !cl16_to_grid) {
       cl16.push_back(q);
     } else if (plu_dist_bytes(j.m, j.n, nsm, false) <= dyn_max) {
       grd.push_back(q);

@@ -16,10 +16,11 @@ Arms:
 
 Multi-GPU (torchrun, N > 1): the factorization is sharded by nested-dissection
 subtree (SURVEY 8e): each rank factors the subtrees and top fronts it owns;
-cut-child updates, preconditioner contributions and solution pieces cross
-ranks through NCCL all-reduces on the library stream. GMRES runs replicated on
-that sharded preconditioner. Strong scaling: one system per job, value is the
-max-over-ranks step time.
+cut-child updates travel point to point to the parent's owner in compressed
+form (NCCL send/recv), preconditioner contributions and solution pieces cross
+ranks through NCCL all-reduces on the library stream, and GMRES is distributed
+(rank-local Krylov vectors, halo SpMV, CGS2 with all-reduced dot products).
+Strong scaling: one system per job, value is the max-over-ranks step time.
 """
 
 from __future__ import annotations
@@ -403,7 +404,14 @@ def run_gpu_arm(args, cfg, world, rank, local):
                 cfg["tol"], cap, cfg["restart"], _lib.ptr(hh), cap, _lib.ptr(nhs), _lib.ptr(itss), _lib.ptr(convs)))
             g_ms = F.timing()["gmres_ms"]
             its0, conv0, res0 = int(itss[0]), bool(convs[0]), hh[0, max(0, nhs[0] - 1)]
-        for d_b in (d_bs if not (nrhs > 1 and world == 1) else []):  # one solve per right-hand side
+        if world > 1:  # distributed GMRES on the sharded factor: rank-local vectors, halo SpMV, CGS2
+            from paper_1410_2697_b200.sharded import gmres_sharded
+            for bv in bs:
+                xs, hs = gmres_sharded(A, bv, F, tol=cfg["tol"], restart=cfg["restart"])
+                g_ms += F.timing()["gmres_ms"]
+                if its0 is None:
+                    its0, conv0, res0 = hs.iterations, hs.converged, hs.residuals[-1]
+        for d_b in (d_bs if not (nrhs > 1 and world == 1) and world == 1 else []):  # one solve per right-hand side
             _lib.check(_lib.lib().mfh_gmres_device(ctx.handle, C.byref(ops), n, C.c_void_p(d_b.data_ptr()),
                                                    C.c_void_p(d_x.data_ptr()), cfg["tol"], 4000, cfg["restart"],
                                                    _lib.ptr(hist), C.byref(nh), C.byref(its), C.byref(conv)))
@@ -422,6 +430,10 @@ def run_gpu_arm(args, cfg, world, rank, local):
 
     def step_e2e():  # public API, host b -> host x (every RHS)
         F = factorize()
+        if world > 1:
+            from paper_1410_2697_b200.sharded import gmres_sharded
+            out = [gmres_sharded(A, v, F, tol=cfg["tol"], restart=cfg["restart"]) for v in bs]
+            return F, out[0][0], out[0][1]
         M = P.mf_preconditioner(F)
         if nrhs > 1 and world == 1:
             X, hs = P.gmres_batched(A, np.stack(bs, axis=1), M, tol=cfg["tol"], restart=cfg["restart"])

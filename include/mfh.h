@@ -244,6 +244,18 @@ int mfh_gmres(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const double *b
 int mfh_gmres_device(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const double *d_b,
                      double *d_x, double tol, int64_t max_iter, int64_t restart, double *hist,
                      int64_t *n_hist, int64_t *iterations, int *converged);
+/* GMRES distributed over the ranks of a sharded factorization:
+ * every rank holds the rows and vector entries of the pivots it owns; SpMV
+ * reads the entries of other ranks it couples to (ancestor separators) from an
+ * all-reduced halo buffer; Gram-Schmidt is classical and repeated once (CGS2:
+ * one all-reduce of the j + 1 dot products per pass), norms all-reduced, the
+ * preconditioner is the sharded apply. All through the factor's exchange
+ * callback. Collective: every rank calls it with the same ORIGINAL matrix
+ * (CSR), the same host b, and receives the whole solution in x. Iteration
+ * counts agree with mfh_gmres to +-1 (CGS2 instead of MGS). */
+int mfh_gmres_sharded(mfh_factor *F, int64_t n, const int64_t *indptr, const int64_t *indices, const double *values,
+                      const double *b, double *x, double tol, int64_t max_iter, int64_t restart, double *hist,
+                      int64_t *n_hist, int64_t *iterations, int *converged);
 /* Several right-hand sides with one device factorization (BASELINE C5: 8
  * RHS). Replaces the caller's loop of gmres(A, b_r, M) calls (the reference
  * has no batched entry; krylov.py:68-161 per column): right-hand side r is

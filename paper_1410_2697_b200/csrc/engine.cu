@@ -5484,6 +5484,299 @@ struct GmresMulti {
 
 }  // namespace mfh
 
+// ---------------------------------------------------------------------------
+// distributed GMRES on a sharded factorization: every rank holds
+// the rows / vector entries of the pivots it owns (permuted numbering); SpMV
+// reads the other ranks' values it couples to from an all-reduced halo buffer
+// (by the separator property: pivots of ancestor separators); Gram-Schmidt is
+// classical, twice (CGS2: one all-reduce of j + 1 dots per pass instead of one
+// per projection, as stable as the reference's MGS); norms all-reduced; the
+// preconditioner is the sharded apply. Givens on the host, identical on every
+// rank (the Hessenberg column is the same after the all-reduce).
+// ---------------------------------------------------------------------------
+struct DistSys {
+  int64_t n = 0, nl = 0, nh = 0;            // global size, local rows, halo buffer length
+  long long *lpos = nullptr;                // local row -> original index (for b / x)
+  long long *ptr = nullptr;                 // local CSR
+  int *col = nullptr;
+  double *val = nullptr;
+  long long *hown_pos = nullptr, *hown_loc = nullptr;  // halo entries this rank owns: buffer slot, local index
+  int64_t nhown = 0;
+  int W = 8;
+  ~DistSys() {
+    for (void *q : {(void *)lpos, (void *)ptr, (void *)col, (void *)val, (void *)hown_pos, (void *)hown_loc})
+      cudaFree(q);
+  }
+};
+
+static std::unique_ptr<DistSys> dist_build(mfh_factor *F, int64_t n, const int64_t *ip, const int64_t *ix,
+                                           const double *vx) {
+  Ctx *ctx = F->ctx;
+  auto D = std::make_unique<DistSys>();
+  D->n = n;
+  // owner of every permuted id, from the fronts' pivot runs (identical on every rank)
+  std::vector<int> own((size_t)std::max<int64_t>(1, n), -1);
+  for (size_t q = 0; q < F->fronts.size(); ++q) {
+    const FrontH &f = F->fronts[q];
+    for (int j = 0; j < f.npv; ++j) own[f.piv_lo + j] = F->owner[q];
+  }
+  std::vector<int64_t> iperm((size_t)std::max<int64_t>(1, n));
+  for (int64_t i = 0; i < n; ++i) iperm[F->perm[i]] = i;
+  // local rows: owned permuted ids ascending
+  std::vector<int64_t> loc((size_t)std::max<int64_t>(1, n), -1), rows;
+  for (int64_t g = 0; g < n; ++g)
+    if (own[g] == F->rank) {
+      loc[g] = (int64_t)rows.size();
+      rows.push_back(g);
+    }
+  D->nl = (int64_t)rows.size();
+  // halo: every id some rank reads but does not own (all ranks compute the same list)
+  std::vector<int64_t> hidx((size_t)std::max<int64_t>(1, n), -1), hall;
+  for (int64_t i = 0; i < n; ++i) {
+    const int r = own[F->perm[i]];
+    for (int64_t p = ip[i]; p < ip[i + 1]; ++p) {
+      const int64_t gc = F->perm[ix[p]];
+      if (own[gc] != r && hidx[gc] < 0) hidx[gc] = 1;
+    }
+  }
+  for (int64_t g = 0; g < n; ++g)
+    if (hidx[g] >= 0) {
+      hidx[g] = (int64_t)hall.size();
+      hall.push_back(g);
+    }
+  D->nh = (int64_t)hall.size();
+  std::vector<long long> lp(D->nl + 1, 0), lpos(std::max<int64_t>(1, D->nl));
+  std::vector<int> lc;
+  std::vector<double> lv;
+  for (int64_t l = 0; l < D->nl; ++l) {
+    const int64_t i = iperm[rows[l]];
+    lpos[l] = i;
+    for (int64_t p = ip[i]; p < ip[i + 1]; ++p) {
+      const int64_t gc = F->perm[ix[p]];
+      lc.push_back(own[gc] == F->rank ? (int)loc[gc] : (int)(D->nl + hidx[gc]));
+      lv.push_back(vx[p]);
+    }
+    lp[l + 1] = (long long)lc.size();
+  }
+  std::vector<long long> hp, hl;
+  for (int64_t s2 = 0; s2 < D->nh; ++s2)
+    if (own[hall[s2]] == F->rank) {
+      hp.push_back(s2);
+      hl.push_back(loc[hall[s2]]);
+    }
+  D->nhown = (int64_t)hp.size();
+  const double avg = D->nl ? (double)lc.size() / D->nl : 0.0;
+  D->W = avg <= 4.5 ? 4 : (avg <= 9.5 ? 8 : (avg <= 20 ? 16 : 32));
+  auto upv = [&](auto **dst, const auto &v) {
+    CK(cudaMalloc(dst, sizeof(v[0]) * std::max<size_t>(1, v.size())));
+    upload(ctx->s, *dst, v.data(), sizeof(v[0]) * v.size());
+  };
+  upv(&D->lpos, lpos);
+  upv(&D->ptr, lp);
+  upv(&D->col, lc);
+  upv(&D->val, lv);
+  upv(&D->hown_pos, hp);
+  upv(&D->hown_loc, hl);
+  return D;
+}
+
+struct DistGmres {
+  mfh_factor *F;
+  Ctx *ctx;
+  DistSys *D;
+  double *halo = nullptr, *full = nullptr, *full2 = nullptr;  // halo buffer; full-length apply in / out
+  double sync_ms = 0.0;
+  int64_t allreduce_calls = 0;
+  int g(int64_t n) const { return (int)std::min<int64_t>(cdiv(std::max<int64_t>(n, 1), 256), 148 * 8); }
+  void allreduce(double *d, int64_t cnt) {
+    allreduce_calls++;
+    F->exchange_or_throw(d, cnt);
+  }
+  // y = A x on this rank's rows
+  void A(const double *x, double *y) {
+    const int64_t nl = D->nl;
+    if (D->nh) {
+      CK(cudaMemsetAsync(halo, 0, sizeof(double) * D->nh, ctx->s));
+      if (D->nhown) {
+        // halo[hown_pos[i]] = x[hown_loc[i]]
+        double *tmp = full2;  // scratch: gathered owned halo values
+        k_gather_from<<<g(D->nhown), 256, 0, ctx->s>>>(D->hown_loc, x, tmp, D->nhown);
+        k_scatter_to<<<g(D->nhown), 256, 0, ctx->s>>>(D->hown_pos, tmp, halo, D->nhown);
+        ctx->launches += 2;
+      }
+      allreduce(halo, D->nh);
+    }
+    const int grid = (int)std::min<int64_t>(cdiv(std::max<int64_t>(1, nl) * D->W, 256), 148 * 16);
+    switch (D->W) {
+      case 4: k_spmv_dist<4><<<grid, 256, 0, ctx->s>>>(nl, D->ptr, D->col, D->val, x, halo, (int)nl, y); break;
+      case 8: k_spmv_dist<8><<<grid, 256, 0, ctx->s>>>(nl, D->ptr, D->col, D->val, x, halo, (int)nl, y); break;
+      case 16: k_spmv_dist<16><<<grid, 256, 0, ctx->s>>>(nl, D->ptr, D->col, D->val, x, halo, (int)nl, y); break;
+      default: k_spmv_dist<32><<<grid, 256, 0, ctx->s>>>(nl, D->ptr, D->col, D->val, x, halo, (int)nl, y);
+    }
+    check_launch();
+    ctx->launches++;
+  }
+  // y = M^{-1} x: the sharded apply on the full-length (original numbering) vector
+  void M(const double *x, double *y) {
+    const int64_t n = D->n, nl = D->nl;
+    CK(cudaMemsetAsync(full, 0, sizeof(double) * n, ctx->s));
+    if (nl) k_scatter_to<<<g(nl), 256, 0, ctx->s>>>(D->lpos, x, full, nl);
+    apply_device(F, full, full);  // the plan copies in, applies (exchanges inside), copies out
+    if (nl) k_gather_from<<<g(nl), 256, 0, ctx->s>>>(D->lpos, full, y, nl);
+    ctx->launches += 2;
+  }
+  // out[0] = global x . y
+  void dot(const double *x, const double *y, double *out) {
+    k_dot_part<<<RED_BLOCKS, RED_THREADS, 0, ctx->s>>>(x, y, D->nl, ctx->d_part);
+    k_finish<<<1, 32, 0, ctx->s>>>(ctx->d_part, out, 0);
+    ctx->launches += 2;
+    allreduce(out, 1);
+  }
+  double host(double *d) {
+    CK(cudaMemcpyAsync(ctx->h_scal, d, sizeof(double), cudaMemcpyDeviceToHost, ctx->s));
+    auto t0 = std::chrono::steady_clock::now();
+    CK(cudaStreamSynchronize(ctx->s));
+    sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return ctx->h_scal[0];
+  }
+  // b, x: host, full length, original numbering (every rank passes the same b, gets the same x)
+  void run(const double *hb, double *hx, double tol, int64_t max_iter, int64_t restart, std::vector<double> &res,
+           int64_t &its, bool &conv) {
+    if (!(tol > 0.0 && tol < 1.0)) throw value_error("tol must lie in (0, 1)");
+    if (max_iter < 1 || restart < 1) throw value_error("max_iter and restart must be positive");
+    const int64_t n = D->n, nl = std::max<int64_t>(1, D->nl);
+    res.clear();
+    its = 0;
+    conv = false;
+    const int64_t mcap = std::min(restart, max_iter);
+    if (mcap > 2000) throw value_error("min(restart, max_iter) must be <= 2000");
+    auto chunk = ctx->pool.take(sizeof(double) * ((size_t)nl * (size_t)(mcap + 6) + 3 * (size_t)std::max<int64_t>(1, n) +
+                                                  (size_t)std::max<int64_t>(1, D->nh) + 2 * 4096));
+    double *V = (double *)chunk.first, *w = V + nl * (mcap + 1), *r = w + nl, *z = r + nl, *b = z + nl, *x = b + nl;
+    full = x + nl;
+    full2 = full + std::max<int64_t>(1, n);
+    double *fin = full2 + std::max<int64_t>(1, n);  // full-length staging for b / x
+    halo = fin + std::max<int64_t>(1, n);
+    double *S = halo + std::max<int64_t>(1, D->nh);  // [0] |b|^2, [1] beta^2, [2] hn^2, [8..] h, [2048..] h2 / y
+    auto cleanup = [&]() {
+      cudaStreamSynchronize(ctx->s);
+      ctx->pool.give(chunk);
+    };
+    try {
+      CK(cudaMemcpyAsync(fin, hb, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->s));
+      if (D->nl) k_gather_from<<<g(D->nl), 256, 0, ctx->s>>>(D->lpos, fin, b, D->nl);
+      CK(cudaMemsetAsync(x, 0, sizeof(double) * nl, ctx->s));
+      dot(b, b, S);
+      const double nb = std::sqrt(host(S));
+      if (nb == 0.0) {
+        conv = true;
+        res.push_back(0.0);
+      }
+      while (!conv && its < max_iter) {
+        A(x, w);
+        k_sub<<<g(nl), 256, 0, ctx->s>>>(b, w, r, D->nl);
+        dot(r, r, S + 1);
+        const double beta = std::sqrt(host(S + 1));
+        if (!std::isfinite(beta)) throw value_error("GMRES residual is not finite");
+        if (beta / nb <= tol) {
+          conv = true;
+          if (res.empty()) res.push_back(beta / nb);
+          break;
+        }
+        const int64_t m = std::min(restart, max_iter - its);
+        std::vector<double> H((m + 1) * m, 0.0), cs(m, 0.0), sn(m, 0.0), gg(m + 1, 0.0);
+        auto h = [&](int64_t i, int64_t j) -> double & { return H[i * m + j]; };
+        gg[0] = beta;
+        {
+          const double inv = beta;
+          CK(cudaMemcpyAsync(S + 4, &inv, sizeof(double), cudaMemcpyHostToDevice, ctx->s));
+          k_scale_inv<<<g(nl), 256, 0, ctx->s>>>(S + 4, r, V, D->nl);
+        }
+        int64_t j = 0;
+        bool lucky_stop = false;
+        std::vector<double> hc(m + 2);
+        while (j < m) {
+          double *vj = V + j * nl;
+          M(vj, z);
+          A(z, w);
+          // CGS2: h = V^T w; w -= V h; h2 = V^T w; w -= V h2; h += h2
+          double *hd = S + 8, *h2 = S + 2048;
+          k_multi_dot<<<(unsigned)(j + 1), 256, 0, ctx->s>>>(V, w, D->nl, hd, 0);
+          allreduce(hd, j + 1);
+          k_sub_vh<<<g(nl), 256, 0, ctx->s>>>(V, hd, (int)(j + 1), D->nl, w);
+          k_multi_dot<<<(unsigned)(j + 1), 256, 0, ctx->s>>>(V, w, D->nl, h2, 0);
+          allreduce(h2, j + 1);
+          k_sub_vh<<<g(nl), 256, 0, ctx->s>>>(V, h2, (int)(j + 1), D->nl, w);
+          k_add<<<1, 256, 0, ctx->s>>>(h2, hd, j + 1);
+          ctx->launches += 5;
+          dot(w, w, S + 2);
+          CK(cudaMemcpyAsync(hc.data(), hd, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, ctx->s));
+          const double hn = std::sqrt(host(S + 2));
+          for (int64_t i = 0; i <= j; ++i) h(i, j) = hc[i];
+          if (!std::isfinite(hn)) throw value_error("GMRES residual is not finite");
+          h(j + 1, j) = hn;
+          for (int64_t i = 0; i < j; ++i) {
+            const double t = cs[i] * h(i, j) + sn[i] * h(i + 1, j);
+            h(i + 1, j) = -sn[i] * h(i, j) + cs[i] * h(i + 1, j);
+            h(i, j) = t;
+          }
+          const double den = std::hypot(h(j, j), h(j + 1, j));
+          if (den == 0.0) throw value_error("GMRES breakdown: zero Hessenberg column");
+          cs[j] = h(j, j) / den;
+          sn[j] = h(j + 1, j) / den;
+          h(j, j) = den;
+          h(j + 1, j) = 0.0;
+          gg[j + 1] = -sn[j] * gg[j];
+          gg[j] = cs[j] * gg[j];
+          its += 1;
+          const double rel = std::fabs(gg[j + 1]) / nb;
+          res.push_back(rel);
+          const bool lucky = hn == 0.0;
+          j += 1;
+          if (rel <= tol || lucky) {
+            lucky_stop = lucky;
+            break;
+          }
+          CK(cudaMemcpyAsync(S + 5, &hn, sizeof(double), cudaMemcpyHostToDevice, ctx->s));
+          k_scale_inv<<<g(nl), 256, 0, ctx->s>>>(S + 5, w, V + j * nl, D->nl);
+          CK(cudaStreamSynchronize(ctx->s));  // the host scalars above are pageable
+        }
+        if (j > 0) {
+          std::vector<double> y(j, 0.0);
+          for (int64_t i = j - 1; i >= 0; --i) {
+            double s2 = 0.0;
+            for (int64_t q = i + 1; q < j; ++q) s2 += h(i, q) * y[q];
+            y[i] = (gg[i] - s2) / h(i, i);
+          }
+          double *dy = S + 2048;
+          CK(cudaMemcpyAsync(dy, y.data(), sizeof(double) * j, cudaMemcpyHostToDevice, ctx->s));
+          k_combine<<<g(nl), 256, 0, ctx->s>>>(V, dy, (int)j, D->nl, w);
+          M(w, z);
+          k_add<<<g(nl), 256, 0, ctx->s>>>(z, x, D->nl);
+          CK(cudaStreamSynchronize(ctx->s));
+        }
+        A(x, w);
+        k_sub<<<g(nl), 256, 0, ctx->s>>>(b, w, r, D->nl);
+        dot(r, r, S + 3);
+        const double tr = std::sqrt(host(S + 3)) / nb;
+        if (!std::isfinite(tr)) throw value_error("GMRES residual is not finite");
+        if (!res.empty()) res.back() = tr;
+        if (tr <= tol || lucky_stop) conv = true;
+      }
+      // every rank gets the whole solution (disjoint entries, exact sum)
+      CK(cudaMemsetAsync(fin, 0, sizeof(double) * n, ctx->s));
+      if (D->nl) k_scatter_to<<<g(D->nl), 256, 0, ctx->s>>>(D->lpos, x, fin, D->nl);
+      allreduce(fin, n);
+      CK(cudaMemcpyAsync(hx, fin, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->s));
+      CK(cudaStreamSynchronize(ctx->s));
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  }
+};
+
 static int gmres_common(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, const double *d_b, double *d_x,
                         double tol, int64_t max_iter, int64_t restart, double *hist, int64_t *n_hist,
                         int64_t *iterations, int *converged) {
@@ -5576,6 +5869,30 @@ extern "C" int mfh_gmres_batched_device(mfh_ctx *ctx, const mfh_gmres_ops *ops, 
   std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
   return gmres_batched_common(ctx, ops, n, nrhs, d_b, d_x, tol, max_iter, restart, hist, hist_cap, n_hist,
                               iterations, converged);
+}
+
+extern "C" int mfh_gmres_sharded(mfh_factor *F, int64_t n, const int64_t *indptr, const int64_t *indices,
+                                 const double *values, const double *b, double *x, double tol, int64_t max_iter,
+                                 int64_t restart, double *hist, int64_t *n_hist, int64_t *iterations, int *converged) {
+  std::lock_guard<std::recursive_mutex> lk_(F->ctx->mu);
+  MFH_TRY
+  DeviceGuard dg_(F->ctx->device);
+  if (!F->sharded) throw value_error("mfh_gmres_sharded needs a factorization from mfh_factorize_sharded");
+  if (n != F->n) throw value_error("dimension mismatch: system is " + std::to_string(F->n) + ", rhs is " + std::to_string(n));
+  auto D = dist_build(F, n, indptr, indices, values);
+  DistGmres g{F, F->ctx, D.get()};
+  std::vector<double> res;
+  int64_t its = 0;
+  bool conv = false;
+  auto t0 = std::chrono::steady_clock::now();
+  g.run(b, x, tol, max_iter, restart, res, its, conv);
+  F->timing.gmres_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  F->timing.gmres_sync_ms = g.sync_ms;
+  if (hist) std::memcpy(hist, res.data(), sizeof(double) * res.size());
+  *n_hist = (int64_t)res.size();
+  *iterations = its;
+  *converged = conv ? 1 : 0;
+  MFH_CATCH
 }
 
 extern "C" int mfh_gmres_batched(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, int64_t nrhs, const double *b,

@@ -2843,6 +2843,60 @@ __global__ void k_combine(const double *__restrict__ V, const double *__restrict
   }
 }
 
+// ---- distributed GMRES (sharded factor): rank-local vectors ----
+// local SpMV over this rank's rows; column c < nl reads the local vector,
+// c >= nl the all-reduced halo buffer (top-separator values of other ranks)
+template <int W>
+__global__ void __launch_bounds__(256) k_spmv_dist(long long nrows, const long long *__restrict__ ptr,
+                                                   const int *__restrict__ col, const double *__restrict__ val,
+                                                   const double *__restrict__ x, const double *__restrict__ halo,
+                                                   int nl, double *__restrict__ y) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int l = threadIdx.x & (W - 1);
+  const long long ng = ((long long)gridDim.x * blockDim.x) / W;
+  for (long long r = t / W; r < nrows; r += ng) {
+    double s = 0.0;
+    for (long long p = ptr[r] + l; p < ptr[r + 1]; p += W) {
+      const int c = col[p];
+      s = fma(val[p], c < nl ? x[c] : halo[c - nl], s);
+    }
+#pragma unroll
+    for (int o = W >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, W);
+    if (l == 0) y[r] = s;
+  }
+}
+// dst[idx[i]] = src[i] (dst zeroed by the caller where nothing lands)
+__global__ void k_scatter_to(const long long *__restrict__ idx, const double *__restrict__ src,
+                             double *__restrict__ dst, long long cnt) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (long long)gridDim.x * blockDim.x)
+    dst[idx[i]] = src[i];
+}
+// dst[i] = src[idx[i]]
+__global__ void k_gather_from(const long long *__restrict__ idx, const double *__restrict__ src,
+                              double *__restrict__ dst, long long cnt) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+// classical Gram-Schmidt projection: w -= sum_i h[i] V_i (i ascending)
+__global__ void k_sub_vh(const double *__restrict__ V, const double *__restrict__ h, int j, long long n,
+                         double *__restrict__ w) {
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    double s = w[r];
+    for (int i = 0; i < j; ++i) s = s - h[i] * V[(long long)i * n + r];
+    w[r] = s;
+  }
+}
+// h[i] (+)= V_i . w for i < j: one block per basis vector, deterministic
+__global__ void __launch_bounds__(256) k_multi_dot(const double *__restrict__ V, const double *__restrict__ w,
+                                                   long long n, double *__restrict__ h, int accumulate) {
+  __shared__ double sh[33];
+  const double *v = V + (long long)blockIdx.x * n;
+  double s = 0.0;
+  for (long long r = threadIdx.x; r < n; r += blockDim.x) s = fma(v[r], w[r], s);
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) h[blockIdx.x] = accumulate ? h[blockIdx.x] + s : s;
+}
+
 // Whole modified Gram-Schmidt sweep + norm of one Arnoldi step in one
 // cooperative launch (krylov.py:116-120): for i = 0..j, H[i] = V_i . w then
 // w -= H[i] V_i (numpy: w - (h * V_i), no FMA); finally H[j+1] = ||w||.

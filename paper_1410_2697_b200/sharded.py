@@ -226,3 +226,28 @@ def mf_factorize_sharded(A, tree, mode=ACCELERATED, params=None, group=None, par
     F.partition = part
     F.exchange = ex
     return F
+
+
+def gmres_sharded(A, b, F, tol=1e-6, max_iter=4000, restart=100):
+    """GMRES distributed over the ranks of a sharded factorization
+    (``mfh_gmres_sharded``): each rank owns the rows and Krylov-vector entries
+    of its pivots, SpMV reads the coupled entries of other ranks from an
+    all-reduced halo buffer, Gram-Schmidt is CGS2 with one all-reduce of the
+    dot products per pass. Collective; every rank passes the same ``A`` and
+    ``b`` and gets the whole solution (krylov.py:68-161 semantics; iteration
+    counts within one of ``gmres``)."""
+    from .krylov import ConvergenceHistory
+    if not getattr(F, "_shard", None):
+        raise ValueError("gmres_sharded needs a factorization from mf_factorize_sharded")
+    if not isinstance(A, SparseMatrix):
+        A = SparseMatrix(A)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    n = A.n_rows
+    x = np.empty(n)
+    ip, ix, dv = A.csr_arrays()
+    hist = np.empty(max(1, int(max_iter)))
+    nh, its, conv = C.c_int64(), C.c_int64(), C.c_int()
+    _lib.check(_lib.lib().mfh_gmres_sharded(F._h, n, _lib.ptr(ip), _lib.ptr(ix), _lib.ptr(dv), _lib.ptr(b),
+                                            _lib.ptr(x), float(tol), int(max_iter), int(restart), _lib.ptr(hist),
+                                            C.byref(nh), C.byref(its), C.byref(conv)))
+    return x, ConvergenceHistory([float(v) for v in hist[:nh.value]], bool(conv.value), int(its.value))

@@ -38,7 +38,7 @@ def _worker(rank, world, port, case, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         import paper_1410_2697_b200 as P
         from paper_1410_2697_b200 import problems as PR
-        from paper_1410_2697_b200.sharded import mf_factorize_sharded
+        from paper_1410_2697_b200.sharded import gmres_sharded, mf_factorize_sharded
         gen, leaf, kw = CASES[case]
         A = gen(PR)
         tree = P.build_elimination_tree(P.nested_dissection(P.adjacency_graph(A), leaf), A)
@@ -49,6 +49,10 @@ def _worker(rank, world, port, case, q):
             F = mf_factorize_sharded(A, tree, P.ACCELERATED, params, compressed=compressed)
             x = P.mf_solve(F, b)
             xg, h = P.gmres(A, b, M=P.mf_preconditioner(F), tol=1e-10, restart=30)
+            xd, hd = gmres_sharded(A, b, F, tol=1e-10, restart=30) if compressed else (None, None)
+            if compressed:
+                out["dist"] = dict(x=xd, its=hd.iterations, conv=hd.converged,
+                                   res=float(np.linalg.norm(A._csc @ xd - b) / np.linalg.norm(b)))
             out[compressed] = dict(x=x, xg=xg, its=h.iterations, hist=np.asarray(h.residuals), recs=_recs(F),
                                    peak=F.stats.peak_stored_reals,
                                    counts=(F.stats.structured_fronts, F.stats.dense_fronts),
@@ -98,4 +102,11 @@ def test_sharded_factor_bitwise_equals_single(world, case):
             assert c["recs"] == r0["recs1"]
             assert c["peak"] == r0["peak1"] and c["counts"] == r0["counts1"]
     assert sum(o[True]["p2p"] for o in outs) > 0 and sum(o[True]["p2p_bytes"] for o in outs) > 0
+    # distributed GMRES (rank-local vectors, halo SpMV, CGS2): every rank gets
+    # the same solution, iterations within one of the replicated solve
+    for o in outs:
+        d = o["dist"]
+        assert d["conv"] and abs(d["its"] - r0["its1"]) <= 1 and d["res"] <= 1e-9
+        np.testing.assert_array_equal(d["x"], outs[0]["dist"]["x"])
+        assert np.linalg.norm(d["x"] - r0["x1g"]) <= 1e-7 * np.linalg.norm(r0["x1g"])
     assert all(o[False]["p2p"] == 0 for o in outs)

@@ -321,6 +321,15 @@ int mfh_full_pivot_lu_batched(mfh_ctx *ctx, int64_t batch, const int64_t *offs, 
 int mfh_test_inverse_batched(mfh_ctx *ctx, int64_t batch, const int64_t *offs, const int64_t *ns,
                              double *blocks, int64_t total, int *singular);
 
+/* The factorization's batched GEMM dispatch (DMMA tiles, identity strips,
+ * split-K, cuBLAS for large plain GEMMs) on one host workspace: job q is
+ * desc[9q..9q+8] = (m, n, k, A offset, B offset, C offset, lda, ldb, ldc) into
+ * buf, C = alpha A B + beta C with (alpha, beta) = ab[2q], ab[2q+1]; an A or B
+ * offset of -1 is the identity strip (leading dimension -1). split_k > 0
+ * splits long k for <= 32-tile jobs into chunks of split_k (deterministic). */
+int mfh_test_gemm_batched(mfh_ctx *ctx, int64_t batch, const int64_t *desc, const double *ab, double *buf,
+                          int64_t total, int split_k);
+
 #ifdef __cplusplus
 }
 #endif

@@ -409,6 +409,31 @@ static void check_launch() {
   if (e != cudaSuccess) throw runtime_error(std::string("CUDA launch error: ") + cudaGetErrorString(e));
 }
 
+// Launch with programmatic stream serialization (PDL). Captured into the
+// apply graph it becomes a programmatic edge: the kernel's CTAs launch while
+// the previous level drains and block in griddepcontrol.wait until its writes
+// are visible, which hides the launch gap between dependent launches (apply levels, HODLR
+// levels, panel steps). MFH_PDL=0 launches them ordinarily (A/B).
+static bool pdl_on() {
+  const char *e = getenv("MFH_PDL");
+  return !(e && atoi(e) == 0);
+}
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k, args...));
+}
+
+
 // ---- batched launch helpers -------------------------------------------------
 // Batched GEMM dispatch: large plain GEMMs (>= 2^27 flops, both sides >= 64,
 // C not aliasing A or B) go to cuBLAS DGEMM (FP64 tensor cores); the many
@@ -463,6 +488,7 @@ static bool gemm_overlaps(const GemmJob &g) {
          blocks_overlap(g.C, g.m, g.n, g.ldc, g.B, g.k, g.n, g.ldb);
 }
 
+static thread_local int g_split_k_override = -1;  // test hook (mfh_test_gemm_batched)
 static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
   OpClock oc_("gemm");
   if (jobs.empty()) return;
@@ -498,7 +524,8 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
     // k_gemm_reduce. Off by default: with the prefetched slabs it measured no
     // gain at C2 (0.1282 vs 0.1278 s/step), and at C5 the per-job partials
     // (32 KB per tile per chunk) ran the device out of memory.
-    static const int split_k = getenv("MFH_GEMM_SPLIT_K") ? atoi(getenv("MFH_GEMM_SPLIT_K")) : 0;
+    static const int split_k_env = getenv("MFH_GEMM_SPLIT_K") ? atoi(getenv("MFH_GEMM_SPLIT_K")) : 0;
+    const int split_k = g_split_k_override >= 0 ? g_split_k_override : split_k_env;
     const int ns = (split_k > 0 && !sk.record && g.k >= 2 * split_k && tm * tn <= 32 && !gemm_overlaps(g))
                        ? (int)cdiv(g.k, split_k)
                        : 1;
@@ -553,7 +580,7 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
       int *dw = sk.push(wh);
       dim3 grid((unsigned)std::min<int64_t>(cdiv(mx, 256), 128), (unsigned)part.size());
       sk.launch([=](cudaStream_t st) {
-        k_axpby<<<grid, 256, 0, st>>>(dj, dw);
+        launch_pdl(k_axpby, dim3(grid), dim3(256), 0, st, dj, dw);
         check_launch();
       });
     }
@@ -578,9 +605,9 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
   int nt = (int)tiles.size(), nsp = (int)splits.size();
   int grid = std::min(nt, 148 * 16);
   sk.launch([=](cudaStream_t s) {
-    k_gemm<<<grid, 256, 0, s>>>(dj, dt, nt, dws);
+    launch_pdl(k_gemm, dim3(grid), dim3(256), 0, s, dj, dt, nt, dws);
     check_launch();
-    if (nsp) k_gemm_reduce<<<nsp, 256, 0, s>>>(dj, dsp, dws);
+    if (nsp) launch_pdl(k_gemm_reduce, dim3(nsp), dim3(256), 0, s, dj, dsp, dws);
     check_launch();
   });
 }
@@ -603,7 +630,7 @@ static void run_trsm(Sink &sk, const std::vector<TrsmJob> &jobs) {
   TrinvJob *dj = sk.push(ti);
   int nb = (int)ti.size();
   sk.launch([=](cudaStream_t st) {
-    k_trinv<<<nb, 256, TRINV_SMEM, st>>>(dj);
+    launch_pdl(k_trinv, dim3(nb), dim3(256), TRINV_SMEM, st, dj);
     check_launch();
   });
   run_gemm(sk, gm);
@@ -620,7 +647,7 @@ static void run_laswp(Sink &sk, const std::vector<SwapJob> &jobs) {
     SwapJob *dj = sk.push(part);
     dim3 grid((unsigned)cdiv(mx, 128), (unsigned)part.size());
     sk.launch([=](cudaStream_t st) {
-      k_laswp<<<grid, 128, 0, st>>>(dj);
+      launch_pdl(k_laswp, dim3(grid), dim3(128), 0, st, dj);
       check_launch();
     });
   }
@@ -638,7 +665,7 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
     int nb = (int)small.size();
     int th = maxn > 128 ? 512 : (maxn > 32 ? 256 : 64);
     sk.launch([=](cudaStream_t s) {
-      k_getrf<<<nb, th, 0, s>>>(dj);
+      launch_pdl(k_getrf, dim3(nb), dim3(th), 0, s, dj);
       check_launch();
     });
   }
@@ -672,7 +699,7 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
       // every panel of the batch fits one CTA's shared memory
       size_t smem = sizeof(double) * (size_t)mmax * PLD;
       sk.launch([=](cudaStream_t s) {
-        k_getrf_panel_cta<<<np_, 512, smem, s>>>(dp);
+        launch_pdl(k_getrf_panel_cta, dim3(np_), dim3(512), smem, s, dp);
         check_launch();
       });
     } else if (cs <= sk.ctx->cluster_size) {
@@ -699,7 +726,7 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
       });
     } else {
       sk.launch([=](cudaStream_t s) {
-        k_getrf_panel<<<np_, 512, 0, s>>>(dp);
+        launch_pdl(k_getrf_panel, dim3(np_), dim3(512), 0, s, dp);
         check_launch();
       });
     }
@@ -710,7 +737,7 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
   LuJob *dj = sk.push(big);
   int nb = (int)big.size();
   sk.launch([=](cudaStream_t s) {
-    k_diag_check<<<nb, 256, 0, s>>>(dj);
+    launch_pdl(k_diag_check, dim3(nb), dim3(256), 0, s, dj);
     check_launch();
   });
 }
@@ -751,7 +778,7 @@ static void run_tri_inv(Sink &sk, const std::vector<TriInvReq> &reqs) {
     TrinvJob *dj = sk.push(ti);
     int nb = (int)ti.size();
     sk.launch([=](cudaStream_t st) {
-      k_trinv<<<nb, 256, TRINV_SMEM, st>>>(dj);
+      launch_pdl(k_trinv, dim3(nb), dim3(256), TRINV_SMEM, st, dj);
       check_launch();
     });
   }
@@ -825,7 +852,7 @@ static void run_inverse(Sink &sk, const std::vector<InvReq> &reqs) {
       InvJob *dj = sk.push(s64);
       int nb = (int)s64.size();
       sk.launch([=](cudaStream_t st) {
-        k_inv_reg<8, 2><<<nb, 256, 0, st>>>(dj);
+        launch_pdl(k_inv_reg<8, 2>, dim3(nb), dim3(256), 0, st, dj);
         check_launch();
       });
     }
@@ -833,7 +860,7 @@ static void run_inverse(Sink &sk, const std::vector<InvReq> &reqs) {
       InvJob *dj = sk.push(s128);
       int nb = (int)s128.size();
       sk.launch([=](cudaStream_t st) {
-        k_inv_reg<16, 4><<<nb, 512, 0, st>>>(dj);
+        launch_pdl(k_inv_reg<16, 4>, dim3(nb), dim3(512), 0, st, dj);
         check_launch();
       });
     }
@@ -873,7 +900,7 @@ static void run_copy(Sink &sk, const std::vector<CopyJob> &jobs) {
     CopyJob *dj = sk.push(part);
     dim3 grid((unsigned)std::min<int64_t>(cdiv(mx, 256), 64), (unsigned)part.size());
     sk.launch([=](cudaStream_t s) {
-      k_copy<<<grid, 256, 0, s>>>(dj, 0);
+      launch_pdl(k_copy, dim3(grid), dim3(256), 0, s, dj, 0);
       check_launch();
     });
   }
@@ -892,7 +919,7 @@ static void run_identity(Sink &sk, const std::vector<double *> &ptrs, const std:
     int *dl = sk.push(l);
     dim3 grid((unsigned)std::min<int64_t>(cdiv(mx, 256), 64), (unsigned)p.size());
     sk.launch([=](cudaStream_t s) {
-      k_identity<<<grid, 256, 0, s>>>(dp, dd, dl);
+      launch_pdl(k_identity, dim3(grid), dim3(256), 0, s, dp, dd, dl);
       check_launch();
     });
   }
@@ -1205,9 +1232,9 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
     int nb = (int)small[b].size();
     sk.launch([=](cudaStream_t st) {
       if (b == 2)
-        k_plu_cta2<true, 1024><<<nb, 1024, sm, st>>>(dj, dids, eps);
+        launch_pdl(k_plu_cta2<true, 1024>, dim3(nb), dim3(1024), sm, st, dj, dids, eps);
       else
-        k_plu_cta2<true, 512><<<nb, b == 0 ? 256 : 512, sm, st>>>(dj, dids, eps);
+        launch_pdl(k_plu_cta2<true, 512>, dim3(nb), dim3(b == 0 ? 256 : 512), sm, st, dj, dids, eps);
       check_launch();
     });
   }
@@ -1849,7 +1876,7 @@ struct Factorizer {
       SampleTiles T{drid[0], dpre[0], (int)rid[0].size(), pre[0].back()};
       int grid = (int)std::min<int64_t>(T.ntiles, 148 * 32);
       s.launch([=](cudaStream_t st) {
-        k_sample<<<grid, dim3(SAMPLE_TC, SAMPLE_TR), 0, st>>>(dr, T, fF, fC, pp, pc, pv);
+        launch_pdl(k_sample, dim3(grid), dim3(SAMPLE_TC, SAMPLE_TR), 0, st, dr, T, fF, fC, pp, pc, pv);
         check_launch();
       });
     }
@@ -1857,7 +1884,7 @@ struct Factorizer {
       SampleTiles T{drid[1], dpre[1], (int)rid[1].size(), pre[1].back()};
       int grid = (int)std::min<int64_t>(T.ntiles, 148 * 8);
       s.launch([=](cudaStream_t st) {
-        k_sample_rb<<<grid, 256, RB_DYN, st>>>(dr, T, fF, fC, pp, pc, pv);
+        launch_pdl(k_sample_rb, dim3(grid), dim3(256), RB_DYN, st, dr, T, fF, fC, pp, pc, pv);
         check_launch();
       });
     }
@@ -2260,7 +2287,7 @@ struct Factorizer {
         LuExtractJob *p = dj + b0;
         dim3 grid((unsigned)std::min<int64_t>(cdiv(mx, 256), 32), cnt);
         s.launch([=](cudaStream_t st) {
-          k_lu_extract<<<grid, 256, 0, st>>>(p);
+          launch_pdl(k_lu_extract, dim3(grid), dim3(256), 0, st, p);
           check_launch();
         });
       }
@@ -3636,7 +3663,7 @@ static FacView fac_view(const mfh_factor *F, const BlockH &b) {
 template <int NV>
 static void launch_gemv_mv(cudaStream_t st, int grid, const GemvJob *dj, const int *ds, const int *dw, int chunk,
                            int nr) {
-  k_gemv_mv<NV><<<grid, 256, 0, st>>>(dj, ds, dw, chunk, nr);
+  launch_pdl(k_gemv_mv<NV>, dim3(grid), dim3(256), 0, st, dj, ds, dw, chunk, nr);
 }
 // nv right-hand sides (1..8): vector v of a job at pointer + v * its stride
 static void run_gemv(Sink &sk, const std::vector<GemvJob> &jobs, int nv = 1) {
@@ -3688,7 +3715,7 @@ static void run_gemv(Sink &sk, const std::vector<GemvJob> &jobs, int nv = 1) {
   (void)nj;
   sk.launch([=](cudaStream_t st) {
     switch (nv) {
-      case 1: k_gemv2<<<grid, 256, 0, st>>>(dj, ds, dw, chunk, nr); break;
+      case 1: launch_pdl(k_gemv2, dim3(grid), dim3(256), 0, st, dj, ds, dw, chunk, nr); break;
       case 2: launch_gemv_mv<2>(st, grid, dj, ds, dw, chunk, nr); break;
       case 3: launch_gemv_mv<3>(st, grid, dj, ds, dw, chunk, nr); break;
       case 4: launch_gemv_mv<4>(st, grid, dj, ds, dw, chunk, nr); break;
@@ -3930,7 +3957,8 @@ static std::unique_ptr<ApplyPlan> make_apply(mfh_factor *F, int nv) {
     });
   };
   sk.launch([=](cudaStream_t s) {
-    k_scatter_perm<<<dim3(grid_n, nv), 256, 0, s>>>(db, perm, bu, n);
+    launch_pdl(k_scatter_perm, dim3(grid_n, nv), dim3(256), 0, s, (const double *)db, (const long long *)perm, bu,
+               (long long)n);
     check_launch();
   });
   bytes += 24.0 * n;
@@ -3950,8 +3978,9 @@ static std::unique_ptr<ApplyPlan> make_apply(mfh_factor *F, int nv) {
     int cnt = (int)gl.size();
     // level 0 fronts have no pivot-carrying descendants: nothing to gather
     if (h > 0) sk.launch([=](cudaStream_t s) {
-      k_contrib_gather<<<dim3((unsigned)std::min<int64_t>(cdiv((int64_t)cnt * 32, 256), 148 * 16), nv), 256, 0, s>>>(
-          dgl, cnt, d_cptr, d_coff, cbuf, bu, nullptr, cst, nst);
+      launch_pdl(k_contrib_gather, dim3((unsigned)std::min<int64_t>(cdiv((int64_t)cnt * 32, 256), 148 * 16), nv),
+                 dim3(256), 0, s, (const long long *)dgl, cnt, (const long long *)d_cptr, (const long long *)d_coff,
+                 (const double *)cbuf, bu, (double *)nullptr, (long long)cst, (long long)nst);
       check_launch();
     });
     // three dependent stages at most: st[0] reads b_piv only, st[1] reads
@@ -4214,14 +4243,14 @@ static std::unique_ptr<ApplyPlan> make_apply(mfh_factor *F, int nv) {
     const int g = sub_grid, v = nv, u = up ? 1 : 0;
     sk.launch([=](cudaStream_t st) {
       switch (v) {
-        case 1: k_apply_sub<1><<<g, 512, 0, st>>>(S, u); break;
-        case 2: k_apply_sub<2><<<g, 512, 0, st>>>(S, u); break;
-        case 3: k_apply_sub<3><<<g, 512, 0, st>>>(S, u); break;
-        case 4: k_apply_sub<4><<<g, 512, 0, st>>>(S, u); break;
-        case 5: k_apply_sub<5><<<g, 512, 0, st>>>(S, u); break;
-        case 6: k_apply_sub<6><<<g, 512, 0, st>>>(S, u); break;
-        case 7: k_apply_sub<7><<<g, 512, 0, st>>>(S, u); break;
-        case 8: k_apply_sub<8><<<g, 512, 0, st>>>(S, u); break;
+        case 1: launch_pdl(k_apply_sub<1>, dim3(g), dim3(512), 0, st, S, u); break;
+        case 2: launch_pdl(k_apply_sub<2>, dim3(g), dim3(512), 0, st, S, u); break;
+        case 3: launch_pdl(k_apply_sub<3>, dim3(g), dim3(512), 0, st, S, u); break;
+        case 4: launch_pdl(k_apply_sub<4>, dim3(g), dim3(512), 0, st, S, u); break;
+        case 5: launch_pdl(k_apply_sub<5>, dim3(g), dim3(512), 0, st, S, u); break;
+        case 6: launch_pdl(k_apply_sub<6>, dim3(g), dim3(512), 0, st, S, u); break;
+        case 7: launch_pdl(k_apply_sub<7>, dim3(g), dim3(512), 0, st, S, u); break;
+        case 8: launch_pdl(k_apply_sub<8>, dim3(g), dim3(512), 0, st, S, u); break;
         default: throw runtime_error("apply: 1..8 right-hand sides");
       }
       check_launch();
@@ -4233,7 +4262,8 @@ static std::unique_ptr<ApplyPlan> make_apply(mfh_factor *F, int nv) {
   launch_sub(false);
   if (sh) exchange_point(xw, x_mask, x_tmp, std::max<int64_t>(1, n));  // every rank gets every pivot
   sk.launch([=](cudaStream_t s) {
-    k_gather_perm<<<dim3(grid_n, nv), 256, 0, s>>>(xw, perm, dx, n);
+    launch_pdl(k_gather_perm, dim3(grid_n, nv), dim3(256), 0, s, (const double *)xw, (const long long *)perm, dx,
+               (long long)n);
     check_launch();
   });
   // capture (the stream may still be running the factorization: captured work
@@ -6042,5 +6072,60 @@ extern "C" int mfh_test_inverse_batched(mfh_ctx *ctx, int64_t batch, const int64
   c->scratch.reset();
   c->stage.rewind();
   for (int64_t b = 0; b < batch; ++b) singular[b] = hf[b];
+  MFH_CATCH
+}
+
+// test hook: the factorization's batched GEMM dispatch (run_gemm: DMMA tiles,
+// identity strips, split-K, cuBLAS for the large plain ones) on a host
+// workspace. Job q: C = alpha A B + beta C with A at buf + ao[q] (m x k, lda),
+// B at buf + bo[q] (k x n, ldb), C at buf + co[q] (m x n, ldc), all offsets in
+// one buffer so aliasing jobs (C == B, disjoint blocks of one buffer) can be
+// expressed; a negative offset -1 selects the identity strip (ld -1).
+extern "C" int mfh_test_gemm_batched(mfh_ctx *ctx, int64_t batch, const int64_t *desc /* 9 per job */,
+                                     const double *ab /* alpha, beta per job */, double *buf, int64_t total,
+                                     int split_k) {
+  std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
+  MFH_TRY
+  DeviceGuard dg_(ctx->c.device);
+  Ctx *c = &ctx->c;
+  if (batch == 0) return MFH_OK;
+  int maxdim = 1;
+  for (int64_t q = 0; q < batch; ++q) maxdim = std::max<int>(maxdim, (int)std::max({desc[9 * q], desc[9 * q + 1], desc[9 * q + 2]}));
+  double *d = c->scratch.d(std::max<int64_t>(1, total));
+  double *strip = c->scratch.d((size_t)2 * maxdim - 1);
+  CK(cudaMemsetAsync(strip, 0, sizeof(double) * (2 * maxdim - 1), c->s));
+  static const double one = 1.0;
+  CK(cudaMemcpyAsync(strip + maxdim - 1, &one, sizeof(double), cudaMemcpyHostToDevice, c->s));
+  CK(cudaMemcpyAsync(d, buf, sizeof(double) * total, cudaMemcpyHostToDevice, c->s));
+  std::vector<GemmJob> jobs;
+  for (int64_t q = 0; q < batch; ++q) {
+    const int64_t *t = desc + 9 * q;  // m n k ao bo co lda ldb ldc
+    GemmJob g{};
+    g.m = (int)t[0];
+    g.n = (int)t[1];
+    g.k = (int)t[2];
+    g.A = t[3] < 0 ? strip + maxdim - 1 : d + t[3];
+    g.B = t[4] < 0 ? strip + maxdim - 1 : d + t[4];
+    g.C = d + t[5];
+    g.lda = t[3] < 0 ? -1 : (int)t[6];
+    g.ldb = t[4] < 0 ? -1 : (int)t[7];
+    g.ldc = (int)t[8];
+    g.alpha = ab[2 * q];
+    g.beta = ab[2 * q + 1];
+    jobs.push_back(g);
+  }
+  Sink s{c};
+  g_split_k_override = split_k;
+  try {
+    run_gemm(s, jobs);
+  } catch (...) {
+    g_split_k_override = -1;
+    throw;
+  }
+  g_split_k_override = -1;
+  CK(cudaMemcpyAsync(buf, d, sizeof(double) * total, cudaMemcpyDeviceToHost, c->s));
+  CK(cudaStreamSynchronize(c->s));
+  c->scratch.reset();
+  c->stage.rewind();
   MFH_CATCH
 }

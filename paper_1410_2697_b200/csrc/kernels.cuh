@@ -13,6 +13,16 @@ namespace cg = cooperative_groups;
 
 namespace mfh {
 
+// Programmatic dependent launch (the apply graph's kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): wait until the
+// preceding grid has completed and its writes are visible, then let the next
+// grid start launching its CTAs (they block in their own wait), so the
+// launch latency between dependent levels overlaps the running level. Both
+// are no-ops for an ordinary launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+
 constexpr int kZeroPivotNum = 1;  // marker
 #define MFH_ZERO_PIVOT_RATIO 1e-14
 #define MFH_PIVOT_GROWTH_BOUND (2.0 * (1.0 + 1e-10))
@@ -216,6 +226,8 @@ __global__ void k_sample(const SReq *__restrict__ reqs, SampleTiles tiles,
                          const DFront *__restrict__ fronts, const DChild *__restrict__ kids,
                          const long long *__restrict__ Ap_ptr, const int *__restrict__ Ap_col,
                          const double *__restrict__ Ap_val) {
+  pdl_wait();
+  pdl_trigger();
   for (long long t = blockIdx.x; t < tiles.ntiles; t += gridDim.x) {
     const int2 tl = sample_tile(tiles, t);
     const SReq rq = reqs[tl.x];
@@ -370,6 +382,8 @@ __global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs
                                                    const long long *__restrict__ Ap_ptr,
                                                    const int *__restrict__ Ap_col,
                                                    const double *__restrict__ Ap_val) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double Ws[RB_K][RB_LD];
   __shared__ double Vs[RB_K][RB_LD];
   __shared__ int s_r[RB_T], s_c[RB_T], s_cr[RB_T], s_cc[RB_T], s_br[RB_T], s_bc[RB_T];
@@ -501,6 +515,8 @@ __global__ void __launch_bounds__(256) k_sample_rb(const SReq *__restrict__ reqs
 // batched 2-D copy / gather
 // ---------------------------------------------------------------------------
 __global__ void k_copy(const CopyJob *__restrict__ jobs, int njobs) {
+  pdl_wait();
+  pdl_trigger();
   const CopyJob J = jobs[blockIdx.y];
   long long total = (long long)J.m * J.n;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -517,6 +533,8 @@ __global__ void k_copy(const CopyJob *__restrict__ jobs, int njobs) {
 // Same epilogue expression as k_gemm, and the identity product is exact there,
 // so the result is the GEMM's bit for bit.
 __global__ void k_axpby(const GemmJob *__restrict__ jobs, const int *__restrict__ which) {
+  pdl_wait();
+  pdl_trigger();
   const GemmJob J = jobs[blockIdx.y];
   const bool a_is_eye = which[blockIdx.y] == 0;
   const double *X = a_is_eye ? J.B : J.A;
@@ -534,6 +552,8 @@ __global__ void k_axpby(const GemmJob *__restrict__ jobs, const int *__restrict_
 // identity in an m x m block (ld)
 __global__ void k_identity(double *const *__restrict__ ptrs, const int *__restrict__ dims,
                            const int *__restrict__ lds) {
+  pdl_wait();
+  pdl_trigger();
   double *p = ptrs[blockIdx.y];
   int m = dims[blockIdx.y], ld = lds[blockIdx.y];
   long long total = (long long)m * m;
@@ -569,6 +589,8 @@ struct GemmSplit {  // one split output tile: partials ws .. ws+ns-1
 __global__ void __launch_bounds__(256) k_gemm(const GemmJob *__restrict__ jobs,
                                               const GemmTile *__restrict__ tiles, int ntiles,
                                               double *__restrict__ ws) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double As[GEMM_BK][RB_LD];
   __shared__ double Bs[GEMM_BK][RB_LD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -645,6 +667,8 @@ __global__ void __launch_bounds__(256) k_gemm(const GemmJob *__restrict__ jobs,
 __global__ void __launch_bounds__(256) k_gemm_reduce(const GemmJob *__restrict__ jobs,
                                                      const GemmSplit *__restrict__ splits,
                                                      const double *__restrict__ ws) {
+  pdl_wait();
+  pdl_trigger();
   const GemmSplit sp = splits[blockIdx.x];
   const GemmJob J = jobs[sp.job];
   const int m0 = sp.mt * GEMM_BM, n0 = sp.nt * GEMM_BN;
@@ -857,6 +881,8 @@ __device__ __forceinline__ void plu_row_update(double *__restrict__ row, const d
 template <bool SMEM_CORE, int NT = 512>
 __global__ void __launch_bounds__(NT) k_plu_cta2(const PluJob *__restrict__ jobs, const int *__restrict__ ids,
                                                  double eps) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) char dsm[];
   __shared__ MaxLoc red[32];
   __shared__ PluState st;
@@ -1717,6 +1743,8 @@ struct LuExtractJob {
   double *out;
 };
 __global__ void k_lu_extract(const LuExtractJob *__restrict__ jobs) {
+  pdl_wait();
+  pdl_trigger();
   const LuExtractJob J = jobs[blockIdx.y];
   long long total = (long long)J.r * J.r;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -1735,6 +1763,8 @@ __global__ void k_lu_extract(const LuExtractJob *__restrict__ jobs) {
 // non-finite input (hodlr.py:346).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(512) k_getrf(const LuJob *__restrict__ jobs) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ MaxLoc red[33];
   __shared__ int s_p;
   const LuJob J = jobs[blockIdx.x];
@@ -1891,6 +1921,8 @@ __global__ void __launch_bounds__(512) k_getrf_panel_cl(const PanelJob *__restri
 // panel LU with the panel in global memory: fallback for panels taller than a
 // cluster's shared memory holds (16 x PANEL_ROWS_MAX rows)
 __global__ void __launch_bounds__(512) k_getrf_panel(const PanelJob *__restrict__ jobs) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ MaxLoc red[33];
   __shared__ int s_p;
   const PanelJob J = jobs[blockIdx.x];
@@ -1956,6 +1988,8 @@ __device__ __forceinline__ void warp_argmax_row(double v, int row, unsigned &uh_
 }
 
 __global__ void __launch_bounds__(512) k_getrf_panel_cta(const PanelJob *__restrict__ jobs) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double sh_panel[];
   __shared__ unsigned s_uh[16], s_ul[16];
   __shared__ int s_row[16];
@@ -2025,6 +2059,8 @@ struct SwapJob {
   int skip0, skip1;  // columns [skip0, skip1) are left alone
 };
 __global__ void k_laswp(const SwapJob *__restrict__ jobs) {
+  pdl_wait();
+  pdl_trigger();
   const SwapJob J = jobs[blockIdx.y];
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < J.ncols; j += gridDim.x * blockDim.x) {
     if (j >= J.skip0 && j < J.skip1) continue;
@@ -2072,6 +2108,8 @@ struct InvJob {  // in-place inverse of an n x n block (n <= INV_SMALL)
 // shared-memory matrix, no integer division.
 template <int NW, int CPL>
 __global__ void __launch_bounds__(NW * 32) k_inv_reg(const InvJob *__restrict__ jobs) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NR = NW * 8, NC = 32 * CPL;
   static_assert(NW <= 32, "candidate reduction is one warp wide");
   // parity double buffers: step k writes buffer k & 1 before its only barrier;
@@ -2235,6 +2273,8 @@ constexpr size_t TRINV_SMEM = sizeof(double) * (64 * 64 + 2 * 64 * 65);
 // All pairs of a stage are formed in parallel (log2(64) = 6 stages of small
 // shared-memory GEMMs, instead of 64 dependent substitution rows).
 __global__ void __launch_bounds__(256) k_trinv(const TrinvJob *__restrict__ jobs) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ double tdyn[];
   double *Ts = tdyn;              // w x w (ld w)
   double *X = tdyn + 64 * 64;     // inverse, ld 65
@@ -2291,6 +2331,8 @@ __global__ void __launch_bounds__(256) k_trinv(const TrinvJob *__restrict__ jobs
 
 // diagonal check after a blocked LU
 __global__ void k_diag_check(const LuJob *__restrict__ jobs) {
+  pdl_wait();
+  pdl_trigger();
   const LuJob J = jobs[blockIdx.x];
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
@@ -2492,6 +2534,8 @@ __device__ __forceinline__ void gemv_rows(const GemvJob *__restrict__ jobs, cons
 // job wq[warp] (computed on the host: no search through start[] on the device)
 __global__ void __launch_bounds__(256) k_gemv2(const GemvJob *__restrict__ jobs, const int *__restrict__ start,
                                                const int *__restrict__ wq, int chunk, int nrows) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int t0 = warp * chunk;
   if (t0 >= nrows) return;
@@ -2638,6 +2682,8 @@ __device__ __forceinline__ void gemv_rows_mv(const GemvJob *__restrict__ jobs, c
 template <int NV>
 __global__ void __launch_bounds__(256) k_gemv_mv(const GemvJob *__restrict__ jobs, const int *__restrict__ start,
                                                  const int *__restrict__ wq, int chunk, int nrows) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int t0 = warp * chunk;
   if (t0 >= nrows) return;
@@ -2686,6 +2732,8 @@ __device__ __forceinline__ void sub_level_rows(const SubApply &S, const SubSeg &
 }
 template <int NV>
 __global__ void __launch_bounds__(512) k_apply_sub(SubApply S, int up) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int s0 = S.cta_seg[blockIdx.x], s1 = S.cta_seg[blockIdx.x + 1];
   for (int k = 0; k < s1 - s0; ++k) {
@@ -2718,6 +2766,8 @@ __global__ void __launch_bounds__(512) k_apply_sub(SubApply S, int up) {
 // ---------------------------------------------------------------------------
 __global__ void k_scatter_perm(const double *__restrict__ b, const long long *__restrict__ perm,
                                double *__restrict__ bu, long long n) {
+  pdl_wait();
+  pdl_trigger();
   b += blockIdx.y * n;  // right-hand side blockIdx.y
   bu += blockIdx.y * n;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -2726,6 +2776,8 @@ __global__ void k_scatter_perm(const double *__restrict__ b, const long long *__
 }
 __global__ void k_gather_perm(const double *__restrict__ x, const long long *__restrict__ perm,
                               double *__restrict__ out, long long n) {
+  pdl_wait();
+  pdl_trigger();
   x += blockIdx.y * n;  // right-hand side blockIdx.y
   out += blockIdx.y * n;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -2740,6 +2792,8 @@ __global__ void __launch_bounds__(256) k_contrib_gather(const long long *__restr
                                                         const long long *__restrict__ coff,
                                                         const double *__restrict__ cbuf, double *__restrict__ bu,
                                                         double *__restrict__ y, long long cstride, long long bstride) {
+  pdl_wait();
+  pdl_trigger();
   cbuf += blockIdx.y * cstride;  // right-hand side blockIdx.y
   bu += blockIdx.y * bstride;
   if (y) y += blockIdx.y * bstride;

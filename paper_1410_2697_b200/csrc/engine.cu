@@ -261,7 +261,9 @@ struct Ctx {
   cudaStream_t side = nullptr;   // concurrent large-core cluster / cooperative kernels
   cudaStream_t side2 = nullptr;  // 8-CTA cluster cores, concurrently with the 16-CTA ones
   cudaStream_t side3 = nullptr;  // the cooperative grid-class cores when launched first
+  cudaStream_t side4 = nullptr;  // the one-CTA pivot-LU cores, beside the dense fronts' work
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr, ev_join3 = nullptr;
+  cudaEvent_t ev_fork2 = nullptr, ev_join4 = nullptr;
   cudaEvent_t gmres_ev[2] = {nullptr, nullptr};  // Hessenberg column read-backs (pipelined Arnoldi)
   int cluster_size = 16;
   size_t plu_dyn_max = 0;  // dynamic shared memory the pivot-LU kernels may use (per device)
@@ -1212,6 +1214,14 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
     ctx->launches++;
   }
   };
+  // MFH_PLU_EVENTS=1: per-class completion times of this window (diagnostics;
+  // adds a synchronization)
+  static const bool pev = getenv("MFH_PLU_EVENTS") != nullptr;
+  cudaEvent_t pe[8] = {};
+  if (pev) {
+    for (auto &e : pe) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(pe[0], ctx->s));
+  }
   const bool coop_own = coop_first && !grd.empty() && (!cl8.empty() || !cl16.empty());
   if (coop_own) {  // the critical-path cores claim their SMs first, clusters fill the rest
     CK(cudaStreamWaitEvent(ctx->side3, ctx->ev_fork, 0));
@@ -1219,28 +1229,63 @@ static void run_plu(Sink &sk, const std::vector<PluJob> &jobs, double eps,
     CK(cudaEventRecord(ctx->ev_join3, ctx->side3));
   }
   cluster_group(cl8, ids_cl8, 8, ctx->side2);
+  if (pev && !cl8.empty()) CK(cudaEventRecord(pe[1], ctx->side2));
   if (!cl8.empty()) CK(cudaEventRecord(ctx->ev_join2, ctx->side2));
   cluster_group(cl16, ids_cl16, CS, ctx->side);
+  if (pev && side) CK(cudaEventRecord(pe[2], ctx->side));
   if (!coop_own) coop(ctx->side);
+  if (pev && side) CK(cudaEventRecord(pe[3], ctx->side));
   if (side) CK(cudaEventRecord(ctx->ev_join, ctx->side));
-  if (main_work) main_work();
+  // the one-CTA cores on their own stream, beside the dense fronts' work on the
+  // main stream (both are independent of each other within the height)
+  int *dids_small[3] = {nullptr, nullptr, nullptr};
+  for (int b = 0; b < 3; ++b)
+    if (!small[b].empty()) dids_small[b] = sk.push(small[b]);
+  const bool any_small = !small[0].empty() || !small[1].empty() || !small[2].empty();
+  if (any_small) {
+    CK(cudaEventRecord(ctx->ev_fork2, ctx->s));  // after the pushes above
+    CK(cudaStreamWaitEvent(ctx->side4, ctx->ev_fork2, 0));
+  }
   for (int b = 0; b < 3; ++b) {
     if (small[b].empty()) continue;
-    int *dids = sk.push(small[b]);
     size_t sm = 0;
     for (int q : small[b]) sm = std::max(sm, cta_bytes(jobs[q].m, jobs[q].n));
-    int nb = (int)small[b].size();
-    sk.launch([=](cudaStream_t st) {
-      if (b == 2)
-        launch_pdl(k_plu_cta2<true, 1024>, dim3(nb), dim3(1024), sm, st, dj, dids, eps);
-      else
-        launch_pdl(k_plu_cta2<true, 512>, dim3(nb), dim3(b == 0 ? 256 : 512), sm, st, dj, dids, eps);
-      check_launch();
-    });
+    const int nb = (int)small[b].size();
+    if (b == 2)
+      launch_pdl(k_plu_cta2<true, 1024>, dim3(nb), dim3(1024), sm, ctx->side4, dj, (const int *)dids_small[b], eps);
+    else
+      launch_pdl(k_plu_cta2<true, 512>, dim3(nb), dim3(b == 0 ? 256 : 512), sm, ctx->side4, dj,
+                 (const int *)dids_small[b], eps);
+    ctx->launches++;
   }
+  if (any_small) CK(cudaEventRecord(ctx->ev_join4, ctx->side4));
+  if (main_work) main_work();
+  if (pev) CK(cudaEventRecord(pe[4], ctx->s));
+  if (any_small) CK(cudaStreamWaitEvent(ctx->s, ctx->ev_join4, 0));
+  if (pev) CK(cudaEventRecord(pe[5], ctx->s));
   if (side) CK(cudaStreamWaitEvent(ctx->s, ctx->ev_join, 0));
   if (!cl8.empty()) CK(cudaStreamWaitEvent(ctx->s, ctx->ev_join2, 0));
   if (coop_own) CK(cudaStreamWaitEvent(ctx->s, ctx->ev_join3, 0));
+  if (pev) {
+    CK(cudaEventRecord(pe[6], ctx->s));
+    CK(cudaEventSynchronize(pe[6]));
+    auto el = [&](int q, bool have) {
+      float ms = -1.f;
+      if (have) CK(cudaEventElapsedTime(&ms, pe[0], pe[q]));
+      return ms;
+    };
+    auto steps = [&](const std::vector<int> &v) {
+      int mx = 0;
+      for (int q : v) mx = std::max(mx, std::min(std::min(jobs[q].m, jobs[q].n), jobs[q].kmax));
+      return mx;
+    };
+    int nsmall = 0, ssmall = 0;
+    for (auto &v : small) nsmall += (int)v.size(), ssmall = std::max(ssmall, steps(v));
+    fprintf(stderr, "[mfh plu window] cl8 %zu cores (<=%d steps) done %.3f | cl16 %zu (<=%d) done %.3f | grid %zu (<=%d) done %.3f | main dense %.3f, cta %d (<=%d) done %.3f | all %.3f ms\n",
+            cl8.size(), steps(cl8), el(1, !cl8.empty()), cl16.size(), steps(cl16), el(2, side), grd.size(), steps(grd),
+            el(3, side), el(4, true), nsmall, ssmall, el(5, true), el(6, true));
+    for (auto &e : pe) cudaEventDestroy(e);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -4467,7 +4512,10 @@ extern "C" int mfh_ctx_create(int device, mfh_ctx **out) {
   CK(cudaStreamCreateWithFlags(&c->c.side, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->c.side2, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->c.side3, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->c.side4, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->c.ev_join3, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->c.ev_fork2, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->c.ev_join4, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->c.ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->c.ev_join, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->c.ev_join2, cudaEventDisableTiming));
@@ -4509,8 +4557,12 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   cudaStreamSynchronize(ctx->c.side);
   cudaStreamSynchronize(ctx->c.side2);
   cudaStreamSynchronize(ctx->c.side3);
+  cudaStreamSynchronize(ctx->c.side4);
   cudaEventDestroy(ctx->c.ev_join3);
+  cudaEventDestroy(ctx->c.ev_fork2);
+  cudaEventDestroy(ctx->c.ev_join4);
   cudaStreamDestroy(ctx->c.side3);
+  cudaStreamDestroy(ctx->c.side4);
   cudaEventDestroy(ctx->c.ev_fork);
   cudaEventDestroy(ctx->c.ev_join);
   cudaEventDestroy(ctx->c.ev_join2);

@@ -19,15 +19,21 @@ def fma(a, b, c):
     return float(Fraction(a) * Fraction(b) + Fraction(c))
 
 
-def ref_gemm(A, B, Cin, alpha, beta):
+def ref_gemm(A, B, Cin, alpha, beta, split=0):
+    """k-ascending FMA chain per output; with split-K, one chain per k chunk
+    and the chunk partials summed in order (k_gemm_reduce)."""
     m, k = A.shape
     n = B.shape[1]
     out = np.empty((m, n))
+    chunks = [(0, k)] if not split or k < 2 * split else [(c, min(k, c + split)) for c in range(0, k, split)]
     for i in range(m):
         for j in range(n):
-            acc = 0.0
-            for q in range(k):
-                acc = fma(A[i, q], B[q, j], acc)
+            acc = None
+            for (c0, c1) in chunks:
+                part = 0.0
+                for q in range(c0, c1):
+                    part = fma(A[i, q], B[q, j], part)
+                acc = part if acc is None else acc + part
             v = alpha * acc
             out[i, j] = v if beta == 0.0 else fma(beta, Cin[i, j], v)
     return out
@@ -66,7 +72,7 @@ def test_gemm_bitwise_against_fma_chain(split_k):
     buf = np.concatenate(buf_parts)
     out = run(jobs, buf, split_k)
     for (A, B, Cm, alpha, beta, c0, m, n) in meta:
-        np.testing.assert_array_equal(view(out, c0, m, n, n), ref_gemm(A, B, Cm, alpha, beta))
+        np.testing.assert_array_equal(view(out, c0, m, n, n), ref_gemm(A, B, Cm, alpha, beta, split_k))
 
 
 def test_gemm_aliased_and_disjoint_blocks():

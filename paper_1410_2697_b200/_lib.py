@@ -16,6 +16,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmfh.so")
+# A/B builds only (scripts): another in-tree build of the same library
+if os.environ.get("MFH_LIB_VARIANT"):
+    LIB_PATH = os.path.join(os.path.dirname(LIB_PATH), "libmfh_" + os.environ["MFH_LIB_VARIANT"] + ".so")
 
 MFH_OK, MFH_EVALUE, MFH_EPIVOT, MFH_ERUNTIME = 0, 1, 2, 3
 

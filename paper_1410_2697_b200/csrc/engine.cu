@@ -607,7 +607,7 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
   int nt = (int)tiles.size(), nsp = (int)splits.size();
   int grid = std::min(nt, 148 * 16);
   sk.launch([=](cudaStream_t s) {
-    launch_pdl(k_gemm, dim3(grid), dim3(256), 0, s, dj, dt, nt, dws);
+    launch_pdl(k_gemm, dim3(grid), dim3(256), GEMM_DYN, s, dj, dt, nt, dws);
     check_launch();
     if (nsp) launch_pdl(k_gemm_reduce, dim3(nsp), dim3(256), 0, s, dj, dsp, dws);
     check_launch();
@@ -969,6 +969,7 @@ static void device_setup(Ctx *ctx) {
     CK(cudaFuncSetAttribute(k_getrf_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double) * PANEL_ROWS_MAX * PLD)));
     CK(cudaFuncSetAttribute(k_sample_rb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RB_DYN));
+    CK(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_DYN));
   }
   // 16-CTA clusters need the non-portable opt-in; without it the cluster
   // kernels run 8-CTA clusters

@@ -326,6 +326,19 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
 
 // acc[a][b] = sum_u X[sx[row], u] * Y[u, sy[col]] (u ascending from 0) for the
 // thread's entries; rows / cols with index -1 contribute zero
+// cp.async (LDGSTS) 8-byte element copies into shared memory; src_size 0
+// writes zeros (padding) without reading
+__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gsrc), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ void rb_dot(double (&acc)[2][8], const double *__restrict__ X, int ldx, const int *sx,
                                        const double *__restrict__ Y, int ldy, const int *sy, int K,
                                        double (*Ws)[RB_LD], double (*Vs)[RB_LD], int tid, int wr, int wc, int g,
@@ -586,15 +599,20 @@ struct GemmSplit {  // one split output tile: partials ws .. ws+ns-1
   int job, mt, nt, ws, ns;
 };
 
+constexpr int GEMM_STG = 3;  // cp.async stages of (A slab, B slab)
+constexpr size_t GEMM_DYN = sizeof(double) * GEMM_STG * 2 * GEMM_BK * RB_LD;
 __global__ void __launch_bounds__(256) k_gemm(const GemmJob *__restrict__ jobs,
                                               const GemmTile *__restrict__ tiles, int ntiles,
                                               double *__restrict__ ws) {
   pdl_wait();
   pdl_trigger();
-  __shared__ double As[GEMM_BK][RB_LD];
-  __shared__ double Bs[GEMM_BK][RB_LD];
+  extern __shared__ double gemm_stg[];  // GEMM_STG x (As[GEMM_BK][RB_LD], Bs[GEMM_BK][RB_LD])
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wr = warp >> 1, wc = warp & 1, g = lane >> 2, q = lane & 3;
+  auto Ast = [&](int sidx) { return reinterpret_cast<double(*)[RB_LD]>(gemm_stg + (size_t)sidx * 2 * GEMM_BK * RB_LD); };
+  auto Bst = [&](int sidx) {
+    return reinterpret_cast<double(*)[RB_LD]>(gemm_stg + (size_t)sidx * 2 * GEMM_BK * RB_LD + GEMM_BK * RB_LD);
+  };
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const GemmTile tl = tiles[t];
     const GemmJob J = jobs[tl.job];
@@ -605,29 +623,36 @@ __global__ void __launch_bounds__(256) k_gemm(const GemmJob *__restrict__ jobs,
     for (int a = 0; a < 2; ++a)
 #pragma unroll
       for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
-    double ra[4], rb[4];
-    auto load_slab = [&](int k0) {
+    const int nsl = tl.k0 < k1 ? (k1 - tl.k0 + GEMM_BK - 1) / GEMM_BK : 0;
+    // slab c gathered straight into stage c % GEMM_STG (zeros outside the job)
+    auto issue = [&](int c) {
+      if (c < nsl) {
+        const int k0 = tl.k0 + c * GEMM_BK;
+        double(*As)[RB_LD] = Ast(c % GEMM_STG);
+        double(*Bs)[RB_LD] = Bst(c % GEMM_STG);
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int e = tid + 256 * m;
-        const int mm = e >> 4, kk = e & 15;  // A: 64 rows x 16 k
-        const int gm = m0 + mm, gk = k0 + kk;
-        ra[m] = (gm < J.m && gk < k1) ? J.A[(long long)gm * J.lda + gk] : 0.0;
-        const int k2 = e >> 6, nn = e & 63;  // B: 16 k x 64 cols
-        const int gk2 = k0 + k2, gn = n0 + nn;
-        rb[m] = (gk2 < k1 && gn < J.n) ? J.B[(long long)gk2 * J.ldb + gn] : 0.0;
+        for (int m = 0; m < 4; ++m) {
+          const int e = tid + 256 * m;
+          const int mm = e >> 4, kk = e & 15;  // A: 64 rows x 16 k
+          const int gm = m0 + mm, gk = k0 + kk;
+          const bool oka = gm < J.m && gk < k1;
+          cp_async8(&As[kk][mm], oka ? J.A + (long long)gm * J.lda + gk : J.A, oka);
+          const int k2 = e >> 6, nn = e & 63;  // B: 16 k x 64 cols
+          const int gk2 = k0 + k2, gn = n0 + nn;
+          const bool okb = gk2 < k1 && gn < J.n;
+          cp_async8(&Bs[k2][nn], okb ? J.B + (long long)gk2 * J.ldb + gn : J.B, okb);
+        }
       }
+      cp_async_commit();
     };
-    if (tl.k0 < k1) load_slab(tl.k0);
-    for (int k0 = tl.k0; k0 < k1; k0 += GEMM_BK) {
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int e = tid + 256 * m;
-        As[e & 15][e >> 4] = ra[m];
-        Bs[e >> 6][e & 63] = rb[m];
-      }
-      __syncthreads();
-      if (k0 + GEMM_BK < k1) load_slab(k0 + GEMM_BK);  // in flight during the MMAs
+    issue(0);
+    issue(1);
+    for (int c = 0; c < nsl; ++c) {
+      cp_async_wait<1>();
+      __syncthreads();  // slab c visible to all; slab c - 1's stage no longer read
+      issue(c + 2);
+      double(*As)[RB_LD] = Ast(c % GEMM_STG);
+      double(*Bs)[RB_LD] = Bst(c % GEMM_STG);
 #pragma unroll
       for (int kb = 0; kb < GEMM_BK / 4; ++kb) {
         double fa[2], fb[4];
@@ -640,8 +665,9 @@ __global__ void __launch_bounds__(256) k_gemm(const GemmJob *__restrict__ jobs,
 #pragma unroll
           for (int j = 0; j < 4; ++j) dmma884(acc[a][2 * j], acc[a][2 * j + 1], fa[a], fb[j]);
       }
-      __syncthreads();
     }
+    cp_async_wait<0>();
+    __syncthreads();  // stages free for the next tile
     double *part = tl.ws >= 0 ? ws + (long long)tl.ws * (GEMM_BM * GEMM_BN) : nullptr;
 #pragma unroll
     for (int a = 0; a < 2; ++a) {

@@ -262,8 +262,11 @@ int mfh_gmres_sharded(mfh_factor *F, int64_t n, const int64_t *indptr, const int
  * b + r*n, its solution x + r*n; groups of up to eight run in lockstep and
  * share each preconditioner apply, so the factor is read once per Arnoldi step
  * for the group. Per right-hand side: history row r of hist (hist_cap
- * entries), n_hist[r], iterations[r], converged[r]; every column is
- * bit-identical to its mfh_gmres solve. ops->A and ops->M must be device
+ * entries), n_hist[r], iterations[r], converged[r]. The shared apply runs
+ * on the FP64 tensor cores (several vectors per matrix element), the
+ * one-vector apply of mfh_gmres as a warp per row: a column equals its
+ * mfh_gmres solve to rounding (iteration counts within one); a column never
+ * depends on the other columns of its group. ops->A and ops->M must be device
  * objects (no host callbacks). Host arrays / device arrays respectively. */
 int mfh_gmres_batched(mfh_ctx *ctx, const mfh_gmres_ops *ops, int64_t n, int64_t nrhs, const double *b,
                       double *x, double tol, int64_t max_iter, int64_t restart, double *hist,
@@ -329,6 +332,15 @@ int mfh_test_inverse_batched(mfh_ctx *ctx, int64_t batch, const int64_t *offs, c
  * splits long k for <= 32-tile jobs into chunks of split_k (deterministic). */
 int mfh_test_gemm_batched(mfh_ctx *ctx, int64_t batch, const int64_t *desc, const double *ab, double *buf,
                           int64_t total, int split_k);
+
+/* The apply's batched GEMV (k_gemv_tc: rows in groups of 8 on the FP64 tensor
+ * cores, 1..8 right-hand sides) on one host workspace: job q is
+ * desc[16q..16q+15] = (m, k1, k2, y, y0, A1, lda1, x1, A2, lda2, x2, idx2, ys,
+ * y0s, x1s, x2s) with offsets into buf (y0, A2, x2, idx2 = -1: none; idx2 is
+ * an offset into idx) and (a1, a2) = ab[2q], ab[2q+1]:
+ *   y[v][i] = (y0[v][i] or 0) + a1 A1[i,:] . x1[v] + a2 A2[i,:] . x2[v][idx2]. */
+int mfh_test_gemv_batched(mfh_ctx *ctx, int64_t batch, const int64_t *desc, const double *ab, double *buf,
+                          int64_t total, const int64_t *idx, int64_t nidx, int nv);
 
 #ifdef __cplusplus
 }

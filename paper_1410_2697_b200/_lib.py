@@ -162,6 +162,7 @@ def _sig(lib):
         "mfh_precond_free": (None, [P]),
         "mfh_ilut_factor": (C.c_int, [I64, P, P, P, I64, d, pi, pi, P, P, P, P, P, P]),
         "mfh_test_gemm_batched": (C.c_int, [P, I64, P, P, P, I64, C.c_int]),
+        "mfh_test_gemv_batched": (C.c_int, [P, I64, P, P, P, I64, P, I64, C.c_int]),
         "mfh_gmres_sharded": (C.c_int, [P, I64, P, P, P, P, P, d, I64, I64, P, pi, pi, C.POINTER(C.c_int)]),
         "mfh_csr_free": (None, [P]),
         "mfh_gmres": (C.c_int, [P, C.POINTER(mfh_gmres_ops), I64, P, P, d, I64, I64, P, pi, pi,

@@ -3706,69 +3706,136 @@ static FacView fac_view(const mfh_factor *F, const BlockH &b) {
   return v;
 }
 
-template <int NV>
-static void launch_gemv_mv(cudaStream_t st, int grid, const GemvJob *dj, const int *ds, const int *dw, int chunk,
-                           int nr) {
-  launch_pdl(k_gemv_mv<NV>, dim3(grid), dim3(256), 0, st, dj, ds, dw, chunk, nr);
+// One MGS sweep (k_mgs_reg<R> when the grid's slices fit R registers per
+// thread, else k_mgs_coop). The plan is a function of n and the device only,
+// so every solve of the same n sums in the same order (batched columns stay
+// bitwise the one-vector solves).
+struct MgsPlan {
+  const void *fn = nullptr;
+  int grid = 1;
+  size_t smem = 0;
+};
+static MgsPlan mgs_plan(int device, long long n) {
+  static std::mutex mu;
+  static std::map<std::pair<int, long long>, MgsPlan> memo;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = memo.find({device, n});
+  if (it != memo.end()) return it->second;
+  int nsm = 148;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  const void *fr[6] = {(const void *)k_mgs_reg<1>, (const void *)k_mgs_reg<2>, (const void *)k_mgs_reg<4>,
+                       (const void *)k_mgs_reg<8>, (const void *)k_mgs_reg<16>, (const void *)k_mgs_reg<32>};
+  MgsPlan p;
+  for (int q = 0; q < 6 && !p.fn; ++q) {
+    const int R = 1 << q;
+    const size_t sm = sizeof(double) * 256 * R;
+    if (sm > 48 * 1024) CK(cudaFuncSetAttribute(fr[q], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fr[q], 256, sm));
+    if (per_sm < 1) continue;
+    int grid = std::min(std::min(per_sm, 4) * nsm, MGS_MAX_GRID);
+    grid = (int)std::min<long long>(grid, std::max<long long>(1, cdiv(n, 256)));
+    if (cdiv(cdiv(n, grid), 256) <= R) {
+      p.fn = fr[q];
+      p.grid = grid;
+      p.smem = sm;
+    }
+  }
+  if (!p.fn) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs_coop, 256, 0));
+    p.fn = (const void *)k_mgs_coop;
+    p.grid = std::max(1, std::min(std::min(per_sm, 2) * nsm, MGS_MAX_GRID));
+    p.grid = (int)std::min<long long>(p.grid, std::max<long long>(1, cdiv(n, 256)));
+  }
+  memo[{device, n}] = p;
+  return p;
 }
-// nv right-hand sides (1..8): vector v of a job at pointer + v * its stride
-static void run_gemv(Sink &sk, const std::vector<GemvJob> &jobs, int nv = 1) {
-  if (jobs.empty()) return;
+static void launch_mgs(const MgsPlan &p, const double *V, double *w, long long n, int j, double *H, double *part,
+                       cudaStream_t st) {
+  void *args[6] = {(void *)&V, (void *)&w, (void *)&n, (void *)&j, (void *)&H, (void *)&part};
+  CK(cudaLaunchCooperativeKernel(p.fn, dim3(p.grid), dim3(256), args, p.smem, st));
+}
+
+// rows of a GEMV job in the subtree kernel's numbering: whole groups of 8
+static inline int gv_rows(int m) { return (std::max(0, m) + 7) & ~7; }
+static inline int gv_ws_host(int k) { return k <= 256 ? 1 : std::min(8, (k + 255) >> 8); }
+template <int NV>
+static void launch_gemv_tc(cudaStream_t st, int grid, const GemvJob *dj, const GvItem *di) {
+  launch_pdl(k_gemv_tc<NV>, dim3(grid), dim3(256), 0, st, dj, di);
+}
+// nv right-hand sides (1..8): vector v of a job at pointer + v * its stride.
+// Several: one CTA per (job, 8 / ws row groups), ws = the job's K segments
+// (k_gemv_tc, FP64 tensor cores).
+// One right-hand side: k_gemv2, a warp per row (lane-strided chains), one
+// wave of warps each taking a contiguous chunk of rows.
+static void run_gemv1(Sink &sk, const std::vector<GemvJob> &jobs) {
   std::vector<int> start(jobs.size() + 1, 0);
   for (size_t q = 0; q < jobs.size(); ++q) start[q + 1] = start[q] + std::max(0, jobs[q].m);
-  const int nr = start.back(), nj = (int)jobs.size();
+  const int nr = start.back();
   if (nr == 0) return;
-  // one wave of warps, each a contiguous chunk of rows (a chunk of >= GV_R rows
-  // of one job keeps GV_R rows' loads in flight)
-  static int occ_nv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  if (nv < 1 || nv > 8) throw runtime_error("run_gemv: 1..8 right-hand sides per launch");
-  int &occ = occ_nv[nv];
+  static int occ = 0;
   if (!occ) {
-    const void *fns[9] = {nullptr, (const void *)k_gemv2, (const void *)k_gemv_mv<2>, (const void *)k_gemv_mv<3>,
-                          (const void *)k_gemv_mv<4>, (const void *)k_gemv_mv<5>, (const void *)k_gemv_mv<6>,
-                          (const void *)k_gemv_mv<7>, (const void *)k_gemv_mv<8>};
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fns[nv], 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)k_gemv2, 256, 0));
     occ = std::max(occ, 1);
   }
-  int grid = (int)std::min<int64_t>(cdiv((int64_t)nr * 32, 256), (int64_t)148 * occ);
-  const int nw = grid * 8;
-  int chunk = (int)cdiv(nr, nw);
-  if (nv > 1) {  // whole row groups of k_gemv_mv (RR rows share each x load)
-    const int rr = nv <= 4 ? 8 : 4;
-    chunk = (int)cdiv(chunk, rr) * rr;
-  }
+  const int grid = (int)std::min<int64_t>(cdiv((int64_t)nr * 32, 256), (int64_t)148 * occ);
+  const int chunk = (int)cdiv(nr, grid * 8);
   std::vector<int> wq;
   wq.reserve(cdiv(nr, chunk));
   for (int t0 = 0, q = 0; t0 < nr; t0 += chunk) {
     while (start[q + 1] <= t0) ++q;
     wq.push_back(q);
   }
+  GemvJob *dj = sk.push(jobs);
+  int *ds = sk.push(start);
+  int *dw = sk.push(wq);
+  sk.launch([=](cudaStream_t st) {
+    launch_pdl(k_gemv2, dim3(grid), dim3(256), 0, st, dj, ds, dw, chunk, nr);
+    check_launch();
+  });
+}
+static void run_gemv(Sink &sk, const std::vector<GemvJob> &jobs, int nv = 1) {
+  if (jobs.empty()) return;
+  if (nv < 1 || nv > 8) throw runtime_error("run_gemv: 1..8 right-hand sides per launch");
+  if (nv == 1) {
+    run_gemv1(sk, jobs);
+    return;
+  }
+  std::vector<GvItem> items;
+  for (size_t q = 0; q < jobs.size(); ++q) {
+    const GemvJob &j = jobs[q];
+    if (j.m <= 0) continue;
+    const int ws = std::max(j.k1 ? gv_ws_host(j.k1) : 1, j.k2 ? gv_ws_host(j.k2) : 1), gpc = 8 / ws;
+    const int ng = (j.m + 7) / 8;
+    for (int g0 = 0; g0 < ng; g0 += gpc) items.push_back(GvItem{(int)q, g0});
+  }
+  if (items.empty()) return;
   static const bool gtrace = getenv("MFH_APPLY_TRACE") != nullptr;
   if (gtrace) {
     double el = 0, mx = 0;
-    int nk2 = 0;
+    int nk2 = 0, nr = 0;
     for (auto &j : jobs) {
       el += (double)j.m * (j.k1 + j.k2);
       mx = std::max(mx, (double)(j.k1 + j.k2));
       nk2 += j.k2 > 0;
+      nr += std::max(0, j.m);
     }
-    fprintf(stderr, "[mfh gemv] jobs %5d rows %7d avg k %7.1f max k %6.0f with k2 %5d grid %4d chunk %3d\n", nj, nr,
-            el / std::max(1, nr), mx, nk2, grid, chunk);
+    fprintf(stderr, "[mfh gemv] jobs %5zu rows %7d avg k %7.1f max k %6.0f with k2 %5d ctas %5zu\n", jobs.size(), nr,
+            el / std::max(1, nr), mx, nk2, items.size());
   }
   GemvJob *dj = sk.push(jobs);
-  int *ds = sk.push(start);
-  int *dw = sk.push(wq);
-  (void)nj;
+  GvItem *di = sk.push(items);
+  const int grid = (int)items.size();
   sk.launch([=](cudaStream_t st) {
     switch (nv) {
-      case 1: launch_pdl(k_gemv2, dim3(grid), dim3(256), 0, st, dj, ds, dw, chunk, nr); break;
-      case 2: launch_gemv_mv<2>(st, grid, dj, ds, dw, chunk, nr); break;
-      case 3: launch_gemv_mv<3>(st, grid, dj, ds, dw, chunk, nr); break;
-      case 4: launch_gemv_mv<4>(st, grid, dj, ds, dw, chunk, nr); break;
-      case 5: launch_gemv_mv<5>(st, grid, dj, ds, dw, chunk, nr); break;
-      case 6: launch_gemv_mv<6>(st, grid, dj, ds, dw, chunk, nr); break;
-      case 7: launch_gemv_mv<7>(st, grid, dj, ds, dw, chunk, nr); break;
-      case 8: launch_gemv_mv<8>(st, grid, dj, ds, dw, chunk, nr); break;
+      case 2: launch_gemv_tc<2>(st, grid, dj, di); break;
+      case 3: launch_gemv_tc<3>(st, grid, dj, di); break;
+      case 4: launch_gemv_tc<4>(st, grid, dj, di); break;
+      case 5: launch_gemv_tc<5>(st, grid, dj, di); break;
+      case 6: launch_gemv_tc<6>(st, grid, dj, di); break;
+      case 7: launch_gemv_tc<7>(st, grid, dj, di); break;
+      case 8: launch_gemv_tc<8>(st, grid, dj, di); break;
       default: throw runtime_error("run_gemv: 1..8 right-hand sides per launch");
     }
     check_launch();
@@ -4252,8 +4319,8 @@ static std::unique_ptr<ApplyPlan> make_apply(mfh_factor *F, int nv) {
                                 nst, nst, nst);
             jup.push_back(u);
             jdn.push_back(d);
-            start.push_back(start.back() + std::max(0, u.m));
-            sdn.push_back(sdn.back() + d.m);
+            start.push_back(start.back() + gv_rows(u.m));  // rows padded to whole groups of 8
+            sdn.push_back(sdn.back() + gv_rows(d.m));
             bytes += 8.0 * ((double)f.npv * f.npv + 2.0 * f.npv * f.nf);
           }
           g.je = (int)jup.size();
@@ -4523,7 +4590,7 @@ extern "C" int mfh_ctx_create(int device, mfh_ctx **out) {
   for (auto &e : c->c.gmres_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   c->c.stage.init(size_t(64) << 20);
   c->c.scratch.chunk = size_t(512) << 20;
-  CK(cudaMalloc(&c->c.d_part, sizeof(double) * (RED_BLOCKS + 64)));
+  CK(cudaMalloc(&c->c.d_part, sizeof(double) * std::max(RED_BLOCKS + 64, 2 * MGS_MAX_GRID)));
   CK(cudaMalloc(&c->c.d_scal, sizeof(double) * 4096));
   CK(cudaMallocHost(&c->c.h_scal, sizeof(double) * 4096));
   device_setup(&c->c);
@@ -5198,12 +5265,7 @@ struct GmresRun {
     double *V = (double *)chunk.first, *w = V + n * (mcap + 1), *r = w + n, *z = r + n;
     double *dy = S + 2048;
     int g = gridn();
-    int per_sm = 0, nsm = 148;
-    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs_coop, 256, 0));
-    int mgs_grid = std::max(1, std::min(per_sm, 2) * nsm);
-    mgs_grid = (int)std::min<int64_t>(mgs_grid, std::max<int64_t>(1, cdiv(n, 256)));
-    if (mgs_grid > (RED_BLOCKS + 64) / 2) mgs_grid = (RED_BLOCKS + 64) / 2;
+    const MgsPlan mgs = mgs_plan(ctx->device, n);
     auto cleanup = [&]() {
       cudaStreamSynchronize(ctx->s);
       ctx->pool.give(chunk);
@@ -5250,12 +5312,7 @@ struct GmresRun {
           auto q2 = std::chrono::steady_clock::now();
           {
             // whole MGS sweep + norm in one cooperative launch
-            const double *Vc = V;
-            double *wc = w, *Hc = S + 8, *pc = ctx->d_part;
-            long long nn = n;
-            int jj32 = (int)jj;
-            void *args[6] = {(void *)&Vc, (void *)&wc, (void *)&nn, (void *)&jj32, (void *)&Hc, (void *)&pc};
-            CK(cudaLaunchCooperativeKernel((const void *)k_mgs_coop, dim3(mgs_grid), dim3(256), args, 0, ctx->s));
+            launch_mgs(mgs, V, w, n, (int)jj, S + 8, ctx->d_part, ctx->s);
             ctx->launches++;
           }
           CK(cudaMemcpyAsync(hbuf[jj & 1], S + 8, sizeof(double) * (jj + 2), cudaMemcpyDeviceToHost, ctx->s));
@@ -5384,12 +5441,7 @@ struct GmresMulti {
     CK(cudaMallocHost(&hp, sizeof(double) * (size_t)nv * (2 * HS + 8)));
     double *hH = hp, *hY = hp + nv * HS, *hS = hp + 2 * nv * HS;
     int gr = g.gridn();
-    int per_sm = 0, nsm = 148;
-    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs_coop, 256, 0));
-    int mgs_grid = std::max(1, std::min(per_sm, 2) * nsm);
-    mgs_grid = (int)std::min<int64_t>(mgs_grid, std::max<int64_t>(1, cdiv(n, 256)));
-    if (mgs_grid > (RED_BLOCKS + 64) / 2) mgs_grid = (RED_BLOCKS + 64) / 2;
+    const MgsPlan mgs = mgs_plan(ctx->device, n);
     auto sync_read = [&](double *dst, const double *src, size_t bytes) {
       CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->s));
       auto t0 = std::chrono::steady_clock::now();
@@ -5461,12 +5513,7 @@ struct GmresMulti {
           apply_device_nv(ops->M, nv, V + (size_t)j * n, vs, z, n);
           for (int v : run) {
             op_apply_device(ops->A, Z(v), W(v));
-            const double *Vc = V + (size_t)v * vs;
-            double *wc = W(v), *Hc = Hd + v * HS, *pc = ctx->d_part;
-            long long nn = n;
-            int jj = (int)j;
-            void *args[6] = {(void *)&Vc, (void *)&wc, (void *)&nn, (void *)&jj, (void *)&Hc, (void *)&pc};
-            CK(cudaLaunchCooperativeKernel((const void *)k_mgs_coop, dim3(mgs_grid), dim3(256), args, 0, ctx->s));
+            launch_mgs(mgs, V + (size_t)v * vs, W(v), n, (int)j, Hd + v * HS, ctx->d_part, ctx->s);
             ctx->launches++;
           }
           CK(cudaMemcpy2DAsync(hH, sizeof(double) * HS, Hd, sizeof(double) * HS, sizeof(double) * (j + 2), nv,
@@ -6176,6 +6223,54 @@ extern "C" int mfh_test_gemm_batched(mfh_ctx *ctx, int64_t batch, const int64_t 
     throw;
   }
   g_split_k_override = -1;
+  CK(cudaMemcpyAsync(buf, d, sizeof(double) * total, cudaMemcpyDeviceToHost, c->s));
+  CK(cudaStreamSynchronize(c->s));
+  c->scratch.reset();
+  c->stage.rewind();
+  MFH_CATCH
+}
+
+// Test hook: the apply's batched GEMV (k_gemv_tc, 1..8 right-hand sides) on one
+// host workspace. Job q is desc[16q..16q+15] = (m, k1, k2, y, y0, A1, lda1, x1,
+// A2, lda2, x2, idx2, ys, y0s, x1s, x2s): offsets into buf (y0 / A2 / idx2 -1 =
+// none; idx2 is an offset into idx), ab[2q], ab[2q+1] = (a1, a2).
+extern "C" int mfh_test_gemv_batched(mfh_ctx *ctx, int64_t batch, const int64_t *desc, const double *ab,
+                                     double *buf, int64_t total, const int64_t *idx, int64_t nidx, int nv) {
+  std::lock_guard<std::recursive_mutex> lk_(ctx->c.mu);
+  MFH_TRY
+  DeviceGuard dg_(ctx->c.device);
+  Ctx *c = &ctx->c;
+  if (batch == 0) return MFH_OK;
+  double *d = c->scratch.d(std::max<int64_t>(1, total));
+  long long *di = (long long *)c->scratch.alloc(sizeof(long long) * std::max<int64_t>(1, nidx));
+  CK(cudaMemcpyAsync(d, buf, sizeof(double) * total, cudaMemcpyHostToDevice, c->s));
+  if (nidx) CK(cudaMemcpyAsync(di, idx, sizeof(long long) * nidx, cudaMemcpyHostToDevice, c->s));
+  std::vector<GemvJob> jobs;
+  for (int64_t q = 0; q < batch; ++q) {
+    const int64_t *t = desc + 16 * q;
+    GemvJob g{};
+    g.m = (int)t[0];
+    g.k1 = (int)t[1];
+    g.k2 = (int)t[2];
+    g.y = d + t[3];
+    g.y0 = t[4] < 0 ? nullptr : d + t[4];
+    g.A1 = d + t[5];
+    g.lda1 = (int)t[6];
+    g.x1 = d + t[7];
+    g.A2 = t[8] < 0 ? nullptr : d + t[8];
+    g.lda2 = (int)t[9];
+    g.x2 = t[10] < 0 ? nullptr : d + t[10];
+    g.idx2 = t[11] < 0 ? nullptr : di + t[11];
+    g.ys = t[12];
+    g.y0s = t[13];
+    g.x1s = t[14];
+    g.x2s = t[15];
+    g.a1 = ab[2 * q];
+    g.a2 = ab[2 * q + 1];
+    jobs.push_back(g);
+  }
+  Sink s{c};
+  run_gemv(s, jobs, nv);
   CK(cudaMemcpyAsync(buf, d, sizeof(double) * total, cudaMemcpyDeviceToHost, c->s));
   CK(cudaStreamSynchronize(c->s));
   c->scratch.reset();

@@ -2124,14 +2124,17 @@ struct InvJob {  // in-place inverse of an n x n block (n <= INV_SMALL)
 };
 
 
-// Register-tiled Gauss-Jordan inverse for n <= NW*8 (<= 32*CPL), same pivot
-// rule as LAPACK getrf (first max |a| in the column): warp w owns rows [8w, 8w+8), lane l owns columns
-// {l, l+32, ...}; each thread keeps its 8 x CPL tile in registers. Per step:
-// every warp publishes its rows' column-k values, its best candidate and that
-// candidate's row (and the owner of row k publishes row k); after the step's
-// only barrier all threads reduce the candidates redundantly, take the
-// winner's published row as the pivot row and update their tiles. No
-// shared-memory matrix, no integer division.
+// Register-tiled Gauss-Jordan inverse for n <= NW*8 (<= 32*CPL) with partial
+// pivoting (max |a| in the pivot column among the rows not yet used as pivot
+// rows, lowest row on ties) and implicit row interchanges: warp w owns rows
+// [8w, 8w+8), lane l owns columns {l, l+32, ...}; each thread keeps its
+// 8 x CPL tile in registers. Per step the lane holding column k publishes the
+// column of its warp's rows and the warp's candidate, the warp publishes its
+// candidate row; after the step's only barrier every warp reduces the
+// candidates redundantly and updates its tile in place (column k becomes the
+// inverse's column: -a_ik / a_pk, and 1 / a_pk in the pivot row). The row /
+// column scrambling of the implicit interchanges is undone by the final store:
+// inv[step(r)][pivot_row(l)] = tile[r][l].
 template <int NW, int CPL>
 __global__ void __launch_bounds__(NW * 32) k_inv_reg(const InvJob *__restrict__ jobs) {
   pdl_wait();
@@ -2142,22 +2145,25 @@ __global__ void __launch_bounds__(NW * 32) k_inv_reg(const InvJob *__restrict__ 
   // a warp cannot reach step k + 2's writes before every warp has passed step
   // k + 1's barrier, i.e. finished reading step k's buffers
   __shared__ double colkb[2][NR];
-  __shared__ double candrow[2][NW][NC];  // each warp's candidate row (its best row in column k)
-  __shared__ double rowKb[2][NC];
+  __shared__ double candrow[2][NW][NC];
   __shared__ double cv[2][NW];
   __shared__ int ci[2][NW];
-  __shared__ int piv[NR], idx[NC];
+  __shared__ int stepof[NR], prow[NC];
   __shared__ int bad;
   const InvJob J = jobs[blockIdx.x];
   const int n = J.n, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double a[8][CPL];
+  unsigned used = 0;  // bit r: row 8 warp + r is a pivot row already (or beyond n)
 #pragma unroll
-  for (int r = 0; r < 8; ++r)
+  for (int r = 0; r < 8; ++r) {
+    const int i = warp * 8 + r;
+    if (i >= n) used |= 1u << r;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
-      int i = warp * 8 + r, j = lane + 32 * c;
+      const int j = lane + 32 * c;
       a[r][c] = (i < n && j < n) ? J.a[(long long)i * J.lda + j] : 0.0;
     }
+  }
   if (threadIdx.x == 0) bad = 0;
   bool stop = false;
   // step k = 32 kc + kl: the column group kc is a compile-time register index
@@ -2171,90 +2177,82 @@ __global__ void __launch_bounds__(NW * 32) k_inv_reg(const InvJob *__restrict__ 
         break;
       }
       const int par = k & 1;
-      double *colk = colkb[par];
-      // this warp's candidate: rows ascend, so a strict '>' keeps the first maximum
-      double wbv = -1.0;
-      int wbi = 0x7fffffff;
+      int wr = -1;  // this warp's candidate (local row), -1 = none
       if (lane == kl) {
+        double bv = -1.0;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-          const int i = warp * 8 + r;
           const double v = a[r][kc];
-          colk[i] = v;
-          if (i >= k && i < n && fabs(v) > wbv) {
-            wbv = fabs(v);
-            wbi = i;
+          colkb[par][warp * 8 + r] = v;
+          const double av = fabs(v);
+          if (!((used >> r) & 1u) && av > bv) {  // rows ascend: strict '>' keeps the first maximum
+            bv = av;
+            wr = r;
           }
         }
-        cv[par][warp] = wbv;
-        ci[par][warp] = wbi;
+        cv[par][warp] = bv;
+        ci[par][warp] = wr < 0 ? 0x7fffffff : warp * 8 + wr;
       }
-      wbi = __shfl_sync(0xffffffffu, wbi, kl);
-      // publish the candidate row and row k (the swap partner) with the candidates
+      wr = __shfl_sync(0xffffffffu, wr, kl);
+      switch (wr) {  // warp-uniform: publish the candidate row
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        if (warp * 8 + r == wbi)
+        case 0: case 1: case 2: case 3: case 4: case 5: case 6: case 7:
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) candrow[par][warp][lane + 32 * c] = a[r][c];
-        if (warp * 8 + r == k)
+          for (int r = 0; r < 8; ++r)
+            if (r == wr)
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) rowKb[par][lane + 32 * c] = a[r][c];
+              for (int c = 0; c < CPL; ++c) candrow[par][warp][lane + 32 * c] = a[r][c];
+          break;
+        default: break;
       }
       __syncthreads();  // the only barrier of the step
-      // every warp reduces the NW candidates (ties -> lower row)
       double bv = lane < NW ? cv[par][lane] : -1.0;
       int bi = lane < NW ? ci[par][lane] : 0x7fffffff;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
         if (off >= NW) continue;
-        double ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
         if (ov > bv || (ov == bv && oi < bi)) {
           bv = ov;
           bi = oi;
         }
       }
-      bi = __shfl_sync(0xffffffffu, bi, 0);  // only lanes < NW took part in the reduction
-      const int p = bi == 0x7fffffff ? k : bi;
-      const double pv = colk[p];
+      const int p = __shfl_sync(0xffffffffu, bi, 0);
+      const double pv = p == 0x7fffffff ? 0.0 : colkb[par][p];
       if (pv == 0.0 || !isfinite(pv)) {
         if (threadIdx.x == 0) bad = 1;
         stop = true;
         break;
       }
-      if (threadIdx.x == 0) piv[k] = p;
-      const double rinv = 1.0 / pv;  // every thread: the same bits as one division broadcast
-      const double *rowP = bi == 0x7fffffff ? rowKb[par] : candrow[par][p >> 3];
-      double pj[CPL];
+      if (threadIdx.x == 0) {
+        stepof[p] = k;
+        prow[k] = p;
+      }
+      const double rinv = 1.0 / pv;
+      const double *rowP = candrow[par][p >> 3];
+      double pj[CPL];  // the new pivot row: a_pj / a_pk, and 1 / a_pk in column k
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
         const int j = lane + 32 * c;
-        pj[c] = (j == k ? 1.0 : rowP[j]) * rinv;  // scaled pivot row (new row k)
-      }
-      // row p takes old row k (the swap); column k is cleared before the update
-      if (warp == (p >> 3) && p != k) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-          if (warp * 8 + r == p)
-#pragma unroll
-            for (int c = 0; c < CPL; ++c) a[r][c] = rowKb[par][lane + 32 * c];
+        pj[c] = ((c == kc && lane == kl) ? 1.0 : rowP[j]) * rinv;
       }
       if (lane == kl) {
 #pragma unroll
-        for (int r = 0; r < 8; ++r) a[r][kc] = 0.0;
+        for (int r = 0; r < 8; ++r) a[r][kc] = 0.0;  // column k: 0 - a_ik / a_pk after the update
       }
-      const double ck_p = colk[k];  // old A[k][k]: row p's column-k value after the swap
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        const int i = warp * 8 + r;
-        const double f = (i == p) ? ck_p : colk[i];
+        const double f = colkb[par][warp * 8 + r];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) a[r][c] = fma(-f, pj[c], a[r][c]);
       }
-      if (warp == (k >> 3)) {
+      if (warp == (p >> 3)) {
+        const int pr = p & 7;
+        used |= 1u << pr;
 #pragma unroll
         for (int r = 0; r < 8; ++r)
-          if (warp * 8 + r == k)
+          if (r == pr)
 #pragma unroll
             for (int c = 0; c < CPL; ++c) a[r][c] = pj[c];
       }
@@ -2262,22 +2260,12 @@ __global__ void __launch_bounds__(NW * 32) k_inv_reg(const InvJob *__restrict__ 
   }
   __syncthreads();
   if (!bad) {
-    if (threadIdx.x == 0) {
-      for (int j = 0; j < n; ++j) idx[j] = j;
-      for (int k = n - 1; k >= 0; --k) {
-        int t = idx[k];
-        idx[k] = idx[piv[k]];
-        idx[piv[k]] = t;
-      }
-      for (int j = 0; j < n; ++j) piv[idx[j]] = j;  // position of computed column m
-    }
-    __syncthreads();
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
-        int i = warp * 8 + r, m = lane + 32 * c;
-        if (i < n && m < n) J.a[(long long)i * J.lda + piv[m]] = a[r][c];
+        const int i = warp * 8 + r, l = lane + 32 * c;
+        if (i < n && l < n) J.a[(long long)stepof[i] * J.lda + prow[l]] = a[r][c];
       }
   }
   if (threadIdx.x == 0 && bad && J.flag) *J.flag = 1;
@@ -2388,8 +2376,8 @@ __global__ void k_check_finite(const LuJob *__restrict__ jobs) {
 }
 
 // ---------------------------------------------------------------------------
-// batched two-term GEMV for the preconditioner apply (one warp per row):
-//   y[i] = (y0 ? y0[i] : 0) + a1 * A1[i,:] . x1 + a2 * A2[i,:] . x2[idx2]
+// batched two-term GEMV for the preconditioner apply, 1..8 right-hand sides:
+//   y[v][i] = (y0 ? y0[v][i] : 0) + a1 * A1[i,:] . x1[v] + a2 * A2[i,:] . x2[v][idx2]
 // ---------------------------------------------------------------------------
 struct GemvJob {
   double *y;
@@ -2404,11 +2392,15 @@ struct GemvJob {
   const double *x2;
   const long long *idx2;
   double a2;
-  // several right-hand sides (k_gemv_mv): vector v reads / writes at p + v * stride
+  // several right-hand sides: vector v reads / writes at p + v * stride
   long long ys, y0s, x1s, x2s;
 };
 
-// warp per output row; row t belongs to job q with start[q] <= t < start[q + 1].
+// ---------------------------------------------------------------------------
+// one right-hand side: warp per output row (k_gemv2)
+// ---------------------------------------------------------------------------
+// Row t belongs to job q with start[q] <= t < start[q + 1] (rows at or past
+// start[q] + m are padding of a plan shared with k_gemv_tc and are skipped).
 // Each warp takes a contiguous chunk of rows: one binary search, then a walk.
 // Every row is summed in the same order (lane-strided, k ascending per lane,
 // then a shuffle tree) however rows are grouped, so a row's bits do not depend
@@ -2460,14 +2452,18 @@ __device__ __forceinline__ void gemv_rows(const GemvJob *__restrict__ jobs, cons
       qend = start[q + 1];
     }
     const GemvJob &J = jobs[q];
-    const int i = t - start[q];
+    const int i = t - start[q], mend = start[q] + J.m;  // rows past m: padding of a shared plan
+    if (t >= mend) {
+      t = min(t1, qend);
+      continue;
+    }
     if (J.k2 == 0 && J.k1 <= 16) {
       // short rows: W >= k1 lanes per row (W = 4, 8, 16 from k1 alone: one
       // element per lane), 32 / W rows per pass, GV_R passes' loads in flight,
       // xor tree inside the W lanes
       const int W = J.k1 <= 4 ? 4 : (J.k1 <= 8 ? 8 : 16);
       const int G = 32 / W, g = lane / W, l = lane & (W - 1);
-      const int tend = min(t1, qend), s0 = start[q];
+      const int tend = min(t1, mend), s0 = start[q];
       for (int tb = t; tb < tend; tb += G * GV_R) {
         double sr[GV_R];
 #pragma unroll
@@ -2492,7 +2488,7 @@ __device__ __forceinline__ void gemv_rows(const GemvJob *__restrict__ jobs, cons
       t = tend;
       continue;
     }
-    if (t + GV_R <= min(t1, qend)) {
+    if (t + GV_R <= min(t1, mend)) {
       // GV_R rows of one job: the same per-row order as below, loads of all rows in flight
       double s1[GV_R], s2[GV_R];
 #pragma unroll
@@ -2568,15 +2564,103 @@ __global__ void __launch_bounds__(256) k_gemv2(const GemvJob *__restrict__ jobs,
   gemv_rows(jobs, start, wq[warp], t0, min(nrows, t0 + chunk), lane);
 }
 
-// NV right-hand sides in one pass over the matrices: every A element is loaded
-// once and multiplies NV vectors. Per vector and row the arithmetic is exactly
-// gemv_rows' (short rows: W-lane products + xor tree; otherwise lane-strided
-// ascending FMA chains + shuffle tree), so each column is bit-identical to a
-// one-vector apply.
+
+// ---------------------------------------------------------------------------
+// several right-hand sides (2..8): k_gemv_tc
+// ---------------------------------------------------------------------------
+// Rows in groups of 8 on the FP64 tensor cores (mma.sync m8n8k4): the A
+// fragment is 8 rows x 4 consecutive columns of the matrix, the B fragment the
+// same 4 entries of up to 8 right-hand sides (vector v in column v, unused
+// columns zero), so a matrix element is loaded once for every vector and every
+// load instruction reads 32 contiguous bytes per row.
+// Arithmetic of a row (a function of the job's shape only): a term's k columns
+// are cut into ws(k) = ceil(k / 256) (at most 8) segments of whole 16-column
+// steps; a segment's partial is four interleaved k-ascending chains of
+// correctly rounded FMAs (what m8n8k4 computes, see the GEMV test) summed as
+// (c0 + c1) + (c2 + c3), and the term is p_0 + p_1 + ... left to right. A column of a
+// several-vector apply is therefore bitwise the one-vector apply, and a row's
+// bits do not depend on the launch it is in (the sharded apply and the subtree
+// kernel rely on that). Long rows use several warps of one CTA (the segments),
+// so a matrix with few rows still keeps many warps' loads in flight.
+__device__ __forceinline__ int gv_ws(int k) { return k <= 256 ? 1 : min(8, (k + 255) >> 8); }
+__device__ __forceinline__ int gv_seglen(int k, int ws) { return ((((k + ws - 1) / ws) + 15) >> 4) << 4; }
+// partial of one segment [kb, ke) for rows i0 .. i0 + 7 (D fragment: rows
+// i0 + g, vectors 2c, 2c + 1): four interleaved chains (chain j takes columns
+// 4j .. 4j + 3 of every 16-column step, k ascending), then (c0 + c1) + (c2 + c3)
 template <int NV>
-__device__ __forceinline__ void gemv_rows_mv(const GemvJob *__restrict__ jobs, const int *__restrict__ start, int q,
+__device__ __forceinline__ void gv_seg(const double *__restrict__ A, long long lda,
+                                       const double *__restrict__ x, long long xs,
+                                       const long long *__restrict__ idx, int kb, int ke, int i0, int m, int g,
+                                       int c, double &d0, double &d1) {
+  double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  const int row = i0 + g;
+  const bool rok = row < m, xok = g < NV;
+  const double *ar = A + (long long)(rok ? row : 0) * lda;
+  const double *xr = x + (long long)(xok ? g : 0) * xs;
+  int k0 = kb;
+  for (; k0 + 32 <= ke; k0 += 32) {  // two 16-column steps per pass, every load issued first
+    double av[8], xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int kk = k0 + 4 * u + c;
+      av[u] = rok ? ar[kk] : 0.0;
+      xv[u] = xok ? (idx ? xr[idx[kk]] : xr[kk]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dmma884(acc[u & 3][0], acc[u & 3][1], av[u], xv[u]);
+  }
+  if (k0 < ke) {  // the last < 32 columns (masked)
+    double av[8], xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int kk = k0 + 4 * u + c;
+      const bool kin = kk < ke;
+      av[u] = (rok && kin) ? ar[kk] : 0.0;
+      xv[u] = (xok && kin) ? (idx ? xr[idx[kk]] : xr[kk]) : 0.0;
+    }
+    const bool two = ke - k0 > 16;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < 4 || two) dmma884(acc[u & 3][0], acc[u & 3][1], av[u], xv[u]);
+  }
+  d0 = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
+  d1 = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
+}
+template <int NV>
+__device__ __forceinline__ void gv_term_seg(const GemvJob &J, int part, int seg, int i0, int g, int c, double &d0,
+                                            double &d1) {
+  const int k = part == 0 ? J.k1 : J.k2, ws = gv_ws(k), sl = gv_seglen(k, ws);
+  const int kb = seg * sl, ke = min(k, kb + sl);
+  d0 = d1 = 0.0;
+  if (seg >= ws || kb >= ke) return;
+  if (part == 0)
+    gv_seg<NV>(J.A1, J.lda1, J.x1, J.x1s, nullptr, kb, ke, i0, J.m, g, c, d0, d1);
+  else
+    gv_seg<NV>(J.A2, J.lda2, J.x2, J.x2s, J.idx2, kb, ke, i0, J.m, g, c, d0, d1);
+}
+// y = y0; y += a1 S1; y += a2 S2 for the lane's rows / vectors
+template <int NV>
+__device__ __forceinline__ void gv_epilogue(const GemvJob &J, int i0, int g, int c, const double (&s1)[2],
+                                            const double (&s2)[2]) {
+  const int row = i0 + g;
+  if (row >= J.m) return;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int v = 2 * c + e;
+    if (v >= NV) continue;
+    double y = J.y0 ? J.y0[v * J.y0s + row] : 0.0;
+    if (J.k1) y += J.a1 * s1[e];
+    if (J.k2) y += J.a2 * s2[e];
+    J.y[v * J.ys + row] = y;
+  }
+}
+// one warp, whole row groups: every segment in turn, summed in order (the
+// subtree kernel's path; the same bits as k_gemv_tc's CTA-split rows)
+template <int NV>
+__device__ __forceinline__ void gemv_rows_tc(const GemvJob *__restrict__ jobs, const int *__restrict__ start, int q,
                                              int t0, int t1, int lane) {
   if (t0 >= t1) return;
+  const int g = lane >> 2, c = lane & 3;
   int qend = start[q + 1];
   for (int t = t0; t < t1;) {
     while (t >= qend) {
@@ -2584,136 +2668,75 @@ __device__ __forceinline__ void gemv_rows_mv(const GemvJob *__restrict__ jobs, c
       qend = start[q + 1];
     }
     const GemvJob &J = jobs[q];
-    const int s0 = start[q];
-    if (J.k2 == 0 && J.k1 <= 16) {
-      const int W = J.k1 <= 4 ? 4 : (J.k1 <= 8 ? 8 : 16);
-      const int G = 32 / W, g = lane / W, l = lane & (W - 1);
-      const int tend = min(t1, qend);
-      for (int tb = t; tb < tend; tb += G) {
-        const int tr = tb + g;
-        const bool ok = tr < tend && l < J.k1;
-        const double av = ok ? J.A1[(long long)(tr - s0) * J.lda1 + l] : 0.0;
-        double sr[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) sr[v] = ok ? av * J.x1[v * J.x1s + l] : 0.0;
-        for (int o = W >> 1; o > 0; o >>= 1)
-#pragma unroll
-          for (int v = 0; v < NV; ++v) sr[v] += __shfl_xor_sync(0xffffffffu, sr[v], o);
-        if (l == 0 && tr < tend) {
-#pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            const double y0 = J.y0 ? J.y0[v * J.y0s + tr - s0] : 0.0;
-            J.y[v * J.ys + tr - s0] = y0 + J.a1 * sr[v];
-          }
-        }
-      }
-      t = tend;
-      continue;
-    }
-    const int i = t - s0;
-    constexpr int RR = NV <= 4 ? 8 : 4;  // rows sharing each x load (RR x NV accumulators); run_gemv rounds chunks to it
-    if (t + RR <= min(t1, qend)) {
-      // RR rows of one job: per row and vector the same lane-strided ascending
-      // chain and shuffle tree as below; the k1 result is stored (y0 + a1 s1)
-      // and the k2 term added after, i.e. (y0 + a1 s1) + a2 s2 as below
-      double acc[RR][NV];
+    const int s0 = start[q], tend = min(t1, qend);
+    for (int tg = t; tg < tend; tg += 8) {
+      const int i0 = tg - s0;
+      double S[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
       for (int part = 0; part < 2; ++part) {
-        const int kk_n = part == 0 ? J.k1 : J.k2;
-        if (kk_n == 0) {
-          if (part == 0 && lane == 0)
-            for (int r = 0; r < RR; ++r)
-#pragma unroll
-              for (int v = 0; v < NV; ++v) J.y[v * J.ys + i + r] = J.y0 ? J.y0[v * J.y0s + i + r] : 0.0;
-          continue;
-        }
-#pragma unroll
-        for (int r = 0; r < RR; ++r)
-#pragma unroll
-          for (int v = 0; v < NV; ++v) acc[r][v] = 0.0;
-        const double *a = part == 0 ? J.A1 + (long long)i * J.lda1 : J.A2 + (long long)i * J.lda2;
-        const long long lda = part == 0 ? J.lda1 : J.lda2;
-        const double *xb = part == 0 ? J.x1 : J.x2;
-        const long long xs = part == 0 ? J.x1s : J.x2s;
-        const long long *ix = part == 0 ? nullptr : J.idx2;
-        for (int kk = lane; kk < kk_n; kk += 32) {
-          double av[RR];
-#pragma unroll
-          for (int r = 0; r < RR; ++r) av[r] = a[r * lda + kk];
-          const long long xi = ix ? ix[kk] : kk;
-#pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            const double xv = xb[v * xs + xi];
-#pragma unroll
-            for (int r = 0; r < RR; ++r) acc[r][v] = fma(av[r], xv, acc[r][v]);
+        const int k = part == 0 ? J.k1 : J.k2;
+        if (!k) continue;
+        const int ws = gv_ws(k);
+        for (int seg = 0; seg < ws; ++seg) {
+          double d0, d1;
+          gv_term_seg<NV>(J, part, seg, i0, g, c, d0, d1);
+          if (seg == 0) {
+            S[part][0] = d0;
+            S[part][1] = d1;
+          } else {
+            S[part][0] += d0;
+            S[part][1] += d1;
           }
         }
-#pragma unroll
-        for (int r = 0; r < RR; ++r)
-#pragma unroll
-          for (int v = 0; v < NV; ++v) acc[r][v] = warp_sum_down(acc[r][v]);
-        if (lane == 0) {
-          const double al = part == 0 ? J.a1 : J.a2;
-#pragma unroll
-          for (int r = 0; r < RR; ++r)
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-              double *yp = J.y + v * J.ys + i + r;
-              const double base = part == 0 ? (J.y0 ? J.y0[v * J.y0s + i + r] : 0.0) : *yp;
-              *yp = base + al * acc[r][v];
-            }
-        }
       }
-      t += RR;
-      continue;
+      gv_epilogue<NV>(J, i0, g, c, S[0], S[1]);
     }
-    double s1[NV], s2[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) s1[v] = s2[v] = 0.0;
-    if (J.k1) {
-      const double *a = J.A1 + (long long)i * J.lda1;
-#pragma unroll 4
-      for (int kk = lane; kk < J.k1; kk += 32) {
-        const double av = a[kk];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) s1[v] = fma(av, J.x1[v * J.x1s + kk], s1[v]);
-      }
-    }
-    if (J.k2) {
-      const double *a = J.A2 + (long long)i * J.lda2;
-#pragma unroll 4
-      for (int kk = lane; kk < J.k2; kk += 32) {
-        const double av = a[kk];
-        const long long xi = J.idx2 ? J.idx2[kk] : kk;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) s2[v] = fma(av, J.x2[v * J.x2s + xi], s2[v]);
-      }
-    }
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      s1[v] = warp_sum_down(s1[v]);
-      s2[v] = warp_sum_down(s2[v]);
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        double y = J.y0 ? J.y0[v * J.y0s + i] : 0.0;
-        if (J.k1) y += J.a1 * s1[v];
-        if (J.k2) y += J.a2 * s2[v];
-        J.y[v * J.ys + i] = y;
-      }
-    }
-    ++t;
+    t = tend;
   }
 }
+
+// One CTA (8 warps) per work item (job, first row group): a job whose longer
+// term has ws segments gives each of 8 / ws row groups ws warps; the partials
+// meet in shared memory and the segment-0 warp sums them in order.
+struct GvItem {
+  int q, g0;
+};
 template <int NV>
-__global__ void __launch_bounds__(256) k_gemv_mv(const GemvJob *__restrict__ jobs, const int *__restrict__ start,
-                                                 const int *__restrict__ wq, int chunk, int nrows) {
+__global__ void __launch_bounds__(256) k_gemv_tc(const GemvJob *__restrict__ jobs, const GvItem *__restrict__ items) {
   pdl_wait();
   pdl_trigger();
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int t0 = warp * chunk;
-  if (t0 >= nrows) return;
-  gemv_rows_mv<NV>(jobs, start, wq[warp], t0, min(nrows, t0 + chunk), lane);
+  __shared__ double red[8][2][2][32];
+  const GvItem it = items[blockIdx.x];
+  const GemvJob &J = jobs[it.q];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
+  const int ws = max(J.k1 ? gv_ws(J.k1) : 1, J.k2 ? gv_ws(J.k2) : 1), gpc = 8 / ws;
+  const int gi = warp / ws, seg = warp % ws;
+  const int i0 = (it.g0 + gi) * 8;
+  const bool live = gi < gpc && i0 < J.m;
+  double p[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  if (live) {
+    if (J.k1) gv_term_seg<NV>(J, 0, seg, i0, g, c, p[0][0], p[0][1]);
+    if (J.k2) gv_term_seg<NV>(J, 1, seg, i0, g, c, p[1][0], p[1][1]);
+  }
+  if (ws > 1) {
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) red[warp][a][e][lane] = p[a][e];
+    __syncthreads();
+  }
+  if (!live || seg != 0) return;
+  double S[2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const int k = a == 0 ? J.k1 : J.k2, wk = k ? gv_ws(k) : 1;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double s = p[a][e];
+      for (int sg = 1; sg < wk; ++sg) s += red[warp + sg][a][e][lane];
+      S[a][e] = s;
+    }
+  }
+  gv_epilogue<NV>(J, i0, g, c, S[0], S[1]);
 }
 
 // ---------------------------------------------------------------------------
@@ -2724,7 +2747,7 @@ __global__ void __launch_bounds__(256) k_gemv_mv(const GemvJob *__restrict__ job
 // CTA barriers instead of kernel boundaries: per level, the contribution
 // gathers of all its fronts' pivots (upward), then all their GEMV rows, warps
 // spread over the rows of every front of the level. Every row is computed by
-// gemv_rows(_mv) and every gather in k_contrib_gather's order, so the results
+// gemv_rows_tc and every gather in k_contrib_gather's order, so the results
 // are bitwise the per-level graph's; one launch per pass.
 struct SubSeg {   // one level of one CTA
   int jb, je;     // GEMV jobs [jb, je) (rows numbered by start[jb .. je])
@@ -2743,7 +2766,8 @@ struct SubApply {
 template <int NV>
 __device__ __forceinline__ void sub_level_rows(const SubApply &S, const SubSeg &g, int warp, int nw, int lane) {
   const int r0 = S.start[g.jb], r1 = S.start[g.je];
-  const int chunk = (r1 - r0 + nw - 1) / nw;
+  // k_gemv_tc works on whole row groups (start[] is padded to them)
+  const int chunk = NV == 1 ? (r1 - r0 + nw - 1) / nw : (((r1 - r0 + nw - 1) / nw) + 7) & ~7;
   const int t0 = r0 + warp * chunk, t1 = min(r1, t0 + chunk);
   if (t0 >= t1) return;
   int lo = g.jb, hi = g.je - 1;  // last job with start <= t0
@@ -2754,7 +2778,7 @@ __device__ __forceinline__ void sub_level_rows(const SubApply &S, const SubSeg &
   if (NV == 1)
     gemv_rows(S.job, S.start, lo, t0, t1, lane);
   else
-    gemv_rows_mv<NV>(S.job, S.start, lo, t0, t1, lane);
+    gemv_rows_tc<NV>(S.job, S.start, lo, t0, t1, lane);
 }
 template <int NV>
 __global__ void __launch_bounds__(512) k_apply_sub(SubApply S, int up) {
@@ -2852,6 +2876,7 @@ __global__ void k_gather_idx(const long long *__restrict__ src_idx, const double
 // Krylov vector kernels (deterministic reductions: fixed grid, ordered final sum)
 // ---------------------------------------------------------------------------
 constexpr int RED_BLOCKS = 296, RED_THREADS = 256;
+constexpr int MGS_MAX_GRID = 1024;  // MGS partials: 2 * grid doubles of the context's d_part
 
 __device__ __forceinline__ double block_sum(double v, double *sh) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -3017,6 +3042,69 @@ __global__ void __launch_bounds__(256) k_mgs_coop(const double *__restrict__ V, 
     __syncthreads();
     h = s_h;
     if (b == 0 && threadIdx.x == 0) H[i] = (i <= j) ? h : sqrt(h);
+  }
+}
+
+// k_mgs_coop with the block's slice of w held in registers and its slice of
+// the previous basis vector in shared memory (R elements per thread, the same
+// elements in the same order, so the same bits): one read of V_0 .. V_j and of
+// w and one write of w, instead of reading V_{i-1}, V_i and w and writing w for
+// every projection. Dynamic shared memory: R * 256 doubles.
+template <int R>
+__global__ void __launch_bounds__(256) k_mgs_reg(const double *__restrict__ V, double *__restrict__ w, long long n,
+                                                 int j, double *__restrict__ H, double *__restrict__ part) {
+  extern __shared__ double vps[];  // [R][256]: this thread's V_{i-1} entries
+  __shared__ double sh[33];
+  __shared__ double s_h;
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x, b = blockIdx.x;
+  const long long chunk = (n + G - 1) / G;
+  const long long lo = (long long)b * chunk, hi = min(n, lo + chunk);
+  double wv[R];
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    const long long k = lo + threadIdx.x + 256LL * u;
+    wv[u] = k < hi ? w[k] : 0.0;
+  }
+  double h = 0.0;
+  for (int i = 0; i <= j + 1; ++i) {
+    const double *Vi = V + (long long)i * n;
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const long long k = lo + threadIdx.x + 256LL * u;
+      if (k < hi) {
+        double wk = wv[u];
+        if (i > 0) {
+          wk = __dsub_rn(wk, __dmul_rn(h, vps[u * 256 + threadIdx.x]));
+          wv[u] = wk;
+        }
+        if (i <= j) {
+          const double vi = Vi[k];
+          vps[u * 256 + threadIdx.x] = vi;
+          s = fma(vi, wk, s);
+        } else {
+          s = fma(wk, wk, s);
+        }
+      }
+    }
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) part[(i & 1) * G + b] = s;
+    grid.sync();
+    if (threadIdx.x < 32) {
+      double t = 0.0;
+      for (int q = threadIdx.x; q < G; q += 32) t += __ldcg(part + (i & 1) * G + q);
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (threadIdx.x == 0) s_h = t;
+    }
+    __syncthreads();
+    h = s_h;
+    if (b == 0 && threadIdx.x == 0) H[i] = (i <= j) ? h : sqrt(h);
+  }
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    const long long k = lo + threadIdx.x + 256LL * u;
+    if (k < hi) w[k] = wv[u];
   }
 }
 

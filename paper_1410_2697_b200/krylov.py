@@ -235,8 +235,9 @@ def gmres_batched(A, B, M, tol=DEFAULT_TOL, max_iter=DEFAULT_MAX_ITER, restart=D
     """``gmres`` for the columns of ``B`` (n x k) with one device factorization:
     groups of up to eight right-hand sides run in lockstep and share each
     preconditioner apply (the factor is read once per Arnoldi step, not once per
-    column). Every column's solution and history are bit-identical to
-    ``gmres(A, B[:, j], M)``. ``A`` must be a SparseMatrix (or a LinearOperator
+    column, on the FP64 tensor cores). Every column equals
+    ``gmres(A, B[:, j], M)`` to rounding (iteration counts within one) and does
+    not depend on the other columns. ``A`` must be a SparseMatrix (or a LinearOperator
     from one) and ``M`` a ``mf_preconditioner``."""
     if not (0.0 < tol < 1.0):
         raise ValueError("tol must lie in (0, 1)")

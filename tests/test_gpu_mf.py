@@ -88,15 +88,17 @@ def test_multiple_rhs_and_zero_rhs():
     F = P.mf_factorize(A, et, P.ACCELERATED, P.MfParams(n_c=40, eps=1e-3, n_leaf=16))
     B = np.random.default_rng(0).standard_normal((A.n_rows, 3))
     X = P.mf_solve(F, B)
-    for j in range(3):
-        np.testing.assert_array_equal(X[:, j], P.mf_solve(F, B[:, j]))
+    for j in range(3):  # several vectors: tensor-core apply; one vector: warp per row
+        x = P.mf_solve(F, B[:, j])
+        np.testing.assert_allclose(X[:, j], x, rtol=0, atol=1e-12 * np.abs(x).max())
     np.testing.assert_array_equal(P.mf_solve(F, np.zeros(A.n_rows)), np.zeros(A.n_rows))
 
 
-def test_batched_rhs_bitwise_equal_to_single():
+def test_batched_rhs_independent_of_group():
     """Up to eight right-hand sides share one graph replay (the factor is read
-    once per group): every column is bit-identical to its single-vector apply,
-    across a group boundary (11 = 8 + 3) and with structured fronts."""
+    once per group, on the FP64 tensor cores): a column is bitwise the same in
+    any group width (11 = 8 + 3 against pairs), and equals its one-vector
+    apply to rounding; with structured fronts."""
     import paper_1410_2697_b200 as P
     A, _ = P.gen_poisson7(14, 13, 12)
     et = P.build_elimination_tree(P.nested_dissection(P.adjacency_graph(A), 32), A)
@@ -104,8 +106,11 @@ def test_batched_rhs_bitwise_equal_to_single():
     assert F.stats.n_blocks > 0
     B = np.random.default_rng(3).standard_normal((A.n_rows, 11))
     X = P.mf_solve(F, B)
+    for j in range(0, 10, 2):
+        np.testing.assert_array_equal(X[:, j:j + 2], P.mf_solve(F, B[:, j:j + 2]))
     for j in range(11):
-        np.testing.assert_array_equal(X[:, j], P.mf_solve(F, B[:, j]))
+        x = P.mf_solve(F, B[:, j])
+        np.testing.assert_allclose(X[:, j], x, rtol=0, atol=1e-12 * np.abs(x).max())
 
 
 def test_errors():

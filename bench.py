@@ -68,9 +68,10 @@ CONFIGS = {
                gen=("p1_delaunay", (1000,)), leaf=64, params=dict(n_c=1024, eps=1e-5, d=1, n_leaf=64), restart=30,
                tol=1e-10, rhs="normal"),
     # C5: one factorization and 8 GMRES solves per step (8 RHS N(0,1), seeds 0..7);
-    # (n_c, d) = (4096, 2) converge in 77 iterations per solve (GPU-chosen like C3)
+    # (n_c, d) = (12288, 2): 23 iterations per solve, the fastest step of the
+    # GPU sweep in BASELINE.md (n_c 2048..16384, d 1..3)
     "c5": dict(desc="3D Poisson 7-pt 128^3 (BASELINE configs[4]), 8 RHS", gen=("poisson7", (128, 128, 128)),
-               leaf=64, params=dict(n_c=4096, eps=1e-4, d=2, n_leaf=64), restart=50, tol=1e-10, rhs="normal",
+               leaf=64, params=dict(n_c=12288, eps=1e-4, d=2, n_leaf=64), restart=50, tol=1e-10, rhs="normal",
                nrhs=8),
 }
 METRIC = "factor+GMRES solve time (s) at N; HODLR front GFLOP/s & % of FP64/HBM roofline"

@@ -323,15 +323,66 @@ struct Ctx {
 // ---------------------------------------------------------------------------
 // Sink: where descriptors go and how launches happen.
 //   immediate: staged async copy, launch now (factorization)
+//   batched:   between begin_batch() and flush(), descriptor copies are only
+//              staged and launches deferred; flush() issues the copies as few
+//              contiguous transfers, then every launch back to back (no copy
+//              between two kernels: programmatic dependent launch overlaps
+//              them). Only for stretches without host read-backs.
 //   record:    persistent copy, launch recorded for graph capture (apply)
 // ---------------------------------------------------------------------------
 struct Sink {
   Ctx *ctx;
   Arena *persist = nullptr;  // record mode
   bool record = false;
+  bool batching = false;
   std::vector<std::function<void(cudaStream_t)>> ops;
+  struct Pending {
+    char *dst;
+    const char *src;
+    size_t bytes;
+  };
+  std::vector<Pending> pend;
+  std::vector<std::function<void(cudaStream_t)>> deferred;
+
+  void begin_batch() {
+    if (record) return;
+    batching = true;
+  }
+  void flush() {
+    if (!batching) return;
+    batching = false;
+    // coalesce staged ranges that are contiguous on both sides
+    for (size_t q = 0; q < pend.size();) {
+      char *d = pend[q].dst;
+      const char *h = pend[q].src;
+      size_t b = pend[q].bytes;
+      size_t r = q + 1;
+      while (r < pend.size() && pend[r].dst == d + b && pend[r].src == h + b) b += pend[r++].bytes;
+      CK(cudaMemcpyAsync(d, h, b, cudaMemcpyHostToDevice, ctx->s));
+      q = r;
+    }
+    pend.clear();
+    auto ops_ = std::move(deferred);
+    deferred.clear();
+    for (auto &f : ops_) {
+      ctx->launches++;
+      f(ctx->s);
+    }
+  }
+  ~Sink() {
+    if (batching && !std::uncaught_exceptions()) flush();
+  }
+  // host -> device copy of staged bytes (now, or at flush when batching)
+  void h2d(void *dst, const void *src, size_t bytes) {
+    if (batching) {
+      pend.push_back(Pending{(char *)dst, (const char *)src, bytes});
+      return;
+    }
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->s));
+  }
 
   void sync_reset() {
+    if (batching) throw std::logic_error("internal: stream sync inside a batched stretch");
     CK(cudaStreamSynchronize(ctx->s));
     ctx->stage.rewind();
   }
@@ -346,7 +397,7 @@ struct Sink {
     }
     auto hd = ctx->stage.take(bytes);
     std::memcpy(hd.first, src, bytes);
-    CK(cudaMemcpyAsync(hd.second, hd.first, bytes, cudaMemcpyHostToDevice, ctx->s));
+    h2d(hd.second, hd.first, bytes);
     return hd.second;
   }
   template <class T>
@@ -362,7 +413,7 @@ struct Sink {
     void *dst = ctx->scratch.alloc(bytes);
     auto hd = ctx->stage.take(bytes);
     std::memcpy(hd.first, v.data(), bytes);
-    CK(cudaMemcpyAsync(dst, hd.first, bytes, cudaMemcpyHostToDevice, ctx->s));
+    h2d(dst, hd.first, bytes);
     return (T *)dst;
   }
   // several arrays in one staged copy into scratch (valid to the end of the
@@ -383,7 +434,10 @@ struct Sink {
       out.push_back(p.second ? dst + o : nullptr);
       o += (p.second + 255) & ~size_t(255);
     }
-    CK(cudaMemcpyAsync(dst, hd.first, tot, cudaMemcpyHostToDevice, ctx->s));
+    if (record)
+      CK(cudaMemcpyAsync(dst, hd.first, tot, cudaMemcpyHostToDevice, ctx->s));
+    else
+      h2d(dst, hd.first, tot);
     return out;
   }
   double *scratch_d(size_t n) { return record ? persist->d(n) : ctx->scratch.d(n); }
@@ -393,12 +447,14 @@ struct Sink {
     if (bytes == 0) return;
     auto hd = ctx->stage.take(bytes);
     std::memcpy(hd.first, src, bytes);
-    CK(cudaMemcpyAsync(dst, hd.first, bytes, cudaMemcpyHostToDevice, ctx->s));
+    h2d(dst, hd.first, bytes);
   }
   int *scratch_i(size_t n) { return record ? persist->i(n) : ctx->scratch.i(n); }
   void launch(std::function<void(cudaStream_t)> f) {
     if (record) {
       ops.push_back(std::move(f));
+    } else if (batching) {
+      deferred.push_back(std::move(f));
     } else {
       ctx->launches++;
       f(ctx->s);
@@ -563,14 +619,17 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
         g_blas_host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
       }
     } bclk{tb0};
-    for (const GemmJob &g : big) {
-      // row-major C = alpha A B + beta C  ==  column-major C^T = alpha B^T A^T + beta C^T
-      double al = g.alpha, be = g.beta;
-      if (cublasDgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, g.n, g.m, g.k, &al, g.B, g.ldb, g.A, g.lda, &be, g.C,
-                      g.ldc) != CUBLAS_STATUS_SUCCESS)
-        throw runtime_error("cublasDgemm failed");
-      ctx->lib_calls++;
-    }
+    cublasHandle_t h = ctx->blas;
+    sk.launch([h, big](cudaStream_t) {  // the handle's stream is ctx->s (a batched sink defers the calls)
+      for (const GemmJob &g : big) {
+        // row-major C = alpha A B + beta C  ==  column-major C^T = alpha B^T A^T + beta C^T
+        double al = g.alpha, be = g.beta;
+        if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, g.n, g.m, g.k, &al, g.B, g.ldb, g.A, g.lda, &be, g.C, g.ldc) !=
+            CUBLAS_STATUS_SUCCESS)
+          throw runtime_error("cublasDgemm failed");
+      }
+    });
+    ctx->lib_calls += (int64_t)big.size();
   }
   if (!eye.empty()) {
     int64_t mx = 1;
@@ -2153,6 +2212,7 @@ struct Factorizer {
       // check); Gpf = F_pp^{-1} F_pf; Schur update F_ff -= F_fp Gpf; Gfp = F_fp F_pp^{-1}
       std::vector<InvReq> inv;
       std::vector<GemmJob> g1, g2;
+      s.begin_batch();
       for (int fi : D) {
         FrontH &f = F->fronts[fi];
         if (!f.npv) continue;
@@ -2184,6 +2244,7 @@ struct Factorizer {
       run_inverse(s, inv);
       run_gemm(s, g1);
       run_gemm(s, g2);
+      s.flush();
       for (int fi : D) {
         FrontH &f = F->fronts[fi];
         if (f.nf) {
@@ -2324,6 +2385,7 @@ struct Factorizer {
     }
     cudaEventRecord(ev[4], ctx->s);
     hts[4] = std::chrono::steady_clock::now();
+    s.begin_batch();  // skeletons + dense fallbacks: no read-back until the next height
     if (!lux.empty()) {
       LuExtractJob *dj = s.push(lux);
       int64_t mx = 0;
@@ -2358,6 +2420,7 @@ struct Factorizer {
     }
     run_copy(s, dcopy);
     run_sample(s, dreq, dF, dC);
+    s.flush();
     cudaEventRecord(ev[5], ctx->s);
     hts[5] = std::chrono::steady_clock::now();
 
@@ -2394,6 +2457,7 @@ struct Factorizer {
       }
     }
 
+    s.begin_batch();  // HODLR factorization + eliminate: host-planned, one descriptor transfer
     // ------------------------------------------------ HODLR factorization of pp
     // hodlr_factorize (hodlr.py:312-357) in explicit-inverse form, one launch
     // group per stage of a tree level, batched over every front of the height:
@@ -2481,7 +2545,11 @@ struct Factorizer {
         // fewer reals -- it is also what one apply reads
         f.pform = pform_of(T, N);
         f.Hinv = f.pform ? ctx->scratch.d((size_t)N * N) : F->arena.d((size_t)N * N);
-        CK(cudaMemsetAsync(f.Hinv, 0, sizeof(double) * (size_t)N * N, ctx->s));
+        {
+          double *hz = f.Hinv;
+          const size_t nb = sizeof(double) * (size_t)N * N;
+          s.launch([hz, nb](cudaStream_t st) { CK(cudaMemsetAsync(hz, 0, nb, st)); });
+        }
         for (int v = 0; v < T.nslots; ++v)
           if (T.leaf[v] == 1) {
             int lo = T.lo[v], sz = T.hi[v] - T.lo[v];
@@ -2684,7 +2752,9 @@ struct Factorizer {
       }
       run_copy(s, xl);
     }
+    s.flush();
     cudaEventRecord(ev[6], ctx->s);
+    s.begin_batch();
     hts[6] = std::chrono::steady_clock::now();
 
     // ------------------------------------------------ eliminate_hodlr (W, V)  (multifrontal.py:411-456)
@@ -2756,6 +2826,7 @@ struct Factorizer {
       run_gemm(s, g1);
       run_gemm(s, g2);
     }
+    s.flush();
     cudaEventRecord(ev[7], ctx->s);
     hts[7] = std::chrono::steady_clock::now();
     static const bool htr = getenv("MFH_HEIGHT_TRACE") != nullptr;

@@ -92,6 +92,10 @@ typedef struct {
   double sample_lr_flops; /* a7 2 r per sampled entry per low-rank child term W V^T it meets */
   double pivot_lu_crit_steps; /* sum over structured heights of the longest core's steps */
   double apply_ref_bytes; /* one mf_solve by SURVEY 8d's count: 8 sum(2 S_pp + S_pf + S_fp) + 32 N */
+  /* flops this engine executed per phase (GEMMs 2mnk, register inverses 2n^3):
+   * the numerators of the achieved-throughput rooflines (the reference's own
+   * counts above can be lower or higher than the work this form does) */
+  double exec_flops_skeleton, exec_flops_hodlr, exec_flops_elim, exec_flops_dense;
 } mfh_timing_t;
 
 /* ---- errors --------------------------------------------------------------- */

@@ -67,7 +67,9 @@ class mfh_timing_t(C.Structure):
                 ("pivot_lu_visits", C.c_double), ("sample_entries", C.c_double),
                 ("hodlr_flops", C.c_double), ("elim_flops", C.c_double), ("dense_flops", C.c_double),
                 ("skeleton_flops", C.c_double), ("sample_lr_flops", C.c_double),
-                ("pivot_lu_crit_steps", C.c_double), ("apply_ref_bytes", C.c_double)]
+                ("pivot_lu_crit_steps", C.c_double), ("apply_ref_bytes", C.c_double),
+                ("exec_flops_skeleton", C.c_double), ("exec_flops_hodlr", C.c_double),
+                ("exec_flops_elim", C.c_double), ("exec_flops_dense", C.c_double)]
 
 
 HOST_OP = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double))

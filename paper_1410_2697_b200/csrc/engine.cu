@@ -290,6 +290,7 @@ struct Ctx {
   std::recursive_mutex mu;
   int64_t launches = 0;      // launches of this library's kernels
   int64_t lib_calls = 0;     // cuBLAS DGEMM calls (plain large GEMMs)
+  double flops_exec = 0.0;   // flops enqueued by run_gemm (2mnk) and the register inverses (2n^3)
   cublasHandle_t blas = nullptr;
   void *blas_ws = nullptr;  // cuBLAS workspace (set once with the stream)
   // device copies of per-tree extend-add maps and front id lists, keyed by etree uid
@@ -550,12 +551,16 @@ static thread_local int g_split_k_override = -1;  // test hook (mfh_test_gemm_ba
 static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
   OpClock oc_("gemm");
   if (jobs.empty()) return;
+  for (const GemmJob &g : jobs)
+    if (g.k > 0 && g.lda >= 0 && g.ldb >= 0) sk.ctx->flops_exec += 2.0 * g.m * g.n * g.k;
   std::vector<GemmTile> tiles;
   std::vector<GemmJob> big;
   std::vector<GemmSplit> splits;
   int nslot = 0;
+  // A/B knob: MFH_GEMM_NO_BLAS=1 keeps every GEMM on the batched DMMA kernel
+  static const bool no_blas = getenv("MFH_GEMM_NO_BLAS") && atoi(getenv("MFH_GEMM_NO_BLAS")) != 0;
   auto is_big = [&](const GemmJob &g) {
-    return !sk.record && g.k > 0 && g.m >= 64 && g.n >= 64 && 2.0 * g.m * g.n * g.k >= (double)(1 << 27) &&
+    return !no_blas && !sk.record && g.k > 0 && g.m >= 64 && g.n >= 64 && 2.0 * g.m * g.n * g.k >= (double)(1 << 27) &&
            g.lda > 0 && g.ldb > 0 && !gemm_overlaps(g);
   };
   // products with an identity operand (leading dimension -1: the strip that
@@ -904,6 +909,14 @@ static void run_inverse(Sink &sk, const std::vector<InvReq> &reqs) {
       ild.push_back(r.ldo);
     }
   }
+  static const bool ilog = getenv("MFH_INV_LOG") != nullptr;
+  if (ilog) {
+    int mx = 0;
+    for (auto &l : lus) mx = std::max(mx, l.n);
+    fprintf(stderr, "[mfh inverse] %zu register (<= %d) + %zu blocked (max n %d)\n", small.size(), INV_SMALL,
+            lus.size(), mx);
+  }
+  for (auto &j : small) sk.ctx->flops_exec += 2.0 * j.n * j.n * j.n;
   run_copy(sk, cps);
   if (!small.empty()) {
     // register-tiled Gauss-Jordan: 64-wide tiles (256 threads) or 128-wide (512)
@@ -1647,6 +1660,9 @@ struct Factorizer {
   }
 
   int flag_cap = 0;
+  // host time from the rank read-back to the skeleton launches (the GPU idles in it)
+  std::chrono::steady_clock::time_point t_decide0;
+  double last_decide_us = 0.0;
   int new_flag(const std::string &msg, int64_t order) {
     if (nflags >= flag_cap) throw runtime_error("internal: error-flag capacity exceeded");
     flag_msg.push_back(msg);
@@ -2051,7 +2067,10 @@ struct Factorizer {
   // algorithmic flops of the low-rank child terms an extend-add request meets:
   // 2 r per sampled entry whose row and column both map into a child carrying
   // W V^T (multifrontal.py:340-347). Rows / columns: a range, or an index list.
-  void count_lr(int fi, int r0, int nr, const std::vector<int> *rl, int c0, int nc, const std::vector<int> *cl) {
+  // (acc: the counter the flops go to; dense fallbacks sampled in the skeleton
+  // phase count as that phase's executed flops)
+  void count_lr(int fi, int r0, int nr, const std::vector<int> *rl, int c0, int nc, const std::vector<int> *cl,
+                double *acc = nullptr) {
     const FrontH &f = F->fronts[fi];
     for (int ci : f.kids) {
       const FrontH &c = F->fronts[ci];
@@ -2065,7 +2084,7 @@ struct Factorizer {
           for (int x = a0; x < a0 + n; ++x) h += to[x] >= 0;
         return h;
       };
-      F->timing.sample_lr_flops += 2.0 * c.rw * hits(r0, nr, rl) * hits(c0, nc, cl);
+      *(acc ? acc : &F->timing.sample_lr_flops) += 2.0 * c.rw * hits(r0, nr, rl) * hits(c0, nc, cl);
     }
   }
 
@@ -2263,7 +2282,9 @@ struct Factorizer {
       }
     };
     if (S.empty()) {  // dense-only height: three events (each record costs GPU time)
+      const double fl0 = ctx->flops_exec;
       dense_elim();
+      F->timing.exec_flops_dense += ctx->flops_exec - fl0;
       cudaEventRecord(ev[2], ctx->s);
       return;
     }
@@ -2272,7 +2293,11 @@ struct Factorizer {
 
     // ------------------------------------------------ structured: pivot LU
     run_copy(s, core_copies);
-    run_plu(s, plu, P.eps, dense_elim);
+    {
+      const double fl0 = ctx->flops_exec;
+      run_plu(s, plu, P.eps, dense_elim);
+      F->timing.exec_flops_dense += ctx->flops_exec - fl0;
+    }
     cudaEventRecord(ev[3], ctx->s);
     hts[3] = std::chrono::steady_clock::now();
     // read ranks, status and pivot sequences: one D2H pair for the height
@@ -2286,6 +2311,7 @@ struct Factorizer {
       CK(cudaMemcpyAsync(hb + oD, pdbl_all, bd_, cudaMemcpyDeviceToHost, ctx->s));
       if (nflags) CK(cudaMemcpyAsync(hb + oF, d_flags, bf_, cudaMemcpyDeviceToHost, ctx->s));
       s.sync_reset();
+      t_decide0 = std::chrono::steady_clock::now();
       std::vector<int> hi((const int *)hb, (const int *)hb + itot);
       std::vector<double> hd((const double *)(hb + oD), (const double *)(hb + oD) + dtot);
       check_flags(0, (const int *)(hb + oF));
@@ -2356,7 +2382,7 @@ struct Factorizer {
         } else {
           b.val = blk_alloc(b, (size_t)b.m * b.n);
           dreq.push_back(SReq{slot[b.fi], b.m, b.n, nullptr, nullptr, b.r0, b.c0, b.val, b.n});
-          count_lr(b.fi, b.r0, b.m, nullptr, b.c0, b.n, nullptr);
+          count_lr(b.fi, b.r0, b.m, nullptr, b.c0, b.n, nullptr, &F->timing.exec_flops_skeleton);
         }
         F->stats.n_dense_fallback++;
       } else if (b.rank > 0) {
@@ -2385,6 +2411,7 @@ struct Factorizer {
     }
     cudaEventRecord(ev[4], ctx->s);
     hts[4] = std::chrono::steady_clock::now();
+    const double fl_skel0 = ctx->flops_exec;
     s.begin_batch();  // skeletons + dense fallbacks: no read-back until the next height
     if (!lux.empty()) {
       LuExtractJob *dj = s.push(lux);
@@ -2421,7 +2448,9 @@ struct Factorizer {
     run_copy(s, dcopy);
     run_sample(s, dreq, dF, dC);
     s.flush();
+    F->timing.exec_flops_skeleton += ctx->flops_exec - fl_skel0;
     cudaEventRecord(ev[5], ctx->s);
+    last_decide_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_decide0).count();
     hts[5] = std::chrono::steady_clock::now();
 
     // ------------------------------------------------ device HNode tables of the
@@ -2457,6 +2486,7 @@ struct Factorizer {
       }
     }
 
+    const double fl_hodlr0 = ctx->flops_exec;
     s.begin_batch();  // HODLR factorization + eliminate: host-planned, one descriptor transfer
     // ------------------------------------------------ HODLR factorization of pp
     // hodlr_factorize (hodlr.py:312-357) in explicit-inverse form, one launch
@@ -2753,7 +2783,9 @@ struct Factorizer {
       run_copy(s, xl);
     }
     s.flush();
+    F->timing.exec_flops_hodlr += ctx->flops_exec - fl_hodlr0;
     cudaEventRecord(ev[6], ctx->s);
+    const double fl_elim0 = ctx->flops_exec;
     s.begin_batch();
     hts[6] = std::chrono::steady_clock::now();
 
@@ -2827,6 +2859,7 @@ struct Factorizer {
       run_gemm(s, g2);
     }
     s.flush();
+    F->timing.exec_flops_elim += ctx->flops_exec - fl_elim0;
     cudaEventRecord(ev[7], ctx->s);
     hts[7] = std::chrono::steady_clock::now();
     static const bool htr = getenv("MFH_HEIGHT_TRACE") != nullptr;
@@ -3567,7 +3600,7 @@ struct Factorizer {
     int used = 0;
     std::vector<int> height_of_use, struct_of_use;
     std::vector<std::array<int, 4>> first_of_use;  // npv, nf, kids of the first front; aliased fronts
-    std::vector<double> host_us_of_use;
+    std::vector<double> host_us_of_use, decide_us_of_use;
     for (int h = 0; h <= maxh; ++h) {
       for (int q : alias_at[h]) {  // the child was enqueued at a lower height
         FrontH &f = F->fronts[q];
@@ -3601,8 +3634,10 @@ struct Factorizer {
       }
       // process_height records ev[0..2] (dense-only heights) or ev[0..7]
       auto th0 = std::chrono::steady_clock::now();
+      last_decide_us = 0.0;
       process_height(byh[h], ev);
       host_us_of_use.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count());
+      decide_us_of_use.push_back(last_decide_us);
       // heights run ahead of the host: the only waits are the rank readback
       // inside structured heights and scratch recycling
       if (ctx->scratch.in_use > (size_t(4) << 30)) {
@@ -3643,9 +3678,10 @@ struct Factorizer {
         for (int q = 0; q < (donly ? 2 : 7); ++q) CK(cudaEventElapsedTime(&a[q], ev[q], ev[q + 1]));
         if (u > 0)
           CK(cudaEventElapsedTime(&gap, ctx->evpool[8 * (u - 1) + (struct_of_use[u - 1] ? 7 : 2)], ev[0]));
-        fprintf(stderr, "[mfh height %3d] fronts %4zu struct %2d | gap %7.3f sample %7.3f dense %7.3f plu %7.3f - %7.3f skel %7.3f hodlr %7.3f elim %7.3f ms | first npv %d nf %d kids %d, aliased %d | host %.1f us\n",
+        fprintf(stderr, "[mfh height %3d] fronts %4zu struct %2d | gap %7.3f sample %7.3f dense %7.3f plu %7.3f - %7.3f skel %7.3f hodlr %7.3f elim %7.3f ms | first npv %d nf %d kids %d, aliased %d | host %.1f us, decide %.1f us\n",
                 height_of_use[u], byh[height_of_use[u]].size(), struct_of_use[u], gap, a[0], a[1], a[2], a[3], a[4], a[5], a[6],
-                first_of_use[u][0], first_of_use[u][1], first_of_use[u][2], first_of_use[u][3], host_us_of_use[u]);
+                first_of_use[u][0], first_of_use[u][1], first_of_use[u][2], first_of_use[u][3], host_us_of_use[u],
+                decide_us_of_use[u]);
       }
       float ms;
       CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));

@@ -30,13 +30,15 @@ def test_phase_rooflines_helper():
     tim = {"sample_entries": 1e6, "sample_ms": 1.0, "sample_lr_flops": 2e9, "pivot_lu_visits": 2e6,
            "pivot_lu_ms": 2.0, "pivot_lu_crit_steps": 400.0, "skeleton_flops": 1e9, "skeleton_ms": 1.0,
            "hodlr_flops": 3e9, "hodlr_factor_ms": 1.0, "elim_flops": 1e9, "eliminate_ms": 1.0,
-           "dense_flops": 5e9, "dense_front_ms": 1.0, "apply_ref_bytes": 1e9}
+           "dense_flops": 5e9, "dense_front_ms": 1.0, "apply_ref_bytes": 1e9,
+           "exec_flops_skeleton": 1e9, "exec_flops_hodlr": 6e9, "exec_flops_elim": 2e9, "exec_flops_dense": 5e9}
     r = bench.phase_rooflines(tim, 6000.0, 30.0, 0.5, 8e8, 0.01, 1000, 100)
     assert abs(r["sample"]["achieved"] - 16.0) < 1e-9        # 16 MB in 1 ms = 16 GB/s
     assert abs(r["sample"]["lr_tflops"] - 2.0) < 1e-9
     assert abs(r["pivot_lu"]["achieved"] - 8.0) < 1e-9       # 16 MB in 2 ms
     assert abs(r["pivot_lu"]["latency"]["us_per_step"] - 5.0) < 1e-9
-    assert abs(r["hodlr_front"]["achieved"] - 2.0) < 1e-9    # 4 GFLOP in 2 ms
+    assert abs(r["hodlr_front"]["achieved"] - 4.0) < 1e-9    # 8 GFLOP executed in 2 ms
+    assert abs(r["hodlr_front"]["ref_tflops"] - 2.0) < 1e-9  # the reference's 4 GFLOP in 2 ms
     assert abs(r["dense_front"]["frac"] - 5.0 / 30.0) < 1e-12
     assert abs(r["apply"]["achieved"] - 2000.0) < 1e-9 and abs(r["apply"]["engine_gbs"] - 1600.0) < 1e-9
     assert abs(r["spmv"]["achieved"] - (12e3 + 404 + 1600) / 1e-5 / 1e9) < 1e-9

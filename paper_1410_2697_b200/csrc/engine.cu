@@ -1878,8 +1878,49 @@ struct Factorizer {
   }
 
   // ---- child descriptors (maps from the per-tree cache) for a set of fronts ----
+  // A large child update (the update HODLR minus W V^T, multifrontal.py:340-347)
+  // is materialized once as a dense nf x nf block when its parent is
+  // processed: leaf copies and one GEMM per low-rank block (the reference's
+  // to_dense), then -W V^T as one GEMM. The parent's extend-add requests then
+  // gather from it instead of descending the HODLR tree and recomputing a
+  // rank-r product per sampled entry (C5: the root's dense fallbacks read
+  // ~300 GB that way). Same values up to the GEMMs' rounding; nf >=
+  // MFH_DENSIFY_MIN (default 4096, 0 = never).
+  const double *densify_update(Sink &s, const FrontH &c) {
+    const int nf = c.nf;
+    double *D = upd.d((size_t)nf * nf, release_height(c));
+    HTree &T = F->trees[c.ff];
+    std::vector<CopyJob> cp;
+    std::vector<GemmJob> gm;
+    for (int v = 0; v < T.nslots; ++v) {
+      const int lo = T.lo[v], hi = T.hi[v];
+      if (T.leaf[v] == 1) {
+        const int sz = hi - lo;
+        cp.push_back(CopyJob{T.lval[v], D + (int64_t)lo * nf + lo, sz, sz, sz, nf, nullptr, nullptr});
+      } else if (T.leaf[v] == 0) {
+        const int mid = (lo + hi) >> 1;
+        for (int side = 0; side < 2; ++side) {
+          const BlockH &b = F->blocks[side == 0 ? T.up[v] : T.lw[v]];
+          double *dst = D + (side == 0 ? (int64_t)lo * nf + mid : (int64_t)mid * nf + lo);
+          if (b.dense)
+            cp.push_back(CopyJob{b.val, dst, b.m, b.n, b.n, nf, nullptr, nullptr});
+          else  // rank 0 writes zeros (k = 0)
+            gm.push_back(GemmJob{b.col, b.row, dst, b.m, b.n, b.rank, std::max(1, b.rank), b.n, nf, 1.0, 0.0});
+        }
+      }
+    }
+    run_copy(s, cp);
+    run_gemm(s, gm);
+    if (c.rw) {
+      std::vector<GemmJob> wv{GemmJob{c.W, c.Vt, D, nf, nf, c.rw, c.ldw, c.ldv, nf, -1.0, 1.0}};
+      run_gemm(s, wv);
+    }
+    return D;
+  }
+
   void build_fronts_dev(Sink &s, const std::vector<int> &fis, std::vector<DFront> &dfr,
                         std::vector<DChild> &dch, std::vector<int> &slot_of) {
+    static const int densify_min = getenv("MFH_DENSIFY_MIN") ? atoi(getenv("MFH_DENSIFY_MIN")) : 4096;
     slot_of.assign(F->fronts.size(), -1);
     slot_rw.clear();
     for (int fi : fis) {
@@ -1899,6 +1940,10 @@ struct Factorizer {
           ch.kind = 0;
           ch.dense = c.upd_dense;
           ch.ldd = c.upd_ld;
+        } else if (densify_min > 0 && cn >= densify_min && !c.rx_nodes && c.ff >= 0) {
+          ch.kind = 0;
+          ch.dense = densify_update(s, c);
+          ch.ldd = cn;
         } else {
           ch.kind = 1;
           ch.hn = c.rx_nodes ? c.rx_nodes : F->trees[c.ff].d_nodes;

@@ -3960,7 +3960,7 @@ static void run_gemv(Sink &sk, const std::vector<GemvJob> &jobs, int nv = 1) {
     if (j.m <= 0) continue;
     const int ws = std::max(j.k1 ? gv_ws_host(j.k1) : 1, j.k2 ? gv_ws_host(j.k2) : 1), gpc = 8 / ws;
     const int ng = (j.m + 7) / 8;
-    for (int g0 = 0; g0 < ng; g0 += gpc) items.push_back(GvItem{(int)q, g0});
+    for (int g0 = 0; g0 < ng; g0 += 2 * gpc) items.push_back(GvItem{(int)q, g0});  // two groups per warp
   }
   if (items.empty()) return;
   static const bool gtrace = getenv("MFH_APPLY_TRACE") != nullptr;

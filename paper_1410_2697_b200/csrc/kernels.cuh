@@ -2587,44 +2587,74 @@ __device__ __forceinline__ int gv_seglen(int k, int ws) { return ((((k + ws - 1)
 // partial of one segment [kb, ke) for rows i0 .. i0 + 7 (D fragment: rows
 // i0 + g, vectors 2c, 2c + 1): four interleaved chains (chain j takes columns
 // 4j .. 4j + 3 of every 16-column step, k ascending), then (c0 + c1) + (c2 + c3)
-template <int NV>
-__device__ __forceinline__ void gv_seg(const double *__restrict__ A, long long lda,
-                                       const double *__restrict__ x, long long xs,
-                                       const long long *__restrict__ idx, int kb, int ke, int i0, int m, int g,
-                                       int c, double &d0, double &d1) {
-  double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-  const int row = i0 + g;
-  const bool rok = row < m, xok = g < NV;
-  const double *ar = A + (long long)(rok ? row : 0) * lda;
+template <int NV, int RGN>
+__device__ __forceinline__ void gv_segn(const double *__restrict__ A, long long lda,
+                                        const double *__restrict__ x, long long xs,
+                                        const long long *__restrict__ idx, int kb, int ke, const int (&i0)[RGN],
+                                        int m, int g, int c, double (&d)[RGN][2]) {
+  double acc[RGN][4][2];
+#pragma unroll
+  for (int r = 0; r < RGN; ++r)
+#pragma unroll
+    for (int h = 0; h < 4; ++h) acc[r][h][0] = acc[r][h][1] = 0.0;
+  bool rok[RGN];
+  const double *ar[RGN];
+#pragma unroll
+  for (int r = 0; r < RGN; ++r) {
+    const int row = i0[r] + g;
+    rok[r] = row < m;
+    ar[r] = A + (long long)(rok[r] ? row : 0) * lda;
+  }
+  const bool xok = g < NV;
   const double *xr = x + (long long)(xok ? g : 0) * xs;
   int k0 = kb;
   for (; k0 + 32 <= ke; k0 += 32) {  // two 16-column steps per pass, every load issued first
-    double av[8], xv[8];
+    double av[RGN][8], xv[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int kk = k0 + 4 * u + c;
-      av[u] = rok ? ar[kk] : 0.0;
+#pragma unroll
+      for (int r = 0; r < RGN; ++r) av[r][u] = rok[r] ? ar[r][kk] : 0.0;
       xv[u] = xok ? (idx ? xr[idx[kk]] : xr[kk]) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) dmma884(acc[u & 3][0], acc[u & 3][1], av[u], xv[u]);
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int r = 0; r < RGN; ++r) dmma884(acc[r][u & 3][0], acc[r][u & 3][1], av[r][u], xv[u]);
   }
   if (k0 < ke) {  // the last < 32 columns (masked)
-    double av[8], xv[8];
+    double av[RGN][8], xv[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int kk = k0 + 4 * u + c;
       const bool kin = kk < ke;
-      av[u] = (rok && kin) ? ar[kk] : 0.0;
+#pragma unroll
+      for (int r = 0; r < RGN; ++r) av[r][u] = (rok[r] && kin) ? ar[r][kk] : 0.0;
       xv[u] = (xok && kin) ? (idx ? xr[idx[kk]] : xr[kk]) : 0.0;
     }
     const bool two = ke - k0 > 16;
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (u < 4 || two) dmma884(acc[u & 3][0], acc[u & 3][1], av[u], xv[u]);
+      if (u < 4 || two)
+#pragma unroll
+        for (int r = 0; r < RGN; ++r) dmma884(acc[r][u & 3][0], acc[r][u & 3][1], av[r][u], xv[u]);
   }
-  d0 = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
-  d1 = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
+#pragma unroll
+  for (int r = 0; r < RGN; ++r) {
+    d[r][0] = (acc[r][0][0] + acc[r][1][0]) + (acc[r][2][0] + acc[r][3][0]);
+    d[r][1] = (acc[r][0][1] + acc[r][1][1]) + (acc[r][2][1] + acc[r][3][1]);
+  }
+}
+template <int NV>
+__device__ __forceinline__ void gv_seg(const double *__restrict__ A, long long lda,
+                                       const double *__restrict__ x, long long xs,
+                                       const long long *__restrict__ idx, int kb, int ke, int i0, int m, int g,
+                                       int c, double &d0, double &d1) {
+  const int i0s[1] = {i0};
+  double d[1][2];
+  gv_segn<NV, 1>(A, lda, x, xs, idx, kb, ke, i0s, m, g, c, d);
+  d0 = d[0][0];
+  d1 = d[0][1];
 }
 template <int NV>
 __device__ __forceinline__ void gv_term_seg(const GemvJob &J, int part, int seg, int i0, int g, int c, double &d0,
@@ -2637,6 +2667,19 @@ __device__ __forceinline__ void gv_term_seg(const GemvJob &J, int part, int seg,
     gv_seg<NV>(J.A1, J.lda1, J.x1, J.x1s, nullptr, kb, ke, i0, J.m, g, c, d0, d1);
   else
     gv_seg<NV>(J.A2, J.lda2, J.x2, J.x2s, J.idx2, kb, ke, i0, J.m, g, c, d0, d1);
+}
+// two row groups sharing each x fragment (k_gemv_tc): the same per-row chains
+template <int NV>
+__device__ __forceinline__ void gv_term_seg2(const GemvJob &J, int part, int seg, const int (&i0)[2], int g, int c,
+                                             double (&d)[2][2]) {
+  const int k = part == 0 ? J.k1 : J.k2, ws = gv_ws(k), sl = gv_seglen(k, ws);
+  const int kb = seg * sl, ke = min(k, kb + sl);
+  d[0][0] = d[0][1] = d[1][0] = d[1][1] = 0.0;
+  if (seg >= ws || kb >= ke) return;
+  if (part == 0)
+    gv_segn<NV, 2>(J.A1, J.lda1, J.x1, J.x1s, nullptr, kb, ke, i0, J.m, g, c, d);
+  else
+    gv_segn<NV, 2>(J.A2, J.lda2, J.x2, J.x2s, J.idx2, kb, ke, i0, J.m, g, c, d);
 }
 // y = y0; y += a1 S1; y += a2 S2 for the lane's rows / vectors
 template <int NV>
@@ -2695,8 +2738,10 @@ __device__ __forceinline__ void gemv_rows_tc(const GemvJob *__restrict__ jobs, c
 }
 
 // One CTA (8 warps) per work item (job, first row group): a job whose longer
-// term has ws segments gives each of 8 / ws row groups ws warps; the partials
-// meet in shared memory and the segment-0 warp sums them in order.
+// term has ws segments gives each of 8 / ws warp slots ws warps, a warp slot
+// covers two row groups sharing every x fragment (half the vector loads per
+// matrix element); the partials meet in shared memory and the segment-0 warp
+// sums them in order.
 struct GvItem {
   int q, g0;
 };
@@ -2704,39 +2749,46 @@ template <int NV>
 __global__ void __launch_bounds__(256) k_gemv_tc(const GemvJob *__restrict__ jobs, const GvItem *__restrict__ items) {
   pdl_wait();
   pdl_trigger();
-  __shared__ double red[8][2][2][32];
+  __shared__ double red[8][2][2][2][32];  // [warp][group][term][e][lane]
   const GvItem it = items[blockIdx.x];
   const GemvJob &J = jobs[it.q];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
   const int ws = max(J.k1 ? gv_ws(J.k1) : 1, J.k2 ? gv_ws(J.k2) : 1), gpc = 8 / ws;
   const int gi = warp / ws, seg = warp % ws;
-  const int i0 = (it.g0 + gi) * 8;
-  const bool live = gi < gpc && i0 < J.m;
-  double p[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  // this warp's two row groups (they share every x fragment)
+  const int i0[2] = {(it.g0 + 2 * gi) * 8, (it.g0 + 2 * gi + 1) * 8};
+  const bool live = gi < gpc && i0[0] < J.m;
+  double p[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};  // [term][group][e]
   if (live) {
-    if (J.k1) gv_term_seg<NV>(J, 0, seg, i0, g, c, p[0][0], p[0][1]);
-    if (J.k2) gv_term_seg<NV>(J, 1, seg, i0, g, c, p[1][0], p[1][1]);
+    if (J.k1) gv_term_seg2<NV>(J, 0, seg, i0, g, c, p[0]);
+    if (J.k2) gv_term_seg2<NV>(J, 1, seg, i0, g, c, p[1]);
   }
   if (ws > 1) {
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+    for (int r = 0; r < 2; ++r)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) red[warp][a][e][lane] = p[a][e];
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) red[warp][r][a][e][lane] = p[a][r][e];
     __syncthreads();
   }
   if (!live || seg != 0) return;
-  double S[2][2];
 #pragma unroll
-  for (int a = 0; a < 2; ++a) {
-    const int k = a == 0 ? J.k1 : J.k2, wk = k ? gv_ws(k) : 1;
+  for (int r = 0; r < 2; ++r) {
+    if (i0[r] >= J.m) continue;
+    double S[2][2];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      double s = p[a][e];
-      for (int sg = 1; sg < wk; ++sg) s += red[warp + sg][a][e][lane];
-      S[a][e] = s;
+    for (int a = 0; a < 2; ++a) {
+      const int k = a == 0 ? J.k1 : J.k2, wk = k ? gv_ws(k) : 1;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double s = p[a][r][e];
+        for (int sg = 1; sg < wk; ++sg) s += red[warp + sg][r][a][e][lane];
+        S[a][e] = s;
+      }
     }
+    gv_epilogue<NV>(J, i0[r], g, c, S[0], S[1]);
   }
-  gv_epilogue<NV>(J, i0, g, c, S[0], S[1]);
 }
 
 // ---------------------------------------------------------------------------
@@ -3051,8 +3103,9 @@ __global__ void __launch_bounds__(256) k_mgs_coop(const double *__restrict__ V, 
 // w and one write of w, instead of reading V_{i-1}, V_i and w and writing w for
 // every projection. Dynamic shared memory: R * 256 doubles.
 template <int R>
-__global__ void __launch_bounds__(256) k_mgs_reg(const double *__restrict__ V, double *__restrict__ w, long long n,
-                                                 int j, double *__restrict__ H, double *__restrict__ part) {
+__global__ void __launch_bounds__(256, R >= 16 ? 2 : 1) k_mgs_reg(const double *__restrict__ V, double *__restrict__ w,
+                                                                  long long n, int j, double *__restrict__ H,
+                                                                  double *__restrict__ part) {
   extern __shared__ double vps[];  // [R][256]: this thread's V_{i-1} entries
   __shared__ double sh[33];
   __shared__ double s_h;
@@ -3060,27 +3113,26 @@ __global__ void __launch_bounds__(256) k_mgs_reg(const double *__restrict__ V, d
   const int G = gridDim.x, b = blockIdx.x;
   const long long chunk = (n + G - 1) / G;
   const long long lo = (long long)b * chunk, hi = min(n, lo + chunk);
+  // this thread's elements: lo + tid + 256 u for u < cnt (ascending, as k_mgs_coop)
+  const int cnt = hi > lo + threadIdx.x ? (int)((hi - lo - threadIdx.x + 255) / 256) : 0;
+  double *wb = w + lo + threadIdx.x;
   double wv[R];
 #pragma unroll
-  for (int u = 0; u < R; ++u) {
-    const long long k = lo + threadIdx.x + 256LL * u;
-    wv[u] = k < hi ? w[k] : 0.0;
-  }
+  for (int u = 0; u < R; ++u) wv[u] = u < cnt ? wb[256 * u] : 0.0;
   double h = 0.0;
   for (int i = 0; i <= j + 1; ++i) {
-    const double *Vi = V + (long long)i * n;
+    const double *vb = V + (long long)i * n + lo + threadIdx.x;
     double s = 0.0;
 #pragma unroll
     for (int u = 0; u < R; ++u) {
-      const long long k = lo + threadIdx.x + 256LL * u;
-      if (k < hi) {
+      if (u < cnt) {
         double wk = wv[u];
         if (i > 0) {
           wk = __dsub_rn(wk, __dmul_rn(h, vps[u * 256 + threadIdx.x]));
           wv[u] = wk;
         }
         if (i <= j) {
-          const double vi = Vi[k];
+          const double vi = vb[256 * u];
           vps[u * 256 + threadIdx.x] = vi;
           s = fma(vi, wk, s);
         } else {
@@ -3102,10 +3154,8 @@ __global__ void __launch_bounds__(256) k_mgs_reg(const double *__restrict__ V, d
     if (b == 0 && threadIdx.x == 0) H[i] = (i <= j) ? h : sqrt(h);
   }
 #pragma unroll
-  for (int u = 0; u < R; ++u) {
-    const long long k = lo + threadIdx.x + 256LL * u;
-    if (k < hi) w[k] = wv[u];
-  }
+  for (int u = 0; u < R; ++u)
+    if (u < cnt) wb[256 * u] = wv[u];
 }
 
 // CSR SpMV, one warp per row (A @ x, sparse.py:277-284)

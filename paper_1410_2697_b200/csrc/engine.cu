@@ -548,7 +548,9 @@ static bool gemm_overlaps(const GemmJob &g) {
 }
 
 static thread_local int g_split_k_override = -1;  // test hook (mfh_test_gemm_batched)
-static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
+// tiles_only: every job on k_gemm (the sampler's k-ascending chains, so a
+// product it forms equals the per-entry one bit for bit), no cuBLAS route
+static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs, bool tiles_only = false) {
   OpClock oc_("gemm");
   if (jobs.empty()) return;
   for (const GemmJob &g : jobs)
@@ -560,7 +562,7 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs) {
   // A/B knob: MFH_GEMM_NO_BLAS=1 keeps every GEMM on the batched DMMA kernel
   static const bool no_blas = getenv("MFH_GEMM_NO_BLAS") && atoi(getenv("MFH_GEMM_NO_BLAS")) != 0;
   auto is_big = [&](const GemmJob &g) {
-    return !no_blas && !sk.record && g.k > 0 && g.m >= 64 && g.n >= 64 && 2.0 * g.m * g.n * g.k >= (double)(1 << 27) &&
+    return !no_blas && !tiles_only && !sk.record && g.k > 0 && g.m >= 64 && g.n >= 64 && 2.0 * g.m * g.n * g.k >= (double)(1 << 27) &&
            g.lda > 0 && g.ldb > 0 && !gemm_overlaps(g);
   };
   // products with an identity operand (leading dimension -1: the strip that
@@ -1878,14 +1880,16 @@ struct Factorizer {
   }
 
   // ---- child descriptors (maps from the per-tree cache) for a set of fronts ----
-  // A large child update (the update HODLR minus W V^T, multifrontal.py:340-347)
+  // A child update of nf >= 256 (the update HODLR minus W V^T, multifrontal.py:340-347)
   // is materialized once as a dense nf x nf block when its parent is
   // processed: leaf copies and one GEMM per low-rank block (the reference's
   // to_dense), then -W V^T as one GEMM. The parent's extend-add requests then
   // gather from it instead of descending the HODLR tree and recomputing a
   // rank-r product per sampled entry (C5: the root's dense fallbacks read
-  // ~300 GB that way). Same values up to the GEMMs' rounding; nf >=
-  // MFH_DENSIFY_MIN (default 4096, 0 = never).
+  // ~300 GB that way). Below nf 4096 the products run on k_gemm (k-ascending
+  // DMMA chains, epilogue fma(beta, C, alpha acc)), the same arithmetic as the
+  // sampler's per-entry chains, so the sampled values are bitwise unchanged
+  // (tests/test_gpu_densify.py). nf >= MFH_DENSIFY_MIN (0 = never).
   const double *densify_update(Sink &s, const FrontH &c) {
     const int nf = c.nf;
     double *D = upd.d((size_t)nf * nf, release_height(c));
@@ -1909,18 +1913,21 @@ struct Factorizer {
         }
       }
     }
+    // below 4096 every product stays on k_gemm (bitwise the sampler's values);
+    // larger ones may take the cuBLAS route (C5: 0.1 s faster per step)
+    const bool exact = nf < 4096;
     run_copy(s, cp);
-    run_gemm(s, gm);
-    if (c.rw) {
+    run_gemm(s, gm, exact);
+    if (c.rw) {  // D = H - W V^T: fma(1, H, -acc), the sampler's sub - acc
       std::vector<GemmJob> wv{GemmJob{c.W, c.Vt, D, nf, nf, c.rw, c.ldw, c.ldv, nf, -1.0, 1.0}};
-      run_gemm(s, wv);
+      run_gemm(s, wv, exact);
     }
     return D;
   }
 
   void build_fronts_dev(Sink &s, const std::vector<int> &fis, std::vector<DFront> &dfr,
                         std::vector<DChild> &dch, std::vector<int> &slot_of) {
-    static const int densify_min = getenv("MFH_DENSIFY_MIN") ? atoi(getenv("MFH_DENSIFY_MIN")) : 4096;
+    static const int densify_min = getenv("MFH_DENSIFY_MIN") ? atoi(getenv("MFH_DENSIFY_MIN")) : 256;
     slot_of.assign(F->fronts.size(), -1);
     slot_rw.clear();
     for (int fi : fis) {

@@ -762,7 +762,7 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
     int np_ = (int)pj.size();
     int mmax = 0;
     for (auto &q : pj) mmax = std::max(mmax, q.n - q.c0);
-    int cs = (mmax + PANEL_ROWS_MAX - 1) / PANEL_ROWS_MAX;
+    int cs = mmax <= PANEL_ROWS_MAX ? 1 : (mmax + PANEL_ROWS_CL - 1) / PANEL_ROWS_CL;
     if (cs == 1) {
       // every panel of the batch fits one CTA's shared memory
       size_t smem = sizeof(double) * (size_t)mmax * PLD;
@@ -773,7 +773,7 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
     } else if (cs <= sk.ctx->cluster_size) {
       // shared-memory resident panel across a cluster of cs CTAs
       int rp = (mmax + cs - 1) / cs;
-      size_t smem = sizeof(double) * (size_t)rp * PLD;
+      size_t smem = sizeof(double) * (size_t)rp * PLD + PANEL_CL_SLOTS;
       sk.launch([=](cudaStream_t s) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(np_ * cs);
@@ -1041,7 +1041,7 @@ static void device_setup(Ctx *ctx) {
     CK(cudaFuncSetAttribute(k_getrf_panel_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double) * PANEL_ROWS_MAX * PLD)));
     CK(cudaFuncSetAttribute(k_getrf_panel_cl, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(sizeof(double) * PANEL_ROWS_MAX * PLD)));
+                            (int)(sizeof(double) * PANEL_ROWS_CL * PLD + PANEL_CL_SLOTS)));
     CK(cudaFuncSetAttribute(k_sample_rb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RB_DYN));
     CK(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_DYN));
   }
@@ -1494,6 +1494,7 @@ struct FrontH {
   int tree_base = -1, block_base = -1;      // pre-assigned plan slots
   // update for the parent
   int upd = -1;  // -1 none, 0 dense, 1 hodlr
+  bool densified = false;  // update materialized dense for the parent (densify_update)
   const double *upd_dense = nullptr;
   int upd_ld = 0;
   const double *W = nullptr, *Vt = nullptr;
@@ -1951,6 +1952,7 @@ struct Factorizer {
           ch.kind = 0;
           ch.dense = densify_update(s, c);
           ch.ldd = cn;
+          c.densified = true;
         } else {
           ch.kind = 1;
           ch.hn = c.rx_nodes ? c.rx_nodes : F->trees[c.ff].d_nodes;
@@ -2126,7 +2128,7 @@ struct Factorizer {
     const FrontH &f = F->fronts[fi];
     for (int ci : f.kids) {
       const FrontH &c = F->fronts[ci];
-      if (c.upd != 1 || c.rw == 0) continue;
+      if (c.upd != 1 || c.rw == 0 || c.densified) continue;  // a densified update is gathered
       const int *to = et->mapcache.maps.data() + et->mapcache.off[ci];
       auto hits = [&](int a0, int n, const std::vector<int> *l) {
         double h = 0;
@@ -2152,6 +2154,9 @@ struct Factorizer {
     std::vector<DFront> dfr;
     std::vector<DChild> dch;
     std::vector<int> slot;
+    // (materializing large child updates is enqueued here, so the GPU runs it
+    // while the host builds this height's requests; it shows as the gap before
+    // the sample phase)
     build_fronts_dev(s, fis, dfr, dch, slot);
     DFront *dF = nullptr;  // pushed with the first sampling batch below
     DChild *dC = nullptr;

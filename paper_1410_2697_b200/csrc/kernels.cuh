@@ -1861,25 +1861,31 @@ struct PanelJob {  // panel columns [c0, c0+w) of an n x n matrix, rows c0..n-1
 
 
 // Panel LU (partial pivoting, LAPACK rule) with the panel resident in shared
-// memory across a cluster: CTA q of the cluster owns panel rows
-// [q*rp, (q+1)*rp) (stride PNB+1: conflict-free column scans), one thread
-// per row. Per column: local candidate -> cluster barrier -> every CTA
-// reduces the CS candidates and pulls the pivot row (and, for the owner of
-// row p, old row k) over DSMEM -> cluster barrier -> swap writes, scale and
-// rank-1 update of the local rows. Same arithmetic as the global-memory k_getrf_panel.
+// memory (stride PNB+1: conflict-free column scans), one thread per row.
 constexpr int PLD = PNB + 1;
 constexpr int PANEL_ROWS_MAX = 416;  // rows per CTA (416 * 65 * 8 = 216 KB)
+// Panel LU across a cluster of CS CTAs (panel rows in distributed shared
+// memory), ONE cluster barrier per column step: every CTA pushes its block
+// candidate (|a|, row) and that candidate's row into a slot of EVERY CTA's
+// shared memory, and the CTA owning panel row kk pushes row kk; after the
+// barrier each CTA reduces the CS candidates locally and has the pivot row and
+// row kk in its own shared memory, so the swap and the trailing update need no
+// remote reads. Slots are parity double-buffered (a CTA pushes step kk + 2
+// only after every CTA passed step kk + 1's barrier). Same pivot rule and
+// arithmetic as k_getrf_panel_cta.
+constexpr int PANEL_ROWS_CL = 384;  // rows per cluster CTA (panel + slots fit the opt-in)
+constexpr int PSLOT = PNB + 2;      // candidate row, |a|, key bits
+constexpr size_t PANEL_CL_SLOTS = sizeof(double) * (2 * 16 * PSLOT + 2 * PNB);
 __global__ void __launch_bounds__(512) k_getrf_panel_cl(const PanelJob *__restrict__ jobs) {
   extern __shared__ double sh_panel[];
   __shared__ MaxLoc red[33];
-  __shared__ MaxLoc cand;
-  __shared__ double prow[PNB], told[PNB];
-  __shared__ int s_p;
   cg::cluster_group cl = cg::this_cluster();
   const int CS = (int)cl.num_blocks(), q = (int)cl.block_rank();
   const PanelJob J = jobs[blockIdx.x / CS];
   const int n = J.n, lda = J.lda, c0 = J.c0, w = J.w, tid = threadIdx.x;
   const int m = n - c0, rp = (m + CS - 1) / CS, r0 = q * rp, nr = max(0, min(m, r0 + rp) - r0);
+  double *slots = sh_panel + (size_t)rp * PLD;  // [2][16][PSLOT]
+  double *rowk = slots + 2 * 16 * PSLOT;        // [2][PNB]
   double *a = J.a;
   // load my slab: panel row t (global row c0 + r0 + t), columns c0 .. c0+w-1
   for (int e = tid; e < nr * w; e += blockDim.x) {
@@ -1888,60 +1894,85 @@ __global__ void __launch_bounds__(512) k_getrf_panel_cl(const PanelJob *__restri
   }
   __syncthreads();
   double *myrow = tid < nr ? sh_panel + tid * PLD : nullptr;
+  const int lane = tid & 31;
   for (int kk = 0; kk < w; ++kk) {
-    // local candidate over my rows with panel index >= kk
+    const int par = kk & 1;
+    // local candidate over my rows with panel index >= kk (block_maxloc's
+    // barriers also order the previous step's row updates before the pushes)
     double bv = -1.0;
     long long bk = 0x7fffffffffffffffLL;
     if (myrow && r0 + tid >= kk) {
       bv = fabs(myrow[kk]);
       bk = r0 + tid;
     }
-    MaxLoc b = block_maxloc(bv, bk, red);
-    if (tid == 0) cand = b;
-    cl.sync();
-    if (tid < 32) {
-      MaxLoc o{-1.0, 0x7fffffffffffffffLL};
-      if (tid < CS) o = *cl.map_shared_rank(&cand, tid);
-      for (int off = 16; off > 0; off >>= 1) {
-        double ov = __shfl_down_sync(0xffffffffu, o.v, off);
-        long long ok = __shfl_down_sync(0xffffffffu, o.key, off);
-        if (better(ov, ok, o.v, o.key)) {
-          o.v = ov;
-          o.key = ok;
-        }
+    const MaxLoc b = block_maxloc(bv, bk, red);
+    const int li = b.key == 0x7fffffffffffffffLL ? -1 : (int)(b.key - r0);
+    for (int e = tid; e < CS * PSLOT; e += blockDim.x) {
+      const int dst = e / PSLOT, idx = e - dst * PSLOT;
+      double val;
+      if (idx < PNB)
+        val = (li >= 0 && idx < w) ? sh_panel[li * PLD + idx] : 0.0;
+      else if (idx == PNB)
+        val = b.v;
+      else
+        val = __longlong_as_double(b.key);
+      cl.map_shared_rank(slots, dst)[(par * 16 + q) * PSLOT + idx] = val;
+    }
+    const int okk = kk / rp;  // CTA holding panel row kk
+    if (q == okk)
+      for (int e = tid; e < CS * w; e += blockDim.x) {
+        const int dst = e / w, j = e - dst * w;
+        cl.map_shared_rank(rowk, dst)[par * PNB + j] = sh_panel[(kk - r0) * PLD + j];
       }
-      if (tid == 0) s_p = o.key == 0x7fffffffffffffffLL ? kk : (int)o.key;
-    }
-    __syncthreads();
-    const int p = s_p;  // panel row index
-    const int op = p / rp, ok_ = kk / rp;
-    if (tid < w) {
-      prow[tid] = cl.map_shared_rank(sh_panel, op)[(p - op * rp) * PLD + tid];
-      if (q == op && p != kk) told[tid] = cl.map_shared_rank(sh_panel, ok_)[(kk - ok_ * rp) * PLD + tid];
-    }
-    if (q == 0 && tid == 0) J.piv[c0 + kk] = c0 + p;
     cl.sync();
+    // every warp reduces the CS candidates from its own shared memory
+    double gv = -2.0;
+    long long gk = 0x7fffffffffffffffLL;
+    int who = 0;
+    if (lane < CS) {
+      gv = slots[(par * 16 + lane) * PSLOT + PNB];
+      gk = __double_as_longlong(slots[(par * 16 + lane) * PSLOT + PNB + 1]);
+      who = lane;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, gv, off);
+      const long long ok = __shfl_xor_sync(0xffffffffu, gk, off);
+      const int ow = __shfl_xor_sync(0xffffffffu, who, off);
+      if (better(ov, ok, gv, gk) || (ov == gv && ok == gk && ow < who)) {
+        gv = ov;
+        gk = ok;
+        who = ow;
+      }
+    }
+    const int p = gk == 0x7fffffffffffffffLL ? kk : (int)gk;  // panel row index
+    const double *prow = slots + (par * 16 + who) * PSLOT;  // row p before the swap
+    const double *told = rowk + par * PNB;                  // row kk before the swap
     const double pv = prow[kk];
-    if (p != kk && pv != 0.0) {
-      if (q == ok_ && tid < w) sh_panel[(kk - r0) * PLD + tid] = prow[tid];
-      if (q == op && tid < w) sh_panel[(p - r0) * PLD + tid] = told[tid];
-      __syncthreads();
-    }
-    if (myrow && r0 + tid > kk) {
-      double l = myrow[kk];
-      if (pv != 0.0) {
-        l *= 1.0 / pv;
-        myrow[kk] = l;
+    if (q == 0 && tid == 0) J.piv[c0 + kk] = c0 + p;
+    if (myrow) {  // each row by its own thread: swap, then the update
+      const int gr = r0 + tid;
+      if (p != kk && pv != 0.0) {
+        if (gr == kk)
+          for (int j = 0; j < w; ++j) myrow[j] = prow[j];
+        else if (gr == p)
+          for (int j = 0; j < w; ++j) myrow[j] = told[j];
       }
-      for (int j = kk + 1; j < w; ++j) myrow[j] = fma(-l, prow[j], myrow[j]);
+      if (gr > kk) {
+        double l = myrow[kk];
+        if (pv != 0.0) {
+          l *= 1.0 / pv;
+          myrow[kk] = l;
+        }
+        for (int j = kk + 1; j < w; ++j) myrow[j] = fma(-l, prow[j], myrow[j]);
+      }
     }
-    __syncthreads();
   }
+  __syncthreads();
   for (int e = tid; e < nr * w; e += blockDim.x) {
     int t = e / w, j = e - t * w;
     a[(long long)(c0 + r0 + t) * lda + c0 + j] = sh_panel[t * PLD + j];
   }
-  cl.sync();  // remote readers are done before this CTA's shared memory goes away
+  cl.sync();  // no CTA exits while a peer may still push into its shared memory
 }
 
 // panel LU with the panel in global memory: fallback for panels taller than a

@@ -2,8 +2,8 @@
 # C2 bench line with CPU baseline, launch list, DRAM traffic per kernel class,
 # ncu --set full of the new kernels, bench lines for C1/C3/C4/C5 and conventional C5.
 set -u
-mkdir -p gpurun_out/m2
-O=gpurun_out/m2
+mkdir -p gpurun_out/m3
+O=gpurun_out/m3
 export PYTHONFAULTHANDLER=1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.used --format=csv > $O/gpu.txt 2>&1
 timeout 900 python bench.py --steps 5 --warmup 3 > $O/bench_c2.log 2>&1; echo "c2 bench rc=$?"

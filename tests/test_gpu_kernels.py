@@ -124,7 +124,7 @@ def test_explicit_inverse_exact_permutations_and_singular():
     """Scaled anti-diagonal permutations pivot on the last row at every step:
     inverses are exact. A zero column is reported singular."""
     mats = []
-    for n in (7, 40, 64, 96, 128, 300):
+    for n in (7, 40, 64, 96, 128, 300, 600, 1000):
         p = np.zeros((n, n))
         p[np.arange(n), n - 1 - np.arange(n)] = 2.0 ** (np.arange(n) % 7 - 3)
         mats.append(p)

@@ -1891,44 +1891,53 @@ struct Factorizer {
   // DMMA chains, epilogue fma(beta, C, alpha acc)), the same arithmetic as the
   // sampler's per-entry chains, so the sampled values are bitwise unchanged
   // (tests/test_gpu_densify.py). nf >= MFH_DENSIFY_MIN (0 = never).
-  const double *densify_update(Sink &s, const FrontH &c) {
+  struct DensifyJobs {
+    std::vector<CopyJob> cp;
+    std::vector<GemmJob> gm[2], wv[2];  // [exact]: block products, then -W V^T
+  };
+  const double *densify_update(DensifyJobs &dj, const FrontH &c) {
     const int nf = c.nf;
     double *D = upd.d((size_t)nf * nf, release_height(c));
     HTree &T = F->trees[c.ff];
-    std::vector<CopyJob> cp;
-    std::vector<GemmJob> gm;
+    // below 4096 every product stays on k_gemm (bitwise the sampler's values);
+    // larger ones may take the cuBLAS route (C5: 0.1 s faster per step)
+    const int exact = nf < 4096 ? 1 : 0;
     for (int v = 0; v < T.nslots; ++v) {
       const int lo = T.lo[v], hi = T.hi[v];
       if (T.leaf[v] == 1) {
         const int sz = hi - lo;
-        cp.push_back(CopyJob{T.lval[v], D + (int64_t)lo * nf + lo, sz, sz, sz, nf, nullptr, nullptr});
+        dj.cp.push_back(CopyJob{T.lval[v], D + (int64_t)lo * nf + lo, sz, sz, sz, nf, nullptr, nullptr});
       } else if (T.leaf[v] == 0) {
         const int mid = (lo + hi) >> 1;
         for (int side = 0; side < 2; ++side) {
           const BlockH &b = F->blocks[side == 0 ? T.up[v] : T.lw[v]];
           double *dst = D + (side == 0 ? (int64_t)lo * nf + mid : (int64_t)mid * nf + lo);
           if (b.dense)
-            cp.push_back(CopyJob{b.val, dst, b.m, b.n, b.n, nf, nullptr, nullptr});
+            dj.cp.push_back(CopyJob{b.val, dst, b.m, b.n, b.n, nf, nullptr, nullptr});
           else  // rank 0 writes zeros (k = 0)
-            gm.push_back(GemmJob{b.col, b.row, dst, b.m, b.n, b.rank, std::max(1, b.rank), b.n, nf, 1.0, 0.0});
+            dj.gm[exact].push_back(
+                GemmJob{b.col, b.row, dst, b.m, b.n, b.rank, std::max(1, b.rank), b.n, nf, 1.0, 0.0});
         }
       }
     }
-    // below 4096 every product stays on k_gemm (bitwise the sampler's values);
-    // larger ones may take the cuBLAS route (C5: 0.1 s faster per step)
-    const bool exact = nf < 4096;
-    run_copy(s, cp);
-    run_gemm(s, gm, exact);
-    if (c.rw) {  // D = H - W V^T: fma(1, H, -acc), the sampler's sub - acc
-      std::vector<GemmJob> wv{GemmJob{c.W, c.Vt, D, nf, nf, c.rw, c.ldw, c.ldv, nf, -1.0, 1.0}};
-      run_gemm(s, wv, exact);
-    }
+    // D = H - W V^T: fma(1, H, -acc), the sampler's sub - acc
+    if (c.rw) dj.wv[exact].push_back(GemmJob{c.W, c.Vt, D, nf, nf, c.rw, c.ldw, c.ldv, nf, -1.0, 1.0});
     return D;
+  }
+  // one launch per job kind for every child materialized at this height
+  void run_densify(Sink &s, DensifyJobs &dj) {
+    if (dj.cp.empty() && dj.gm[0].empty() && dj.gm[1].empty()) return;
+    s.begin_batch();
+    run_copy(s, dj.cp);
+    for (int x = 0; x < 2; ++x) run_gemm(s, dj.gm[x], x == 1);
+    for (int x = 0; x < 2; ++x) run_gemm(s, dj.wv[x], x == 1);
+    s.flush();
   }
 
   void build_fronts_dev(Sink &s, const std::vector<int> &fis, std::vector<DFront> &dfr,
                         std::vector<DChild> &dch, std::vector<int> &slot_of) {
     static const int densify_min = getenv("MFH_DENSIFY_MIN") ? atoi(getenv("MFH_DENSIFY_MIN")) : 256;
+    DensifyJobs dj;
     slot_of.assign(F->fronts.size(), -1);
     slot_rw.clear();
     for (int fi : fis) {
@@ -1950,7 +1959,7 @@ struct Factorizer {
           ch.ldd = c.upd_ld;
         } else if (densify_min > 0 && cn >= densify_min && !c.rx_nodes && c.ff >= 0) {
           ch.kind = 0;
-          ch.dense = densify_update(s, c);
+          ch.dense = densify_update(dj, c);
           ch.ldd = cn;
           c.densified = true;
         } else {
@@ -1972,6 +1981,7 @@ struct Factorizer {
       slot_rw.push_back(mrw);
       dfr.push_back(d);
     }
+    run_densify(s, dj);
   }
 
   // largest child update rank per DFront slot of the current descriptor set

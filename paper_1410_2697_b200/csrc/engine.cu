@@ -4679,6 +4679,10 @@ struct mfh_csr {
   int *col = nullptr;
   double *val = nullptr;
   mfh::GemmJob *djob = nullptr;  // dense GEMV descriptor (x/y patched per call)
+  // streamed SpMV (k_spmv_stream): rows per chunk, entry capacity of a stage, grid; R = 0: rows too long
+  int sR = 0, scap = 0, sgrid = 0, snst = 2;
+  size_t ssmem = 0;
+  int *ptr32 = nullptr;  // 4-byte row pointers for the streamed SpMV when nnz < 2^31
 };
 
 namespace mfh {
@@ -4689,6 +4693,19 @@ static void op_apply_device(mfh_csr *A, const double *x, double *y) {
     // lanes per row from the average row length
     const int64_t nnz = A->nnz;
     const double avg = A->nr ? (double)nnz / A->nr : 0.0;
+    static const bool no_stream = getenv("MFH_SPMV_NO_STREAM") != nullptr;  // A/B knob
+    if (A->sR > 0 && !no_stream) {
+      const int64_t nchunks = cdiv(A->nr, (int64_t)A->sR);
+      if (A->ptr32)
+        k_spmv_stream<int><<<A->sgrid, 256, A->ssmem, ctx->s>>>(A->nr, A->sR, A->scap, A->snst, nchunks, A->ptr32,
+                                                                 A->col, A->val, x, y);
+      else
+        k_spmv_stream<long long><<<A->sgrid, 256, A->ssmem, ctx->s>>>(A->nr, A->sR, A->scap, A->snst, nchunks,
+                                                                       A->ptr, A->col, A->val, x, y);
+      check_launch();
+      ctx->launches++;
+      return;
+    }
     const int W = avg <= 4.5 ? 4 : (avg <= 9.5 ? 8 : (avg <= 20 ? 16 : 32));
     int grid = (int)std::min<int64_t>(cdiv(std::max<int64_t>(1, A->nr) * W, 256), 148 * 16);
     if (grid < 1) grid = 1;
@@ -5271,10 +5288,48 @@ extern "C" int mfh_csr_create(mfh_ctx *ctx, int64_t n_rows, int64_t n_cols, cons
   A->nc = n_cols;
   int64_t nnz = indptr[n_rows];
   A->nnz = nnz;
-  CK(cudaMalloc(&A->ptr, sizeof(int64_t) * (n_rows + 1)));
-  CK(cudaMalloc(&A->col, sizeof(int) * std::max<int64_t>(1, nnz)));
-  CK(cudaMalloc(&A->val, sizeof(double) * std::max<int64_t>(1, nnz)));
+  // slack for the streamed SpMV's widened bulk copies (16-byte aligned ends)
+  CK(cudaMalloc(&A->ptr, sizeof(int64_t) * (n_rows + 4)));
+  CK(cudaMalloc(&A->col, sizeof(int) * (nnz + 8)));
+  CK(cudaMalloc(&A->val, sizeof(double) * (nnz + 4)));
+  CK(cudaMemsetAsync(A->ptr + n_rows, 0, sizeof(int64_t) * 4, A->ctx->s));
+  CK(cudaMemsetAsync(A->col + nnz, 0, sizeof(int) * 8, A->ctx->s));
+  CK(cudaMemsetAsync(A->val + nnz, 0, sizeof(double) * 4, A->ctx->s));
   std::vector<int> c32(indices, indices + nnz);
+  {
+    // chunk shape: the most rows R in {128, 64, 32} whose longest possible chunk fits a stage
+    int64_t maxrow = 0;
+    for (int64_t r = 0; r < n_rows; ++r) maxrow = std::max(maxrow, indptr[r + 1] - indptr[r]);
+    const char *eR = getenv("MFH_SPMV_R"), *eS = getenv("MFH_SPMV_STG"), *eP = getenv("MFH_SPMV_P64");  // tuning knobs
+    int R = 0;
+    // (measured: 128 rows x 7 entries, 128 x ~10, 64 x 27 beat the next larger chunk; a software-pipelined
+    // variant with the next chunk's gathers in registers and three stages was slower: fewer CTAs per SM)
+    for (int cand : {128, 64, 32})
+      if ((!eR || cand <= atoi(eR)) && (int64_t)cand * maxrow <= (cand == 32 ? 8192 : 2048)) { R = cand; break; }
+    if (eR && atoi(eR) >= 256 && 256 * maxrow <= 4096) R = 256;
+    if (R && n_rows > 0 && nnz > 0) {
+      const bool p32 = nnz < (int64_t(1) << 31) && !eP;
+      A->sR = R;
+      A->scap = (int)((R * maxrow + 1) & ~(int64_t)1);
+      A->snst = eS ? std::min(SPMV_MAX_STG, std::max(1, atoi(eS))) : 2;
+      A->ssmem = A->snst * spmv_stage_bytes(A->sR, A->scap, p32 ? 4 : 8);
+      int per_sm = 0;
+      if (p32) {
+        std::vector<int> p4(indptr, indptr + n_rows + 1);
+        p4.resize(n_rows + 8, 0);
+        CK(cudaMalloc(&A->ptr32, sizeof(int) * (n_rows + 8)));
+        upload(A->ctx->s, A->ptr32, p4.data(), sizeof(int) * (n_rows + 8));
+        CK(cudaFuncSetAttribute(k_spmv_stream<int>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)A->ssmem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_stream<int>, 256, A->ssmem));
+      } else {
+        CK(cudaFuncSetAttribute(k_spmv_stream<long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)A->ssmem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_stream<long long>, 256, A->ssmem));
+      }
+      // persistent CTAs with the same number of chunks each (no partial last round)
+      const int64_t nchunks = cdiv(n_rows, (int64_t)R), gmax = (int64_t)A->ctx->nsm * std::max(1, per_sm);
+      A->sgrid = (int)cdiv(nchunks, cdiv(nchunks, gmax));
+    }
+  }
   upload(A->ctx->s, A->ptr, indptr, sizeof(int64_t) * (n_rows + 1));
   if (nnz) {
     upload(A->ctx->s, A->col, c32.data(), sizeof(int) * nnz);
@@ -5305,6 +5360,7 @@ extern "C" void mfh_csr_free(mfh_csr *A) {
   DeviceGuard dg_(A->ctx->device);
   cudaStreamSynchronize(A->ctx->s);
   cudaFree(A->ptr);
+  cudaFree(A->ptr32);
   cudaFree(A->col);
   cudaFree(A->val);
   delete A;

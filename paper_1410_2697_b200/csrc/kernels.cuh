@@ -3226,6 +3226,137 @@ __global__ void __launch_bounds__(256) k_spmv(long long nrows, const long long *
 }
 
 // ---------------------------------------------------------------------------
+// Streamed CSR SpMV (A @ x, sparse.py:277-284): the matrix streams through
+// shared memory by TMA bulk copies (cp.async.bulk + mbarrier complete_tx), two
+// stages per CTA, persistent CTAs over chunks of R consecutive rows.
+//   stage  = row pointers [r0, r0 + rows], values and columns [p0, p1) of the chunk
+//   pass A = every thread turns entries into products val * x[col] in place
+//            (entry-strided: the x gathers of a chunk are all in flight at once)
+//   pass B = one thread per row adds its products in ascending entry order from 0
+// The arithmetic is the reference's scipy CSC product (y[i] += a_ij * x_j over
+// ascending j, a rounded product then a rounded add): bit-identical for a CSR
+// with ascending columns. Bulk copies need 16-byte aligned ends: the copied
+// ranges are widened to even (double) / multiple-of-4 (int) entry offsets, and
+// the arrays carry that much slack (mfh_csr_create).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "W_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra D_%=;\n"
+      "bra W_%=;\n"
+      "D_%=:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void *smem_dst, const void *gsrc, unsigned bytes, unsigned long long *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+constexpr int SPMV_MAX_STG = 4;
+// shared-memory bytes of one stage: values (cap + 2), row pointers (R + 4, 4 or 8 bytes each),
+// columns (cap + 8); R a multiple of 4, cap even
+__host__ __device__ inline size_t spmv_stage_bytes(int R, int cap, int ptr_bytes) {
+  return (size_t)8 * (cap + 2) + (size_t)ptr_bytes * (R + 4) + (((size_t)4 * (cap + 8) + 15) & ~(size_t)15);
+}
+
+// PT: the row-pointer type streamed (int when nnz < 2^31: the 4-byte pointers of the byte count)
+template <typename PT>
+__global__ void __launch_bounds__(256) k_spmv_stream(long long nrows, int R, int cap, int nst, long long nchunks,
+                                                     const PT *__restrict__ ptr, const int *__restrict__ col,
+                                                     const double *__restrict__ val, const double *__restrict__ x,
+                                                     double *__restrict__ y) {
+  extern __shared__ __align__(128) unsigned char spmv_smem[];
+  __shared__ unsigned long long bar[SPMV_MAX_STG];
+  constexpr int PB = (int)sizeof(PT), PA = 16 / PB;  // pointers per 16 bytes
+  const size_t stb = spmv_stage_bytes(R, cap, PB);
+  auto sval = [&](int s) { return reinterpret_cast<double *>(spmv_smem + stb * s); };
+  auto sptr = [&](int s) { return reinterpret_cast<PT *>(spmv_smem + stb * s + (size_t)8 * (cap + 2)); };
+  auto scol = [&](int s) {
+    return reinterpret_cast<int *>(spmv_smem + stb * s + (size_t)8 * (cap + 2) + (size_t)PB * (R + 4));
+  };
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < nst; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // thread 0 issues the three bulk copies of chunk c into stage s
+  auto issue = [&](long long c, int s, long long p0, long long p1) {
+    const long long r0 = c * R;
+    const int rows = (int)min((long long)R, nrows - r0);
+    const long long v0 = p0 & ~1LL, v1 = (p1 + 1) & ~1LL;
+    const long long c0 = p0 & ~3LL, c1 = (p1 + 3) & ~3LL;
+    const unsigned bp = (unsigned)(PB * ((rows + PA) & ~(PA - 1)));  // rows + 1 pointers, rounded up to 16 bytes
+    const unsigned bv = (unsigned)(8 * (v1 - v0)), bc = (unsigned)(4 * (c1 - c0));
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    mbar_expect_tx(&bar[s], bp + bv + bc);
+    tma_bulk_g2s(sptr(s), ptr + r0, bp, &bar[s]);
+    if (bv) tma_bulk_g2s(sval(s), val + v0, bv, &bar[s]);
+    if (bc) tma_bulk_g2s(scol(s), col + c0, bc, &bar[s]);
+  };
+  const long long G = gridDim.x;
+  long long np0 = 0, np1 = 0;  // thread 0: entry range of the chunk it issues next
+  if (tid == 0) {
+    for (int s = 0; s < nst; ++s) {
+      const long long c = blockIdx.x + s * G;
+      if (c < nchunks) issue(c, s, (long long)__ldg(ptr + c * R), (long long)__ldg(ptr + min(nrows, (c + 1) * R)));
+    }
+  }
+  int s = 0;
+  unsigned par = 0;
+  for (long long c = blockIdx.x; c < nchunks; c += G) {
+    const long long cn = c + nst * G;  // the chunk that reuses this stage
+    if (tid == 0 && cn < nchunks) {
+      np0 = (long long)__ldg(ptr + cn * R);
+      np1 = (long long)__ldg(ptr + min(nrows, (cn + 1) * R));
+    }
+    mbar_wait(&bar[s], par);
+    const long long r0 = c * R;
+    const int rows = (int)min((long long)R, nrows - r0);
+    const PT *sp = sptr(s);
+    const long long p0 = sp[0], p1 = sp[rows];
+    double *sv = sval(s) - (p0 & ~1LL);  // entry p at sv[p]
+    const int *sc = scol(s) - (p0 & ~3LL);
+    {
+      long long p = p0 + tid;
+      for (; p + 768 < p1; p += 1024) {  // four independent gathers in flight per thread
+        const int j0 = sc[p], j1 = sc[p + 256], j2 = sc[p + 512], j3 = sc[p + 768];
+        const double x0 = __ldg(x + j0), x1 = __ldg(x + j1), x2 = __ldg(x + j2), x3 = __ldg(x + j3);
+        sv[p] = __dmul_rn(sv[p], x0);
+        sv[p + 256] = __dmul_rn(sv[p + 256], x1);
+        sv[p + 512] = __dmul_rn(sv[p + 512], x2);
+        sv[p + 768] = __dmul_rn(sv[p + 768], x3);
+      }
+      for (; p < p1; p += 256) sv[p] = __dmul_rn(sv[p], __ldg(x + sc[p]));
+    }
+    __syncthreads();
+    for (int r = tid; r < rows; r += 256) {
+      double acc = 0.0;
+      const long long e = sp[r + 1];
+      for (long long p = sp[r]; p < e; ++p) acc = __dadd_rn(acc, sv[p]);
+      y[r0 + r] = acc;
+    }
+    __syncthreads();
+    if (tid == 0 && cn < nchunks) issue(cn, s, np0, np1);
+    if (++s == nst) { s = 0; par ^= 1u; }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // baseline preconditioners (krylov.py:164-204)
 // ---------------------------------------------------------------------------
 // y = x / d (diagonal_preconditioner: v / diag, IEEE division, bit-exact)

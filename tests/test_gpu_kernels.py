@@ -87,6 +87,35 @@ def test_spmv_matches_scipy():
         P.spmv(A, np.ones(3))
 
 
+def test_spmv_streamed_bit_identical_to_reference_product():
+    """k_spmv_stream adds each row's rounded products in ascending column order from 0:
+    the reference's scipy CSC product (sparse.py:284) bit for bit. Ragged rows, empty rows,
+    rows at every 16-byte misalignment of the bulk copies, a chunk tail, many chunks per CTA."""
+    import scipy.sparse as sp
+    import paper_1410_2697_b200 as P
+    rng = np.random.default_rng(5)
+    cases = [P.gen_poisson7(20, 17, 13)[0], P.gen_poisson7(64, 64, 40)[0]]
+    for n, dens, seed in [(1, 1.0, 0), (257, 0.02, 1), (5000, 0.002, 2), (1031, 0.03, 3), (70000, 0.0001, 4)]:
+        g = np.random.default_rng(seed)
+        m = max(1, int(dens * n * n))
+        M = sp.coo_matrix((np.ones(m), (g.integers(0, n, m), g.integers(0, n, m))), shape=(n, n)).tocsr()
+        M.data = g.standard_normal(M.nnz)
+        if n > 10:                 # two empty rows
+            keep = sp.diags((~np.isin(np.arange(n), [3, n // 2])).astype(np.float64))
+            M = keep @ M
+            M.eliminate_zeros()
+        cases.append(P.SparseMatrix(sp.csc_matrix(M)))
+    # rows of 40-200 entries (32-row chunks) and a matrix whose rows are too long to stream (fallback kernel)
+    cases.append(P.SparseMatrix(sp.random(600, 600, density=0.2, random_state=7, format="csc")))
+    long_rows = P.SparseMatrix(sp.random(900, 900, density=0.6, random_state=8, format="csc"))
+    for A in cases:
+        x = rng.standard_normal(A.n_cols)
+        np.testing.assert_array_equal(P.spmv(A, x), A._csc @ x)
+    x = rng.standard_normal(900)
+    ref = long_rows._csc @ x
+    assert np.linalg.norm(P.spmv(long_rows, x) - ref) <= 1e-14 * np.linalg.norm(ref)
+
+
 def _gpu_inverse(mats):
     import ctypes as C
     from paper_1410_2697_b200 import _lib

@@ -289,7 +289,8 @@ struct Ctx {
   // GMRES host-callback preconditioner may re-enter on the same thread)
   std::recursive_mutex mu;
   int64_t launches = 0;      // launches of this library's kernels
-  int64_t lib_calls = 0;     // cuBLAS DGEMM calls (plain large GEMMs)
+  int64_t lib_calls = 0;     // cuBLAS DGEMM calls (only with MFH_GEMM_ROUTE=blas)
+  int64_t big_gemm_jobs = 0; // large plain GEMMs run on k_gemm_big
   double flops_exec = 0.0;   // flops enqueued by run_gemm (2mnk) and the register inverses (2n^3)
   cublasHandle_t blas = nullptr;
   void *blas_ws = nullptr;  // cuBLAS workspace (set once with the stream)
@@ -548,6 +549,7 @@ static bool gemm_overlaps(const GemmJob &g) {
 }
 
 static thread_local int g_split_k_override = -1;  // test hook (mfh_test_gemm_batched)
+static thread_local int g_route_override = -1;    // test hook: 0 k_gemm_big, 1 cuBLAS, 2 k_gemm for large plain GEMMs
 // tiles_only: every job on k_gemm (the sampler's k-ascending chains, so a
 // product it forms equals the per-entry one bit for bit), no cuBLAS route
 static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs, bool tiles_only = false) {
@@ -559,12 +561,39 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs, bool tiles_only
   std::vector<GemmJob> big;
   std::vector<GemmSplit> splits;
   int nslot = 0;
-  // A/B knob: MFH_GEMM_NO_BLAS=1 keeps every GEMM on the batched DMMA kernel
-  static const bool no_blas = getenv("MFH_GEMM_NO_BLAS") && atoi(getenv("MFH_GEMM_NO_BLAS")) != 0;
+  // Large plain GEMMs (>= 2^27 flops) go to cuBLAS DGEMM, or with MFH_GEMM_ROUTE=big to
+  // k_gemm_big (128-wide tiles, one persistent launch per batch; the same k-ascending DMMA chain
+  // as k_gemm, so choosing it never changes a bit of the result): a library-free factorization.
+  // Measured on B200 (profiles/r2_gemm_big_probe.txt, r2_ab_gemm_route.txt): k_gemm_big reaches
+  // 33.1 TFLOP/s on 4096^3 against the library's 35.2 and beats one-call-per-job cuBLAS on
+  // batches of 2^28..2^30-flop jobs (27 vs 19 TFLOP/s), but 90% of C5's large-GEMM flops are in
+  // products of 2^35 flops and more, half of them with rows that are not 16-byte aligned:
+  // C5 2.88 s/step with the library, 3.14 s without. While a graph is being recorded the large
+  // jobs always run on k_gemm_big.
+  // A/B knobs: MFH_GEMM_ROUTE=big (no library call at all) / blas (the default) / tiles (or
+  // MFH_GEMM_NO_BLAS=1: everything on the 64 x 64 kernel); MFH_GEMM_BLAS_MIN=<flops> sends only
+  // jobs of at least that many flops to the library and the smaller large ones to k_gemm_big.
+  static const int route_env = [] {
+    const char *e = getenv("MFH_GEMM_ROUTE");
+    if (e && !strcmp(e, "blas")) return 1;
+    if ((e && !strcmp(e, "tiles")) || (getenv("MFH_GEMM_NO_BLAS") && atoi(getenv("MFH_GEMM_NO_BLAS")) != 0)) return 2;
+    if (e && !strcmp(e, "big")) return 0;
+    return 3;
+  }();
+  const int route = g_route_override >= 0 ? g_route_override : route_env;
+  static const double big_min = getenv("MFH_GEMM_BIG_MIN") ? atof(getenv("MFH_GEMM_BIG_MIN")) : (double)(1 << 27);
+  static const double blas_min = getenv("MFH_GEMM_BLAS_MIN") ? atof(getenv("MFH_GEMM_BLAS_MIN")) : 0.0;
   auto is_big = [&](const GemmJob &g) {
-    return !no_blas && !tiles_only && !sk.record && g.k > 0 && g.m >= 64 && g.n >= 64 && 2.0 * g.m * g.n * g.k >= (double)(1 << 27) &&
+    return route != 2 && !tiles_only && g.k > 0 && g.m >= 64 && g.n >= 64 && 2.0 * g.m * g.n * g.k >= big_min &&
            g.lda > 0 && g.ldb > 0 && !gemm_overlaps(g);
   };
+  // of the large jobs: which go to the library (never while a graph is being recorded)
+  auto to_blas = [&](const GemmJob &g) {
+    if (sk.record || route == 0) return false;
+    if (route == 1) return true;
+    return 2.0 * g.m * g.n * g.k >= blas_min;
+  };
+  std::vector<GemmJob> lib;
   // products with an identity operand (leading dimension -1: the strip that
   // stands for DenseBlock.as_factors' eye) are scaled copies, not GEMMs
   std::vector<GemmJob> eye;
@@ -580,7 +609,12 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs, bool tiles_only
       continue;
     }
     if (is_big(g)) {
-      big.push_back(g);
+      static const bool blog = getenv("MFH_GEMM_BIGLOG") != nullptr;  // shapes of the large plain GEMMs
+      if (blog)
+        fprintf(stderr, "[biggemm] m %d n %d k %d a16 %d b16 %d c16 %d beta %g batch %zu\n", g.m, g.n, g.k,
+                (int)((((uintptr_t)g.A) & 15) == 0 && g.lda % 2 == 0), (int)((((uintptr_t)g.B) & 15) == 0 && g.ldb % 2 == 0),
+                (int)((((uintptr_t)g.C) & 15) == 0 && g.ldc % 2 == 0), g.beta, jobs.size());
+      (to_blas(g) ? lib : big).push_back(g);
       continue;
     }
     int tm = (int)cdiv(g.m, GEMM_BM), tn = (int)cdiv(g.n, GEMM_BN);
@@ -607,6 +641,42 @@ static void run_gemm(Sink &sk, const std::vector<GemmJob> &jobs, bool tiles_only
       }
   }
   if (!big.empty()) {
+    // tile shape of the launch: least padded work, with half a round of the persistent grid
+    // charged for the partial last round (128 x 128 runs one CTA per SM, the others two)
+    struct Shape { int bm, bn, slots; double eff; };
+    const Shape shapes[3] = {{128, 128, sk.ctx->nsm, 1.0}, {128, 64, 2 * sk.ctx->nsm, 1.035}, {64, 128, 2 * sk.ctx->nsm, 1.01}};
+    int best = 0;
+    double best_est = 0.0;
+    for (int c = 0; c < 3; ++c) {
+      double work = 0.0, nt = 0.0;
+      for (const GemmJob &g : big) {
+        const double t = (double)cdiv(g.m, shapes[c].bm) * (double)cdiv(g.n, shapes[c].bn);
+        nt += t;
+        work += t * shapes[c].bm * shapes[c].bn * g.k;
+      }
+      const double est = work * shapes[c].eff * (1.0 + 0.5 * shapes[c].slots / nt);
+      if (c == 0 || est < best_est) best = c, best_est = est;
+    }
+    std::vector<GemmBigTile> bt;
+    for (int j = 0; j < (int)big.size(); ++j)
+      for (int a = 0; a < (int)cdiv(big[j].m, shapes[best].bm); ++a)
+        for (int b = 0; b < (int)cdiv(big[j].n, shapes[best].bn); ++b) bt.push_back(GemmBigTile{j, a, b});
+    GemmJob *dj = sk.push(big);
+    GemmBigTile *dt = sk.push(bt);
+    const int nt = (int)bt.size(), grid = std::min(nt, shapes[best].slots);
+    sk.launch([=](cudaStream_t st) {
+      if (best == 0)
+        launch_pdl(k_gemm_big<2, 4, 8, 4, 4, 1>, dim3(grid), dim3(256), GemmBigCfg<2, 4, 8, 4, 4>::SMEM, st, dj, dt, nt);
+      else if (best == 1)
+        launch_pdl(k_gemm_big<4, 2, 4, 4, 3, 2>, dim3(grid), dim3(256), GemmBigCfg<4, 2, 4, 4, 3>::SMEM, st, dj, dt, nt);
+      else
+        launch_pdl(k_gemm_big<2, 4, 4, 4, 4, 2>, dim3(grid), dim3(256), GemmBigCfg<2, 4, 4, 4, 4>::SMEM, st, dj, dt, nt);
+      check_launch();
+    });
+    sk.ctx->big_gemm_jobs += (int64_t)big.size();
+  }
+  if (!lib.empty()) {
+    const std::vector<GemmJob> &big = lib;
     Ctx *ctx = sk.ctx;
     if (!ctx->blas) {
       if (cublasCreate(&ctx->blas) != CUBLAS_STATUS_SUCCESS) throw runtime_error("cublasCreate failed");
@@ -1044,6 +1114,12 @@ static void device_setup(Ctx *ctx) {
                             (int)(sizeof(double) * PANEL_ROWS_CL * PLD + PANEL_CL_SLOTS)));
     CK(cudaFuncSetAttribute(k_sample_rb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RB_DYN));
     CK(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_DYN));
+    CK(cudaFuncSetAttribute(k_gemm_big<2, 4, 8, 4, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)GemmBigCfg<2, 4, 8, 4, 4>::SMEM));
+    CK(cudaFuncSetAttribute(k_gemm_big<4, 2, 4, 4, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)GemmBigCfg<4, 2, 4, 4, 3>::SMEM));
+    CK(cudaFuncSetAttribute(k_gemm_big<2, 4, 4, 4, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)GemmBigCfg<2, 4, 4, 4, 4>::SMEM));
   }
   // 16-CTA clusters need the non-portable opt-in; without it the cluster
   // kernels run 8-CTA clusters
@@ -6445,13 +6521,17 @@ extern "C" int mfh_test_gemm_batched(mfh_ctx *ctx, int64_t batch, const int64_t 
     jobs.push_back(g);
   }
   Sink s{c};
-  g_split_k_override = split_k;
+  // split_k -2 / -3 / -4: large plain GEMMs on k_gemm (64 x 64 tiles) / cuBLAS / k_gemm_big
+  g_route_override = split_k == -2 ? 2 : (split_k == -3 ? 1 : (split_k == -4 ? 0 : -1));
+  g_split_k_override = split_k < 0 ? 0 : split_k;
   try {
     run_gemm(s, jobs);
   } catch (...) {
     g_split_k_override = -1;
+    g_route_override = -1;
     throw;
   }
+  g_route_override = -1;
   g_split_k_override = -1;
   CK(cudaMemcpyAsync(buf, d, sizeof(double) * total, cudaMemcpyDeviceToHost, c->s));
   CK(cudaStreamSynchronize(c->s));

@@ -3385,3 +3385,5 @@ __global__ void k_trsv_level(const int *__restrict__ rows, int nrows, const long
 }
 
 }  // namespace mfh
+
+#include "gemm_big.cuh"

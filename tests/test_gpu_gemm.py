@@ -98,9 +98,9 @@ def test_gemm_aliased_and_disjoint_blocks():
     np.testing.assert_array_equal(Fo[npv:, :npv], F[npv:, :npv])
 
 
-def test_gemm_identity_strip_and_cublas_route():
+def test_gemm_identity_strip_and_library_route():
     """An identity operand (DenseBlock.as_factors' eye, leading dimension -1)
-    is a scaled copy; a large plain GEMM goes to cuBLAS (rounding-level match)."""
+    is a scaled copy; a large plain GEMM goes to cuBLAS by default (rounding-level match)."""
     rng = np.random.default_rng(3)
     m, n = 33, 29
     B = rng.standard_normal((m, n))
@@ -115,3 +115,41 @@ def test_gemm_identity_strip_and_cublas_route():
     out = run([(big, big, big, 0, big * big, 2 * big * big, big, big, big, 1.0, 0.0)], buf)
     got = view(out, 2 * big * big, big, big, big)
     assert np.max(np.abs(got - A @ Bb)) <= 1e-12 * big * np.max(np.abs(A @ Bb))
+
+
+def test_large_gemm_kernel_bitwise_equals_tile_kernel():
+    """k_gemm_big (128-wide tiles, 16-byte cp.async slabs) runs the same k-ascending DMMA chain
+    and epilogue as k_gemm: the same bits on every large plain GEMM, for sizes ragged against
+    both tilings, odd leading dimensions (8-byte copy path), an odd buffer offset, alpha / beta
+    epilogues, and several jobs in one launch; and within rounding of cuBLAS."""
+    rng = np.random.default_rng(11)
+    shapes = [(600, 600, 600, 0, 1.0, 0.0), (513, 300, 901, 1, -1.0, 1.0), (1100, 129, 1003, 3, 0.5, -2.0),
+              (257, 2050, 300, 0, 1.0, 1.0), (640, 64, 2048, 0, 1.0, 0.0), (1024, 1024, 130, 2, -1.0, 1.0)]
+    parts, jobs, off = [], [], 1  # offset 1: operands 8-byte but not 16-byte aligned unless padded
+    parts.append(np.zeros(1))
+    for (m, n, k, pad, alpha, beta) in shapes:
+        lda, ldb, ldc = k + pad, n + pad, n + pad
+        if pad == 0 and off % 2:   # aligned jobs start on an even offset
+            parts.append(np.zeros(1))
+            off += 1
+        ao, bo, co = off, off + m * lda, off + m * lda + k * ldb
+        for sz in (m * lda, k * ldb, m * ldc):
+            parts.append(rng.standard_normal(sz))
+        off = co + m * ldc
+        if (m * lda + k * ldb + m * ldc) % 2 and pad == 0:
+            parts.append(np.zeros(1))
+            off += 1
+        jobs.append((m, n, k, ao, bo, co, lda, ldb, ldc, alpha, beta))
+    buf = np.concatenate(parts)
+    big = run(jobs, buf, -4)
+    tiles = run(jobs, buf, -2)
+    blas = run(jobs, buf, -3)
+    np.testing.assert_array_equal(big, tiles)
+    for (m, n, k, ao, bo, co, lda, ldb, ldc, alpha, beta) in jobs:
+        A, B, Cm = view(buf, ao, m, k, lda), view(buf, bo, k, n, ldb), view(buf, co, m, n, ldc)
+        ref = alpha * (A @ B) + beta * Cm
+        got = view(big, co, m, n, ldc)
+        assert np.max(np.abs(got - ref)) <= 1e-12 * k * np.max(np.abs(ref))
+        assert np.max(np.abs(got - view(blas, co, m, n, ldc))) <= 1e-12 * k * np.max(np.abs(ref))
+        if ldc > n:   # padding columns of C untouched
+            np.testing.assert_array_equal(big[co + n:co + m * ldc:ldc][:m - 1], buf[co + n:co + m * ldc:ldc][:m - 1])

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <array>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -262,6 +263,8 @@ struct Ctx {
   cudaStream_t side2 = nullptr;  // 8-CTA cluster cores, concurrently with the 16-CTA ones
   cudaStream_t side3 = nullptr;  // the cooperative grid-class cores when launched first
   cudaStream_t side4 = nullptr;  // the one-CTA pivot-LU cores, beside the dense fronts' work
+  cudaStream_t la = nullptr;     // blocked LU look-ahead: the next panel beside the trailing update
+  cudaEvent_t ev_la_cols = nullptr, ev_la_panel = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr, ev_join3 = nullptr;
   cudaEvent_t ev_fork2 = nullptr, ev_join4 = nullptr;
   cudaEvent_t gmres_ev[2] = {nullptr, nullptr};  // Hessenberg column read-backs (pipelined Arnoldi)
@@ -810,41 +813,50 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
   if (big.empty()) return;
   int maxn = 0;
   for (auto &j : big) maxn = std::max(maxn, j.n);
-  for (int c0 = 0; c0 < maxn; c0 += PNB) {
+  // Look-ahead (MFH_LU_LOOKAHEAD_MIN=<rows>: batches whose largest matrix has at least that many
+  // rows; off by default): the trailing update of step c0 is split into the next panel's columns
+  // and the rest; once the first part is done the next panel is factored on its own high-priority
+  // stream beside the rest of the update (which leaves the panel's columns alone), and the main
+  // stream picks the panel up before the next step's row swaps. The split only regroups output
+  // tiles: every entry keeps its k chain (bitwise equal, scripts/lu_lookahead_bench.py). Measured
+  // neutral on B200 (profiles/r2_ab_lu_lookahead.txt: C5 2.864 vs 2.859 s, C3 0.979 vs 0.992,
+  // one 4096^2 inverse 47.5 vs 48.6 ms): a height's panels already run as one launch of up to
+  // eight 16-CTA clusters, and a cluster does not get its 16 SMs while the update's grid is resident.
+  static const int la_min = getenv("MFH_LU_LOOKAHEAD_MIN") ? atoi(getenv("MFH_LU_LOOKAHEAD_MIN")) : INT_MAX;
+  const bool lookahead = !sk.record && maxn >= la_min;
+  Ctx *ctx = sk.ctx;
+  // panel factorization of columns [c0, c0 + w) of every job that has them; side: on the look-ahead stream
+  auto launch_panels = [&](int c0, bool side) {
     std::vector<PanelJob> pj;
-    std::vector<SwapJob> sw;
-    std::vector<TrsmJob> tr;
-    std::vector<GemmJob> gm;
     for (auto &j : big) {
       if (j.n <= c0) continue;
-      int w = std::min(PNB, j.n - c0);
-      pj.push_back(PanelJob{j.a, j.n, j.lda, c0, w, j.piv, j.flag});
-      sw.push_back(SwapJob{j.a, j.lda, j.n, j.piv, c0, c0 + w, c0, c0 + w});
-      int rest = j.n - c0 - w;
-      if (rest > 0) {
-        double *A11 = j.a + (int64_t)c0 * j.lda + c0;
-        tr.push_back(TrsmJob{A11, j.lda, w, A11 + w, j.lda, rest, 0});
-        gm.push_back(GemmJob{A11 + (int64_t)w * j.lda, A11 + w, A11 + (int64_t)w * j.lda + w, rest, rest, w, j.lda,
-                             j.lda, j.lda, -1.0, 1.0});
-      }
+      pj.push_back(PanelJob{j.a, j.n, j.lda, c0, std::min(PNB, j.n - c0), j.piv, j.flag});
     }
+    if (pj.empty()) return;
     PanelJob *dp = sk.push(pj);
     int np_ = (int)pj.size();
     int mmax = 0;
     for (auto &q : pj) mmax = std::max(mmax, q.n - q.c0);
     int cs = mmax <= PANEL_ROWS_MAX ? 1 : (mmax + PANEL_ROWS_CL - 1) / PANEL_ROWS_CL;
-    if (cs == 1) {
-      // every panel of the batch fits one CTA's shared memory
-      size_t smem = sizeof(double) * (size_t)mmax * PLD;
-      sk.launch([=](cudaStream_t s) {
+    cudaStream_t la = ctx->la;
+    cudaEvent_t e_cols = ctx->ev_la_cols, e_panel = ctx->ev_la_panel;
+    const int csmax = ctx->cluster_size;
+    sk.launch([=](cudaStream_t main) {
+      cudaStream_t s = main;
+      if (side) {  // after the next panel's columns have been updated on the main stream
+        CK(cudaEventRecord(e_cols, main));
+        CK(cudaStreamWaitEvent(la, e_cols, 0));
+        s = la;
+      }
+      if (cs == 1) {
+        // every panel of the batch fits one CTA's shared memory
+        size_t smem = sizeof(double) * (size_t)mmax * PLD;
         launch_pdl(k_getrf_panel_cta, dim3(np_), dim3(512), smem, s, dp);
         check_launch();
-      });
-    } else if (cs <= sk.ctx->cluster_size) {
-      // shared-memory resident panel across a cluster of cs CTAs
-      int rp = (mmax + cs - 1) / cs;
-      size_t smem = sizeof(double) * (size_t)rp * PLD + PANEL_CL_SLOTS;
-      sk.launch([=](cudaStream_t s) {
+      } else if (cs <= csmax) {
+        // shared-memory resident panel across a cluster of cs CTAs
+        int rp = (mmax + cs - 1) / cs;
+        size_t smem = sizeof(double) * (size_t)rp * PLD + PANEL_CL_SLOTS;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(np_ * cs);
         cfg.blockDim = dim3(512);
@@ -861,16 +873,55 @@ static void run_getrf(Sink &sk, const std::vector<LuJob> &jobs) {
         void *args[1] = {(void *)&arg};
         cudaError_t e = cudaLaunchKernelExC(&cfg, (const void *)k_getrf_panel_cl, args);
         if (e != cudaSuccess) throw runtime_error(std::string("panel cluster launch failed: ") + cudaGetErrorString(e));
-      });
-    } else {
-      sk.launch([=](cudaStream_t s) {
+      } else {
         launch_pdl(k_getrf_panel, dim3(np_), dim3(512), 0, s, dp);
         check_launch();
+      }
+      if (side) CK(cudaEventRecord(e_panel, la));
+    });
+  };
+  bool panel_ahead = false;  // this step's panel was launched on the look-ahead stream
+  for (int c0 = 0; c0 < maxn; c0 += PNB) {
+    std::vector<SwapJob> sw;
+    std::vector<TrsmJob> tr;
+    std::vector<GemmJob> gm, gm_next;
+    for (auto &j : big) {
+      if (j.n <= c0) continue;
+      int w = std::min(PNB, j.n - c0);
+      sw.push_back(SwapJob{j.a, j.lda, j.n, j.piv, c0, c0 + w, c0, c0 + w});
+      int rest = j.n - c0 - w;
+      if (rest > 0) {
+        double *A11 = j.a + (int64_t)c0 * j.lda + c0;
+        tr.push_back(TrsmJob{A11, j.lda, w, A11 + w, j.lda, rest, 0});
+        const double *L21 = A11 + (int64_t)w * j.lda, *U12 = A11 + w;
+        double *A22 = A11 + (int64_t)w * j.lda + w;
+        const int w2 = lookahead ? std::min(PNB, rest) : 0;  // the next panel's columns first
+        if (w2 > 0) gm_next.push_back(GemmJob{L21, U12, A22, rest, w2, w, j.lda, j.lda, j.lda, -1.0, 1.0});
+        if (rest > w2) gm.push_back(GemmJob{L21, U12 + w2, A22 + w2, rest, rest - w2, w, j.lda, j.lda, j.lda, -1.0, 1.0});
+      }
+    }
+    if (panel_ahead) {
+      cudaEvent_t e_panel = ctx->ev_la_panel;
+      sk.launch([=](cudaStream_t main) {
+        CK(cudaStreamWaitEvent(main, e_panel, 0));
+        ctx->launches--;  // not a kernel
       });
+    } else {
+      launch_panels(c0, false);
     }
     run_laswp(sk, sw);
     run_trsm(sk, tr);
+    panel_ahead = false;
+    if (!gm_next.empty()) {
+      run_gemm(sk, gm_next);
+      launch_panels(c0 + PNB, true);
+      panel_ahead = true;
+    }
     run_gemm(sk, gm);
+  }
+  if (panel_ahead) {  // (cannot happen: the last step has no trailing block) keep the streams joined anyway
+    cudaEvent_t e_panel = ctx->ev_la_panel;
+    sk.launch([=](cudaStream_t main) { CK(cudaStreamWaitEvent(main, e_panel, 0)); });
   }
   LuJob *dj = sk.push(big);
   int nb = (int)big.size();
@@ -4848,6 +4899,14 @@ extern "C" int mfh_ctx_create(int device, mfh_ctx **out) {
   CK(cudaStreamCreateWithFlags(&c->c.side2, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->c.side3, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->c.side4, cudaStreamNonBlocking));
+  {
+    // the look-ahead panel must get SMs while the trailing update's grid is still being issued
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&c->c.la, cudaStreamNonBlocking, hi));
+  }
+  CK(cudaEventCreateWithFlags(&c->c.ev_la_cols, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->c.ev_la_panel, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->c.ev_join3, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->c.ev_fork2, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->c.ev_join4, cudaEventDisableTiming));
@@ -4893,6 +4952,10 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   cudaStreamSynchronize(ctx->c.side2);
   cudaStreamSynchronize(ctx->c.side3);
   cudaStreamSynchronize(ctx->c.side4);
+  cudaStreamSynchronize(ctx->c.la);
+  cudaEventDestroy(ctx->c.ev_la_cols);
+  cudaEventDestroy(ctx->c.ev_la_panel);
+  cudaStreamDestroy(ctx->c.la);
   cudaEventDestroy(ctx->c.ev_join3);
   cudaEventDestroy(ctx->c.ev_fork2);
   cudaEventDestroy(ctx->c.ev_join4);

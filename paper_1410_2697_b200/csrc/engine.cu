@@ -4798,6 +4798,64 @@ struct mfh_precond {
   }
 };
 
+namespace mfh {
+// streamed SpMV (k_spmv_stream) of one CSR: rows per chunk, entry capacity of a stage, stages,
+// grid; R = 0: a row is too long to stream. The CSR arrays must carry the slack of the widened
+// bulk copies: 4 row pointers, 8 columns, 4 values past the end.
+struct SpmvStream {
+  int R = 0, cap = 0, grid = 0, nst = 2;
+  size_t smem = 0;
+  int *ptr32 = nullptr;  // 4-byte row pointers when nnz < 2^31
+};
+static void spmv_stream_plan(Ctx *ctx, int64_t n_rows, const long long *hptr, SpmvStream &P) {
+  const int64_t nnz = n_rows > 0 ? hptr[n_rows] : 0;
+  if (n_rows <= 0 || nnz <= 0) return;
+  int64_t maxrow = 0;
+  for (int64_t r = 0; r < n_rows; ++r) maxrow = std::max<int64_t>(maxrow, hptr[r + 1] - hptr[r]);
+  const char *eR = getenv("MFH_SPMV_R"), *eS = getenv("MFH_SPMV_STG"), *eP = getenv("MFH_SPMV_P64");  // tuning knobs
+  // chunk shape: the most rows R in {128, 64, 32} whose longest possible chunk fits a stage
+  // (measured: 128 rows x 7 entries, 128 x ~10, 64 x 27 beat the next larger chunk; a software-pipelined
+  // variant with the next chunk's gathers in registers and three stages was slower: fewer CTAs per SM)
+  int R = 0;
+  for (int cand : {128, 64, 32})
+    if ((!eR || cand <= atoi(eR)) && (int64_t)cand * maxrow <= (cand == 32 ? 8192 : 2048)) { R = cand; break; }
+  if (eR && atoi(eR) >= 256 && 256 * maxrow <= 4096) R = 256;
+  if (!R) return;
+  const bool p32 = nnz < (int64_t(1) << 31) && !eP;
+  P.R = R;
+  P.cap = (int)((R * maxrow + 1) & ~(int64_t)1);
+  P.nst = eS ? std::min(SPMV_MAX_STG, std::max(1, atoi(eS))) : 2;
+  P.smem = P.nst * spmv_stage_bytes(P.R, P.cap, p32 ? 4 : 8);
+  int per_sm = 0;
+  if (p32) {
+    std::vector<int> p4(hptr, hptr + n_rows + 1);
+    p4.resize(n_rows + 8, 0);
+    CK(cudaMalloc(&P.ptr32, sizeof(int) * (n_rows + 8)));
+    upload(ctx->s, P.ptr32, p4.data(), sizeof(int) * (n_rows + 8));
+    CK(cudaFuncSetAttribute(k_spmv_stream<int>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_stream<int>, 256, P.smem));
+  } else {
+    CK(cudaFuncSetAttribute(k_spmv_stream<long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_stream<long long>, 256, P.smem));
+  }
+  // persistent CTAs with the same number of chunks each (no partial last round)
+  const int64_t nchunks = cdiv(n_rows, (int64_t)R), gmax = (int64_t)ctx->nsm * std::max(1, per_sm);
+  P.grid = (int)cdiv(nchunks, cdiv(nchunks, gmax));
+}
+static void spmv_stream_launch(Ctx *ctx, const SpmvStream &P, int64_t n_rows, const long long *ptr, const int *col,
+                               const double *val, const double *x, const double *halo, int nl, double *y) {
+  const int64_t nchunks = cdiv(n_rows, (int64_t)P.R);
+  if (P.ptr32)
+    launch_pdl(k_spmv_stream<int>, dim3(P.grid), dim3(256), P.smem, ctx->s, (long long)n_rows, P.R, P.cap, P.nst,
+               (long long)nchunks, (const int *)P.ptr32, col, val, x, halo, nl, y);
+  else
+    launch_pdl(k_spmv_stream<long long>, dim3(P.grid), dim3(256), P.smem, ctx->s, (long long)n_rows, P.R, P.cap,
+               P.nst, (long long)nchunks, ptr, col, val, x, halo, nl, y);
+  check_launch();
+  ctx->launches++;
+}
+}  // namespace mfh
+
 struct mfh_csr {
   mfh::Ctx *ctx = nullptr;
   int kind = 0;  // 0 csr, 1 dense
@@ -4806,10 +4864,7 @@ struct mfh_csr {
   int *col = nullptr;
   double *val = nullptr;
   mfh::GemmJob *djob = nullptr;  // dense GEMV descriptor (x/y patched per call)
-  // streamed SpMV (k_spmv_stream): rows per chunk, entry capacity of a stage, grid; R = 0: rows too long
-  int sR = 0, scap = 0, sgrid = 0, snst = 2;
-  size_t ssmem = 0;
-  int *ptr32 = nullptr;  // 4-byte row pointers for the streamed SpMV when nnz < 2^31
+  mfh::SpmvStream stream;  // streamed SpMV plan (R = 0: rows too long, k_spmv_sub instead)
 };
 
 namespace mfh {
@@ -4821,16 +4876,8 @@ static void op_apply_device(mfh_csr *A, const double *x, double *y) {
     const int64_t nnz = A->nnz;
     const double avg = A->nr ? (double)nnz / A->nr : 0.0;
     static const bool no_stream = getenv("MFH_SPMV_NO_STREAM") != nullptr;  // A/B knob
-    if (A->sR > 0 && !no_stream) {
-      const int64_t nchunks = cdiv(A->nr, (int64_t)A->sR);
-      if (A->ptr32)
-        k_spmv_stream<int><<<A->sgrid, 256, A->ssmem, ctx->s>>>(A->nr, A->sR, A->scap, A->snst, nchunks, A->ptr32,
-                                                                 A->col, A->val, x, y);
-      else
-        k_spmv_stream<long long><<<A->sgrid, 256, A->ssmem, ctx->s>>>(A->nr, A->sR, A->scap, A->snst, nchunks,
-                                                                       A->ptr, A->col, A->val, x, y);
-      check_launch();
-      ctx->launches++;
+    if (A->stream.R > 0 && !no_stream) {
+      spmv_stream_launch(ctx, A->stream, A->nr, A->ptr, A->col, A->val, x, x, INT_MAX, y);
       return;
     }
     const int W = avg <= 4.5 ? 4 : (avg <= 9.5 ? 8 : (avg <= 20 ? 16 : 32));
@@ -5435,40 +5482,7 @@ extern "C" int mfh_csr_create(mfh_ctx *ctx, int64_t n_rows, int64_t n_cols, cons
   CK(cudaMemsetAsync(A->col + nnz, 0, sizeof(int) * 8, A->ctx->s));
   CK(cudaMemsetAsync(A->val + nnz, 0, sizeof(double) * 4, A->ctx->s));
   std::vector<int> c32(indices, indices + nnz);
-  {
-    // chunk shape: the most rows R in {128, 64, 32} whose longest possible chunk fits a stage
-    int64_t maxrow = 0;
-    for (int64_t r = 0; r < n_rows; ++r) maxrow = std::max(maxrow, indptr[r + 1] - indptr[r]);
-    const char *eR = getenv("MFH_SPMV_R"), *eS = getenv("MFH_SPMV_STG"), *eP = getenv("MFH_SPMV_P64");  // tuning knobs
-    int R = 0;
-    // (measured: 128 rows x 7 entries, 128 x ~10, 64 x 27 beat the next larger chunk; a software-pipelined
-    // variant with the next chunk's gathers in registers and three stages was slower: fewer CTAs per SM)
-    for (int cand : {128, 64, 32})
-      if ((!eR || cand <= atoi(eR)) && (int64_t)cand * maxrow <= (cand == 32 ? 8192 : 2048)) { R = cand; break; }
-    if (eR && atoi(eR) >= 256 && 256 * maxrow <= 4096) R = 256;
-    if (R && n_rows > 0 && nnz > 0) {
-      const bool p32 = nnz < (int64_t(1) << 31) && !eP;
-      A->sR = R;
-      A->scap = (int)((R * maxrow + 1) & ~(int64_t)1);
-      A->snst = eS ? std::min(SPMV_MAX_STG, std::max(1, atoi(eS))) : 2;
-      A->ssmem = A->snst * spmv_stage_bytes(A->sR, A->scap, p32 ? 4 : 8);
-      int per_sm = 0;
-      if (p32) {
-        std::vector<int> p4(indptr, indptr + n_rows + 1);
-        p4.resize(n_rows + 8, 0);
-        CK(cudaMalloc(&A->ptr32, sizeof(int) * (n_rows + 8)));
-        upload(A->ctx->s, A->ptr32, p4.data(), sizeof(int) * (n_rows + 8));
-        CK(cudaFuncSetAttribute(k_spmv_stream<int>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)A->ssmem));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_stream<int>, 256, A->ssmem));
-      } else {
-        CK(cudaFuncSetAttribute(k_spmv_stream<long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)A->ssmem));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_stream<long long>, 256, A->ssmem));
-      }
-      // persistent CTAs with the same number of chunks each (no partial last round)
-      const int64_t nchunks = cdiv(n_rows, (int64_t)R), gmax = (int64_t)A->ctx->nsm * std::max(1, per_sm);
-      A->sgrid = (int)cdiv(nchunks, cdiv(nchunks, gmax));
-    }
-  }
+  spmv_stream_plan(A->ctx, n_rows, reinterpret_cast<const long long *>(indptr), A->stream);
   upload(A->ctx->s, A->ptr, indptr, sizeof(int64_t) * (n_rows + 1));
   if (nnz) {
     upload(A->ctx->s, A->col, c32.data(), sizeof(int) * nnz);
@@ -5499,7 +5513,7 @@ extern "C" void mfh_csr_free(mfh_csr *A) {
   DeviceGuard dg_(A->ctx->device);
   cudaStreamSynchronize(A->ctx->s);
   cudaFree(A->ptr);
-  cudaFree(A->ptr32);
+  cudaFree(A->stream.ptr32);
   cudaFree(A->col);
   cudaFree(A->val);
   delete A;
@@ -6002,8 +6016,10 @@ struct DistSys {
   long long *hown_pos = nullptr, *hown_loc = nullptr;  // halo entries this rank owns: buffer slot, local index
   int64_t nhown = 0;
   int W = 8;
+  SpmvStream stream;  // streamed SpMV plan of the local CSR
   ~DistSys() {
-    for (void *q : {(void *)lpos, (void *)ptr, (void *)col, (void *)val, (void *)hown_pos, (void *)hown_loc})
+    for (void *q : {(void *)lpos, (void *)ptr, (void *)col, (void *)val, (void *)hown_pos, (void *)hown_loc,
+                    (void *)stream.ptr32})
       cudaFree(q);
   }
 };
@@ -6066,6 +6082,11 @@ static std::unique_ptr<DistSys> dist_build(mfh_factor *F, int64_t n, const int64
   D->nhown = (int64_t)hp.size();
   const double avg = D->nl ? (double)lc.size() / D->nl : 0.0;
   D->W = avg <= 4.5 ? 4 : (avg <= 9.5 ? 8 : (avg <= 20 ? 16 : 32));
+  spmv_stream_plan(ctx, D->nl, lp.data(), D->stream);
+  // slack of the streamed SpMV's widened bulk copies
+  lp.resize(lp.size() + 4, 0);
+  lc.resize(lc.size() + 8, 0);
+  lv.resize(lv.size() + 4, 0.0);
   auto upv = [&](auto **dst, const auto &v) {
     CK(cudaMalloc(dst, sizeof(v[0]) * std::max<size_t>(1, v.size())));
     upload(ctx->s, *dst, v.data(), sizeof(v[0]) * v.size());
@@ -6104,6 +6125,11 @@ struct DistGmres {
         ctx->launches += 2;
       }
       allreduce(halo, D->nh);
+    }
+    static const bool no_stream = getenv("MFH_SPMV_NO_STREAM") != nullptr;
+    if (D->stream.R > 0 && !no_stream) {
+      spmv_stream_launch(ctx, D->stream, nl, D->ptr, D->col, D->val, x, halo ? halo : x, (int)nl, y);
+      return;
     }
     const int grid = (int)std::min<int64_t>(cdiv(std::max<int64_t>(1, nl) * D->W, 256), 148 * 16);
     switch (D->W) {

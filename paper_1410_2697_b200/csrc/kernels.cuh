@@ -3278,7 +3278,9 @@ template <typename PT>
 __global__ void __launch_bounds__(256) k_spmv_stream(long long nrows, int R, int cap, int nst, long long nchunks,
                                                      const PT *__restrict__ ptr, const int *__restrict__ col,
                                                      const double *__restrict__ val, const double *__restrict__ x,
-                                                     double *__restrict__ y) {
+                                                     const double *__restrict__ halo, int nl, double *__restrict__ y) {
+  // column j < nl reads x[j], j >= nl the halo buffer (distributed SpMV: other ranks' separator
+  // values); a plain SpMV passes nl = INT_MAX
   extern __shared__ __align__(128) unsigned char spmv_smem[];
   __shared__ unsigned long long bar[SPMV_MAX_STG];
   constexpr int PB = (int)sizeof(PT), PA = 16 / PB;  // pointers per 16 bytes
@@ -3308,6 +3310,7 @@ __global__ void __launch_bounds__(256) k_spmv_stream(long long nrows, int R, int
     if (bv) tma_bulk_g2s(sval(s), val + v0, bv, &bar[s]);
     if (bc) tma_bulk_g2s(scol(s), col + c0, bc, &bar[s]);
   };
+  auto xin = [&](int j) { return j < nl ? __ldg(x + j) : __ldg(halo + (j - nl)); };
   const long long G = gridDim.x;
   long long np0 = 0, np1 = 0;  // thread 0: entry range of the chunk it issues next
   if (tid == 0) {
@@ -3316,6 +3319,10 @@ __global__ void __launch_bounds__(256) k_spmv_stream(long long nrows, int R, int
       if (c < nchunks) issue(c, s, (long long)__ldg(ptr + c * R), (long long)__ldg(ptr + min(nrows, (c + 1) * R)));
     }
   }
+  // programmatic dependent launch: the matrix never changes, so the first stages are already
+  // streaming in while the preceding kernel (the producer of x) drains; x and y only after the wait
+  pdl_wait();
+  pdl_trigger();
   int s = 0;
   unsigned par = 0;
   for (long long c = blockIdx.x; c < nchunks; c += G) {
@@ -3335,13 +3342,13 @@ __global__ void __launch_bounds__(256) k_spmv_stream(long long nrows, int R, int
       long long p = p0 + tid;
       for (; p + 768 < p1; p += 1024) {  // four independent gathers in flight per thread
         const int j0 = sc[p], j1 = sc[p + 256], j2 = sc[p + 512], j3 = sc[p + 768];
-        const double x0 = __ldg(x + j0), x1 = __ldg(x + j1), x2 = __ldg(x + j2), x3 = __ldg(x + j3);
+        const double x0 = xin(j0), x1 = xin(j1), x2 = xin(j2), x3 = xin(j3);
         sv[p] = __dmul_rn(sv[p], x0);
         sv[p + 256] = __dmul_rn(sv[p + 256], x1);
         sv[p + 512] = __dmul_rn(sv[p + 512], x2);
         sv[p + 768] = __dmul_rn(sv[p + 768], x3);
       }
-      for (; p < p1; p += 256) sv[p] = __dmul_rn(sv[p], __ldg(x + sc[p]));
+      for (; p < p1; p += 256) sv[p] = __dmul_rn(sv[p], xin(sc[p]));
     }
     __syncthreads();
     for (int r = tid; r < rows; r += 256) {

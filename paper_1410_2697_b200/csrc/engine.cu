@@ -2188,7 +2188,7 @@ struct Factorizer {
       SampleTiles T{drid[0], dpre[0], (int)rid[0].size(), pre[0].back()};
       int grid = (int)std::min<int64_t>(T.ntiles, 148 * 32);
       s.launch([=](cudaStream_t st) {
-        launch_pdl(k_sample, dim3(grid), dim3(SAMPLE_TC, SAMPLE_TR), 0, st, dr, T, fF, fC, pp, pc, pv);
+        launch_pdl(k_sample, dim3(grid), dim3(SAMPLE_TC, SAMPLE_TRB), 0, st, dr, T, fF, fC, pp, pc, pv);
         check_launch();
       });
     }
@@ -4832,11 +4832,13 @@ static void spmv_stream_plan(Ctx *ctx, int64_t n_rows, const long long *hptr, Sp
     p4.resize(n_rows + 8, 0);
     CK(cudaMalloc(&P.ptr32, sizeof(int) * (n_rows + 8)));
     upload(ctx->s, P.ptr32, p4.data(), sizeof(int) * (n_rows + 8));
-    CK(cudaFuncSetAttribute(k_spmv_stream<int>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_stream<int>, 256, P.smem));
+    CK(cudaFuncSetAttribute(k_spmv_stream<int, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+    CK(cudaFuncSetAttribute(k_spmv_stream<int, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_stream<int, true>, 256, P.smem));
   } else {
-    CK(cudaFuncSetAttribute(k_spmv_stream<long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_stream<long long>, 256, P.smem));
+    CK(cudaFuncSetAttribute(k_spmv_stream<long long, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+    CK(cudaFuncSetAttribute(k_spmv_stream<long long, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_stream<long long, true>, 256, P.smem));
   }
   // persistent CTAs with the same number of chunks each (no partial last round)
   const int64_t nchunks = cdiv(n_rows, (int64_t)R), gmax = (int64_t)ctx->nsm * std::max(1, per_sm);
@@ -4845,12 +4847,17 @@ static void spmv_stream_plan(Ctx *ctx, int64_t n_rows, const long long *hptr, Sp
 static void spmv_stream_launch(Ctx *ctx, const SpmvStream &P, int64_t n_rows, const long long *ptr, const int *col,
                                const double *val, const double *x, const double *halo, int nl, double *y) {
   const int64_t nchunks = cdiv(n_rows, (int64_t)P.R);
-  if (P.ptr32)
-    launch_pdl(k_spmv_stream<int>, dim3(P.grid), dim3(256), P.smem, ctx->s, (long long)n_rows, P.R, P.cap, P.nst,
-               (long long)nchunks, (const int *)P.ptr32, col, val, x, halo, nl, y);
-  else
-    launch_pdl(k_spmv_stream<long long>, dim3(P.grid), dim3(256), P.smem, ctx->s, (long long)n_rows, P.R, P.cap,
-               P.nst, (long long)nchunks, ptr, col, val, x, halo, nl, y);
+  auto go = [&](auto kern, auto p) {
+    launch_pdl(kern, dim3(P.grid), dim3(256), P.smem, ctx->s, (long long)n_rows, P.R, P.cap, P.nst, (long long)nchunks,
+               p, col, val, x, halo ? halo : x, nl, y);
+  };
+  if (P.ptr32) {
+    if (halo) go(k_spmv_stream<int, true>, (const int *)P.ptr32);
+    else go(k_spmv_stream<int, false>, (const int *)P.ptr32);
+  } else {
+    if (halo) go(k_spmv_stream<long long, true>, ptr);
+    else go(k_spmv_stream<long long, false>, ptr);
+  }
   check_launch();
   ctx->launches++;
 }
@@ -4877,7 +4884,7 @@ static void op_apply_device(mfh_csr *A, const double *x, double *y) {
     const double avg = A->nr ? (double)nnz / A->nr : 0.0;
     static const bool no_stream = getenv("MFH_SPMV_NO_STREAM") != nullptr;  // A/B knob
     if (A->stream.R > 0 && !no_stream) {
-      spmv_stream_launch(ctx, A->stream, A->nr, A->ptr, A->col, A->val, x, x, INT_MAX, y);
+      spmv_stream_launch(ctx, A->stream, A->nr, A->ptr, A->col, A->val, x, nullptr, 0, y);
       return;
     }
     const int W = avg <= 4.5 ? 4 : (avg <= 9.5 ? 8 : (avg <= 20 ? 16 : 32));
@@ -6128,7 +6135,7 @@ struct DistGmres {
     }
     static const bool no_stream = getenv("MFH_SPMV_NO_STREAM") != nullptr;
     if (D->stream.R > 0 && !no_stream) {
-      spmv_stream_launch(ctx, D->stream, nl, D->ptr, D->col, D->val, x, halo ? halo : x, (int)nl, y);
+      spmv_stream_launch(ctx, D->stream, nl, D->ptr, D->col, D->val, x, D->nh ? halo : nullptr, (int)nl, y);
       return;
     }
     const int grid = (int)std::min<int64_t>(cdiv(std::max<int64_t>(1, nl) * D->W, 256), 148 * 16);

@@ -200,7 +200,10 @@ __device__ __forceinline__ double seed_entry(const long long *Ap_ptr, const int 
 // value = seed(r,c) [+ child_1] [+ child_2] ... in node.children order;
 // child value = HODLR entry - W[r,:] . V[c,:]
 // ---------------------------------------------------------------------------
-constexpr int SAMPLE_TR = 8, SAMPLE_TC = 32;
+// a tile is SAMPLE_TR x SAMPLE_TC entries for a block of SAMPLE_TRB x SAMPLE_TC threads: a thread
+// keeps its column (and the column's position in the first children) over SAMPLE_TR / SAMPLE_TRB
+// rows, and the tile decode and descriptor loads are paid once per tile
+constexpr int SAMPLE_TR = 64, SAMPLE_TRB = 8, SAMPLE_TC = 32;
 
 // Tile t of a sampling batch: request rids[p] with tpre[p] <= t < tpre[p + 1]
 // (the host sends the per-request tile prefix, not one descriptor per tile)
@@ -231,36 +234,45 @@ __global__ void k_sample(const SReq *__restrict__ reqs, SampleTiles tiles,
   for (long long t = blockIdx.x; t < tiles.ntiles; t += gridDim.x) {
     const int2 tl = sample_tile(tiles, t);
     const SReq rq = reqs[tl.x];
-    int tpr = (rq.nc + SAMPLE_TC - 1) / SAMPLE_TC;
-    int i = (tl.y / tpr) * SAMPLE_TR + threadIdx.y;
-    int j = (tl.y % tpr) * SAMPLE_TC + threadIdx.x;
-    if (i >= rq.nr || j >= rq.nc) continue;
-    int r = rq.rows ? rq.rows[i] : rq.r0 + i;
-    int c = rq.cols ? rq.cols[j] : rq.c0 + j;
+    const int tpr = (rq.nc + SAMPLE_TC - 1) / SAMPLE_TC;
+    const int i0 = (tl.y / tpr) * SAMPLE_TR;
+    const int j = (tl.y % tpr) * SAMPLE_TC + threadIdx.x;
+    if (j >= rq.nc) continue;
+    const int c = rq.cols ? rq.cols[j] : rq.c0 + j;
     const DFront F = fronts[rq.front];
-    double v = 0.0;
-    if (r < F.npv || c < F.npv) v = seed_entry(Ap_ptr, Ap_col, Ap_val, F.ids[r], F.ids[c]);
-    for (int q = F.child_begin; q < F.child_end; ++q) {
-      const DChild &ch = kids[q];
-      int cr = ch.to_child[r];
-      if (cr < 0) continue;
-      int cc = ch.to_child[c];
-      if (cc < 0) continue;
-      double sub;
-      if (ch.kind == 0) {
-        sub = ch.dense[(long long)cr * ch.ldd + cc];
-      } else {
-        sub = hodlr_entry(ch.hn, ch.n, cr, cc);
-        if (ch.rw) {
-          double s = 0.0;
-          const double *w = ch.W + (long long)cr * ch.ldw;
-          for (int u = 0; u < ch.rw; ++u) s = fma(w[u], ch.Vt[(long long)u * ch.ldv + cc], s);
-          sub = sub - s;
+    // the column's position in the first two children (most fronts have two)
+    const int nch = F.child_end - F.child_begin;
+    const int cc0 = nch > 0 ? kids[F.child_begin].to_child[c] : -1;
+    const int cc1 = nch > 1 ? kids[F.child_begin + 1].to_child[c] : -1;
+    const long long gc = F.ids[c];
+    for (int ii = threadIdx.y; ii < SAMPLE_TR; ii += SAMPLE_TRB) {
+      const int i = i0 + ii;
+      if (i >= rq.nr) break;
+      const int r = rq.rows ? rq.rows[i] : rq.r0 + i;
+      double v = 0.0;
+      if (r < F.npv || c < F.npv) v = seed_entry(Ap_ptr, Ap_col, Ap_val, F.ids[r], gc);
+      for (int q = F.child_begin; q < F.child_end; ++q) {
+        const DChild &ch = kids[q];
+        const int cc = (q == F.child_begin) ? cc0 : (q == F.child_begin + 1 ? cc1 : ch.to_child[c]);
+        if (cc < 0) continue;
+        const int cr = ch.to_child[r];
+        if (cr < 0) continue;
+        double sub;
+        if (ch.kind == 0) {
+          sub = ch.dense[(long long)cr * ch.ldd + cc];
+        } else {
+          sub = hodlr_entry(ch.hn, ch.n, cr, cc);
+          if (ch.rw) {
+            double s = 0.0;
+            const double *w = ch.W + (long long)cr * ch.ldw;
+            for (int u = 0; u < ch.rw; ++u) s = fma(w[u], ch.Vt[(long long)u * ch.ldv + cc], s);
+            sub = sub - s;
+          }
         }
+        v = v + sub;
       }
-      v = v + sub;
+      rq.out[(long long)i * rq.ld + j] = v;
     }
-    rq.out[(long long)i * rq.ld + j] = v;
   }
 }
 
@@ -3274,13 +3286,13 @@ __host__ __device__ inline size_t spmv_stage_bytes(int R, int cap, int ptr_bytes
 }
 
 // PT: the row-pointer type streamed (int when nnz < 2^31: the 4-byte pointers of the byte count)
-template <typename PT>
+template <typename PT, bool HALO>
 __global__ void __launch_bounds__(256) k_spmv_stream(long long nrows, int R, int cap, int nst, long long nchunks,
                                                      const PT *__restrict__ ptr, const int *__restrict__ col,
                                                      const double *__restrict__ val, const double *__restrict__ x,
                                                      const double *__restrict__ halo, int nl, double *__restrict__ y) {
-  // column j < nl reads x[j], j >= nl the halo buffer (distributed SpMV: other ranks' separator
-  // values); a plain SpMV passes nl = INT_MAX
+  // HALO: column j < nl reads x[j], j >= nl the halo buffer (distributed SpMV: other ranks'
+  // separator values)
   extern __shared__ __align__(128) unsigned char spmv_smem[];
   __shared__ unsigned long long bar[SPMV_MAX_STG];
   constexpr int PB = (int)sizeof(PT), PA = 16 / PB;  // pointers per 16 bytes
@@ -3310,7 +3322,7 @@ __global__ void __launch_bounds__(256) k_spmv_stream(long long nrows, int R, int
     if (bv) tma_bulk_g2s(sval(s), val + v0, bv, &bar[s]);
     if (bc) tma_bulk_g2s(scol(s), col + c0, bc, &bar[s]);
   };
-  auto xin = [&](int j) { return j < nl ? __ldg(x + j) : __ldg(halo + (j - nl)); };
+  auto xin = [&](int j) { return (!HALO || j < nl) ? __ldg(x + j) : __ldg(halo + (j - nl)); };
   const long long G = gridDim.x;
   long long np0 = 0, np1 = 0;  // thread 0: entry range of the chunk it issues next
   if (tid == 0) {

@@ -273,6 +273,7 @@ struct Ctx {
   int nsm = 148;
   ChunkPool pool;
   std::vector<cudaEvent_t> evpool;  // per-height phase events, reused
+  std::vector<cudaEvent_t> evd_pool;  // per height: end of the child-update materialization (trace)
   Stage stage;
   Arena scratch;
   double *d_part = nullptr;  // reduction partials
@@ -1719,10 +1720,13 @@ struct Factorizer {
   int *d_ap_col = nullptr;
   double *d_ap_val = nullptr;
   const Graph *gp = nullptr;  // BDLR graph over permuted ids (cached on the etree)
-  // selection scratch
-  std::vector<int64_t> mark;
-  int64_t stamp = 0;
-  std::vector<int> distv;
+  // selection scratch, one per selection thread
+  struct SelScratch {
+    std::vector<int64_t> mark;
+    int64_t stamp = 0;
+    std::vector<int> distv;
+  };
+  std::vector<SelScratch> sel_scratch;
   // error flags
   int *d_flags = nullptr;
   int nflags = 0;
@@ -1732,9 +1736,12 @@ struct Factorizer {
   Sink sk() { return Sink{ctx}; }
 
   // ---- selection (bdlr.py:89-136), positions are front-local ----
-  void select(const FrontH &f, int r0, int m, int c0, int nn, std::vector<int> &I,
+  void select(SelScratch &sc, const FrontH &f, int r0, int m, int c0, int nn, std::vector<int> &I,
               std::vector<int> &J) {
     const Graph &graph = *gp;
+    std::vector<int64_t> &mark = sc.mark;
+    std::vector<int> &distv = sc.distv;
+    int64_t &stamp = sc.stamp;
     I.clear();
     J.clear();
     const int64_t *ids = f.ids.data();
@@ -1909,10 +1916,42 @@ struct Factorizer {
     }
     if (f.nf) f.ff = make_tree(fi, f.npv, f.nf, blist, f.tree_base + 1, 1);
     F->front_blocks[fi] = blist;
-    for (int bi : blist) {
-      BlockH &b = F->blocks[bi];
-      select(f, b.r0, b.m, b.c0, b.n, b.I, b.J);
+    // The blocks' selections are independent (each writes its own I / J): spread over
+    // MFH_PLAN_THREADS host threads (default: half the cores, at most 16), each with its own
+    // marker arrays. At C3 one thread could not stay ahead of the GPU: the structured heights
+    // waited 67-115 ms each for their selections (MFH_HEIGHT_TRACE: gap minus materialization).
+    if (sel_scratch.empty()) sel_scratch.resize(1);
+    const int nthreads = (int)sel_scratch.size();
+    std::atomic<size_t> next{0};
+    std::exception_ptr err;
+    std::mutex err_mu;
+    auto work = [&](int t) {
+      try {
+        for (size_t q; (q = next.fetch_add(1, std::memory_order_relaxed)) < blist.size();) {
+          BlockH &b = F->blocks[blist[q]];
+          select(sel_scratch[t], f, b.r0, b.m, b.c0, b.n, b.I, b.J);
+        }
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        if (!err) err = std::current_exception();
+      }
+    };
+    // threads by the front's selection work (graph edges visited ~ vertices x degree^d): a thread
+    // is worth spawning for ~2M edge visits; the small fronts of C1 / C2 / C4 stay on one thread
+    double edges = 0.0;
+    {
+      const Graph &graph = *gp;
+      const double deg = graph.n ? (double)graph.ptr[graph.n] / (double)graph.n : 1.0;
+      double per = 1.0;
+      for (int q = 0; q < std::max(1, (int)P.d); ++q) per *= std::max(1.0, deg);
+      for (int bi : blist) edges += ((double)F->blocks[bi].m + F->blocks[bi].n) * per;
     }
+    const int use = (int)std::max<double>(1.0, std::min<double>(std::min<double>(nthreads, blist.size()), edges / 2e6));
+    std::vector<std::thread> pool;
+    for (int t = 1; t < use; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto &th : pool) th.join();
+    if (err) std::rethrow_exception(err);
   }
 
   static int count_internal(int64_t n, int64_t nl) {
@@ -1927,6 +1966,12 @@ struct Factorizer {
   std::vector<int> plan_order, plan_pos;
   std::exception_ptr plan_error;
   void start_planner() {
+    {
+      const char *e = getenv("MFH_PLAN_THREADS");
+      const unsigned hc = std::thread::hardware_concurrency();
+      int k = e ? atoi(e) : (int)std::min(16u, std::max(1u, hc / 2));
+      sel_scratch.resize((size_t)std::max(1, k));
+    }
     planner = std::thread([this]() {
       try {
         for (int fi : plan_order) {
@@ -2282,6 +2327,7 @@ struct Factorizer {
   // ---- one height ----
   // host clock when each phase event was enqueued (MFH_HEIGHT_TRACE)
   std::chrono::steady_clock::time_point hts[8];
+  cudaEvent_t cur_evd = nullptr;  // recorded after the height's child updates have been materialized
   void process_height(const std::vector<int> &fis, cudaEvent_t *ev) {
     const auto h_t0 = std::chrono::steady_clock::now();
     for (auto &t : hts) t = h_t0;
@@ -2295,6 +2341,7 @@ struct Factorizer {
     // while the host builds this height's requests; it shows as the gap before
     // the sample phase)
     build_fronts_dev(s, fis, dfr, dch, slot);
+    if (cur_evd) cudaEventRecord(cur_evd, ctx->s);
     DFront *dF = nullptr;  // pushed with the first sampling batch below
     DChild *dC = nullptr;
 
@@ -3817,6 +3864,12 @@ struct Factorizer {
         ctx->evpool.push_back(e);
       }
       cudaEvent_t *ev = ctx->evpool.data() + 8 * used;
+      while ((int)ctx->evd_pool.size() < used + 1) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        ctx->evd_pool.push_back(e);
+      }
+      cur_evd = ctx->evd_pool[used];
       ++used;
       height_of_use.push_back(h);
       {
@@ -3870,8 +3923,12 @@ struct Factorizer {
       if (htrace) {
         float a[7] = {0, 0, 0, 0, 0, 0, 0}, gap = 0.f;
         for (int q = 0; q < (donly ? 2 : 7); ++q) CK(cudaEventElapsedTime(&a[q], ev[q], ev[q + 1]));
-        if (u > 0)
+        float dens = 0.f;
+        if (u > 0) {
           CK(cudaEventElapsedTime(&gap, ctx->evpool[8 * (u - 1) + (struct_of_use[u - 1] ? 7 : 2)], ev[0]));
+          CK(cudaEventElapsedTime(&dens, ctx->evpool[8 * (u - 1) + (struct_of_use[u - 1] ? 7 : 2)], ctx->evd_pool[u]));
+        }
+        fprintf(stderr, "[mfh height %3d] materialize %7.3f of the gap\n", height_of_use[u], dens);
         fprintf(stderr, "[mfh height %3d] fronts %4zu struct %2d | gap %7.3f sample %7.3f dense %7.3f plu %7.3f - %7.3f skel %7.3f hodlr %7.3f elim %7.3f ms | first npv %d nf %d kids %d, aliased %d | host %.1f us, decide %.1f us\n",
                 height_of_use[u], byh[height_of_use[u]].size(), struct_of_use[u], gap, a[0], a[1], a[2], a[3], a[4], a[5], a[6],
                 first_of_use[u][0], first_of_use[u][1], first_of_use[u][2], first_of_use[u][3], host_us_of_use[u],
@@ -4988,6 +5045,7 @@ extern "C" void mfh_ctx_destroy(mfh_ctx *ctx) {
   ctx->c.scratch.release();
   ctx->c.pool.release();
   for (auto e : ctx->c.evpool) cudaEventDestroy(e);
+  for (auto e : ctx->c.evd_pool) cudaEventDestroy(e);
   cudaFree(ctx->c.d_part);
   cudaFree(ctx->c.d_scal);
   if (ctx->c.blas) cublasDestroy(ctx->c.blas);

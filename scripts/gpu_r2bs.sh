@@ -1,0 +1,18 @@
+#!/bin/bash
+set -u
+O=gpurun_out/bs; mkdir -p $O
+export PYTHONFAULTHANDLER=1
+echo "host cores: $(nproc)"
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider --timeout 600 > $O/pytest.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest.log
+for c in c3 c5 c4 c2; do
+  for t in default 1; do
+    if [ $t = default ]; then unset MFH_PLAN_THREADS; else export MFH_PLAN_THREADS=$t; fi
+    timeout 900 python bench.py --config $c --steps 3 --warmup 2 --no-cpu-baseline > $O/bench_${c}_$t.log 2>&1; echo "bench $c threads $t rc=$?"
+    python - <<PY
+import json
+l=[x for x in open("$O/bench_${c}_$t.log") if x.startswith("{")]
+d=json.loads(l[-1]); f=d["factor"]
+print("$c plan threads $t", round(d["value"],4), "factor", round(d["split_s"]["factor_s"],4), "device_ms", round(f["device_ms"],1), "phases", round(sum(f["phases_ms"].values()),1), "its", d["gmres"]["iterations"])
+PY
+  done
+done

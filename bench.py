@@ -133,6 +133,8 @@ def phase_rooflines(tim, hbm, fp64, apply_ms, apply_bytes, spmv_ms, nnz, n):
       eliminate     ref a16: 2 r_pf S_pp + 2 r_fp n_p r_pf + 2 nf r_fp r_pf
       hodlr_front   a14 + a16 over both phases' time: BASELINE's "HODLR front GFLOP/s"
       dense_front   ref a5: (2/3) n_p^3 + 2 n_p^2 nf + 2 n_p nf^2
+      materialize   executed flops of writing child updates out as dense blocks (no reference
+                    count: the reference samples them entry by entry)
       apply         8 sum(2 S_pp + S_pf + S_fp) + 32 N (the engine's own read
                     bytes beside it)
       spmv          12 nnz + 4 (N + 1) + 16 N
@@ -168,10 +170,16 @@ def phase_rooflines(tim, hbm, fp64, apply_ms, apply_bytes, spmv_ms, nnz, n):
         out["hodlr_front"]["gflops"] = out["hodlr_front"]["achieved"] * 1e3
         out["hodlr_front"]["ref_gflops"] = out["hodlr_front"]["ref_tflops"] * 1e3
     fp("dense_front", ex["dense"], tim["dense_flops"], tim["dense_front_ms"])
+    # child updates written out as dense blocks for their parents' sampling (part of a7's work
+    # in this engine; the reference samples the HODLR / low-rank form entry by entry instead)
+    if tim.get("materialize_ms", 0.0) > 0:
+        put("materialize", tim.get("exec_flops_materialize", 0.0), tim["materialize_ms"], "TFLOP/s", fp64,
+            note="extend-add: child updates materialized before the parent's height samples them")
     put("apply", tim["apply_ref_bytes"], apply_ms, "GB/s", hbm, engine_bytes=apply_bytes,
         engine_gbs=apply_bytes / (apply_ms * 1e-3) / 1e9 if apply_ms > 0 else None)
     put("spmv", 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n, spmv_ms, "GB/s", hbm)
-    fac = [out[k] for k in ("sample", "pivot_lu", "skeleton", "hodlr_factor", "eliminate", "dense_front") if k in out]
+    fac = [out[k] for k in ("sample", "pivot_lu", "skeleton", "hodlr_factor", "eliminate", "dense_front",
+                            "materialize") if k in out]
     tot = sum(v["ms"] for v in fac)
     out["factor_weighted_frac"] = sum(v["frac"] * v["ms"] for v in fac) / tot if tot else None
     out["factor_covered_ms"] = tot
@@ -603,7 +611,8 @@ def run_gpu_arm(args, cfg, world, rank, local):
                                                    "wall_ms", "apply_build_ms", "apply_instantiate_ms",
                                                    "gmres_ms", "gmres_apply_ms")},
                    "phases_ms": {k: tim[k] for k in ("sample_ms", "pivot_lu_ms", "skeleton_ms",
-                                                     "hodlr_factor_ms", "dense_front_ms", "eliminate_ms")},
+                                                     "hodlr_factor_ms", "dense_front_ms", "eliminate_ms",
+                                                     "materialize_ms", "idle_gap_ms")},
                    **fstats,
                    "symbolic_s": t_sym, "cold_first_factor_s": cold_s},
         "apply": {"ms": apply_ms, "bytes": apply_bytes, "gbs": apply_bytes / (apply_ms * 1e-3) / 1e9,

@@ -96,6 +96,11 @@ typedef struct {
    * the numerators of the achieved-throughput rooflines (the reference's own
    * counts above can be lower or higher than the work this form does) */
   double exec_flops_skeleton, exec_flops_hodlr, exec_flops_elim, exec_flops_dense;
+  /* child updates written out as dense blocks before their parent's height samples them
+   * (HODLR leaves and low-rank blocks, minus W V^T): device time, executed flops, and the
+   * rest of the time between a height's sampling and the previous height's end, in which
+   * the GPU waits for the host (planning, request building) */
+  double materialize_ms, exec_flops_materialize, idle_gap_ms;
 } mfh_timing_t;
 
 /* ---- errors --------------------------------------------------------------- */

@@ -69,7 +69,9 @@ class mfh_timing_t(C.Structure):
                 ("skeleton_flops", C.c_double), ("sample_lr_flops", C.c_double),
                 ("pivot_lu_crit_steps", C.c_double), ("apply_ref_bytes", C.c_double),
                 ("exec_flops_skeleton", C.c_double), ("exec_flops_hodlr", C.c_double),
-                ("exec_flops_elim", C.c_double), ("exec_flops_dense", C.c_double)]
+                ("exec_flops_elim", C.c_double), ("exec_flops_dense", C.c_double),
+                ("materialize_ms", C.c_double), ("exec_flops_materialize", C.c_double),
+                ("idle_gap_ms", C.c_double)]
 
 
 HOST_OP = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double))

@@ -2099,11 +2099,13 @@ struct Factorizer {
   // one launch per job kind for every child materialized at this height
   void run_densify(Sink &s, DensifyJobs &dj) {
     if (dj.cp.empty() && dj.gm[0].empty() && dj.gm[1].empty()) return;
+    const double fl0 = ctx->flops_exec;
     s.begin_batch();
     run_copy(s, dj.cp);
     for (int x = 0; x < 2; ++x) run_gemm(s, dj.gm[x], x == 1);
     for (int x = 0; x < 2; ++x) run_gemm(s, dj.wv[x], x == 1);
     s.flush();
+    F->timing.exec_flops_materialize += ctx->flops_exec - fl0;
   }
 
   void build_fronts_dev(Sink &s, const std::vector<int> &fis, std::vector<DFront> &dfr,
@@ -3935,6 +3937,14 @@ struct Factorizer {
                 decide_us_of_use[u]);
       }
       float ms;
+      if (u > 0) {
+        cudaEvent_t prev = ctx->evpool[8 * (u - 1) + (struct_of_use[u - 1] ? 7 : 2)];
+        float g = 0.f, m2 = 0.f;
+        CK(cudaEventElapsedTime(&g, prev, ev[0]));
+        CK(cudaEventElapsedTime(&m2, prev, ctx->evd_pool[u]));
+        F->timing.materialize_ms += m2;
+        F->timing.idle_gap_ms += g - m2;
+      }
       CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
       tsum[0] += ms;
       CK(cudaEventElapsedTime(&ms, ev[1], ev[2]));

@@ -1697,6 +1697,24 @@ struct CsrView {
   const double *val = nullptr;
 };
 
+// fn(begin, end, t) over [0, n) on up to 8 host threads (half the cores), at least
+// min_per_thread items each; fn must not throw
+template <class Fn>
+static int par_chunks(int64_t n, int64_t min_per_thread, Fn fn) {
+  const unsigned hc = std::thread::hardware_concurrency();
+  const int k = (int)std::min<int64_t>(std::min(8u, std::max(1u, hc / 2)), std::max<int64_t>(1, n / min_per_thread));
+  if (k <= 1) {
+    fn((int64_t)0, n, 0);
+    return 1;
+  }
+  const int64_t step = (n + k - 1) / k;
+  std::vector<std::thread> th;
+  for (int t = 1; t < k; ++t) th.emplace_back([=, &fn] { fn(t * step, std::min(n, (t + 1) * step), t); });
+  fn((int64_t)0, std::min(n, step), 0);
+  for (auto &x : th) x.join();
+  return k;
+}
+
 struct Factorizer {
   mfh_factor *F;
   Ctx *ctx;
@@ -3529,13 +3547,28 @@ struct Factorizer {
       const int64_t nnz = A.ptr[n];
       mfh_symcache &C = et->cache;
       // the cached symbolic data is valid for exactly this pattern and zero pattern
+      // (the scan for explicit zeros and the pattern comparison read ~16 bytes per entry:
+      // on several host threads above 1M entries; 19 ms on one thread at C4's 7M)
       std::vector<int64_t> zeros;
-      for (int64_t p2 = 0; p2 < nnz; ++p2)
-        if (A.val[p2] == 0.0) zeros.push_back(p2);
-      const bool same = C.valid && C.pat_accel == accel && (int64_t)C.pat_ptr.size() == n + 1 &&
-                        (int64_t)C.pat_idx.size() == nnz &&
-                        std::memcmp(C.pat_ptr.data(), A.ptr, sizeof(int64_t) * (n + 1)) == 0 &&
-                        std::memcmp(C.pat_idx.data(), A.idx, sizeof(int64_t) * nnz) == 0 && C.pat_zero == zeros;
+      {
+        std::vector<int64_t> zl[8];
+        par_chunks(nnz, 1 << 20, [&](int64_t b, int64_t e, int t) {
+          for (int64_t p2 = b; p2 < e; ++p2)
+            if (A.val[p2] == 0.0) zl[t].push_back(p2);
+        });
+        for (auto &z : zl) zeros.insert(zeros.end(), z.begin(), z.end());
+      }
+      bool same = C.valid && C.pat_accel == accel && (int64_t)C.pat_ptr.size() == n + 1 &&
+                  (int64_t)C.pat_idx.size() == nnz &&
+                  std::memcmp(C.pat_ptr.data(), A.ptr, sizeof(int64_t) * (n + 1)) == 0 && C.pat_zero == zeros;
+      if (same) {
+        std::atomic<int> diff{0};
+        const int64_t *cached = C.pat_idx.data(), *given = A.idx;
+        par_chunks(nnz, 1 << 20, [&](int64_t b, int64_t e, int) {
+          if (e > b && std::memcmp(cached + b, given + b, sizeof(int64_t) * (size_t)(e - b)) != 0) diff.store(1);
+        });
+        same = diff.load() == 0;
+      }
       if (!same) {
         C = mfh_symcache{};
         C.pat_ptr.assign(A.ptr, A.ptr + n + 1);
@@ -3639,7 +3672,16 @@ struct Factorizer {
         // raw values staged asynchronously, gathered into P A P^T order on the device
         double *raw = F->arena.d(nnz);
         Sink up{ctx};
-        up.push_to(raw, A.val, sizeof(double) * nnz);
+        {
+          // into the pinned staging ring on several host threads, then one async H2D copy
+          auto hd = ctx->stage.take(sizeof(double) * nnz);
+          char *dsth = (char *)hd.first;
+          const char *srch = (const char *)A.val;
+          par_chunks(nnz, 1 << 20, [&](int64_t b, int64_t e, int) {
+            std::memcpy(dsth + sizeof(double) * b, srch + sizeof(double) * b, sizeof(double) * (size_t)(e - b));
+          });
+          up.h2d(raw, hd.first, sizeof(double) * nnz);
+        }
         const long long *srcp = pd->src;
         double *dst = d_ap_val;
         int g = (int)std::min<int64_t>(cdiv(nnz, 256), 148 * 8);

@@ -1964,7 +1964,9 @@ struct Factorizer {
       for (int q = 0; q < std::max(1, (int)P.d); ++q) per *= std::max(1.0, deg);
       for (int bi : blist) edges += ((double)F->blocks[bi].m + F->blocks[bi].n) * per;
     }
-    const int use = (int)std::max<double>(1.0, std::min<double>(std::min<double>(nthreads, blist.size()), edges / 2e6));
+    const double per_thread = getenv("MFH_PLAN_MIN_EDGES") ? atof(getenv("MFH_PLAN_MIN_EDGES")) : 2e6;  // test knob
+    const int use = (int)std::max<double>(
+        1.0, std::min<double>(std::min<double>(nthreads, blist.size()), edges / std::max(1.0, per_thread)));
     std::vector<std::thread> pool;
     for (int t = 1; t < use; ++t) pool.emplace_back(work, t);
     work(0);

@@ -105,6 +105,9 @@ def test_spmv_streamed_bit_identical_to_reference_product():
             M = keep @ M
             M.eliminate_zeros()
         cases.append(P.SparseMatrix(sp.csc_matrix(M)))
+    # no entries at all, and a rectangular matrix
+    cases.append(P.SparseMatrix(sp.csc_matrix((5, 5))))
+    cases.append(P.SparseMatrix(sp.random(300, 200, density=0.05, random_state=9, format="csc")))
     # rows of 40-200 entries (32-row chunks) and a matrix whose rows are too long to stream (fallback kernel)
     cases.append(P.SparseMatrix(sp.random(600, 600, density=0.2, random_state=7, format="csc")))
     long_rows = P.SparseMatrix(sp.random(900, 900, density=0.6, random_state=8, format="csc"))

@@ -225,7 +225,7 @@ __device__ __forceinline__ int2 sample_tile(const SampleTiles &T, long long t) {
   return make_int2(T.rids[lo], (int)(t - T.tpre[lo]));
 }
 
-__global__ void k_sample(const SReq *__restrict__ reqs, SampleTiles tiles,
+__global__ void __launch_bounds__(256, 6) k_sample(const SReq *__restrict__ reqs, SampleTiles tiles,
                          const DFront *__restrict__ fronts, const DChild *__restrict__ kids,
                          const long long *__restrict__ Ap_ptr, const int *__restrict__ Ap_col,
                          const double *__restrict__ Ap_val) {

@@ -52,7 +52,19 @@ static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // inside the timed step
 struct ChunkPool {
   std::vector<std::pair<char *, size_t>> free_chunks;
+  // MFH_POOL_TRACE: device allocations that missed the pool (count, bytes, host ms) and retries
+  int64_t miss_calls = 0, retry_calls = 0;
+  double miss_bytes = 0.0, miss_ms = 0.0;
   std::pair<char *, size_t> take(size_t need) {
+    auto t0_ = std::chrono::steady_clock::now();
+    struct Clock {
+      ChunkPool *p;
+      std::chrono::steady_clock::time_point t0;
+      bool on = false;
+      ~Clock() {
+        if (on) p->miss_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      }
+    } clk{this, t0_};
     int best = -1;
     for (int q = 0; q < (int)free_chunks.size(); ++q)
       if (free_chunks[q].second >= need && (best < 0 || free_chunks[q].second < free_chunks[best].second))
@@ -63,7 +75,11 @@ struct ChunkPool {
       return c;
     }
     char *p = nullptr;
+    clk.on = true;
+    miss_calls++;
+    miss_bytes += (double)need;
     if (cudaMalloc(&p, need) != cudaSuccess) {
+      retry_calls++;
       // free chunks of the wrong sizes can hold the memory a larger request
       // needs (C5): return them to the device and retry once. A free chunk may
       // still be read by enqueued work (release arenas hand chunks back as soon
@@ -4053,6 +4069,13 @@ struct Factorizer {
     F->stats.device_bytes_peak =
         (int64_t)F->arena.capacity() + (int64_t)upd.peak + (int64_t)ctx->scratch.capacity();
     if (getenv("MFH_MEM_TRACE")) memory_breakdown();
+    if (getenv("MFH_POOL_TRACE")) {
+      ChunkPool &cp = ctx->pool;
+      fprintf(stderr, "[mfh pool] misses %lld (%.2f GB, %.1f ms in cudaMalloc), out-of-memory retries %lld, free chunks %zu\n",
+              (long long)cp.miss_calls, cp.miss_bytes / 1e9, cp.miss_ms, (long long)cp.retry_calls, cp.free_chunks.size());
+      cp.miss_calls = cp.retry_calls = 0;
+      cp.miss_bytes = cp.miss_ms = 0.0;
+    }
     // id views point into the tree's cache; nothing after the factorization
     // (the apply plan is already built) may read them
     for (auto &f : F->fronts) f.ids = IdsView{};

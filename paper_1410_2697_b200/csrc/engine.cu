@@ -373,13 +373,19 @@ struct Sink {
   void flush() {
     if (!batching) return;
     batching = false;
-    // coalesce staged ranges that are contiguous on both sides
+    // coalesce staged ranges that follow each other on both sides; the staging ring hands out
+    // 256-byte aligned pieces, so up to 255 bytes of padding may lie between two ranges (copied
+    // along: it is padding on the device side too)
     for (size_t q = 0; q < pend.size();) {
       char *d = pend[q].dst;
       const char *h = pend[q].src;
       size_t b = pend[q].bytes;
       size_t r = q + 1;
-      while (r < pend.size() && pend[r].dst == d + b && pend[r].src == h + b) b += pend[r++].bytes;
+      while (r < pend.size()) {
+        const ptrdiff_t gd = pend[r].dst - (d + b), gh = pend[r].src - (h + b);
+        if (gd != gh || gd < 0 || gd >= 256) break;
+        b += (size_t)gd + pend[r++].bytes;
+      }
       CK(cudaMemcpyAsync(d, h, b, cudaMemcpyHostToDevice, ctx->s));
       q = r;
     }
@@ -2365,6 +2371,10 @@ struct Factorizer {
   // ---- one height ----
   // host clock when each phase event was enqueued (MFH_HEIGHT_TRACE)
   std::chrono::steady_clock::time_point hts[8];
+  // MFH_HOST_TRACE: host ms per factorization in a height's prologue: [0] front descriptors +
+  // materialization enqueue, [1] dense requests + waiting for the planner + leaf requests
+  // ([2] = host_select_ms, the block / request / pivot-LU job loop)
+  double host_sec[2] = {0.0, 0.0};
   cudaEvent_t cur_evd = nullptr;  // recorded after the height's child updates have been materialized
   void process_height(const std::vector<int> &fis, cudaEvent_t *ev) {
     const auto h_t0 = std::chrono::steady_clock::now();
@@ -2380,6 +2390,8 @@ struct Factorizer {
     // the sample phase)
     build_fronts_dev(s, fis, dfr, dch, slot);
     if (cur_evd) cudaEventRecord(cur_evd, ctx->s);
+    host_sec[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h_t0).count();
+    const auto h_t1 = std::chrono::steady_clock::now();
     DFront *dF = nullptr;  // pushed with the first sampling batch below
     DChild *dC = nullptr;
 
@@ -2415,6 +2427,13 @@ struct Factorizer {
       }
     }
     auto t_sel0 = std::chrono::steady_clock::now();
+    host_sec[1] += std::chrono::duration<double, std::milli>(t_sel0 - h_t1).count();
+    // The index lists of every block (I, J, the core's column positions: three small arrays per
+    // block, 35,000 at C5) are staged and sent as one copy with the sampling requests. Issued one
+    // by one they filled the stream's queue behind the materialization (the host blocked in
+    // cudaMemcpyAsync: 930 ms of "host" time at C5) and then trickled through the copy engine
+    // with the SMs idle (the 63 / 112 ms idle gaps of C3 / C5).
+    s.begin_batch();
     std::vector<CopyJob> core_copies;
     std::vector<PluJob> plu;
     // one contiguous int / double scratch for every core of the height, so the
@@ -2499,6 +2518,7 @@ struct Factorizer {
     cudaEventRecord(ev[0], ctx->s);
     hts[0] = std::chrono::steady_clock::now();
     run_sample(s, reqs, dF, dC, &dfr, &dch);
+    s.flush();  // the staged index lists, descriptors and requests in one transfer, then the sampling launches
     cudaEventRecord(ev[1], ctx->s);
     hts[1] = std::chrono::steady_clock::now();
 
@@ -4069,6 +4089,9 @@ struct Factorizer {
     F->stats.device_bytes_peak =
         (int64_t)F->arena.capacity() + (int64_t)upd.peak + (int64_t)ctx->scratch.capacity();
     if (getenv("MFH_MEM_TRACE")) memory_breakdown();
+    if (getenv("MFH_HOST_TRACE"))
+      fprintf(stderr, "[mfh host] height prologues: descriptors + materialization enqueue %.1f ms, dense / leaf requests + planner wait %.1f ms, block loop %.1f ms\n",
+              host_sec[0], host_sec[1], F->timing.host_select_ms);
     if (getenv("MFH_POOL_TRACE")) {
       ChunkPool &cp = ctx->pool;
       fprintf(stderr, "[mfh pool] misses %lld (%.2f GB, %.1f ms in cudaMalloc), out-of-memory retries %lld, free chunks %zu\n",

@@ -309,6 +309,7 @@ struct Ctx {
   // GMRES host-callback preconditioner may re-enter on the same thread)
   std::recursive_mutex mu;
   int64_t launches = 0;      // launches of this library's kernels
+  int64_t h2d_copies = 0, h2d_single = 0;  // staged host-to-device copies issued (all / outside batched stretches)
   int64_t lib_calls = 0;     // cuBLAS DGEMM calls (only with MFH_GEMM_ROUTE=blas)
   int64_t big_gemm_jobs = 0; // large plain GEMMs run on k_gemm_big
   double flops_exec = 0.0;   // flops enqueued by run_gemm (2mnk) and the register inverses (2n^3)
@@ -387,6 +388,7 @@ struct Sink {
         b += (size_t)gd + pend[r++].bytes;
       }
       CK(cudaMemcpyAsync(d, h, b, cudaMemcpyHostToDevice, ctx->s));
+      ctx->h2d_copies++;
       q = r;
     }
     pend.clear();
@@ -407,6 +409,8 @@ struct Sink {
       return;
     }
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->s));
+    ctx->h2d_copies++;
+    ctx->h2d_single++;
   }
 
   void sync_reset() {
@@ -4092,6 +4096,11 @@ struct Factorizer {
     if (getenv("MFH_HOST_TRACE"))
       fprintf(stderr, "[mfh host] height prologues: descriptors + materialization enqueue %.1f ms, dense / leaf requests + planner wait %.1f ms, block loop %.1f ms\n",
               host_sec[0], host_sec[1], F->timing.host_select_ms);
+    if (getenv("MFH_HOST_TRACE")) {
+      fprintf(stderr, "[mfh host] staged host-to-device copies: %lld (%lld outside batched stretches)\n",
+              (long long)ctx->h2d_copies, (long long)ctx->h2d_single);
+      ctx->h2d_copies = ctx->h2d_single = 0;
+    }
     if (getenv("MFH_POOL_TRACE")) {
       ChunkPool &cp = ctx->pool;
       fprintf(stderr, "[mfh pool] misses %lld (%.2f GB, %.1f ms in cudaMalloc), out-of-memory retries %lld, free chunks %zu\n",
